@@ -1,0 +1,225 @@
+"""CPU oracle for the batched SNP transition step (TEST INFRASTRUCTURE ONLY).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+/ ``--impl reference`` legs may import this package.  The product path
+(``paper_1104_1824_b200``) never imports it and shares no code with it.
+
+Two independent implementations live here:
+
+* ``oracle.cpp`` → ``liboracle.so``: a plain C++17 BFS over the computation tree
+  (Alg. 1), exact int64 counts, ``std::set`` dedup.
+* ``brute.py``: an even plainer pure-Python enumerator (all 2^n 0/1 vectors,
+  validity per PAPER.md:111-113) used to pin the C++ oracle on tiny systems.
+
+Parity pins for every function are in ``tests/test_oracle_*.py``; readings of
+silent or garbled passages are listed in DESIGN.md §3.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+OR_OK = 0
+OR_E_ARG = -1
+OR_E_INVALID_SYSTEM = -2
+OR_E_OVERFLOW = -3
+OR_E_CAPACITY = -4
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_U64 = ctypes.c_uint64
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.cpp into liboracle.so (plain g++, no GPU code)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        L.oracle_load.argtypes = [_I64, _I64, _P, _P, _P, _P, ctypes.POINTER(_P), ctypes.c_char_p, _I64]
+        L.oracle_load.restype = ctypes.c_int
+        L.oracle_free.argtypes = [_P]
+        L.oracle_applicability.argtypes = [_P, _P, _P, _P]
+        L.oracle_children.argtypes = [_P, _P, _I64, _P, _P, ctypes.POINTER(_U64)]
+        L.oracle_children.restype = ctypes.c_int
+        L.oracle_fingerprint.argtypes = [_P, _I64, _U64, _U64, _P]
+        L.oracle_fmix64.argtypes = [_U64]
+        L.oracle_fmix64.restype = _U64
+        L.oracle_thinning_tau.argtypes = [_I64, _I64]
+        L.oracle_thinning_tau.restype = _U64
+        L.oracle_explore.argtypes = [_P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _U64, _U64, ctypes.POINTER(_P)]
+        L.oracle_explore.restype = ctypes.c_int
+        L.oracle_run_status.argtypes = [_P]
+        L.oracle_run_error.argtypes = [_P]
+        L.oracle_run_error.restype = ctypes.c_char_p
+        for f in ("oracle_run_num_configs", "oracle_run_num_levels", "oracle_run_num_expanded"):
+            getattr(L, f).argtypes = [_P]
+            getattr(L, f).restype = _I64
+        L.oracle_run_level_offsets.argtypes = [_P, _P]
+        L.oracle_run_configs.argtypes = [_P, _I64, _P]
+        L.oracle_run_tree.argtypes = [_P, _P, _P, _P, _P]
+        L.oracle_run_counters.argtypes = [_P, _P, _P, _P]
+        L.oracle_run_free.argtypes = [_P]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        super().__init__(f"oracle status {status}: {msg}")
+        self.status = status
+
+
+class System:
+    """An SNP system loaded into the oracle (rules n×6 int32, M as CSR)."""
+
+    def __init__(self, m: int, rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.ndarray):
+        self.m = int(m)
+        self.rules = np.ascontiguousarray(rules, dtype=np.int32).reshape(-1, 6)
+        self.n = self.rules.shape[0]
+        self._keep = (np.ascontiguousarray(row_ptr, dtype=np.int64), np.ascontiguousarray(col, dtype=np.int32),
+                      np.ascontiguousarray(val, dtype=np.int32))
+        h = _P()
+        err = ctypes.create_string_buffer(256)
+        st = lib().oracle_load(self.m, self.n, _ptr(self.rules), _ptr(self._keep[0]), _ptr(self._keep[1]),
+                               _ptr(self._keep[2]), ctypes.byref(h), err, 256)
+        if st != OR_OK:
+            raise OracleError(st, err.value.decode())
+        self._h = h
+
+    @classmethod
+    def from_dense(cls, rules: np.ndarray, M: np.ndarray) -> "System":
+        M = np.asarray(M, dtype=np.int64)
+        n, m = M.shape
+        row_ptr = [0]
+        col, val = [], []
+        for r in range(n):
+            for j in range(m):
+                if M[r, j] != 0:
+                    col.append(j)
+                    val.append(int(M[r, j]))
+            row_ptr.append(len(col))
+        return cls(m, rules, np.array(row_ptr), np.array(col, dtype=np.int32), np.array(val, dtype=np.int32))
+
+    @classmethod
+    def from_workload(cls, w) -> "System":
+        return cls(w.m, w.rules, w.row_ptr, w.col, w.val)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().oracle_free(self._h)
+            self._h = None
+
+    # Alg. 2 II-1: per-rule marks tmp and per-neuron |σ_V|
+    def applicability(self, C):
+        C = np.ascontiguousarray(C, dtype=np.int32)
+        tmp = np.zeros(self.n, np.int32)
+        d = np.zeros(self.m, np.int32)
+        lib().oracle_applicability(self._h, _ptr(C), _ptr(tmp), _ptr(d))
+        return tmp, d
+
+    # Alg. 1 II+III: all (S, C') pairs of one configuration, t order
+    def children(self, C, cap: int = 1 << 20):
+        C = np.ascontiguousarray(C, dtype=np.int32)
+        psi = _U64()
+        st = lib().oracle_children(self._h, _ptr(C), 0, None, None, ctypes.byref(psi))
+        if st != OR_OK:
+            raise OracleError(st)
+        k = min(int(psi.value), cap)
+        S = np.zeros((k, self.n), np.uint8)
+        Cn = np.zeros((k, self.m), np.int64)
+        lib().oracle_children(self._h, _ptr(C), k, _ptr(S), _ptr(Cn), ctypes.byref(psi))
+        return int(psi.value), S, Cn
+
+    def explore(self, level0, depth: int, dedup: int = 0, count_bits: int = 32, frontier_target: int = 0,
+                max_transitions: int = 0, seeds=(0x5EED0, 0x5EED1)) -> "Run":
+        L0 = np.ascontiguousarray(np.atleast_2d(level0), dtype=np.int32)
+        assert L0.shape[1] == self.m
+        h = _P()
+        st = lib().oracle_explore(self._h, L0.shape[0], _ptr(L0), depth, dedup, count_bits, frontier_target,
+                                  max_transitions, seeds[0], seeds[1], ctypes.byref(h))
+        if st == OR_E_ARG and not h:
+            raise OracleError(st, "bad argument")
+        return Run(self, h, st)
+
+
+@dataclass
+class Counters:
+    T: np.ndarray
+    new: np.ndarray
+    kept: np.ndarray
+
+
+class Run:
+    """Result of ``System.explore`` — the BFS computation tree."""
+
+    def __init__(self, sys: System, h, status: int):
+        L = lib()
+        self.status = status
+        self.error = L.oracle_run_error(h).decode() if h else ""
+        try:
+            nc = L.oracle_run_num_configs(h)
+            nl = L.oracle_run_num_levels(h)
+            ne = L.oracle_run_num_expanded(h)
+            self.level_offsets = np.zeros(nl + 1, np.int64)
+            L.oracle_run_level_offsets(h, _ptr(self.level_offsets))
+            self.configs = np.zeros((nc, sys.m), np.int64)
+            L.oracle_run_configs(h, sys.m, _ptr(self.configs))
+            self.parent = np.zeros(nc, np.int64)
+            self.t = np.zeros(nc, np.uint64)
+            self.halting = np.zeros(nc, np.uint8)
+            self.fp = np.zeros((nc, 2), np.uint64)
+            if status == OR_OK:
+                L.oracle_run_tree(h, _ptr(self.parent), _ptr(self.t), _ptr(self.halting), _ptr(self.fp))
+            T = np.zeros(ne, np.int64)
+            nn = np.zeros(ne, np.int64)
+            kp = np.zeros(ne, np.int64)
+            L.oracle_run_counters(h, _ptr(T), _ptr(nn), _ptr(kp))
+            self.counters = Counters(T, nn, kp)
+        finally:
+            L.oracle_run_free(h)
+
+    def level(self, L: int) -> np.ndarray:
+        return self.configs[self.level_offsets[L]:self.level_offsets[L + 1]]
+
+    @property
+    def num_levels(self) -> int:
+        return len(self.level_offsets) - 1
+
+
+def fingerprint(C, seeds=(0x5EED0, 0x5EED1)):
+    C = np.ascontiguousarray(C, dtype=np.int64)
+    out = np.zeros(2, np.uint64)
+    lib().oracle_fingerprint(_ptr(C), C.shape[0], seeds[0], seeds[1], _ptr(out))
+    return int(out[0]), int(out[1])
+
+
+def fmix64(k: int) -> int:
+    return int(lib().oracle_fmix64(k))
+
+
+def thinning_tau(F: int, n_new: int) -> int:
+    return int(lib().oracle_thinning_tau(F, n_new))

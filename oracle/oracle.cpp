@@ -1,0 +1,459 @@
+// ============================================================================
+// oracle.cpp — plain, slow, obviously-correct CPU oracle for the batched SNP
+// transition step  C_{k+1} = C_k + S_k · M_Π  and the breadth-first
+// computation tree it grows.
+//
+// TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+// cpu_baseline / --impl reference legs of bench.py may load this library.  It
+// shares no code, header, table or constant generator with the CUDA engine
+// under paper_1104_1824_b200/ (the engine must never route through it).
+//
+// Source of truth: /root/reference/PAPER.md, Cabarle, Adorna, Martínez-del-Amor,
+// "Simulating Spiking Neural P systems without delays using GPUs".
+// Every function cites the passage it follows as PAPER.md:<line> (§, eq., alg.).
+// Readings of silent / garbled passages are the A-numbered readings listed in
+// DESIGN.md §3 (they follow SURVEY.md §8(c)).
+//
+// Arithmetic: spike counts are exact int64 (the paper's host uses unbounded
+// Python ints); fingerprints are arithmetic mod 2^64 (DESIGN.md
+// reading A18).  No blocking, fusion or reordering beyond the definitions.
+// ============================================================================
+#include <cstdint>
+#include <cstring>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include <set>
+#include <utility>
+#include <algorithm>
+
+namespace {
+
+// Status codes (defined here independently of the engine's header).
+enum {
+  OR_OK = 0,
+  OR_E_ARG = -1,
+  OR_E_INVALID_SYSTEM = -2,
+  OR_E_OVERFLOW = -3,
+  OR_E_CAPACITY = -4,
+};
+
+enum { RE_EXACT = 0, RE_PERIODIC = 1 };
+
+// One rule  E/a^c -> a^p  of neuron σ (Def. 1 (b-1)); p = 0 is a
+// forgetting rule ((b-2)).  The regular expression E is either
+//   EXACT(k)       E = a^k          (form (b-3))
+//   PERIODIC(i,j)  E = a^i (a^j)*   (the paper-simulator reading, A1)
+struct Rule {
+  int64_t neuron;
+  int64_t kind;
+  int64_t a;  // k (EXACT) or i (PERIODIC)
+  int64_t b;  // j (PERIODIC), unused for EXACT
+  int64_t consumed;  // c >= 1
+  int64_t produced;  // p >= 0
+};
+
+struct System {
+  int64_t m = 0;  // neurons
+  int64_t n = 0;  // rules, in the paper's total order
+  std::vector<Rule> rules;
+  // M_Π (Def. 2): n rows (rules) x m columns (neurons),
+  // held as a plain compressed-row list of (column, value) per rule.
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> M_rows;
+};
+
+// ---------------------------------------------------------------------------
+// a^v ∈ L(E)?  (regex kinds per reading A1)
+bool regex_matches(const Rule& r, int64_t v) {
+  if (r.kind == RE_EXACT) return v == r.a;
+  // PERIODIC(i, j): v = i + x·j for some x >= 0
+  return v >= r.a && (v - r.a) % r.b == 0;
+}
+
+// Rule applicability: the neuron holds v spikes, a^v ∈ L(E) and
+// v >= c.
+bool applicable(const Rule& r, const std::vector<int64_t>& C) {
+  int64_t v = C[r.neuron];
+  return regex_matches(r, v) && v >= r.consumed;
+}
+
+// Alg. 2 step II-1 (worked example 268-294): copy of the rule
+// list where every applicable rule of a neuron is marked 1, 2, 3, ... in the
+// total order, and every non-applicable rule is marked 0.
+std::vector<int64_t> mark_applicable(const System& sys, const std::vector<int64_t>& C) {
+  std::vector<int64_t> tmp(sys.n, 0);
+  std::vector<int64_t> running(sys.m, 0);
+  for (int64_t r = 0; r < sys.n; ++r) {
+    if (applicable(sys.rules[r], C)) {
+      running[sys.rules[r].neuron] += 1;
+      tmp[r] = running[sys.rules[r].neuron];
+    }
+  }
+  return tmp;
+}
+
+// |σ_{V_i}| of eq. (8): the number of applicable rules of
+// each neuron, in increasing neuron order; A_s = those rules in total order.
+std::vector<std::vector<int64_t>> applicable_rules_per_neuron(const System& sys,
+                                                              const std::vector<int64_t>& C) {
+  std::vector<std::vector<int64_t>> A(sys.m);
+  for (int64_t r = 0; r < sys.n; ++r)
+    if (applicable(sys.rules[r], C)) A[sys.rules[r].neuron].push_back(r);
+  return A;
+}
+
+// Ψ, eq. (8): product of |σ_{V_i}| over the neurons.  Reading
+// A3: a neuron with no applicable rule contributes a factor 1 (it does not
+// fire); reading A5: if no neuron has an applicable rule the configuration is
+// halting and has no children (Ψ = 0).  Returns false if Ψ exceeds 2^62.
+bool count_children(const std::vector<std::vector<int64_t>>& A, uint64_t* psi) {
+  bool any = false;
+  unsigned __int128 prod = 1;
+  for (const auto& As : A) {
+    if (As.empty()) continue;
+    any = true;
+    prod *= (unsigned __int128)As.size();
+    if (prod > ((unsigned __int128)1 << 62)) return false;
+  }
+  *psi = any ? (uint64_t)prod : 0;
+  return true;
+}
+
+// Alg. 2 steps II-2/II-3: the t-th valid spiking
+// vector, t in [0, Ψ).  II-3 distributes every string of the first neuron over
+// the strings of the next ones, so the first neuron with applicable rules is
+// the most significant mixed-radix digit (tmp3 = ['10110','01110'],
+// PAPER.md:351, 376; reading A7).  Digit x_s selects A_s[x_s]; exactly one
+// rule fires per neuron with applicable rules (reading A4).
+std::vector<uint8_t> spiking_vector(const System& sys, const std::vector<std::vector<int64_t>>& A,
+                                    uint64_t t) {
+  std::vector<uint8_t> S(sys.n, 0);
+  for (int64_t s = sys.m - 1; s >= 0; --s) {  // least significant digit last
+    if (A[s].empty()) continue;
+    uint64_t d = A[s].size();
+    uint64_t x = t % d;
+    t /= d;
+    S[A[s][x]] = 1;
+  }
+  return S;
+}
+
+// Eq. (2): C_{k+1} = C_k + S_k · M_Π, as the plain row sum
+// of M_Π over the rules that fire, in exact int64 arithmetic.
+std::vector<int64_t> transition(const System& sys, const std::vector<int64_t>& C,
+                                const std::vector<uint8_t>& S) {
+  std::vector<int64_t> Cn = C;
+  for (int64_t r = 0; r < sys.n; ++r) {
+    if (!S[r]) continue;
+    for (const auto& jv : sys.M_rows[r]) Cn[jv.first] += jv.second;
+  }
+  return Cn;
+}
+
+// ---- fingerprints (reading A18; used as the dedup key in mode dedup=1 and
+// as the thinning key in both modes) ---------------------------------------
+uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+uint64_t fmix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xFF51AFD7ED558CCDULL;
+  k ^= k >> 33;
+  k *= 0xC4CEB9FE1A85EC53ULL;
+  k ^= k >> 33;
+  return k;
+}
+// fp_ℓ(C) = Σ_j C[j]·R_ℓ[j] mod 2^64, R_ℓ[j] = splitmix64(seed_ℓ XOR j) | 1.
+std::pair<uint64_t, uint64_t> fingerprint(const std::vector<int64_t>& C, uint64_t seed0, uint64_t seed1) {
+  uint64_t f0 = 0, f1 = 0;
+  for (size_t j = 0; j < C.size(); ++j) {
+    uint64_t R0 = splitmix64(seed0 ^ (uint64_t)j) | 1ULL;
+    uint64_t R1 = splitmix64(seed1 ^ (uint64_t)j) | 1ULL;
+    f0 += (uint64_t)C[j] * R0;
+    f1 += (uint64_t)C[j] * R1;
+  }
+  return {f0, f1};
+}
+
+// ---- validation (SURVEY §8(b) list; Def. 1 and Def. 2) --------------------
+std::string validate(const System& sys) {
+  char buf[256];
+  for (int64_t r = 0; r < sys.n; ++r) {
+    const Rule& R = sys.rules[r];
+    if (R.neuron < 0 || R.neuron >= sys.m) { snprintf(buf, sizeof buf, "rule %lld: neuron out of range", (long long)r); return buf; }
+    if (r > 0 && R.neuron < sys.rules[r - 1].neuron) { snprintf(buf, sizeof buf, "rule %lld: rules not grouped by neuron", (long long)r); return buf; }
+    if (R.kind != RE_EXACT && R.kind != RE_PERIODIC) { snprintf(buf, sizeof buf, "rule %lld: bad regex kind", (long long)r); return buf; }
+    if (R.consumed < 1) { snprintf(buf, sizeof buf, "rule %lld: c < 1", (long long)r); return buf; }
+    if (R.produced < 0) { snprintf(buf, sizeof buf, "rule %lld: p < 0", (long long)r); return buf; }
+    if (R.a < 0) { snprintf(buf, sizeof buf, "rule %lld: regex exponent < 0", (long long)r); return buf; }
+    if (R.kind == RE_PERIODIC && R.b < 1) { snprintf(buf, sizeof buf, "rule %lld: period j < 1", (long long)r); return buf; }
+  }
+  std::vector<int64_t> per_neuron(sys.m, 0);
+  for (const Rule& R : sys.rules) per_neuron[R.neuron]++;
+  for (int64_t s = 0; s < sys.m; ++s)
+    if (per_neuron[s] > 255) { snprintf(buf, sizeof buf, "neuron %lld: more than 255 rules", (long long)s); return buf; }
+  // Def. 2: a_{r,σ(r)} = -c ; a_{r,j} = p if (σ(r), j) ∈ syn, else 0.  All
+  // spiking rules of a neuron share that neuron's synapse set.
+  std::vector<std::vector<int64_t>> syn_of(sys.m);
+  std::vector<int> syn_seen(sys.m, 0);
+  for (int64_t r = 0; r < sys.n; ++r) {
+    const Rule& R = sys.rules[r];
+    bool diag = false;
+    std::vector<int64_t> targets;
+    for (const auto& jv : sys.M_rows[r]) {
+      if (jv.first < 0 || jv.first >= sys.m) { snprintf(buf, sizeof buf, "M row %lld: column out of range", (long long)r); return buf; }
+      if (jv.second == 0) continue;
+      if (jv.first == R.neuron) {
+        if (jv.second != -R.consumed) { snprintf(buf, sizeof buf, "M[%lld][%lld] != -c", (long long)r, (long long)jv.first); return buf; }
+        diag = true;
+      } else {
+        if (jv.second != R.produced) { snprintf(buf, sizeof buf, "M[%lld][%lld] not in {0, p}", (long long)r, (long long)jv.first); return buf; }
+        targets.push_back(jv.first);
+      }
+    }
+    if (!diag) { snprintf(buf, sizeof buf, "M[%lld][neuron] != -c", (long long)r); return buf; }
+    std::sort(targets.begin(), targets.end());
+    for (size_t i = 1; i < targets.size(); ++i)
+      if (targets[i] == targets[i - 1]) { snprintf(buf, sizeof buf, "M row %lld: repeated column", (long long)r); return buf; }
+    if (R.produced > 0) {
+      if (!syn_seen[R.neuron]) { syn_seen[R.neuron] = 1; syn_of[R.neuron] = targets; }
+      else if (syn_of[R.neuron] != targets) { snprintf(buf, sizeof buf, "rule %lld: synapse set differs from neuron's other spiking rules", (long long)r); return buf; }
+    }
+  }
+  return "";
+}
+
+struct Run {
+  int status = OR_OK;
+  std::string error;
+  std::vector<std::vector<int64_t>> configs;   // discovery order
+  std::vector<int64_t> level_offsets;          // depth_reached + 2 entries
+  std::vector<int64_t> parent;                 // index within the previous level, -1 at level 0
+  std::vector<uint64_t> t;                     // spiking-vector index (0 at level 0)
+  std::vector<uint8_t> halting;
+  std::vector<uint64_t> fp0, fp1;
+  std::vector<int64_t> level_T, level_new, level_kept;  // per expanded level
+};
+
+}  // namespace
+
+// ============================================================================
+// C ABI of the oracle (own header: oracle/oracle.h)
+// ============================================================================
+extern "C" {
+
+struct oracle_system { System s; };
+struct oracle_run { Run r; };
+
+int oracle_load(int64_t m, int64_t n, const int32_t* rules6, const int64_t* row_ptr,
+                const int32_t* col, const int32_t* val, oracle_system** out, char* err,
+                int64_t errlen) {
+  if (!out || m < 1 || n < 0 || (n > 0 && (!rules6 || !row_ptr))) return OR_E_ARG;
+  auto* h = new oracle_system();
+  System& s = h->s;
+  s.m = m;
+  s.n = n;
+  s.rules.resize(n);
+  s.M_rows.resize(n);
+  for (int64_t r = 0; r < n; ++r) {
+    const int32_t* q = rules6 + 6 * r;
+    s.rules[r] = Rule{q[0], q[1], q[2], q[3], q[4], q[5]};
+    for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) s.M_rows[r].push_back({col[e], val[e]});
+  }
+  std::string msg = validate(s);
+  if (!msg.empty()) {
+    if (err && errlen > 0) snprintf(err, (size_t)errlen, "%s", msg.c_str());
+    delete h;
+    return OR_E_INVALID_SYSTEM;
+  }
+  *out = h;
+  return OR_OK;
+}
+
+void oracle_free(oracle_system* h) { delete h; }
+
+// Alg. 2 II-1 marks (tmp) and |σ_{V_i}| per neuron (eq. 8).
+int oracle_applicability(const oracle_system* h, const int32_t* C32, int32_t* tmp_out, int32_t* d_out) {
+  const System& s = h->s;
+  std::vector<int64_t> C(C32, C32 + s.m);
+  auto tmp = mark_applicable(s, C);
+  auto A = applicable_rules_per_neuron(s, C);
+  for (int64_t r = 0; r < s.n; ++r) tmp_out[r] = (int32_t)tmp[r];
+  for (int64_t j = 0; j < s.m; ++j) d_out[j] = (int32_t)A[j].size();
+  return OR_OK;
+}
+
+// All children of one configuration, t = 0..Ψ-1 (Alg. 1 II + III).  Writes
+// min(Ψ, cap) spiking vectors (n bytes each) and children (m int64 each).
+int oracle_children(const oracle_system* h, const int32_t* C32, int64_t cap, uint8_t* S_out,
+                    int64_t* C_out, uint64_t* psi_out) {
+  const System& s = h->s;
+  std::vector<int64_t> C(C32, C32 + s.m);
+  auto A = applicable_rules_per_neuron(s, C);
+  uint64_t psi = 0;
+  if (!count_children(A, &psi)) return OR_E_CAPACITY;
+  *psi_out = psi;
+  for (uint64_t t = 0; t < psi && (int64_t)t < cap; ++t) {
+    auto S = spiking_vector(s, A, t);
+    auto Cn = transition(s, C, S);
+    if (S_out) memcpy(S_out + t * s.n, S.data(), s.n);
+    if (C_out) memcpy(C_out + t * s.m, Cn.data(), s.m * sizeof(int64_t));
+  }
+  return OR_OK;
+}
+
+void oracle_fingerprint(const int64_t* C, int64_t m, uint64_t seed0, uint64_t seed1, uint64_t* out2) {
+  std::vector<int64_t> v(C, C + m);
+  auto f = fingerprint(v, seed0, seed1);
+  out2[0] = f.first;
+  out2[1] = f.second;
+}
+
+uint64_t oracle_fmix64(uint64_t k) { return fmix64(k); }
+
+// Thinning threshold of reading A19: τ = floor(F·2^64 / N_new) (exact).
+uint64_t oracle_thinning_tau(int64_t F, int64_t n_new) {
+  unsigned __int128 num = (unsigned __int128)(uint64_t)F << 64;
+  return (uint64_t)(num / (unsigned __int128)(uint64_t)n_new);
+}
+
+// Breadth-first computation tree (Alg. 1; dedup per the
+// second stopping criterion PAPER.md:229; readings A5-A7, A16-A20).
+//   level0:        F0 configurations (row-major, F0 x m); duplicates keep their
+//                  first occurrence (reading A20).
+//   depth:         number of levels to expand; configurations of level `depth`
+//                  are classified (halting) but not expanded.
+//   dedup:         0 = full-configuration equality, 1 = 128-bit fingerprint.
+//   count_bits:    8/16/32; a kept configuration with a count above the
+//                  storage range is SNP overflow (reading A16).
+//   frontier_target F: 0 = no cap; otherwise thinning (reading A19).
+//   max_transitions:   per-level budget on T; 0 = unlimited (capacity error).
+int oracle_explore(const oracle_system* h, int64_t F0, const int32_t* level0, int32_t depth,
+                   int32_t dedup, int32_t count_bits, int64_t frontier_target,
+                   int64_t max_transitions, uint64_t seed0, uint64_t seed1, oracle_run** out) {
+  const System& s = h->s;
+  if (!out || F0 < 1 || depth < 0 || (dedup != 0 && dedup != 1)) return OR_E_ARG;
+  if (count_bits != 8 && count_bits != 16 && count_bits != 32) return OR_E_ARG;
+  const int64_t cmax = count_bits == 8 ? 255 : count_bits == 16 ? 65535 : 2147483647LL;
+  auto* hr = new oracle_run();
+  Run& run = hr->r;
+  *out = hr;
+
+  std::set<std::vector<int64_t>> visited_rows;      // dedup = 0
+  std::set<std::pair<uint64_t, uint64_t>> visited_fp;  // dedup = 1
+  auto seen = [&](const std::vector<int64_t>& C, const std::pair<uint64_t, uint64_t>& f) {
+    return dedup == 0 ? visited_rows.count(C) > 0 : visited_fp.count(f) > 0;
+  };
+  auto insert = [&](const std::vector<int64_t>& C, const std::pair<uint64_t, uint64_t>& f) {
+    if (dedup == 0) visited_rows.insert(C);
+    else visited_fp.insert(f);
+  };
+  auto push = [&](const std::vector<int64_t>& C, const std::pair<uint64_t, uint64_t>& f,
+                  int64_t parent, uint64_t t) {
+    run.configs.push_back(C);
+    run.parent.push_back(parent);
+    run.t.push_back(t);
+    run.fp0.push_back(f.first);
+    run.fp1.push_back(f.second);
+  };
+
+  // Level 0 (reading A20): every distinct configuration of level0, in order.
+  run.level_offsets.push_back(0);
+  for (int64_t i = 0; i < F0; ++i) {
+    std::vector<int64_t> C(level0 + i * s.m, level0 + (i + 1) * s.m);
+    for (int64_t v : C)
+      if (v < 0 || v > cmax) { run.status = OR_E_OVERFLOW; run.error = "level 0 count out of range"; return run.status; }
+    auto f = fingerprint(C, seed0, seed1);
+    if (seen(C, f)) continue;
+    insert(C, f);
+    push(C, f, -1, 0);
+  }
+  run.level_offsets.push_back((int64_t)run.configs.size());
+
+  for (int32_t L = 0; L < depth; ++L) {
+    const int64_t lo = run.level_offsets[L], hi = run.level_offsets[L + 1];
+    if (lo == hi) break;  // stopping criterion 2: nothing new
+    struct Cand { int64_t parent; uint64_t t; std::vector<int64_t> C; std::pair<uint64_t, uint64_t> f; };
+    std::vector<Cand> fresh;  // new children in tag order (parent order, then t)
+    std::set<std::vector<int64_t>> level_rows;
+    std::set<std::pair<uint64_t, uint64_t>> level_fp;
+    int64_t T = 0;
+    for (int64_t i = lo; i < hi; ++i) {
+      const std::vector<int64_t> C = run.configs[i];
+      auto A = applicable_rules_per_neuron(s, C);
+      uint64_t psi = 0;
+      if (!count_children(A, &psi)) { run.status = OR_E_CAPACITY; run.error = "psi above 2^62"; return run.status; }
+      for (uint64_t t = 0; t < psi; ++t) {
+        ++T;
+        if (max_transitions > 0 && T > max_transitions) { run.status = OR_E_CAPACITY; run.error = "transition budget exceeded"; return run.status; }
+        auto S = spiking_vector(s, A, t);
+        auto Cn = transition(s, C, S);
+        auto f = fingerprint(Cn, seed0, seed1);
+        if (seen(Cn, f)) continue;  // produced at an earlier level (A6)
+        bool dup_here = dedup == 0 ? !level_rows.insert(Cn).second : !level_fp.insert(f).second;
+        if (dup_here) continue;  // same-level duplicate: first (minimum) tag wins
+        fresh.push_back(Cand{i - lo, t, Cn, f});
+      }
+    }
+    const int64_t n_new = (int64_t)fresh.size();
+    int64_t kept = 0;
+    const bool thin = frontier_target > 0 && n_new > frontier_target;
+    const uint64_t tau = thin ? oracle_thinning_tau(frontier_target, n_new) : 0;
+    for (const Cand& c : fresh) {
+      if (thin && !(fmix64(c.f.first) < tau)) continue;  // reading A19
+      for (int64_t v : c.C) {
+        if (v < 0) { run.status = OR_E_OVERFLOW; run.error = "negative count"; return run.status; }
+        if (v > cmax) { run.status = OR_E_OVERFLOW; run.error = "count above storage range"; return run.status; }
+      }
+      insert(c.C, c.f);
+      push(c.C, c.f, c.parent, c.t);
+      ++kept;
+    }
+    run.level_T.push_back(T);
+    run.level_new.push_back(n_new);
+    run.level_kept.push_back(kept);
+    run.level_offsets.push_back((int64_t)run.configs.size());
+    if (kept == 0) break;
+  }
+  // Halting classification of every configuration (reading A5).
+  run.halting.resize(run.configs.size());
+  for (size_t i = 0; i < run.configs.size(); ++i) {
+    auto A = applicable_rules_per_neuron(s, run.configs[i]);
+    bool any = false;
+    for (const auto& As : A) any = any || !As.empty();
+    run.halting[i] = any ? 0 : 1;
+  }
+  return OR_OK;
+}
+
+int oracle_run_status(const oracle_run* h) { return h->r.status; }
+const char* oracle_run_error(const oracle_run* h) { return h->r.error.c_str(); }
+int64_t oracle_run_num_configs(const oracle_run* h) { return (int64_t)h->r.configs.size(); }
+int64_t oracle_run_num_levels(const oracle_run* h) { return (int64_t)h->r.level_offsets.size() - 1; }
+int64_t oracle_run_num_expanded(const oracle_run* h) { return (int64_t)h->r.level_T.size(); }
+void oracle_run_level_offsets(const oracle_run* h, int64_t* out) {
+  std::copy(h->r.level_offsets.begin(), h->r.level_offsets.end(), out);
+}
+void oracle_run_configs(const oracle_run* h, int64_t m, int64_t* out) {
+  for (size_t i = 0; i < h->r.configs.size(); ++i) std::copy(h->r.configs[i].begin(), h->r.configs[i].end(), out + i * m);
+}
+void oracle_run_tree(const oracle_run* h, int64_t* parent, uint64_t* t, uint8_t* halting, uint64_t* fp2) {
+  const Run& r = h->r;
+  for (size_t i = 0; i < r.configs.size(); ++i) {
+    parent[i] = r.parent[i];
+    t[i] = r.t[i];
+    halting[i] = r.halting[i];
+    fp2[2 * i] = r.fp0[i];
+    fp2[2 * i + 1] = r.fp1[i];
+  }
+}
+void oracle_run_counters(const oracle_run* h, int64_t* T, int64_t* n_new, int64_t* kept) {
+  const Run& r = h->r;
+  for (size_t i = 0; i < r.level_T.size(); ++i) { T[i] = r.level_T[i]; n_new[i] = r.level_new[i]; kept[i] = r.level_kept[i]; }
+}
+void oracle_run_free(oracle_run* h) { delete h; }
+
+}  // extern "C"
