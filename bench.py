@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py — config transitions/s of the batched SNP transition step on B200.
+
+One "step" = one BFS level of the hot path (applicability,
+Ψ + scan, mixed-radix decode + child fingerprints, dedup + thinning, C + S·M
+for the kept children) over the whole frontier of BASELINE.json config 4
+(random SNP system m = 16384 neurons, n = 65536 rules, out-degree 8,
+frontier F = 2^22, uint8 counts, 128-bit fingerprint dedup, 20 levels).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+value       Σ T over the K timed levels ÷ their device time (CUDA events on the
+            engine's stream, inputs resident in HBM).
+e2e         the same metric through the public C ABI from a pinned HOST level 0
+            (row-major uint8, H2D inside the timed region) with the per-level
+            result (edges + fingerprints of the new frontier) read back.
+roofline    dominant kernel phase: algorithmic bytes ÷ its
+            CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the CPU oracle (oracle/, single thread, as it stands) on a
+            bounded sample of the same workload.
+--impl reference  the oracle as the reference arm (this tier has no reference
+            code): each step = the oracle on a bounded sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1104_1824_b200 import workloads as W  # noqa: E402
+
+METRIC = "config transitions/s (C+S·M) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "transitions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=17)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[3, 4])
+    ap.add_argument("--F", type=int, default=0, help="override frontier size (testing only)")
+    ap.add_argument("--m", type=int, default=0, help="override neuron count (testing only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload_for(args):
+    cfg = dict(W.CONFIGS[args.config])
+    if args.F:
+        cfg["F"] = args.F
+        cfg["frontier_target"] = args.F
+    if args.m:
+        cfg["m"] = args.m
+    w = W.random_system(cfg["m"], outdeg=8, k_nd=cfg["k_nd"], seed=cfg["seed"], name=f"config{args.config}")
+    return cfg, w
+
+
+def config_json(args, cfg, w, K):
+    bytes_per = cfg["count_bits"] // 8
+    return {
+        "workload": f"config{args.config}: random SNP system m={w.m} n={w.n} outdeg 8 k_nd={cfg['k_nd']}, "
+                    f"frontier F={cfg['F']} (thinning target), {cfg['depth']} levels",
+        "m": w.m, "n": w.n, "F": cfg["F"], "storage": f"u{cfg['count_bits']}" if bytes_per < 4 else "i32",
+        "dedup": "fp128" if cfg["dedup"] else "exact", "levels_warmup": args.warmup, "levels_timed": K,
+        "l2": f"inputs > L2: each level reads a {w.m * cfg['F'] * bytes_per / 1e9:.1f} GB frontier (L2 = 126 MB)",
+        "seed": cfg["seed"],
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for ln in open(self.path):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_phase):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    summary (profiles/ncu_summary.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(path))
+        return d["kernels"][kernel_phase]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline and the reference arm)
+# ---------------------------------------------------------------------------
+def oracle_sample(w, cfg, rows_begin, n_rows):
+    import oracle
+    sysw = oracle.System.from_workload(w)
+    L0 = W.level0_counts(w, n_rows, cfg["seed"], row_begin=rows_begin)
+    t0 = time.perf_counter()
+    run = sysw.explore(L0, depth=1, dedup=cfg["dedup"], count_bits=cfg["count_bits"])
+    dt = time.perf_counter() - t0
+    assert run.status == 0, run.error
+    return int(run.counters.T.sum()), dt
+
+
+def calibrate_rows(w, cfg, target_s):
+    T, dt = oracle_sample(w, cfg, 0, 4)
+    per_row = max(dt / 4, 1e-4)
+    return max(4, min(4096, int(target_s / per_row)))
+
+
+def cpu_baseline(w, cfg, target_s=12.0):
+    rows = calibrate_rows(w, cfg, target_s)
+    T, dt = oracle_sample(w, cfg, 0, rows)
+    return {"value": T / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle BFS (C++ oracle/, 1 thread) expanding {rows} level-0 parents of the same workload "
+                      f"by one level: {T} transitions in {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg, w = workload_for(args)
+    rows = calibrate_rows(w, cfg, 2.0)
+    for i in range(args.warmup):
+        oracle_sample(w, cfg, i * rows, rows)
+    Ts, dts = [], []
+    for i in range(args.steps):
+        T, dt = oracle_sample(w, cfg, (args.warmup + i) * rows, rows)
+        Ts.append(T)
+        dts.append(dt)
+    value = sum(Ts) / sum(dts)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(dts) / len(dts),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+           "data": "synthetic", "config": config_json(args, cfg, w, args.steps),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"each step: oracle BFS expanding {rows} level-0 parents by one level"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# native arm
+# ---------------------------------------------------------------------------
+def step_bytes(c, m, w_bytes):
+    """SURVEY §8(d-3) algorithmic bytes of one level: parents read once, kept
+    children written once, one 32-B probe per transition, 48 B per kept key."""
+    return c["parents"] * m * w_bytes + c["kept"] * m * w_bytes + c["T"] * 32 + c["kept"] * 48
+
+
+def run_native(args, rank, world):
+    import torch
+    from paper_1104_1824_b200 import snp
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda")
+    if world > 1:
+        raise SystemExit("bench.py: multi-GPU exploration is not built yet (DESIGN.md §9); run with --gpus 1")
+    cfg, w = workload_for(args)
+    m, F = w.m, cfg["F"]
+    wb = cfg["count_bits"] // 8
+    eng = snp.System(w, count_bits=cfg["count_bits"], dedup=cfg["dedup"], frontier_target=cfg["frontier_target"],
+                     keep_tree=0)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    eng.set_profiling(True)
+    # level 0 generated on the device (inputs resident in HBM)
+    buf = torch.empty((m, F), dtype=torch.uint8 if wb == 1 else torch.int32, device=dev)
+    snp.generate_level0_device(w, F, cfg["seed"], buf.data_ptr(), wb, snp.SNP_LAYOUT_NEURON_MAJOR, F,
+                               stream.cuda_stream)
+    eng.begin(snp.configs_from_device(buf.data_ptr(), F, F, wb, snp.SNP_LAYOUT_NEURON_MAJOR))
+    del buf
+    torch.cuda.empty_cache()
+    for _ in range(args.warmup):
+        eng.advance()
+    prof0 = eng.profile()
+    launches0 = snp.snp_kernel_launches()
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    levels = []
+    for _ in range(args.steps):
+        levels.append(eng.advance())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    elapsed_ms = e0.elapsed_time(e1)
+    launches = snp.snp_kernel_launches() - launches0
+    prof1 = eng.profile()
+    phase_ms = {k: prof1[k] - prof0[k] for k in prof1}
+    T_sum = sum(c["T"] for c in levels)
+    value = T_sum / (elapsed_ms / 1e3)
+    peak, peak_src = measured_peak()
+    # per-phase algorithmic bytes
+    alg = {
+        "expand": sum(c["parents"] * m * wb for c in levels),
+        "materialize": sum(c["kept"] * m * wb for c in levels),
+        "dedup": sum(c["T"] * 32 + c["kept"] * 48 for c in levels),
+        "keys": sum(c["T"] * 16 for c in levels),
+    }
+    dom = max(("expand", "materialize", "dedup", "keys"), key=lambda k: phase_ms.get(k, 0.0))
+    achieved = alg[dom] / (phase_ms[dom] / 1e3) / 1e9 if phase_ms[dom] > 0 else 0.0
+    sb = sum(step_bytes(c, m, wb) for c in levels)
+    n_conf, T_total, digest = eng.summary()
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": f"u{8 * wb}" if wb < 4 else "i32", "data": "synthetic",
+        "config": config_json(args, cfg, w, args.steps),
+        "roofline": {"bound": "hbm", "kernel": f"phase '{dom}' ({'k_expand' if dom == 'expand' else 'k_materialize+k_patch' if dom == 'materialize' else dom})",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(dom), "peak_source": peak_src},
+        "step_roofline": {"algorithmic_GB_per_step": sb / len(levels) / 1e9,
+                          "achieved": sb / (elapsed_ms / 1e3) / 1e9, "frac": sb / (elapsed_ms / 1e3) / 1e9 / peak},
+        "phase_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
+        "levels": [{k: c[k] for k in ("parents", "halting", "T", "n_new", "kept")} | {"ms": round(c["ms"], 3)}
+                   for c in levels],
+        "digest": f"{digest:016x}", "gpu_launches": launches, "clocks": clk,
+    }
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        out["e2e"] = run_e2e(args, cfg, w, snp, torch)
+    if not args.no_cpu and rank == 0:
+        out["cpu_baseline"] = cpu_baseline(w, cfg)
+    print(json.dumps(out), flush=True)
+
+
+def run_e2e(args, cfg, w, snp, torch):
+    """The user's call path: snp_begin from a pinned host level 0 (row-major),
+    then snp_advance per level, reading each level's edges back to the host."""
+    m, F = w.m, cfg["F"]
+    wb = cfg["count_bits"] // 8
+    dt = torch.uint8 if wb == 1 else torch.int32
+    try:
+        host = torch.empty((F, m), dtype=dt, pin_memory=True)
+    except Exception as e:  # pinned allocation failed
+        return {"value": None, "unit": UNIT, "error": f"pinned host buffer: {e}"}
+    # fill the host buffer with the same level 0 (device generator, chunked D2H; setup, untimed)
+    chunk = max(1, (1 << 31) // (m * wb))
+    tmp = torch.empty((chunk, m), dtype=dt, device="cuda")
+    for r0 in range(0, F, chunk):
+        n = min(chunk, F - r0)
+        snp.generate_level0_device(w, n, cfg["seed"], tmp.data_ptr(), wb, snp.SNP_LAYOUT_ROW_MAJOR, m, 0,
+                                   row_begin=r0)
+        host[r0:r0 + n].copy_(tmp[:n])
+    del tmp
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    eng = snp.System(w, count_bits=cfg["count_bits"], dedup=cfg["dedup"], frontier_target=cfg["frontier_target"],
+                     keep_tree=0)
+    c0 = snp.snp_configs(host.data_ptr(), F, m, wb, snp.SNP_LAYOUT_ROW_MAJOR, 0, 0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng.begin(c0)
+    T_sum = 0
+    d2h = 0
+    for _ in range(args.steps):
+        c = eng.advance()
+        T_sum += c["T"]
+        parent, t, halting, fp = eng.level_edges(eng.depth)
+        d2h += parent.nbytes + t.nbytes + fp.nbytes + halting.nbytes
+    dt_s = time.perf_counter() - t0
+    eng.close()
+    del host
+    return {"value": T_sum / dt_s, "unit": UNIT, "h2d_bytes_per_step": F * m * wb // args.steps,
+            "d2h_bytes_per_step": d2h // args.steps,
+            "note": "snp_begin(pinned host row-major level 0) + K x (snp_advance + snp_level_edges D2H); "
+                    "wall clock around synchronous ABI calls"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus else 1))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_native(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/*
+ * snp.h — C ABI of the B200-native SNP transition engine (libsnp.so).
+ *
+ * The engine computes, on the GPU, the batched transition step of Cabarle,
+ * Adorna and Martínez-del-Amor's matrix formulation of spiking neural P
+ * systems without delays:
+ *
+ *     C_{k+1} = C_k + S_k · M_Π                     (eq. (2))
+ *
+ * over a whole breadth-first frontier of configurations: rule applicability
+ * (Alg. 2 II-1), enumeration of every valid spiking
+ * vector as a mixed-radix product of per-neuron rule choices (eq. (8),
+ * PAPER.md:250; Alg. 2 II-2/II-3), the integer transition,
+ * and deduplication of the children into the computation tree (Alg. 1,
+ * PAPER.md:231-238; stopping criteria PAPER.md:229).  Readings of silent or
+ * garbled passages are numbered A1..A22 in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns snp_status; SNP_OK == 0.  On failure a thread-local
+ *     message is available from snp_last_error().  No exception crosses the ABI.
+ *   - Caller-owned inputs are deep-copied; the caller may free them on return.
+ *   - snp_system / snp_tree / snp_frontier are owned by the library and released
+ *     with the matching snp_*_free.  A handle is not thread-safe.
+ *   - Integers are little-endian; host arrays are C-contiguous.
+ *   - Host-buffer calls are synchronous.  Device-buffer inputs (snp_configs with
+ *     on_device = 1) are read on the system's stream (snp_set_stream).
+ *   - There is no CPU fallback: without a CUDA device every compute call
+ *     returns SNP_E_CUDA.
+ */
+#ifndef SNP_H_
+#define SNP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNP_ABI_VERSION 1
+
+typedef enum {
+  SNP_OK = 0,
+  SNP_E_ARG = -1,            /* bad argument (NULL, size, enum value)                        */
+  SNP_E_INVALID_SYSTEM = -2, /* system violates Def. 1 / Def. 2 (first offending index in msg) */
+  SNP_E_OVERFLOW = -3,       /* a stored count leaves the storage range (reading A16)        */
+  SNP_E_CAPACITY = -4,       /* Ψ > 2^62, transition budget, or table capacity exceeded      */
+  SNP_E_OOM = -5,            /* device allocation failed                                     */
+  SNP_E_CUDA = -6,           /* CUDA runtime error (including: no device)                    */
+  SNP_E_NCCL = -7,           /* NCCL error (multi-GPU)                                       */
+  SNP_E_COLLISION = -8,      /* dedup=0 found two different configurations with equal 128-bit
+                                fingerprints (probability < 2^-100; the run is aborted rather
+                                than silently merged, reading A18)                            */
+  SNP_E_STATE = -9           /* call not valid in the handle's current state                 */
+} snp_status;
+
+/* Regular-expression kinds of a rule's E (reading A1):
+ *   SNP_RE_EXACT    E = a^a            (form (b-3)): n == a
+ *   SNP_RE_PERIODIC E = a^a (a^b)*     (b >= 1):  n >= a && (n - a) % b == 0     */
+enum { SNP_RE_EXACT = 0, SNP_RE_PERIODIC = 1 };
+
+/* One rule E/a^c -> a^p of neuron `neuron`.  produced = 0 is a
+ * forgetting rule (b-2).  Rules are given in the paper's total order and must be
+ * grouped by non-decreasing neuron.  A rule is applicable to
+ * a neuron holding n spikes iff a^n ∈ L(E) and n >= consumed.   */
+typedef struct {
+  int32_t neuron;    /* 0-based neuron index σ(r)               */
+  int32_t kind;      /* SNP_RE_EXACT or SNP_RE_PERIODIC         */
+  int32_t a;         /* k (EXACT) or i (PERIODIC), >= 0          */
+  int32_t b;         /* j >= 1 (PERIODIC), ignored for EXACT     */
+  int32_t consumed;  /* c >= 1                                   */
+  int32_t produced;  /* p >= 0                                   */
+} snp_rule;
+
+/* Spiking transition matrix M_Π (Def. 2): n_rules rows,
+ * n_neurons columns; either dense (row-major, eq. (3)) or CSR.
+ * Validation: M[r][σ(r)] = -c_r; off-diagonal entries are 0 or p_r; all
+ * spiking rules of a neuron share one synapse set; no self-synapse.          */
+typedef struct {
+  int64_t n_rules;
+  int64_t n_neurons;
+  const int32_t *dense;    /* n_rules × n_neurons row-major, or NULL           */
+  const int64_t *row_ptr;  /* CSR (used when dense == NULL): n_rules + 1 offsets */
+  const int32_t *col;
+  const int32_t *val;
+} snp_matrix;
+
+typedef struct {
+  int32_t count_bits;        /* 8, 16 or 32: device storage of spike counts (reading A16)   */
+  int32_t dedup;             /* 0 = full-configuration equality, 1 = 128-bit fingerprint    */
+  int64_t frontier_target;   /* F for fingerprint thinning (reading A19); 0 = exact BFS      */
+  int64_t max_transitions;   /* per-level budget on T; 0 = unlimited                        */
+  uint64_t fp_seed[2];       /* fingerprint seeds (reading A18)                             */
+  int32_t keep_tree;         /* 1 = retain every level's configurations for snp_tree_configs */
+  int32_t reserved;
+} snp_options;
+
+/* A batch of configurations (a frontier).  elem_bytes ∈ {1, 2, 4} (unsigned
+ * for 1/2, int32 for 4).  layout ROW_MAJOR: n_configs rows of n_neurons counts
+ * (ld = row stride in elements, >= n_neurons; 0 = n_neurons).  NEURON_MAJOR:
+ * n_neurons rows of n_configs counts (ld = row stride in elements, >=
+ * n_configs; 0 = n_configs).  on_device = 1: data is a CUDA device pointer.   */
+enum { SNP_LAYOUT_ROW_MAJOR = 0, SNP_LAYOUT_NEURON_MAJOR = 1 };
+typedef struct {
+  const void *data;
+  int64_t n_configs;
+  int64_t ld;
+  int32_t elem_bytes;
+  int32_t layout;
+  int32_t on_device;
+  int32_t reserved;
+} snp_configs;
+
+/* Per-level counters of one expansion. */
+typedef struct {
+  int64_t parents;     /* configurations expanded                              */
+  int64_t halting;     /* of which halting (no applicable rule, reading A5)    */
+  int64_t T;           /* transitions generated = Σ Ψ (every (parent, S) pair)  */
+  int64_t n_new;       /* distinct children not seen at an earlier level        */
+  int64_t kept;        /* children kept in the next frontier (after thinning)   */
+  uint64_t tau;        /* thinning threshold used (0 = no thinning)             */
+  double ms;           /* device time of the level (CUDA events)                */
+} snp_level_counters;
+
+typedef struct snp_system snp_system;
+typedef struct snp_tree snp_tree;
+
+int         snp_abi_version(void);
+const char *snp_last_error(void);
+
+/* Validate and upload a system (host buffers, deep-copied).  C0 (m counts) is
+ * the default level 0.  opt may be NULL (defaults: count_bits 32, dedup 0, no
+ * thinning, no budget, keep_tree 1).                                          */
+snp_status snp_load(const snp_matrix *M, const snp_rule *rules, int64_t n_rules, const int32_t *C0,
+                    int64_t m, const snp_options *opt, snp_system **out);
+void       snp_system_free(snp_system *sys);
+
+/* Launch all device work of `sys` on this cudaStream_t (NULL = library stream). */
+snp_status snp_set_stream(snp_system *sys, void *cuda_stream);
+
+/* Incremental exploration (what bench.py times one level at a time):
+ *   snp_begin    level 0 := distinct configurations of `level0` (first
+ *                occurrence kept; NULL = {C0}) (reading A20), visited := level 0.
+ *   snp_advance  expand the current frontier by one level (§8(a) a1-a6);
+ *                fills *counters (may be NULL).  An empty frontier is a no-op. */
+snp_status snp_begin(snp_system *sys, const snp_configs *level0);
+snp_status snp_advance(snp_system *sys, snp_level_counters *counters);
+int64_t    snp_frontier_size(const snp_system *sys);
+int32_t    snp_depth(const snp_system *sys);
+/* Summary of the exploration so far: total configurations, total transitions,
+ * and an order-sensitive digest of (level, index, parent, t, fingerprint) of
+ * every stored configuration.                                  */
+snp_status snp_summary(const snp_system *sys, int64_t *n_configs, int64_t *transitions, uint64_t *digest);
+
+/* Direct access to level L (0 <= L <= snp_depth) of the current exploration:
+ *   snp_level_size     configurations of level L
+ *   snp_level_edges    parent (index in level L-1, -1 at level 0), t, halting
+ *                      (valid once level L was expanded or classified), fp (2 per
+ *                      configuration); any pointer may be NULL
+ *   snp_level_columns  configurations idx[0..n) of level L as n × m int32 rows;
+ *                      needs the level's counts on the device (the current level,
+ *                      or every level when keep_tree = 1 or dedup = 0).        */
+int64_t    snp_level_size(const snp_system *sys, int32_t level);
+snp_status snp_level_edges(snp_system *sys, int32_t level, int64_t *parent, uint64_t *t, uint8_t *halting,
+                           uint64_t *fp2);
+snp_status snp_level_columns(snp_system *sys, int32_t level, const int64_t *idx, int64_t n, int32_t *out);
+
+/* Phase timing (CUDA events on the system's stream), accumulated since the
+ * last snp_begin while profiling is on.  Phases (SNP_NUM_PHASES):
+ *   0 K-a expand (applicability, Ψ, base fingerprint, emits)
+ *   1 K-b offsets scan + child keys (mixed-radix decode, fingerprints)
+ *   2 K-d dedup (visited probe, level table, winners, thinning, compaction)
+ *   3 K-c materialize kept children (gather-add, ND patches)
+ *   4 dedup = 0 full-configuration verification                            */
+#define SNP_NUM_PHASES 5
+snp_status snp_set_profiling(snp_system *sys, int32_t on);
+snp_status snp_profile(const snp_system *sys, double *ms /* SNP_NUM_PHASES */);
+/* Kernels launched by this process through libsnp.so so far. */
+int64_t    snp_kernel_launches(void);
+
+/* snp_begin + `depth` × snp_advance + halting classification of the last
+ * level; the tree is a snapshot owned by the caller.                          */
+snp_status snp_explore(snp_system *sys, const snp_configs *level0, int32_t depth, snp_tree **out);
+/* One level from an arbitrary frontier: explore with depth 1.                 */
+snp_status snp_step(snp_system *sys, const snp_configs *frontier, snp_tree **out);
+
+int32_t    snp_tree_num_levels(const snp_tree *tree);
+int64_t    snp_tree_num_configs(const snp_tree *tree);
+snp_status snp_tree_level_offsets(const snp_tree *tree, int64_t *out /* num_levels + 1 */);
+/* configurations in discovery order, row-major int32 (needs keep_tree).       */
+snp_status snp_tree_configs(const snp_tree *tree, int32_t *out /* N × m */);
+/* parent = index in the previous level (-1 at level 0), t = spiking-vector index,
+ * halting flags, fingerprints (2 per configuration). Any pointer may be NULL. */
+snp_status snp_tree_edges(const snp_tree *tree, int64_t *parent, uint64_t *t, uint8_t *halting,
+                          uint64_t *fp2);
+snp_status snp_tree_counters(const snp_tree *tree, snp_level_counters *out /* num_levels - 1 */);
+/* The spiking vector S (n bytes of 0/1) that produced each configuration of
+ * level L >= 1 from its parent (needs keep_tree).                             */
+snp_status snp_tree_spiking_vectors(const snp_tree *tree, int32_t level, uint8_t *S_out /* count × n */);
+void       snp_tree_free(snp_tree *tree);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNP_H_ */

@@ -1,0 +1,50 @@
+"""Build the in-tree CUDA libraries for sm_100a (no JIT cache, no CPU path).
+
+* ``libsnp.so``     — the engine: kernels + C ABI of include/snp.h
+* ``libsnpgen.so``  — device-side level-0 input generator (workloads only)
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB_SNP = os.path.join(HERE, "libsnp.so")
+LIB_GEN = os.path.join(HERE, "libsnpgen.so")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+
+SNP_SOURCES = ["snp_engine.cu", "snp_kernels.cu"]
+SNP_DEPS = SNP_SOURCES + ["snp_device.cuh", "snp_internal.h", "../../include/snp.h"]
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(os.path.join(CSRC, d)) > t for d in deps)
+
+
+def _nvcc(out: str, sources, extra=()):
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-o", tmp, *[os.path.join(CSRC, s) for s in sources]]
+    subprocess.check_call(cmd)
+    os.replace(tmp, out)
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    if force or _stale(LIB_SNP, SNP_DEPS):
+        if verbose:
+            print("[build] nvcc libsnp.so (sm_100a)")
+        _nvcc(LIB_SNP, SNP_SOURCES)
+    if force or _stale(LIB_GEN, ["workload_gen.cu"]):
+        if verbose:
+            print("[build] nvcc libsnpgen.so (sm_100a)")
+        _nvcc(LIB_GEN, ["workload_gen.cu"])
+
+
+if __name__ == "__main__":
+    build(force=True, verbose=True)

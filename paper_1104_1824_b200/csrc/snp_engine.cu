@@ -1,0 +1,1071 @@
+// snp_engine.cu — host side of the SNP engine: validation, upload, the level
+// pipeline (SURVEY §8(a) a1-a6 / DESIGN.md §2) and the C ABI of include/snp.h.
+//
+// Every step of the path runs in the kernels of snp_kernels.cu; the host only
+// sizes buffers, launches, and reads back per-level counters.  There is no CPU
+// fallback: without a CUDA device every compute call fails with SNP_E_CUDA.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/snp.h"
+#include "snp_internal.h"
+
+using namespace snp;
+
+namespace {
+
+thread_local std::string g_err;
+
+snp_status fail(snp_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      if (e_ == cudaErrorMemoryAllocation) { cudaGetLastError(); return fail(SNP_E_OOM, "%s: %s", #expr, cudaGetErrorString(e_)); } \
+      return fail(SNP_E_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));                      \
+    }                                                                                        \
+  } while (0)
+
+#define SNP_TRY(expr)            \
+  do {                           \
+    snp_status s_ = (expr);      \
+    if (s_ != SNP_OK) return s_; \
+  } while (0)
+
+uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+uint64_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int64_t round_pitch(int64_t F) { return std::max<int64_t>(TILE, (F + TILE - 1) / TILE * TILE); }
+
+// A growable device allocation.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  snp_status ensure(size_t need, bool slack = true) {
+    if (need <= bytes && p) return SNP_OK;
+    release();
+    size_t want = slack ? need + need / 8 : need;
+    if (want < 256) want = 256;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      return fail(SNP_E_OOM, "cudaMalloc(%zu bytes): %s", want, cudaGetErrorString(e));
+    }
+    bytes = want;
+    return SNP_OK;
+  }
+  template <class U> U* as() const { return reinterpret_cast<U*>(p); }
+};
+
+// One level of the tree on the device.
+struct Level {
+  DBuf data;  // m × pitch counts (may be released when not retained)
+  int64_t F = 0, pitch = 0;
+  DBuf fp0, fp1, parent, t, halting;
+  bool has_data() const { return data.p != nullptr; }
+};
+
+}  // namespace
+
+struct snp_system {
+  // ---- host copy of the system
+  int64_t m = 0, n = 0;
+  snp_options opt{};
+  int32_t bytes = 4;       // storage bytes per count
+  int64_t count_max = 0;
+  std::vector<int32_t> C0;
+  bool binary_emit = true;
+  // ---- device system
+  DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1;
+  SysView view{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // ---- exploration state
+  uint64_t generation = 0;
+  bool begun = false;
+  std::vector<std::unique_ptr<Level>> levels;
+  std::vector<snp_level_counters> counters;
+  int64_t n_visited = 0;
+  int64_t total_T = 0;
+  uint64_t digest = 0;
+  bool halting_current_valid = false;
+  // hash tables
+  DBuf vis, ltab;
+  uint64_t vis_cap = 0, ltab_cap = 0;
+  // scratch
+  DBuf psi, off, fpb0, fpb1, ndc, nd, halting_tmp, ebits, evals;
+  DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
+  DBuf counters_dev;  // [0] err, [1..] u64 counters
+  std::vector<DBuf> spare;  // released level buffers kept for reuse
+  // phase profiling (snp_set_profiling)
+  bool profiling = false;
+  double prof_ms[SNP_NUM_PHASES] = {0, 0, 0, 0, 0};
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Mark { int phase; cudaEvent_t a, b; };
+  std::vector<Mark> marks;
+};
+
+struct snp_tree {
+  snp_system* sys = nullptr;
+  uint64_t generation = 0;
+  int64_t m = 0, n = 0;
+  std::vector<int64_t> level_offsets;
+  std::vector<int64_t> parent;
+  std::vector<uint64_t> t;
+  std::vector<uint8_t> halting;
+  std::vector<uint64_t> fp;
+  std::vector<snp_level_counters> counters;
+};
+
+namespace {
+
+// device counter block layout
+struct DevCounters {
+  int32_t err;
+  int32_t pad;
+  unsigned long long n_new;
+  unsigned long long n_halting;
+  unsigned long long n_ovf;
+  unsigned long long digest;
+};
+
+snp_status sync(snp_system* s) {
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return SNP_OK;
+}
+
+cudaEvent_t pool_event(snp_system* s) {
+  if (s->ev_used == s->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    s->ev_pool.push_back(e);
+  }
+  return s->ev_pool[s->ev_used++];
+}
+
+void phase_begin(snp_system* s, int phase) {
+  if (!s->profiling) return;
+  cudaEvent_t e = pool_event(s);
+  cudaEventRecord(e, s->stream);
+  s->marks.push_back({phase, e, nullptr});
+}
+
+void phase_end(snp_system* s) {
+  if (!s->profiling || s->marks.empty()) return;
+  cudaEvent_t e = pool_event(s);
+  cudaEventRecord(e, s->stream);
+  s->marks.back().b = e;
+}
+
+// after a stream synchronize: fold the recorded phase intervals into prof_ms
+void phase_collect(snp_system* s) {
+  for (auto& mk : s->marks) {
+    float ms = 0;
+    if (mk.b && cudaEventElapsedTime(&ms, mk.a, mk.b) == cudaSuccess) s->prof_ms[mk.phase] += ms;
+  }
+  s->marks.clear();
+  s->ev_used = 0;
+}
+
+snp_status read_counters(snp_system* s, DevCounters* h) {
+  CUDA_TRY(cudaMemcpyAsync(h, s->counters_dev.p, sizeof(DevCounters), cudaMemcpyDeviceToHost, s->stream));
+  return sync(s);
+}
+
+snp_status check_err(int32_t err) {
+  if (err & ERR_COLLISION) return fail(SNP_E_COLLISION, "two distinct configurations share a 128-bit fingerprint (or a fingerprint equals the empty-slot sentinel)");
+  if (err & ERR_TABLE_FULL) return fail(SNP_E_CAPACITY, "hash table full");
+  if (err & ERR_CAPACITY) return fail(SNP_E_CAPACITY, "a configuration has more than 2^62 valid spiking vectors");
+  if (err & ERR_OVERFLOW) return fail(SNP_E_OVERFLOW, "a spike count leaves the %s storage range", "count_bits");
+  return SNP_OK;
+}
+
+snp_status take_buffer(snp_system* s, size_t bytes, DBuf* out) {
+  // reuse the smallest spare that fits
+  int best = -1;
+  for (int i = 0; i < (int)s->spare.size(); ++i)
+    if (s->spare[i].bytes >= bytes && (best < 0 || s->spare[i].bytes < s->spare[best].bytes)) best = i;
+  if (best >= 0) {
+    *out = std::move(s->spare[best]);
+    s->spare.erase(s->spare.begin() + best);
+    return SNP_OK;
+  }
+  // free spares before a fresh allocation (they are too small)
+  s->spare.clear();
+  return out->ensure(bytes + bytes / 32, false);
+}
+
+void release_level_data(snp_system* s, Level* L) {
+  if (L->data.p) {
+    s->spare.push_back(std::move(L->data));
+    while (s->spare.size() > 2) s->spare.erase(s->spare.begin());
+  }
+}
+
+snp_status ensure_visited(snp_system* s, uint64_t needed_entries) {
+  uint64_t want = next_pow2(std::max<uint64_t>(1024, 2 * needed_entries));
+  if (want <= s->vis_cap) return SNP_OK;
+  DBuf nt;
+  SNP_TRY(nt.ensure(want * sizeof(Slot), false));
+  CUDA_TRY(cudaMemsetAsync(nt.p, 0xFF, want * sizeof(Slot), s->stream));
+  int32_t* err = s->counters_dev.as<int32_t>();
+  if (s->vis_cap) launch_rehash(s->vis.as<Slot>(), s->vis_cap, nt.as<Slot>(), want - 1, err, s->stream);
+  CUDA_TRY(cudaGetLastError());
+  SNP_TRY(sync(s));
+  s->vis = std::move(nt);
+  s->vis_cap = want;
+  return SNP_OK;
+}
+
+snp_status ensure_ltab(snp_system* s, uint64_t T) {
+  uint64_t want = next_pow2(std::max<uint64_t>(1024, 2 * T));
+  if (want > s->ltab_cap) {
+    SNP_TRY(s->ltab.ensure(want * sizeof(Slot), false));
+    s->ltab_cap = want;
+  }
+  // use only `want` slots this level (smaller clears for small levels)
+  CUDA_TRY(cudaMemsetAsync(s->ltab.p, 0xFF, want * sizeof(Slot), s->stream));
+  s->ltab_cap = std::max(s->ltab_cap, want);
+  return SNP_OK;
+}
+
+Tables tables(snp_system* s, uint64_t ltab_slots) {
+  return Tables{s->vis.as<Slot>(), s->vis_cap ? s->vis_cap - 1 : 0, s->ltab.as<Slot>(), ltab_slots - 1};
+}
+
+snp_status ensure_children(snp_system* s, uint64_t T) {
+  SNP_TRY(s->cpar.ensure(T * 4 + 16));
+  SNP_TRY(s->cfp0.ensure(T * 8 + 16));
+  SNP_TRY(s->cfp1.ensure(T * 8 + 16));
+  SNP_TRY(s->verdict.ensure(T + 16));
+  SNP_TRY(s->cslot.ensure(T * 8 + 16));
+  SNP_TRY(s->cref.ensure(T * 8 + 16));
+  SNP_TRY(s->kept.ensure((T + 1) * 8 + 16));
+  SNP_TRY(s->kpos.ensure((T + 1) * 8 + 16));
+  size_t tb = scan_temp_bytes((int64_t)T + 1);
+  SNP_TRY(s->scan_tmp.ensure(tb + 256));
+  return SNP_OK;
+}
+
+ChildArrays child_arrays(snp_system* s) {
+  return ChildArrays{s->cpar.as<uint32_t>(), s->cfp0.as<uint64_t>(), s->cfp1.as<uint64_t>(),
+                     s->verdict.as<uint8_t>(), s->cslot.as<uint64_t>(), s->cref.as<uint64_t>(),
+                     s->kept.as<uint64_t>(), s->kpos.as<uint64_t>()};
+}
+
+snp_status alloc_level_meta(Level* L, int64_t K) {
+  size_t k = (size_t)std::max<int64_t>(K, 1);
+  SNP_TRY(L->fp0.ensure(k * 8, false));
+  SNP_TRY(L->fp1.ensure(k * 8, false));
+  SNP_TRY(L->parent.ensure(k * 8, false));
+  SNP_TRY(L->t.ensure(k * 8, false));
+  SNP_TRY(L->halting.ensure(k, false));
+  return SNP_OK;
+}
+
+bool retain_levels(const snp_system* s) { return s->opt.keep_tree || s->opt.dedup == 0; }
+
+snp_status update_stored_table(snp_system* s) {
+  std::vector<StoredLevel> h(s->levels.size());
+  for (size_t i = 0; i < s->levels.size(); ++i) h[i] = StoredLevel{s->levels[i]->data.p, s->levels[i]->pitch};
+  SNP_TRY(s->stored.ensure(h.size() * sizeof(StoredLevel) + 16));
+  CUDA_TRY(cudaMemcpyAsync(s->stored.p, h.data(), h.size() * sizeof(StoredLevel), cudaMemcpyHostToDevice, s->stream));
+  return sync(s);  // h is a stack buffer
+}
+
+// ---------------------------------------------------------------------------
+// validation + upload (snp_load)
+// ---------------------------------------------------------------------------
+snp_status validate_and_build(snp_system* s, const snp_matrix* M, const snp_rule* rules, int64_t n_rules,
+                              std::vector<std::vector<std::pair<int32_t, int32_t>>>* rows,
+                              std::vector<std::vector<int32_t>>* out_syn) {
+  const int64_t m = s->m, n = n_rules;
+  rows->assign(n, {});
+  for (int64_t r = 0; r < n; ++r) {
+    const snp_rule& R = rules[r];
+    if (R.neuron < 0 || R.neuron >= m) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: neuron out of range", (long long)r);
+    if (r > 0 && R.neuron < rules[r - 1].neuron) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: rules not grouped by neuron", (long long)r);
+    if (R.kind != SNP_RE_EXACT && R.kind != SNP_RE_PERIODIC) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: bad regex kind", (long long)r);
+    if (R.consumed < 1) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: c < 1", (long long)r);
+    if (R.produced < 0) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: p < 0", (long long)r);
+    if (R.a < 0) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: regex exponent < 0", (long long)r);
+    if (R.kind == SNP_RE_PERIODIC && R.b < 1) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: period j < 1", (long long)r);
+    if (M->dense) {
+      for (int64_t j = 0; j < m; ++j) {
+        int32_t v = M->dense[r * m + j];
+        if (v) (*rows)[r].push_back({(int32_t)j, v});
+      }
+    } else {
+      for (int64_t e = M->row_ptr[r]; e < M->row_ptr[r + 1]; ++e) {
+        if (M->col[e] < 0 || M->col[e] >= m) return fail(SNP_E_INVALID_SYSTEM, "M row %lld: column out of range", (long long)r);
+        if (M->val[e]) (*rows)[r].push_back({M->col[e], M->val[e]});
+      }
+    }
+  }
+  std::vector<int64_t> per(m, 0);
+  for (int64_t r = 0; r < n; ++r) per[rules[r].neuron]++;
+  for (int64_t j = 0; j < m; ++j)
+    if (per[j] > 255) return fail(SNP_E_INVALID_SYSTEM, "neuron %lld: more than 255 rules", (long long)j);
+  out_syn->assign(m, {});
+  std::vector<char> seen(m, 0);
+  for (int64_t r = 0; r < n; ++r) {
+    const snp_rule& R = rules[r];
+    bool diag = false;
+    std::vector<int32_t> targets;
+    for (auto& jv : (*rows)[r]) {
+      if (jv.first == R.neuron) {
+        if (jv.second != -R.consumed) return fail(SNP_E_INVALID_SYSTEM, "M[%lld][%d] != -c", (long long)r, jv.first);
+        diag = true;
+      } else {
+        if (jv.second != R.produced) return fail(SNP_E_INVALID_SYSTEM, "M[%lld][%d] not in {0, p}", (long long)r, jv.first);
+        targets.push_back(jv.first);
+      }
+    }
+    if (!diag) return fail(SNP_E_INVALID_SYSTEM, "M[%lld][neuron] != -c", (long long)r);
+    std::sort(targets.begin(), targets.end());
+    for (size_t i = 1; i < targets.size(); ++i)
+      if (targets[i] == targets[i - 1]) return fail(SNP_E_INVALID_SYSTEM, "M row %lld: repeated column", (long long)r);
+    if (R.produced > 0) {
+      if (!seen[R.neuron]) { seen[R.neuron] = 1; (*out_syn)[R.neuron] = targets; }
+      else if ((*out_syn)[R.neuron] != targets)
+        return fail(SNP_E_INVALID_SYSTEM, "rule %lld: synapse set differs from neuron's other spiking rules", (long long)r);
+    }
+  }
+  return SNP_OK;
+}
+
+template <class U>
+snp_status upload(snp_system* s, DBuf& b, const std::vector<U>& v) {
+  SNP_TRY(b.ensure(std::max<size_t>(v.size(), 1) * sizeof(U), false));
+  if (!v.empty()) CUDA_TRY(cudaMemcpy(b.p, v.data(), v.size() * sizeof(U), cudaMemcpyHostToDevice));
+  return SNP_OK;
+}
+
+snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const int32_t* C0) {
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> rows;
+  std::vector<std::vector<int32_t>> out_syn;
+  SNP_TRY(validate_and_build(s, M, rules, n_rules, &rows, &out_syn));
+  const int64_t m = s->m, n = n_rules;
+  s->n = n;
+  for (int64_t j = 0; j < m; ++j)
+    if (C0[j] < 0 || C0[j] > s->count_max) return fail(SNP_E_OVERFLOW, "C0[%lld] outside the storage range", (long long)j);
+  s->C0.assign(C0, C0 + m);
+  // rule table
+  std::vector<int32_t> rule_off(m + 1, 0);
+  std::vector<DevRule> dr(n);
+  s->binary_emit = true;
+  for (int64_t r = 0; r < n; ++r) {
+    const snp_rule& R = rules[r];
+    rule_off[R.neuron + 1]++;
+    DevRule d{};
+    d.c = R.consumed;
+    d.p = R.produced;
+    if (R.kind == SNP_RE_EXACT) {
+      d.lo = std::max(R.a, R.consumed);
+      d.hi = R.a;
+      d.base = R.a;
+      d.j = 1;
+    } else {
+      d.lo = std::max(R.a, R.consumed);
+      d.hi = 0x7FFFFFFF;
+      d.base = R.a;
+      d.j = R.b;
+    }
+    d.jmask = (d.j & (d.j - 1)) == 0 ? d.j - 1 : -1;
+    dr[r] = d;
+    if (R.produced > 1) s->binary_emit = false;
+  }
+  for (int64_t j = 0; j < m; ++j) rule_off[j + 1] += rule_off[j];
+  // fingerprint weights R_ℓ[j] = splitmix64(seed_ℓ ^ j) | 1 and h_ℓ[r] = Σ_j M[r][j]·R_ℓ[j]
+  std::vector<uint64_t> R0(m), R1(m), h0(n, 0), h1(n, 0);
+  for (int64_t j = 0; j < m; ++j) {
+    R0[j] = splitmix64(s->opt.fp_seed[0] ^ (uint64_t)j) | 1ULL;
+    R1[j] = splitmix64(s->opt.fp_seed[1] ^ (uint64_t)j) | 1ULL;
+  }
+  for (int64_t r = 0; r < n; ++r)
+    for (auto& jv : rows[r]) {
+      h0[r] += (uint64_t)(int64_t)jv.second * R0[jv.first];
+      h1[r] += (uint64_t)(int64_t)jv.second * R1[jv.first];
+    }
+  // synapse graph: out-CSR (by source) and in-CSR (by target)
+  std::vector<int32_t> out_off(m + 1, 0), out_dst, in_off(m + 1, 0), in_src;
+  for (int64_t s_ = 0; s_ < m; ++s_) out_off[s_ + 1] = out_off[s_] + (int32_t)out_syn[s_].size();
+  out_dst.reserve(out_off[m]);
+  for (int64_t s_ = 0; s_ < m; ++s_) out_dst.insert(out_dst.end(), out_syn[s_].begin(), out_syn[s_].end());
+  for (int64_t s_ = 0; s_ < m; ++s_)
+    for (int32_t j : out_syn[s_]) in_off[j + 1]++;
+  for (int64_t j = 0; j < m; ++j) in_off[j + 1] += in_off[j];
+  in_src.assign(in_off[m], 0);
+  {
+    std::vector<int32_t> fill(in_off.begin(), in_off.end() - 1);
+    for (int64_t s_ = 0; s_ < m; ++s_)
+      for (int32_t j : out_syn[s_]) in_src[fill[j]++] = (int32_t)s_;
+  }
+  SNP_TRY(upload(s, s->d_rule_off, rule_off));
+  SNP_TRY(upload(s, s->d_rules, dr));
+  SNP_TRY(upload(s, s->d_h0, h0));
+  SNP_TRY(upload(s, s->d_h1, h1));
+  SNP_TRY(upload(s, s->d_in_off, in_off));
+  SNP_TRY(upload(s, s->d_in_src, in_src));
+  SNP_TRY(upload(s, s->d_out_off, out_off));
+  SNP_TRY(upload(s, s->d_out_dst, out_dst));
+  SNP_TRY(upload(s, s->d_R0, R0));
+  SNP_TRY(upload(s, s->d_R1, R1));
+  SysView& v = s->view;
+  v.m = (int32_t)m;
+  v.n = n;
+  v.binary_emit = s->binary_emit ? 1 : 0;
+  v.count_max = s->count_max;
+  v.rule_off = s->d_rule_off.as<int32_t>();
+  v.rules = s->d_rules.as<DevRule>();
+  v.h0 = s->d_h0.as<uint64_t>();
+  v.h1 = s->d_h1.as<uint64_t>();
+  v.in_off = s->d_in_off.as<int32_t>();
+  v.in_src = s->d_in_src.as<int32_t>();
+  v.out_off = s->d_out_off.as<int32_t>();
+  v.out_dst = s->d_out_dst.as<int32_t>();
+  v.R0 = s->d_R0.as<uint64_t>();
+  v.R1 = s->d_R1.as<uint64_t>();
+  SNP_TRY(s->counters_dev.ensure(sizeof(DevCounters), false));
+  CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  s->own_stream = true;
+  CUDA_TRY(cudaEventCreate(&s->ev0));
+  CUDA_TRY(cudaEventCreate(&s->ev1));
+  return SNP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exploration
+// ---------------------------------------------------------------------------
+snp_status reset_state(snp_system* s) {
+  for (double& x : s->prof_ms) x = 0;
+  s->marks.clear();
+  s->ev_used = 0;
+  s->levels.clear();
+  s->counters.clear();
+  s->n_visited = 0;
+  s->total_T = 0;
+  s->digest = 0;
+  s->begun = false;
+  s->generation++;
+  s->halting_current_valid = false;
+  if (s->vis_cap) CUDA_TRY(cudaMemsetAsync(s->vis.p, 0xFF, s->vis_cap * sizeof(Slot), s->stream));
+  return SNP_OK;
+}
+
+snp_status zero_counters(snp_system* s) {
+  CUDA_TRY(cudaMemsetAsync(s->counters_dev.p, 0, sizeof(DevCounters), s->stream));
+  return SNP_OK;
+}
+
+DevCounters* dc(snp_system* s) { return s->counters_dev.as<DevCounters>(); }
+
+snp_status begin_impl(snp_system* s, const snp_configs* level0) {
+  SNP_TRY(reset_state(s));
+  snp_configs c0{};
+  if (!level0) {
+    c0.data = s->C0.data();
+    c0.n_configs = 1;
+    c0.elem_bytes = 4;
+    c0.layout = SNP_LAYOUT_ROW_MAJOR;
+    c0.on_device = 0;
+    level0 = &c0;
+  }
+  const int64_t F0 = level0->n_configs, m = s->m;
+  if (F0 < 1 || F0 > 0x7FFFFFFFLL || !level0->data) return fail(SNP_E_ARG, "level0: need 1 <= n_configs < 2^31 and data");
+  if (level0->elem_bytes != 1 && level0->elem_bytes != 2 && level0->elem_bytes != 4) return fail(SNP_E_ARG, "level0: elem_bytes");
+  if (level0->layout != SNP_LAYOUT_ROW_MAJOR && level0->layout != SNP_LAYOUT_NEURON_MAJOR) return fail(SNP_E_ARG, "level0: layout");
+  const int64_t ld = level0->ld ? level0->ld : (level0->layout == SNP_LAYOUT_ROW_MAJOR ? m : F0);
+  const size_t in_bytes = (size_t)(level0->layout == SNP_LAYOUT_ROW_MAJOR ? (F0 - 1) * ld + m : (m - 1) * ld + F0) *
+                          level0->elem_bytes;
+  // stage host input on the device
+  DBuf staged;
+  const void* src = level0->data;
+  if (!level0->on_device) {
+    SNP_TRY(staged.ensure(in_bytes, false));
+    CUDA_TRY(cudaMemcpyAsync(staged.p, level0->data, in_bytes, cudaMemcpyHostToDevice, s->stream));
+    src = staged.p;
+  }
+  SNP_TRY(zero_counters(s));
+  const int64_t pitch = round_pitch(F0);
+  DBuf raw;
+  SNP_TRY(take_buffer(s, (size_t)m * pitch * s->bytes, &raw));
+  int32_t* err = &dc(s)->err;
+  launch_import(src, level0->elem_bytes, level0->layout, ld, F0, (int32_t)m, raw.p, s->bytes, pitch, s->count_max, err,
+                s->stream);
+  CUDA_TRY(cudaGetLastError());
+  // fingerprints of level 0
+  DBuf fp0, fp1;
+  SNP_TRY(fp0.ensure(F0 * 8, false));
+  SNP_TRY(fp1.ensure(F0 * 8, false));
+  launch_fingerprint(s->view, s->bytes, raw.p, pitch, F0, fp0.as<uint64_t>(), fp1.as<uint64_t>(), s->stream);
+  // dedup level 0: first occurrence wins (tags = index)
+  SNP_TRY(ensure_children(s, (uint64_t)F0));
+  SNP_TRY(ensure_ltab(s, (uint64_t)F0));
+  SNP_TRY(ensure_visited(s, (uint64_t)F0));
+  const uint64_t lslots = next_pow2(std::max<uint64_t>(1024, 2 * (uint64_t)F0));
+  Tables tb = tables(s, lslots);
+  ChildArrays C = child_arrays(s);
+  CUDA_TRY(cudaMemcpyAsync(C.cfp0, fp0.p, F0 * 8, cudaMemcpyDeviceToDevice, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(C.cfp1, fp1.p, F0 * 8, cudaMemcpyDeviceToDevice, s->stream));
+  launch_dedup(C, (uint64_t)F0, 0, tb, 0, err, s->stream);
+  launch_winners(C, (uint64_t)F0, 0, tb, 0, 0, &dc(s)->n_new, s->stream);
+  launch_keep(C, (uint64_t)F0, 0, tb, 0, 0, s->stream);
+  launch_exclusive_scan(s->scan_tmp.p, s->scan_tmp.bytes, C.kept, C.kpos, F0 + 1, s->stream);
+  CUDA_TRY(cudaGetLastError());
+  DevCounters hc;
+  SNP_TRY(read_counters(s, &hc));
+  SNP_TRY(check_err(hc.err));
+  if (s->opt.dedup == 0 && (int64_t)hc.n_new < F0) {
+    launch_verify_level0(s->bytes, raw.p, pitch, (int32_t)m, C, (uint64_t)F0, tb, err, s->stream);
+    CUDA_TRY(cudaGetLastError());
+    SNP_TRY(read_counters(s, &hc));
+    SNP_TRY(check_err(hc.err));
+  }
+  const int64_t K = (int64_t)hc.n_new;
+  auto L = std::make_unique<Level>();
+  SNP_TRY(alloc_level_meta(L.get(), K));
+  SNP_TRY(ensure_visited(s, (uint64_t)K));
+  tb = tables(s, lslots);
+  SNP_TRY(s->src_index.ensure(std::max<int64_t>(K, 1) * 8));
+  NextArrays N{nullptr, 0, L->parent.as<int64_t>(), L->t.as<uint64_t>(), L->fp0.as<uint64_t>(), L->fp1.as<uint64_t>()};
+  launch_level0_compact(C.verdict, C.kept, C.kpos, F0, fp0.as<uint64_t>(), fp1.as<uint64_t>(), N,
+                        s->src_index.as<uint64_t>(), tb, err, s->stream);
+  if (K == F0) {
+    L->data = std::move(raw);
+    L->pitch = pitch;
+  } else {
+    L->pitch = round_pitch(K);
+    SNP_TRY(take_buffer(s, (size_t)m * L->pitch * s->bytes, &L->data));
+    launch_gather_columns(s->bytes, raw.p, pitch, s->src_index.as<uint64_t>(), K, (int32_t)m, L->data.p, L->pitch,
+                          s->stream);
+  }
+  N.data = L->data.p;
+  N.pitch = L->pitch;
+  launch_digest(N, K, 0, &dc(s)->digest, s->stream);
+  CUDA_TRY(cudaGetLastError());
+  SNP_TRY(read_counters(s, &hc));
+  SNP_TRY(check_err(hc.err));
+  L->F = K;
+  s->digest += hc.digest;
+  s->n_visited = K;
+  s->levels.push_back(std::move(L));
+  s->begun = true;
+  return SNP_OK;
+}
+
+snp_status classify_level(snp_system* s, Level* L) {
+  // halting flags of a level that is not expanded (reading A5)
+  if (L->F == 0) return SNP_OK;
+  SNP_TRY(zero_counters(s));
+  ExpandOut O{};
+  O.halting = L->halting.as<uint8_t>();
+  O.n_halting = &dc(s)->n_halting;
+  O.err = &dc(s)->err;
+  O.classify_only = 1;
+  LevelView LV{L->data.p, L->F, L->pitch, L->fp0.as<uint64_t>(), L->fp1.as<uint64_t>()};
+  launch_expand(s->view, s->bytes, LV, O, s->stream);
+  CUDA_TRY(cudaGetLastError());
+  return sync(s);
+}
+
+snp_status advance_impl(snp_system* s, snp_level_counters* out) {
+  snp_level_counters lc{};
+  Level* cur = s->levels.back().get();
+  const int64_t F = cur->F, m = s->m;
+  if (F == 0) {
+    if (out) *out = lc;
+    return SNP_OK;
+  }
+  if (!cur->has_data()) return fail(SNP_E_STATE, "current level has no data");
+  cudaStream_t st = s->stream;
+  CUDA_TRY(cudaEventRecord(s->ev0, st));
+  SNP_TRY(zero_counters(s));
+  int32_t* err = &dc(s)->err;
+  // ---- K-a expand
+  const int64_t n_tiles = (F + TILE - 1) / TILE;
+  SNP_TRY(s->psi.ensure((F + 1) * 8));
+  SNP_TRY(s->off.ensure((F + 1) * 8));
+  SNP_TRY(s->fpb0.ensure(F * 8));
+  SNP_TRY(s->fpb1.ensure(F * 8));
+  SNP_TRY(s->ndc.ensure(F * 4));
+  SNP_TRY(s->nd.ensure((size_t)F * KMAX * 8));
+  ExpandOut O{};
+  O.psi = s->psi.as<uint64_t>();
+  O.fpb0 = s->fpb0.as<uint64_t>();
+  O.fpb1 = s->fpb1.as<uint64_t>();
+  O.ndc = s->ndc.as<int32_t>();
+  O.nd = s->nd.as<uint64_t>();
+  O.halting = cur->halting.as<uint8_t>();
+  O.n_halting = &dc(s)->n_halting;
+  O.err = err;
+  if (s->binary_emit) {
+    O.ebits_ld = n_tiles * 32;
+    SNP_TRY(s->ebits.ensure((size_t)((m + 7) / 8) * O.ebits_ld * 4));
+    O.ebits = s->ebits.as<uint32_t>();
+  } else {
+    O.evals_ld = round_pitch(F);
+    SNP_TRY(s->evals.ensure((size_t)m * O.evals_ld * 4));
+    O.evals = s->evals.as<int32_t>();
+  }
+  CUDA_TRY(cudaMemsetAsync(O.psi + F, 0, 8, st));
+  LevelView LV{cur->data.p, F, cur->pitch, cur->fp0.as<uint64_t>(), cur->fp1.as<uint64_t>()};
+  phase_begin(s, 0);
+  launch_expand(s->view, s->bytes, LV, O, st);
+  phase_end(s);
+  // ---- K-b offsets
+  SNP_TRY(s->scan_tmp.ensure(scan_temp_bytes(F + 1) + 256));
+  phase_begin(s, 1);
+  launch_exclusive_scan(s->scan_tmp.p, s->scan_tmp.bytes, O.psi, s->off.as<uint64_t>(), F + 1, st);
+  phase_end(s);
+  CUDA_TRY(cudaGetLastError());
+  uint64_t T = 0;
+  CUDA_TRY(cudaMemcpyAsync(&T, s->off.as<uint64_t>() + F, 8, cudaMemcpyDeviceToHost, st));
+  DevCounters hc;
+  SNP_TRY(read_counters(s, &hc));
+  SNP_TRY(check_err(hc.err));
+  lc.parents = F;
+  lc.halting = (int64_t)hc.n_halting;
+  lc.T = (int64_t)T;
+  s->halting_current_valid = true;
+  if (s->opt.max_transitions > 0 && (int64_t)T > s->opt.max_transitions)
+    return fail(SNP_E_CAPACITY, "level %zu: %llu transitions exceed the budget", s->levels.size() - 1, (unsigned long long)T);
+  if (T > 0xFFFFFFFFFFULL) return fail(SNP_E_CAPACITY, "level has more than 2^40 transitions");
+  const uint64_t* off = s->off.as<uint64_t>();
+  // ---- K-b/K-d children, keys, dedup
+  auto next = std::make_unique<Level>();
+  int64_t K = 0;
+  uint64_t tau = 0;
+  if (T > 0) {
+    SNP_TRY(ensure_children(s, T));
+    SNP_TRY(ensure_ltab(s, T));
+    const uint64_t lslots = next_pow2(std::max<uint64_t>(1024, 2 * T));
+    ChildArrays C = child_arrays(s);
+    Tables tb = tables(s, lslots);
+    const uint64_t tag_base = 0;
+    phase_begin(s, 1);
+    launch_child_parent(off, F, C.cpar, st);
+    launch_child_keys(s->view, off, O, T, C, st);
+    phase_end(s);
+    phase_begin(s, 2);
+    launch_dedup(C, T, tag_base, tb, 1, err, st);
+    launch_winners(C, T, tag_base, tb, 0, 0, &dc(s)->n_new, st);
+    phase_end(s);
+    CUDA_TRY(cudaGetLastError());
+    SNP_TRY(read_counters(s, &hc));
+    SNP_TRY(check_err(hc.err));
+    const int64_t n_new = (int64_t)hc.n_new;
+    lc.n_new = n_new;
+    const int thin = s->opt.frontier_target > 0 && n_new > s->opt.frontier_target;
+    if (thin) {
+      unsigned __int128 num = (unsigned __int128)(uint64_t)s->opt.frontier_target << 64;
+      tau = (uint64_t)(num / (unsigned __int128)(uint64_t)n_new);
+    }
+    lc.tau = tau;
+    phase_begin(s, 2);
+    launch_keep(C, T, tag_base, tb, tau, thin, st);
+    launch_exclusive_scan(s->scan_tmp.p, s->scan_tmp.bytes, C.kept, C.kpos, (int64_t)T + 1, st);
+    phase_end(s);
+    CUDA_TRY(cudaGetLastError());
+    uint64_t Kh = 0;
+    CUDA_TRY(cudaMemcpyAsync(&Kh, C.kpos + T, 8, cudaMemcpyDeviceToHost, st));
+    SNP_TRY(sync(s));
+    K = (int64_t)Kh;
+    // ---- next level buffers + visited insert
+    next->F = K;
+    next->pitch = round_pitch(K);
+    SNP_TRY(alloc_level_meta(next.get(), K));
+    SNP_TRY(ensure_visited(s, (uint64_t)(s->n_visited + K)));
+    tb = tables(s, lslots);
+    NextArrays N{nullptr, next->pitch, next->parent.as<int64_t>(), next->t.as<uint64_t>(), next->fp0.as<uint64_t>(),
+                 next->fp1.as<uint64_t>()};
+    phase_begin(s, 2);
+    launch_compact(C, off, T, N, tb, (uint64_t)s->levels.size() << 40, err, st);
+    phase_end(s);
+    if (K > 0) {
+      SNP_TRY(take_buffer(s, (size_t)m * next->pitch * s->bytes, &next->data));
+      N.data = next->data.p;
+      // ---- K-c materialize kept children
+      SNP_TRY(s->kq_off.ensure((F + 1) * 8));
+      const uint64_t ovf_cap = 1ULL << 22;
+      SNP_TRY(s->ovf.ensure(ovf_cap * 8));
+      phase_begin(s, 3);
+      launch_kq_off(off, C.kpos, F, s->kq_off.as<uint64_t>(), st);
+      launch_materialize(s->view, s->bytes, LV, O, s->kq_off.as<uint64_t>(), N, s->ovf.as<uint64_t>(),
+                         &dc(s)->n_ovf, ovf_cap, st);
+      launch_patch(s->view, s->bytes, LV, O, N, K, err, st);
+      phase_end(s);
+      CUDA_TRY(cudaGetLastError());
+      SNP_TRY(read_counters(s, &hc));
+      if (hc.n_ovf > ovf_cap) return fail(SNP_E_CAPACITY, "too many counts at the storage limit (%llu)", hc.n_ovf);
+      if (hc.n_ovf) {
+        phase_begin(s, 3);
+        launch_overflow_fix(s->view, s->bytes, LV, O, s->kq_off.as<uint64_t>(), N, s->ovf.as<uint64_t>(), hc.n_ovf,
+                            err, st);
+        phase_end(s);
+        CUDA_TRY(cudaGetLastError());
+      }
+      launch_digest(N, K, (uint64_t)s->levels.size(), &dc(s)->digest, st);
+    }
+    if (s->opt.dedup == 0) {
+      SNP_TRY(update_stored_table(s));
+      phase_begin(s, 4);
+      launch_verify(s->view, s->bytes, LV, O, off, C, T, tag_base, tb, s->stored.as<StoredLevel>(), err, st);
+      phase_end(s);
+      CUDA_TRY(cudaGetLastError());
+    }
+  }
+  CUDA_TRY(cudaEventRecord(s->ev1, st));
+  SNP_TRY(read_counters(s, &hc));
+  phase_collect(s);
+  SNP_TRY(check_err(hc.err));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  lc.kept = K;
+  lc.ms = ms;
+  s->digest += hc.digest;
+  s->n_visited += K;
+  s->total_T += (int64_t)T;
+  s->counters.push_back(lc);
+  if (!retain_levels(s)) release_level_data(s, cur);
+  s->levels.push_back(std::move(next));
+  s->halting_current_valid = false;
+  if (out) *out = lc;
+  return SNP_OK;
+}
+
+snp_status snapshot(snp_system* s, snp_tree** out) {
+  // halting flags of the last level
+  Level* last = s->levels.back().get();
+  if (!s->halting_current_valid && last->F > 0) {
+    if (!last->has_data()) return fail(SNP_E_STATE, "last level has no data");
+    SNP_TRY(classify_level(s, last));
+    s->halting_current_valid = true;
+  }
+  auto t = std::make_unique<snp_tree>();
+  t->sys = s;
+  t->generation = s->generation;
+  t->m = s->m;
+  t->n = s->n;
+  t->counters = s->counters;
+  int64_t total = 0;
+  t->level_offsets.push_back(0);
+  for (auto& L : s->levels) {
+    total += L->F;
+    t->level_offsets.push_back(total);
+  }
+  t->parent.resize(total);
+  t->t.resize(total);
+  t->halting.resize(total);
+  t->fp.resize(2 * total);
+  std::vector<uint64_t> f0, f1;
+  int64_t o = 0;
+  for (auto& L : s->levels) {
+    const int64_t F = L->F;
+    if (F) {
+      f0.resize(F);
+      f1.resize(F);
+      CUDA_TRY(cudaMemcpyAsync(t->parent.data() + o, L->parent.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(cudaMemcpyAsync(t->t.data() + o, L->t.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(cudaMemcpyAsync(t->halting.data() + o, L->halting.p, F, cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(cudaMemcpyAsync(f0.data(), L->fp0.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(cudaMemcpyAsync(f1.data(), L->fp1.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+      SNP_TRY(sync(s));
+      for (int64_t i = 0; i < F; ++i) {
+        t->fp[2 * (o + i)] = f0[i];
+        t->fp[2 * (o + i) + 1] = f1[i];
+      }
+    }
+    o += F;
+  }
+  *out = t.release();
+  return SNP_OK;
+}
+
+snp_status tree_check(const snp_tree* t, bool need_data) {
+  if (!t) return fail(SNP_E_ARG, "tree is NULL");
+  if (need_data) {
+    if (!t->sys || t->sys->generation != t->generation) return fail(SNP_E_STATE, "the system has started another exploration since this tree was taken");
+    for (size_t i = 0; i + 1 < t->level_offsets.size() && i < t->sys->levels.size(); ++i)
+      if (t->sys->levels[i]->F && !t->sys->levels[i]->has_data())
+        return fail(SNP_E_STATE, "configurations were not retained (set keep_tree = 1)");
+  }
+  return SNP_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int snp_abi_version(void) { return SNP_ABI_VERSION; }
+const char* snp_last_error(void) { return g_err.c_str(); }
+
+snp_status snp_load(const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const int32_t* C0, int64_t m,
+                    const snp_options* opt, snp_system** out) {
+  if (!M || !C0 || !out || m < 1 || m > 0x7FFFFFFF || n_rules < 0 || (n_rules > 0 && !rules))
+    return fail(SNP_E_ARG, "snp_load: bad arguments");
+  if (M->n_rules != n_rules || M->n_neurons != m) return fail(SNP_E_ARG, "snp_load: matrix shape != (n_rules, m)");
+  if (!M->dense && n_rules > 0 && (!M->row_ptr || !M->col || !M->val)) return fail(SNP_E_ARG, "snp_load: no matrix data");
+  snp_options o{};
+  o.count_bits = 32;
+  o.dedup = 0;
+  o.keep_tree = 1;
+  o.fp_seed[0] = 0x5EED0;
+  o.fp_seed[1] = 0x5EED1;
+  if (opt) o = *opt;
+  if (o.count_bits != 8 && o.count_bits != 16 && o.count_bits != 32) return fail(SNP_E_ARG, "count_bits must be 8, 16 or 32");
+  if (o.dedup != 0 && o.dedup != 1) return fail(SNP_E_ARG, "dedup must be 0 or 1");
+  if (o.frontier_target < 0 || o.max_transitions < 0) return fail(SNP_E_ARG, "negative frontier_target / max_transitions");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(SNP_E_CUDA, "no CUDA device: the engine has no CPU fallback");
+  }
+  auto s = std::make_unique<snp_system>();
+  s->m = m;
+  s->opt = o;
+  s->bytes = o.count_bits / 8;
+  s->count_max = o.count_bits == 8 ? 255 : o.count_bits == 16 ? 65535 : 0x7FFFFFFF;
+  snp_status st = load_impl(s.get(), M, rules, n_rules, C0);
+  if (st != SNP_OK) return st;
+  *out = s.release();
+  return SNP_OK;
+}
+
+void snp_system_free(snp_system* s) {
+  if (!s) return;
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  s->levels.clear();
+  s->spare.clear();
+  if (s->ev0) cudaEventDestroy(s->ev0);
+  if (s->ev1) cudaEventDestroy(s->ev1);
+  for (auto e : s->ev_pool) cudaEventDestroy(e);
+  if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+snp_status snp_set_stream(snp_system* s, void* stream) {
+  if (!s) return fail(SNP_E_ARG, "NULL system");
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (s->own_stream) cudaStreamDestroy(s->stream);
+  if (stream) {
+    s->stream = (cudaStream_t)stream;
+    s->own_stream = false;
+  } else {
+    CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    s->own_stream = true;
+  }
+  return SNP_OK;
+}
+
+snp_status snp_begin(snp_system* s, const snp_configs* level0) {
+  if (!s) return fail(SNP_E_ARG, "NULL system");
+  snp_status st = begin_impl(s, level0);
+  if (st != SNP_OK) s->begun = false;
+  return st;
+}
+
+snp_status snp_advance(snp_system* s, snp_level_counters* counters) {
+  if (!s) return fail(SNP_E_ARG, "NULL system");
+  if (!s->begun) return fail(SNP_E_STATE, "snp_advance before snp_begin (or after an error)");
+  snp_status st = advance_impl(s, counters);
+  if (st != SNP_OK) s->begun = false;
+  return st;
+}
+
+int64_t snp_frontier_size(const snp_system* s) { return (s && !s->levels.empty()) ? s->levels.back()->F : 0; }
+int32_t snp_depth(const snp_system* s) { return s ? (int32_t)s->levels.size() - 1 : -1; }
+
+snp_status snp_summary(const snp_system* s, int64_t* n_configs, int64_t* transitions, uint64_t* digest) {
+  if (!s) return fail(SNP_E_ARG, "NULL system");
+  if (n_configs) *n_configs = s->n_visited;
+  if (transitions) *transitions = s->total_T;
+  if (digest) *digest = s->digest;
+  return SNP_OK;
+}
+
+snp_status snp_set_profiling(snp_system* s, int32_t on) {
+  if (!s) return fail(SNP_E_ARG, "NULL system");
+  s->profiling = on != 0;
+  return SNP_OK;
+}
+
+snp_status snp_profile(const snp_system* s, double* ms) {
+  if (!s || !ms) return fail(SNP_E_ARG, "snp_profile: bad arguments");
+  for (int i = 0; i < SNP_NUM_PHASES; ++i) ms[i] = s->prof_ms[i];
+  return SNP_OK;
+}
+
+int64_t snp_kernel_launches(void) { return snp::g_kernel_launches.load(); }
+
+int64_t snp_level_size(const snp_system* s, int32_t level) {
+  if (!s || level < 0 || level >= (int32_t)s->levels.size()) return -1;
+  return s->levels[level]->F;
+}
+
+snp_status snp_level_edges(snp_system* s, int32_t level, int64_t* parent, uint64_t* t, uint8_t* halting,
+                           uint64_t* fp2) {
+  if (!s || level < 0 || level >= (int32_t)s->levels.size()) return fail(SNP_E_ARG, "snp_level_edges: bad level");
+  Level* L = s->levels[level].get();
+  const int64_t F = L->F;
+  if (!F) return SNP_OK;
+  if (parent) CUDA_TRY(cudaMemcpyAsync(parent, L->parent.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+  if (t) CUDA_TRY(cudaMemcpyAsync(t, L->t.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+  if (halting) CUDA_TRY(cudaMemcpyAsync(halting, L->halting.p, F, cudaMemcpyDeviceToHost, s->stream));
+  if (fp2) {
+    std::vector<uint64_t> f0(F), f1(F);
+    CUDA_TRY(cudaMemcpyAsync(f0.data(), L->fp0.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(f1.data(), L->fp1.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+    SNP_TRY(sync(s));
+    for (int64_t i = 0; i < F; ++i) { fp2[2 * i] = f0[i]; fp2[2 * i + 1] = f1[i]; }
+  }
+  return sync(s);
+}
+
+snp_status snp_level_columns(snp_system* s, int32_t level, const int64_t* idx, int64_t n, int32_t* out) {
+  if (!s || level < 0 || level >= (int32_t)s->levels.size() || (n > 0 && (!idx || !out)))
+    return fail(SNP_E_ARG, "snp_level_columns: bad arguments");
+  Level* L = s->levels[level].get();
+  if (!L->has_data()) return fail(SNP_E_STATE, "level %d counts are not retained", level);
+  std::vector<uint64_t> hidx(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (idx[i] < 0 || idx[i] >= L->F) return fail(SNP_E_ARG, "snp_level_columns: index out of range");
+    hidx[i] = (uint64_t)idx[i];
+  }
+  if (n == 0) return SNP_OK;
+  DBuf didx, cols, rows;
+  const int64_t pitch = round_pitch(n);
+  SNP_TRY(didx.ensure(n * 8, false));
+  SNP_TRY(cols.ensure((size_t)s->m * pitch * s->bytes, false));
+  SNP_TRY(rows.ensure((size_t)n * s->m * 4, false));
+  CUDA_TRY(cudaMemcpyAsync(didx.p, hidx.data(), n * 8, cudaMemcpyHostToDevice, s->stream));
+  launch_gather_columns(s->bytes, L->data.p, L->pitch, didx.as<uint64_t>(), n, (int32_t)s->m, cols.p, pitch, s->stream);
+  launch_export(cols.p, s->bytes, pitch, n, (int32_t)s->m, rows.as<int32_t>(), s->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(out, rows.p, (size_t)n * s->m * 4, cudaMemcpyDeviceToHost, s->stream));
+  return sync(s);
+}
+
+snp_status snp_explore(snp_system* s, const snp_configs* level0, int32_t depth, snp_tree** out) {
+  if (!s || !out || depth < 0) return fail(SNP_E_ARG, "snp_explore: bad arguments");
+  snp_status st = snp_begin(s, level0);
+  if (st != SNP_OK) return st;
+  for (int32_t d = 0; d < depth; ++d) {
+    if (s->levels.back()->F == 0) break;
+    st = snp_advance(s, nullptr);
+    if (st != SNP_OK) return st;
+    if (s->levels.back()->F == 0) break;
+  }
+  return snapshot(s, out);
+}
+
+snp_status snp_step(snp_system* s, const snp_configs* frontier, snp_tree** out) {
+  return snp_explore(s, frontier, 1, out);
+}
+
+int32_t snp_tree_num_levels(const snp_tree* t) { return t ? (int32_t)t->level_offsets.size() - 1 : 0; }
+int64_t snp_tree_num_configs(const snp_tree* t) { return t ? t->level_offsets.back() : 0; }
+
+snp_status snp_tree_level_offsets(const snp_tree* t, int64_t* out) {
+  SNP_TRY(tree_check(t, false));
+  std::copy(t->level_offsets.begin(), t->level_offsets.end(), out);
+  return SNP_OK;
+}
+
+snp_status snp_tree_edges(const snp_tree* t, int64_t* parent, uint64_t* tt, uint8_t* halting, uint64_t* fp2) {
+  SNP_TRY(tree_check(t, false));
+  if (parent) std::copy(t->parent.begin(), t->parent.end(), parent);
+  if (tt) std::copy(t->t.begin(), t->t.end(), tt);
+  if (halting) std::copy(t->halting.begin(), t->halting.end(), halting);
+  if (fp2) std::copy(t->fp.begin(), t->fp.end(), fp2);
+  return SNP_OK;
+}
+
+snp_status snp_tree_counters(const snp_tree* t, snp_level_counters* out) {
+  SNP_TRY(tree_check(t, false));
+  std::copy(t->counters.begin(), t->counters.end(), out);
+  return SNP_OK;
+}
+
+snp_status snp_tree_configs(const snp_tree* t, int32_t* out) {
+  SNP_TRY(tree_check(t, true));
+  snp_system* s = t->sys;
+  DBuf tmp;
+  const int32_t nl = snp_tree_num_levels(t);
+  for (int32_t L = 0; L < nl; ++L) {
+    const Level* lv = s->levels[L].get();
+    if (!lv->F) continue;
+    SNP_TRY(tmp.ensure((size_t)lv->F * s->m * 4));
+    launch_export(lv->data.p, s->bytes, lv->pitch, lv->F, (int32_t)s->m, tmp.as<int32_t>(), s->stream);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out + t->level_offsets[L] * s->m, tmp.p, (size_t)lv->F * s->m * 4,
+                             cudaMemcpyDeviceToHost, s->stream));
+    SNP_TRY(sync(s));
+  }
+  return SNP_OK;
+}
+
+snp_status snp_tree_spiking_vectors(const snp_tree* t, int32_t level, uint8_t* S_out) {
+  SNP_TRY(tree_check(t, true));
+  snp_system* s = t->sys;
+  if (level < 1 || level >= snp_tree_num_levels(t)) return fail(SNP_E_ARG, "level must be in [1, num_levels)");
+  const Level* par = s->levels[level - 1].get();
+  const Level* lv = s->levels[level].get();
+  if (!lv->F) return SNP_OK;
+  DBuf tmp;
+  SNP_TRY(tmp.ensure((size_t)lv->F * s->n));
+  launch_spiking_vectors(s->view, s->bytes, par->data.p, par->pitch, lv->parent.as<int64_t>(), lv->t.as<uint64_t>(),
+                         lv->F, tmp.as<uint8_t>(), s->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(S_out, tmp.p, (size_t)lv->F * s->n, cudaMemcpyDeviceToHost, s->stream));
+  return sync(s);
+}
+
+void snp_tree_free(snp_tree* t) { delete t; }
+
+}  // extern "C"
