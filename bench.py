@@ -274,7 +274,8 @@ def run_native(args, rank, world):
                      "traffic": ncu_traffic(dom), "peak_source": peak_src},
         "step_roofline": {"algorithmic_GB_per_step": sb / len(levels) / 1e9,
                           "achieved": sb / (elapsed_ms / 1e3) / 1e9, "frac": sb / (elapsed_ms / 1e3) / 1e9 / peak},
-        "phase_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
+        "phase_ms_per_step": {**{k: v / args.steps for k, v in phase_ms.items()},
+                              "other": elapsed_ms / args.steps - sum(phase_ms.values()) / args.steps},
         "levels": [{k: c[k] for k in ("parents", "halting", "T", "n_new", "kept")} | {"ms": round(c["ms"], 3)}
                    for c in levels],
         "digest": f"{digest:016x}", "gpu_launches": launches, "clocks": clk,

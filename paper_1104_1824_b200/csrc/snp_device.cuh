@@ -1,14 +1,18 @@
 // snp_device.cuh — device-side data model and helpers of the SNP engine.
 //
 // Layout in HBM:
-//   * a frontier is NEURON-MAJOR: element (s, p) = spike count of neuron s in
-//     configuration p, at data[s * pitch + p], stored as uint8/uint16/int32
-//     (count_bits, reading A16).  A warp owns a tile of 128 consecutive
-//     configurations (4 per lane) and walks the neurons, so every rule
-//     descriptor / in-synapse index it reads is warp-uniform (broadcast) and
-//     every count load is a coalesced 128-element row segment.
+//   * a frontier is BLOCKED neuron-major: configurations are grouped in
+//     blocks of PB = 64; block b holds the m × 64 counts of its configurations
+//     neuron by neuron, so element (configuration p, neuron s) lives at
+//         ((p / 64) · m + s) · 64 + p % 64
+//     and a block is one contiguous m·64·w-byte stream.  Kernels that walk
+//     the neurons of a group of configurations (K-a, K-c) read whole
+//     contiguous blocks; every rule descriptor / synapse index is uniform
+//     across the lanes that share a neuron.
 //   * rules are grouped per neuron (rule_off[s] .. rule_off[s+1]) in the
 //     paper's total order.
+//   * per-neuron outcome tables: for a count v the first
+//     applicable rule, whether it spikes, and whether ≥ 2 rules apply.
 //   * the synapse graph is stored twice: in-CSR by target (the gather of the
 //     transition) and out-CSR by source (the sparse ND patches).
 #pragma once
@@ -18,9 +22,11 @@
 namespace snp {
 
 constexpr int KMAX = 64;                    // nondeterministic neurons recorded per parent
-constexpr int TILE = 128;                   // configurations per warp tile (4 per lane)
+constexpr int PB = 64;                      // configurations per storage block
 constexpr uint64_t PSI_LIMIT = 1ULL << 62;  // Ψ above this is SNP_E_CAPACITY
 constexpr uint64_t EMPTY = ~0ULL;           // empty hash-slot key word
+constexpr int TABW_MAX = 512;               // compact outcome-table width limit
+constexpr int MAX_TABLE_RULES = 15;         // rules per neuron representable in a table entry
 
 // error bits raised by kernels (ORed into a device word)
 enum : int32_t {
@@ -29,6 +35,10 @@ enum : int32_t {
   ERR_COLLISION = 4,
   ERR_TABLE_FULL = 8,
 };
+
+__host__ __device__ __forceinline__ int64_t eidx(int64_t p, int32_t s, int32_t m) {
+  return ((p >> 6) * (int64_t)m + s) * PB + (p & (PB - 1));
+}
 
 // Applicability of one rule as an interval + residue test:
 //   a^v ∈ L(E) && v >= c   <=>   lo <= v <= hi  &&  (v - base) ≡ 0 (mod j)
@@ -48,6 +58,30 @@ __device__ __forceinline__ bool rule_app(const DevRule& r, int32_t v) {
   return r.jmask >= 0 ? ((d & r.jmask) == 0) : (d % r.j == 0);
 }
 
+// Per-neuron table descriptor.  For counts v >= L the outcome repeats with
+// period P (every PERIODIC rule's j divides P; no EXACT rule applies), so
+//   idx(v) = v < L ? v : L + (v - L) mod P.
+// pm = P - 1 when P is a power of two, else -P.  flags: bit 0 = no table
+// (evaluate the rules), bit 1 = some count makes >= 2 rules applicable.
+struct NeuronMeta {
+  int32_t rbase;   // first rule of the neuron
+  int32_t L;
+  int32_t pm;
+  int32_t flags;
+};
+enum : int32_t { NM_GENERIC = 1, NM_ND = 2 };
+// outcome-table entry (uint8): bit 0 = the first applicable rule spikes
+// (p > 0), bit 1 = >= 2 rules applicable, bits 4-7 = first applicable local
+// rule + 1 (0 = none) — pre-shifted so (entry & 0xF0) is the byte offset of
+// that rule's 16-B fingerprint delta in a neuron's 256-B slice.
+enum : uint32_t { TE_EMIT = 1u, TE_ND = 2u, TE_F = 0xF0u };
+
+__device__ __forceinline__ uint32_t table_index(uint32_t v, const NeuronMeta& mt) {
+  if ((int32_t)v < mt.L) return v;
+  uint32_t d = v - (uint32_t)mt.L;
+  return (uint32_t)mt.L + (mt.pm >= 0 ? (d & (uint32_t)mt.pm) : d % (uint32_t)(-mt.pm));
+}
+
 struct SysView {
   int32_t m;
   int32_t binary_emit;   // every p <= 1: emits are one bit per (neuron, config)
@@ -63,6 +97,15 @@ struct SysView {
   const int32_t* out_dst;    // targets j with (s, j) ∈ syn, grouped by source s
   const uint64_t* R0;        // m fingerprint weights (reading A18)
   const uint64_t* R1;
+  // outcome tables (valid when tables_ok)
+  int32_t tables_ok;         // every neuron is tabulated or flagged generic
+  int32_t tabw;              // compact table width (multiple of 16)
+  int32_t full8;             // count_bits == 8: tab_full has 256 entries per neuron
+  int32_t max_indeg;
+  const NeuronMeta* meta;    // m
+  const uint8_t* tab;        // m × tabw   (compact)
+  const uint8_t* tab_full;   // m × 256    (count_bits == 8)
+  const void* ctab;          // m × tabw   consumption of the first rule, storage type
 };
 
 // 128-bit hash slot. key (k0,k1) = 128-bit fingerprint; EMPTY/EMPTY = free.
@@ -90,38 +133,79 @@ __device__ __forceinline__ uint64_t sat_mul(uint64_t a, uint64_t b) {
   return r > PSI_LIMIT ? PSI_LIMIT + 1 : r;
 }
 
+// 8 consecutive counts of one neuron row inside a block (p0 % 8 == 0)
 template <typename T>
-__device__ __forceinline__ void load4(const T* row, int64_t p0, int64_t F, int32_t v[4]);
+__device__ __forceinline__ void load8(const T* data, int64_t p0, int32_t s, int32_t m, int64_t F, uint32_t v[8]);
 
 template <>
-__device__ __forceinline__ void load4<uint8_t>(const uint8_t* row, int64_t p0, int64_t F, int32_t v[4]) {
-  if (p0 + 3 < F) {
-    uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(row + p0));
-    v[0] = w & 0xFF; v[1] = (w >> 8) & 0xFF; v[2] = (w >> 16) & 0xFF; v[3] = w >> 24;
+__device__ __forceinline__ void load8<uint8_t>(const uint8_t* data, int64_t p0, int32_t s, int32_t m, int64_t F,
+                                              uint32_t v[8]) {
+  const uint8_t* row = data + eidx(p0, s, m);
+  if (p0 + 7 < F) {
+    uint2 w = __ldg(reinterpret_cast<const uint2*>(row));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { v[k] = (w.x >> (8 * k)) & 0xFF; v[k + 4] = (w.y >> (8 * k)) & 0xFF; }
   } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = (p0 + k < F) ? (int32_t)row[p0 + k] : 0;
+    for (int k = 0; k < 8; ++k) v[k] = (p0 + k < F) ? row[k] : 0u;
   }
 }
 template <>
-__device__ __forceinline__ void load4<uint16_t>(const uint16_t* row, int64_t p0, int64_t F, int32_t v[4]) {
-  if (p0 + 3 < F) {
-    uint2 w = __ldg(reinterpret_cast<const uint2*>(row + p0));
+__device__ __forceinline__ void load8<uint16_t>(const uint16_t* data, int64_t p0, int32_t s, int32_t m, int64_t F,
+                                               uint32_t v[8]) {
+  const uint16_t* row = data + eidx(p0, s, m);
+  if (p0 + 7 < F) {
+    uint4 w = __ldg(reinterpret_cast<const uint4*>(row));
     v[0] = w.x & 0xFFFF; v[1] = w.x >> 16; v[2] = w.y & 0xFFFF; v[3] = w.y >> 16;
+    v[4] = w.z & 0xFFFF; v[5] = w.z >> 16; v[6] = w.w & 0xFFFF; v[7] = w.w >> 16;
   } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = (p0 + k < F) ? (int32_t)row[p0 + k] : 0;
+    for (int k = 0; k < 8; ++k) v[k] = (p0 + k < F) ? row[k] : 0u;
   }
 }
 template <>
-__device__ __forceinline__ void load4<int32_t>(const int32_t* row, int64_t p0, int64_t F, int32_t v[4]) {
-  if (p0 + 3 < F) {
-    int4 w = __ldg(reinterpret_cast<const int4*>(row + p0));
-    v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+__device__ __forceinline__ void load8<int32_t>(const int32_t* data, int64_t p0, int32_t s, int32_t m, int64_t F,
+                                              uint32_t v[8]) {
+  const int32_t* row = data + eidx(p0, s, m);
+  if (p0 + 7 < F) {
+    int4 a = __ldg(reinterpret_cast<const int4*>(row));
+    int4 b = __ldg(reinterpret_cast<const int4*>(row) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
   } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = (p0 + k < F) ? row[p0 + k] : 0;
+    for (int k = 0; k < 8; ++k) v[k] = (p0 + k < F) ? (uint32_t)row[k] : 0u;
   }
+}
+
+// ---- TMA bulk copies (cp.async.bulk) and mbarriers --------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+// global -> shared bulk copy (bytes % 16 == 0, both addresses 16-aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 }  // namespace snp

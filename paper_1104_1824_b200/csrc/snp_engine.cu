@@ -5,6 +5,8 @@
 // sizes buffers, launches, and reads back per-level counters.  There is no CPU
 // fallback: without a CUDA device every compute call fails with SNP_E_CUDA.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -20,6 +22,25 @@ using namespace snp;
 namespace {
 
 thread_local std::string g_err;
+
+// SNP_TRACE=1: host-side wall time of allocation / synchronisation sections
+// per level, printed to stderr (diagnostics only).
+struct HostTrace {
+  bool on = getenv("SNP_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0;
+  std::string line;
+  void start() { if (on) { t0 = std::chrono::steady_clock::now(); line.clear(); } }
+  void mark(const char* what) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    char buf[64];
+    snprintf(buf, sizeof buf, " %s=%.2f", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    line += buf;
+    t0 = t;
+  }
+  void flush(const char* tag) { if (on) fprintf(stderr, "[snp-trace] %s%s\n", tag, line.c_str()); }
+};
+thread_local HostTrace g_trace;
 
 snp_status fail(snp_status st, const char* fmt, ...) {
   char buf[512];
@@ -59,7 +80,8 @@ uint64_t next_pow2(uint64_t x) {
   return p;
 }
 
-int64_t round_pitch(int64_t F) { return std::max<int64_t>(TILE, (F + TILE - 1) / TILE * TILE); }
+// bytes of a blocked frontier of F configurations (ceil(F/64) blocks of m × 64 counts)
+size_t level_bytes(int64_t F, int64_t m, int32_t w) { return (size_t)((F + PB - 1) / PB) * (size_t)m * PB * w; }
 
 // A growable device allocation.
 struct DBuf {
@@ -96,11 +118,44 @@ struct DBuf {
   template <class U> U* as() const { return reinterpret_cast<U*>(p); }
 };
 
+// A non-owning view into an arena allocation.
+struct DView {
+  void* p = nullptr;
+  template <class U> U* as() const { return reinterpret_cast<U*>(p); }
+};
+
+// Bump allocator for per-level metadata (kept for the whole exploration):
+// a few large cudaMallocs instead of five per level.
+struct Arena {
+  std::vector<DBuf> chunks;
+  size_t chunk = 0, used = 0;
+  snp_status alloc(size_t bytes, DView* out) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    if (chunk < chunks.size() && used + bytes <= chunks[chunk].bytes) {
+      out->p = static_cast<uint8_t*>(chunks[chunk].p) + used;
+      used += bytes;
+      return SNP_OK;
+    }
+    if (chunk + 1 < chunks.size() && bytes <= chunks[chunk + 1].bytes) {
+      ++chunk;
+      used = 0;
+      return alloc(bytes, out);
+    }
+    DBuf b;
+    SNP_TRY(b.ensure(std::max<size_t>(bytes, (size_t)1 << 30), false));
+    chunks.push_back(std::move(b));
+    chunk = chunks.size() - 1;
+    used = 0;
+    return alloc(bytes, out);
+  }
+  void reset() { chunk = 0; used = 0; }
+};
+
 // One level of the tree on the device.
 struct Level {
-  DBuf data;  // m × pitch counts (may be released when not retained)
-  int64_t F = 0, pitch = 0;
-  DBuf fp0, fp1, parent, t, halting;
+  DBuf data;  // blocked counts, ceil(F/64) × m × 64 (may be released when not retained)
+  int64_t F = 0;
+  DView fp0, fp1, parent, t, halting;
   bool has_data() const { return data.p != nullptr; }
 };
 
@@ -131,12 +186,14 @@ struct snp_system {
   bool halting_current_valid = false;
   // hash tables
   DBuf vis, ltab;
-  uint64_t vis_cap = 0, ltab_cap = 0;
+  uint64_t vis_cap = 0, ltab_cap = 0, child_cap = 0;
   // scratch
-  DBuf psi, off, fpb0, fpb1, ndc, nd, halting_tmp, ebits, evals;
+  DBuf psi, off, fpb0, fpb1, ndc, nd, ebits;
+  DBuf d_meta, d_tab, d_tab_full, d_ctab;
   DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   std::vector<DBuf> spare;  // released level buffers kept for reuse
+  Arena arena;              // per-level metadata
   // phase profiling (snp_set_profiling)
   bool profiling = false;
   double prof_ms[SNP_NUM_PHASES] = {0, 0, 0, 0, 0};
@@ -233,7 +290,7 @@ snp_status take_buffer(snp_system* s, size_t bytes, DBuf* out) {
   }
   // free spares before a fresh allocation (they are too small)
   s->spare.clear();
-  return out->ensure(bytes + bytes / 32, false);
+  return out->ensure(bytes + bytes / 16, false);
 }
 
 void release_level_data(snp_system* s, Level* L) {
@@ -244,8 +301,10 @@ void release_level_data(snp_system* s, Level* L) {
 }
 
 snp_status ensure_visited(snp_system* s, uint64_t needed_entries) {
+  // keep the load <= 1/2; grow 4x at a time so a long run rehashes rarely
+  if (2 * needed_entries <= s->vis_cap) return SNP_OK;
   uint64_t want = next_pow2(std::max<uint64_t>(1024, 2 * needed_entries));
-  if (want <= s->vis_cap) return SNP_OK;
+  if (s->vis_cap) want = std::max(want, 4 * s->vis_cap);
   DBuf nt;
   SNP_TRY(nt.ensure(want * sizeof(Slot), false));
   CUDA_TRY(cudaMemsetAsync(nt.p, 0xFF, want * sizeof(Slot), s->stream));
@@ -275,16 +334,20 @@ Tables tables(snp_system* s, uint64_t ltab_slots) {
 }
 
 snp_status ensure_children(snp_system* s, uint64_t T) {
-  SNP_TRY(s->cpar.ensure(T * 4 + 16));
-  SNP_TRY(s->cfp0.ensure(T * 8 + 16));
-  SNP_TRY(s->cfp1.ensure(T * 8 + 16));
-  SNP_TRY(s->verdict.ensure(T + 16));
-  SNP_TRY(s->cslot.ensure(T * 8 + 16));
-  SNP_TRY(s->cref.ensure(T * 8 + 16));
-  SNP_TRY(s->kept.ensure((T + 1) * 8 + 16));
-  SNP_TRY(s->kpos.ensure((T + 1) * 8 + 16));
-  size_t tb = scan_temp_bytes((int64_t)T + 1);
-  SNP_TRY(s->scan_tmp.ensure(tb + 256));
+  // per-level T grows along a run: reallocate rarely, to twice the need
+  if (T > s->child_cap) {
+    const uint64_t c = std::max<uint64_t>(2 * T, 4096);
+    SNP_TRY(s->cpar.ensure(c * 4 + 16, false));
+    SNP_TRY(s->cfp0.ensure(c * 8 + 16, false));
+    SNP_TRY(s->cfp1.ensure(c * 8 + 16, false));
+    SNP_TRY(s->verdict.ensure(c + 16, false));
+    SNP_TRY(s->cslot.ensure(c * 8 + 16, false));
+    SNP_TRY(s->cref.ensure(c * 8 + 16, false));
+    SNP_TRY(s->kept.ensure((c + 1) * 8 + 16, false));
+    SNP_TRY(s->kpos.ensure((c + 1) * 8 + 16, false));
+    SNP_TRY(s->scan_tmp.ensure(scan_temp_bytes((int64_t)c + 1) + 256, false));
+    s->child_cap = c;
+  }
   return SNP_OK;
 }
 
@@ -294,13 +357,13 @@ ChildArrays child_arrays(snp_system* s) {
                      s->kept.as<uint64_t>(), s->kpos.as<uint64_t>()};
 }
 
-snp_status alloc_level_meta(Level* L, int64_t K) {
+snp_status alloc_level_meta(snp_system* s, Level* L, int64_t K) {
   size_t k = (size_t)std::max<int64_t>(K, 1);
-  SNP_TRY(L->fp0.ensure(k * 8, false));
-  SNP_TRY(L->fp1.ensure(k * 8, false));
-  SNP_TRY(L->parent.ensure(k * 8, false));
-  SNP_TRY(L->t.ensure(k * 8, false));
-  SNP_TRY(L->halting.ensure(k, false));
+  SNP_TRY(s->arena.alloc(k * 8, &L->fp0));
+  SNP_TRY(s->arena.alloc(k * 8, &L->fp1));
+  SNP_TRY(s->arena.alloc(k * 8, &L->parent));
+  SNP_TRY(s->arena.alloc(k * 8, &L->t));
+  SNP_TRY(s->arena.alloc(k, &L->halting));
   return SNP_OK;
 }
 
@@ -308,7 +371,7 @@ bool retain_levels(const snp_system* s) { return s->opt.keep_tree || s->opt.dedu
 
 snp_status update_stored_table(snp_system* s) {
   std::vector<StoredLevel> h(s->levels.size());
-  for (size_t i = 0; i < s->levels.size(); ++i) h[i] = StoredLevel{s->levels[i]->data.p, s->levels[i]->pitch};
+  for (size_t i = 0; i < s->levels.size(); ++i) h[i] = StoredLevel{s->levels[i]->data.p};
   SNP_TRY(s->stored.ensure(h.size() * sizeof(StoredLevel) + 16));
   CUDA_TRY(cudaMemcpyAsync(s->stored.p, h.data(), h.size() * sizeof(StoredLevel), cudaMemcpyHostToDevice, s->stream));
   return sync(s);  // h is a stack buffer
@@ -452,7 +515,50 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   SNP_TRY(upload(s, s->d_out_dst, out_dst));
   SNP_TRY(upload(s, s->d_R0, R0));
   SNP_TRY(upload(s, s->d_R1, R1));
+  // ---- per-neuron outcome-table descriptors: for counts
+  // v >= L the applicable set repeats with period P = lcm of the PERIODIC
+  // rules' j; counts never exceed count_max.  Neurons with > 15 rules or a
+  // table wider than TABW_MAX are evaluated rule by rule (NM_GENERIC).
+  std::vector<NeuronMeta> meta(m);
+  int64_t tabw = 16;
+  for (int64_t j = 0; j < m; ++j) {
+    const int32_t r0 = rule_off[j], r1 = rule_off[j + 1];
+    int64_t L = 0, P = 1;
+    bool ok = (r1 - r0) <= MAX_TABLE_RULES;
+    for (int32_t r = r0; r < r1 && ok; ++r) {
+      const snp_rule& R = rules[r];
+      if (R.kind == SNP_RE_EXACT) {
+        L = std::max<int64_t>(L, (int64_t)R.a + 1);
+      } else {
+        L = std::max<int64_t>(L, std::max<int64_t>(R.a, R.consumed));
+        const int64_t g = std::__gcd<int64_t>(P, R.b);
+        P = P / g * R.b;
+        if (P > TABW_MAX) ok = false;
+      }
+    }
+    if (ok && L > s->count_max + 1) { L = s->count_max + 1; P = 1; }
+    if (ok && L + P > TABW_MAX) ok = false;
+    NeuronMeta mt{r0, (int32_t)L, (P & (P - 1)) == 0 ? (int32_t)(P - 1) : (int32_t)(-P), ok ? 0 : NM_GENERIC};
+    if (!ok) { mt.L = 0; mt.pm = 0; }
+    else tabw = std::max<int64_t>(tabw, L + P);
+    meta[j] = mt;
+  }
+  tabw = (tabw + 15) / 16 * 16;
+  int32_t max_indeg = 0;
+  for (int64_t j = 0; j < m; ++j) max_indeg = std::max(max_indeg, in_off[j + 1] - in_off[j]);
+  SNP_TRY(upload(s, s->d_meta, meta));
+  SNP_TRY(s->d_tab.ensure((size_t)m * tabw, false));
+  SNP_TRY(s->d_ctab.ensure((size_t)m * tabw * s->bytes, false));
+  if (s->bytes == 1) SNP_TRY(s->d_tab_full.ensure((size_t)m * 256, false));
   SysView& v = s->view;
+  v.tables_ok = 1;
+  v.tabw = (int32_t)tabw;
+  v.full8 = s->bytes == 1 ? 1 : 0;
+  v.max_indeg = max_indeg;
+  v.meta = s->d_meta.as<NeuronMeta>();
+  v.tab = s->d_tab.as<uint8_t>();
+  v.tab_full = s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr;
+  v.ctab = s->d_ctab.p;
   v.m = (int32_t)m;
   v.n = n;
   v.binary_emit = s->binary_emit ? 1 : 0;
@@ -470,6 +576,10 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   SNP_TRY(s->counters_dev.ensure(sizeof(DevCounters), false));
   CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   s->own_stream = true;
+  launch_build_tables(v, s->bytes, s->d_tab.as<uint8_t>(), s->d_ctab.p,
+                      s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr, s->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
   CUDA_TRY(cudaEventCreate(&s->ev0));
   CUDA_TRY(cudaEventCreate(&s->ev1));
   return SNP_OK;
@@ -483,6 +593,7 @@ snp_status reset_state(snp_system* s) {
   s->marks.clear();
   s->ev_used = 0;
   s->levels.clear();
+  s->arena.reset();
   s->counters.clear();
   s->n_visited = 0;
   s->total_T = 0;
@@ -528,29 +639,28 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
     src = staged.p;
   }
   SNP_TRY(zero_counters(s));
-  const int64_t pitch = round_pitch(F0);
   DBuf raw;
-  SNP_TRY(take_buffer(s, (size_t)m * pitch * s->bytes, &raw));
+  SNP_TRY(take_buffer(s, level_bytes(F0, m, s->bytes), &raw));
   int32_t* err = &dc(s)->err;
-  launch_import(src, level0->elem_bytes, level0->layout, ld, F0, (int32_t)m, raw.p, s->bytes, pitch, s->count_max, err,
+  launch_import(src, level0->elem_bytes, level0->layout, ld, F0, (int32_t)m, raw.p, s->bytes, s->count_max, err,
                 s->stream);
   CUDA_TRY(cudaGetLastError());
   // fingerprints of level 0
   DBuf fp0, fp1;
   SNP_TRY(fp0.ensure(F0 * 8, false));
   SNP_TRY(fp1.ensure(F0 * 8, false));
-  launch_fingerprint(s->view, s->bytes, raw.p, pitch, F0, fp0.as<uint64_t>(), fp1.as<uint64_t>(), s->stream);
+  launch_fingerprint(s->view, s->bytes, raw.p, F0, fp0.as<uint64_t>(), fp1.as<uint64_t>(), s->stream);
   // dedup level 0: first occurrence wins (tags = index)
   SNP_TRY(ensure_children(s, (uint64_t)F0));
   SNP_TRY(ensure_ltab(s, (uint64_t)F0));
-  SNP_TRY(ensure_visited(s, (uint64_t)F0));
+  SNP_TRY(ensure_visited(s, 4 * (uint64_t)F0));
   const uint64_t lslots = next_pow2(std::max<uint64_t>(1024, 2 * (uint64_t)F0));
   Tables tb = tables(s, lslots);
   ChildArrays C = child_arrays(s);
   CUDA_TRY(cudaMemcpyAsync(C.cfp0, fp0.p, F0 * 8, cudaMemcpyDeviceToDevice, s->stream));
   CUDA_TRY(cudaMemcpyAsync(C.cfp1, fp1.p, F0 * 8, cudaMemcpyDeviceToDevice, s->stream));
   launch_dedup(C, (uint64_t)F0, 0, tb, 0, err, s->stream);
-  launch_winners(C, (uint64_t)F0, 0, tb, 0, 0, &dc(s)->n_new, s->stream);
+  launch_winners(C, (uint64_t)F0, 0, tb, &dc(s)->n_new, s->stream);
   launch_keep(C, (uint64_t)F0, 0, tb, 0, 0, s->stream);
   launch_exclusive_scan(s->scan_tmp.p, s->scan_tmp.bytes, C.kept, C.kpos, F0 + 1, s->stream);
   CUDA_TRY(cudaGetLastError());
@@ -558,31 +668,27 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
   SNP_TRY(read_counters(s, &hc));
   SNP_TRY(check_err(hc.err));
   if (s->opt.dedup == 0 && (int64_t)hc.n_new < F0) {
-    launch_verify_level0(s->bytes, raw.p, pitch, (int32_t)m, C, (uint64_t)F0, tb, err, s->stream);
+    launch_verify_level0(s->bytes, raw.p, (int32_t)m, C, (uint64_t)F0, tb, err, s->stream);
     CUDA_TRY(cudaGetLastError());
     SNP_TRY(read_counters(s, &hc));
     SNP_TRY(check_err(hc.err));
   }
   const int64_t K = (int64_t)hc.n_new;
   auto L = std::make_unique<Level>();
-  SNP_TRY(alloc_level_meta(L.get(), K));
+  SNP_TRY(alloc_level_meta(s, L.get(), K));
   SNP_TRY(ensure_visited(s, (uint64_t)K));
   tb = tables(s, lslots);
   SNP_TRY(s->src_index.ensure(std::max<int64_t>(K, 1) * 8));
-  NextArrays N{nullptr, 0, L->parent.as<int64_t>(), L->t.as<uint64_t>(), L->fp0.as<uint64_t>(), L->fp1.as<uint64_t>()};
+  NextArrays N{nullptr, L->parent.as<int64_t>(), L->t.as<uint64_t>(), L->fp0.as<uint64_t>(), L->fp1.as<uint64_t>()};
   launch_level0_compact(C.verdict, C.kept, C.kpos, F0, fp0.as<uint64_t>(), fp1.as<uint64_t>(), N,
                         s->src_index.as<uint64_t>(), tb, err, s->stream);
   if (K == F0) {
     L->data = std::move(raw);
-    L->pitch = pitch;
   } else {
-    L->pitch = round_pitch(K);
-    SNP_TRY(take_buffer(s, (size_t)m * L->pitch * s->bytes, &L->data));
-    launch_gather_columns(s->bytes, raw.p, pitch, s->src_index.as<uint64_t>(), K, (int32_t)m, L->data.p, L->pitch,
-                          s->stream);
+    SNP_TRY(take_buffer(s, level_bytes(K, m, s->bytes), &L->data));
+    launch_gather_columns(s->bytes, raw.p, s->src_index.as<uint64_t>(), K, (int32_t)m, L->data.p, s->stream);
   }
   N.data = L->data.p;
-  N.pitch = L->pitch;
   launch_digest(N, K, 0, &dc(s)->digest, s->stream);
   CUDA_TRY(cudaGetLastError());
   SNP_TRY(read_counters(s, &hc));
@@ -604,7 +710,7 @@ snp_status classify_level(snp_system* s, Level* L) {
   O.n_halting = &dc(s)->n_halting;
   O.err = &dc(s)->err;
   O.classify_only = 1;
-  LevelView LV{L->data.p, L->F, L->pitch, L->fp0.as<uint64_t>(), L->fp1.as<uint64_t>()};
+  LevelView LV{L->data.p, L->F, L->fp0.as<uint64_t>(), L->fp1.as<uint64_t>()};
   launch_expand(s->view, s->bytes, LV, O, s->stream);
   CUDA_TRY(cudaGetLastError());
   return sync(s);
@@ -620,17 +726,18 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
   }
   if (!cur->has_data()) return fail(SNP_E_STATE, "current level has no data");
   cudaStream_t st = s->stream;
+  g_trace.start();
   CUDA_TRY(cudaEventRecord(s->ev0, st));
   SNP_TRY(zero_counters(s));
   int32_t* err = &dc(s)->err;
   // ---- K-a expand
-  const int64_t n_tiles = (F + TILE - 1) / TILE;
   SNP_TRY(s->psi.ensure((F + 1) * 8));
   SNP_TRY(s->off.ensure((F + 1) * 8));
   SNP_TRY(s->fpb0.ensure(F * 8));
   SNP_TRY(s->fpb1.ensure(F * 8));
   SNP_TRY(s->ndc.ensure(F * 4));
   SNP_TRY(s->nd.ensure((size_t)F * KMAX * 8));
+  g_trace.mark("alloc_a");
   ExpandOut O{};
   O.psi = s->psi.as<uint64_t>();
   O.fpb0 = s->fpb0.as<uint64_t>();
@@ -640,17 +747,13 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
   O.halting = cur->halting.as<uint8_t>();
   O.n_halting = &dc(s)->n_halting;
   O.err = err;
-  if (s->binary_emit) {
-    O.ebits_ld = n_tiles * 32;
-    SNP_TRY(s->ebits.ensure((size_t)((m + 7) / 8) * O.ebits_ld * 4));
-    O.ebits = s->ebits.as<uint32_t>();
-  } else {
-    O.evals_ld = round_pitch(F);
-    SNP_TRY(s->evals.ensure((size_t)m * O.evals_ld * 4));
-    O.evals = s->evals.as<int32_t>();
+  if (fast_materialize_ok(s->view)) {
+    // emit words: one uint64 per (storage block, neuron), rows rounded to even
+    SNP_TRY(s->ebits.ensure((size_t)((F + PB - 1) / PB) * (size_t)((m + 1) & ~1) * 8));
+    O.ebits = s->ebits.as<uint64_t>();
   }
   CUDA_TRY(cudaMemsetAsync(O.psi + F, 0, 8, st));
-  LevelView LV{cur->data.p, F, cur->pitch, cur->fp0.as<uint64_t>(), cur->fp1.as<uint64_t>()};
+  LevelView LV{cur->data.p, F, cur->fp0.as<uint64_t>(), cur->fp1.as<uint64_t>()};
   phase_begin(s, 0);
   launch_expand(s->view, s->bytes, LV, O, st);
   phase_end(s);
@@ -663,7 +766,9 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
   uint64_t T = 0;
   CUDA_TRY(cudaMemcpyAsync(&T, s->off.as<uint64_t>() + F, 8, cudaMemcpyDeviceToHost, st));
   DevCounters hc;
+  g_trace.mark("launch_a");
   SNP_TRY(read_counters(s, &hc));
+  g_trace.mark("sync_a");
   SNP_TRY(check_err(hc.err));
   lc.parents = F;
   lc.halting = (int64_t)hc.n_halting;
@@ -680,6 +785,7 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
   if (T > 0) {
     SNP_TRY(ensure_children(s, T));
     SNP_TRY(ensure_ltab(s, T));
+    g_trace.mark("alloc_children");
     const uint64_t lslots = next_pow2(std::max<uint64_t>(1024, 2 * T));
     ChildArrays C = child_arrays(s);
     Tables tb = tables(s, lslots);
@@ -690,10 +796,11 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     phase_end(s);
     phase_begin(s, 2);
     launch_dedup(C, T, tag_base, tb, 1, err, st);
-    launch_winners(C, T, tag_base, tb, 0, 0, &dc(s)->n_new, st);
+    launch_winners(C, T, tag_base, tb, &dc(s)->n_new, st);
     phase_end(s);
     CUDA_TRY(cudaGetLastError());
     SNP_TRY(read_counters(s, &hc));
+    g_trace.mark("sync_dedup");
     SNP_TRY(check_err(hc.err));
     const int64_t n_new = (int64_t)hc.n_new;
     lc.n_new = n_new;
@@ -714,17 +821,20 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     K = (int64_t)Kh;
     // ---- next level buffers + visited insert
     next->F = K;
-    next->pitch = round_pitch(K);
-    SNP_TRY(alloc_level_meta(next.get(), K));
+    g_trace.mark("sync_keep");
+    SNP_TRY(alloc_level_meta(s, next.get(), K));
+    g_trace.mark("alloc_meta");
     SNP_TRY(ensure_visited(s, (uint64_t)(s->n_visited + K)));
+    g_trace.mark("visited");
     tb = tables(s, lslots);
-    NextArrays N{nullptr, next->pitch, next->parent.as<int64_t>(), next->t.as<uint64_t>(), next->fp0.as<uint64_t>(),
+    NextArrays N{nullptr, next->parent.as<int64_t>(), next->t.as<uint64_t>(), next->fp0.as<uint64_t>(),
                  next->fp1.as<uint64_t>()};
     phase_begin(s, 2);
     launch_compact(C, off, T, N, tb, (uint64_t)s->levels.size() << 40, err, st);
     phase_end(s);
     if (K > 0) {
-      SNP_TRY(take_buffer(s, (size_t)m * next->pitch * s->bytes, &next->data));
+      SNP_TRY(take_buffer(s, level_bytes(K, m, s->bytes), &next->data));
+      g_trace.mark("take_buffer");
       N.data = next->data.p;
       // ---- K-c materialize kept children
       SNP_TRY(s->kq_off.ensure((F + 1) * 8));
@@ -732,8 +842,8 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
       SNP_TRY(s->ovf.ensure(ovf_cap * 8));
       phase_begin(s, 3);
       launch_kq_off(off, C.kpos, F, s->kq_off.as<uint64_t>(), st);
-      launch_materialize(s->view, s->bytes, LV, O, s->kq_off.as<uint64_t>(), N, s->ovf.as<uint64_t>(),
-                         &dc(s)->n_ovf, ovf_cap, st);
+      launch_materialize(s->view, s->bytes, LV, O, s->kq_off.as<uint64_t>(), N, K, s->ovf.as<uint64_t>(),
+                         &dc(s)->n_ovf, ovf_cap, err, st);
       launch_patch(s->view, s->bytes, LV, O, N, K, err, st);
       phase_end(s);
       CUDA_TRY(cudaGetLastError());
@@ -757,7 +867,10 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     }
   }
   CUDA_TRY(cudaEventRecord(s->ev1, st));
+  g_trace.mark("launch_c");
   SNP_TRY(read_counters(s, &hc));
+  g_trace.mark("sync_end");
+  g_trace.flush("level");
   phase_collect(s);
   SNP_TRY(check_err(hc.err));
   float ms = 0;
@@ -979,13 +1092,12 @@ snp_status snp_level_columns(snp_system* s, int32_t level, const int64_t* idx, i
   }
   if (n == 0) return SNP_OK;
   DBuf didx, cols, rows;
-  const int64_t pitch = round_pitch(n);
   SNP_TRY(didx.ensure(n * 8, false));
-  SNP_TRY(cols.ensure((size_t)s->m * pitch * s->bytes, false));
+  SNP_TRY(cols.ensure(level_bytes(n, s->m, s->bytes), false));
   SNP_TRY(rows.ensure((size_t)n * s->m * 4, false));
   CUDA_TRY(cudaMemcpyAsync(didx.p, hidx.data(), n * 8, cudaMemcpyHostToDevice, s->stream));
-  launch_gather_columns(s->bytes, L->data.p, L->pitch, didx.as<uint64_t>(), n, (int32_t)s->m, cols.p, pitch, s->stream);
-  launch_export(cols.p, s->bytes, pitch, n, (int32_t)s->m, rows.as<int32_t>(), s->stream);
+  launch_gather_columns(s->bytes, L->data.p, didx.as<uint64_t>(), n, (int32_t)s->m, cols.p, s->stream);
+  launch_export(cols.p, s->bytes, n, (int32_t)s->m, rows.as<int32_t>(), s->stream);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(out, rows.p, (size_t)n * s->m * 4, cudaMemcpyDeviceToHost, s->stream));
   return sync(s);
@@ -1041,7 +1153,7 @@ snp_status snp_tree_configs(const snp_tree* t, int32_t* out) {
     const Level* lv = s->levels[L].get();
     if (!lv->F) continue;
     SNP_TRY(tmp.ensure((size_t)lv->F * s->m * 4));
-    launch_export(lv->data.p, s->bytes, lv->pitch, lv->F, (int32_t)s->m, tmp.as<int32_t>(), s->stream);
+    launch_export(lv->data.p, s->bytes, lv->F, (int32_t)s->m, tmp.as<int32_t>(), s->stream);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(out + t->level_offsets[L] * s->m, tmp.p, (size_t)lv->F * s->m * 4,
                              cudaMemcpyDeviceToHost, s->stream));
@@ -1059,7 +1171,7 @@ snp_status snp_tree_spiking_vectors(const snp_tree* t, int32_t level, uint8_t* S
   if (!lv->F) return SNP_OK;
   DBuf tmp;
   SNP_TRY(tmp.ensure((size_t)lv->F * s->n));
-  launch_spiking_vectors(s->view, s->bytes, par->data.p, par->pitch, lv->parent.as<int64_t>(), lv->t.as<uint64_t>(),
+  launch_spiking_vectors(s->view, s->bytes, par->data.p, lv->parent.as<int64_t>(), lv->t.as<uint64_t>(),
                          lv->F, tmp.as<uint8_t>(), s->stream);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(S_out, tmp.p, (size_t)lv->F * s->n, cudaMemcpyDeviceToHost, s->stream));

@@ -10,11 +10,10 @@ namespace snp {
 
 extern std::atomic<int64_t> g_kernel_launches;
 
-// A frontier level on the device (neuron-major, see snp_device.cuh).
+// A frontier level on the device (blocked layout, see snp_device.cuh).
 struct LevelView {
   const void* data;
   int64_t F;
-  int64_t pitch;  // elements per neuron row (multiple of TILE)
   const uint64_t* fp0;
   const uint64_t* fp1;
 };
@@ -26,10 +25,7 @@ struct ExpandOut {
   int32_t* ndc;       // number of nondeterministic neurons (d_s >= 2)
   uint64_t* nd;       // F × KMAX entries (s << 32 | count)
   uint8_t* halting;   // F
-  uint32_t* ebits;    // binary emits: ceil(m/8) rows × ebits_ld words
-  int64_t ebits_ld;   // = n_tiles × 32
-  int32_t* evals;     // general emits: m rows × evals_ld int32 (p of the first rule)
-  int64_t evals_ld;
+  uint64_t* ebits;    // binary emits per (block, neuron): bit k = configuration 64·b + k spikes
   unsigned long long* n_halting;
   int32_t* err;
   int classify_only;
@@ -47,8 +43,7 @@ struct ChildArrays {
 };
 
 struct NextArrays {
-  void* data;         // m × pitch
-  int64_t pitch;
+  void* data;         // blocked, ceil(K/64) blocks
   int64_t* parent;    // K
   uint64_t* t;        // K
   uint64_t* fp0;      // K
@@ -57,7 +52,6 @@ struct NextArrays {
 
 struct StoredLevel {  // device table of retained level buffers (exact verification)
   const void* data;
-  int64_t pitch;
 };
 
 struct Tables {
@@ -67,29 +61,36 @@ struct Tables {
   uint64_t lmask;
 };
 
+// True when the fast kernels apply (outcome tables built, binary emits, the
+// per-block emit words of a materialize tile fit in shared memory).
+bool fast_expand_ok(const SysView& S);
+bool fast_materialize_ok(const SysView& S);
+size_t materialize_smem_bytes(const SysView& S, int32_t bytes);
+
 // ---- launchers (all asynchronous on `st`) ----------------------------------
+void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ctab, uint8_t* tab_full,
+                         cudaStream_t st);
 void launch_import(const void* src, int32_t src_bytes, int32_t src_layout, int64_t src_ld, int64_t F, int32_t m,
-                   void* dst, int32_t dst_bytes, int64_t dst_pitch, int64_t count_max, int32_t* err, cudaStream_t st);
-void launch_export(const void* src, int32_t bytes, int64_t pitch, int64_t F, int32_t m, int32_t* dst_rowmajor,
-                   cudaStream_t st);
-void launch_fingerprint(const SysView& S, int32_t bytes, const void* data, int64_t pitch, int64_t F, uint64_t* fp0,
-                        uint64_t* fp1, cudaStream_t st);
+                   void* dst, int32_t dst_bytes, int64_t count_max, int32_t* err, cudaStream_t st);
+void launch_export(const void* src, int32_t bytes, int64_t F, int32_t m, int32_t* dst_rowmajor, cudaStream_t st);
+void launch_fingerprint(const SysView& S, int32_t bytes, const void* data, int64_t F, uint64_t* fp0, uint64_t* fp1,
+                        cudaStream_t st);
 void launch_expand(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, cudaStream_t st);
 void launch_child_parent(const uint64_t* off, int64_t F, uint32_t* cpar, cudaStream_t st);
 void launch_child_keys(const SysView& S, const uint64_t* off, const ExpandOut& O, uint64_t T, const ChildArrays& C,
                        cudaStream_t st);
 void launch_dedup(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, int use_visited, int32_t* err,
                   cudaStream_t st);
-void launch_winners(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, uint64_t tau, int thin,
-                    unsigned long long* n_new, cudaStream_t st);
+void launch_winners(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, unsigned long long* n_new,
+                    cudaStream_t st);
 void launch_keep(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, uint64_t tau, int thin,
                  cudaStream_t st);
 void launch_compact(const ChildArrays& C, const uint64_t* off, uint64_t T, const NextArrays& N, const Tables& tb,
                     uint64_t level_ref, int32_t* err, cudaStream_t st);
 void launch_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, uint64_t* kq_off, cudaStream_t st);
 void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O,
-                        const uint64_t* kq_off, const NextArrays& N, uint64_t* ovf, unsigned long long* n_ovf,
-                        uint64_t ovf_cap, cudaStream_t st);
+                        const uint64_t* kq_off, const NextArrays& N, int64_t K, uint64_t* ovf,
+                        unsigned long long* n_ovf, uint64_t ovf_cap, int32_t* err, cudaStream_t st);
 void launch_patch(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const NextArrays& N,
                   int64_t K, int32_t* err, cudaStream_t st);
 void launch_overflow_fix(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O,
@@ -101,15 +102,15 @@ void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const Ex
 void launch_level0_compact(const uint8_t* verdict, const uint64_t* kept, const uint64_t* kpos, int64_t F0,
                            const uint64_t* fp0, const uint64_t* fp1, const NextArrays& N, uint64_t* src_index,
                            const Tables& tb, int32_t* err, cudaStream_t st);
-void launch_gather_columns(int32_t bytes, const void* src, int64_t src_pitch, const uint64_t* src_index, int64_t K,
-                           int32_t m, void* dst, int64_t dst_pitch, cudaStream_t st);
-void launch_verify_level0(int32_t bytes, const void* data, int64_t pitch, int32_t m, const ChildArrays& C,
-                          uint64_t F0, const Tables& tb, int32_t* err, cudaStream_t st);
+void launch_gather_columns(int32_t bytes, const void* src, const uint64_t* src_index, int64_t K, int32_t m, void* dst,
+                           cudaStream_t st);
+void launch_verify_level0(int32_t bytes, const void* data, int32_t m, const ChildArrays& C, uint64_t F0,
+                          const Tables& tb, int32_t* err, cudaStream_t st);
 void launch_rehash(const Slot* old_tab, uint64_t old_cap, Slot* new_tab, uint64_t new_mask, int32_t* err,
                    cudaStream_t st);
 void launch_digest(const NextArrays& N, int64_t K, uint64_t level, unsigned long long* digest, cudaStream_t st);
-void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_data, int64_t parent_pitch,
-                            const int64_t* parent, const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st);
+void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_data, const int64_t* parent,
+                            const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st);
 
 // CUB exclusive scan of n uint64 values (temp storage managed by the caller).
 size_t scan_temp_bytes(int64_t n);

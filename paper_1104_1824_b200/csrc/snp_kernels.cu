@@ -1,22 +1,22 @@
 // snp_kernels.cu — sm_100a kernels of the batched SNP transition step.
 //
-//   K-a  k_expand        rule applicability per (neuron, configuration)
+//   K-a  k_expand_t / k_expand_g   rule applicability per (neuron, configuration)
 //                        (Alg. 2 II-1), Ψ (eq. (8),
 //                        PAPER.md:250, readings A3/A5), the base-child
-//                        fingerprint and the first-choice emits.
+//                        fingerprint and the first-choice emit bits.
 //   K-b  CUB scan + k_child_parent + k_child_keys: child offsets, mixed-radix
 //                        decode of t (Alg. 2 II-2/II-3, PAPER.md:263-264,
 //                        reading A7) and the child fingerprint by linearity.
 //   K-d  k_dedup / k_winners / k_keep / k_compact: GPU open-addressing sets
 //                        (visited + level table with minimum-tag resolution,
 //                        readings A6, A19, A22).
-//   K-c  k_materialize + k_patch + k_overflow_fix: C' = C + S·M (eq. (2),
-//                        PAPER.md:129) for the kept children only, as a
-//                        gather-add over the in-synapses (Def. 2,
-//                        PAPER.md:115-119) plus exact sparse ND corrections.
+//   K-c  k_materialize_bs (+ k_patch, k_overflow_fix) or k_materialize_exact:
+//                        C' = C + S·M (eq. (2)) for the kept
+//                        children only, as a gather-add over the in-synapses
+//                        (Def. 2).
 //
-// Every kernel is plain CUDA C++ for sm_100a; the path is integer and bound
-// by HBM / issue bandwidth, not by tensor cores.
+// Every kernel is plain CUDA C++ / PTX for sm_100a; the path is integer and
+// bound by HBM / issue bandwidth, not by tensor cores.
 #include <atomic>
 
 #include <cub/cub.cuh>
@@ -40,8 +40,8 @@ inline unsigned grid_for(uint64_t n, int blk = BLK) {
 }
 
 template <typename T>
-__device__ __forceinline__ int32_t ld_count(const void* data, int64_t pitch, int32_t j, int64_t p) {
-  return (int32_t) reinterpret_cast<const T*>(data)[(int64_t)j * pitch + p];
+__device__ __forceinline__ int32_t ld_count(const void* data, int64_t p, int32_t j, int32_t m) {
+  return (int32_t) reinterpret_cast<const T*>(data)[eidx(p, j, m)];
 }
 
 // Applicable rules of neuron s holding v spikes: count and the x-th one.
@@ -95,21 +95,20 @@ __device__ int fired_rule(const SysView& S, int32_t s, int32_t v, const ChildCtx
 // Exact value of the child at neuron j: eq. (2) restricted to column j,
 // C'[j] = C[j] - c_{fired(j)} + Σ_{s ∈ in(j)} p_{fired(s)}  (Def. 2).
 template <typename T>
-__device__ int64_t exact_value(const SysView& S, const void* data, int64_t pitch, int64_t p, int32_t j,
-                               const ChildCtx& cx) {
-  int32_t vj = ld_count<T>(data, pitch, j, p);
+__device__ int64_t exact_value(const SysView& S, const void* data, int64_t p, int32_t j, const ChildCtx& cx) {
+  int32_t vj = ld_count<T>(data, p, j, S.m);
   int rj = fired_rule(S, j, vj, cx);
   int64_t val = (int64_t)vj - (rj >= 0 ? S.rules[rj].c : 0);
   for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) {
     int32_t s = S.in_src[e];
-    int rs = fired_rule(S, s, ld_count<T>(data, pitch, s, p), cx);
+    int rs = fired_rule(S, s, ld_count<T>(data, p, s, S.m), cx);
     if (rs >= 0) val += S.rules[rs].p;
   }
   return val;
 }
 
 // ---------------------------------------------------------------------------
-// import / export between the ABI's layouts and the device frontier
+// import / export between the ABI's layouts and the blocked device frontier
 // ---------------------------------------------------------------------------
 template <typename Tin>
 __device__ __forceinline__ int64_t ld_in(const void* src, int64_t idx) {
@@ -117,7 +116,7 @@ __device__ __forceinline__ int64_t ld_in(const void* src, int64_t idx) {
 }
 
 template <typename Tin, typename Tout>
-__global__ void k_import(const void* src, int32_t layout, int64_t ld, int64_t F, int32_t m, Tout* dst, int64_t pitch,
+__global__ void k_import(const void* src, int32_t layout, int64_t ld, int64_t F, int32_t m, Tout* dst,
                          int64_t count_max, int32_t* err) {
   // 32×32 tiles; row-major input is transposed through shared memory.
   __shared__ int64_t tile[32][33];
@@ -138,7 +137,7 @@ __global__ void k_import(const void* src, int32_t layout, int64_t ld, int64_t F,
       if (p < F && j < m) {
         int64_t v = tile[tx][r];
         bad |= (v < 0 || v > count_max);
-        dst[(int64_t)j * pitch + p] = (Tout)v;
+        dst[eidx(p, j, m)] = (Tout)v;
       }
     }
   } else {  // neuron-major: element (p, j) at src[j * ld + p]
@@ -148,7 +147,7 @@ __global__ void k_import(const void* src, int32_t layout, int64_t ld, int64_t F,
       if (p < F && j < m) {
         int64_t v = ld_in<Tin>(src, (int64_t)j * ld + p);
         bad |= (v < 0 || v > count_max);
-        dst[(int64_t)j * pitch + p] = (Tout)v;
+        dst[eidx(p, j, m)] = (Tout)v;
       }
     }
   }
@@ -156,7 +155,7 @@ __global__ void k_import(const void* src, int32_t layout, int64_t ld, int64_t F,
 }
 
 template <typename T>
-__global__ void k_export(const T* src, int64_t pitch, int64_t F, int32_t m, int32_t* dst) {
+__global__ void k_export(const T* src, int64_t F, int32_t m, int32_t* dst) {
   __shared__ int32_t tile[32][33];
   const int64_t p_base = (int64_t)blockIdx.x * 32;
   const int32_t j_base = blockIdx.y * 32;
@@ -164,7 +163,7 @@ __global__ void k_export(const T* src, int64_t pitch, int64_t F, int32_t m, int3
   for (int r = ty; r < 32; r += 8) {
     int32_t j = j_base + r;
     int64_t p = p_base + tx;
-    tile[r][tx] = (p < F && j < m) ? (int32_t)src[(int64_t)j * pitch + p] : 0;
+    tile[r][tx] = (p < F && j < m) ? (int32_t)src[eidx(p, j, m)] : 0;
   }
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
@@ -174,115 +173,380 @@ __global__ void k_export(const T* src, int64_t pitch, int64_t F, int32_t m, int3
   }
 }
 
-// fp_ℓ(C) = Σ_j C[j]·R_ℓ[j] mod 2^64 (reading A18), one column per thread
-// slot; warp tiles of 128 configurations as in k_expand.
+// fp_ℓ(C) = Σ_j C[j]·R_ℓ[j] mod 2^64 (reading A18), one configuration per thread.
 template <typename T>
-__global__ void __launch_bounds__(128) k_fingerprint(SysView S, const T* data, int64_t pitch, int64_t F,
-                                                      uint64_t* fp0, uint64_t* fp1) {
-  const int lane = threadIdx.x & 31;
-  const int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t p0 = tile * TILE + 4 * lane;
-  if (tile * TILE >= F) return;
-  uint64_t a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0};
+__global__ void k_fingerprint(SysView S, const T* data, int64_t F, uint64_t* fp0, uint64_t* fp1) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= F) return;
+  uint64_t a = 0, b = 0;
   for (int32_t j = 0; j < S.m; ++j) {
-    int32_t v[4];
-    load4<T>(data + (int64_t)j * pitch, p0, F, v);
-    const uint64_t r0 = __ldg(S.R0 + j), r1 = __ldg(S.R1 + j);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      a[k] += (uint64_t)v[k] * r0;
-      b[k] += (uint64_t)v[k] * r1;
-    }
+    const uint64_t v = (uint64_t)data[eidx(p, j, S.m)];
+    a += v * __ldg(S.R0 + j);
+    b += v * __ldg(S.R1 + j);
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (p0 + k < F) { fp0[p0 + k] = a[k]; fp1[p0 + k] = b[k]; }
+  fp0[p] = a;
+  fp1[p] = b;
 }
 
 // ---------------------------------------------------------------------------
 // K-a: applicability, Ψ, base fingerprint, emits
 // ---------------------------------------------------------------------------
-template <typename T, bool BIN>
-__global__ void __launch_bounds__(128) k_expand(SysView S, LevelView L, ExpandOut O) {
-  const int lane = threadIdx.x & 31;
-  const int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t p0 = tile * TILE + 4 * lane;
-  if (tile * TILE >= L.F) return;  // warp-uniform
-  const T* data = reinterpret_cast<const T*>(L.data);
-  uint64_t f0[4], f1[4], psi[4];
-  int ndc[4];
-  bool any[4];
+constexpr int XW = 8;       // warps per CTA
+constexpr int XPPL = 8;     // configurations per lane
+constexpr int XTILE = 256;  // configurations per warp (4 storage blocks)
+
+__device__ __forceinline__ void nd_event(const SysView& S, const ExpandOut& O, int32_t s, uint32_t v, int64_t p,
+                                         int& ndc, uint64_t& psi) {
+  const int d = count_applicable(S, s, (int32_t)v);
+  if (!O.classify_only && ndc < KMAX) O.nd[p * KMAX + ndc] = ((uint64_t)(uint32_t)s << 32) | v;
+  ++ndc;
+  psi = sat_mul(psi, (uint64_t)d);
+}
+
+__device__ __forceinline__ int64_t emit_index(int64_t p, int32_t s, int32_t m) {
+  const int64_t mE = (m + 1) & ~1;  // rows per block rounded to even: 16-B aligned block slices
+  return ((p >> 6) * mE + s) * 8 + ((p & 63) >> 3);
+}
+
+// Evaluate the rules of one neuron for a lane's 8 configurations (no table).
+__device__ void expand_generic_neuron(const SysView& S, const ExpandOut& O, int32_t s, const uint32_t v[8],
+                                      int64_t p0, int64_t F, uint64_t a[8], uint64_t b[8], uint64_t psi[8],
+                                      int ndc[8], uint32_t& anyb, uint32_t& eb) {
+  const int r0 = S.rule_off[s], r1 = S.rule_off[s + 1];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 8; ++k) {
+    int first = -1, d = 0;
+    for (int r = r0; r < r1; ++r)
+      if (rule_app(S.rules[r], (int32_t)v[k])) {
+        if (!d) first = r;
+        ++d;
+      }
+    if (d) {
+      a[k] += __ldg(S.h0 + first);
+      b[k] += __ldg(S.h1 + first);
+      anyb |= 1u << k;
+      eb |= (S.rules[first].p > 0 ? 1u : 0u) << k;
+      if (d >= 2 && p0 + k < F) {
+        if (!O.classify_only && ndc[k] < KMAX) O.nd[(p0 + k) * KMAX + ndc[k]] = ((uint64_t)(uint32_t)s << 32) | v[k];
+        ++ndc[k];
+        psi[k] = sat_mul(psi[k], (uint64_t)d);
+      }
+    }
+  }
+}
+
+// 4 table entries (one byte each) → 4-bit mask of their TE_EMIT bits
+__device__ __forceinline__ uint32_t emit_nibble(uint32_t w4) {
+  return ((w4 & 0x01010101u) * 0x01020408u) >> 24;
+}
+
+// Table-driven K-a.  A CTA owns 32 storage blocks (2048 configurations; warp w
+// owns blocks 4w..4w+3, 8 configurations per lane) and walks the neurons in
+// chunks of NC = 16/w.  For every chunk, one thread issues TMA bulk copies of
+// the 32 contiguous block slices (NC rows × 64 counts) into a double-buffered
+// shared-memory stage one chunk ahead (mbarrier complete_tx), while all
+// threads stage the chunk's outcome tables and rule fingerprint deltas.  Per
+// (neuron, configuration): one table byte, one 16-B fingerprint delta (slot 0
+// of a neuron is zero = "no rule fires"); neurons are consumed in pairs so the
+// two deltas enter the 64-bit accumulators through 3-input adds.  Ψ and the
+// ND lists are rare and live in global memory.
+template <typename T>
+struct ExpandGeom {
+  static constexpr int NC = 16 / (int)sizeof(T);      // neurons per chunk
+  static constexpr int ROWB = PB * (int)sizeof(T);    // bytes of one block row
+  static constexpr int BLKB = NC * ROWB;              // bytes of one block slice (1 KB)
+  static constexpr int BLKS = BLKB + 64;              // padded slice stride (bank spread)
+  static constexpr int CNT_STAGE = 32 * BLKS;         // count bytes per stage
+};
+
+template <typename T>
+size_t expand_smem_bytes(int W) {
+  using G = ExpandGeom<T>;
+  return 2 * (size_t)G::CNT_STAGE + 2 * (size_t)G::NC * W + 2 * (size_t)G::NC * 256 + 2 * G::NC * sizeof(NeuronMeta) +
+         64;
+}
+
+template <typename T>
+__device__ __forceinline__ void smem_counts8(const uint8_t* p, uint32_t v[8]) {
+  if constexpr (sizeof(T) == 1) {
+    const uint2 w = *reinterpret_cast<const uint2*>(p);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { v[k] = (w.x >> (8 * k)) & 0xFFu; v[k + 4] = (w.y >> (8 * k)) & 0xFFu; }
+  } else if constexpr (sizeof(T) == 2) {
+    const uint4 w = *reinterpret_cast<const uint4*>(p);
+    const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (x[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+  } else {
+    const uint4 a = *reinterpret_cast<const uint4*>(p);
+    const uint4 b = *reinterpret_cast<const uint4*>(p + 16);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+
+template <typename T, bool FULL>
+__global__ void __launch_bounds__(256, 2) k_expand_t(SysView S, LevelView L, ExpandOut O) {
+  using G = ExpandGeom<T>;
+  constexpr int NC = G::NC;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int W = FULL ? 256 : S.tabw;
+  uint8_t* s_cnt = smem;                                                    // [2][32][BLKS]
+  uint8_t* s_tab = s_cnt + 2 * G::CNT_STAGE;                                // [2][NC][W]
+  uint8_t* s_hs = s_tab + 2 * NC * W;                                       // [2][NC][256]
+  NeuronMeta* s_meta = reinterpret_cast<NeuronMeta*>(s_hs + 2 * NC * 256);  // [2][NC]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_meta + 2 * NC);             // [2]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t blk0 = (int64_t)blockIdx.x * 32;
+  const int64_t nblk_total = (L.F + PB - 1) / PB;
+  const int nb = (nblk_total - blk0 < 32) ? (int)(nblk_total - blk0) : 32;
+  const int bl = warp * 4 + (lane >> 3);  // this lane's block within the CTA
+  const int64_t p0 = (blk0 + bl) * PB + (lane & 7) * 8;
+  const int nvalid = p0 >= L.F ? 0 : (L.F - p0 >= 8 ? 8 : (int)(L.F - p0));
+  const uint8_t* gtab = FULL ? S.tab_full : S.tab;
+  const int m = S.m;
+  const int nchunks = (m + NC - 1) / NC;
+
+  uint64_t a[8], b[8];
+  uint32_t any0 = 0, any1 = 0, anyb_generic = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const bool ok = k < nvalid;
+    a[k] = ok ? L.fp0[p0 + k] : 0;
+    b[k] = ok ? L.fp1[p0 + k] : 0;
+    if (ok && !O.classify_only) {
+      O.psi[p0 + k] = 1;
+      O.ndc[p0 + k] = 0;
+    }
+  }
+  uint8_t* ep = nullptr;  // this lane's emit byte of neuron 0; +8 per neuron
+  if (O.ebits != nullptr && !O.classify_only && nvalid > 0)
+    ep = reinterpret_cast<uint8_t*>(O.ebits) + emit_index(p0, 0, m);
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int c) {  // TMA: chunk c's count slices of the CTA's blocks
+    if (tid == 0) {
+      const int st = c & 1, c0 = c * NC, rows = min(NC, m - c0);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&bar[st], (uint32_t)(nb * rows * G::ROWB));
+      const uint8_t* base = reinterpret_cast<const uint8_t*>(L.data);
+      for (int bb = 0; bb < nb; ++bb)
+        bulk_g2s(s_cnt + st * G::CNT_STAGE + bb * G::BLKS,
+                 base + (((blk0 + bb) * (int64_t)m + c0) * PB) * (int64_t)sizeof(T), (uint32_t)(rows * G::ROWB),
+                 &bar[st]);
+    }
+  };
+  auto stage_tables = [&](int c) {
+    const int st = c & 1, c0 = c * NC, rows = min(NC, m - c0);
+    const uint4* src = reinterpret_cast<const uint4*>(gtab + (int64_t)c0 * W);
+    uint4* dst = reinterpret_cast<uint4*>(s_tab + st * NC * W);
+    for (int i = tid; i < rows * W / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    ulonglong2* hs = reinterpret_cast<ulonglong2*>(s_hs + st * NC * 256);
+    for (int i = tid; i < rows * 16; i += blockDim.x) {
+      const int sl = i >> 4, f = i & 15;
+      const int r0 = __ldg(S.rule_off + c0 + sl), r1 = __ldg(S.rule_off + c0 + sl + 1);
+      ulonglong2 h = make_ulonglong2(0ULL, 0ULL);
+      if (f >= 1 && f <= r1 - r0 && f <= MAX_TABLE_RULES)
+        h = make_ulonglong2(__ldg(S.h0 + r0 + f - 1), __ldg(S.h1 + r0 + f - 1));
+      hs[i] = h;
+    }
+    if (tid < rows) s_meta[st * NC + tid] = S.meta[c0 + tid];
+  };
+
+  issue(0);
+  stage_tables(0);
+  __syncthreads();
+  for (int c = 0; c < nchunks; ++c) {
+    const int st = c & 1, c0 = c * NC, rows = min(NC, m - c0);
+    if (c + 1 < nchunks) {
+      issue(c + 1);
+      stage_tables(c + 1);
+    }
+    mbar_wait(&bar[st], (uint32_t)((c >> 1) & 1));
+    if (nvalid > 0) {
+      const uint8_t* crow = s_cnt + st * G::CNT_STAGE + bl * G::BLKS + (lane & 7) * 8 * (int)sizeof(T);
+      const uint8_t* tab = s_tab + st * NC * W;
+      const uint8_t* hsb = s_hs + st * NC * 256;
+      const NeuronMeta* mts = s_meta + st * NC;
+      for (int sl = 0; sl < rows; sl += 2) {
+        const bool pair = sl + 1 < rows;
+        const NeuronMeta mA = mts[sl];
+        const NeuronMeta mB = pair ? mts[sl + 1] : mA;
+        if (((mA.flags | mB.flags) & NM_GENERIC) || !pair) {
+          // slow path: one neuron at a time (generic neurons, odd tail)
+          for (int u = 0; u < (pair ? 2 : 1); ++u) {
+            const int su = sl + u;
+            const int32_t s = c0 + su;
+            const NeuronMeta mt = mts[su];
+            uint32_t v[8];
+            smem_counts8<T>(crow + su * G::ROWB, v);
+            uint32_t eb = 0;
+            if (mt.flags & NM_GENERIC) {
+              uint64_t psi[8];
+              int ndc[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                psi[k] = 1;
+                ndc[k] = (!O.classify_only && k < nvalid) ? O.ndc[p0 + k] : 0;
+              }
+              expand_generic_neuron(S, O, s, v, p0, L.F, a, b, psi, ndc, anyb_generic, eb);
+              if (!O.classify_only) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                  if (k < nvalid && psi[k] != 1) {
+                    O.psi[p0 + k] = sat_mul(O.psi[p0 + k], psi[k]);
+                    O.ndc[p0 + k] = ndc[k];
+                  }
+              }
+            } else {
+              uint32_t o[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                o[k] = tab[su * W + (FULL ? v[k] : table_index(v[k], mt))];
+                const ulonglong2 h = *reinterpret_cast<const ulonglong2*>(hsb + su * 256 + (o[k] & TE_F));
+                a[k] += h.x;
+                b[k] += h.y;
+              }
+              const uint32_t w0 = o[0] | (o[1] << 8) | (o[2] << 16) | (o[3] << 24);
+              const uint32_t w1 = o[4] | (o[5] << 8) | (o[6] << 16) | (o[7] << 24);
+              any0 |= w0;
+              any1 |= w1;
+              eb = emit_nibble(w0) | (emit_nibble(w1) << 4);
+              if (((w0 | w1) & 0x02020202u) && !O.classify_only) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                  if ((o[k] & TE_ND) && k < nvalid) {
+                    int nk = O.ndc[p0 + k];
+                    uint64_t pk = O.psi[p0 + k];
+                    nd_event(S, O, s, v[k], p0 + k, nk, pk);
+                    O.ndc[p0 + k] = nk;
+                    O.psi[p0 + k] = pk;
+                  }
+              }
+            }
+            if (ep) ep[(int64_t)s * 8] = (uint8_t)eb;
+          }
+          continue;
+        }
+        // fast path: a pair of tabulated neurons
+        uint32_t vA[8], vB[8];
+        smem_counts8<T>(crow + sl * G::ROWB, vA);
+        smem_counts8<T>(crow + (sl + 1) * G::ROWB, vB);
+        uint32_t oA[8], oB[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          oA[k] = tab[sl * W + (FULL ? vA[k] : table_index(vA[k], mA))];
+          oB[k] = tab[(sl + 1) * W + (FULL ? vB[k] : table_index(vB[k], mB))];
+          const ulonglong2 hA = *reinterpret_cast<const ulonglong2*>(hsb + sl * 256 + (oA[k] & TE_F));
+          const ulonglong2 hB = *reinterpret_cast<const ulonglong2*>(hsb + (sl + 1) * 256 + (oB[k] & TE_F));
+          a[k] += hA.x + hB.x;
+          b[k] += hA.y + hB.y;
+        }
+        const uint32_t wA0 = oA[0] | (oA[1] << 8) | (oA[2] << 16) | (oA[3] << 24);
+        const uint32_t wA1 = oA[4] | (oA[5] << 8) | (oA[6] << 16) | (oA[7] << 24);
+        const uint32_t wB0 = oB[0] | (oB[1] << 8) | (oB[2] << 16) | (oB[3] << 24);
+        const uint32_t wB1 = oB[4] | (oB[5] << 8) | (oB[6] << 16) | (oB[7] << 24);
+        any0 |= wA0 | wB0;
+        any1 |= wA1 | wB1;
+        if (ep) {
+          ep[(int64_t)(c0 + sl) * 8] = (uint8_t)(emit_nibble(wA0) | (emit_nibble(wA1) << 4));
+          ep[(int64_t)(c0 + sl + 1) * 8] = (uint8_t)(emit_nibble(wB0) | (emit_nibble(wB1) << 4));
+        }
+        if (((wA0 | wA1 | wB0 | wB1) & 0x02020202u) && !O.classify_only) {  // rare: nondeterminism
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (k >= nvalid) continue;
+            if (oA[k] & TE_ND) {
+              int nk = O.ndc[p0 + k];
+              uint64_t pk = O.psi[p0 + k];
+              nd_event(S, O, c0 + sl, vA[k], p0 + k, nk, pk);
+              O.ndc[p0 + k] = nk;
+              O.psi[p0 + k] = pk;
+            }
+            if (oB[k] & TE_ND) {
+              int nk = O.ndc[p0 + k];
+              uint64_t pk = O.psi[p0 + k];
+              nd_event(S, O, c0 + sl + 1, vB[k], p0 + k, nk, pk);
+              O.ndc[p0 + k] = nk;
+              O.psi[p0 + k] = pk;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (nvalid == 0) return;
+  unsigned nh = 0;
+  bool cap = false;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (k >= nvalid) continue;
+    const int64_t p = p0 + k;
+    const uint32_t fb = ((k < 4 ? any0 : any1) >> (8 * (k & 3))) & TE_F;
+    const bool any = fb != 0 || ((anyb_generic >> k) & 1u);
+    O.halting[p] = any ? 0 : 1;
+    nh += any ? 0 : 1;
+    if (!O.classify_only) {
+      if (!any) O.psi[p] = 0;  // halting: no children (reading A5)
+      cap |= O.psi[p] > PSI_LIMIT || O.ndc[p] > KMAX;
+      O.fpb0[p] = a[k];
+      O.fpb1[p] = b[k];
+    }
+  }
+  if (cap) atomicOr(O.err, ERR_CAPACITY);
+  if (nh) atomicAdd(O.n_halting, (unsigned long long)nh);
+}
+
+// Generic K-a (systems whose neurons cannot all be tabulated): the same walk,
+// every rule evaluated from its descriptor.
+template <typename T>
+__global__ void __launch_bounds__(256) k_expand_g(SysView S, LevelView L, ExpandOut O) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tile = (int64_t)blockIdx.x * XW + warp;
+  const int64_t p0 = tile * XTILE + lane * XPPL;
+  if (tile * XTILE >= L.F) return;
+  const T* data = reinterpret_cast<const T*>(L.data);
+  uint64_t a[8], b[8], psi[8];
+  int ndc[8];
+  uint32_t anyb = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
     const bool ok = p0 + k < L.F;
-    f0[k] = ok ? L.fp0[p0 + k] : 0;
-    f1[k] = ok ? L.fp1[p0 + k] : 0;
+    a[k] = ok ? L.fp0[p0 + k] : 0;
+    b[k] = ok ? L.fp1[p0 + k] : 0;
     psi[k] = 1;
     ndc[k] = 0;
-    any[k] = false;
   }
-  uint32_t eword = 0;
+  uint8_t* Eb = reinterpret_cast<uint8_t*>(O.ebits);
   for (int32_t s = 0; s < S.m; ++s) {
-    int32_t v[4];
-    load4<T>(data + (int64_t)s * L.pitch, p0, L.F, v);
-    const int r0 = __ldg(S.rule_off + s), r1 = __ldg(S.rule_off + s + 1);
-    int first[4] = {-1, -1, -1, -1};
-    int d[4] = {0, 0, 0, 0};
-    for (int r = r0; r < r1; ++r) {
-      const DevRule R = S.rules[r];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (rule_app(R, v[k])) {
-          if (d[k] == 0) first[k] = r;
-          ++d[k];
-        }
-      }
-    }
-    uint32_t nib = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (p0 + k >= L.F) d[k] = 0;
-      if (d[k] > 0) {
-        any[k] = true;
-        f0[k] += __ldg(S.h0 + first[k]);
-        f1[k] += __ldg(S.h1 + first[k]);
-        if (d[k] >= 2) {
-          if (!O.classify_only && ndc[k] < KMAX)
-            O.nd[(p0 + k) * KMAX + ndc[k]] = ((uint64_t)(uint32_t)s << 32) | (uint32_t)v[k];
-          ++ndc[k];
-          psi[k] = sat_mul(psi[k], (uint64_t)d[k]);
-        }
-        if (BIN && S.rules[first[k]].p > 0) nib |= 1u << k;
-      }
-    }
-    if (!O.classify_only) {
-      if (BIN) {
-        eword |= nib << (4 * (s & 7));
-        if ((s & 7) == 7 || s == S.m - 1) {
-          O.ebits[(int64_t)(s >> 3) * O.ebits_ld + tile * 32 + lane] = eword;
-          eword = 0;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (p0 + k < L.F) O.evals[(int64_t)s * O.evals_ld + p0 + k] = d[k] > 0 ? S.rules[first[k]].p : 0;
-      }
-    }
+    uint32_t v[8];
+    load8<T>(data, p0, s, S.m, L.F, v);
+    uint32_t eb = 0;
+    expand_generic_neuron(S, O, s, v, p0, L.F, a, b, psi, ndc, anyb, eb);
+    if (Eb && !O.classify_only && p0 < L.F) Eb[emit_index(p0, s, S.m)] = (uint8_t)eb;
   }
   unsigned nh = 0;
   bool cap = false;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 8; ++k) {
     const int64_t p = p0 + k;
     if (p >= L.F) continue;
-    const uint64_t ps = any[k] ? psi[k] : 0;  // halting: no children (reading A5)
+    const bool any = (anyb >> k) & 1u;
+    const uint64_t ps = any ? psi[k] : 0;
     cap |= ps > PSI_LIMIT || ndc[k] > KMAX;
-    O.halting[p] = any[k] ? 0 : 1;
-    nh += any[k] ? 0 : 1;
+    O.halting[p] = any ? 0 : 1;
+    nh += any ? 0 : 1;
     if (!O.classify_only) {
       O.psi[p] = ps;
-      O.fpb0[p] = f0[k];
-      O.fpb1[p] = f1[k];
+      O.fpb0[p] = a[k];
+      O.fpb1[p] = b[k];
       O.ndc[p] = ndc[k];
     }
   }
@@ -434,68 +698,216 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 }
 
 // ---------------------------------------------------------------------------
-// K-c: materialize kept children.  Base value per (neuron j, parent):
-//   x = C[j] - c_first(j) + Σ_{s ∈ in(j)} p_first(s)
-// written to every kept child of the parent; children whose ND digits differ
-// from the base are corrected exactly by k_patch.
+// K-c (fast): one CTA per storage block of 64 parents.
+//   1. TMA bulk-copies the block's emit words E[s] (bit k = parent k of the
+//      block fires a spiking rule at neuron s) into shared memory;
+//   2. lane = target neuron j: the in-synapse gather Σ_{s∈in(j)} emit(s, ·) is
+//      a bit-sliced counter over the 64 parents (ripple-carry on NPL planes);
+//   3. x = C[j] - c_first(j) + count per parent (consumption from the compact
+//      outcome table, staged per lane in shared memory), staged per lane and
+//      written to every kept child of the parent (row j of the output blocks).
+// ND digits ≠ 0 are corrected afterwards by k_patch (exact), out-of-range
+// base values by k_overflow_fix.
 // ---------------------------------------------------------------------------
-template <typename T, bool BIN>
-__global__ void __launch_bounds__(128) k_materialize(SysView S, LevelView L, ExpandOut O, const uint64_t* kq_off,
-                                                      NextArrays N, uint64_t* ovf, unsigned long long* n_ovf,
-                                                      uint64_t ovf_cap) {
-  const int lane = threadIdx.x & 31;
-  const int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t p0 = tile * TILE + 4 * lane;
-  if (tile * TILE >= L.F) return;
-  uint64_t qa[4];
-  uint64_t hi = 0;
-  if (p0 < L.F) {
+constexpr int MW = 16;       // warps per K-c CTA
+constexpr int QCAP = 4092;   // outputs per block resolved through the r(q) table (+4 alignment slack)
+constexpr int CROW = 64;     // staged consumption-table bytes per lane
+
+template <typename T>
+__host__ __device__ constexpr int xs_stride() { return PB * (int)sizeof(T) + 4; }
+
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+template <int NPL>
+__device__ __forceinline__ uint32_t count_quad(const uint64_t (&c)[NPL], int r0) {
+  uint32_t acc = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) qa[k] = kq_off[min(p0 + k, L.F)];
-    hi = kq_off[min(p0 + 4, L.F)];
-  } else {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) qa[k] = 0;
+  for (int b = 0; b < NPL; ++b) acc |= spread4((uint32_t)(c[b] >> r0) & 0xFu) << b;
+  return acc;
+}
+
+template <typename T, int NPL>
+__global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView L, ExpandOut O,
+                                                             const uint64_t* kq_off, NextArrays N, uint64_t* ovf,
+                                                             unsigned long long* n_ovf, uint64_t ovf_cap) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int32_t m = S.m;
+  const int64_t mE = (m + 1) & ~1;
+  uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words
+  uint8_t* sX = smem + mE * 8;                                          // MW×32×xs_stride
+  uint8_t* sC = sX + (size_t)MW * 32 * xs_stride<T>();                  // MW×32×(CROW+4)
+  uint8_t* sR = sC + (size_t)MW * 32 * (CROW + 4);                      // QCAP
+  uint64_t* sQ = reinterpret_cast<uint64_t*>(sR + QCAP + 4);            // 65 (+1 pad)
+  uint64_t* bar = sQ + 66;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t blk = blockIdx.x;
+  const int64_t pb0 = blk * PB;
+  const int np = (L.F - pb0 < PB) ? (int)(L.F - pb0) : PB;
+  const uint64_t Q0 = kq_off[pb0], Q1 = kq_off[pb0 + np];
+  if (Q1 == Q0) return;  // no kept child in this block (CTA-uniform)
+  const uint32_t ebytes = (uint32_t)(mE * 8);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
   }
-  const uint64_t lo = qa[0];
-  if (__ballot_sync(0xFFFFFFFFu, hi > lo) == 0) return;
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bar, ebytes);
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(O.ebits) + (size_t)blk * ebytes;
+    for (uint32_t off = 0; off < ebytes; off += 32768u)
+      bulk_g2s(reinterpret_cast<uint8_t*>(sE) + off, src + off, min(32768u, ebytes - off), bar);
+  }
+  if (tid <= np) sQ[tid] = kq_off[pb0 + tid];
+  __syncthreads();
+  const uint64_t nq = Q1 - Q0;
+  const uint64_t Qb = Q0 & ~3ULL;  // sR[q - Qb]: 4-aligned for q % 4 == 0
+  if (nq <= QCAP) {
+    if (tid < np)
+      for (uint64_t q = sQ[tid]; q < sQ[tid + 1]; ++q) sR[q - Qb] = (uint8_t)tid;
+  }
+  // parents with kept children (bit r), for the overflow bookkeeping
+  uint64_t haskids = 0;
+  for (int r = 0; r < np; ++r) haskids |= (uint64_t)(sQ[r + 1] > sQ[r]) << r;
+  __syncthreads();
+  mbar_wait(bar, 0);
+
   const T* data = reinterpret_cast<const T*>(L.data);
   T* out = reinterpret_cast<T*>(N.data);
-  for (int32_t j = 0; j < S.m; ++j) {
-    int32_t v[4];
-    load4<T>(data + (int64_t)j * L.pitch, p0, L.F, v);
-    const int r0 = __ldg(S.rule_off + j), r1 = __ldg(S.rule_off + j + 1);
-    int32_t x[4] = {0, 0, 0, 0};
-    bool found[4] = {false, false, false, false};
-    for (int r = r0; r < r1; ++r) {
-      const DevRule R = S.rules[r];
+  uint8_t* xsb = sX + (size_t)(warp * 32 + lane) * xs_stride<T>();
+  T* xs = reinterpret_cast<T*>(xsb);
+  uint8_t* crow_s = sC + (size_t)(warp * 32 + lane) * (CROW + 4);
+  const int crow_bytes = S.tabw * (int)sizeof(T);
+  const bool crow_staged = crow_bytes <= CROW;
+  const T* ctab = reinterpret_cast<const T*>(S.ctab);
+  const int j_iters = (m + MW * 32 - 1) / (MW * 32);
+  for (int it = 0; it < j_iters; ++it) {
+    const int32_t j = it * MW * 32 + warp * 32 + lane;
+    if (j >= m) continue;
+    // ---- bit-sliced in-synapse count over the 64 parents of the block
+    uint64_t c[NPL];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (!found[k] && rule_app(R, v[k])) { found[k] = true; x[k] = -R.c; }
-    }
-    for (int e = __ldg(S.in_off + j), e1 = __ldg(S.in_off + j + 1); e < e1; ++e) {
-      const int32_t s = __ldg(S.in_src + e);
-      if (BIN) {
-        const uint32_t w = O.ebits[(int64_t)(s >> 3) * O.ebits_ld + tile * 32 + lane] >> (4 * (s & 7));
+    for (int b = 0; b < NPL; ++b) c[b] = 0;
+    const int e0 = __ldg(S.in_off + j), e1 = __ldg(S.in_off + j + 1);
+    for (int e = e0; e < e1; ++e) {
+      uint64_t carry = sE[__ldg(S.in_src + e)];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] += (w >> k) & 1;
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] += (p0 + k < L.F) ? O.evals[(int64_t)s * O.evals_ld + p0 + k] : 0;
+      for (int b = 0; b < NPL; ++b) {
+        const uint64_t t = c[b] & carry;
+        c[b] ^= carry;
+        carry = t;
       }
     }
+    const NeuronMeta mt = S.meta[j];
+    const T* crow_g = ctab + (int64_t)j * S.tabw;
+    const T* row = data + eidx(pb0, j, m);
+    const bool generic = mt.flags & NM_GENERIC;
+    uint64_t ovf_bits = 0;
+    if (sizeof(T) == 1 && !generic && crow_staged && mt.pm >= 0) {
+      // fast path: consumption table row staged in this lane's shared slice,
+      // branch-free power-of-two fold, SWAR over 4 parents per 32-bit word
+      {
+        const uint32_t* g = reinterpret_cast<const uint32_t*>(crow_g);
+        uint32_t* d = reinterpret_cast<uint32_t*>(crow_s);
+        for (int i = 0; i < crow_bytes / 4; ++i) d[i] = __ldg(g + i);
+      }
+      const int32_t Lj = mt.L;
+      const uint32_t pm = (uint32_t)mt.pm;
+      const uint4* row4 = reinterpret_cast<const uint4*>(row);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      x[k] += v[k];
-      if ((x[k] > S.count_max || x[k] < 0) && p0 + k < L.F && (k < 3 ? qa[k + 1] : hi) > qa[k]) {
-        unsigned long long slot = atomicAdd(n_ovf, 1ULL);
-        if (slot < ovf_cap) ovf[slot] = ((uint64_t)(uint32_t)j << 32) | (uint64_t)(p0 + k);
+      for (int g = 0; g < 4; ++g) {
+        const uint4 vv = (16 * g < np) ? __ldg(row4 + g) : make_uint4(0, 0, 0, 0);
+        const uint32_t vw[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          const int r0 = 16 * g + 4 * qd;
+          const uint32_t v4 = vw[qd];
+          uint32_t c4 = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int32_t v = (int32_t)((v4 >> (8 * i)) & 0xFFu);
+            const uint32_t idx = (uint32_t)min(v, Lj) + ((uint32_t)max(v - Lj, 0) & pm);
+            c4 |= (uint32_t)crow_s[idx] << (8 * i);
+          }
+          const uint32_t t4 = v4 - c4;  // no borrow: c_first <= v per byte
+          const uint32_t k4 = count_quad<NPL>(c, r0);
+          const uint32_t s7 = (t4 & 0x7F7F7F7Fu) + (k4 & 0x7F7F7F7Fu);
+          const uint32_t co = ((t4 & k4) | ((t4 | k4) & s7)) & 0x80808080u;  // carry out of each byte
+          const uint32_t x4 = s7 ^ ((t4 ^ k4) & 0x80808080u);
+          reinterpret_cast<uint32_t*>(xsb)[r0 >> 2] = x4;
+          if (co) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if ((co >> (8 * i + 7)) & 1u) ovf_bits |= 1ULL << (r0 + i);
+          }
+        }
+      }
+    } else {
+      for (int r = 0; r < PB; ++r) {
+        const int32_t v = (r < np) ? (int32_t)row[r] : 0;
+        int32_t cons;
+        if (generic) {
+          const int rf = nth_applicable(S, j, v, 0);
+          cons = rf >= 0 ? S.rules[rf].c : 0;
+        } else {
+          cons = (int32_t)crow_g[table_index((uint32_t)v, mt)];
+        }
+        int32_t cnt = 0;
+#pragma unroll
+        for (int b = 0; b < NPL; ++b) cnt |= (int32_t)((c[b] >> r) & 1ULL) << b;
+        const int64_t x = (int64_t)v - cons + cnt;
+        if (x > S.count_max) ovf_bits |= 1ULL << r;
+        xs[r] = (T)x;
       }
     }
-    for (uint64_t q = lo; q < hi; ++q) {
-      const int k = (q >= qa[1]) + (q >= qa[2]) + (q >= qa[3]);
-      out[(int64_t)j * N.pitch + q] = (T)x[k];
+    ovf_bits &= haskids;
+    while (ovf_bits) {  // rare: base value beyond the storage range
+      const int r = __ffsll((long long)ovf_bits) - 1;
+      ovf_bits &= ovf_bits - 1;
+      unsigned long long slot = atomicAdd(n_ovf, 1ULL);
+      if (slot < ovf_cap) ovf[slot] = ((uint64_t)(uint32_t)j << 32) | (uint64_t)(pb0 + r);
     }
+    // ---- write x to every kept child of the block's parents (row j of the output)
+    if (nq <= QCAP) {
+      uint64_t q = Q0;
+      while (q < Q1) {
+        const uint64_t qe = min(Q1, (q | (PB - 1)) + 1);  // end of this output block
+        T* orow = out + (((int64_t)(q >> 6) * m + j) << 6);
+        if (sizeof(T) == 1) {
+          for (; q < qe && (q & 3); ++q) orow[q & 63] = xs[sR[q - Qb]];
+          for (; q + 4 <= qe; q += 4) {
+            const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (q - Qb));  // 4 parent indices
+            const uint32_t w = (uint32_t)xsb[rr & 0xFF] | ((uint32_t)xsb[(rr >> 8) & 0xFF] << 8) |
+                               ((uint32_t)xsb[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xsb[rr >> 24] << 24);
+            *reinterpret_cast<uint32_t*>(orow + (q & 63)) = w;
+          }
+        }
+        for (; q < qe; ++q) orow[q & 63] = xs[sR[q - Qb]];
+      }
+    } else {
+      for (int r = 0; r < np; ++r)
+        for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = xs[r];
+    }
+  }
+}
+
+// K-c (generic): every (kept child, neuron) computed exactly.
+template <typename T>
+__global__ void k_materialize_exact(SysView S, LevelView L, ExpandOut O, NextArrays N, int64_t K, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  T* out = reinterpret_cast<T*>(N.data);
+  for (int64_t q = warp; q < K; q += nwarps) {
+    const int64_t p = N.parent[q];
+    ChildCtx cx;
+    decode_child(S, O.nd + p * KMAX, O.ndc[p], N.t[q], cx);
+    bool bad = false;
+    for (int32_t j = lane; j < S.m; j += 32) {
+      const int64_t val = exact_value<T>(S, L.data, p, j, cx);
+      bad |= (val < 0 || val > S.count_max);
+      out[eidx(q, j, S.m)] = (T)val;
+    }
+    if (bad) atomicOr(err, ERR_OVERFLOW);
   }
 }
 
@@ -515,9 +927,9 @@ __global__ void k_patch(SysView S, LevelView L, ExpandOut O, NextArrays N, int64
       const int32_t s = cx.s[i];
       for (int e = -1; e < S.out_off[s + 1] - S.out_off[s]; ++e) {
         const int32_t j = e < 0 ? s : S.out_dst[S.out_off[s] + e];
-        const int64_t val = exact_value<T>(S, L.data, L.pitch, p, j, cx);
+        const int64_t val = exact_value<T>(S, L.data, p, j, cx);
         if (val < 0 || val > S.count_max) atomicOr(err, ERR_OVERFLOW);
-        out[(int64_t)j * N.pitch + q] = (T)val;
+        out[eidx(q, j, S.m)] = (T)val;
       }
     }
   }
@@ -535,9 +947,9 @@ __global__ void k_overflow_fix(SysView S, LevelView L, ExpandOut O, const uint64
     for (uint64_t q = kq_off[p]; q < kq_off[p + 1]; ++q) {
       ChildCtx cx;
       decode_child(S, O.nd + p * KMAX, O.ndc[p], N.t[q], cx);
-      const int64_t val = exact_value<T>(S, L.data, L.pitch, p, j, cx);
+      const int64_t val = exact_value<T>(S, L.data, p, j, cx);
       if (val < 0 || val > S.count_max) atomicOr(err, ERR_OVERFLOW);
-      else out[(int64_t)j * N.pitch + q] = (T)val;
+      else out[eidx((int64_t)q, j, S.m)] = (T)val;
     }
   }
 }
@@ -571,14 +983,13 @@ __global__ void k_verify(SysView S, LevelView L, ExpandOut O, const uint64_t* of
     }
     bool diff = false;
     for (int32_t j = lane; j < S.m; j += 32) {
-      const int64_t a = exact_value<T>(S, L.data, L.pitch, p, j, cx);
+      const int64_t a = exact_value<T>(S, L.data, p, j, cx);
       int64_t b;
       if (vd == 1) {
-        b = exact_value<T>(S, L.data, L.pitch, po, j, co);
+        b = exact_value<T>(S, L.data, po, j, co);
       } else {
         const uint64_t ref = C.cref[c];
-        const StoredLevel sl = stored[ref >> 40];
-        b = ld_count<T>(sl.data, sl.pitch, j, (int64_t)(ref & ((1ULL << 40) - 1)));
+        b = ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, S.m);
       }
       diff |= (a != b);
     }
@@ -603,17 +1014,15 @@ __global__ void k_level0_compact(const uint8_t* verdict, const uint64_t* kept, c
 }
 
 template <typename T>
-__global__ void k_gather_columns(const T* src, int64_t src_pitch, const uint64_t* src_index, int64_t K, int32_t m,
-                                 T* dst, int64_t dst_pitch) {
+__global__ void k_gather_columns(const T* src, const uint64_t* src_index, int64_t K, int32_t m, T* dst) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= K) return;
-  const uint64_t c = src_index[q];
-  for (int32_t j = blockIdx.y; j < m; j += gridDim.y) dst[(int64_t)j * dst_pitch + q] = src[(int64_t)j * src_pitch + c];
+  const int64_t c = (int64_t)src_index[q];
+  for (int32_t j = blockIdx.y; j < m; j += gridDim.y) dst[eidx(q, j, m)] = src[eidx(c, j, m)];
 }
 
 template <typename T>
-__global__ void k_verify_level0(const T* data, int64_t pitch, int32_t m, ChildArrays C, uint64_t F0, Tables tb,
-                                int32_t* err) {
+__global__ void k_verify_level0(const T* data, int32_t m, ChildArrays C, uint64_t F0, Tables tb, int32_t* err) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -621,7 +1030,7 @@ __global__ void k_verify_level0(const T* data, int64_t pitch, int32_t m, ChildAr
     const uint64_t w = tb.ltab[C.cslot[c]].tag;
     if (w == c) continue;
     bool diff = false;
-    for (int32_t j = lane; j < m; j += 32) diff |= data[(int64_t)j * pitch + c] != data[(int64_t)j * pitch + w];
+    for (int32_t j = lane; j < m; j += 32) diff |= data[eidx((int64_t)c, j, m)] != data[eidx((int64_t)w, j, m)];
     if (__any_sync(0xFFFFFFFFu, diff) && lane == 0) atomicOr(err, ERR_COLLISION);
   }
 }
@@ -630,12 +1039,11 @@ __global__ void k_rehash(const Slot* old_tab, uint64_t old_cap, Slot* new_tab, u
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < old_cap; i += (uint64_t)gridDim.x * blockDim.x) {
     const Key128 key = ld_key(old_tab + i);
     if (key.k0 == EMPTY && key.k1 == EMPTY) continue;
-    Tables tb{new_tab, new_mask, nullptr, 0};
     uint64_t h = fmix64(key.k0) & new_mask;
     bool ok = false;
     for (uint64_t probes = 0; probes <= new_mask; ++probes, h = (h + 1) & new_mask) {
       Key128 empty{EMPTY, EMPTY};
-      const Key128 prev = atomicCAS(reinterpret_cast<Key128*>(tb.vis + h), empty, key);
+      const Key128 prev = atomicCAS(reinterpret_cast<Key128*>(new_tab + h), empty, key);
       if (prev.k0 == EMPTY && prev.k1 == EMPTY) {
         new_tab[h].ref = old_tab[i].ref;
         ok = true;
@@ -665,21 +1073,60 @@ __global__ void k_digest(NextArrays N, int64_t K, uint64_t level, unsigned long 
 
 // The spiking vector that produced each child (Alg. 2 II-2/II-3 decode).
 template <typename T>
-__global__ void k_spiking_vectors(SysView S, const T* pdata, int64_t ppitch, const int64_t* parent, const uint64_t* tt,
-                                  int64_t K, uint8_t* S_out) {
+__global__ void k_spiking_vectors(SysView S, const T* pdata, const int64_t* parent, const uint64_t* tt, int64_t K,
+                                  uint8_t* S_out) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < K; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = parent[q];
     uint64_t t = tt[q];
     uint8_t* Sq = S_out + q * S.n;
     for (int64_t r = 0; r < S.n; ++r) Sq[r] = 0;
     for (int32_t s = S.m - 1; s >= 0; --s) {  // least significant digit = last neuron
-      const int32_t v = (int32_t)pdata[(int64_t)s * ppitch + p];
+      const int32_t v = (int32_t)pdata[eidx(p, s, S.m)];
       const int d = count_applicable(S, s, v);
       if (d == 0) continue;
       const int x = (int)(t % (uint64_t)d);
       t /= (uint64_t)d;
       Sq[nth_applicable(S, s, v, x)] = 1;
     }
+  }
+}
+
+// Outcome tables, one thread per (neuron, table index): the
+// applicability of every rule at count v evaluated once per
+// system instead of once per (neuron, configuration).
+template <typename T>
+__global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_full) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t w = S.tabw;
+  const int64_t n_c = (int64_t)S.m * w;
+  const int64_t n_f = tab_full ? (int64_t)S.m * 256 : 0;
+  if (i >= n_c + n_f) return;
+  const bool full = i >= n_c;
+  const int32_t s = (int32_t)(full ? (i - n_c) / 256 : i / w);
+  const uint32_t slot = (uint32_t)(full ? (i - n_c) % 256 : i % w);
+  const NeuronMeta mt = S.meta[s];
+  uint32_t entry = 0;
+  int32_t cons = 0;
+  const bool valid = !(mt.flags & NM_GENERIC) && (full || (int64_t)slot < (int64_t)mt.L + (mt.pm >= 0 ? mt.pm + 1 : -mt.pm));
+  if (valid) {
+    // compact slot idx stands for count v = idx (idx < L + P); full slot is v itself
+    const int32_t v = (int32_t)slot;
+    int first = -1, d = 0;
+    for (int r = S.rule_off[s]; r < S.rule_off[s + 1]; ++r)
+      if (rule_app(S.rules[r], v)) {
+        if (!d) first = r;
+        ++d;
+      }
+    if (d) {
+      entry = ((uint32_t)(first - S.rule_off[s] + 1) << 4) | (S.rules[first].p > 0 ? TE_EMIT : 0u) | (d >= 2 ? TE_ND : 0u);
+      cons = S.rules[first].c;
+    }
+  }
+  if (full) {
+    tab_full[i - n_c] = (uint8_t)entry;
+  } else {
+    tab[i] = (uint8_t)entry;
+    ctab[i] = (T)cons;
   }
 }
 
@@ -695,47 +1142,81 @@ void dispatch_bytes(int32_t bytes, F&& f) {
 // ===========================================================================
 // launchers
 // ===========================================================================
+bool fast_expand_ok(const SysView& S) { return S.tables_ok != 0; }
+
+void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ctab, uint8_t* tab_full,
+                         cudaStream_t st) {
+  const uint64_t n = (uint64_t)S.m * S.tabw + (tab_full ? (uint64_t)S.m * 256 : 0);
+  dispatch_bytes(bytes, [&](auto tt) {
+    using T = decltype(tt);
+    k_build_tables<T><<<grid_for(n), BLK, 0, st>>>(S, tab, reinterpret_cast<T*>(ctab), tab_full);
+  });
+  count_launch();
+}
+
+size_t materialize_smem_bytes(const SysView& S, int32_t bytes) {
+  const size_t mE = (size_t)((S.m + 1) & ~1);
+  const size_t xs = (size_t)MW * 32 * (PB * bytes + 4);
+  const size_t cs = (size_t)MW * 32 * (CROW + 4);
+  return mE * 8 + xs + cs + (QCAP + 4) + 67 * 8 + 16;
+}
+
+bool fast_materialize_ok(const SysView& S) {
+  const int32_t w = S.count_max <= 255 ? 1 : S.count_max <= 65535 ? 2 : 4;
+  return S.tables_ok && S.binary_emit && S.max_indeg < 256 && materialize_smem_bytes(S, w) <= 220 * 1024;
+}
+
 void launch_import(const void* src, int32_t src_bytes, int32_t src_layout, int64_t src_ld, int64_t F, int32_t m,
-                   void* dst, int32_t dst_bytes, int64_t dst_pitch, int64_t count_max, int32_t* err, cudaStream_t st) {
+                   void* dst, int32_t dst_bytes, int64_t count_max, int32_t* err, cudaStream_t st) {
   dim3 grid((unsigned)((F + 31) / 32), (unsigned)((m + 31) / 32)), block(32, 8);
   dispatch_bytes(src_bytes, [&](auto tin) {
     using Tin = decltype(tin);
     dispatch_bytes(dst_bytes, [&](auto tout) {
       using Tout = decltype(tout);
       k_import<Tin, Tout><<<grid, block, 0, st>>>(src, src_layout, src_ld, F, m, reinterpret_cast<Tout*>(dst),
-                                                  dst_pitch, count_max, err);
-      count_launch();
+                                                  count_max, err);
     });
   });
+  count_launch();
 }
 
-void launch_export(const void* src, int32_t bytes, int64_t pitch, int64_t F, int32_t m, int32_t* dst, cudaStream_t st) {
+void launch_export(const void* src, int32_t bytes, int64_t F, int32_t m, int32_t* dst, cudaStream_t st) {
   dim3 grid((unsigned)((F + 31) / 32), (unsigned)((m + 31) / 32)), block(32, 8);
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    k_export<T><<<grid, block, 0, st>>>(reinterpret_cast<const T*>(src), pitch, F, m, dst);
-    count_launch();
+    k_export<T><<<grid, block, 0, st>>>(reinterpret_cast<const T*>(src), F, m, dst);
   });
+  count_launch();
 }
 
-static unsigned tiles_grid(int64_t F) { return (unsigned)((F + 4 * TILE - 1) / (4 * TILE)); }
-
-void launch_fingerprint(const SysView& S, int32_t bytes, const void* data, int64_t pitch, int64_t F, uint64_t* fp0,
-                        uint64_t* fp1, cudaStream_t st) {
+void launch_fingerprint(const SysView& S, int32_t bytes, const void* data, int64_t F, uint64_t* fp0, uint64_t* fp1,
+                        cudaStream_t st) {
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    k_fingerprint<T><<<tiles_grid(F), 128, 0, st>>>(S, reinterpret_cast<const T*>(data), pitch, F, fp0, fp1);
-    count_launch();
+    k_fingerprint<T><<<grid_for(F), BLK, 0, st>>>(S, reinterpret_cast<const T*>(data), F, fp0, fp1);
   });
+  count_launch();
 }
+
+static unsigned expand_grid(int64_t F) { return (unsigned)((F + XW * XTILE - 1) / (XW * XTILE)); }
 
 void launch_expand(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, cudaStream_t st) {
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    if (S.binary_emit) k_expand<T, true><<<tiles_grid(L.F), 128, 0, st>>>(S, L, O);
-    else k_expand<T, false><<<tiles_grid(L.F), 128, 0, st>>>(S, L, O);
-    count_launch();
+    if (!fast_expand_ok(S)) {
+      k_expand_g<T><<<expand_grid(L.F), XW * 32, 0, st>>>(S, L, O);
+    } else {
+      const bool full = S.full8 && sizeof(T) == 1;
+      const size_t smem = expand_smem_bytes<T>(full ? 256 : S.tabw);
+      auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<expand_grid(L.F), XW * 32, smem, st>>>(S, L, O);
+      };
+      if (full) go(k_expand_t<T, true>);
+      else go(k_expand_t<T, false>);
+    }
   });
+  count_launch();
 }
 
 void launch_child_parent(const uint64_t* off, int64_t F, uint32_t* cpar, cudaStream_t st) {
@@ -755,8 +1236,8 @@ void launch_dedup(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tab
   count_launch();
 }
 
-void launch_winners(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, uint64_t, int,
-                    unsigned long long* n_new, cudaStream_t st) {
+void launch_winners(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, unsigned long long* n_new,
+                    cudaStream_t st) {
   unsigned g = grid_for(T);
   if (g > 148u * 16u) g = 148u * 16u;
   k_winners<<<g, BLK, 0, st>>>(C, T, tag_base, tb, n_new);
@@ -781,26 +1262,42 @@ void launch_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, uint64_
 }
 
 void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O,
-                        const uint64_t* kq_off, const NextArrays& N, uint64_t* ovf, unsigned long long* n_ovf,
-                        uint64_t ovf_cap, cudaStream_t st) {
-  dispatch_bytes(bytes, [&](auto tt) {
-    using T = decltype(tt);
-    if (S.binary_emit)
-      k_materialize<T, true><<<tiles_grid(L.F), 128, 0, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
-    else
-      k_materialize<T, false><<<tiles_grid(L.F), 128, 0, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
-    count_launch();
-  });
+                        const uint64_t* kq_off, const NextArrays& N, int64_t K, uint64_t* ovf,
+                        unsigned long long* n_ovf, uint64_t ovf_cap, int32_t* err, cudaStream_t st) {
+  if (K <= 0) return;
+  if (fast_materialize_ok(S)) {
+    const size_t smem = materialize_smem_bytes(S, bytes);
+    const unsigned nblk = (unsigned)((L.F + PB - 1) / PB);
+    dispatch_bytes(bytes, [&](auto tt) {
+      using T = decltype(tt);
+      auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<nblk, MW * 32, smem, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
+      };
+      if (S.max_indeg < 16) go(k_materialize_bs<T, 4>);
+      else if (S.max_indeg < 32) go(k_materialize_bs<T, 5>);
+      else if (S.max_indeg < 64) go(k_materialize_bs<T, 6>);
+      else go(k_materialize_bs<T, 8>);
+    });
+  } else {
+    unsigned g = grid_for((uint64_t)K * 32, 256);
+    if (g > 148u * 32u) g = 148u * 32u;
+    dispatch_bytes(bytes, [&](auto tt) {
+      using T = decltype(tt);
+      k_materialize_exact<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
+    });
+  }
+  count_launch();
 }
 
 void launch_patch(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const NextArrays& N,
                   int64_t K, int32_t* err, cudaStream_t st) {
-  if (K <= 0) return;
+  if (K <= 0 || !fast_materialize_ok(S)) return;  // the exact path needs no patch
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
     k_patch<T><<<grid_for(K, 128), 128, 0, st>>>(S, L, O, N, K, err);
-    count_launch();
   });
+  count_launch();
 }
 
 void launch_overflow_fix(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O,
@@ -810,8 +1307,8 @@ void launch_overflow_fix(const SysView& S, int32_t bytes, const LevelView& L, co
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
     k_overflow_fix<T><<<grid_for(n_ovf, 128), 128, 0, st>>>(S, L, O, kq_off, N, ovf, n_ovf, err);
-    count_launch();
   });
+  count_launch();
 }
 
 void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
@@ -823,8 +1320,8 @@ void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const Ex
   dispatch_bytes(bytes, [&](auto tt) {
     using TT = decltype(tt);
     k_verify<TT><<<g, 256, 0, st>>>(S, L, O, off, C, T, tag_base, tb, stored, err);
-    count_launch();
   });
+  count_launch();
 }
 
 void launch_level0_compact(const uint8_t* verdict, const uint64_t* kept, const uint64_t* kpos, int64_t F0,
@@ -834,27 +1331,27 @@ void launch_level0_compact(const uint8_t* verdict, const uint64_t* kept, const u
   count_launch();
 }
 
-void launch_gather_columns(int32_t bytes, const void* src, int64_t src_pitch, const uint64_t* src_index, int64_t K,
-                           int32_t m, void* dst, int64_t dst_pitch, cudaStream_t st) {
+void launch_gather_columns(int32_t bytes, const void* src, const uint64_t* src_index, int64_t K, int32_t m, void* dst,
+                           cudaStream_t st) {
   if (K <= 0) return;
   dim3 grid(grid_for(K), (unsigned)min(m, 1024));
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    k_gather_columns<T><<<grid, BLK, 0, st>>>(reinterpret_cast<const T*>(src), src_pitch, src_index, K, m,
-                                              reinterpret_cast<T*>(dst), dst_pitch);
-    count_launch();
+    k_gather_columns<T><<<grid, BLK, 0, st>>>(reinterpret_cast<const T*>(src), src_index, K, m,
+                                              reinterpret_cast<T*>(dst));
   });
+  count_launch();
 }
 
-void launch_verify_level0(int32_t bytes, const void* data, int64_t pitch, int32_t m, const ChildArrays& C,
-                          uint64_t F0, const Tables& tb, int32_t* err, cudaStream_t st) {
+void launch_verify_level0(int32_t bytes, const void* data, int32_t m, const ChildArrays& C, uint64_t F0,
+                          const Tables& tb, int32_t* err, cudaStream_t st) {
   unsigned g = grid_for(F0 * 32, 256);
   if (g > 148u * 64u) g = 148u * 64u;
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    k_verify_level0<T><<<g, 256, 0, st>>>(reinterpret_cast<const T*>(data), pitch, m, C, F0, tb, err);
-    count_launch();
+    k_verify_level0<T><<<g, 256, 0, st>>>(reinterpret_cast<const T*>(data), m, C, F0, tb, err);
   });
+  count_launch();
 }
 
 void launch_rehash(const Slot* old_tab, uint64_t old_cap, Slot* new_tab, uint64_t new_mask, int32_t* err,
@@ -871,15 +1368,15 @@ void launch_digest(const NextArrays& N, int64_t K, uint64_t level, unsigned long
   count_launch();
 }
 
-void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_data, int64_t parent_pitch,
-                            const int64_t* parent, const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st) {
+void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_data, const int64_t* parent,
+                            const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st) {
   if (K <= 0) return;
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    k_spiking_vectors<T><<<grid_for(K, 128), 128, 0, st>>>(S, reinterpret_cast<const T*>(parent_data), parent_pitch,
-                                                         parent, t, K, S_out);
-    count_launch();
+    k_spiking_vectors<T><<<grid_for(K, 128), 128, 0, st>>>(S, reinterpret_cast<const T*>(parent_data), parent, t, K,
+                                                         S_out);
   });
+  count_launch();
 }
 
 size_t scan_temp_bytes(int64_t n) {

@@ -250,3 +250,32 @@ def test_device_level0_generator_matches_host(snp):
     torch.cuda.synchronize()
     host = W.level0_counts(w, F, 77, dtype=np.uint8)
     assert (buf.cpu().numpy().T == host).all()
+
+
+def test_generic_neurons(snp):
+    """Neurons the outcome tables cannot hold (> 15 rules; an EXACT exponent
+    beyond the table width) take the rule-by-rule path inside the same kernels."""
+    rng = np.random.default_rng(1)
+    m = 40
+    out = [np.sort(rng.choice([j for j in range(m) if j != s], 5, replace=False)) for s in range(m)]
+    rules = []
+    for s in range(m):
+        if s == 3:
+            for x in range(20):
+                rules.append([s, W.PERIODIC, 2 + x, 3, 1 + x % 3, x % 2])
+        elif s == 7:
+            rules += [[s, W.EXACT, 700, 0, 5, 1], [s, W.PERIODIC, 2, 1, 1, 1]]
+        else:
+            rules.append([s, W.PERIODIC, 2, 1, 2, 1])
+    rules = np.array(rules, np.int32)
+    row_ptr, col, val = W._csr_from_rows(W.matrix_rows_from_rules(rules, out))
+    C0 = rng.integers(0, 8, m).astype(np.int32)
+    C0[3] = 30
+    C0[7] = 700
+    w = W.Workload("generic", m, rules, row_ptr, col, val, C0, np.full(m, 8, np.int32))
+    for bits in (16, 32):
+        for dedup in (0, 1):
+            tree = snp.System(w, count_bits=bits, dedup=dedup, frontier_target=300).explore(None, depth=4)
+            ref = oracle.System.from_workload(w).explore(C0, depth=4, dedup=dedup, count_bits=bits,
+                                                         frontier_target=300)
+            assert_same_tree(tree, ref)
