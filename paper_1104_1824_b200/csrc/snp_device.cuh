@@ -93,6 +93,11 @@ struct SysView {
   const uint64_t* h1;
   const int32_t* in_off;     // m + 1
   const int32_t* in_src;     // sources s with (s, j) ∈ syn, grouped by target j
+  // the same in-synapses "edge-major" per group of 32 consecutive targets:
+  // group g holds in_pad_deg[g] rows of 32 sources (row e, lane l = e-th
+  // in-synapse of target 32g + l), padded with the index m_even (a zero word)
+  const int32_t* in_pad;
+  const int64_t* in_pad_off;   // m/32 + 1 row offsets (×32 entries)
   const int32_t* out_off;    // m + 1
   const int32_t* out_dst;    // targets j with (s, j) ∈ syn, grouped by source s
   const uint64_t* R0;        // m fingerprint weights (reading A18)

@@ -170,7 +170,7 @@ struct snp_system {
   std::vector<int32_t> C0;
   bool binary_emit = true;
   // ---- device system
-  DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1;
+  DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1, d_in_pad, d_in_pad_off;
   SysView view{};
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -511,6 +511,24 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   SNP_TRY(upload(s, s->d_h1, h1));
   SNP_TRY(upload(s, s->d_in_off, in_off));
   SNP_TRY(upload(s, s->d_in_src, in_src));
+  // edge-major padded in-CSR per group of 32 targets (coalesced K-c gathers)
+  {
+    const int64_t ng = (m + 31) / 32;
+    const int32_t pad = (int32_t)((m + 1) & ~1);  // index of the zero emit word
+    std::vector<int64_t> pad_off(ng + 1, 0);
+    for (int64_t g = 0; g < ng; ++g) {
+      int32_t mx = 0;
+      for (int64_t j = 32 * g; j < std::min<int64_t>(m, 32 * g + 32); ++j) mx = std::max(mx, in_off[j + 1] - in_off[j]);
+      pad_off[g + 1] = pad_off[g] + mx;
+    }
+    std::vector<int32_t> in_pad((size_t)pad_off[ng] * 32, pad);
+    for (int64_t g = 0; g < ng; ++g)
+      for (int64_t j = 32 * g; j < std::min<int64_t>(m, 32 * g + 32); ++j)
+        for (int32_t e = in_off[j]; e < in_off[j + 1]; ++e)
+          in_pad[(size_t)(pad_off[g] + (e - in_off[j])) * 32 + (j - 32 * g)] = in_src[e];
+    SNP_TRY(upload(s, s->d_in_pad, in_pad));
+    SNP_TRY(upload(s, s->d_in_pad_off, pad_off));
+  }
   SNP_TRY(upload(s, s->d_out_off, out_off));
   SNP_TRY(upload(s, s->d_out_dst, out_dst));
   SNP_TRY(upload(s, s->d_R0, R0));
@@ -569,6 +587,8 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.h1 = s->d_h1.as<uint64_t>();
   v.in_off = s->d_in_off.as<int32_t>();
   v.in_src = s->d_in_src.as<int32_t>();
+  v.in_pad = s->d_in_pad.as<int32_t>();
+  v.in_pad_off = s->d_in_pad_off.as<int64_t>();
   v.out_off = s->d_out_off.as<int32_t>();
   v.out_dst = s->d_out_dst.as<int32_t>();
   v.R0 = s->d_R0.as<uint64_t>();

@@ -733,10 +733,10 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   extern __shared__ __align__(16) uint8_t smem[];
   const int32_t m = S.m;
   const int64_t mE = (m + 1) & ~1;
-  uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words
-  uint8_t* sX = smem + mE * 8;                                          // MW×32×xs_stride
+  uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words + 2 zero words
+  uint8_t* sX = smem + (mE + 2) * 8;                                    // MW×32×xs_stride
   uint8_t* sC = sX + (size_t)MW * 32 * xs_stride<T>();                  // MW×32×(CROW+4)
-  uint8_t* sR = sC + (size_t)MW * 32 * (CROW + 4);                      // QCAP
+  uint8_t* sR = sC + (size_t)MW * 32 * CROW;                            // QCAP
   uint64_t* sQ = reinterpret_cast<uint64_t*>(sR + QCAP + 4);            // 65 (+1 pad)
   uint64_t* bar = sQ + 66;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -758,6 +758,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       bulk_g2s(reinterpret_cast<uint8_t*>(sE) + off, src + off, min(32768u, ebytes - off), bar);
   }
   if (tid <= np) sQ[tid] = kq_off[pb0 + tid];
+  if (tid < 2) sE[mE + tid] = 0;  // target of padded in-synapses
   __syncthreads();
   const uint64_t nq = Q1 - Q0;
   const uint64_t Qb = Q0 & ~3ULL;  // sR[q - Qb]: 4-aligned for q % 4 == 0
@@ -775,26 +776,42 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   T* out = reinterpret_cast<T*>(N.data);
   uint8_t* xsb = sX + (size_t)(warp * 32 + lane) * xs_stride<T>();
   T* xs = reinterpret_cast<T*>(xsb);
-  uint8_t* crow_s = sC + (size_t)(warp * 32 + lane) * (CROW + 4);
+  uint8_t* crow_t = sC + (size_t)warp * 32 * CROW + lane * 4;  // transposed: [word][lane]
   const int crow_bytes = S.tabw * (int)sizeof(T);
   const bool crow_staged = crow_bytes <= CROW;
   const T* ctab = reinterpret_cast<const T*>(S.ctab);
   const int j_iters = (m + MW * 32 - 1) / (MW * 32);
   for (int it = 0; it < j_iters; ++it) {
-    const int32_t j = it * MW * 32 + warp * 32 + lane;
-    if (j >= m) continue;
+    const int32_t jbase = it * MW * 32 + warp * 32;
+    if (jbase >= m) break;  // warp-uniform
+    const int32_t j = jbase + lane;
+    const bool jok = j < m;
+    if (jok) {
     // ---- bit-sliced in-synapse count over the 64 parents of the block
     uint64_t c[NPL];
 #pragma unroll
     for (int b = 0; b < NPL; ++b) c[b] = 0;
-    const int e0 = __ldg(S.in_off + j), e1 = __ldg(S.in_off + j + 1);
-    for (int e = e0; e < e1; ++e) {
-      uint64_t carry = sE[__ldg(S.in_src + e)];
+    {
+      // edge-major padded in-CSR: row e of the group holds the e-th source
+      // of every lane's target (coalesced), padding points at a zero word
+      const int64_t g = jbase >> 5;
+      const int64_t r0 = __ldg(S.in_pad_off + g), r1 = __ldg(S.in_pad_off + g + 1);
+      const int32_t* col = S.in_pad + r0 * 32 + lane;
+      const int ne = (int)(r1 - r0);
+      for (int e0 = 0; e0 < ne; e0 += 8) {
+        int32_t src[8];
 #pragma unroll
-      for (int b = 0; b < NPL; ++b) {
-        const uint64_t t = c[b] & carry;
-        c[b] ^= carry;
-        carry = t;
+        for (int u = 0; u < 8; ++u) src[u] = (e0 + u < ne) ? __ldg(col + (e0 + u) * 32) : (int32_t)mE;  // batch the loads
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint64_t carry = sE[src[u]];
+#pragma unroll
+          for (int b = 0; b < NPL; ++b) {
+            const uint64_t t = c[b] & carry;
+            c[b] ^= carry;
+            carry = t;
+          }
+        }
       }
     }
     const NeuronMeta mt = S.meta[j];
@@ -806,9 +823,14 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       // fast path: consumption table row staged in this lane's shared slice,
       // branch-free power-of-two fold, SWAR over 4 parents per 32-bit word
       {
-        const uint32_t* g = reinterpret_cast<const uint32_t*>(crow_g);
-        uint32_t* d = reinterpret_cast<uint32_t*>(crow_s);
-        for (int i = 0; i < crow_bytes / 4; ++i) d[i] = __ldg(g + i);
+        // word w of this lane's table row lives at column (w, lane): every
+        // lookup of a lane hits its own bank
+        const uint4* g = reinterpret_cast<const uint4*>(crow_g);
+        uint32_t* d = reinterpret_cast<uint32_t*>(crow_t);
+        for (int i = 0; i < crow_bytes / 16; ++i) {
+          const uint4 x = __ldg(g + i);
+          d[(4 * i) * 32] = x.x; d[(4 * i + 1) * 32] = x.y; d[(4 * i + 2) * 32] = x.z; d[(4 * i + 3) * 32] = x.w;
+        }
       }
       const int32_t Lj = mt.L;
       const uint32_t pm = (uint32_t)mt.pm;
@@ -826,7 +848,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
           for (int i = 0; i < 4; ++i) {
             const int32_t v = (int32_t)((v4 >> (8 * i)) & 0xFFu);
             const uint32_t idx = (uint32_t)min(v, Lj) + ((uint32_t)max(v - Lj, 0) & pm);
-            c4 |= (uint32_t)crow_s[idx] << (8 * i);
+            c4 |= (uint32_t)crow_t[((idx & ~3u) << 5) | (idx & 3u)] << (8 * i);
           }
           const uint32_t t4 = v4 - c4;  // no borrow: c_first <= v per byte
           const uint32_t k4 = count_quad<NPL>(c, r0);
@@ -873,13 +895,18 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         const uint64_t qe = min(Q1, (q | (PB - 1)) + 1);  // end of this output block
         T* orow = out + (((int64_t)(q >> 6) * m + j) << 6);
         if (sizeof(T) == 1) {
+          auto quad = [&](uint64_t qq) {
+            const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (qq - Qb));  // 4 parent indices
+            return (uint32_t)xsb[rr & 0xFF] | ((uint32_t)xsb[(rr >> 8) & 0xFF] << 8) |
+                   ((uint32_t)xsb[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xsb[rr >> 24] << 24);
+          };
           for (; q < qe && (q & 3); ++q) orow[q & 63] = xs[sR[q - Qb]];
-          for (; q + 4 <= qe; q += 4) {
-            const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (q - Qb));  // 4 parent indices
-            const uint32_t w = (uint32_t)xsb[rr & 0xFF] | ((uint32_t)xsb[(rr >> 8) & 0xFF] << 8) |
-                               ((uint32_t)xsb[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xsb[rr >> 24] << 24);
-            *reinterpret_cast<uint32_t*>(orow + (q & 63)) = w;
+          for (; q + 4 <= qe && (q & 15); q += 4) *reinterpret_cast<uint32_t*>(orow + (q & 63)) = quad(q);
+          for (; q + 16 <= qe; q += 16) {  // 16 children per store: overlap the smem latencies
+            const uint32_t w0 = quad(q), w1 = quad(q + 4), w2 = quad(q + 8), w3 = quad(q + 12);
+            *reinterpret_cast<uint4*>(orow + (q & 63)) = make_uint4(w0, w1, w2, w3);
           }
+          for (; q + 4 <= qe; q += 4) *reinterpret_cast<uint32_t*>(orow + (q & 63)) = quad(q);
         }
         for (; q < qe; ++q) orow[q & 63] = xs[sR[q - Qb]];
       }
@@ -887,6 +914,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       for (int r = 0; r < np; ++r)
         for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = xs[r];
     }
+    }  // jok
   }
 }
 
@@ -1157,8 +1185,8 @@ void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ct
 size_t materialize_smem_bytes(const SysView& S, int32_t bytes) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
   const size_t xs = (size_t)MW * 32 * (PB * bytes + 4);
-  const size_t cs = (size_t)MW * 32 * (CROW + 4);
-  return mE * 8 + xs + cs + (QCAP + 4) + 67 * 8 + 16;
+  const size_t cs = (size_t)MW * 32 * CROW;
+  return (mE + 2) * 8 + xs + cs + (QCAP + 4) + 67 * 8 + 16;
 }
 
 bool fast_materialize_ok(const SysView& S) {
