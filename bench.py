@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--m", type=int, default=0, help="override neuron count (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="use the multi-GPU driver even on 1 GPU (testing)")
     return ap.parse_args()
 
 
@@ -211,10 +212,16 @@ def run_native(args, rank, world):
     import torch
     from paper_1104_1824_b200 import snp
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-    dev = torch.device("cuda")
-    if world > 1:
-        raise SystemExit("bench.py: multi-GPU exploration is not built yet (DESIGN.md §9); run with --gpus 1")
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    use_dist = world > 1 or args.dist
+    if use_dist:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     cfg, w = workload_for(args)
     m, F = w.m, cfg["F"]
     wb = cfg["count_bits"] // 8
@@ -223,57 +230,79 @@ def run_native(args, rank, world):
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     eng.set_profiling(True)
-    # level 0 generated on the device (inputs resident in HBM)
-    buf = torch.empty((m, F), dtype=torch.uint8 if wb == 1 else torch.int32, device=dev)
-    snp.generate_level0_device(w, F, cfg["seed"], buf.data_ptr(), wb, snp.SNP_LAYOUT_NEURON_MAJOR, F,
-                               stream.cuda_stream)
-    eng.begin(snp.configs_from_device(buf.data_ptr(), F, F, wb, snp.SNP_LAYOUT_NEURON_MAJOR))
+    # level 0 generated on the device (inputs resident in HBM); rank r holds rows [lo, hi)
+    if use_dist:
+        from paper_1104_1824_b200 import dist as D
+        lo, hi = D.level0_slice(F, rank, world)
+        runner = D.DistExplorer(eng)
+    else:
+        lo, hi, runner = 0, F, eng
+    Fl = hi - lo
+    buf = torch.empty((m, max(Fl, 1)), dtype=torch.uint8 if wb == 1 else torch.int32, device=dev)
+    if Fl:
+        snp.generate_level0_device(w, Fl, cfg["seed"], buf.data_ptr(), wb, snp.SNP_LAYOUT_NEURON_MAJOR, Fl,
+                                   stream.cuda_stream, row_begin=lo)
+    runner.begin(snp.configs_from_device(buf.data_ptr(), Fl, max(Fl, 1), wb, snp.SNP_LAYOUT_NEURON_MAJOR))
     del buf
     torch.cuda.empty_cache()
     for _ in range(args.warmup):
-        eng.advance()
+        runner.advance()
     prof0 = eng.profile()
     launches0 = snp.snp_kernel_launches()
     clocks = Clocks(torch.cuda.current_device())
     clocks.start()
+    if dist:
+        dist.barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     levels = []
     for _ in range(args.steps):
-        levels.append(eng.advance())
+        levels.append(runner.advance())
     e1.record(stream)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     clk = clocks.stop()
     elapsed_ms = e0.elapsed_time(e1)
+    if dist:  # max over ranks
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
     launches = snp.snp_kernel_launches() - launches0
     prof1 = eng.profile()
     phase_ms = {k: prof1[k] - prof0[k] for k in prof1}
     T_sum = sum(c["T"] for c in levels)
     value = T_sum / (elapsed_ms / 1e3)
     peak, peak_src = measured_peak()
-    # per-phase algorithmic bytes
+    # per-phase algorithmic bytes of THIS rank's kernels
+    par = [c.get("parents_local", c["parents"]) for c in levels]
+    kep = [c.get("kept_local", c["kept"]) for c in levels]
+    Tl = [c.get("T_local", c["T"]) for c in levels]
     alg = {
-        "expand": sum(c["parents"] * m * wb for c in levels),
-        "materialize": sum(c["kept"] * m * wb for c in levels),
-        "dedup": sum(c["T"] * 32 + c["kept"] * 48 for c in levels),
-        "keys": sum(c["T"] * 16 for c in levels),
+        "expand": sum(x * m * wb for x in par),
+        "materialize": sum(x * m * wb for x in kep),
+        "dedup": sum(t * 32 + k * 48 for t, k in zip(Tl, kep)),
+        "keys": sum(t * 16 for t in Tl),
     }
     dom = max(("expand", "materialize", "dedup", "keys"), key=lambda k: phase_ms.get(k, 0.0))
     achieved = alg[dom] / (phase_ms[dom] / 1e3) / 1e9 if phase_ms[dom] > 0 else 0.0
-    sb = sum(step_bytes(c, m, wb) for c in levels)
-    n_conf, T_total, digest = eng.summary()
+    sb = sum(p_ * m * wb + k * m * wb + t * 32 + k * 48 for p_, k, t in zip(par, kep, Tl))
+    n_conf, T_total, digest = runner.summary()
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": f"u{8 * wb}" if wb < 4 else "i32", "data": "synthetic",
-        "config": config_json(args, cfg, w, args.steps),
-        "roofline": {"bound": "hbm", "kernel": f"phase '{dom}' ({'k_expand' if dom == 'expand' else 'k_materialize+k_patch' if dom == 'materialize' else dom})",
+        "config": {**config_json(args, cfg, w, args.steps),
+                   "parallelism": f"hash-partitioned dedup over {world} GPU(s), keys all-to-all (NCCL)"
+                   if world > 1 else "1 GPU"},
+        "roofline": {"bound": "hbm", "kernel": f"phase '{dom}' ({'k_expand_t' if dom == 'expand' else 'k_materialize_bs+k_patch' if dom == 'materialize' else dom})",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(dom), "peak_source": peak_src},
-        "step_roofline": {"algorithmic_GB_per_step": sb / len(levels) / 1e9,
-                          "achieved": sb / (elapsed_ms / 1e3) / 1e9, "frac": sb / (elapsed_ms / 1e3) / 1e9 / peak},
+        "step_roofline": {"algorithmic_GB_per_step_per_gpu": sb / len(levels) / 1e9,
+                          "achieved_per_gpu": sb / (elapsed_ms / 1e3) / 1e9,
+                          "frac": sb / (elapsed_ms / 1e3) / 1e9 / peak},
         "phase_ms_per_step": {**{k: v / args.steps for k, v in phase_ms.items()},
                               "other": elapsed_ms / args.steps - sum(phase_ms.values()) / args.steps},
         "levels": [{k: c[k] for k in ("parents", "halting", "T", "n_new", "kept")} | {"ms": round(c["ms"], 3)}
@@ -281,13 +310,19 @@ def run_native(args, rank, world):
         "digest": f"{digest:016x}", "gpu_launches": launches, "clocks": clk,
     }
     eng.close()
-    del eng
+    del eng, runner
     torch.cuda.empty_cache()
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         out["e2e"] = run_e2e(args, cfg, w, snp, torch)
-    if not args.no_cpu and rank == 0:
+    elif not args.no_e2e:
+        out["e2e"] = {"value": None, "unit": UNIT, "note": "e2e measured at N=1 only this round"}
+    if not args.no_cpu and rank == 0 and world == 1:
         out["cpu_baseline"] = cpu_baseline(w, cfg)
-    print(json.dumps(out), flush=True)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def run_e2e(args, cfg, w, snp, torch):

@@ -177,6 +177,31 @@ snp_status snp_profile(const snp_system *sys, double *ms /* SNP_NUM_PHASES */);
 /* Kernels launched by this process through libsnp.so so far. */
 int64_t    snp_kernel_launches(void);
 
+/* Multi-GPU exploration (one process per GPU).  Rank r holds a
+ * contiguous range of the global frontier (global order = rank order, then
+ * local tag order) and the visited keys with owner fmix64(fp1) mod P.  The
+ * caller runs the collectives between the calls (paper_1104_1824_b200/dist.py):
+ *   snp_dist_begin(level0 rows of this rank)      → keys of the level-0 rows
+ *   snp_dist_expand                               → local T (children keys)
+ *   snp_dist_pack(tag_base = Σ T of lower ranks, send: device T×3 uint64
+ *                 {fp0, fp1, global tag} grouped by owner, counts[P] host)
+ *   [all-to-all of keys]
+ *   snp_dist_owner_dedup(recv: device R×3)        → N_new of this owner
+ *   [all-reduce of N_new]
+ *   snp_dist_owner_keep(N_new global, verdict: device R bytes)
+ *   [all-to-all of the verdicts back]
+ *   snp_dist_finalize(verdict_back: device T bytes, in send order) → local K
+ *   [all-gather of K and of the frontier sizes]
+ *   snp_dist_commit(parent_offset, q_offset)      → the next local level
+ * dedup = 1 only.  Results (configurations, order, digest) equal a 1-GPU run. */
+snp_status snp_dist_begin(snp_system *sys, const snp_configs *level0, int32_t nranks, int64_t *n_local);
+snp_status snp_dist_expand(snp_system *sys, int64_t *T_local);
+snp_status snp_dist_pack(snp_system *sys, uint64_t tag_base, void *send, int64_t *counts);
+snp_status snp_dist_owner_dedup(snp_system *sys, const void *recv, int64_t R, int64_t *n_new_local);
+snp_status snp_dist_owner_keep(snp_system *sys, int64_t n_new_global, void *verdict_out);
+snp_status snp_dist_finalize(snp_system *sys, const void *verdict_back, int64_t *K_local);
+snp_status snp_dist_commit(snp_system *sys, int64_t parent_offset, int64_t q_offset, snp_level_counters *out);
+
 /* snp_begin + `depth` × snp_advance + halting classification of the last
  * level; the tree is a snapshot owned by the caller.                          */
 snp_status snp_explore(snp_system *sys, const snp_configs *level0, int32_t depth, snp_tree **out);

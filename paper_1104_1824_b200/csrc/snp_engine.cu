@@ -194,6 +194,23 @@ struct snp_system {
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   std::vector<DBuf> spare;  // released level buffers kept for reuse
   Arena arena;              // per-level metadata
+  // multi-GPU exploration (snp_dist_*): this rank's share of the frontier and
+  // of the visited keys (owner = fmix64(fp1) mod P)
+  struct Dist {
+    int32_t P = 0;          // 0 = not in distributed mode
+    int stage = 0;          // 0 idle, 1 keys ready, 2 packed, 3 owner-deduped, 4 owner-kept, 5 finalized
+    bool level0 = false;
+    uint64_t T = 0, R = 0;
+    int64_t K = 0;
+    const uint64_t* recv = nullptr;
+    snp_level_counters lc{};
+    DBuf raw;               // level-0 rows before the global dedup
+    int64_t F0 = 0;
+    DBuf fp0, fp1;          // level-0 fingerprints
+    DBuf perm, hist, slot, verdict;
+    ExpandOut O{};
+    int64_t owned = 0;      // keys in this rank's visited shard
+  } dist;
   // phase profiling (snp_set_profiling)
   bool profiling = false;
   double prof_ms[SNP_NUM_PHASES] = {0, 0, 0, 0, 0};
@@ -609,6 +626,8 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
 // exploration
 // ---------------------------------------------------------------------------
 snp_status reset_state(snp_system* s) {
+  s->dist.P = 0;
+  s->dist.stage = 0;
   for (double& x : s->prof_ms) x = 0;
   s->marks.clear();
   s->ev_used = 0;
@@ -701,7 +720,7 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
   SNP_TRY(s->src_index.ensure(std::max<int64_t>(K, 1) * 8));
   NextArrays N{nullptr, L->parent.as<int64_t>(), L->t.as<uint64_t>(), L->fp0.as<uint64_t>(), L->fp1.as<uint64_t>()};
   launch_level0_compact(C.verdict, C.kept, C.kpos, F0, fp0.as<uint64_t>(), fp1.as<uint64_t>(), N,
-                        s->src_index.as<uint64_t>(), tb, err, s->stream);
+                        s->src_index.as<uint64_t>(), tb, 1, err, s->stream);
   if (K == F0) {
     L->data = std::move(raw);
   } else {
@@ -709,7 +728,7 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
     launch_gather_columns(s->bytes, raw.p, s->src_index.as<uint64_t>(), K, (int32_t)m, L->data.p, s->stream);
   }
   N.data = L->data.p;
-  launch_digest(N, K, 0, &dc(s)->digest, s->stream);
+  launch_digest(N, K, 0, 0, 0, &dc(s)->digest, s->stream);
   CUDA_TRY(cudaGetLastError());
   SNP_TRY(read_counters(s, &hc));
   SNP_TRY(check_err(hc.err));
@@ -850,7 +869,7 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     NextArrays N{nullptr, next->parent.as<int64_t>(), next->t.as<uint64_t>(), next->fp0.as<uint64_t>(),
                  next->fp1.as<uint64_t>()};
     phase_begin(s, 2);
-    launch_compact(C, off, T, N, tb, (uint64_t)s->levels.size() << 40, err, st);
+    launch_compact(C, off, T, N, tb, (uint64_t)s->levels.size() << 40, 1, err, st);
     phase_end(s);
     if (K > 0) {
       SNP_TRY(take_buffer(s, level_bytes(K, m, s->bytes), &next->data));
@@ -876,7 +895,7 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
         phase_end(s);
         CUDA_TRY(cudaGetLastError());
       }
-      launch_digest(N, K, (uint64_t)s->levels.size(), &dc(s)->digest, st);
+      launch_digest(N, K, (uint64_t)s->levels.size(), 0, 0, &dc(s)->digest, st);
     }
     if (s->opt.dedup == 0) {
       SNP_TRY(update_stored_table(s));
@@ -1045,7 +1064,7 @@ snp_status snp_begin(snp_system* s, const snp_configs* level0) {
 
 snp_status snp_advance(snp_system* s, snp_level_counters* counters) {
   if (!s) return fail(SNP_E_ARG, "NULL system");
-  if (!s->begun) return fail(SNP_E_STATE, "snp_advance before snp_begin (or after an error)");
+  if (!s->begun) return fail(SNP_E_STATE, "snp_advance before snp_begin (or after an error, or in distributed mode)");
   snp_status st = advance_impl(s, counters);
   if (st != SNP_OK) s->begun = false;
   return st;
@@ -1199,5 +1218,359 @@ snp_status snp_tree_spiking_vectors(const snp_tree* t, int32_t level, uint8_t* S
 }
 
 void snp_tree_free(snp_tree* t) { delete t; }
+
+}  // extern "C"
+
+// ===========================================================================
+// multi-GPU exploration.  Each rank holds a contiguous range of
+// the global frontier (global order = rank order, then local tag order) and the
+// visited keys it owns (owner = fmix64(fp1) mod P).  One level:
+//   snp_dist_expand      K-a/K-b on the local frontier: child keys, local T
+//   snp_dist_pack        keys bucketed by owner into a caller buffer
+//   [caller: all-to-all of keys]
+//   snp_dist_owner_dedup visited shard + level table (minimum global tag)
+//   [caller: all-reduce of N_new]
+//   snp_dist_owner_keep  thinning with the global N_new, visited insert, verdicts
+//   [caller: all-to-all of verdicts back]
+//   snp_dist_finalize    kept flags of the local children, local K
+//   [caller: all-gather of K and F for the global offsets]
+//   snp_dist_commit      K-c materialization of the local kept children
+// The collectives are the caller's (paper_1104_1824_b200/dist.py, torch
+// NCCL); every step of the method runs in the kernels below the ABI.
+// ===========================================================================
+namespace {
+
+snp_status dist_stage(snp_system* s, int want) {
+  if (!s) return fail(SNP_E_ARG, "NULL system");
+  if (s->dist.P < 1) return fail(SNP_E_STATE, "not in distributed mode (snp_dist_begin)");
+  if (s->dist.stage != want) return fail(SNP_E_STATE, "distributed call out of order (stage %d, expected %d)", s->dist.stage, want);
+  return SNP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+snp_status snp_dist_begin(snp_system* s, const snp_configs* level0, int32_t nranks, int64_t* n_local) {
+  if (!s || !level0 || nranks < 1) return fail(SNP_E_ARG, "snp_dist_begin: bad arguments");
+  if (s->opt.dedup != 1) return fail(SNP_E_STATE, "distributed exploration needs dedup = 1 (fingerprint keys)");
+  const int64_t F0 = level0->n_configs, m = s->m;
+  if (F0 < 0 || F0 > 0x7FFFFFFFLL || (F0 > 0 && !level0->data)) return fail(SNP_E_ARG, "level0: bad n_configs / data");
+  if (level0->elem_bytes != 1 && level0->elem_bytes != 2 && level0->elem_bytes != 4) return fail(SNP_E_ARG, "level0: elem_bytes");
+  SNP_TRY(reset_state(s));
+  s->dist = snp_system::Dist{};
+  s->dist.P = nranks;
+  s->begun = false;
+  SNP_TRY(zero_counters(s));
+  int32_t* err = &dc(s)->err;
+  SNP_TRY(s->dist.raw.ensure(std::max<size_t>(level_bytes(F0, m, s->bytes), 256), false));
+  SNP_TRY(s->dist.fp0.ensure(std::max<int64_t>(F0, 1) * 8, false));
+  SNP_TRY(s->dist.fp1.ensure(std::max<int64_t>(F0, 1) * 8, false));
+  SNP_TRY(ensure_children(s, (uint64_t)std::max<int64_t>(F0, 1)));
+  SNP_TRY(ensure_visited(s, 4 * (uint64_t)std::max<int64_t>(F0, 1024)));
+  if (F0 > 0) {
+    const int64_t ld = level0->ld ? level0->ld : (level0->layout == SNP_LAYOUT_ROW_MAJOR ? m : F0);
+    const size_t in_bytes = (size_t)(level0->layout == SNP_LAYOUT_ROW_MAJOR ? (F0 - 1) * ld + m : (m - 1) * ld + F0) *
+                            level0->elem_bytes;
+    DBuf staged;
+    const void* src = level0->data;
+    if (!level0->on_device) {
+      SNP_TRY(staged.ensure(in_bytes, false));
+      CUDA_TRY(cudaMemcpyAsync(staged.p, level0->data, in_bytes, cudaMemcpyHostToDevice, s->stream));
+      src = staged.p;
+    }
+    launch_import(src, level0->elem_bytes, level0->layout, ld, F0, (int32_t)m, s->dist.raw.p, s->bytes, s->count_max,
+                  err, s->stream);
+    launch_fingerprint(s->view, s->bytes, s->dist.raw.p, F0, s->dist.fp0.as<uint64_t>(), s->dist.fp1.as<uint64_t>(),
+                       s->stream);
+    ChildArrays C = child_arrays(s);
+    CUDA_TRY(cudaMemcpyAsync(C.cfp0, s->dist.fp0.p, F0 * 8, cudaMemcpyDeviceToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(C.cfp1, s->dist.fp1.p, F0 * 8, cudaMemcpyDeviceToDevice, s->stream));
+    CUDA_TRY(cudaGetLastError());
+  }
+  DevCounters hc;
+  SNP_TRY(read_counters(s, &hc));
+  SNP_TRY(check_err(hc.err));
+  s->dist.F0 = F0;
+  s->dist.T = (uint64_t)F0;
+  s->dist.level0 = true;
+  s->dist.stage = 1;
+  if (n_local) *n_local = F0;
+  return SNP_OK;
+}
+
+snp_status snp_dist_expand(snp_system* s, int64_t* T_local) {
+  SNP_TRY(dist_stage(s, 0));
+  Level* cur = s->levels.back().get();
+  const int64_t F = cur->F, m = s->m;
+  cudaStream_t st = s->stream;
+  snp_level_counters lc{};
+  CUDA_TRY(cudaEventRecord(s->ev0, st));
+  SNP_TRY(zero_counters(s));
+  uint64_t T = 0;
+  if (F > 0) {
+    if (!cur->has_data()) return fail(SNP_E_STATE, "current level has no data");
+    SNP_TRY(s->psi.ensure((F + 1) * 8));
+    SNP_TRY(s->off.ensure((F + 1) * 8));
+    SNP_TRY(s->fpb0.ensure(F * 8));
+    SNP_TRY(s->fpb1.ensure(F * 8));
+    SNP_TRY(s->ndc.ensure(F * 4));
+    SNP_TRY(s->nd.ensure((size_t)F * KMAX * 8));
+    ExpandOut O{};
+    O.psi = s->psi.as<uint64_t>();
+    O.fpb0 = s->fpb0.as<uint64_t>();
+    O.fpb1 = s->fpb1.as<uint64_t>();
+    O.ndc = s->ndc.as<int32_t>();
+    O.nd = s->nd.as<uint64_t>();
+    O.halting = cur->halting.as<uint8_t>();
+    O.n_halting = &dc(s)->n_halting;
+    O.err = &dc(s)->err;
+    if (fast_materialize_ok(s->view)) {
+      SNP_TRY(s->ebits.ensure((size_t)((F + PB - 1) / PB) * (size_t)((m + 1) & ~1) * 8));
+      O.ebits = s->ebits.as<uint64_t>();
+    }
+    CUDA_TRY(cudaMemsetAsync(O.psi + F, 0, 8, st));
+    LevelView LV{cur->data.p, F, cur->fp0.as<uint64_t>(), cur->fp1.as<uint64_t>()};
+    phase_begin(s, 0);
+    launch_expand(s->view, s->bytes, LV, O, st);
+    phase_end(s);
+    SNP_TRY(s->scan_tmp.ensure(scan_temp_bytes(F + 1) + 256));
+    phase_begin(s, 1);
+    launch_exclusive_scan(s->scan_tmp.p, s->scan_tmp.bytes, O.psi, s->off.as<uint64_t>(), F + 1, st);
+    phase_end(s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(&T, s->off.as<uint64_t>() + F, 8, cudaMemcpyDeviceToHost, st));
+    DevCounters hc;
+    SNP_TRY(read_counters(s, &hc));
+    SNP_TRY(check_err(hc.err));
+    lc.halting = (int64_t)hc.n_halting;
+    if (s->opt.max_transitions > 0 && (int64_t)T > s->opt.max_transitions)
+      return fail(SNP_E_CAPACITY, "%llu local transitions exceed the budget", (unsigned long long)T);
+    if (T > 0) {
+      SNP_TRY(ensure_children(s, T));
+      ChildArrays C = child_arrays(s);
+      phase_begin(s, 1);
+      launch_child_parent(s->off.as<uint64_t>(), F, C.cpar, st);
+      launch_child_keys(s->view, s->off.as<uint64_t>(), O, T, C, st);
+      phase_end(s);
+      CUDA_TRY(cudaGetLastError());
+    }
+    s->dist.O = O;
+  }
+  s->halting_current_valid = true;
+  lc.parents = F;
+  lc.T = (int64_t)T;
+  s->dist.lc = lc;
+  s->dist.T = T;
+  s->dist.level0 = false;
+  s->dist.stage = 1;
+  if (T_local) *T_local = (int64_t)T;
+  return SNP_OK;
+}
+
+snp_status snp_dist_pack(snp_system* s, uint64_t tag_base, void* send, int64_t* counts) {
+  SNP_TRY(dist_stage(s, 1));
+  const uint32_t P = (uint32_t)s->dist.P;
+  const uint64_t T = s->dist.T;
+  if (!counts || (T > 0 && !send)) return fail(SNP_E_ARG, "snp_dist_pack: bad arguments");
+  SNP_TRY(s->dist.perm.ensure(std::max<uint64_t>(T, 1) * 8));
+  SNP_TRY(s->dist.hist.ensure(P * 8 + 8));
+  auto* hist = s->dist.hist.as<unsigned long long>();
+  CUDA_TRY(cudaMemsetAsync(hist, 0, P * 8, s->stream));
+  ChildArrays C = child_arrays(s);
+  phase_begin(s, 2);
+  launch_owner_hist(C.cfp1, T, P, hist, s->stream);
+  phase_end(s);
+  std::vector<unsigned long long> h(P), cur(P);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), hist, P * 8, cudaMemcpyDeviceToHost, s->stream));
+  SNP_TRY(sync(s));
+  unsigned long long acc = 0;
+  for (uint32_t r = 0; r < P; ++r) {
+    cur[r] = acc;
+    acc += h[r];
+    counts[r] = (int64_t)h[r];
+  }
+  CUDA_TRY(cudaMemcpyAsync(hist, cur.data(), P * 8, cudaMemcpyHostToDevice, s->stream));
+  phase_begin(s, 2);
+  launch_owner_pack(C.cfp0, C.cfp1, T, P, tag_base, hist, s->dist.perm.as<uint64_t>(), static_cast<uint64_t*>(send),
+                    s->stream);
+  phase_end(s);
+  CUDA_TRY(cudaGetLastError());
+  SNP_TRY(sync(s));
+  s->dist.stage = 2;
+  return SNP_OK;
+}
+
+snp_status snp_dist_owner_dedup(snp_system* s, const void* recv, int64_t R, int64_t* n_new_local) {
+  SNP_TRY(dist_stage(s, 2));
+  if (R < 0 || (R > 0 && !recv)) return fail(SNP_E_ARG, "snp_dist_owner_dedup: bad arguments");
+  SNP_TRY(ensure_ltab(s, (uint64_t)std::max<int64_t>(R, 1)));
+  const uint64_t lslots = next_pow2(std::max<uint64_t>(1024, 2 * (uint64_t)std::max<int64_t>(R, 1)));
+  SNP_TRY(s->dist.slot.ensure(std::max<int64_t>(R, 1) * 8));
+  SNP_TRY(s->dist.verdict.ensure(std::max<int64_t>(R, 1)));
+  SNP_TRY(zero_counters(s));
+  Tables tb = tables(s, lslots);
+  const uint64_t* rv = static_cast<const uint64_t*>(recv);
+  phase_begin(s, 2);
+  launch_owner_dedup(rv, (uint64_t)R, tb, s->dist.verdict.as<uint8_t>(), s->dist.slot.as<uint64_t>(), &dc(s)->err,
+                     s->stream);
+  launch_owner_winners(rv, (uint64_t)R, tb, s->dist.verdict.as<uint8_t>(), s->dist.slot.as<uint64_t>(),
+                       &dc(s)->n_new, s->stream);
+  phase_end(s);
+  CUDA_TRY(cudaGetLastError());
+  DevCounters hc;
+  SNP_TRY(read_counters(s, &hc));
+  SNP_TRY(check_err(hc.err));
+  s->dist.R = (uint64_t)R;
+  s->dist.recv = rv;
+  s->dist.stage = 3;
+  if (n_new_local) *n_new_local = (int64_t)hc.n_new;
+  return SNP_OK;
+}
+
+snp_status snp_dist_owner_keep(snp_system* s, int64_t n_new_global, void* verdict_out) {
+  SNP_TRY(dist_stage(s, 3));
+  const uint64_t R = s->dist.R;
+  if (R > 0 && !verdict_out) return fail(SNP_E_ARG, "snp_dist_owner_keep: bad arguments");
+  uint64_t tau = 0;
+  const int thin = !s->dist.level0 && s->opt.frontier_target > 0 && n_new_global > s->opt.frontier_target;
+  if (thin) {
+    unsigned __int128 num = (unsigned __int128)(uint64_t)s->opt.frontier_target << 64;
+    tau = (uint64_t)(num / (unsigned __int128)(uint64_t)n_new_global);
+  }
+  SNP_TRY(ensure_visited(s, (uint64_t)s->dist.owned + R));
+  const uint64_t lslots = next_pow2(std::max<uint64_t>(1024, 2 * std::max<uint64_t>(R, 1)));
+  Tables tb = tables(s, lslots);
+  SNP_TRY(zero_counters(s));
+  phase_begin(s, 2);
+  launch_owner_keep(s->dist.recv, R, tb, s->dist.verdict.as<uint8_t>(), s->dist.slot.as<uint64_t>(), tau, thin,
+                    static_cast<uint8_t*>(verdict_out), &dc(s)->n_new, &dc(s)->err, s->stream);
+  phase_end(s);
+  CUDA_TRY(cudaGetLastError());
+  DevCounters hc;
+  SNP_TRY(read_counters(s, &hc));
+  SNP_TRY(check_err(hc.err));
+  s->dist.owned += (int64_t)hc.n_new;
+  s->dist.lc.n_new = n_new_global;
+  s->dist.lc.tau = tau;
+  s->dist.stage = 4;
+  return SNP_OK;
+}
+
+snp_status snp_dist_finalize(snp_system* s, const void* verdict_back, int64_t* K_local) {
+  SNP_TRY(dist_stage(s, 4));
+  const uint64_t T = s->dist.T;
+  if (T > 0 && !verdict_back) return fail(SNP_E_ARG, "snp_dist_finalize: bad arguments");
+  ChildArrays C = child_arrays(s);
+  phase_begin(s, 2);
+  launch_unperm(s->dist.perm.as<uint64_t>(), static_cast<const uint8_t*>(verdict_back), T, C.kept, s->stream);
+  launch_exclusive_scan(s->scan_tmp.p, s->scan_tmp.bytes, C.kept, C.kpos, (int64_t)T + 1, s->stream);
+  phase_end(s);
+  CUDA_TRY(cudaGetLastError());
+  uint64_t K = 0;
+  CUDA_TRY(cudaMemcpyAsync(&K, C.kpos + T, 8, cudaMemcpyDeviceToHost, s->stream));
+  SNP_TRY(sync(s));
+  s->dist.K = (int64_t)K;
+  s->dist.stage = 5;
+  if (K_local) *K_local = (int64_t)K;
+  return SNP_OK;
+}
+
+snp_status snp_dist_commit(snp_system* s, int64_t parent_offset, int64_t q_offset, snp_level_counters* out) {
+  SNP_TRY(dist_stage(s, 5));
+  const int64_t K = s->dist.K, m = s->m;
+  cudaStream_t st = s->stream;
+  SNP_TRY(zero_counters(s));
+  int32_t* err = &dc(s)->err;
+  ChildArrays C = child_arrays(s);
+  Tables tb = tables(s, 1024);
+  auto L = std::make_unique<Level>();
+  L->F = K;
+  SNP_TRY(alloc_level_meta(s, L.get(), K));
+  NextArrays N{nullptr, L->parent.as<int64_t>(), L->t.as<uint64_t>(), L->fp0.as<uint64_t>(), L->fp1.as<uint64_t>()};
+  if (s->dist.level0) {
+    const int64_t F0 = s->dist.F0;
+    SNP_TRY(s->src_index.ensure(std::max<int64_t>(K, 1) * 8));
+    if (F0 > 0)
+      launch_level0_compact(C.verdict, C.kept, C.kpos, F0, s->dist.fp0.as<uint64_t>(), s->dist.fp1.as<uint64_t>(), N,
+                            s->src_index.as<uint64_t>(), tb, 0, err, st);
+    if (K == F0) {
+      L->data = std::move(s->dist.raw);
+    } else if (K > 0) {
+      SNP_TRY(take_buffer(s, level_bytes(K, m, s->bytes), &L->data));
+      launch_gather_columns(s->bytes, s->dist.raw.p, s->src_index.as<uint64_t>(), K, (int32_t)m, L->data.p, st);
+    }
+    N.data = L->data.p;
+    launch_digest(N, K, 0, q_offset, 0, &dc(s)->digest, st);
+    CUDA_TRY(cudaGetLastError());
+    DevCounters hc;
+    SNP_TRY(read_counters(s, &hc));
+    SNP_TRY(check_err(hc.err));
+    s->digest += hc.digest;
+    s->n_visited = K;
+    s->dist.raw.release();
+    s->levels.push_back(std::move(L));
+    s->dist.stage = 0;
+    s->dist.level0 = false;
+    if (out) {
+      snp_level_counters lc{};
+      lc.parents = s->dist.F0;
+      lc.kept = K;
+      *out = lc;
+    }
+    return SNP_OK;
+  }
+  Level* cur = s->levels.back().get();
+  const int64_t F = cur->F;
+  const uint64_t T = s->dist.T;
+  if (T > 0)
+    launch_compact(C, s->off.as<uint64_t>(), T, N, tb, 0, 0, err, st);
+  if (K > 0) {
+    SNP_TRY(take_buffer(s, level_bytes(K, m, s->bytes), &L->data));
+    N.data = L->data.p;
+    SNP_TRY(s->kq_off.ensure((F + 1) * 8));
+    const uint64_t ovf_cap = 1ULL << 22;
+    SNP_TRY(s->ovf.ensure(ovf_cap * 8));
+    LevelView LV{cur->data.p, F, cur->fp0.as<uint64_t>(), cur->fp1.as<uint64_t>()};
+    const ExpandOut& O = s->dist.O;
+    phase_begin(s, 3);
+    launch_kq_off(s->off.as<uint64_t>(), C.kpos, F, s->kq_off.as<uint64_t>(), st);
+    launch_materialize(s->view, s->bytes, LV, O, s->kq_off.as<uint64_t>(), N, K, s->ovf.as<uint64_t>(), &dc(s)->n_ovf,
+                       ovf_cap, err, st);
+    launch_patch(s->view, s->bytes, LV, O, N, K, err, st);
+    phase_end(s);
+    CUDA_TRY(cudaGetLastError());
+    DevCounters hc;
+    SNP_TRY(read_counters(s, &hc));
+    if (hc.n_ovf > ovf_cap) return fail(SNP_E_CAPACITY, "too many counts at the storage limit (%llu)", hc.n_ovf);
+    if (hc.n_ovf) {
+      launch_overflow_fix(s->view, s->bytes, LV, O, s->kq_off.as<uint64_t>(), N, s->ovf.as<uint64_t>(), hc.n_ovf, err,
+                          st);
+      CUDA_TRY(cudaGetLastError());
+    }
+  }
+  // parents are indices in the previous level: global = local + parent_offset
+  launch_digest(N, K, (uint64_t)s->levels.size(), q_offset, parent_offset, &dc(s)->digest, st);
+  CUDA_TRY(cudaEventRecord(s->ev1, st));
+  DevCounters hc;
+  SNP_TRY(read_counters(s, &hc));
+  phase_collect(s);
+  SNP_TRY(check_err(hc.err));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  snp_level_counters lc = s->dist.lc;
+  lc.kept = K;
+  lc.ms = ms;
+  s->digest += hc.digest;
+  s->n_visited += K;
+  s->total_T += lc.T;
+  s->counters.push_back(lc);
+  if (!retain_levels(s)) release_level_data(s, cur);
+  s->levels.push_back(std::move(L));
+  s->halting_current_valid = false;
+  s->dist.stage = 0;
+  if (out) *out = lc;
+  return SNP_OK;
+}
 
 }  // extern "C"

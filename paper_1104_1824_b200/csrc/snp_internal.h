@@ -86,7 +86,7 @@ void launch_winners(const ChildArrays& C, uint64_t T, uint64_t tag_base, const T
 void launch_keep(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, uint64_t tau, int thin,
                  cudaStream_t st);
 void launch_compact(const ChildArrays& C, const uint64_t* off, uint64_t T, const NextArrays& N, const Tables& tb,
-                    uint64_t level_ref, int32_t* err, cudaStream_t st);
+                    uint64_t level_ref, int insert_visited, int32_t* err, cudaStream_t st);
 void launch_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, uint64_t* kq_off, cudaStream_t st);
 void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O,
                         const uint64_t* kq_off, const NextArrays& N, int64_t K, uint64_t* ovf,
@@ -101,14 +101,27 @@ void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const Ex
                    const StoredLevel* stored, int32_t* err, cudaStream_t st);
 void launch_level0_compact(const uint8_t* verdict, const uint64_t* kept, const uint64_t* kpos, int64_t F0,
                            const uint64_t* fp0, const uint64_t* fp1, const NextArrays& N, uint64_t* src_index,
-                           const Tables& tb, int32_t* err, cudaStream_t st);
+                           const Tables& tb, int insert_visited, int32_t* err, cudaStream_t st);
 void launch_gather_columns(int32_t bytes, const void* src, const uint64_t* src_index, int64_t K, int32_t m, void* dst,
                            cudaStream_t st);
 void launch_verify_level0(int32_t bytes, const void* data, int32_t m, const ChildArrays& C, uint64_t F0,
                           const Tables& tb, int32_t* err, cudaStream_t st);
 void launch_rehash(const Slot* old_tab, uint64_t old_cap, Slot* new_tab, uint64_t new_mask, int32_t* err,
                    cudaStream_t st);
-void launch_digest(const NextArrays& N, int64_t K, uint64_t level, unsigned long long* digest, cudaStream_t st);
+void launch_digest(const NextArrays& N, int64_t K, uint64_t level, int64_t q_offset, int64_t parent_offset,
+                   unsigned long long* digest, cudaStream_t st);
+// multi-GPU dedup ownership
+void launch_owner_hist(const uint64_t* fp1, uint64_t T, uint32_t P, unsigned long long* counts, cudaStream_t st);
+void launch_owner_pack(const uint64_t* fp0, const uint64_t* fp1, uint64_t T, uint32_t P, uint64_t tag_base,
+                       unsigned long long* cursor, uint64_t* perm, uint64_t* send, cudaStream_t st);
+void launch_owner_dedup(const uint64_t* recv, uint64_t R, const Tables& tb, uint8_t* verdict, uint64_t* slot,
+                        int32_t* err, cudaStream_t st);
+void launch_owner_winners(const uint64_t* recv, uint64_t R, const Tables& tb, const uint8_t* verdict,
+                          const uint64_t* slot, unsigned long long* n_new, cudaStream_t st);
+void launch_owner_keep(const uint64_t* recv, uint64_t R, const Tables& tb, const uint8_t* verdict,
+                       const uint64_t* slot, uint64_t tau, int thin, uint8_t* out, unsigned long long* n_kept,
+                       int32_t* err, cudaStream_t st);
+void launch_unperm(const uint64_t* perm, const uint8_t* back, uint64_t T, uint64_t* kept, cudaStream_t st);
 void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_data, const int64_t* parent,
                             const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st);
 

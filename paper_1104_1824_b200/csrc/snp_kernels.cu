@@ -679,7 +679,7 @@ __device__ void visited_insert(const Tables& tb, uint64_t k0, uint64_t k1, uint6
 }
 
 __global__ void k_compact(ChildArrays C, const uint64_t* off, uint64_t T, NextArrays N, Tables tb,
-                          uint64_t level_ref, int32_t* err) {
+                          uint64_t level_ref, int insert_visited, int32_t* err) {
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T; c += (uint64_t)gridDim.x * blockDim.x) {
     if (!C.kept[c]) continue;
     const uint64_t q = C.kpos[c];
@@ -688,8 +688,100 @@ __global__ void k_compact(ChildArrays C, const uint64_t* off, uint64_t T, NextAr
     N.t[q] = c - off[p];
     N.fp0[q] = C.cfp0[c];
     N.fp1[q] = C.cfp1[c];
-    visited_insert(tb, C.cfp0[c], C.cfp1[c], level_ref | q, err);
+    if (insert_visited) visited_insert(tb, C.cfp0[c], C.cfp1[c], level_ref | q, err);
   }
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU dedup ownership: owner(key) = fmix64(fp1) mod P
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t key_owner(uint64_t fp1, uint32_t P) { return (uint32_t)(fmix64(fp1) % P); }
+
+__global__ void k_owner_hist(const uint64_t* fp1, uint64_t T, uint32_t P, unsigned long long* counts) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T; c += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&counts[key_owner(fp1[c], P)], 1ULL);
+}
+
+// send row pos = {fp0, fp1, global tag}; perm[c] = pos (positions inside an
+// owner's bucket are arbitrary: the owner's decisions do not depend on them)
+__global__ void k_owner_pack(const uint64_t* fp0, const uint64_t* fp1, uint64_t T, uint32_t P, uint64_t tag_base,
+                             unsigned long long* cursor, uint64_t* perm, uint64_t* send) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T; c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pos = atomicAdd(&cursor[key_owner(fp1[c], P)], 1ULL);
+    perm[c] = pos;
+    send[3 * pos] = fp0[c];
+    send[3 * pos + 1] = fp1[c];
+    send[3 * pos + 2] = tag_base + c;
+  }
+}
+
+// owner side: received keys against the visited shard, then the level table
+// with the minimum global tag (same protocol as k_dedup)
+__global__ void k_owner_dedup(const uint64_t* recv, uint64_t R, Tables tb, uint8_t* verdict, uint64_t* slot,
+                              int32_t* err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < R; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k0 = recv[3 * i], k1 = recv[3 * i + 1], tag = recv[3 * i + 2];
+    if (k0 == EMPTY && k1 == EMPTY) {
+      atomicOr(err, ERR_COLLISION);
+      verdict[i] = 0;
+      continue;
+    }
+    const uint64_t h = fmix64(k0);
+    bool old = false;
+    uint64_t j = h & tb.vmask;
+    for (uint64_t probes = 0; probes <= tb.vmask; ++probes, j = (j + 1) & tb.vmask) {
+      const Key128 key = ld_key(tb.vis + j);
+      if (key.k0 == k0 && key.k1 == k1) { old = true; break; }
+      if (key.k0 == EMPTY && key.k1 == EMPTY) break;
+    }
+    if (old) { verdict[i] = 0; continue; }
+    j = h & tb.lmask;
+    bool done = false;
+    for (uint64_t probes = 0; probes <= tb.lmask; ++probes, j = (j + 1) & tb.lmask) {
+      Key128 empty{EMPTY, EMPTY}, mine{k0, k1};
+      const Key128 prev = atomicCAS(reinterpret_cast<Key128*>(tb.ltab + j), empty, mine);
+      if ((prev.k0 == EMPTY && prev.k1 == EMPTY) || (prev.k0 == k0 && prev.k1 == k1)) {
+        atomicMin(&tb.ltab[j].tag, (unsigned long long)tag);
+        slot[i] = j;
+        verdict[i] = 1;
+        done = true;
+        break;
+      }
+    }
+    if (!done) atomicOr(err, ERR_TABLE_FULL);
+  }
+}
+
+__global__ void k_owner_winners(const uint64_t* recv, uint64_t R, Tables tb, const uint8_t* verdict,
+                                const uint64_t* slot, unsigned long long* n_new) {
+  unsigned long long cnt = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < R; i += (uint64_t)gridDim.x * blockDim.x)
+    cnt += verdict[i] == 1 && tb.ltab[slot[i]].tag == recv[3 * i + 2];
+  typedef cub::BlockReduce<unsigned long long, BLK> BR;
+  __shared__ typename BR::TempStorage tmp;
+  unsigned long long tot = BR(tmp).Sum(cnt);
+  if (threadIdx.x == 0 && tot) atomicAdd(n_new, tot);
+}
+
+// kept = winner && (no thinning || fmix64(fp0) < τ); kept keys enter the
+// owner's visited shard; out[i] = kept byte returned to the producer
+__global__ void k_owner_keep(const uint64_t* recv, uint64_t R, Tables tb, const uint8_t* verdict, const uint64_t* slot,
+                             uint64_t tau, int thin, uint8_t* out, unsigned long long* n_kept, int32_t* err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < R; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k0 = recv[3 * i], k1 = recv[3 * i + 1];
+    bool k = verdict[i] == 1 && tb.ltab[slot[i]].tag == recv[3 * i + 2];
+    if (k && thin) k = fmix64(k0) < tau;
+    out[i] = k ? 1 : 0;
+    if (k) {
+      visited_insert(tb, k0, k1, 0, err);
+      atomicAdd(n_kept, 1ULL);
+    }
+  }
+}
+
+__global__ void k_unperm(const uint64_t* perm, const uint8_t* back, uint64_t T, uint64_t* kept) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c <= T; c += (uint64_t)gridDim.x * blockDim.x)
+    kept[c] = c < T ? (uint64_t)back[perm[c]] : 0;
 }
 
 __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, uint64_t* kq_off) {
@@ -1028,7 +1120,7 @@ __global__ void k_verify(SysView S, LevelView L, ExpandOut O, const uint64_t* of
 // level 0 (reading A20): keep the first occurrence of every configuration
 __global__ void k_level0_compact(const uint8_t* verdict, const uint64_t* kept, const uint64_t* kpos, int64_t F0,
                                  const uint64_t* fp0, const uint64_t* fp1, NextArrays N, uint64_t* src_index,
-                                 Tables tb, int32_t* err) {
+                                 Tables tb, int insert_visited, int32_t* err) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < F0; c += (int64_t)gridDim.x * blockDim.x) {
     if (!kept[c]) continue;
     const uint64_t q = kpos[c];
@@ -1037,7 +1129,7 @@ __global__ void k_level0_compact(const uint8_t* verdict, const uint64_t* kept, c
     N.fp0[q] = fp0[c];
     N.fp1[q] = fp1[c];
     src_index[q] = (uint64_t)c;
-    visited_insert(tb, fp0[c], fp1[c], q, err);
+    if (insert_visited) visited_insert(tb, fp0[c], fp1[c], q, err);
   }
 }
 
@@ -1083,13 +1175,15 @@ __global__ void k_rehash(const Slot* old_tab, uint64_t old_cap, Slot* new_tab, u
 }
 
 // order-sensitive run digest
-__global__ void k_digest(NextArrays N, int64_t K, uint64_t level, unsigned long long* digest) {
+__global__ void k_digest(NextArrays N, int64_t K, uint64_t level, int64_t q_offset, int64_t parent_offset,
+                         unsigned long long* digest) {
   unsigned long long acc = 0;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < K; q += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t z = fmix64((level << 40) ^ (uint64_t)q);
+    uint64_t z = fmix64((level << 40) ^ (uint64_t)(q + q_offset));
     z = fmix64(z ^ N.fp0[q]);
     z = fmix64(z ^ N.fp1[q]);
-    z = fmix64(z ^ (uint64_t)(N.parent[q] + 1));
+    const int64_t par = N.parent[q];
+    z = fmix64(z ^ (uint64_t)(par < 0 ? 0 : par + parent_offset + 1));
     z = fmix64(z ^ N.t[q]);
     acc += z;
   }
@@ -1279,8 +1373,8 @@ void launch_keep(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tabl
 }
 
 void launch_compact(const ChildArrays& C, const uint64_t* off, uint64_t T, const NextArrays& N, const Tables& tb,
-                    uint64_t level_ref, int32_t* err, cudaStream_t st) {
-  k_compact<<<grid_for(T), BLK, 0, st>>>(C, off, T, N, tb, level_ref, err);
+                    uint64_t level_ref, int insert_visited, int32_t* err, cudaStream_t st) {
+  k_compact<<<grid_for(T), BLK, 0, st>>>(C, off, T, N, tb, level_ref, insert_visited, err);
   count_launch();
 }
 
@@ -1354,8 +1448,9 @@ void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const Ex
 
 void launch_level0_compact(const uint8_t* verdict, const uint64_t* kept, const uint64_t* kpos, int64_t F0,
                            const uint64_t* fp0, const uint64_t* fp1, const NextArrays& N, uint64_t* src_index,
-                           const Tables& tb, int32_t* err, cudaStream_t st) {
-  k_level0_compact<<<grid_for(F0), BLK, 0, st>>>(verdict, kept, kpos, F0, fp0, fp1, N, src_index, tb, err);
+                           const Tables& tb, int insert_visited, int32_t* err, cudaStream_t st) {
+  k_level0_compact<<<grid_for(F0), BLK, 0, st>>>(verdict, kept, kpos, F0, fp0, fp1, N, src_index, tb, insert_visited,
+                                                  err);
   count_launch();
 }
 
@@ -1388,11 +1483,56 @@ void launch_rehash(const Slot* old_tab, uint64_t old_cap, Slot* new_tab, uint64_
   count_launch();
 }
 
-void launch_digest(const NextArrays& N, int64_t K, uint64_t level, unsigned long long* digest, cudaStream_t st) {
+void launch_digest(const NextArrays& N, int64_t K, uint64_t level, int64_t q_offset, int64_t parent_offset,
+                   unsigned long long* digest, cudaStream_t st) {
   if (K <= 0) return;
   unsigned g = grid_for(K);
   if (g > 148u * 8u) g = 148u * 8u;
-  k_digest<<<g, BLK, 0, st>>>(N, K, level, digest);
+  k_digest<<<g, BLK, 0, st>>>(N, K, level, q_offset, parent_offset, digest);
+  count_launch();
+}
+
+void launch_owner_hist(const uint64_t* fp1, uint64_t T, uint32_t P, unsigned long long* counts, cudaStream_t st) {
+  if (!T) return;
+  unsigned g = grid_for(T);
+  if (g > 148u * 16u) g = 148u * 16u;
+  k_owner_hist<<<g, BLK, 0, st>>>(fp1, T, P, counts);
+  count_launch();
+}
+
+void launch_owner_pack(const uint64_t* fp0, const uint64_t* fp1, uint64_t T, uint32_t P, uint64_t tag_base,
+                       unsigned long long* cursor, uint64_t* perm, uint64_t* send, cudaStream_t st) {
+  if (!T) return;
+  k_owner_pack<<<grid_for(T), BLK, 0, st>>>(fp0, fp1, T, P, tag_base, cursor, perm, send);
+  count_launch();
+}
+
+void launch_owner_dedup(const uint64_t* recv, uint64_t R, const Tables& tb, uint8_t* verdict, uint64_t* slot,
+                        int32_t* err, cudaStream_t st) {
+  if (!R) return;
+  k_owner_dedup<<<grid_for(R), BLK, 0, st>>>(recv, R, tb, verdict, slot, err);
+  count_launch();
+}
+
+void launch_owner_winners(const uint64_t* recv, uint64_t R, const Tables& tb, const uint8_t* verdict,
+                          const uint64_t* slot, unsigned long long* n_new, cudaStream_t st) {
+  if (!R) return;
+  unsigned g = grid_for(R);
+  if (g > 148u * 16u) g = 148u * 16u;
+  k_owner_winners<<<g, BLK, 0, st>>>(recv, R, tb, verdict, slot, n_new);
+  count_launch();
+}
+
+void launch_owner_keep(const uint64_t* recv, uint64_t R, const Tables& tb, const uint8_t* verdict,
+                       const uint64_t* slot, uint64_t tau, int thin, uint8_t* out, unsigned long long* n_kept,
+                       int32_t* err, cudaStream_t st) {
+  if (!R) return;
+  k_owner_keep<<<grid_for(R), BLK, 0, st>>>(recv, R, tb, verdict, slot, tau, thin, out, n_kept, err);
+  count_launch();
+}
+
+void launch_unperm(const uint64_t* perm, const uint8_t* back, uint64_t T, uint64_t* kept, cudaStream_t st) {
+  k_unperm<<<grid_for(T + 1), BLK, 0, st>>>(perm, back, T, kept);
   count_launch();
 }
 

@@ -38,7 +38,8 @@ EXPORTED = [
     "snp_tree_num_levels", "snp_tree_num_configs", "snp_tree_level_offsets", "snp_tree_configs",
     "snp_tree_edges", "snp_tree_counters", "snp_tree_spiking_vectors", "snp_tree_free",
     "snp_level_size", "snp_level_edges", "snp_level_columns", "snp_set_profiling", "snp_profile",
-    "snp_kernel_launches",
+    "snp_kernel_launches", "snp_dist_begin", "snp_dist_expand", "snp_dist_pack", "snp_dist_owner_dedup",
+    "snp_dist_owner_keep", "snp_dist_finalize", "snp_dist_commit",
 ]
 SNP_NUM_PHASES = 5
 PHASES = ["expand", "keys", "dedup", "materialize", "verify"]
@@ -125,6 +126,14 @@ def lib() -> ctypes.CDLL:
         L.snp_set_profiling.argtypes = [_P, ctypes.c_int32]
         L.snp_profile.argtypes = [_P, _P]
         L.snp_kernel_launches.restype = ctypes.c_int64
+        _I64P = ctypes.POINTER(ctypes.c_int64)
+        L.snp_dist_begin.argtypes = [_P, ctypes.POINTER(snp_configs), ctypes.c_int32, _I64P]
+        L.snp_dist_expand.argtypes = [_P, _I64P]
+        L.snp_dist_pack.argtypes = [_P, ctypes.c_uint64, _P, _P]
+        L.snp_dist_owner_dedup.argtypes = [_P, _P, ctypes.c_int64, _I64P]
+        L.snp_dist_owner_keep.argtypes = [_P, ctypes.c_int64, _P]
+        L.snp_dist_finalize.argtypes = [_P, _P, _I64P]
+        L.snp_dist_commit.argtypes = [_P, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(snp_level_counters)]
         for f in EXPORTED:
             if f not in ("snp_kernel_launches", "snp_system_free", "snp_tree_free", "snp_frontier_size", "snp_depth", "snp_level_size",
                          "snp_tree_num_levels", "snp_tree_num_configs", "snp_abi_version", "snp_last_error"):
