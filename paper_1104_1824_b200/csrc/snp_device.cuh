@@ -111,6 +111,7 @@ struct SysView {
   const uint8_t* tab;        // m × tabw   (compact)
   const uint8_t* tab_full;   // m × 256    (count_bits == 8)
   const void* ctab;          // m × tabw   consumption of the first rule, storage type
+  int32_t ablate;            // diagnostics only (SNP_ABLATE): skip K-c sections
 };
 
 // 128-bit hash slot. key (k0,k1) = 128-bit fingerprint; EMPTY/EMPTY = free.

@@ -594,6 +594,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.tab = s->d_tab.as<uint8_t>();
   v.tab_full = s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr;
   v.ctab = s->d_ctab.p;
+  v.ablate = getenv("SNP_ABLATE") ? atoi(getenv("SNP_ABLATE")) : 0;
   v.m = (int32_t)m;
   v.n = n;
   v.binary_emit = s->binary_emit ? 1 : 0;

@@ -868,7 +868,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   T* out = reinterpret_cast<T*>(N.data);
   uint8_t* xsb = sX + (size_t)(warp * 32 + lane) * xs_stride<T>();
   T* xs = reinterpret_cast<T*>(xsb);
-  uint8_t* crow_t = sC + (size_t)warp * 32 * CROW + lane * 4;  // transposed: [word][lane]
+  uint8_t* crow_t = sC + (size_t)warp * 32 * CROW + lane;  // interleaved: [byte][lane]
   const int crow_bytes = S.tabw * (int)sizeof(T);
   const bool crow_staged = crow_bytes <= CROW;
   const T* ctab = reinterpret_cast<const T*>(S.ctab);
@@ -889,7 +889,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       const int64_t g = jbase >> 5;
       const int64_t r0 = __ldg(S.in_pad_off + g), r1 = __ldg(S.in_pad_off + g + 1);
       const int32_t* col = S.in_pad + r0 * 32 + lane;
-      const int ne = (int)(r1 - r0);
+      const int ne = (S.ablate & 1) ? 0 : (int)(r1 - r0);
       for (int e0 = 0; e0 < ne; e0 += 8) {
         int32_t src[8];
 #pragma unroll
@@ -911,17 +911,20 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
     const T* row = data + eidx(pb0, j, m);
     const bool generic = mt.flags & NM_GENERIC;
     uint64_t ovf_bits = 0;
-    if (sizeof(T) == 1 && !generic && crow_staged && mt.pm >= 0) {
+    if (S.ablate & 2) {
+      for (int r = 0; r < PB; r += 4) reinterpret_cast<uint32_t*>(xsb)[r >> 2] = (uint32_t)c[0];
+    } else if (sizeof(T) == 1 && !generic && crow_staged && mt.pm >= 0) {
       // fast path: consumption table row staged in this lane's shared slice,
       // branch-free power-of-two fold, SWAR over 4 parents per 32-bit word
       {
-        // word w of this lane's table row lives at column (w, lane): every
-        // lookup of a lane hits its own bank
+        // byte idx of this lane's table row lives at [idx][lane]: one multiply-
+        // add per lookup, lanes of a quad share a word
         const uint4* g = reinterpret_cast<const uint4*>(crow_g);
-        uint32_t* d = reinterpret_cast<uint32_t*>(crow_t);
         for (int i = 0; i < crow_bytes / 16; ++i) {
           const uint4 x = __ldg(g + i);
-          d[(4 * i) * 32] = x.x; d[(4 * i + 1) * 32] = x.y; d[(4 * i + 2) * 32] = x.z; d[(4 * i + 3) * 32] = x.w;
+          const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int b = 0; b < 16; ++b) crow_t[(16 * i + b) * 32] = (uint8_t)(w4[b >> 2] >> (8 * (b & 3)));
         }
       }
       const int32_t Lj = mt.L;
@@ -940,7 +943,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
           for (int i = 0; i < 4; ++i) {
             const int32_t v = (int32_t)((v4 >> (8 * i)) & 0xFFu);
             const uint32_t idx = (uint32_t)min(v, Lj) + ((uint32_t)max(v - Lj, 0) & pm);
-            c4 |= (uint32_t)crow_t[((idx & ~3u) << 5) | (idx & 3u)] << (8 * i);
+            c4 |= (uint32_t)crow_t[idx * 32] << (8 * i);
           }
           const uint32_t t4 = v4 - c4;  // no borrow: c_first <= v per byte
           const uint32_t k4 = count_quad<NPL>(c, r0);
@@ -981,7 +984,8 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       if (slot < ovf_cap) ovf[slot] = ((uint64_t)(uint32_t)j << 32) | (uint64_t)(pb0 + r);
     }
     // ---- write x to every kept child of the block's parents (row j of the output)
-    if (nq <= QCAP) {
+    if (S.ablate & 4) {
+    } else if (nq <= QCAP) {
       uint64_t q = Q0;
       while (q < Q1) {
         const uint64_t qe = min(Q1, (q | (PB - 1)) + 1);  // end of this output block
