@@ -104,14 +104,14 @@ struct SysView {
   const uint64_t* R1;
   // outcome tables (valid when tables_ok)
   int32_t tables_ok;         // every neuron is tabulated or flagged generic
-  int32_t tabw;              // compact table width (multiple of 16)
+  int32_t tabw;              // compact table width (power of two >= every L + P)
   int32_t full8;             // count_bits == 8: tab_full has 256 entries per neuron
   int32_t max_indeg;
   const NeuronMeta* meta;    // m
   const uint8_t* tab;        // m × tabw   (compact)
   const uint8_t* tab_full;   // m × 256    (count_bits == 8)
   const void* ctab;          // m × tabw   consumption of the first rule, storage type
-  int32_t ablate;            // diagnostics only (SNP_ABLATE): skip K-c sections
+  const uint8_t* ttab;       // m × 32     (count_bits == 8) v - c_first(v) for v < 32
 };
 
 // 128-bit hash slot. key (k0,k1) = 128-bit fingerprint; EMPTY/EMPTY = free.

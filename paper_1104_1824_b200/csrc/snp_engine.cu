@@ -189,7 +189,7 @@ struct snp_system {
   uint64_t vis_cap = 0, ltab_cap = 0, child_cap = 0;
   // scratch
   DBuf psi, off, fpb0, fpb1, ndc, nd, ebits;
-  DBuf d_meta, d_tab, d_tab_full, d_ctab;
+  DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab;
   DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   std::vector<DBuf> spare;  // released level buffers kept for reuse
@@ -578,13 +578,20 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     else tabw = std::max<int64_t>(tabw, L + P);
     meta[j] = mt;
   }
-  tabw = (tabw + 15) / 16 * 16;
+  // power of two >= every L + P: a count v < tabw indexes its own entry
+  // (every slot holds the outcome at v = slot), larger counts fold
+  {
+    int64_t w = 16;
+    while (w < tabw) w <<= 1;
+    tabw = w;
+  }
   int32_t max_indeg = 0;
   for (int64_t j = 0; j < m; ++j) max_indeg = std::max(max_indeg, in_off[j + 1] - in_off[j]);
   SNP_TRY(upload(s, s->d_meta, meta));
   SNP_TRY(s->d_tab.ensure((size_t)m * tabw, false));
   SNP_TRY(s->d_ctab.ensure((size_t)m * tabw * s->bytes, false));
   if (s->bytes == 1) SNP_TRY(s->d_tab_full.ensure((size_t)m * 256, false));
+  if (s->bytes == 1) SNP_TRY(s->d_ttab.ensure((size_t)m * 32, false));
   SysView& v = s->view;
   v.tables_ok = 1;
   v.tabw = (int32_t)tabw;
@@ -594,7 +601,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.tab = s->d_tab.as<uint8_t>();
   v.tab_full = s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr;
   v.ctab = s->d_ctab.p;
-  v.ablate = getenv("SNP_ABLATE") ? atoi(getenv("SNP_ABLATE")) : 0;
+  v.ttab = s->bytes == 1 ? s->d_ttab.as<uint8_t>() : nullptr;
   v.m = (int32_t)m;
   v.n = n;
   v.binary_emit = s->binary_emit ? 1 : 0;
@@ -615,7 +622,8 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   s->own_stream = true;
   launch_build_tables(v, s->bytes, s->d_tab.as<uint8_t>(), s->d_ctab.p,
-                      s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr, s->stream);
+                      s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr,
+                      s->bytes == 1 ? s->d_ttab.as<uint8_t>() : nullptr, s->stream);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   CUDA_TRY(cudaEventCreate(&s->ev0));

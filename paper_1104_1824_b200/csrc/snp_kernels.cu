@@ -803,19 +803,49 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 // ---------------------------------------------------------------------------
 constexpr int MW = 16;       // warps per K-c CTA
 constexpr int QCAP = 4092;   // outputs per block resolved through the r(q) table (+4 alignment slack)
-constexpr int CROW = 64;     // staged consumption-table bytes per lane
 
 template <typename T>
 __host__ __device__ constexpr int xs_stride() { return PB * (int)sizeof(T) + 4; }
 
-__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
 
+// t[v] for the four byte counts v < 32 of v4, t = 32 bytes in tt[0..7]:
+// bits 0-2 of each count select a byte inside a register pair (one PRMT per
+// pair), bits 3 and 4 choose between the pairs (sign-replicate PRMT masks)
+__device__ __forceinline__ uint32_t lut32(uint32_t v4, const uint32_t (&tt)[8]) {
+  const uint32_t x = v4 & 0x07070707u;
+  const uint32_t sel = prmt(x | (x >> 4), 0u, 0x4420u);
+  const uint32_t m3 = prmt(v4 << 4, 0u, 0xBA98u);  // 0xFF in bytes whose bit 3 is set
+  const uint32_t m4 = prmt(v4 << 3, 0u, 0xBA98u);  // ... bit 4
+  const uint32_t a = prmt(tt[0], tt[1], sel), b = prmt(tt[2], tt[3], sel);
+  const uint32_t c = prmt(tt[4], tt[5], sel), d = prmt(tt[6], tt[7], sel);
+  const uint32_t lo = (a & ~m3) | (b & m3), hi = (c & ~m3) | (d & m3);
+  return (lo & ~m4) | (hi & m4);
+}
+
+// Counts of parents 8k .. 8k+7 as bytes (lo: 8k..8k+3, hi: 8k+4..8k+7) from
+// the bit planes: byte k of every plane gathered into one 64-bit word (plane
+// b in byte b), then an 8x8 bit-matrix transpose (three delta swaps).
 template <int NPL>
-__device__ __forceinline__ uint32_t count_quad(const uint64_t (&c)[NPL], int r0) {
-  uint32_t acc = 0;
+__device__ __forceinline__ void counts8(const uint64_t (&c)[NPL], int k, uint32_t& lo, uint32_t& hi) {
+  uint32_t p[8];
 #pragma unroll
-  for (int b = 0; b < NPL; ++b) acc |= spread4((uint32_t)(c[b] >> r0) & 0xFu) << b;
-  return acc;
+  for (int b = 0; b < 8; ++b) p[b] = b < NPL ? (uint32_t)(c[b < NPL ? b : 0] >> (32 * (k >> 2))) : 0u;
+  const uint32_t s2 = (uint32_t)(k & 3) | ((uint32_t)(4 + (k & 3)) << 4);
+  lo = prmt(prmt(p[0], p[1], s2), prmt(p[2], p[3], s2), 0x5410u);
+  if (NPL <= 4) hi = 0;
+  else if (NPL == 5) hi = prmt(p[4], 0u, (uint32_t)(k & 3) | 0x4440u);
+  else hi = prmt(prmt(p[4], p[5], s2), prmt(p[6], p[7], s2), 0x5410u);
+  uint32_t t;
+  t = (lo ^ (lo >> 7)) & 0x00AA00AAu; lo ^= t ^ (t << 7);
+  t = (hi ^ (hi >> 7)) & 0x00AA00AAu; hi ^= t ^ (t << 7);
+  t = (lo ^ (lo >> 14)) & 0x0000CCCCu; lo ^= t ^ (t << 14);
+  t = (hi ^ (hi >> 14)) & 0x0000CCCCu; hi ^= t ^ (t << 14);
+  t = (lo ^ (hi << 4)) & 0xF0F0F0F0u; lo ^= t; hi ^= t >> 4;
 }
 
 template <typename T, int NPL>
@@ -827,8 +857,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   const int64_t mE = (m + 1) & ~1;
   uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words + 2 zero words
   uint8_t* sX = smem + (mE + 2) * 8;                                    // MW×32×xs_stride
-  uint8_t* sC = sX + (size_t)MW * 32 * xs_stride<T>();                  // MW×32×(CROW+4)
-  uint8_t* sR = sC + (size_t)MW * 32 * CROW;                            // QCAP
+  uint8_t* sR = sX + (size_t)MW * 32 * xs_stride<T>();                  // QCAP
   uint64_t* sQ = reinterpret_cast<uint64_t*>(sR + QCAP + 4);            // 65 (+1 pad)
   uint64_t* bar = sQ + 66;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -868,9 +897,6 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   T* out = reinterpret_cast<T*>(N.data);
   uint8_t* xsb = sX + (size_t)(warp * 32 + lane) * xs_stride<T>();
   T* xs = reinterpret_cast<T*>(xsb);
-  uint8_t* crow_t = sC + (size_t)warp * 32 * CROW + lane;  // interleaved: [byte][lane]
-  const int crow_bytes = S.tabw * (int)sizeof(T);
-  const bool crow_staged = crow_bytes <= CROW;
   const T* ctab = reinterpret_cast<const T*>(S.ctab);
   const int j_iters = (m + MW * 32 - 1) / (MW * 32);
   for (int it = 0; it < j_iters; ++it) {
@@ -889,7 +915,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       const int64_t g = jbase >> 5;
       const int64_t r0 = __ldg(S.in_pad_off + g), r1 = __ldg(S.in_pad_off + g + 1);
       const int32_t* col = S.in_pad + r0 * 32 + lane;
-      const int ne = (S.ablate & 1) ? 0 : (int)(r1 - r0);
+      const int ne = (int)(r1 - r0);
       for (int e0 = 0; e0 < ne; e0 += 8) {
         int32_t src[8];
 #pragma unroll
@@ -911,50 +937,54 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
     const T* row = data + eidx(pb0, j, m);
     const bool generic = mt.flags & NM_GENERIC;
     uint64_t ovf_bits = 0;
-    if (S.ablate & 2) {
-      for (int r = 0; r < PB; r += 4) reinterpret_cast<uint32_t*>(xsb)[r >> 2] = (uint32_t)c[0];
-    } else if (sizeof(T) == 1 && !generic && crow_staged && mt.pm >= 0) {
-      // fast path: consumption table row staged in this lane's shared slice,
-      // branch-free power-of-two fold, SWAR over 4 parents per 32-bit word
+    if (sizeof(T) == 1 && !generic) {
+      // fast path (u8): the post-consumption table t(v) = v - c_first(v) for
+      // v < 32 lives in 8 registers and is looked up 4 parents at a time by
+      // byte permutes; the bit-sliced counts become bytes by an 8x8 bit
+      // transpose per 8 parents; x = t + count is one 32-bit add per 4 parents
+      uint32_t tt[8];
       {
-        // byte idx of this lane's table row lives at [idx][lane]: one multiply-
-        // add per lookup, lanes of a quad share a word
-        const uint4* g = reinterpret_cast<const uint4*>(crow_g);
-        for (int i = 0; i < crow_bytes / 16; ++i) {
-          const uint4 x = __ldg(g + i);
-          const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int b = 0; b < 16; ++b) crow_t[(16 * i + b) * 32] = (uint8_t)(w4[b >> 2] >> (8 * (b & 3)));
-        }
+        const uint4* g = reinterpret_cast<const uint4*>(S.ttab + (int64_t)j * 32);
+        const uint4 a = __ldg(g), b = __ldg(g + 1);
+        tt[0] = a.x; tt[1] = a.y; tt[2] = a.z; tt[3] = a.w;
+        tt[4] = b.x; tt[5] = b.y; tt[6] = b.z; tt[7] = b.w;
       }
-      const int32_t Lj = mt.L;
-      const uint32_t pm = (uint32_t)mt.pm;
+      const uint8_t* crow8 = reinterpret_cast<const uint8_t*>(crow_g);
       const uint4* row4 = reinterpret_cast<const uint4*>(row);
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         const uint4 vv = (16 * g < np) ? __ldg(row4 + g) : make_uint4(0, 0, 0, 0);
         const uint32_t vw[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-          const int r0 = 16 * g + 4 * qd;
-          const uint32_t v4 = vw[qd];
-          uint32_t c4 = 0;
+        for (int h = 0; h < 2; ++h) {
+          uint32_t kq[2];
+          counts8<NPL>(c, 2 * g + h, kq[0], kq[1]);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int32_t v = (int32_t)((v4 >> (8 * i)) & 0xFFu);
-            const uint32_t idx = (uint32_t)min(v, Lj) + ((uint32_t)max(v - Lj, 0) & pm);
-            c4 |= (uint32_t)crow_t[idx * 32] << (8 * i);
-          }
-          const uint32_t t4 = v4 - c4;  // no borrow: c_first <= v per byte
-          const uint32_t k4 = count_quad<NPL>(c, r0);
-          const uint32_t s7 = (t4 & 0x7F7F7F7Fu) + (k4 & 0x7F7F7F7Fu);
-          const uint32_t co = ((t4 & k4) | ((t4 | k4) & s7)) & 0x80808080u;  // carry out of each byte
-          const uint32_t x4 = s7 ^ ((t4 ^ k4) & 0x80808080u);
-          reinterpret_cast<uint32_t*>(xsb)[r0 >> 2] = x4;
-          if (co) {
+          for (int e = 0; e < 2; ++e) {
+            const int r0 = 16 * g + 8 * h + 4 * e;
+            const uint32_t v4 = vw[2 * h + e];
+            uint32_t t4;
+            if ((v4 & 0xE0E0E0E0u) == 0) {
+              t4 = lut32(v4, tt);
+            } else {  // rare: a count >= 32, fold through the compact table
+              t4 = 0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if ((co >> (8 * i + 7)) & 1u) ovf_bits |= 1ULL << (r0 + i);
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t v = (v4 >> (8 * i)) & 0xFFu;
+                t4 |= (v - (uint32_t)crow8[table_index(v, mt)]) << (8 * i);
+              }
+            }
+            const uint32_t k4 = kq[e];
+            uint32_t x4 = t4 + k4;
+            if ((t4 | k4) & 0x80808080u) {  // a byte may carry: per-byte SWAR add
+              const uint32_t s7 = (t4 & 0x7F7F7F7Fu) + (k4 & 0x7F7F7F7Fu);
+              const uint32_t co = ((t4 & k4) | ((t4 | k4) & s7)) & 0x80808080u;
+              x4 = s7 ^ ((t4 ^ k4) & 0x80808080u);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if ((co >> (8 * i + 7)) & 1u) ovf_bits |= 1ULL << (r0 + i);
+            }
+            reinterpret_cast<uint32_t*>(xsb)[r0 >> 2] = x4;
           }
         }
       }
@@ -984,8 +1014,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       if (slot < ovf_cap) ovf[slot] = ((uint64_t)(uint32_t)j << 32) | (uint64_t)(pb0 + r);
     }
     // ---- write x to every kept child of the block's parents (row j of the output)
-    if (S.ablate & 4) {
-    } else if (nq <= QCAP) {
+    if (nq <= QCAP) {
       uint64_t q = Q0;
       while (q < Q1) {
         const uint64_t qe = min(Q1, (q | (PB - 1)) + 1);  // end of this output block
@@ -1221,7 +1250,7 @@ __global__ void k_spiking_vectors(SysView S, const T* pdata, const int64_t* pare
 // applicability of every rule at count v evaluated once per
 // system instead of once per (neuron, configuration).
 template <typename T>
-__global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_full) {
+__global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_full, uint8_t* ttab) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t w = S.tabw;
   const int64_t n_c = (int64_t)S.m * w;
@@ -1233,9 +1262,10 @@ __global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_fu
   const NeuronMeta mt = S.meta[s];
   uint32_t entry = 0;
   int32_t cons = 0;
-  const bool valid = !(mt.flags & NM_GENERIC) && (full || (int64_t)slot < (int64_t)mt.L + (mt.pm >= 0 ? mt.pm + 1 : -mt.pm));
+  const bool valid = !(mt.flags & NM_GENERIC);
   if (valid) {
-    // compact slot idx stands for count v = idx (idx < L + P); full slot is v itself
+    // every slot holds the outcome at count v = slot (slots >= L + P repeat the
+    // periodic part, so idx(v) of table_index lands on the same outcome)
     const int32_t v = (int32_t)slot;
     int first = -1, d = 0;
     for (int r = S.rule_off[s]; r < S.rule_off[s + 1]; ++r)
@@ -1250,6 +1280,8 @@ __global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_fu
   }
   if (full) {
     tab_full[i - n_c] = (uint8_t)entry;
+    // post-consumption value v - c_first(v) for the small counts (K-c lookup)
+    if (slot < 32) ttab[(int64_t)s * 32 + slot] = (uint8_t)(slot - (uint32_t)cons);
   } else {
     tab[i] = (uint8_t)entry;
     ctab[i] = (T)cons;
@@ -1271,11 +1303,11 @@ void dispatch_bytes(int32_t bytes, F&& f) {
 bool fast_expand_ok(const SysView& S) { return S.tables_ok != 0; }
 
 void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ctab, uint8_t* tab_full,
-                         cudaStream_t st) {
+                         uint8_t* ttab, cudaStream_t st) {
   const uint64_t n = (uint64_t)S.m * S.tabw + (tab_full ? (uint64_t)S.m * 256 : 0);
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    k_build_tables<T><<<grid_for(n), BLK, 0, st>>>(S, tab, reinterpret_cast<T*>(ctab), tab_full);
+    k_build_tables<T><<<grid_for(n), BLK, 0, st>>>(S, tab, reinterpret_cast<T*>(ctab), tab_full, ttab);
   });
   count_launch();
 }
@@ -1283,8 +1315,7 @@ void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ct
 size_t materialize_smem_bytes(const SysView& S, int32_t bytes) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
   const size_t xs = (size_t)MW * 32 * (PB * bytes + 4);
-  const size_t cs = (size_t)MW * 32 * CROW;
-  return (mE + 2) * 8 + xs + cs + (QCAP + 4) + 67 * 8 + 16;
+  return (mE + 2) * 8 + xs + (QCAP + 4) + 67 * 8 + 16;
 }
 
 bool fast_materialize_ok(const SysView& S) {
