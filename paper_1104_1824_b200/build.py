@@ -46,5 +46,10 @@ def build(force: bool = False, verbose: bool = False) -> None:
         _nvcc(LIB_GEN, ["workload_gen.cu"])
 
 
+def build_variant(out: str, defines) -> None:
+    """Tuning aid: build libsnp.so with extra -D defines to another path."""
+    _nvcc(out, SNP_SOURCES, [f"-D{d}" for d in defines])
+
+
 if __name__ == "__main__":
     build(force=True, verbose=True)

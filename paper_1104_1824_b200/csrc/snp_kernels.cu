@@ -801,7 +801,10 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 // ND digits ≠ 0 are corrected afterwards by k_patch (exact), out-of-range
 // base values by k_overflow_fix.
 // ---------------------------------------------------------------------------
-constexpr int MW = 16;       // warps per K-c CTA
+#ifndef SNP_KC_WARPS
+#define SNP_KC_WARPS 32
+#endif
+constexpr int MW = SNP_KC_WARPS;  // warps per K-c CTA
 constexpr int QCAP = 4092;   // outputs per block resolved through the r(q) table (+4 alignment slack)
 
 template <typename T>
