@@ -816,6 +816,18 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return d;
 }
 
+// 32-byte global load / store (sm_100 LDG.256 / STG.256): one full sector per lane
+__device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void stg256(void* p, const uint32_t (&r)[8]) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+               "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
 // t[v] for the four byte counts v < 32 of v4, t = 32 bytes in tt[0..7]:
 // bits 0-2 of each count select a byte inside a register pair (one PRMT per
 // pair), bits 3 and 4 choose between the pairs (sign-replicate PRMT masks)
@@ -947,24 +959,23 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       // transpose per 8 parents; x = t + count is one 32-bit add per 4 parents
       uint32_t tt[8];
       {
-        const uint4* g = reinterpret_cast<const uint4*>(S.ttab + (int64_t)j * 32);
-        const uint4 a = __ldg(g), b = __ldg(g + 1);
-        tt[0] = a.x; tt[1] = a.y; tt[2] = a.z; tt[3] = a.w;
-        tt[4] = b.x; tt[5] = b.y; tt[6] = b.z; tt[7] = b.w;
+        ldg256(S.ttab + (int64_t)j * 32, tt);
       }
       const uint8_t* crow8 = reinterpret_cast<const uint8_t*>(crow_g);
-      const uint4* row4 = reinterpret_cast<const uint4*>(row);
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const uint4 vv = (16 * g < np) ? __ldg(row4 + g) : make_uint4(0, 0, 0, 0);
-        const uint32_t vw[4] = {vv.x, vv.y, vv.z, vv.w};
+      for (int g = 0; g < 2; ++g) {
+        uint32_t vw[8];
+        if (32 * g < np) ldg256(row + 32 * g, vw);
+        else
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+          for (int i = 0; i < 8; ++i) vw[i] = 0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
           uint32_t kq[2];
-          counts8<NPL>(c, 2 * g + h, kq[0], kq[1]);
+          counts8<NPL>(c, 4 * g + h, kq[0], kq[1]);
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int r0 = 16 * g + 8 * h + 4 * e;
+            const int r0 = 32 * g + 8 * h + 4 * e;
             const uint32_t v4 = vw[2 * h + e];
             uint32_t t4;
             if ((v4 & 0xE0E0E0E0u) == 0) {
@@ -1030,9 +1041,21 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
           };
           for (; q < qe && (q & 3); ++q) orow[q & 63] = xs[sR[q - Qb]];
           for (; q + 4 <= qe && (q & 15); q += 4) *reinterpret_cast<uint32_t*>(orow + (q & 63)) = quad(q);
-          for (; q + 16 <= qe; q += 16) {  // 16 children per store: overlap the smem latencies
+          if ((q & 31) && q + 16 <= qe) {
             const uint32_t w0 = quad(q), w1 = quad(q + 4), w2 = quad(q + 8), w3 = quad(q + 12);
             *reinterpret_cast<uint4*>(orow + (q & 63)) = make_uint4(w0, w1, w2, w3);
+            q += 16;
+          }
+          for (; q + 32 <= qe; q += 32) {  // 32 children per store: one full sector
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = quad(q + 4 * i);
+            stg256(orow + (q & 63), w);
+          }
+          if (q + 16 <= qe) {
+            const uint32_t w0 = quad(q), w1 = quad(q + 4), w2 = quad(q + 8), w3 = quad(q + 12);
+            *reinterpret_cast<uint4*>(orow + (q & 63)) = make_uint4(w0, w1, w2, w3);
+            q += 16;
           }
           for (; q + 4 <= qe; q += 4) *reinterpret_cast<uint32_t*>(orow + (q & 63)) = quad(q);
         }
