@@ -149,6 +149,20 @@ struct Arena {
     return alloc(bytes, out);
   }
   void reset() { chunk = 0; used = 0; }
+  size_t capacity() const {
+    size_t c = 0;
+    for (const DBuf& b : chunks) c += b.bytes;
+    return c;
+  }
+  // one chunk covering `total` bytes beyond what the chunks already hold
+  snp_status reserve(size_t total) {
+    const size_t have = capacity();
+    if (total <= have) return SNP_OK;
+    DBuf b;
+    SNP_TRY(b.ensure(std::max<size_t>(total - have, (size_t)1 << 30), false));
+    chunks.push_back(std::move(b));
+    return SNP_OK;
+  }
 };
 
 // One level of the tree on the device.
@@ -178,6 +192,7 @@ struct snp_system {
   // ---- exploration state
   uint64_t generation = 0;
   bool begun = false;
+  bool horizon_reserved = false;  // reserve_horizon succeeded since the last begin
   std::vector<std::unique_ptr<Level>> levels;
   std::vector<snp_level_counters> counters;
   int64_t n_visited = 0;
@@ -331,6 +346,32 @@ snp_status ensure_visited(snp_system* s, uint64_t needed_entries) {
   SNP_TRY(sync(s));
   s->vis = std::move(nt);
   s->vis_cap = want;
+  return SNP_OK;
+}
+
+// Growing the visited table or the level-metadata arena mid-run costs a
+// cudaMalloc (tens of ms per GB) plus a rehash inside a level.  Reserve both
+// up front for RESERVE_LEVELS levels of Ft configurations, within what the
+// device can spare beside the per-level working set (next frontier, emit
+// words, child arrays, level table).
+constexpr int64_t RESERVE_LEVELS = 32;
+snp_status reserve_horizon(snp_system* s, int64_t Ft) {
+  if (Ft <= 0) return SNP_OK;
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  const size_t working = level_bytes(Ft, s->m, s->bytes) + (size_t)((Ft + PB - 1) / PB) * ((s->m + 1) & ~1) * 8 +
+                         (size_t)Ft * 8 * 64 + ((size_t)4 << 30);
+  if (free_b <= working) return SNP_OK;
+  size_t spare = free_b - working;
+  s->horizon_reserved = true;
+  const uint64_t entries = (uint64_t)RESERVE_LEVELS * (uint64_t)Ft;
+  const size_t vis_b = next_pow2(2 * entries) * sizeof(Slot);
+  if (vis_b <= spare && 2 * entries > s->vis_cap) {
+    SNP_TRY(ensure_visited(s, entries));
+    spare -= vis_b;
+  }
+  const size_t meta_b = (size_t)entries * 40;
+  if (meta_b <= spare) SNP_TRY(s->arena.reserve(meta_b));
   return SNP_OK;
 }
 
@@ -746,7 +787,8 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
   s->n_visited = K;
   s->levels.push_back(std::move(L));
   s->begun = true;
-  return SNP_OK;
+  s->horizon_reserved = false;
+  return reserve_horizon(s, std::max<int64_t>(K, s->opt.frontier_target));
 }
 
 snp_status classify_level(snp_system* s, Level* L) {
@@ -773,6 +815,8 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     return SNP_OK;
   }
   if (!cur->has_data()) return fail(SNP_E_STATE, "current level has no data");
+  // the caller may have released its level-0 input since snp_begin
+  if (!s->horizon_reserved) SNP_TRY(reserve_horizon(s, std::max<int64_t>(F, s->opt.frontier_target)));
   cudaStream_t st = s->stream;
   g_trace.start();
   CUDA_TRY(cudaEventRecord(s->ev0, st));

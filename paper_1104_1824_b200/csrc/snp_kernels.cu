@@ -235,6 +235,45 @@ __device__ void expand_generic_neuron(const SysView& S, const ExpandOut& O, int3
   }
 }
 
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// bit-sliced full adder: (h, l) = a + b + c per bit position
+__device__ __forceinline__ void csa(uint64_t& h, uint64_t& l, uint64_t a, uint64_t b, uint64_t c) {
+  const uint64_t u = a ^ b;
+  h = (a & b) | (u & c);
+  l = u ^ c;
+}
+
+// 32-byte global load / store (sm_100 LDG.256 / STG.256): one full sector per lane
+__device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void stg256(void* p, const uint32_t (&r)[8]) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+               "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+// t[v] for the four byte counts v < 32 of v4, t = 32 bytes in tt[0..7]:
+// bits 0-2 of each count select a byte inside a register pair (one PRMT per
+// pair), bits 3 and 4 choose between the pairs (sign-replicate PRMT masks)
+__device__ __forceinline__ uint32_t lut32(uint32_t v4, const uint32_t (&tt)[8]) {
+  const uint32_t x = v4 & 0x07070707u;
+  const uint32_t sel = prmt(x | (x >> 4), 0u, 0x4420u);
+  const uint32_t m3 = prmt(v4 << 4, 0u, 0xBA98u);  // 0xFF in bytes whose bit 3 is set
+  const uint32_t m4 = prmt(v4 << 3, 0u, 0xBA98u);  // ... bit 4
+  const uint32_t a = prmt(tt[0], tt[1], sel), b = prmt(tt[2], tt[3], sel);
+  const uint32_t c = prmt(tt[4], tt[5], sel), d = prmt(tt[6], tt[7], sel);
+  const uint32_t lo = (a & ~m3) | (b & m3), hi = (c & ~m3) | (d & m3);
+  return (lo & ~m4) | (hi & m4);
+}
+
 // 4 table entries (one byte each) → 4-bit mask of their TE_EMIT bits
 __device__ __forceinline__ uint32_t emit_nibble(uint32_t w4) {
   return ((w4 & 0x01010101u) * 0x01020408u) >> 24;
@@ -431,6 +470,72 @@ __global__ void __launch_bounds__(256, 2) k_expand_t(SysView S, LevelView L, Exp
               }
             }
             if (ep) ep[(int64_t)s * 8] = (uint8_t)eb;
+          }
+          continue;
+        }
+        if constexpr (sizeof(T) == 1 && FULL) {
+          // u8 fast path: counts stay packed 4 per word; the first 32 bytes of
+          // each neuron's outcome table sit in registers and are looked up 4
+          // counts at a time by byte permutes (a count >= 32 reads the table)
+          uint32_t ltA[8], ltB[8];
+          {
+            const uint4* ta = reinterpret_cast<const uint4*>(tab + sl * W);
+            const uint4* tb = reinterpret_cast<const uint4*>(tab + (sl + 1) * W);
+            const uint4 a0 = ta[0], a1 = ta[1], b0 = tb[0], b1 = tb[1];
+            ltA[0] = a0.x; ltA[1] = a0.y; ltA[2] = a0.z; ltA[3] = a0.w;
+            ltA[4] = a1.x; ltA[5] = a1.y; ltA[6] = a1.z; ltA[7] = a1.w;
+            ltB[0] = b0.x; ltB[1] = b0.y; ltB[2] = b0.z; ltB[3] = b0.w;
+            ltB[4] = b1.x; ltB[5] = b1.y; ltB[6] = b1.z; ltB[7] = b1.w;
+          }
+          const uint2 cA = *reinterpret_cast<const uint2*>(crow + sl * G::ROWB);
+          const uint2 cB = *reinterpret_cast<const uint2*>(crow + (sl + 1) * G::ROWB);
+          auto look = [&](uint32_t v4, const uint32_t(&lt)[8], const uint8_t* trow) {
+            if ((v4 & 0xE0E0E0E0u) == 0) return lut32(v4, lt);
+            uint32_t w = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w |= (uint32_t)trow[(v4 >> (8 * i)) & 0xFFu] << (8 * i);
+            return w;
+          };
+          const uint32_t wA0 = look(cA.x, ltA, tab + sl * W), wA1 = look(cA.y, ltA, tab + sl * W);
+          const uint32_t wB0 = look(cB.x, ltB, tab + (sl + 1) * W), wB1 = look(cB.y, ltB, tab + (sl + 1) * W);
+          const uint8_t* hA = hsb + sl * 256;
+          const uint8_t* hB = hsb + (sl + 1) * 256;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t wa = k < 4 ? wA0 : wA1, wb = k < 4 ? wB0 : wB1;
+            const ulonglong2 dA = *reinterpret_cast<const ulonglong2*>(hA + ((wa >> (8 * (k & 3))) & TE_F));
+            const ulonglong2 dB = *reinterpret_cast<const ulonglong2*>(hB + ((wb >> (8 * (k & 3))) & TE_F));
+            a[k] += dA.x + dB.x;
+            b[k] += dA.y + dB.y;
+          }
+          any0 |= wA0 | wB0;
+          any1 |= wA1 | wB1;
+          if (ep) {
+            ep[(int64_t)(c0 + sl) * 8] = (uint8_t)(emit_nibble(wA0) | (emit_nibble(wA1) << 4));
+            ep[(int64_t)(c0 + sl + 1) * 8] = (uint8_t)(emit_nibble(wB0) | (emit_nibble(wB1) << 4));
+          }
+          if (((wA0 | wA1 | wB0 | wB1) & 0x02020202u) && !O.classify_only) {  // rare: nondeterminism
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              if (k >= nvalid) continue;
+              const int sh = 8 * (k & 3);
+              const uint32_t wa = k < 4 ? wA0 : wA1, wb = k < 4 ? wB0 : wB1;
+              const uint32_t va = ((k < 4 ? cA.x : cA.y) >> sh) & 0xFFu, vb = ((k < 4 ? cB.x : cB.y) >> sh) & 0xFFu;
+              if ((wa >> sh) & TE_ND) {
+                int nk = O.ndc[p0 + k];
+                uint64_t pk = O.psi[p0 + k];
+                nd_event(S, O, c0 + sl, va, p0 + k, nk, pk);
+                O.ndc[p0 + k] = nk;
+                O.psi[p0 + k] = pk;
+              }
+              if ((wb >> sh) & TE_ND) {
+                int nk = O.ndc[p0 + k];
+                uint64_t pk = O.psi[p0 + k];
+                nd_event(S, O, c0 + sl + 1, vb, p0 + k, nk, pk);
+                O.ndc[p0 + k] = nk;
+                O.psi[p0 + k] = pk;
+              }
+            }
           }
           continue;
         }
@@ -810,38 +915,6 @@ constexpr int QCAP = 4092;   // outputs per block resolved through the r(q) tabl
 template <typename T>
 __host__ __device__ constexpr int xs_stride() { return PB * (int)sizeof(T) + 4; }
 
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-  uint32_t d;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-  return d;
-}
-
-// 32-byte global load / store (sm_100 LDG.256 / STG.256): one full sector per lane
-__device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
-  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "l"(p));
-}
-__device__ __forceinline__ void stg256(void* p, const uint32_t (&r)[8]) {
-  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]),
-               "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-               : "memory");
-}
-
-// t[v] for the four byte counts v < 32 of v4, t = 32 bytes in tt[0..7]:
-// bits 0-2 of each count select a byte inside a register pair (one PRMT per
-// pair), bits 3 and 4 choose between the pairs (sign-replicate PRMT masks)
-__device__ __forceinline__ uint32_t lut32(uint32_t v4, const uint32_t (&tt)[8]) {
-  const uint32_t x = v4 & 0x07070707u;
-  const uint32_t sel = prmt(x | (x >> 4), 0u, 0x4420u);
-  const uint32_t m3 = prmt(v4 << 4, 0u, 0xBA98u);  // 0xFF in bytes whose bit 3 is set
-  const uint32_t m4 = prmt(v4 << 3, 0u, 0xBA98u);  // ... bit 4
-  const uint32_t a = prmt(tt[0], tt[1], sel), b = prmt(tt[2], tt[3], sel);
-  const uint32_t c = prmt(tt[4], tt[5], sel), d = prmt(tt[6], tt[7], sel);
-  const uint32_t lo = (a & ~m3) | (b & m3), hi = (c & ~m3) | (d & m3);
-  return (lo & ~m4) | (hi & m4);
-}
-
 // Counts of parents 8k .. 8k+7 as bytes (lo: 8k..8k+3, hi: 8k+4..8k+7) from
 // the bit planes: byte k of every plane gathered into one 64-bit word (plane
 // b in byte b), then an 8x8 bit-matrix transpose (three delta swaps).
@@ -873,7 +946,8 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words + 2 zero words
   uint8_t* sX = smem + (mE + 2) * 8;                                    // MW×32×xs_stride
   uint8_t* sR = sX + (size_t)MW * 32 * xs_stride<T>();                  // QCAP
-  uint64_t* sQ = reinterpret_cast<uint64_t*>(sR + QCAP + 4);            // 65 (+1 pad)
+  uint32_t* sD = reinterpret_cast<uint32_t*>(sR + QCAP + 4);            // (QCAP+4)/4 quad descriptors
+  uint64_t* sQ = reinterpret_cast<uint64_t*>(sD + (QCAP + 4) / 4);      // 65 (+1 pad)
   uint64_t* bar = sQ + 66;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t blk = blockIdx.x;
@@ -901,6 +975,30 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   if (nq <= QCAP) {
     if (tid < np)
       for (uint64_t q = sQ[tid]; q < sQ[tid + 1]; ++q) sR[q - Qb] = (uint8_t)tid;
+  }
+  __syncthreads();
+  // output quads q..q+3 (q % 4 == 0) whose parents lie in one 8-byte window
+  // of the x row: one byte permute of two words (CTA-uniform descriptor:
+  // word in bits 16-19, selector in bits 0-15; bit 31 = use the byte path)
+  if (nq <= QCAP) {
+    const uint64_t nquad = (Q1 - Qb + 3) >> 2;
+    for (uint64_t i = tid; i < nquad; i += blockDim.x) {
+      const uint64_t q = Qb + 4 * i;
+      uint32_t d = 0x80000000u;
+      if (q >= Q0 && q + 3 < Q1) {
+        const uint32_t a = sR[q - Qb] >> 2;
+        uint32_t sel = 0;
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t o = (uint32_t)sR[q + k - Qb] - 4 * a;
+          ok &= o < 8;
+          sel |= (o & 7) << (4 * k);
+        }
+        if (ok) d = (a << 16) | sel;
+      }
+      sD[i] = d;
+    }
   }
   // parents with kept children (bit r), for the overflow bookkeeping
   uint64_t haskids = 0;
@@ -935,15 +1033,26 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         int32_t src[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) src[u] = (e0 + u < ne) ? __ldg(col + (e0 + u) * 32) : (int32_t)mE;  // batch the loads
+        uint64_t x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          uint64_t carry = sE[src[u]];
+        for (int u = 0; u < 8; ++u) x[u] = sE[src[u]];
+        // Harley-Seal carry-save tree: 8 words into the planes with 7 full
+        // adders; the carry out of plane 3 ripples into the upper planes
+        uint64_t twosA, twosB, foursA, foursB, eightsA;
+        csa(twosA, c[0], c[0], x[0], x[1]);
+        csa(twosB, c[0], c[0], x[2], x[3]);
+        csa(foursA, c[1], c[1], twosA, twosB);
+        csa(twosA, c[0], c[0], x[4], x[5]);
+        csa(twosB, c[0], c[0], x[6], x[7]);
+        csa(foursB, c[1], c[1], twosA, twosB);
+        csa(eightsA, c[2], c[2], foursA, foursB);
+        uint64_t carry = c[3] & eightsA;
+        c[3] ^= eightsA;
 #pragma unroll
-          for (int b = 0; b < NPL; ++b) {
-            const uint64_t t = c[b] & carry;
-            c[b] ^= carry;
-            carry = t;
-          }
+        for (int b = 4; b < NPL; ++b) {
+          const uint64_t t = c[b] & carry;
+          c[b] ^= carry;
+          carry = t;
         }
       }
     }
@@ -1035,6 +1144,11 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         T* orow = out + (((int64_t)(q >> 6) * m + j) << 6);
         if (sizeof(T) == 1) {
           auto quad = [&](uint64_t qq) {
+            const uint32_t d = sD[(qq - Qb) >> 2];
+            if (!(d & 0x80000000u)) {
+              const uint32_t* xw = reinterpret_cast<const uint32_t*>(xsb) + (d >> 16);
+              return prmt(xw[0], xw[1], d & 0xFFFFu);
+            }
             const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (qq - Qb));  // 4 parent indices
             return (uint32_t)xsb[rr & 0xFF] | ((uint32_t)xsb[(rr >> 8) & 0xFF] << 8) |
                    ((uint32_t)xsb[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xsb[rr >> 24] << 24);
@@ -1341,7 +1455,7 @@ void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ct
 size_t materialize_smem_bytes(const SysView& S, int32_t bytes) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
   const size_t xs = (size_t)MW * 32 * (PB * bytes + 4);
-  return (mE + 2) * 8 + xs + (QCAP + 4) + 67 * 8 + 16;
+  return (mE + 2) * 8 + xs + 2 * (QCAP + 4) + 67 * 8 + 16;
 }
 
 bool fast_materialize_ok(const SysView& S) {
