@@ -75,6 +75,8 @@ enum : int32_t { NM_GENERIC = 1, NM_ND = 2 };
 // rule + 1 (0 = none) — pre-shifted so (entry & 0xF0) is the byte offset of
 // that rule's 16-B fingerprint delta in a neuron's 256-B slice.
 enum : uint32_t { TE_EMIT = 1u, TE_ND = 2u, TE_F = 0xF0u };
+// kernel selection flags (SysView::kernel_flags)
+enum : int32_t { KF_EXPAND_T = 1 };
 
 __device__ __forceinline__ uint32_t table_index(uint32_t v, const NeuronMeta& mt) {
   if ((int32_t)v < mt.L) return v;
@@ -112,6 +114,10 @@ struct SysView {
   const uint8_t* tab_full;   // m × 256    (count_bits == 8)
   const void* ctab;          // m × tabw   consumption of the first rule, storage type
   const uint8_t* ttab;       // m × 32     (count_bits == 8) v - c_first(v) for v < 32
+  const uint8_t* elut;       // m × 32     (count_bits == 8) outcome entries for v < 32
+  const uint8_t* hsg;        // m × 256    (count_bits == 8) 16-B fingerprint delta per first-rule slot
+  int32_t any_generic;       // some neuron has no table
+  int32_t kernel_flags;      // KF_* (SNP_KERNELS environment variable at snp_load; tuning/tests)
 };
 
 // 128-bit hash slot. key (k0,k1) = 128-bit fingerprint; EMPTY/EMPTY = free.

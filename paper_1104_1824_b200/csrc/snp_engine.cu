@@ -204,7 +204,7 @@ struct snp_system {
   uint64_t vis_cap = 0, ltab_cap = 0, child_cap = 0;
   // scratch
   DBuf psi, off, fpb0, fpb1, ndc, nd, ebits;
-  DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab;
+  DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab, d_elut, d_hsg;
   DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   std::vector<DBuf> spare;  // released level buffers kept for reuse
@@ -354,7 +354,9 @@ snp_status ensure_visited(snp_system* s, uint64_t needed_entries) {
 // up front for RESERVE_LEVELS levels of Ft configurations, within what the
 // device can spare beside the per-level working set (next frontier, emit
 // words, child arrays, level table).
+snp_status ensure_children(snp_system* s, uint64_t T);
 constexpr int64_t RESERVE_LEVELS = 32;
+constexpr int64_t RESERVE_CHILDREN = 8;
 snp_status reserve_horizon(snp_system* s, int64_t Ft) {
   if (Ft <= 0) return SNP_OK;
   size_t free_b = 0, total_b = 0;
@@ -371,7 +373,21 @@ snp_status reserve_horizon(snp_system* s, int64_t Ft) {
     spare -= vis_b;
   }
   const size_t meta_b = (size_t)entries * 40;
-  if (meta_b <= spare) SNP_TRY(s->arena.reserve(meta_b));
+  if (meta_b <= spare) {
+    SNP_TRY(s->arena.reserve(meta_b));
+    spare -= meta_b;
+  }
+  // children per level: up to RESERVE_CHILDREN × Ft before the arrays grow
+  const uint64_t T = (uint64_t)RESERVE_CHILDREN * (uint64_t)Ft;
+  const size_t child_b = (size_t)T * 2 * 60 + next_pow2(2 * T) * sizeof(Slot);
+  if (child_b <= spare) {
+    if (T > s->child_cap) SNP_TRY(ensure_children(s, T / 2));
+    const uint64_t lw = next_pow2(std::max<uint64_t>(1024, 2 * T));
+    if (lw > s->ltab_cap) {
+      SNP_TRY(s->ltab.ensure(lw * sizeof(Slot), false));
+      s->ltab_cap = lw;
+    }
+  }
   return SNP_OK;
 }
 
@@ -633,6 +649,8 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   SNP_TRY(s->d_ctab.ensure((size_t)m * tabw * s->bytes, false));
   if (s->bytes == 1) SNP_TRY(s->d_tab_full.ensure((size_t)m * 256, false));
   if (s->bytes == 1) SNP_TRY(s->d_ttab.ensure((size_t)m * 32, false));
+  if (s->bytes == 1) SNP_TRY(s->d_elut.ensure((size_t)m * 32, false));
+  if (s->bytes == 1) SNP_TRY(s->d_hsg.ensure((size_t)m * 256, false));
   SysView& v = s->view;
   v.tables_ok = 1;
   v.tabw = (int32_t)tabw;
@@ -643,6 +661,15 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.tab_full = s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr;
   v.ctab = s->d_ctab.p;
   v.ttab = s->bytes == 1 ? s->d_ttab.as<uint8_t>() : nullptr;
+  v.elut = s->bytes == 1 ? s->d_elut.as<uint8_t>() : nullptr;
+  v.hsg = s->bytes == 1 ? s->d_hsg.as<uint8_t>() : nullptr;
+  v.any_generic = 0;
+  for (int64_t j = 0; j < m; ++j) v.any_generic |= (meta[j].flags & NM_GENERIC) ? 1 : 0;
+  {
+    // SNP_KERNELS=expand_t: the 8-configuration-per-lane K-a for uint8 too
+    const char* k = getenv("SNP_KERNELS");
+    v.kernel_flags = (k && strstr(k, "expand_t")) ? KF_EXPAND_T : 0;
+  }
   v.m = (int32_t)m;
   v.n = n;
   v.binary_emit = s->binary_emit ? 1 : 0;
@@ -664,7 +691,9 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   s->own_stream = true;
   launch_build_tables(v, s->bytes, s->d_tab.as<uint8_t>(), s->d_ctab.p,
                       s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr,
-                      s->bytes == 1 ? s->d_ttab.as<uint8_t>() : nullptr, s->stream);
+                      s->bytes == 1 ? s->d_ttab.as<uint8_t>() : nullptr,
+                      s->bytes == 1 ? s->d_elut.as<uint8_t>() : nullptr,
+                      s->bytes == 1 ? s->d_hsg.as<uint8_t>() : nullptr, s->stream);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   CUDA_TRY(cudaEventCreate(&s->ev0));

@@ -69,7 +69,7 @@ size_t materialize_smem_bytes(const SysView& S, int32_t bytes);
 
 // ---- launchers (all asynchronous on `st`) ----------------------------------
 void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ctab, uint8_t* tab_full,
-                         uint8_t* ttab, cudaStream_t st);
+                         uint8_t* ttab, uint8_t* elut, uint8_t* hsg, cudaStream_t st);
 void launch_import(const void* src, int32_t src_bytes, int32_t src_layout, int64_t src_ld, int64_t F, int32_t m,
                    void* dst, int32_t dst_bytes, int64_t count_max, int32_t* err, cudaStream_t st);
 void launch_export(const void* src, int32_t bytes, int64_t F, int32_t m, int32_t* dst_rowmajor, cudaStream_t st);

@@ -609,6 +609,178 @@ __global__ void __launch_bounds__(256, 2) k_expand_t(SysView S, LevelView L, Exp
   if (nh) atomicAdd(O.n_halting, (unsigned long long)nh);
 }
 
+// K-a for uint8 counts with every neuron tabulated (the common case): 4
+// configurations per lane so that 64 registers suffice and 32 warps share an
+// SM.  A CTA owns QB = 16 storage blocks (warp w: blocks 2w, 2w+1; lane l:
+// configurations 4(l % 16) .. +3 of its block).  Per chunk of QNC neurons one
+// thread issues TMA bulk copies of the 16 count slices, the chunk's
+// fingerprint-delta rows (hsg) and outcome-table heads (elut) into a
+// double-buffered stage.  Per (neuron, lane): one 32-bit count word, one
+// byte-permute table lookup for its 4 counts, one 16-B delta per firing
+// configuration; the emit nibbles of lane pairs merge into the E byte by one
+// shuffle.
+// outcome-table entries of the 4 byte counts of w: byte permutes on the 32-B
+// table head staged in shared memory, the full table for a count >= 32
+__device__ __forceinline__ uint32_t expand_entries(uint32_t w, const uint8_t* head, const uint8_t* full) {
+  if ((w & 0xE0E0E0E0u) == 0) {
+    uint32_t t[8];
+    const uint4 t0 = reinterpret_cast<const uint4*>(head)[0];
+    const uint4 t1 = reinterpret_cast<const uint4*>(head)[1];
+    t[0] = t0.x; t[1] = t0.y; t[2] = t0.z; t[3] = t0.w;
+    t[4] = t1.x; t[5] = t1.y; t[6] = t1.z; t[7] = t1.w;
+    return lut32(w, t);
+  }
+  uint32_t e = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) e |= (uint32_t)__ldg(full + ((w >> (8 * i)) & 0xFFu)) << (8 * i);
+  return e;
+}
+
+constexpr int QW = 8;                    // warps per CTA
+constexpr int QB = 2 * QW;               // storage blocks per CTA
+constexpr int QNC = 16;                  // neurons per chunk
+constexpr int QBLKS = QNC * PB + 64;     // padded block slice: the two blocks of a warp on opposite bank halves
+constexpr int QSTAGE = QB * QBLKS + QNC * 256 + QNC * 32;
+
+size_t expand_q_smem_bytes() { return 2 * (size_t)QSTAGE + 64; }
+
+__global__ void __launch_bounds__(QW * 32, 3) k_expand_q(SysView S, LevelView L, ExpandOut O) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * QSTAGE);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t blk0 = (int64_t)blockIdx.x * QB;
+  const int64_t nblk_total = (L.F + PB - 1) / PB;
+  const int nb = (nblk_total - blk0 < QB) ? (int)(nblk_total - blk0) : QB;
+  const int bl = warp * 2 + (lane >> 4);
+  const int64_t p0 = (blk0 + bl) * PB + (lane & 15) * 4;
+  const int nvalid = p0 >= L.F ? 0 : (L.F - p0 >= 4 ? 4 : (int)(L.F - p0));
+  const int m = S.m;
+  const int nchunks = (m + QNC - 1) / QNC;
+
+  uint64_t a[4], b[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool ok = k < nvalid;
+    a[k] = ok ? L.fp0[p0 + k] : 0;
+    b[k] = ok ? L.fp1[p0 + k] : 0;
+    if (ok && !O.classify_only) {
+      O.psi[p0 + k] = 1;
+      O.ndc[p0 + k] = 0;
+    }
+  }
+  // E byte of this lane pair (8 configurations), +8 per neuron; written by the even lane
+  uint8_t* ep = nullptr;
+  if (O.ebits != nullptr && !O.classify_only && nvalid > 0 && !(lane & 1))
+    ep = reinterpret_cast<uint8_t*>(O.ebits) + emit_index(p0, 0, m);
+  uint32_t any = 0;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int c) {
+    if (tid == 0) {
+      const int st = c & 1, c0 = c * QNC, rows = min(QNC, m - c0);
+      uint8_t* stg = smem + st * QSTAGE;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&bar[st], (uint32_t)(nb * rows * PB + rows * 256 + rows * 32));
+      const uint8_t* base = reinterpret_cast<const uint8_t*>(L.data);
+      for (int bb = 0; bb < nb; ++bb)
+        bulk_g2s(stg + bb * QBLKS, base + ((blk0 + bb) * (int64_t)m + c0) * PB, (uint32_t)(rows * PB), &bar[st]);
+      bulk_g2s(stg + QB * QBLKS, S.hsg + (int64_t)c0 * 256, (uint32_t)(rows * 256), &bar[st]);
+      bulk_g2s(stg + QB * QBLKS + QNC * 256, S.elut + (int64_t)c0 * 32, (uint32_t)(rows * 32), &bar[st]);
+    }
+  };
+
+  issue(0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int st = c & 1, c0 = c * QNC, rows = min(QNC, m - c0);
+    if (c + 1 < nchunks) issue(c + 1);
+    mbar_wait(&bar[st], (uint32_t)((c >> 1) & 1));
+    const uint8_t* stg = smem + st * QSTAGE;
+    const uint8_t* crow = stg + bl * QBLKS + (lane & 15) * 4;
+    const uint8_t* hs = stg + QB * QBLKS;
+    const uint8_t* lt = hs + QNC * 256;
+    // neurons in pairs: both deltas of a configuration enter its 64-bit
+    // accumulators through one 3-input add (slot 0 of a delta row is zero);
+    // an odd tail pairs the last neuron with a zero row (sl + 1 == rows)
+    for (int sl = 0; sl < rows; sl += 2) {
+      const bool pair = sl + 1 < rows;
+      const uint32_t wA = *reinterpret_cast<const uint32_t*>(crow + sl * PB);
+      const uint32_t wB = pair ? *reinterpret_cast<const uint32_t*>(crow + (sl + 1) * PB) : 0u;
+      const uint32_t eA = expand_entries(wA, lt + sl * 32, S.tab_full + (int64_t)(c0 + sl) * 256);
+      const uint32_t eB = pair ? expand_entries(wB, lt + (sl + 1) * 32, S.tab_full + (int64_t)(c0 + sl + 1) * 256) : 0u;
+      const uint8_t* hA = hs + sl * 256;
+      const uint8_t* hB = pair ? hs + (sl + 1) * 256 : hA;  // eB = 0: slot 0 of a loaded row (zero)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const ulonglong2 dA = *reinterpret_cast<const ulonglong2*>(hA + ((eA >> (8 * k)) & TE_F));
+        const ulonglong2 dB = *reinterpret_cast<const ulonglong2*>(hB + ((eB >> (8 * k)) & TE_F));
+        a[k] += dA.x + dB.x;
+        b[k] += dA.y + dB.y;
+      }
+      any |= eA | eB;
+      // emit nibbles of both neurons, merged with the partner lane's in one shuffle
+      const uint32_t nib = emit_nibble(eA) | (emit_nibble(eB) << 8);
+      const uint32_t hi = __shfl_xor_sync(0xFFFFFFFFu, nib, 1);
+      if (ep) {
+        ep[(int64_t)(c0 + sl) * 8] = (uint8_t)((nib & 0xFu) | ((hi & 0xFu) << 4));
+        if (pair) ep[(int64_t)(c0 + sl + 1) * 8] = (uint8_t)(((nib >> 8) & 0xFu) | (((hi >> 8) & 0xFu) << 4));
+      }
+      if (((eA | eB) & 0x02020202u) && !O.classify_only) {  // rare: nondeterminism
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k >= nvalid) continue;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const uint32_t e = u ? eB : eA, w = u ? wB : wA;
+            if (!((e >> (8 * k)) & TE_ND)) continue;
+            int nk = O.ndc[p0 + k];
+            uint64_t pk = O.psi[p0 + k];
+            nd_event(S, O, c0 + sl + u, (w >> (8 * k)) & 0xFFu, p0 + k, nk, pk);
+            O.ndc[p0 + k] = nk;
+            O.psi[p0 + k] = pk;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (nvalid == 0) return;
+  unsigned nh = 0;
+  bool cap = false;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k >= nvalid) continue;
+    const int64_t p = p0 + k;
+    const bool fired = ((any >> (8 * k)) & TE_F) != 0;
+    O.halting[p] = fired ? 0 : 1;
+    nh += fired ? 0 : 1;
+    if (!O.classify_only) {
+      if (!fired) O.psi[p] = 0;  // halting: no children (reading A5)
+      cap |= O.psi[p] > PSI_LIMIT || O.ndc[p] > KMAX;
+      O.fpb0[p] = a[k];
+      O.fpb1[p] = b[k];
+    }
+  }
+  if (cap) atomicOr(O.err, ERR_CAPACITY);
+  if (nh) atomicAdd(O.n_halting, (unsigned long long)nh);
+}
+
+// Fingerprint delta rows for k_expand_q: hsg[s][f] (16 B) = (h0, h1) of the
+// neuron's f-th rule (f = 1 .. min(#rules, 15)), slot 0 = zero.
+__global__ void k_build_hs(SysView S, uint8_t* hsg) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)S.m * 16) return;
+  const int32_t s = (int32_t)(i >> 4), f = (int32_t)(i & 15);
+  const int32_t r0 = S.rule_off[s], r1 = S.rule_off[s + 1];
+  ulonglong2 h = make_ulonglong2(0ULL, 0ULL);
+  if (f >= 1 && f <= r1 - r0) h = make_ulonglong2(S.h0[r0 + f - 1], S.h1[r0 + f - 1]);
+  reinterpret_cast<ulonglong2*>(hsg)[i] = h;
+}
+
 // Generic K-a (systems whose neurons cannot all be tabulated): the same walk,
 // every rule evaluated from its descriptor.
 template <typename T>
@@ -1071,44 +1243,56 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         ldg256(S.ttab + (int64_t)j * 32, tt);
       }
       const uint8_t* crow8 = reinterpret_cast<const uint8_t*>(crow_g);
-#pragma unroll
+#pragma unroll 1  // two halves of 32 parents; rolled keeps the hot loop in the instruction cache
       for (int g = 0; g < 2; ++g) {
         uint32_t vw[8];
         if (32 * g < np) ldg256(row + 32 * g, vw);
         else
 #pragma unroll
           for (int i = 0; i < 8; ++i) vw[i] = 0;
+        // t = v - c_first(v) for the 32 counts: byte permutes unless some
+        // count >= 32 (rare: that quad folds through the compact table)
+        uint32_t t[8], hiv = 0;
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          uint32_t kq[2];
-          counts8<NPL>(c, 4 * g + h, kq[0], kq[1]);
+        for (int i = 0; i < 8; ++i) hiv |= vw[i];
+        if ((hiv & 0xE0E0E0E0u) == 0) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r0 = 32 * g + 8 * h + 4 * e;
-            const uint32_t v4 = vw[2 * h + e];
-            uint32_t t4;
-            if ((v4 & 0xE0E0E0E0u) == 0) {
-              t4 = lut32(v4, tt);
-            } else {  // rare: a count >= 32, fold through the compact table
-              t4 = 0;
+          for (int i = 0; i < 8; ++i) t[i] = lut32(vw[i], tt);
+        } else {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const uint32_t v = (v4 >> (8 * i)) & 0xFFu;
-                t4 |= (v - (uint32_t)crow8[table_index(v, mt)]) << (8 * i);
+          for (int i = 0; i < 8; ++i) {
+            if ((vw[i] & 0xE0E0E0E0u) == 0) {
+              t[i] = lut32(vw[i], tt);
+            } else {
+              t[i] = 0;
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const uint32_t v = (vw[i] >> (8 * b)) & 0xFFu;
+                t[i] |= (v - (uint32_t)crow8[table_index(v, mt)]) << (8 * b);
               }
             }
-            const uint32_t k4 = kq[e];
-            uint32_t x4 = t4 + k4;
-            if ((t4 | k4) & 0x80808080u) {  // a byte may carry: per-byte SWAR add
-              const uint32_t s7 = (t4 & 0x7F7F7F7Fu) + (k4 & 0x7F7F7F7Fu);
-              const uint32_t co = ((t4 & k4) | ((t4 | k4) & s7)) & 0x80808080u;
-              x4 = s7 ^ ((t4 ^ k4) & 0x80808080u);
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if ((co >> (8 * i + 7)) & 1u) ovf_bits |= 1ULL << (r0 + i);
-            }
-            reinterpret_cast<uint32_t*>(xsb)[r0 >> 2] = x4;
           }
+        }
+        // x = t + count: plain 32-bit adds; a byte can only carry when some
+        // operand byte has its top bit set (rare: redo those quads bytewise)
+        uint32_t kq[8], chk = 0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) counts8<NPL>(c, 4 * g + h, kq[2 * h], kq[2 * h + 1]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) chk |= t[i] | kq[i];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          uint32_t x4 = t[i] + kq[i];
+          if (chk & 0x80808080u) {
+            const uint32_t t4 = t[i], k4 = kq[i];
+            const uint32_t s7 = (t4 & 0x7F7F7F7Fu) + (k4 & 0x7F7F7F7Fu);
+            const uint32_t co = ((t4 & k4) | ((t4 | k4) & s7)) & 0x80808080u;
+            x4 = s7 ^ ((t4 ^ k4) & 0x80808080u);
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if ((co >> (8 * b + 7)) & 1u) ovf_bits |= 1ULL << (32 * g + 4 * i + b);
+          }
+          reinterpret_cast<uint32_t*>(xsb)[8 * g + i] = x4;
         }
       }
     } else {
@@ -1390,7 +1574,7 @@ __global__ void k_spiking_vectors(SysView S, const T* pdata, const int64_t* pare
 // applicability of every rule at count v evaluated once per
 // system instead of once per (neuron, configuration).
 template <typename T>
-__global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_full, uint8_t* ttab) {
+__global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_full, uint8_t* ttab, uint8_t* elut) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t w = S.tabw;
   const int64_t n_c = (int64_t)S.m * w;
@@ -1422,6 +1606,7 @@ __global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_fu
     tab_full[i - n_c] = (uint8_t)entry;
     // post-consumption value v - c_first(v) for the small counts (K-c lookup)
     if (slot < 32) ttab[(int64_t)s * 32 + slot] = (uint8_t)(slot - (uint32_t)cons);
+    if (slot < 32) elut[(int64_t)s * 32 + slot] = (uint8_t)entry;
   } else {
     tab[i] = (uint8_t)entry;
     ctab[i] = (T)cons;
@@ -1443,13 +1628,17 @@ void dispatch_bytes(int32_t bytes, F&& f) {
 bool fast_expand_ok(const SysView& S) { return S.tables_ok != 0; }
 
 void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ctab, uint8_t* tab_full,
-                         uint8_t* ttab, cudaStream_t st) {
+                         uint8_t* ttab, uint8_t* elut, uint8_t* hsg, cudaStream_t st) {
   const uint64_t n = (uint64_t)S.m * S.tabw + (tab_full ? (uint64_t)S.m * 256 : 0);
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    k_build_tables<T><<<grid_for(n), BLK, 0, st>>>(S, tab, reinterpret_cast<T*>(ctab), tab_full, ttab);
+    k_build_tables<T><<<grid_for(n), BLK, 0, st>>>(S, tab, reinterpret_cast<T*>(ctab), tab_full, ttab, elut);
   });
   count_launch();
+  if (hsg) {
+    k_build_hs<<<grid_for((uint64_t)S.m * 16), BLK, 0, st>>>(S, hsg);
+    count_launch();
+  }
 }
 
 size_t materialize_smem_bytes(const SysView& S, int32_t bytes) {
@@ -1509,8 +1698,16 @@ void launch_expand(const SysView& S, int32_t bytes, const LevelView& L, const Ex
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<expand_grid(L.F), XW * 32, smem, st>>>(S, L, O);
       };
-      if (full) go(k_expand_t<T, true>);
-      else go(k_expand_t<T, false>);
+      if (full && S.any_generic == 0 && S.hsg != nullptr && !(S.kernel_flags & KF_EXPAND_T)) {
+        const size_t sq = expand_q_smem_bytes();
+        cudaFuncSetAttribute(k_expand_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq);
+        const unsigned g = (unsigned)((L.F + QB * PB - 1) / (QB * PB));
+        k_expand_q<<<g, QW * 32, sq, st>>>(S, L, O);
+      } else if (full) {
+        go(k_expand_t<T, true>);
+      } else {
+        go(k_expand_t<T, false>);
+      }
     }
   });
   count_launch();

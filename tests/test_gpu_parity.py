@@ -129,6 +129,21 @@ def test_random_system_parity(snp, m, F, depth, bits, dedup, target):
     assert_same_tree(tree, ref)
 
 
+@pytest.mark.parametrize("kernels", ["", "expand_t"])
+def test_uint8_large_counts(snp, monkeypatch, kernels):
+    """uint8 storage with counts well above the 32-entry register tables, so
+    the table-fallback paths of K-a and K-c run; SNP_KERNELS=expand_t selects
+    the 8-configurations-per-lane K-a instead of the 4-per-lane one."""
+    monkeypatch.setenv("SNP_KERNELS", kernels)
+    w = W.random_system(700, outdeg=8, k_nd=5, seed=77)
+    rng = np.random.default_rng(77)
+    L0 = rng.integers(0, 72, size=(900, w.m)).astype(np.int32)
+    L0[::7] = W.level0_counts(w, 900, 77)[::7]  # some rows in the usual range
+    tree = snp.System(w, count_bits=8, dedup=1, frontier_target=800).explore(L0, depth=3)
+    ref = oracle.System.from_workload(w).explore(L0, depth=3, dedup=1, count_bits=8, frontier_target=800)
+    assert_same_tree(tree, ref)
+
+
 def test_level0_duplicates_and_neuron_major_input(snp):
     w = W.random_system(100, outdeg=5, k_nd=4, seed=9)
     L0 = W.level0_counts(w, 200, 9)
