@@ -137,6 +137,10 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+KERNEL_OF = {"expand": "K-a k_expand_q (uint8) / k_expand_t", "materialize": "K-c k_materialize_bs + k_patch",
+             "dedup": "K-d k_dedup..k_compact", "keys": "K-b k_child_keys"}
+
+
 def ncu_traffic(kernel_phase):
     """dram bytes per launch of the dominant kernel from the committed ncu
     summary (profiles/ncu_summary.json), or None."""
@@ -282,7 +286,8 @@ def run_native(args, rank, world):
     Tl = [c.get("T_local", c["T"]) for c in levels]
     alg = {
         "expand": sum(x * m * wb for x in par),
-        "materialize": sum(x * m * wb for x in kep),
+        # K-c reads each parent row once and writes each kept child once
+        "materialize": sum(x * m * wb + k * m * wb for x, k in zip(par, kep)),
         "dedup": sum(t * 32 + k * 48 for t, k in zip(Tl, kep)),
         "keys": sum(t * 16 for t in Tl),
     }
@@ -297,7 +302,7 @@ def run_native(args, rank, world):
         "config": {**config_json(args, cfg, w, args.steps),
                    "parallelism": f"hash-partitioned dedup over {world} GPU(s), keys all-to-all (NCCL)"
                    if world > 1 else "1 GPU"},
-        "roofline": {"bound": "hbm", "kernel": f"phase '{dom}' ({'k_expand_t' if dom == 'expand' else 'k_materialize_bs+k_patch' if dom == 'materialize' else dom})",
+        "roofline": {"bound": "hbm", "kernel": f"phase '{dom}' ({KERNEL_OF.get(dom, dom)})",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(dom), "peak_source": peak_src},
         "step_roofline": {"algorithmic_GB_per_step_per_gpu": sb / len(levels) / 1e9,

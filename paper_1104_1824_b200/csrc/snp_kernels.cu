@@ -1189,6 +1189,12 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
     if (jbase >= m) break;  // warp-uniform
     const int32_t j = jbase + lane;
     const bool jok = j < m;
+#ifdef SNP_KC_PF
+    {  // warm L2 with this lane's count row of the next iteration (latency of the v loads)
+      const int32_t jn = j + MW * 32;
+      if (jn < m) asm volatile("prefetch.global.L2 [%0];" ::"l"(data + eidx(pb0, jn, m)));
+    }
+#endif
     if (jok) {
     // ---- bit-sliced in-synapse count over the 64 parents of the block
     uint64_t c[NPL];
