@@ -1090,20 +1090,27 @@ __host__ __device__ constexpr int xs_stride() { return PB * (int)sizeof(T) + 4; 
 // Counts of parents 8k .. 8k+7 as bytes (lo: 8k..8k+3, hi: 8k+4..8k+7) from
 // the bit planes: byte k of every plane gathered into one 64-bit word (plane
 // b in byte b), then an 8x8 bit-matrix transpose (three delta swaps).
-template <int NPL>
+// P = planes used (<= NPL): P = 4 when the warp knows every count < 16.
+template <int P, int NPL>
 __device__ __forceinline__ void counts8(const uint64_t (&c)[NPL], int k, uint32_t& lo, uint32_t& hi) {
+  constexpr int Q = P < NPL ? P : NPL;
   uint32_t p[8];
 #pragma unroll
-  for (int b = 0; b < 8; ++b) p[b] = b < NPL ? (uint32_t)(c[b < NPL ? b : 0] >> (32 * (k >> 2))) : 0u;
+  for (int b = 0; b < 8; ++b) p[b] = b < Q ? (uint32_t)(c[b < Q ? b : 0] >> (32 * (k >> 2))) : 0u;
   const uint32_t s2 = (uint32_t)(k & 3) | ((uint32_t)(4 + (k & 3)) << 4);
   lo = prmt(prmt(p[0], p[1], s2), prmt(p[2], p[3], s2), 0x5410u);
-  if (NPL <= 4) hi = 0;
-  else if (NPL == 5) hi = prmt(p[4], 0u, (uint32_t)(k & 3) | 0x4440u);
-  else hi = prmt(prmt(p[4], p[5], s2), prmt(p[6], p[7], s2), 0x5410u);
   uint32_t t;
   t = (lo ^ (lo >> 7)) & 0x00AA00AAu; lo ^= t ^ (t << 7);
-  t = (hi ^ (hi >> 7)) & 0x00AA00AAu; hi ^= t ^ (t << 7);
   t = (lo ^ (lo >> 14)) & 0x0000CCCCu; lo ^= t ^ (t << 14);
+  if (Q <= 4) {  // planes 4-7 empty: the last delta swap only moves nibbles out of lo
+    t = lo & 0xF0F0F0F0u;
+    lo ^= t;
+    hi = t >> 4;
+    return;
+  }
+  if (Q == 5) hi = prmt(p[4], 0u, (uint32_t)(k & 3) | 0x4440u);
+  else hi = prmt(prmt(p[4], p[5], s2), prmt(p[6], p[7], s2), 0x5410u);
+  t = (hi ^ (hi >> 7)) & 0x00AA00AAu; hi ^= t ^ (t << 7);
   t = (hi ^ (hi >> 14)) & 0x0000CCCCu; hi ^= t ^ (t << 14);
   t = (lo ^ (hi << 4)) & 0xF0F0F0F0u; lo ^= t; hi ^= t >> 4;
 }
@@ -1249,6 +1256,12 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         ldg256(S.ttab + (int64_t)j * 32, tt);
       }
       const uint8_t* crow8 = reinterpret_cast<const uint8_t*>(crow_g);
+      // counts >= 16 are rare: when no lane of the warp has one, the upper
+      // planes are skipped (warp-uniform branch)
+      uint64_t up = 0;
+#pragma unroll
+      for (int b = 4; b < NPL; ++b) up |= c[b];
+      const bool upper = __any_sync(__activemask(), up != 0);
 #pragma unroll 1  // two halves of 32 parents; rolled keeps the hot loop in the instruction cache
       for (int g = 0; g < 2; ++g) {
         uint32_t vw[8];
@@ -1282,8 +1295,13 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         // x = t + count: plain 32-bit adds; a byte can only carry when some
         // operand byte has its top bit set (rare: redo those quads bytewise)
         uint32_t kq[8], chk = 0;
+        if (upper) {
 #pragma unroll
-        for (int h = 0; h < 4; ++h) counts8<NPL>(c, 4 * g + h, kq[2 * h], kq[2 * h + 1]);
+          for (int h = 0; h < 4; ++h) counts8<NPL, NPL>(c, 4 * g + h, kq[2 * h], kq[2 * h + 1]);
+        } else {
+#pragma unroll
+          for (int h = 0; h < 4; ++h) counts8<4, NPL>(c, 4 * g + h, kq[2 * h], kq[2 * h + 1]);
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) chk |= t[i] | kq[i];
 #pragma unroll
