@@ -1196,12 +1196,6 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
     if (jbase >= m) break;  // warp-uniform
     const int32_t j = jbase + lane;
     const bool jok = j < m;
-#ifdef SNP_KC_PF
-    {  // warm L2 with this lane's count row of the next iteration (latency of the v loads)
-      const int32_t jn = j + MW * 32;
-      if (jn < m) asm volatile("prefetch.global.L2 [%0];" ::"l"(data + eidx(pb0, jn, m)));
-    }
-#endif
     if (jok) {
     // ---- bit-sliced in-synapse count over the 64 parents of the block
     uint64_t c[NPL];
@@ -1252,9 +1246,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       // byte permutes; the bit-sliced counts become bytes by an 8x8 bit
       // transpose per 8 parents; x = t + count is one 32-bit add per 4 parents
       uint32_t tt[8];
-      {
-        ldg256(S.ttab + (int64_t)j * 32, tt);
-      }
+      ldg256(S.ttab + (int64_t)j * 32, tt);
       const uint8_t* crow8 = reinterpret_cast<const uint8_t*>(crow_g);
       // counts >= 16 are rare: when no lane of the warp has one, the upper
       // planes are skipped (warp-uniform branch)

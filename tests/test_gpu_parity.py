@@ -144,6 +144,18 @@ def test_uint8_large_counts(snp, monkeypatch, kernels):
     assert_same_tree(tree, ref)
 
 
+def test_config5_shape_parity(snp):
+    """Config 5's system family at full width (m = 65536, n = 262144, k_nd = 7:
+    mean Ψ ≈ 38 children per parent), scaled-down frontier, bit-exact."""
+    cfg = W.CONFIGS[5]
+    w = W.random_system(cfg["m"], outdeg=8, k_nd=cfg["k_nd"], seed=cfg["seed"])
+    L0 = W.level0_counts(w, 64, cfg["seed"])
+    tree = snp.System(w, count_bits=8, dedup=1, frontier_target=64).explore(L0, depth=2)
+    ref = oracle.System.from_workload(w).explore(L0, depth=2, dedup=1, count_bits=8, frontier_target=64)
+    assert ref.counters.T[0] > 20 * 64
+    assert_same_tree(tree, ref)
+
+
 def test_level0_duplicates_and_neuron_major_input(snp):
     w = W.random_system(100, outdeg=5, k_nd=4, seed=9)
     L0 = W.level0_counts(w, 200, 9)
