@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=17)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--config", type=int, default=4, choices=[3, 4])
+    ap.add_argument("--config", type=int, default=4, choices=[3, 4, 5],
+                    help="BASELINE.json configs[k-1]; 5 is an 8-GPU workload (use --F for a 1-GPU slice)")
     ap.add_argument("--F", type=int, default=0, help="override frontier size (testing only)")
     ap.add_argument("--m", type=int, default=0, help="override neuron count (testing only)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -666,9 +666,13 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.any_generic = 0;
   for (int64_t j = 0; j < m; ++j) v.any_generic |= (meta[j].flags & NM_GENERIC) ? 1 : 0;
   {
-    // SNP_KERNELS=expand_t: the 8-configuration-per-lane K-a for uint8 too
+    // SNP_KERNELS (tests / tuning): "expand_t" = the 8-configuration-per-lane
+    // K-a for uint8 too; "kc_global_e" = K-c reads emit words from global
+    // memory even when they fit in shared memory (the large-m path)
     const char* k = getenv("SNP_KERNELS");
-    v.kernel_flags = (k && strstr(k, "expand_t")) ? KF_EXPAND_T : 0;
+    v.kernel_flags = 0;
+    if (k && strstr(k, "expand_t")) v.kernel_flags |= KF_EXPAND_T;
+    if (k && strstr(k, "kc_global_e")) v.kernel_flags |= KF_KC_GLOBAL_E;
   }
   v.m = (int32_t)m;
   v.n = n;

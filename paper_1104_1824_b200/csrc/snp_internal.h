@@ -65,7 +65,7 @@ struct Tables {
 // per-block emit words of a materialize tile fit in shared memory).
 bool fast_expand_ok(const SysView& S);
 bool fast_materialize_ok(const SysView& S);
-size_t materialize_smem_bytes(const SysView& S, int32_t bytes);
+size_t materialize_smem_bytes(const SysView& S, int32_t bytes, bool staged_e);
 
 // ---- launchers (all asynchronous on `st`) ----------------------------------
 void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ctab, uint8_t* tab_full,

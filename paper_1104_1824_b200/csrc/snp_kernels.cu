@@ -1115,7 +1115,11 @@ __device__ __forceinline__ void counts8(const uint64_t (&c)[NPL], int k, uint32_
   t = (lo ^ (hi << 4)) & 0xF0F0F0F0u; lo ^= t; hi ^= t >> 4;
 }
 
-template <typename T, int NPL>
+__device__ const uint64_t g_zero_word = 0;  // padded in-synapses when the emit words stay in global memory
+
+// ES: the block's emit words are staged in shared memory (m·8 B fit); else
+// (large m) the in-synapse gather reads them from global memory (L2/L1).
+template <typename T, int NPL, bool ES>
 __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView L, ExpandOut O,
                                                              const uint64_t* kq_off, NextArrays N, uint64_t* ovf,
                                                              unsigned long long* n_ovf, uint64_t ovf_cap) {
@@ -1123,7 +1127,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   const int32_t m = S.m;
   const int64_t mE = (m + 1) & ~1;
   uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words + 2 zero words
-  uint8_t* sX = smem + (mE + 2) * 8;                                    // MW×32×xs_stride
+  uint8_t* sX = smem + (ES ? (mE + 2) * 8 : 0);                         // MW×32×xs_stride
   uint8_t* sR = sX + (size_t)MW * 32 * xs_stride<T>();                  // QCAP
   uint32_t* sD = reinterpret_cast<uint32_t*>(sR + QCAP + 4);            // (QCAP+4)/4 quad descriptors
   uint64_t* sQ = reinterpret_cast<uint64_t*>(sD + (QCAP + 4) / 4);      // 65 (+1 pad)
@@ -1140,14 +1144,15 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
     fence_barrier_init();
   }
   __syncthreads();
-  if (tid == 0) {
+  if (ES && tid == 0) {
     mbar_arrive_expect_tx(bar, ebytes);
     const uint8_t* src = reinterpret_cast<const uint8_t*>(O.ebits) + (size_t)blk * ebytes;
     for (uint32_t off = 0; off < ebytes; off += 32768u)
       bulk_g2s(reinterpret_cast<uint8_t*>(sE) + off, src + off, min(32768u, ebytes - off), bar);
   }
   if (tid <= np) sQ[tid] = kq_off[pb0 + tid];
-  if (tid < 2) sE[mE + tid] = 0;  // target of padded in-synapses
+  if (ES && tid < 2) sE[mE + tid] = 0;  // target of padded in-synapses
+  const uint64_t* gE = O.ebits + blk * mE;
   __syncthreads();
   const uint64_t nq = Q1 - Q0;
   const uint64_t Qb = Q0 & ~3ULL;  // sR[q - Qb]: 4-aligned for q % 4 == 0
@@ -1183,7 +1188,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   uint64_t haskids = 0;
   for (int r = 0; r < np; ++r) haskids |= (uint64_t)(sQ[r + 1] > sQ[r]) << r;
   __syncthreads();
-  mbar_wait(bar, 0);
+  if (ES) mbar_wait(bar, 0);
 
   const T* data = reinterpret_cast<const T*>(L.data);
   T* out = reinterpret_cast<T*>(N.data);
@@ -1214,7 +1219,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         for (int u = 0; u < 8; ++u) src[u] = (e0 + u < ne) ? __ldg(col + (e0 + u) * 32) : (int32_t)mE;  // batch the loads
         uint64_t x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = sE[src[u]];
+        for (int u = 0; u < 8; ++u) x[u] = ES ? sE[src[u]] : __ldg(src[u] < mE ? gE + src[u] : &g_zero_word);
         // Harley-Seal carry-save tree: 8 words into the planes with 7 full
         // adders; the carry out of plane 3 ripples into the upper planes
         uint64_t twosA, twosB, foursA, foursB, eightsA;
@@ -1657,15 +1662,22 @@ void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ct
   }
 }
 
-size_t materialize_smem_bytes(const SysView& S, int32_t bytes) {
+constexpr size_t KC_SMEM_MAX = 220 * 1024;
+
+size_t materialize_smem_bytes(const SysView& S, int32_t bytes, bool staged_e) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
   const size_t xs = (size_t)MW * 32 * (PB * bytes + 4);
-  return (mE + 2) * 8 + xs + 2 * (QCAP + 4) + 67 * 8 + 16;
+  return (staged_e ? (mE + 2) * 8 : 0) + xs + 2 * (QCAP + 4) + 67 * 8 + 16;
+}
+
+// emit words staged in shared memory when they fit (else read from L2)
+bool materialize_stage_e(const SysView& S, int32_t bytes) {
+  return !(S.kernel_flags & KF_KC_GLOBAL_E) && materialize_smem_bytes(S, bytes, true) <= KC_SMEM_MAX;
 }
 
 bool fast_materialize_ok(const SysView& S) {
   const int32_t w = S.count_max <= 255 ? 1 : S.count_max <= 65535 ? 2 : 4;
-  return S.tables_ok && S.binary_emit && S.max_indeg < 256 && materialize_smem_bytes(S, w) <= 220 * 1024;
+  return S.tables_ok && S.binary_emit && S.max_indeg < 256 && materialize_smem_bytes(S, w, false) <= KC_SMEM_MAX;
 }
 
 void launch_import(const void* src, int32_t src_bytes, int32_t src_layout, int64_t src_ld, int64_t F, int32_t m,
@@ -1776,7 +1788,8 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
                         unsigned long long* n_ovf, uint64_t ovf_cap, int32_t* err, cudaStream_t st) {
   if (K <= 0) return;
   if (fast_materialize_ok(S)) {
-    const size_t smem = materialize_smem_bytes(S, bytes);
+    const bool staged = materialize_stage_e(S, bytes);
+    const size_t smem = materialize_smem_bytes(S, bytes, staged);
     const unsigned nblk = (unsigned)((L.F + PB - 1) / PB);
     dispatch_bytes(bytes, [&](auto tt) {
       using T = decltype(tt);
@@ -1784,10 +1797,17 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<nblk, MW * 32, smem, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
       };
-      if (S.max_indeg < 16) go(k_materialize_bs<T, 4>);
-      else if (S.max_indeg < 32) go(k_materialize_bs<T, 5>);
-      else if (S.max_indeg < 64) go(k_materialize_bs<T, 6>);
-      else go(k_materialize_bs<T, 8>);
+      if (staged) {
+        if (S.max_indeg < 16) go(k_materialize_bs<T, 4, true>);
+        else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, true>);
+        else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, true>);
+        else go(k_materialize_bs<T, 8, true>);
+      } else {
+        if (S.max_indeg < 16) go(k_materialize_bs<T, 4, false>);
+        else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, false>);
+        else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, false>);
+        else go(k_materialize_bs<T, 8, false>);
+      }
     });
   } else {
     unsigned g = grid_for((uint64_t)K * 32, 256);

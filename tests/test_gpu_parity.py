@@ -113,6 +113,17 @@ def test_tiny_random(snp, seed):
 
 
 # ---- random systems shaped like configs 3-5, scaled to oracle size ---------
+@pytest.mark.parametrize("kernels", ["kc_global_e"])
+def test_random_parity_global_emit_words(snp, monkeypatch, kernels):
+    monkeypatch.setenv("SNP_KERNELS", kernels)
+    for m, F, bits, dedup in [(300, 700, 16, 0), (1024, 900, 8, 1)]:
+        w = W.random_system(m, outdeg=8, k_nd=5, seed=m + 3)
+        L0 = W.level0_counts(w, F, m + 3)
+        tree = snp.System(w, count_bits=bits, dedup=dedup, frontier_target=F).explore(L0, depth=3)
+        ref = oracle.System.from_workload(w).explore(L0, depth=3, dedup=dedup, count_bits=bits, frontier_target=F)
+        assert_same_tree(tree, ref)
+
+
 @pytest.mark.parametrize("m,F,depth,bits,dedup,target", [
     (64, 513, 4, 8, 1, 0),          # ragged F (not a multiple of 4 / 128)
     (300, 1000, 3, 16, 0, 700),     # thinning, exact dedup
@@ -129,11 +140,12 @@ def test_random_system_parity(snp, m, F, depth, bits, dedup, target):
     assert_same_tree(tree, ref)
 
 
-@pytest.mark.parametrize("kernels", ["", "expand_t"])
+@pytest.mark.parametrize("kernels", ["", "expand_t", "kc_global_e"])
 def test_uint8_large_counts(snp, monkeypatch, kernels):
     """uint8 storage with counts well above the 32-entry register tables, so
     the table-fallback paths of K-a and K-c run; SNP_KERNELS=expand_t selects
-    the 8-configurations-per-lane K-a instead of the 4-per-lane one."""
+    the 8-configurations-per-lane K-a instead of the 4-per-lane one,
+    kc_global_e the K-c variant that gathers emit words from global memory."""
     monkeypatch.setenv("SNP_KERNELS", kernels)
     w = W.random_system(700, outdeg=8, k_nd=5, seed=77)
     rng = np.random.default_rng(77)
