@@ -361,8 +361,11 @@ snp_status reserve_horizon(snp_system* s, int64_t Ft) {
   if (Ft <= 0) return SNP_OK;
   size_t free_b = 0, total_b = 0;
   CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-  const size_t working = level_bytes(Ft, s->m, s->bytes) + (size_t)((Ft + PB - 1) / PB) * ((s->m + 1) & ~1) * 8 +
-                         (size_t)Ft * 8 * 64 + ((size_t)4 << 30);
+  // next level (+10 % thinning slack), emit words, ND lists, child arrays and
+  // level table for 16·Ft children, 4 GB of slack
+  const size_t working = level_bytes(Ft + Ft / 10, s->m, s->bytes) +
+                         (size_t)((Ft + PB - 1) / PB) * ((s->m + 1) & ~1) * 8 + (size_t)Ft * KMAX * 8 +
+                         (size_t)Ft * 16 * 60 + next_pow2((uint64_t)Ft * 32) * sizeof(Slot) + ((size_t)4 << 30);
   if (free_b <= working) return SNP_OK;
   size_t spare = free_b - working;
   s->horizon_reserved = true;
