@@ -96,8 +96,9 @@ struct SysView {
   const int32_t* in_off;     // m + 1
   const int32_t* in_src;     // sources s with (s, j) ∈ syn, grouped by target j
   // the same in-synapses "edge-major" per group of 32 consecutive targets:
-  // group g holds in_pad_deg[g] rows of 32 sources (row e, lane l = e-th
-  // in-synapse of target 32g + l), padded with the index m_even (a zero word)
+  // group g holds in_pad_off[g+1] - in_pad_off[g] rows of 32 sources (row e,
+  // lane l = e-th in-synapse of target 32g + l), padded with the index m_even
+  // (a zero word)
   const int32_t* in_pad;
   const int64_t* in_pad_off;   // m/32 + 1 row offsets (×32 entries)
   const int32_t* out_off;    // m + 1
@@ -211,6 +212,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "r"(smem_u32(bar)), "r"(phase)
         : "memory");
   }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // global -> shared bulk copy (bytes % 16 == 0, both addresses 16-aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

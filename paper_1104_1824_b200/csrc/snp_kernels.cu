@@ -1081,8 +1081,11 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_WARPS
 #define SNP_KC_WARPS 32
 #endif
+#ifndef SNP_KC_PREFETCH
+#define SNP_KC_PREFETCH 0
+#endif
 constexpr int MW = SNP_KC_WARPS;  // warps per K-c CTA
-constexpr int QCAP = 4092;   // outputs per block resolved through the r(q) table (+4 alignment slack)
+constexpr int QCAP = 4064;   // outputs per block resolved through the r(q) table (+32 alignment slack)
 
 template <typename T>
 __host__ __device__ constexpr int xs_stride() { return PB * (int)sizeof(T) + 4; }
@@ -1117,6 +1120,16 @@ __device__ __forceinline__ void counts8(const uint64_t (&c)[NPL], int k, uint32_
 
 __device__ const uint64_t g_zero_word = 0;  // padded in-synapses when the emit words stay in global memory
 
+// K-c store program (u8): the output range [Q0, Q1) of a CTA split into
+// aligned stores, identical for every neuron j of the block, so it is built
+// once per CTA into shared memory.  Op (64 bits): bits 0-31 byte offset of
+// the store from the row of neuron j in output block Q0 >> 6 (output block
+// stride m·64); bits 32-33 kind (0: 1 byte, 1: 4 bytes, 2: 16 bytes, 3: 32
+// bytes); bits 48-63 the parent (kind 0) or the quad index (q - Qb) / 4
+// (kinds 1-3).  Qb = Q0 rounded down to 32, so the descriptors of a
+// 16/32-byte store are one/two aligned 16-B loads.
+constexpr int OPCAP = 1100;  // >= 16 ops per output block × (QCAP / 64 + 2)
+
 // ES: the block's emit words are staged in shared memory (m·8 B fit); else
 // (large m) the in-synapse gather reads them from global memory (L2/L1).
 template <typename T, int NPL, bool ES>
@@ -1128,10 +1141,12 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   const int64_t mE = (m + 1) & ~1;
   uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words + 2 zero words
   uint8_t* sX = smem + (ES ? (mE + 2) * 8 : 0);                         // MW×32×xs_stride
-  uint8_t* sR = sX + (size_t)MW * 32 * xs_stride<T>();                  // QCAP
-  uint32_t* sD = reinterpret_cast<uint32_t*>(sR + QCAP + 4);            // (QCAP+4)/4 quad descriptors
-  uint64_t* sQ = reinterpret_cast<uint64_t*>(sD + (QCAP + 4) / 4);      // 65 (+1 pad)
+  uint8_t* sR = sX + (size_t)MW * 32 * xs_stride<T>();                  // QCAP + 32
+  uint32_t* sD = reinterpret_cast<uint32_t*>(sR + QCAP + 32);           // (QCAP+32)/4 quad descriptors
+  uint64_t* sOps = reinterpret_cast<uint64_t*>(sD + (QCAP + 32) / 4);   // OPCAP store ops
+  uint64_t* sQ = sOps + OPCAP;                                          // 65 (+1 pad)
   uint64_t* bar = sQ + 66;
+  uint32_t* sMisc = reinterpret_cast<uint32_t*>(bar + 1);              // [0,1] haskids, [2] #ops
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t blk = blockIdx.x;
   const int64_t pb0 = blk * PB;
@@ -1155,16 +1170,22 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   const uint64_t* gE = O.ebits + blk * mE;
   __syncthreads();
   const uint64_t nq = Q1 - Q0;
-  const uint64_t Qb = Q0 & ~3ULL;  // sR[q - Qb]: 4-aligned for q % 4 == 0
+  const bool prog = sizeof(T) == 1 && nq <= QCAP;  // CTA-uniform: the store program applies
+  const uint64_t Qb = Q0 & ~31ULL;                  // sR[q - Qb]
   if (nq <= QCAP) {
     if (tid < np)
       for (uint64_t q = sQ[tid]; q < sQ[tid + 1]; ++q) sR[q - Qb] = (uint8_t)tid;
   }
+  if (tid < 64) {  // parents with kept children (bit r), for the overflow bookkeeping
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, tid < np && sQ[tid + 1] > sQ[tid]);
+    if (lane == 0) sMisc[warp] = b;
+  }
   __syncthreads();
-  // output quads q..q+3 (q % 4 == 0) whose parents lie in one 8-byte window
-  // of the x row: one byte permute of two words (CTA-uniform descriptor:
-  // word in bits 16-19, selector in bits 0-15; bit 31 = use the byte path)
-  if (nq <= QCAP) {
+  // quad descriptors: output quad q..q+3 (q % 4 == 0) whose parents lie in
+  // one 8-byte window of the x row = one byte permute of two words (word in
+  // bits 16-19, selector in bits 0-15; bit 31 = use the byte path); the
+  // store program reads r(q) too, so both run after the r(q) table is built
+  if (prog) {
     const uint64_t nquad = (Q1 - Qb + 3) >> 2;
     for (uint64_t i = tid; i < nquad; i += blockDim.x) {
       const uint64_t q = Qb + 4 * i;
@@ -1184,10 +1205,36 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       sD[i] = d;
     }
   }
-  // parents with kept children (bit r), for the overflow bookkeeping
-  uint64_t haskids = 0;
-  for (int r = 0; r < np; ++r) haskids |= (uint64_t)(sQ[r + 1] > sQ[r]) << r;
+  if (prog && tid == 64) {  // the store program (one thread; overlaps the emit-word staging)
+    int n = 0;
+    const uint64_t ob0 = Q0 >> 6;
+    for (uint64_t ob = ob0; ob <= (Q1 - 1) >> 6; ++ob) {
+      uint64_t q = Q0 > (ob << 6) ? Q0 : (ob << 6);
+      const uint64_t qe = Q1 < ((ob + 1) << 6) ? Q1 : ((ob + 1) << 6);
+      const uint64_t segoff = ((ob - ob0) * (uint64_t)m) << 6;
+      auto op = [&](uint32_t kind, uint64_t qq) {
+        const uint64_t idx = kind == 0 ? (uint64_t)sR[qq - Qb] : (qq - Qb) >> 2;
+        sOps[n++] = (segoff + (qq & 63)) | ((uint64_t)kind << 32) | (idx << 48);
+      };
+      for (; q < qe && (q & 3); ++q) op(0, q);
+      for (; q + 4 <= qe && (q & 15); q += 4) op(1, q);
+      if ((q & 31) && q + 16 <= qe) {
+        op(2, q);
+        q += 16;
+      }
+      for (; q + 32 <= qe; q += 32) op(3, q);
+      if (q + 16 <= qe) {
+        op(2, q);
+        q += 16;
+      }
+      for (; q + 4 <= qe; q += 4) op(1, q);
+      for (; q < qe; ++q) op(0, q);
+    }
+    sMisc[2] = (uint32_t)n;
+  }
   __syncthreads();
+  const uint64_t haskids = (uint64_t)sMisc[0] | ((uint64_t)sMisc[1] << 32);
+  const int nops = prog ? (int)sMisc[2] : 0;
   if (ES) mbar_wait(bar, 0);
 
   const T* data = reinterpret_cast<const T*>(L.data);
@@ -1200,28 +1247,45 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
     const int32_t jbase = it * MW * 32 + warp * 32;
     if (jbase >= m) break;  // warp-uniform
     const int32_t j = jbase + lane;
-    const bool jok = j < m;
-    if (jok) {
+    if (j < m) {
+    const T* row = data + eidx(pb0, j, m);
+#if SNP_KC_PREFETCH
+    // the first 32 counts of the row are loaded before the gather so their
+    // latency overlaps it; the second half is loaded at the top of half 0
+    uint32_t vw[8];
+    if (sizeof(T) == 1) ldg256(row, vw);
+#endif
     // ---- bit-sliced in-synapse count over the 64 parents of the block
     uint64_t c[NPL];
 #pragma unroll
     for (int b = 0; b < NPL; ++b) c[b] = 0;
     {
       // edge-major padded in-CSR: row e of the group holds the e-th source
-      // of every lane's target (coalesced), padding points at a zero word
+      // of every lane's target (coalesced), padding points at a zero word;
+      // rows come in blocks of 8 (Harley-Seal, 7 full adders), a tail of
+      // <= 4 rows in one block of 4 (3 full adders)
       const int64_t g = jbase >> 5;
       const int64_t r0 = __ldg(S.in_pad_off + g), r1 = __ldg(S.in_pad_off + g + 1);
       const int32_t* col = S.in_pad + r0 * 32 + lane;
       const int ne = (int)(r1 - r0);
-      for (int e0 = 0; e0 < ne; e0 += 8) {
+      auto word = [&](int32_t s) -> uint64_t { return ES ? sE[s] : __ldg(s < mE ? gE + s : &g_zero_word); };
+      auto ripple = [&](int b0, uint64_t carry) {
+#pragma unroll
+        for (int b = 0; b < NPL; ++b) {
+          if (b < b0) continue;
+          const uint64_t t = c[b] & carry;
+          c[b] ^= carry;
+          carry = t;
+        }
+      };
+      int e0 = 0;
+      for (; e0 + 8 <= ne || (e0 < ne && ne - e0 > 4); e0 += 8) {
         int32_t src[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) src[u] = (e0 + u < ne) ? __ldg(col + (e0 + u) * 32) : (int32_t)mE;  // batch the loads
         uint64_t x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = ES ? sE[src[u]] : __ldg(src[u] < mE ? gE + src[u] : &g_zero_word);
-        // Harley-Seal carry-save tree: 8 words into the planes with 7 full
-        // adders; the carry out of plane 3 ripples into the upper planes
+        for (int u = 0; u < 8; ++u) x[u] = word(src[u]);
         uint64_t twosA, twosB, foursA, foursB, eightsA;
         csa(twosA, c[0], c[0], x[0], x[1]);
         csa(twosB, c[0], c[0], x[2], x[3]);
@@ -1230,19 +1294,24 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         csa(twosB, c[0], c[0], x[6], x[7]);
         csa(foursB, c[1], c[1], twosA, twosB);
         csa(eightsA, c[2], c[2], foursA, foursB);
-        uint64_t carry = c[3] & eightsA;
-        c[3] ^= eightsA;
+        ripple(3, eightsA);
+      }
+      if (e0 < ne) {  // 1..4 rows left
+        int32_t src[4];
 #pragma unroll
-        for (int b = 4; b < NPL; ++b) {
-          const uint64_t t = c[b] & carry;
-          c[b] ^= carry;
-          carry = t;
-        }
+        for (int u = 0; u < 4; ++u) src[u] = (e0 + u < ne) ? __ldg(col + (e0 + u) * 32) : (int32_t)mE;
+        uint64_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = word(src[u]);
+        uint64_t twosA, twosB, foursA;
+        csa(twosA, c[0], c[0], x[0], x[1]);
+        csa(twosB, c[0], c[0], x[2], x[3]);
+        csa(foursA, c[1], c[1], twosA, twosB);
+        ripple(2, foursA);
       }
     }
     const NeuronMeta mt = S.meta[j];
     const T* crow_g = ctab + (int64_t)j * S.tabw;
-    const T* row = data + eidx(pb0, j, m);
     const bool generic = mt.flags & NM_GENERIC;
     uint64_t ovf_bits = 0;
     if (sizeof(T) == 1 && !generic) {
@@ -1261,11 +1330,19 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       const bool upper = __any_sync(__activemask(), up != 0);
 #pragma unroll 1  // two halves of 32 parents; rolled keeps the hot loop in the instruction cache
       for (int g = 0; g < 2; ++g) {
+#if SNP_KC_PREFETCH
+        uint32_t vn[8];
+        if (g == 0 && np > 32) ldg256(row + 32, vn);
+        else
+#pragma unroll
+          for (int i = 0; i < 8; ++i) vn[i] = 0;
+#else
         uint32_t vw[8];
         if (32 * g < np) ldg256(row + 32 * g, vw);
         else
 #pragma unroll
           for (int i = 0; i < 8; ++i) vw[i] = 0;
+#endif
         // t = v - c_first(v) for the 32 counts: byte permutes unless some
         // count >= 32 (rare: that quad folds through the compact table)
         uint32_t t[8], hiv = 0;
@@ -1315,6 +1392,10 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
           }
           reinterpret_cast<uint32_t*>(xsb)[8 * g + i] = x4;
         }
+#if SNP_KC_PREFETCH
+#pragma unroll
+        for (int i = 0; i < 8; ++i) vw[i] = vn[i];
+#endif
       }
     } else {
       for (int r = 0; r < PB; ++r) {
@@ -1342,52 +1423,54 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       if (slot < ovf_cap) ovf[slot] = ((uint64_t)(uint32_t)j << 32) | (uint64_t)(pb0 + r);
     }
     // ---- write x to every kept child of the block's parents (row j of the output)
-    if (nq <= QCAP) {
-      uint64_t q = Q0;
-      while (q < Q1) {
-        const uint64_t qe = min(Q1, (q | (PB - 1)) + 1);  // end of this output block
-        T* orow = out + (((int64_t)(q >> 6) * m + j) << 6);
-        if (sizeof(T) == 1) {
-          auto quad = [&](uint64_t qq) {
-            const uint32_t d = sD[(qq - Qb) >> 2];
-            if (!(d & 0x80000000u)) {
-              const uint32_t* xw = reinterpret_cast<const uint32_t*>(xsb) + (d >> 16);
-              return prmt(xw[0], xw[1], d & 0xFFFFu);
-            }
-            const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (qq - Qb));  // 4 parent indices
-            return (uint32_t)xsb[rr & 0xFF] | ((uint32_t)xsb[(rr >> 8) & 0xFF] << 8) |
-                   ((uint32_t)xsb[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xsb[rr >> 24] << 24);
-          };
-          for (; q < qe && (q & 3); ++q) orow[q & 63] = xs[sR[q - Qb]];
-          for (; q + 4 <= qe && (q & 15); q += 4) *reinterpret_cast<uint32_t*>(orow + (q & 63)) = quad(q);
-          if ((q & 31) && q + 16 <= qe) {
-            const uint32_t w0 = quad(q), w1 = quad(q + 4), w2 = quad(q + 8), w3 = quad(q + 12);
-            *reinterpret_cast<uint4*>(orow + (q & 63)) = make_uint4(w0, w1, w2, w3);
-            q += 16;
-          }
-          for (; q + 32 <= qe; q += 32) {  // 32 children per store: one full sector
-            uint32_t w[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) w[i] = quad(q + 4 * i);
-            stg256(orow + (q & 63), w);
-          }
-          if (q + 16 <= qe) {
-            const uint32_t w0 = quad(q), w1 = quad(q + 4), w2 = quad(q + 8), w3 = quad(q + 12);
-            *reinterpret_cast<uint4*>(orow + (q & 63)) = make_uint4(w0, w1, w2, w3);
-            q += 16;
-          }
-          for (; q + 4 <= qe; q += 4) *reinterpret_cast<uint32_t*>(orow + (q & 63)) = quad(q);
+    if (prog) {
+      uint8_t* obase = reinterpret_cast<uint8_t*>(out) + (((int64_t)(Q0 >> 6) * m + j) << 6);
+      const uint32_t* xw = reinterpret_cast<const uint32_t*>(xsb);
+      auto quad = [&](uint32_t d, uint32_t qi) -> uint32_t {
+        if (!(d & 0x80000000u)) {
+          const uint32_t* w = xw + (d >> 16);
+          return prmt(w[0], w[1], d & 0xFFFFu);
         }
-        for (; q < qe; ++q) orow[q & 63] = xs[sR[q - Qb]];
+        const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + 4 * qi);  // 4 parent indices
+        return (uint32_t)xsb[rr & 0xFF] | ((uint32_t)xsb[(rr >> 8) & 0xFF] << 8) |
+               ((uint32_t)xsb[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xsb[rr >> 24] << 24);
+      };
+      for (int i = 0; i < nops; ++i) {
+        const uint64_t op = sOps[i];
+        uint8_t* dst = obase + (uint32_t)op;
+        const uint32_t hi = (uint32_t)(op >> 32), kind = hi & 3u, qi = hi >> 16;
+        if (kind == 3u) {
+          const uint4 d0 = *reinterpret_cast<const uint4*>(sD + qi);
+          const uint4 d1 = *reinterpret_cast<const uint4*>(sD + qi + 4);
+          uint32_t w[8];
+          w[0] = quad(d0.x, qi);
+          w[1] = quad(d0.y, qi + 1);
+          w[2] = quad(d0.z, qi + 2);
+          w[3] = quad(d0.w, qi + 3);
+          w[4] = quad(d1.x, qi + 4);
+          w[5] = quad(d1.y, qi + 5);
+          w[6] = quad(d1.z, qi + 6);
+          w[7] = quad(d1.w, qi + 7);
+          stg256(dst, w);
+        } else if (kind == 2u) {
+          const uint4 d0 = *reinterpret_cast<const uint4*>(sD + qi);
+          *reinterpret_cast<uint4*>(dst) =
+              make_uint4(quad(d0.x, qi), quad(d0.y, qi + 1), quad(d0.z, qi + 2), quad(d0.w, qi + 3));
+        } else if (kind == 1u) {
+          *reinterpret_cast<uint32_t*>(dst) = quad(sD[qi], qi);
+        } else {
+          *dst = xsb[qi];
+        }
       }
+    } else if (nq <= QCAP) {
+      for (uint64_t q = Q0; q < Q1; ++q) out[eidx((int64_t)q, j, m)] = xs[sR[q - Qb]];
     } else {
       for (int r = 0; r < np; ++r)
         for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = xs[r];
     }
-    }  // jok
+    }  // j < m
   }
 }
-
 // K-c (generic): every (kept child, neuron) computed exactly.
 template <typename T>
 __global__ void k_materialize_exact(SysView S, LevelView L, ExpandOut O, NextArrays N, int64_t K, int32_t* err) {
@@ -1667,7 +1750,7 @@ constexpr size_t KC_SMEM_MAX = 220 * 1024;
 size_t materialize_smem_bytes(const SysView& S, int32_t bytes, bool staged_e) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
   const size_t xs = (size_t)MW * 32 * (PB * bytes + 4);
-  return (staged_e ? (mE + 2) * 8 : 0) + xs + 2 * (QCAP + 4) + 67 * 8 + 16;
+  return (staged_e ? (mE + 2) * 8 : 0) + xs + 2 * (QCAP + 32) + 8 * OPCAP + 67 * 8 + 16 + 16;
 }
 
 // emit words staged in shared memory when they fit (else read from L2)

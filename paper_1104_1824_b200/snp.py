@@ -90,9 +90,12 @@ def lib() -> ctypes.CDLL:
     """Load libsnp.so (building it in-tree if it is missing or stale)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_build.LIB_SNP) or os.environ.get("SNP_REBUILD"):
-            _build.build()
-        L = ctypes.CDLL(_build.LIB_SNP)
+        path = os.environ.get("SNP_LIB")  # tuning aid: an in-tree variant build (tools/gpu_ab.sh)
+        if not path:
+            if not os.path.exists(_build.LIB_SNP) or os.environ.get("SNP_REBUILD"):
+                _build.build()
+            path = _build.LIB_SNP
+        L = ctypes.CDLL(path)
         L.snp_abi_version.restype = ctypes.c_int
         L.snp_last_error.restype = ctypes.c_char_p
         L.snp_load.argtypes = [ctypes.POINTER(snp_matrix), _P, ctypes.c_int64, _P, ctypes.c_int64,
