@@ -68,6 +68,12 @@ def lib() -> ctypes.CDLL:
         L.oracle_thinning_tau.restype = _U64
         L.oracle_explore.argtypes = [_P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _U64, _U64, ctypes.POINTER(_P)]
         L.oracle_explore.restype = ctypes.c_int
+        L.oracle_explore_gen.argtypes = [_P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _U64, _U64, _I32,
+                                         ctypes.POINTER(_P)]
+        L.oracle_explore_gen.restype = ctypes.c_int
+        L.oracle_run_num_numbers.argtypes = [_P]
+        L.oracle_run_num_numbers.restype = _I64
+        L.oracle_run_numbers.argtypes = [_P, _P]
         L.oracle_run_status.argtypes = [_P]
         L.oracle_run_error.argtypes = [_P]
         L.oracle_run_error.restype = ctypes.c_char_p
@@ -155,15 +161,24 @@ class System:
         return int(psi.value), S, Cn
 
     def explore(self, level0, depth: int, dedup: int = 0, count_bits: int = 32, frontier_target: int = 0,
-                max_transitions: int = 0, seeds=(0x5EED0, 0x5EED1)) -> "Run":
+                max_transitions: int = 0, seeds=(0x5EED0, 0x5EED1), out_rule: int | None = None) -> "Run":
+        """BFS computation tree.  ``out_rule``: index of
+        the output neuron's rule whose firing is an output spike; the state is
+        then augmented with A (steps since the first output spike), level-0
+        rows may have m (A = 0 appended) or m + 1 columns, and ``Run.numbers``
+        holds the generated numbers (oracle.cpp ``oracle_explore_gen``)."""
         L0 = np.ascontiguousarray(np.atleast_2d(level0), dtype=np.int32)
-        assert L0.shape[1] == self.m
+        width = self.m + (0 if out_rule is None else 1)
+        if out_rule is not None and L0.shape[1] == self.m:
+            L0 = np.ascontiguousarray(np.hstack([L0, np.zeros((L0.shape[0], 1), np.int32)]))
+        assert L0.shape[1] == width
         h = _P()
-        st = lib().oracle_explore(self._h, L0.shape[0], _ptr(L0), depth, dedup, count_bits, frontier_target,
-                                  max_transitions, seeds[0], seeds[1], ctypes.byref(h))
+        st = lib().oracle_explore_gen(self._h, L0.shape[0], _ptr(L0), depth, dedup, count_bits, frontier_target,
+                                      max_transitions, seeds[0], seeds[1], -1 if out_rule is None else out_rule,
+                                      ctypes.byref(h))
         if st == OR_E_ARG and not h:
             raise OracleError(st, "bad argument")
-        return Run(self, h, st)
+        return Run(self, h, st, width)
 
 
 @dataclass
@@ -176,8 +191,9 @@ class Counters:
 class Run:
     """Result of ``System.explore`` — the BFS computation tree."""
 
-    def __init__(self, sys: System, h, status: int):
+    def __init__(self, sys: System, h, status: int, width: int | None = None):
         L = lib()
+        width = sys.m if width is None else width
         self.status = status
         self.error = L.oracle_run_error(h).decode() if h else ""
         try:
@@ -186,8 +202,8 @@ class Run:
             ne = L.oracle_run_num_expanded(h)
             self.level_offsets = np.zeros(nl + 1, np.int64)
             L.oracle_run_level_offsets(h, _ptr(self.level_offsets))
-            self.configs = np.zeros((nc, sys.m), np.int64)
-            L.oracle_run_configs(h, sys.m, _ptr(self.configs))
+            self.configs = np.zeros((nc, width), np.int64)
+            L.oracle_run_configs(h, width, _ptr(self.configs))
             self.parent = np.zeros(nc, np.int64)
             self.t = np.zeros(nc, np.uint64)
             self.halting = np.zeros(nc, np.uint8)
@@ -199,6 +215,9 @@ class Run:
             kp = np.zeros(ne, np.int64)
             L.oracle_run_counters(h, _ptr(T), _ptr(nn), _ptr(kp))
             self.counters = Counters(T, nn, kp)
+            nums = np.zeros(L.oracle_run_num_numbers(h), np.int64)
+            L.oracle_run_numbers(h, _ptr(nums))
+            self.numbers = set(int(x) for x in nums)
         finally:
             L.oracle_run_free(h)
 

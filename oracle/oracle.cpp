@@ -236,6 +236,7 @@ struct Run {
   std::vector<uint8_t> halting;
   std::vector<uint64_t> fp0, fp1;
   std::vector<int64_t> level_T, level_new, level_kept;  // per expanded level
+  std::set<int64_t> numbers;                   // generated numbers (out_rule >= 0)
 };
 
 }  // namespace
@@ -331,10 +332,28 @@ uint64_t oracle_thinning_tau(int64_t F, int64_t n_new) {
 //                  storage range is SNP overflow (reading A16).
 //   frontier_target F: 0 = no cap; otherwise thinning (reading A19).
 //   max_transitions:   per-level budget on T; 0 = unlimited (capacity error).
-int oracle_explore(const oracle_system* h, int64_t F0, const int32_t* level0, int32_t depth,
-                   int32_t dedup, int32_t count_bits, int64_t frontier_target,
-                   int64_t max_transitions, uint64_t seed0, uint64_t seed1, oracle_run** out) {
+//
+//   out_rule >= 0: the result of a computation of a
+//   generating SNP system is the number of steps between the first two spikes
+//   the output neuron sends to the environment (PAPER.md:89 `out`, 95-99: Π
+//   "generates all numbers in N - {1}" and "this generated set is the result
+//   of the computation").  An output spike at step k is the firing of rule
+//   `out_rule` in S_k.  The state is augmented with A = 0 (no output spike yet)
+//   or A = k - t1 >= 1 at level k (steps since the first spike at step t1), a
+//   last column of every configuration (width m + 1).  A transition from
+//   (C, A) by S: if A >= 1 and S fires out_rule, the computation has generated
+//   the number A and ends there (the child is terminal: counted in T, not
+//   stored); else A' = (A == 0 ? [S fires out_rule] : A + 1) and the child is
+//   (C + S·M, A').  Dedup and halting act on the augmented state.  level0 rows
+//   then have m + 1 columns.
+int oracle_explore_gen(const oracle_system* h, int64_t F0, const int32_t* level0, int32_t depth,
+                       int32_t dedup, int32_t count_bits, int64_t frontier_target,
+                       int64_t max_transitions, uint64_t seed0, uint64_t seed1, int32_t out_rule,
+                       oracle_run** out) {
   const System& s = h->s;
+  if (out_rule >= s.n) return OR_E_ARG;
+  const bool gen = out_rule >= 0;
+  const int64_t width = s.m + (gen ? 1 : 0);
   if (!out || F0 < 1 || depth < 0 || (dedup != 0 && dedup != 1)) return OR_E_ARG;
   if (count_bits != 8 && count_bits != 16 && count_bits != 32) return OR_E_ARG;
   const int64_t cmax = count_bits == 8 ? 255 : count_bits == 16 ? 65535 : 2147483647LL;
@@ -363,7 +382,7 @@ int oracle_explore(const oracle_system* h, int64_t F0, const int32_t* level0, in
   // Level 0 (reading A20): every distinct configuration of level0, in order.
   run.level_offsets.push_back(0);
   for (int64_t i = 0; i < F0; ++i) {
-    std::vector<int64_t> C(level0 + i * s.m, level0 + (i + 1) * s.m);
+    std::vector<int64_t> C(level0 + i * width, level0 + (i + 1) * width);
     for (int64_t v : C)
       if (v < 0 || v > cmax) { run.status = OR_E_OVERFLOW; run.error = "level 0 count out of range"; return run.status; }
     auto f = fingerprint(C, seed0, seed1);
@@ -382,7 +401,8 @@ int oracle_explore(const oracle_system* h, int64_t F0, const int32_t* level0, in
     std::set<std::pair<uint64_t, uint64_t>> level_fp;
     int64_t T = 0;
     for (int64_t i = lo; i < hi; ++i) {
-      const std::vector<int64_t> C = run.configs[i];
+      const std::vector<int64_t> Caug = run.configs[i];
+      const std::vector<int64_t> C(Caug.begin(), Caug.begin() + s.m);
       auto A = applicable_rules_per_neuron(s, C);
       uint64_t psi = 0;
       if (!count_children(A, &psi)) { run.status = OR_E_CAPACITY; run.error = "psi above 2^62"; return run.status; }
@@ -391,6 +411,15 @@ int oracle_explore(const oracle_system* h, int64_t F0, const int32_t* level0, in
         if (max_transitions > 0 && T > max_transitions) { run.status = OR_E_CAPACITY; run.error = "transition budget exceeded"; return run.status; }
         auto S = spiking_vector(s, A, t);
         auto Cn = transition(s, C, S);
+        if (gen) {  // NEXT-1: the augmented column
+          const int64_t a = Caug[s.m];
+          const bool fired = S[out_rule] != 0;
+          if (a >= 1 && fired) {  // second output spike: the number a is generated
+            run.numbers.insert(a);
+            continue;
+          }
+          Cn.push_back(a == 0 ? (fired ? 1 : 0) : a + 1);
+        }
         auto f = fingerprint(Cn, seed0, seed1);
         if (seen(Cn, f)) continue;  // produced at an earlier level (A6)
         bool dup_here = dedup == 0 ? !level_rows.insert(Cn).second : !level_fp.insert(f).second;
@@ -421,7 +450,8 @@ int oracle_explore(const oracle_system* h, int64_t F0, const int32_t* level0, in
   // Halting classification of every configuration (reading A5).
   run.halting.resize(run.configs.size());
   for (size_t i = 0; i < run.configs.size(); ++i) {
-    auto A = applicable_rules_per_neuron(s, run.configs[i]);
+    const std::vector<int64_t> C(run.configs[i].begin(), run.configs[i].begin() + s.m);
+    auto A = applicable_rules_per_neuron(s, C);
     bool any = false;
     for (const auto& As : A) any = any || !As.empty();
     run.halting[i] = any ? 0 : 1;
@@ -429,6 +459,15 @@ int oracle_explore(const oracle_system* h, int64_t F0, const int32_t* level0, in
   return OR_OK;
 }
 
+int oracle_explore(const oracle_system* h, int64_t F0, const int32_t* level0, int32_t depth,
+                   int32_t dedup, int32_t count_bits, int64_t frontier_target,
+                   int64_t max_transitions, uint64_t seed0, uint64_t seed1, oracle_run** out) {
+  return oracle_explore_gen(h, F0, level0, depth, dedup, count_bits, frontier_target, max_transitions, seed0,
+                            seed1, -1, out);
+}
+
+int64_t oracle_run_num_numbers(const oracle_run* h) { return (int64_t)h->r.numbers.size(); }
+void oracle_run_numbers(const oracle_run* h, int64_t* out) { std::copy(h->r.numbers.begin(), h->r.numbers.end(), out); }
 int oracle_run_status(const oracle_run* h) { return h->r.status; }
 const char* oracle_run_error(const oracle_run* h) { return h->r.error.c_str(); }
 int64_t oracle_run_num_configs(const oracle_run* h) { return (int64_t)h->r.configs.size(); }
