@@ -91,8 +91,24 @@ typedef struct {
   int64_t max_transitions;   /* per-level budget on T; 0 = unlimited                        */
   uint64_t fp_seed[2];       /* fingerprint seeds (reading A18)                             */
   int32_t keep_tree;         /* 1 = retain every level's configurations for snp_tree_configs */
-  int32_t reserved;
+  int32_t out_rule1;         /* 0 = off.  r + 1: generated numbers with
+                                rule r of the output neuron (PAPER.md:89 `out`) as its spiking
+                                rule — see "Generated numbers" below                          */
 } snp_options;
+
+/* Generated numbers (Π "generates all numbers in N - {1}"; the
+ * generated set "is the result of the computation").  The number a computation
+ * generates is the count of steps between the first two output spikes; an
+ * output spike at step k is rule out_rule1 - 1 firing in S_k.  With out_rule1 >
+ * 0 the engine explores the AUGMENTED state (C, A): every configuration has
+ * snp_state_width = m + 1 entries, the last one A = 0 before the first output
+ * spike, else the number of steps since it.  A transition from (C, A) by S:
+ *   - A >= 1 and S fires the output rule: the number A is generated and the
+ *     computation ends (the transition counts in T, its child is not stored);
+ *   - otherwise the child is (C + S·M, A == 0 ? [output rule fires] : A + 1).
+ * Dedup, thinning and halting act on the augmented state; C0 (snp_load) has m
+ * entries (A = 0 is appended); level0 rows (snp_begin) have m + 1 columns.
+ * Multi-GPU (snp_dist_*) is not available in this mode (SNP_E_STATE).         */
 
 /* A batch of configurations (a frontier).  elem_bytes ∈ {1, 2, 4} (unsigned
  * for 1/2, int32 for 4).  layout ROW_MAJOR: n_configs rows of n_neurons counts
@@ -145,6 +161,12 @@ snp_status snp_set_stream(snp_system *sys, void *cuda_stream);
 snp_status snp_begin(snp_system *sys, const snp_configs *level0);
 snp_status snp_advance(snp_system *sys, snp_level_counters *counters);
 int64_t    snp_frontier_size(const snp_system *sys);
+/* Entries per configuration: m, or m + 1 with generated numbers (out_rule1 > 0). */
+int64_t    snp_state_width(const snp_system *sys);
+/* Numbers generated since the last snp_begin (out_rule1 > 0): bit k of
+ * words[k / 64] set iff k was generated, for k < 64 · n_words;
+ * *max_number = the largest one (-1 if none).  Any pointer may be NULL.      */
+snp_status snp_generated_numbers(snp_system *sys, uint64_t *words, int64_t n_words, int64_t *max_number);
 int32_t    snp_depth(const snp_system *sys);
 /* Summary of the exploration so far: total configurations, total transitions,
  * and an order-sensitive digest of (level, index, parent, t, fingerprint) of

@@ -79,7 +79,9 @@ enum : uint32_t { TE_EMIT = 1u, TE_ND = 2u, TE_F = 0xF0u };
 enum : int32_t { KF_EXPAND_T = 1, KF_KC_GLOBAL_E = 2 };
 
 __device__ __forceinline__ uint32_t table_index(uint32_t v, const NeuronMeta& mt) {
-  if ((int32_t)v < mt.L) return v;
+  // unsigned compare: lanes past F in a partial block may hold any bit
+  // pattern (a negative int32 must still land inside the table)
+  if (v < (uint32_t)mt.L) return v;
   uint32_t d = v - (uint32_t)mt.L;
   return (uint32_t)mt.L + (mt.pm >= 0 ? (d & (uint32_t)mt.pm) : d % (uint32_t)(-mt.pm));
 }
@@ -119,7 +121,15 @@ struct SysView {
   const uint8_t* hsg;        // m × 256    (count_bits == 8) 16-B fingerprint delta per first-rule slot
   int32_t any_generic;       // some neuron has no table
   int32_t kernel_flags;      // KF_* (SNP_KERNELS environment variable at snp_load; tuning/tests)
+  // generated numbers (include/snp.h): the augmented
+  // column A is neuron m - 1 (no rule, no synapse); aug_rule = -1 when off
+  int32_t aug_rule;          // output neuron's spiking rule
+  int32_t aug_neuron;        // its neuron
+  unsigned long long* gen_bits;  // generated-number bitmap
+  int64_t gen_cap_bits;
 };
+// key of a terminal child (second output spike): skipped by the dedup
+constexpr uint64_t KEY_TERMINAL1 = ~0ULL - 1;
 
 // 128-bit hash slot. key (k0,k1) = 128-bit fingerprint; EMPTY/EMPTY = free.
 struct alignas(16) Key128 {

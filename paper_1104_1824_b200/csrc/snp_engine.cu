@@ -207,6 +207,7 @@ struct snp_system {
   DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab, d_elut, d_hsg;
   DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
   DBuf counters_dev;  // [0] err, [1..] u64 counters
+  DBuf gen;           // generated-number bitmap (out_rule1 > 0)
   std::vector<DBuf> spare;  // released level buffers kept for reuse
   Arena arena;              // per-level metadata
   // multi-GPU exploration (snp_dist_*): this rank's share of the frontier and
@@ -674,6 +675,8 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     // memory even when they fit in shared memory (the large-m path)
     const char* k = getenv("SNP_KERNELS");
     v.kernel_flags = 0;
+    v.aug_rule = -1;  // set by snp_load after the tables are built
+    v.aug_neuron = -1;
     if (k && strstr(k, "expand_t")) v.kernel_flags |= KF_EXPAND_T;
     if (k && strstr(k, "kc_global_e")) v.kernel_flags |= KF_KC_GLOBAL_E;
   }
@@ -921,6 +924,7 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     phase_begin(s, 1);
     launch_child_parent(off, F, C.cpar, st);
     launch_child_keys(s->view, off, O, T, C, st);
+    if (s->view.aug_rule >= 0) launch_aug_keys(s->view, s->bytes, LV, off, O, T, C, err, st);
     phase_end(s);
     phase_begin(s, 2);
     launch_dedup(C, T, tag_base, tb, 1, err, st);
@@ -984,6 +988,7 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
         phase_end(s);
         CUDA_TRY(cudaGetLastError());
       }
+      if (s->view.aug_rule >= 0) launch_aug_fix(s->view, s->bytes, LV, O, N, K, err, st);
       launch_digest(N, K, (uint64_t)s->levels.size(), 0, 0, &dc(s)->digest, st);
     }
     if (s->opt.dedup == 0) {
@@ -1107,13 +1112,53 @@ snp_status snp_load(const snp_matrix* M, const snp_rule* rules, int64_t n_rules,
     cudaGetLastError();
     return fail(SNP_E_CUDA, "no CUDA device: the engine has no CPU fallback");
   }
+  // generated numbers (include/snp.h): the state gains column m = A, a neuron
+  // with no rule and no synapse whose value the engine sets (k_aug_keys,
+  // k_aug_fix); M and C0 are widened by one zero column
+  const int32_t out_rule = o.out_rule1 - 1;
+  if (o.out_rule1 < 0 || out_rule >= n_rules) return fail(SNP_E_ARG, "out_rule1 must be 0 (off) or 1..n_rules");
+  snp_matrix Maug{};
+  std::vector<int64_t> arp;
+  std::vector<int32_t> acol, aval, aC0;
+  if (out_rule >= 0) {
+    arp.push_back(0);
+    for (int64_t r = 0; r < n_rules; ++r) {
+      if (M->dense) {
+        for (int64_t j = 0; j < m; ++j)
+          if (M->dense[r * m + j]) { acol.push_back((int32_t)j); aval.push_back(M->dense[r * m + j]); }
+      } else {
+        for (int64_t e = M->row_ptr[r]; e < M->row_ptr[r + 1]; ++e) {
+          if (M->col[e] < 0 || M->col[e] >= m) return fail(SNP_E_INVALID_SYSTEM, "M row %lld: column out of range", (long long)r);
+          acol.push_back(M->col[e]);
+          aval.push_back(M->val[e]);
+        }
+      }
+      arp.push_back((int64_t)acol.size());
+    }
+    acol.push_back(0);  // keep data() non-null
+    aval.push_back(0);
+    Maug = snp_matrix{n_rules, m + 1, nullptr, arp.data(), acol.data(), aval.data()};
+    aC0.assign(C0, C0 + m);
+    aC0.push_back(0);
+  }
   auto s = std::make_unique<snp_system>();
-  s->m = m;
+  s->m = out_rule >= 0 ? m + 1 : m;
   s->opt = o;
   s->bytes = o.count_bits / 8;
   s->count_max = o.count_bits == 8 ? 255 : o.count_bits == 16 ? 65535 : 0x7FFFFFFF;
-  snp_status st = load_impl(s.get(), M, rules, n_rules, C0);
+  snp_status st = out_rule >= 0 ? load_impl(s.get(), &Maug, rules, n_rules, aC0.data())
+                                : load_impl(s.get(), M, rules, n_rules, C0);
   if (st != SNP_OK) return st;
+  s->view.aug_rule = out_rule;
+  s->view.aug_neuron = out_rule >= 0 ? rules[out_rule].neuron : -1;
+  s->view.gen_bits = nullptr;
+  s->view.gen_cap_bits = 0;
+  if (out_rule >= 0) {
+    s->view.gen_cap_bits = 1 << 20;
+    SNP_TRY(s->gen.ensure((size_t)s->view.gen_cap_bits / 8, false));
+    CUDA_TRY(cudaMemset(s->gen.p, 0, (size_t)s->view.gen_cap_bits / 8));
+    s->view.gen_bits = s->gen.as<unsigned long long>();
+  }
   *out = s.release();
   return SNP_OK;
 }
@@ -1146,6 +1191,11 @@ snp_status snp_set_stream(snp_system* s, void* stream) {
 
 snp_status snp_begin(snp_system* s, const snp_configs* level0) {
   if (!s) return fail(SNP_E_ARG, "NULL system");
+  if (s->view.gen_bits) {
+    snp_status z = cudaMemsetAsync(s->view.gen_bits, 0, (size_t)s->view.gen_cap_bits / 8, s->stream) == cudaSuccess
+                       ? SNP_OK : fail(SNP_E_CUDA, "clearing the generated-number bitmap failed");
+    if (z != SNP_OK) return z;
+  }
   snp_status st = begin_impl(s, level0);
   if (st != SNP_OK) s->begun = false;
   return st;
@@ -1160,6 +1210,25 @@ snp_status snp_advance(snp_system* s, snp_level_counters* counters) {
 }
 
 int64_t snp_frontier_size(const snp_system* s) { return (s && !s->levels.empty()) ? s->levels.back()->F : 0; }
+int64_t snp_state_width(const snp_system* s) { return s ? s->m : 0; }
+
+snp_status snp_generated_numbers(snp_system* s, uint64_t* words, int64_t n_words, int64_t* max_number) {
+  if (!s || n_words < 0) return fail(SNP_E_ARG, "snp_generated_numbers: bad arguments");
+  const int64_t nw = s->view.gen_cap_bits / 64;
+  std::vector<uint64_t> h((size_t)nw, 0);
+  if (nw) {
+    CUDA_TRY(cudaMemcpyAsync(h.data(), s->view.gen_bits, (size_t)nw * 8, cudaMemcpyDeviceToHost, s->stream));
+    SNP_TRY(sync(s));
+  }
+  if (words)
+    for (int64_t i = 0; i < n_words; ++i) words[i] = i < nw ? h[(size_t)i] : 0;
+  if (max_number) {
+    *max_number = -1;
+    for (int64_t i = nw - 1; i >= 0 && *max_number < 0; --i)
+      if (h[(size_t)i]) *max_number = i * 64 + 63 - __builtin_clzll(h[(size_t)i]);
+  }
+  return SNP_OK;
+}
 int32_t snp_depth(const snp_system* s) { return s ? (int32_t)s->levels.size() - 1 : -1; }
 
 snp_status snp_summary(const snp_system* s, int64_t* n_configs, int64_t* transitions, uint64_t* digest) {
@@ -1343,6 +1412,7 @@ extern "C" {
 snp_status snp_dist_begin(snp_system* s, const snp_configs* level0, int32_t nranks, int64_t* n_local) {
   if (!s || !level0 || nranks < 1) return fail(SNP_E_ARG, "snp_dist_begin: bad arguments");
   if (s->opt.dedup != 1) return fail(SNP_E_STATE, "distributed exploration needs dedup = 1 (fingerprint keys)");
+  if (s->view.aug_rule >= 0) return fail(SNP_E_STATE, "distributed exploration does not support generated numbers");
   const int64_t F0 = level0->n_configs, m = s->m;
   if (F0 < 0 || F0 > 0x7FFFFFFFLL || (F0 > 0 && !level0->data)) return fail(SNP_E_ARG, "level0: bad n_configs / data");
   if (level0->elem_bytes != 1 && level0->elem_bytes != 2 && level0->elem_bytes != 4) return fail(SNP_E_ARG, "level0: elem_bytes");

@@ -77,6 +77,12 @@ void launch_fingerprint(const SysView& S, int32_t bytes, const void* data, int64
                         cudaStream_t st);
 void launch_expand(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, cudaStream_t st);
 void launch_child_parent(const uint64_t* off, int64_t F, uint32_t* cpar, cudaStream_t st);
+// generated numbers (SysView::aug_rule >= 0): child keys get the augmented
+// column's change, terminal children a skip key; kept children get A'
+void launch_aug_keys(const SysView& S, int32_t bytes, const LevelView& L, const uint64_t* off, const ExpandOut& O,
+                     uint64_t T, const ChildArrays& C, int32_t* err, cudaStream_t st);
+void launch_aug_fix(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const NextArrays& N,
+                    int64_t K, int32_t* err, cudaStream_t st);
 void launch_child_keys(const SysView& S, const uint64_t* off, const ExpandOut& O, uint64_t T, const ChildArrays& C,
                        cudaStream_t st);
 void launch_dedup(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, int use_visited, int32_t* err,

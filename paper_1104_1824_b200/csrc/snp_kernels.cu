@@ -92,10 +92,28 @@ __device__ int fired_rule(const SysView& S, int32_t s, int32_t v, const ChildCtx
   return nth_applicable(S, s, v, x);
 }
 
+// Generated numbers (include/snp.h): the augmented
+// column A (neuron m - 1) of the child.  The output spike is the output
+// rule firing in the child's spiking vector; A >= 1 and a spike = second
+// output spike: *number = A and the child is terminal; else
+// A' = (A == 0 ? [spike] : A + 1) and *number = -1.
+template <typename T>
+__device__ int64_t aug_child(const SysView& S, const void* data, int64_t p, const ChildCtx& cx, int64_t* number) {
+  const int64_t a = ld_count<T>(data, p, S.m - 1, S.m);
+  const int32_t v = ld_count<T>(data, p, S.aug_neuron, S.m);
+  const bool spike = fired_rule(S, S.aug_neuron, v, cx) == S.aug_rule;
+  *number = (a >= 1 && spike) ? a : -1;
+  return a == 0 ? (spike ? 1 : 0) : a + 1;
+}
+
 // Exact value of the child at neuron j: eq. (2) restricted to column j,
 // C'[j] = C[j] - c_{fired(j)} + Σ_{s ∈ in(j)} p_{fired(s)}  (Def. 2).
 template <typename T>
 __device__ int64_t exact_value(const SysView& S, const void* data, int64_t p, int32_t j, const ChildCtx& cx) {
+  if (S.aug_rule >= 0 && j == S.m - 1) {
+    int64_t number;
+    return aug_child<T>(S, data, p, cx, &number);
+  }
   int32_t vj = ld_count<T>(data, p, j, S.m);
   int rj = fired_rule(S, j, vj, cx);
   int64_t val = (int64_t)vj - (rj >= 0 ? S.rules[rj].c : 0);
@@ -865,6 +883,45 @@ __global__ void k_child_keys(SysView S, const uint64_t* off, ExpandOut O, uint64
   }
 }
 
+// Generated numbers: the child key gets (A' - A)·R_ℓ[m-1] (linearity,
+// reading A18); a terminal child records its number and gets the skip key.
+template <typename T>
+__global__ void k_aug_keys(SysView S, LevelView L, const uint64_t* off, ExpandOut O, uint64_t T_, ChildArrays C,
+                           int32_t* err) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T_; c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = C.cpar[c];
+    ChildCtx cx;
+    decode_child(S, O.nd + (uint64_t)p * KMAX, O.ndc[p], c - off[p], cx);
+    int64_t number;
+    const int64_t a2 = aug_child<T>(S, L.data, p, cx, &number);
+    if (number >= 0) {
+      if (number < S.gen_cap_bits) atomicOr(S.gen_bits + (number >> 6), 1ULL << (number & 63));
+      else atomicOr(err, ERR_CAPACITY);
+      C.cfp0[c] = EMPTY;
+      C.cfp1[c] = KEY_TERMINAL1;
+    } else {
+      const uint64_t d = (uint64_t)(a2 - (int64_t)ld_count<T>(L.data, p, S.m - 1, S.m));
+      C.cfp0[c] += d * __ldg(S.R0 + S.m - 1);
+      C.cfp1[c] += d * __ldg(S.R1 + S.m - 1);
+    }
+  }
+}
+
+// Generated numbers: A' of every kept child (after K-c, which copies A).
+template <typename T>
+__global__ void k_aug_fix(SysView S, LevelView L, ExpandOut O, NextArrays N, int64_t K, int32_t* err) {
+  T* out = reinterpret_cast<T*>(N.data);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < K; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = N.parent[q];
+    ChildCtx cx;
+    decode_child(S, O.nd + (uint64_t)p * KMAX, O.ndc[p], N.t[q], cx);
+    int64_t number;
+    const int64_t a2 = aug_child<T>(S, L.data, p, cx, &number);
+    if (a2 > S.count_max) atomicOr(err, ERR_OVERFLOW);
+    out[eidx(q, S.m - 1, S.m)] = (T)a2;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K-d: dedup against visited + same-level minimum tag
 // ---------------------------------------------------------------------------
@@ -873,6 +930,11 @@ __device__ __forceinline__ Key128 ld_key(const Slot* s) { return *reinterpret_ca
 __global__ void k_dedup(ChildArrays C, uint64_t T, uint64_t tag_base, Tables tb, int use_visited, int32_t* err) {
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T; c += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k0 = C.cfp0[c], k1 = C.cfp1[c];
+    if (k0 == EMPTY && k1 == KEY_TERMINAL1) {  // generated numbers: terminal child (never stored)
+      C.verdict[c] = 0;
+      C.cref[c] = EMPTY;
+      continue;
+    }
     if (k0 == EMPTY && k1 == EMPTY) {
       atomicOr(err, ERR_COLLISION);
       C.verdict[c] = 0;
@@ -1900,6 +1962,26 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
       k_materialize_exact<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
     });
   }
+  count_launch();
+}
+
+void launch_aug_keys(const SysView& S, int32_t bytes, const LevelView& L, const uint64_t* off, const ExpandOut& O,
+                     uint64_t T, const ChildArrays& C, int32_t* err, cudaStream_t st) {
+  if (T == 0) return;
+  dispatch_bytes(bytes, [&](auto tt) {
+    using TT = decltype(tt);
+    k_aug_keys<TT><<<grid_for(T, 128), 128, 0, st>>>(S, L, off, O, T, C, err);
+  });
+  count_launch();
+}
+
+void launch_aug_fix(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const NextArrays& N,
+                    int64_t K, int32_t* err, cudaStream_t st) {
+  if (K <= 0) return;
+  dispatch_bytes(bytes, [&](auto tt) {
+    using TT = decltype(tt);
+    k_aug_fix<TT><<<grid_for(K, 128), 128, 0, st>>>(S, L, O, N, K, err);
+  });
   count_launch();
 }
 

@@ -34,7 +34,8 @@ SNP_LAYOUT_NEURON_MAJOR = 1
 
 EXPORTED = [
     "snp_abi_version", "snp_last_error", "snp_load", "snp_system_free", "snp_set_stream", "snp_begin",
-    "snp_advance", "snp_frontier_size", "snp_depth", "snp_summary", "snp_explore", "snp_step",
+    "snp_advance", "snp_frontier_size", "snp_state_width", "snp_generated_numbers", "snp_depth", "snp_summary",
+    "snp_explore", "snp_step",
     "snp_tree_num_levels", "snp_tree_num_configs", "snp_tree_level_offsets", "snp_tree_configs",
     "snp_tree_edges", "snp_tree_counters", "snp_tree_spiking_vectors", "snp_tree_free",
     "snp_level_size", "snp_level_edges", "snp_level_columns", "snp_set_profiling", "snp_profile",
@@ -58,7 +59,7 @@ class snp_matrix(ctypes.Structure):
 class snp_options(ctypes.Structure):
     _fields_ = [("count_bits", ctypes.c_int32), ("dedup", ctypes.c_int32), ("frontier_target", ctypes.c_int64),
                 ("max_transitions", ctypes.c_int64), ("fp_seed", ctypes.c_uint64 * 2),
-                ("keep_tree", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("keep_tree", ctypes.c_int32), ("out_rule1", ctypes.c_int32)]
 
 
 class snp_configs(ctypes.Structure):
@@ -106,6 +107,9 @@ def lib() -> ctypes.CDLL:
         L.snp_advance.argtypes = [_P, ctypes.POINTER(snp_level_counters)]
         L.snp_frontier_size.argtypes = [_P]
         L.snp_frontier_size.restype = ctypes.c_int64
+        L.snp_state_width.argtypes = [_P]
+        L.snp_state_width.restype = ctypes.c_int64
+        L.snp_generated_numbers.argtypes = [_P, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
         L.snp_depth.argtypes = [_P]
         L.snp_depth.restype = ctypes.c_int32
         L.snp_summary.argtypes = [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
@@ -157,7 +161,7 @@ def _ptr(a: np.ndarray):
 # ---- C-named entry points (marshalling only) --------------------------------
 def snp_load(rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.ndarray, C0: np.ndarray,
              count_bits=32, dedup=0, frontier_target=0, max_transitions=0, fp_seed=(0x5EED0, 0x5EED1),
-             keep_tree=1):
+             keep_tree=1, out_rule=None):
     rules = np.ascontiguousarray(rules, np.int32).reshape(-1, 6)
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col = np.ascontiguousarray(col, np.int32)
@@ -165,7 +169,7 @@ def snp_load(rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.nd
     C0 = np.ascontiguousarray(C0, np.int32)
     M = snp_matrix(rules.shape[0], C0.shape[0], None, _ptr(row_ptr).value, _ptr(col).value, _ptr(val).value)
     o = snp_options(count_bits, dedup, frontier_target, max_transitions, (ctypes.c_uint64 * 2)(*fp_seed),
-                    keep_tree, 0)
+                    keep_tree, 0 if out_rule is None else int(out_rule) + 1)
     h = _P()
     _check(lib().snp_load(ctypes.byref(M), _ptr(rules), rules.shape[0], _ptr(C0), C0.shape[0], ctypes.byref(o),
                           ctypes.byref(h)))
@@ -189,13 +193,27 @@ class System:
     """Owning wrapper of an ``snp_system*``."""
 
     def __init__(self, workload, count_bits=32, dedup=0, frontier_target=0, max_transitions=0,
-                 fp_seed=(0x5EED0, 0x5EED1), keep_tree=1):
+                 fp_seed=(0x5EED0, 0x5EED1), keep_tree=1, out_rule=None):
+        """out_rule: generated numbers (include/snp.h) with that output rule;
+        configurations then have ``width = m + 1`` entries (last = A)."""
         self.m = int(workload.m)
         self.n = int(workload.rules.shape[0])
         self.count_bits = count_bits
         self._h = None
         self._h = snp_load(workload.rules, workload.row_ptr, workload.col, workload.val, workload.C0,
-                           count_bits, dedup, frontier_target, max_transitions, fp_seed, keep_tree)
+                           count_bits, dedup, frontier_target, max_transitions, fp_seed, keep_tree, out_rule)
+        self.width = int(lib().snp_state_width(self._h))
+
+    def generated_numbers(self) -> set:
+        """snp_generated_numbers: the numbers generated since the last begin."""
+        mx = ctypes.c_int64(-1)
+        _check(lib().snp_generated_numbers(self._h, None, 0, ctypes.byref(mx)))
+        if mx.value < 0:
+            return set()
+        words = np.zeros(mx.value // 64 + 1, np.uint64)
+        _check(lib().snp_generated_numbers(self._h, _ptr(words), words.shape[0], None))
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")
+        return set(int(i) for i in np.nonzero(bits)[0])
 
     def close(self):
         if self._h:
@@ -217,8 +235,15 @@ class System:
         elif isinstance(level0, snp_configs):
             _check(lib().snp_begin(self._h, ctypes.byref(level0)))
         else:
-            c, keep = configs_from_host(level0)
+            c, keep = configs_from_host(self._widen(level0))
             _check(lib().snp_begin(self._h, ctypes.byref(c)))
+
+    def _widen(self, rows):
+        """Generated-numbers mode: rows of m counts get A = 0 appended."""
+        rows = np.atleast_2d(rows)
+        if self.width == self.m + 1 and rows.shape[1] == self.m:
+            rows = np.hstack([rows, np.zeros((rows.shape[0], 1), rows.dtype)])
+        return rows
 
     def advance(self) -> dict:
         lc = snp_level_counters()
@@ -262,7 +287,7 @@ class System:
 
     def level_columns(self, L: int, idx) -> np.ndarray:
         idx = np.ascontiguousarray(idx, np.int64)
-        out = np.zeros((idx.shape[0], self.m), np.int32)
+        out = np.zeros((idx.shape[0], self.width), np.int32)
         _check(lib().snp_level_columns(self._h, L, _ptr(idx), idx.shape[0], _ptr(out)))
         return out
 
@@ -273,13 +298,13 @@ class System:
         elif isinstance(level0, snp_configs):
             _check(lib().snp_explore(self._h, ctypes.byref(level0), depth, ctypes.byref(h)))
         else:
-            c, keep = configs_from_host(level0)
+            c, keep = configs_from_host(self._widen(level0))
             _check(lib().snp_explore(self._h, ctypes.byref(c), depth, ctypes.byref(h)))
         return Tree(self, h)
 
     def step(self, frontier) -> "Tree":
         h = _P()
-        c, keep = configs_from_host(frontier)
+        c, keep = configs_from_host(self._widen(frontier))
         _check(lib().snp_step(self._h, ctypes.byref(c), ctypes.byref(h)))
         return Tree(self, h)
 
@@ -325,7 +350,7 @@ class Tree:
     @property
     def configs(self) -> np.ndarray:
         if self._configs is None:
-            out = np.zeros((self.num_configs, self.sys.m), np.int32)
+            out = np.zeros((self.num_configs, self.sys.width), np.int32)
             _check(lib().snp_tree_configs(self._h, _ptr(out)))
             self._configs = out
         return self._configs
