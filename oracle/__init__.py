@@ -57,6 +57,8 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(build())
         L.oracle_load.argtypes = [_I64, _I64, _P, _P, _P, _P, ctypes.POINTER(_P), ctypes.c_char_p, _I64]
         L.oracle_load.restype = ctypes.c_int
+        L.oracle_load_unary.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, ctypes.POINTER(_P), ctypes.c_char_p, _I64]
+        L.oracle_load_unary.restype = ctypes.c_int
         L.oracle_free.argtypes = [_P]
         L.oracle_applicability.argtypes = [_P, _P, _P, _P]
         L.oracle_children.argtypes = [_P, _P, _I64, _P, _P, ctypes.POINTER(_U64)]
@@ -102,7 +104,9 @@ class OracleError(RuntimeError):
 class System:
     """An SNP system loaded into the oracle (rules n×6 int32, M as CSR)."""
 
-    def __init__(self, m: int, rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.ndarray):
+    def __init__(self, m: int, rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.ndarray,
+                 re_bits: np.ndarray | None = None):
+        """re_bits: n × 4 uint64 membership rows of UNARY rules (kind 2), or None."""
         self.m = int(m)
         self.rules = np.ascontiguousarray(rules, dtype=np.int32).reshape(-1, 6)
         self.n = self.rules.shape[0]
@@ -110,8 +114,10 @@ class System:
                       np.ascontiguousarray(val, dtype=np.int32))
         h = _P()
         err = ctypes.create_string_buffer(256)
-        st = lib().oracle_load(self.m, self.n, _ptr(self.rules), _ptr(self._keep[0]), _ptr(self._keep[1]),
-                               _ptr(self._keep[2]), ctypes.byref(h), err, 256)
+        self._bits = None if re_bits is None else np.ascontiguousarray(re_bits, dtype=np.uint64).reshape(-1, 4)
+        st = lib().oracle_load_unary(self.m, self.n, _ptr(self.rules),
+                                     None if self._bits is None else _ptr(self._bits), _ptr(self._keep[0]),
+                                     _ptr(self._keep[1]), _ptr(self._keep[2]), ctypes.byref(h), err, 256)
         if st != OR_OK:
             raise OracleError(st, err.value.decode())
         self._h = h
@@ -132,7 +138,7 @@ class System:
 
     @classmethod
     def from_workload(cls, w) -> "System":
-        return cls(w.m, w.rules, w.row_ptr, w.col, w.val)
+        return cls(w.m, w.rules, w.row_ptr, w.col, w.val, getattr(w, "re_bits", None))
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -26,10 +26,13 @@ def rule_applicable(rule, v: int) -> bool:
     return in_lang and v >= c
 
 
-def valid_spiking_vectors(rules, C):
-    """All valid S ∈ {0,1}^n for configuration C, as tuples (any order)."""
+def valid_spiking_vectors(rules, C, app_fn=None):
+    """All valid S ∈ {0,1}^n for configuration C, as tuples (any order).
+    app_fn(r, v): applicability of rule r at v spikes (default: the EXACT /
+    PERIODIC kinds above; tests pass Python-regex membership for UNARY)."""
     n = len(rules)
-    app = [rule_applicable(rules[r], C[int(rules[r][0])]) for r in range(n)]
+    app_fn = app_fn or (lambda r, v: rule_applicable(rules[r], v))
+    app = [app_fn(r, C[int(rules[r][0])]) for r in range(n)]
     neurons = sorted({int(r[0]) for r in rules})
     out = []
     for S in product((0, 1), repeat=n):
@@ -53,17 +56,18 @@ def apply(M, C, S):
     return tuple(C[j] + sum(S[r] * M[r][j] for r in range(len(S))) for j in range(m))
 
 
-def children(rules, M, C):
+def children(rules, M, C, app_fn=None):
     """All (S, C') pairs.  A halting configuration (no applicable rule) has no
     children: the all-zero vector would only reproduce C (reading A5,
     stopping criterion 1)."""
-    if is_halting(rules, C):
+    if is_halting(rules, C, app_fn):
         return []
-    return [(S, apply(M, C, S)) for S in valid_spiking_vectors(rules, C)]
+    return [(S, apply(M, C, S)) for S in valid_spiking_vectors(rules, C, app_fn)]
 
 
-def is_halting(rules, C) -> bool:
-    return not any(rule_applicable(r, C[int(r[0])]) for r in rules)
+def is_halting(rules, C, app_fn=None) -> bool:
+    app_fn = app_fn or (lambda r, v: rule_applicable(rules[r], v))
+    return not any(app_fn(r, C[int(rules[r][0])]) for r in range(len(rules)))
 
 
 def bfs_levels(rules, M, C0, depth: int):

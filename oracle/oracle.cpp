@@ -38,19 +38,25 @@ enum {
   OR_E_CAPACITY = -4,
 };
 
-enum { RE_EXACT = 0, RE_PERIODIC = 1 };
+enum { RE_EXACT = 0, RE_PERIODIC = 1, RE_UNARY = 2 };
 
 // One rule  E/a^c -> a^p  of neuron σ (Def. 1 (b-1)); p = 0 is a
 // forgetting rule ((b-2)).  The regular expression E is either
 //   EXACT(k)       E = a^k          (form (b-3))
 //   PERIODIC(i,j)  E = a^i (a^j)*   (the paper-simulator reading, A1)
+//   UNARY(t,P)     any regular E over {a} (the paper's
+//                  future work).  L(E) ⊆ a* is ultimately
+//                  periodic, so it is given by its membership bits
+//                  member[v] for v < t + P, with a^v ∈ L(E) for v >= t + P
+//                  iff member[t + (v - t) mod P].
 struct Rule {
   int64_t neuron;
   int64_t kind;
-  int64_t a;  // k (EXACT) or i (PERIODIC)
-  int64_t b;  // j (PERIODIC), unused for EXACT
+  int64_t a;  // k (EXACT), i (PERIODIC) or t (UNARY)
+  int64_t b;  // j (PERIODIC), P (UNARY), unused for EXACT
   int64_t consumed;  // c >= 1
   int64_t produced;  // p >= 0
+  std::vector<uint8_t> member;  // UNARY: t + P membership bits
 };
 
 struct System {
@@ -66,6 +72,7 @@ struct System {
 // a^v ∈ L(E)?  (regex kinds per reading A1)
 bool regex_matches(const Rule& r, int64_t v) {
   if (r.kind == RE_EXACT) return v == r.a;
+  if (r.kind == RE_UNARY) return r.member[v < r.a + r.b ? v : r.a + (v - r.a) % r.b] != 0;
   // PERIODIC(i, j): v = i + x·j for some x >= 0
   return v >= r.a && (v - r.a) % r.b == 0;
 }
@@ -185,7 +192,8 @@ std::string validate(const System& sys) {
     const Rule& R = sys.rules[r];
     if (R.neuron < 0 || R.neuron >= sys.m) { snprintf(buf, sizeof buf, "rule %lld: neuron out of range", (long long)r); return buf; }
     if (r > 0 && R.neuron < sys.rules[r - 1].neuron) { snprintf(buf, sizeof buf, "rule %lld: rules not grouped by neuron", (long long)r); return buf; }
-    if (R.kind != RE_EXACT && R.kind != RE_PERIODIC) { snprintf(buf, sizeof buf, "rule %lld: bad regex kind", (long long)r); return buf; }
+    if (R.kind != RE_EXACT && R.kind != RE_PERIODIC && R.kind != RE_UNARY) { snprintf(buf, sizeof buf, "rule %lld: bad regex kind", (long long)r); return buf; }
+    if (R.kind == RE_UNARY && (R.b < 1 || R.a + R.b > 256 || R.member.size() != (size_t)(R.a + R.b))) { snprintf(buf, sizeof buf, "rule %lld: unary regex needs P >= 1, t + P <= 256 and its bits", (long long)r); return buf; }
     if (R.consumed < 1) { snprintf(buf, sizeof buf, "rule %lld: c < 1", (long long)r); return buf; }
     if (R.produced < 0) { snprintf(buf, sizeof buf, "rule %lld: p < 0", (long long)r); return buf; }
     if (R.a < 0) { snprintf(buf, sizeof buf, "rule %lld: regex exponent < 0", (long long)r); return buf; }
@@ -249,9 +257,10 @@ extern "C" {
 struct oracle_system { System s; };
 struct oracle_run { Run r; };
 
-int oracle_load(int64_t m, int64_t n, const int32_t* rules6, const int64_t* row_ptr,
-                const int32_t* col, const int32_t* val, oracle_system** out, char* err,
-                int64_t errlen) {
+// re_bits (may be NULL): n × 4 words, bit v of rule r's row = a^v ∈ L(E_r)
+// for v < 256 (read for UNARY rules only, v < t + P).
+int oracle_load_unary(int64_t m, int64_t n, const int32_t* rules6, const uint64_t* re_bits, const int64_t* row_ptr,
+                      const int32_t* col, const int32_t* val, oracle_system** out, char* err, int64_t errlen) {
   if (!out || m < 1 || n < 0 || (n > 0 && (!rules6 || !row_ptr))) return OR_E_ARG;
   auto* h = new oracle_system();
   System& s = h->s;
@@ -261,7 +270,9 @@ int oracle_load(int64_t m, int64_t n, const int32_t* rules6, const int64_t* row_
   s.M_rows.resize(n);
   for (int64_t r = 0; r < n; ++r) {
     const int32_t* q = rules6 + 6 * r;
-    s.rules[r] = Rule{q[0], q[1], q[2], q[3], q[4], q[5]};
+    s.rules[r] = Rule{q[0], q[1], q[2], q[3], q[4], q[5], {}};
+    if (q[1] == RE_UNARY && re_bits && q[2] >= 0 && q[3] >= 1 && q[2] + q[3] <= 256)
+      for (int64_t v = 0; v < q[2] + q[3]; ++v) s.rules[r].member.push_back((re_bits[4 * r + v / 64] >> (v % 64)) & 1);
     for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) s.M_rows[r].push_back({col[e], val[e]});
   }
   std::string msg = validate(s);
@@ -272,6 +283,11 @@ int oracle_load(int64_t m, int64_t n, const int32_t* rules6, const int64_t* row_
   }
   *out = h;
   return OR_OK;
+}
+
+int oracle_load(int64_t m, int64_t n, const int32_t* rules6, const int64_t* row_ptr, const int32_t* col,
+                const int32_t* val, oracle_system** out, char* err, int64_t errlen) {
+  return oracle_load_unary(m, n, rules6, nullptr, row_ptr, col, val, out, err, errlen);
 }
 
 void oracle_free(oracle_system* h) { delete h; }

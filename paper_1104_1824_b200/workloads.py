@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-EXACT, PERIODIC = 0, 1
+EXACT, PERIODIC, UNARY = 0, 1, 2
 MASK64 = (1 << 64) - 1
 
 
@@ -42,6 +42,7 @@ class Workload:
     level0_range: np.ndarray     # int32 m: level-0 counts are U{0 .. range-1}
     synapses: list = field(default_factory=list)   # (s, j) pairs, 0-based
     meta: dict = field(default_factory=dict)
+    re_bits: np.ndarray | None = None  # uint64 n×4: membership rows of UNARY rules (kind 2)
 
     @property
     def n(self) -> int:
@@ -228,3 +229,130 @@ CONFIGS = {
     5: dict(kind="random", m=65536, k_nd=7, seed=5, F=10_000_000, depth=20, dedup=1, count_bits=8,
             frontier_target=10_000_000),
 }
+
+
+# ---------------------------------------------------------------------------
+# general unary regular expressions
+# ---------------------------------------------------------------------------
+def unary_lengths(regex: str, vmax: int) -> list:
+    """Membership of a^v (v < vmax) in L(regex) for the small grammar of
+    ``random_unary_regex`` (literal a^k, (?:xy), (?:x|y), (?:x)*), by the set
+    of achievable lengths — an input builder, no SNP arithmetic."""
+    def parse(i):
+        # returns (set of lengths, next index); grammar: seq of atoms
+        lens = {0}
+        while i < len(regex) and regex[i] not in "|)":
+            if regex[i] == "a":
+                lens = {x + 1 for x in lens if x + 1 < vmax}
+                i += 1
+            elif regex.startswith("(?:", i):
+                alts = set()
+                i += 3
+                while True:
+                    sub, i = parse(i)
+                    alts |= sub
+                    if regex[i] == "|":
+                        i += 1
+                        continue
+                    break
+                assert regex[i] == ")"
+                i += 1
+                if i < len(regex) and regex[i] == "*":
+                    i += 1
+                    star = {0}
+                    frontier = {0}
+                    while frontier:
+                        frontier = {x + y for x in frontier for y in alts if x + y < vmax} - star
+                        star |= frontier
+                    alts = star
+                lens = {x + y for x in lens for y in alts if x + y < vmax}
+            else:
+                raise ValueError(regex)
+        return lens, i
+
+    lens, i = parse(0)
+    assert i == len(regex)
+    return [v in lens for v in range(vmax)]
+
+
+def unary_bits_from_regex(regex: str, vmax: int = 600):
+    """(t, P, row) of the UNARY rule kind for a regular expression over {a}:
+    membership of a^v for v < vmax (``unary_lengths``), and (t, P) the
+    smallest threshold + period (t + P <= 256) from which the membership
+    sequence repeats through vmax.  row = 4 uint64, bit v = a^v ∈ L for
+    v < t + P.  An input builder only: no applicability is computed here."""
+    mem = unary_lengths(regex, vmax)
+    best = None
+    for P in range(1, 129):
+        for t in range(0, 257 - P):
+            if all(mem[v] == mem[v + P] for v in range(t, vmax - P)):
+                if best is None or t + P < best[0] + best[1]:
+                    best = (t, P)
+                break
+    if best is None:
+        raise ValueError(f"{regex!r}: no period <= 128 with t + P <= 256 found below {vmax}")
+    t, P = best
+    row = np.zeros(4, np.uint64)
+    for v in range(t + P):
+        if mem[v]:
+            row[v // 64] |= np.uint64(1) << np.uint64(v % 64)
+    return t, P, row
+
+
+def random_unary_regex(rng, depth: int = 3, star_ok: bool = True) -> str:
+    """A random regular expression over {a}: literals a^k, concatenation,
+    alternation and Kleene star (no star inside a star, so Python's backtracking
+    ``re`` engine stays fast on the test-side pin)."""
+    if depth == 0 or rng.random() < 0.3:
+        return "a" * int(rng.integers(0, 4))
+    op = int(rng.integers(0, 3 if star_ok else 2)) if star_ok else int(rng.integers(1, 3))
+    if op == 0:
+        return f"(?:{random_unary_regex(rng, depth - 1, False)})*"
+    x = random_unary_regex(rng, depth - 1, star_ok)
+    y = random_unary_regex(rng, depth - 1, star_ok)
+    return f"(?:{x}{y})" if op == 1 else f"(?:{x}|{y})"
+
+
+def tiny_unary_system(seed: int, m_max: int = 4, rules_max: int = 3, count_max: int = 8) -> Workload:
+    """Tiny random systems whose rules carry random unary regexes (kind UNARY);
+    meta["regex"][r] is rule r's expression (the pin: Python's re engine)."""
+    w = tiny_random_system(seed, m_max=m_max, rules_max=rules_max, count_max=count_max)
+    rng = np.random.Generator(np.random.PCG64(7_000_003 + seed))
+    rules = w.rules.copy()
+    bits = np.zeros((w.n, 4), np.uint64)
+    regexes = []
+    for r in range(w.n):
+        rx = random_unary_regex(rng)
+        t, P, row = unary_bits_from_regex(rx)
+        rules[r, 1], rules[r, 2], rules[r, 3] = UNARY, t, P
+        bits[r] = row
+        regexes.append(rx)
+    w.rules = rules
+    w.re_bits = bits
+    w.name = f"tiny-unary-{seed}"
+    w.meta = dict(w.meta, regex=regexes)
+    return w
+
+
+def as_unary(w: Workload) -> Workload:
+    """The same system with every EXACT / PERIODIC rule re-encoded as a UNARY
+    rule of the same language (a^k = threshold k+1, period 1, bit k;
+    a^i(a^j)* = threshold i, period j, bit i)."""
+    rules = w.rules.copy()
+    bits = np.zeros((w.n, 4), np.uint64)
+    for r in range(w.n):
+        kind, a, b = int(rules[r, 1]), int(rules[r, 2]), int(rules[r, 3])
+        if kind == EXACT:
+            t, P, members = a + 1, 1, [a]
+        elif kind == PERIODIC:
+            t, P, members = a, b, [a]
+        else:
+            continue
+        if t + P > 256:
+            raise ValueError("exponent too large for the UNARY encoding")
+        for v in members:
+            bits[r, v // 64] |= np.uint64(1) << np.uint64(v % 64)
+        rules[r, 1], rules[r, 2], rules[r, 3] = UNARY, t, P
+    return Workload(name=w.name + "-unary", m=w.m, rules=rules, row_ptr=w.row_ptr, col=w.col, val=w.val,
+                    C0=w.C0.copy(), level0_range=w.level0_range, synapses=w.synapses, meta=dict(w.meta),
+                    re_bits=bits)
