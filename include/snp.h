@@ -55,8 +55,14 @@ typedef enum {
 
 /* Regular-expression kinds of a rule's E (reading A1):
  *   SNP_RE_EXACT    E = a^a            (form (b-3)): n == a
- *   SNP_RE_PERIODIC E = a^a (a^b)*     (b >= 1):  n >= a && (n - a) % b == 0     */
-enum { SNP_RE_EXACT = 0, SNP_RE_PERIODIC = 1 };
+ *   SNP_RE_PERIODIC E = a^a (a^b)*     (b >= 1):  n >= a && (n - a) % b == 0
+ *   SNP_RE_UNARY    any regular E over {a} (the paper's
+ *                   future work).  L(E) ⊆ a* is ultimately
+ *                   periodic: with threshold t = a >= 0 and period P = b >= 1
+ *                   (t + P <= 256), a^n ∈ L(E) iff bit idx of the rule's
+ *                   256-bit membership row, idx = n < t + P ? n : t + (n - t) % P.
+ *                   The rows are passed to snp_load_unary (reading A24).      */
+enum { SNP_RE_EXACT = 0, SNP_RE_PERIODIC = 1, SNP_RE_UNARY = 2 };
 
 /* One rule E/a^c -> a^p of neuron `neuron`.  produced = 0 is a
  * forgetting rule (b-2).  Rules are given in the paper's total order and must be
@@ -148,6 +154,11 @@ const char *snp_last_error(void);
  * thinning, no budget, keep_tree 1).                                          */
 snp_status snp_load(const snp_matrix *M, const snp_rule *rules, int64_t n_rules, const int32_t *C0,
                     int64_t m, const snp_options *opt, snp_system **out);
+/* snp_load with general unary regexes: re_bits = n_rules × 4 uint64, row r =
+ * membership bits of rule r (bit v of word v / 64: a^v ∈ L(E_r), v < t + P);
+ * read for SNP_RE_UNARY rules only; may be NULL if there are none.           */
+snp_status snp_load_unary(const snp_matrix *M, const snp_rule *rules, int64_t n_rules, const uint64_t *re_bits,
+                          const int32_t *C0, int64_t m, const snp_options *opt, snp_system **out);
 void       snp_system_free(snp_system *sys);
 
 /* Launch all device work of `sys` on this cudaStream_t (NULL = library stream). */

@@ -44,15 +44,25 @@ __host__ __device__ __forceinline__ int64_t eidx(int64_t p, int32_t s, int32_t m
 //   a^v ∈ L(E) && v >= c   <=>   lo <= v <= hi  &&  (v - base) ≡ 0 (mod j)
 //   EXACT(k):      lo = max(k, c), hi = k,       base = k, j = 1
 //   PERIODIC(i,j): lo = max(i, c), hi = INT_MAX, base = i, j = j
+// or, for a general unary regex (UNARY(t, P)), a
+// membership test on the ultimately periodic bit row:
+//   lo = c, hi = INT_MAX, base = t, j = P, unary = 1,
+//   a^v ∈ L(E)  <=>  bit idx of bits, idx = v < t + P ? v : t + (v - t) mod P
 struct DevRule {
   int32_t lo, hi, base, j;
   int32_t jmask;  // j - 1 when j is a power of two, else -1
   int32_t c, p;   // consumed, produced
-  int32_t pad;
+  int32_t unary;  // 1: membership row below
+  uint64_t bits[4];
 };
 
 __device__ __forceinline__ bool rule_app(const DevRule& r, int32_t v) {
   if (v < r.lo || v > r.hi) return false;
+  if (r.unary) {
+    const uint32_t u = (uint32_t)v, t = (uint32_t)r.base, P = (uint32_t)r.j;
+    const uint32_t idx = u < t + P ? u : t + (u - t) % P;
+    return (r.bits[idx >> 6] >> (idx & 63)) & 1ULL;
+  }
   if (r.j == 1) return true;
   int32_t d = v - r.base;
   return r.jmask >= 0 ? ((d & r.jmask) == 0) : (d % r.j == 0);

@@ -459,7 +459,7 @@ snp_status update_stored_table(snp_system* s) {
 // validation + upload (snp_load)
 // ---------------------------------------------------------------------------
 snp_status validate_and_build(snp_system* s, const snp_matrix* M, const snp_rule* rules, int64_t n_rules,
-                              std::vector<std::vector<std::pair<int32_t, int32_t>>>* rows,
+                              const uint64_t* re_bits, std::vector<std::vector<std::pair<int32_t, int32_t>>>* rows,
                               std::vector<std::vector<int32_t>>* out_syn) {
   const int64_t m = s->m, n = n_rules;
   rows->assign(n, {});
@@ -467,7 +467,10 @@ snp_status validate_and_build(snp_system* s, const snp_matrix* M, const snp_rule
     const snp_rule& R = rules[r];
     if (R.neuron < 0 || R.neuron >= m) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: neuron out of range", (long long)r);
     if (r > 0 && R.neuron < rules[r - 1].neuron) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: rules not grouped by neuron", (long long)r);
-    if (R.kind != SNP_RE_EXACT && R.kind != SNP_RE_PERIODIC) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: bad regex kind", (long long)r);
+    if (R.kind != SNP_RE_EXACT && R.kind != SNP_RE_PERIODIC && R.kind != SNP_RE_UNARY)
+      return fail(SNP_E_INVALID_SYSTEM, "rule %lld: bad regex kind", (long long)r);
+    if (R.kind == SNP_RE_UNARY && (!re_bits || R.b < 1 || (int64_t)R.a + R.b > 256))
+      return fail(SNP_E_INVALID_SYSTEM, "rule %lld: unary regex needs P >= 1, t + P <= 256 and its bit row", (long long)r);
     if (R.consumed < 1) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: c < 1", (long long)r);
     if (R.produced < 0) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: p < 0", (long long)r);
     if (R.a < 0) return fail(SNP_E_INVALID_SYSTEM, "rule %lld: regex exponent < 0", (long long)r);
@@ -523,10 +526,11 @@ snp_status upload(snp_system* s, DBuf& b, const std::vector<U>& v) {
   return SNP_OK;
 }
 
-snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const int32_t* C0) {
+snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const uint64_t* re_bits,
+                     const int32_t* C0) {
   std::vector<std::vector<std::pair<int32_t, int32_t>>> rows;
   std::vector<std::vector<int32_t>> out_syn;
-  SNP_TRY(validate_and_build(s, M, rules, n_rules, &rows, &out_syn));
+  SNP_TRY(validate_and_build(s, M, rules, n_rules, re_bits, &rows, &out_syn));
   const int64_t m = s->m, n = n_rules;
   s->n = n;
   for (int64_t j = 0; j < m; ++j)
@@ -547,6 +551,14 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
       d.hi = R.a;
       d.base = R.a;
       d.j = 1;
+    } else if (R.kind == SNP_RE_UNARY) {
+      d.lo = R.consumed;
+      d.hi = 0x7FFFFFFF;
+      d.base = R.a;
+      d.j = R.b;
+      d.unary = 1;
+      for (int64_t v = 0; v < (int64_t)R.a + R.b; ++v)
+        if ((re_bits[4 * r + v / 64] >> (v % 64)) & 1ULL) d.bits[v / 64] |= 1ULL << (v % 64);
     } else {
       d.lo = std::max(R.a, R.consumed);
       d.hi = 0x7FFFFFFF;
@@ -625,6 +637,11 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
       const snp_rule& R = rules[r];
       if (R.kind == SNP_RE_EXACT) {
         L = std::max<int64_t>(L, (int64_t)R.a + 1);
+      } else if (R.kind == SNP_RE_UNARY) {  // membership repeats with period P from t on
+        L = std::max<int64_t>(L, std::max<int64_t>(R.a, R.consumed));
+        const int64_t g = std::__gcd<int64_t>(P, R.b);
+        P = P / g * R.b;
+        if (P > TABW_MAX) ok = false;
       } else {
         L = std::max<int64_t>(L, std::max<int64_t>(R.a, R.consumed));
         const int64_t g = std::__gcd<int64_t>(P, R.b);
@@ -1092,6 +1109,11 @@ const char* snp_last_error(void) { return g_err.c_str(); }
 
 snp_status snp_load(const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const int32_t* C0, int64_t m,
                     const snp_options* opt, snp_system** out) {
+  return snp_load_unary(M, rules, n_rules, nullptr, C0, m, opt, out);
+}
+
+snp_status snp_load_unary(const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const uint64_t* re_bits,
+                          const int32_t* C0, int64_t m, const snp_options* opt, snp_system** out) {
   if (!M || !C0 || !out || m < 1 || m > 0x7FFFFFFF || n_rules < 0 || (n_rules > 0 && !rules))
     return fail(SNP_E_ARG, "snp_load: bad arguments");
   if (M->n_rules != n_rules || M->n_neurons != m) return fail(SNP_E_ARG, "snp_load: matrix shape != (n_rules, m)");
@@ -1146,8 +1168,8 @@ snp_status snp_load(const snp_matrix* M, const snp_rule* rules, int64_t n_rules,
   s->opt = o;
   s->bytes = o.count_bits / 8;
   s->count_max = o.count_bits == 8 ? 255 : o.count_bits == 16 ? 65535 : 0x7FFFFFFF;
-  snp_status st = out_rule >= 0 ? load_impl(s.get(), &Maug, rules, n_rules, aC0.data())
-                                : load_impl(s.get(), M, rules, n_rules, C0);
+  snp_status st = out_rule >= 0 ? load_impl(s.get(), &Maug, rules, n_rules, re_bits, aC0.data())
+                                : load_impl(s.get(), M, rules, n_rules, re_bits, C0);
   if (st != SNP_OK) return st;
   s->view.aug_rule = out_rule;
   s->view.aug_neuron = out_rule >= 0 ? rules[out_rule].neuron : -1;

@@ -33,7 +33,7 @@ SNP_LAYOUT_ROW_MAJOR = 0
 SNP_LAYOUT_NEURON_MAJOR = 1
 
 EXPORTED = [
-    "snp_abi_version", "snp_last_error", "snp_load", "snp_system_free", "snp_set_stream", "snp_begin",
+    "snp_abi_version", "snp_last_error", "snp_load", "snp_load_unary", "snp_system_free", "snp_set_stream", "snp_begin",
     "snp_advance", "snp_frontier_size", "snp_state_width", "snp_generated_numbers", "snp_depth", "snp_summary",
     "snp_explore", "snp_step",
     "snp_tree_num_levels", "snp_tree_num_configs", "snp_tree_level_offsets", "snp_tree_configs",
@@ -107,6 +107,8 @@ def lib() -> ctypes.CDLL:
         L.snp_advance.argtypes = [_P, ctypes.POINTER(snp_level_counters)]
         L.snp_frontier_size.argtypes = [_P]
         L.snp_frontier_size.restype = ctypes.c_int64
+        L.snp_load_unary.argtypes = [ctypes.POINTER(snp_matrix), _P, ctypes.c_int64, _P, _P, ctypes.c_int64,
+                                     ctypes.POINTER(snp_options), ctypes.POINTER(_P)]
         L.snp_state_width.argtypes = [_P]
         L.snp_state_width.restype = ctypes.c_int64
         L.snp_generated_numbers.argtypes = [_P, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
@@ -161,7 +163,7 @@ def _ptr(a: np.ndarray):
 # ---- C-named entry points (marshalling only) --------------------------------
 def snp_load(rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.ndarray, C0: np.ndarray,
              count_bits=32, dedup=0, frontier_target=0, max_transitions=0, fp_seed=(0x5EED0, 0x5EED1),
-             keep_tree=1, out_rule=None):
+             keep_tree=1, out_rule=None, re_bits=None):
     rules = np.ascontiguousarray(rules, np.int32).reshape(-1, 6)
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col = np.ascontiguousarray(col, np.int32)
@@ -171,8 +173,13 @@ def snp_load(rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.nd
     o = snp_options(count_bits, dedup, frontier_target, max_transitions, (ctypes.c_uint64 * 2)(*fp_seed),
                     keep_tree, 0 if out_rule is None else int(out_rule) + 1)
     h = _P()
-    _check(lib().snp_load(ctypes.byref(M), _ptr(rules), rules.shape[0], _ptr(C0), C0.shape[0], ctypes.byref(o),
-                          ctypes.byref(h)))
+    if re_bits is None:
+        _check(lib().snp_load(ctypes.byref(M), _ptr(rules), rules.shape[0], _ptr(C0), C0.shape[0], ctypes.byref(o),
+                              ctypes.byref(h)))
+    else:
+        bits = np.ascontiguousarray(re_bits, np.uint64).reshape(-1, 4)
+        _check(lib().snp_load_unary(ctypes.byref(M), _ptr(rules), rules.shape[0], _ptr(bits), _ptr(C0), C0.shape[0],
+                                    ctypes.byref(o), ctypes.byref(h)))
     return h
 
 
@@ -201,7 +208,8 @@ class System:
         self.count_bits = count_bits
         self._h = None
         self._h = snp_load(workload.rules, workload.row_ptr, workload.col, workload.val, workload.C0,
-                           count_bits, dedup, frontier_target, max_transitions, fp_seed, keep_tree, out_rule)
+                           count_bits, dedup, frontier_target, max_transitions, fp_seed, keep_tree, out_rule,
+                           getattr(workload, "re_bits", None))
         self.width = int(lib().snp_state_width(self._h))
 
     def generated_numbers(self) -> set:
