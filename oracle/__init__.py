@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_explore_gen.argtypes = [_P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _U64, _U64, _I32,
                                          ctypes.POINTER(_P)]
         L.oracle_explore_gen.restype = ctypes.c_int
+        L.oracle_sample.argtypes = [_P, _I64, _P, _U64, _I32, _I32, _P, _I32, _I32, _P]
+        L.oracle_sample.restype = ctypes.c_int
         L.oracle_run_num_numbers.argtypes = [_P]
         L.oracle_run_num_numbers.restype = _I64
         L.oracle_run_numbers.argtypes = [_P, _P]
@@ -165,6 +167,19 @@ class System:
         Cn = np.zeros((k, self.m), np.int64)
         lib().oracle_children(self._h, _ptr(C), k, _ptr(S), _ptr(Cn), ctypes.byref(psi))
         return int(psi.value), S, Cn
+
+    def sample(self, walkers, seed: int, steps: int, input_neuron: int = -1, train=None, count_bits: int = 32):
+        """Single-path sampling (oracle.cpp ``oracle_sample``): returns (final
+        configurations W × m, halted_step W)."""
+        C = np.ascontiguousarray(np.atleast_2d(walkers), dtype=np.int32).copy()
+        assert C.shape[1] == self.m
+        tr = np.ascontiguousarray(np.zeros(0) if train is None else train, dtype=np.int32)
+        hs = np.zeros(C.shape[0], np.int32)
+        st = lib().oracle_sample(self._h, C.shape[0], _ptr(C), seed, steps, input_neuron,
+                                 _ptr(tr) if tr.size else None, tr.size, count_bits, _ptr(hs))
+        if st != OR_OK:
+            raise OracleError(st, "sample")
+        return C, hs
 
     def explore(self, level0, depth: int, dedup: int = 0, count_bits: int = 32, frontier_target: int = 0,
                 max_transitions: int = 0, seeds=(0x5EED0, 0x5EED1), out_rule: int | None = None) -> "Run":

@@ -482,6 +482,48 @@ int oracle_explore(const oracle_system* h, int64_t F0, const int32_t* level0, in
                             seed1, -1, out);
 }
 
+// Single-path sampling with an input spike train (
+// Def. 1 `in`; deep trees take long to explore).
+// Each of W walkers follows ONE computation path: at step k a walker with
+// Ψ > 0 takes the child of index t = u mod Ψ in the enumeration order of
+// Alg. 2 (reading A7), u = splitmix64(splitmix64(seed XOR
+// (k << 32)) XOR w) (reading A25), i.e. C <- C + S_t·M (eq. (2)); a walker
+// with no applicable rule (reading A5) keeps C (no rule fires) while input
+// is still to come and stops (halted_step = k) once it is not (k >=
+// train_len or no input neuron).  After the transition the input neuron
+// (input_neuron >= 0) receives train[k] spikes from the environment (k <
+// train_len).  A count above the storage range is overflow.
+// configs: W × m in/out (int32).  halted_step: W (-1 = still running).
+int oracle_sample(const oracle_system* h, int64_t W, int32_t* configs, uint64_t seed, int32_t steps,
+                  int32_t input_neuron, const int32_t* train, int32_t train_len, int32_t count_bits,
+                  int32_t* halted_step) {
+  const System& s = h->s;
+  if (W < 0 || steps < 0 || input_neuron >= s.m || (count_bits != 8 && count_bits != 16 && count_bits != 32))
+    return OR_E_ARG;
+  const int64_t cmax = count_bits == 8 ? 255 : count_bits == 16 ? 65535 : 2147483647LL;
+  for (int64_t w = 0; w < W; ++w) {
+    std::vector<int64_t> C(configs + w * s.m, configs + (w + 1) * s.m);
+    halted_step[w] = -1;
+    for (int32_t k = 0; k < steps; ++k) {
+      auto A = applicable_rules_per_neuron(s, C);
+      uint64_t psi = 0;
+      if (!count_children(A, &psi)) return OR_E_CAPACITY;
+      const bool input_left = input_neuron >= 0 && k < train_len;
+      if (psi == 0 && !input_left) { halted_step[w] = k; break; }
+      if (psi > 0) {
+        const uint64_t u = splitmix64(splitmix64(seed ^ ((uint64_t)k << 32)) ^ (uint64_t)w);
+        auto S = spiking_vector(s, A, u % psi);
+        C = transition(s, C, S);
+      }
+      if (input_neuron >= 0 && k < train_len) C[input_neuron] += train[k];
+      for (int64_t v : C)
+        if (v < 0 || v > cmax) return OR_E_OVERFLOW;
+    }
+    for (int64_t j = 0; j < s.m; ++j) configs[w * s.m + j] = (int32_t)C[j];
+  }
+  return OR_OK;
+}
+
 int64_t oracle_run_num_numbers(const oracle_run* h) { return (int64_t)h->r.numbers.size(); }
 void oracle_run_numbers(const oracle_run* h, int64_t* out) { std::copy(h->r.numbers.begin(), h->r.numbers.end(), out); }
 int oracle_run_status(const oracle_run* h) { return h->r.status; }
