@@ -209,6 +209,13 @@ snp_status snp_set_profiling(snp_system *sys, int32_t on);
 snp_status snp_profile(const snp_system *sys, double *ms /* SNP_NUM_PHASES */);
 /* Kernels launched by this process through libsnp.so so far. */
 int64_t    snp_kernel_launches(void);
+/* Kernel paths the loaded system takes (bit mask, 0 for NULL):
+ *   SNP_PATH_TC_EXPAND  K-a on the tensor cores (k_expand_tc: uint8 storage,
+ *                       every neuron tabulated, c <= 15, p <= 1, rule deltas
+ *                       linear in (c, p) — DESIGN.md §7); otherwise the CUDA-core
+ *                       K-a kernels run.  SNP_KERNELS=no_tc at snp_load turns it off. */
+#define SNP_PATH_TC_EXPAND 1
+int32_t    snp_kernel_paths(const snp_system *sys);
 
 /* Multi-GPU exploration (one process per GPU).  Rank r holds a
  * contiguous range of the global frontier (global order = rank order, then

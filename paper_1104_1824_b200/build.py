@@ -18,7 +18,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
 SNP_SOURCES = ["snp_engine.cu", "snp_kernels.cu"]
-SNP_DEPS = SNP_SOURCES + ["snp_device.cuh", "snp_internal.h", "../../include/snp.h"]
+SNP_DEPS = SNP_SOURCES + ["snp_device.cuh", "snp_internal.h", "snp_tc.cuh", "../../include/snp.h"]
 
 
 def _stale(target: str, deps) -> bool:

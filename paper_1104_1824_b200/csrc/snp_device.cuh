@@ -86,7 +86,7 @@ enum : int32_t { NM_GENERIC = 1, NM_ND = 2 };
 // that rule's 16-B fingerprint delta in a neuron's 256-B slice.
 enum : uint32_t { TE_EMIT = 1u, TE_ND = 2u, TE_F = 0xF0u };
 // kernel selection flags (SysView::kernel_flags)
-enum : int32_t { KF_EXPAND_T = 1, KF_KC_GLOBAL_E = 2 };
+enum : int32_t { KF_EXPAND_T = 1, KF_KC_GLOBAL_E = 2, KF_NO_TC = 4 };
 
 __device__ __forceinline__ uint32_t table_index(uint32_t v, const NeuronMeta& mt) {
   // unsigned compare: lanes past F in a partial block may hold any bit
@@ -137,6 +137,15 @@ struct SysView {
   int32_t aug_neuron;        // its neuron
   unsigned long long* gen_bits;  // generated-number bitmap
   int64_t gen_cap_bits;
+  // tensor-core K-a (k_expand_tc), valid when tc_ok: uint8
+  // storage, every neuron tabulated, c <= 15, p <= 1 and every rule delta
+  // h_ℓ[r] = −c_r·R_ℓ[s] + p_r·Rout_ℓ[s]
+  int32_t tc_ok;
+  int32_t n_nd;              // neurons with some count making >= 2 rules applicable
+  const int32_t* nd_list;    // n_nd, increasing
+  const uint8_t* xyt;        // m × 32   first rule c | p << 4 for v < 32 (0 = none)
+  const uint8_t* xyf;        // m × 256  the same for every uint8 count
+  const uint8_t* btile;      // ceil(m/64) × 4096: B chunks (−R bytes | 1, Rout bytes), K-major core matrices
 };
 // key of a terminal child (second output spike): skipped by the dedup
 constexpr uint64_t KEY_TERMINAL1 = ~0ULL - 1;

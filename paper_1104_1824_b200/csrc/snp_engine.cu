@@ -204,7 +204,7 @@ struct snp_system {
   uint64_t vis_cap = 0, ltab_cap = 0, child_cap = 0;
   // scratch
   DBuf psi, off, fpb0, fpb1, ndc, nd, ebits;
-  DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab, d_elut, d_hsg;
+  DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab, d_elut, d_hsg, d_xyt, d_xyf, d_btile, d_ndl;
   DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   DBuf gen;           // generated-number bitmap (out_rule1 > 0)
@@ -696,6 +696,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     v.aug_neuron = -1;
     if (k && strstr(k, "expand_t")) v.kernel_flags |= KF_EXPAND_T;
     if (k && strstr(k, "kc_global_e")) v.kernel_flags |= KF_KC_GLOBAL_E;
+    if (k && strstr(k, "no_tc")) v.kernel_flags |= KF_NO_TC;
   }
   v.m = (int32_t)m;
   v.n = n;
@@ -723,6 +724,72 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
                       s->bytes == 1 ? s->d_hsg.as<uint8_t>() : nullptr, s->stream);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(s->stream));
+  // ---- tensor-core K-a (k_expand_tc): X|Y bytes of the first
+  // applicable rule per (neuron, count), the B operand chunks (byte planes of
+  // −R_ℓ[s] and Rout_ℓ[s] = Σ_{j ∈ out(s)} R_ℓ[j]) and the neurons that can be
+  // nondeterministic.  Applies when every rule delta decomposes as
+  // h_ℓ[r] = −c_r·R_ℓ[s] + p_r·Rout_ℓ[s] (reading A18) with c <= 15, p <= 1.
+  v.tc_ok = 0;
+  v.n_nd = 0;
+  if (s->bytes == 1 && !v.any_generic && s->binary_emit) {
+    std::vector<uint8_t> tf((size_t)m * 256);
+    CUDA_TRY(cudaMemcpy(tf.data(), s->d_tab_full.p, tf.size(), cudaMemcpyDeviceToHost));
+    bool ok = true;
+    std::vector<uint8_t> xyf((size_t)m * 256, 0), xyt((size_t)m * 32, 0);
+    std::vector<int32_t> ndl;
+    for (int64_t j = 0; j < m && ok; ++j) {
+      bool nd = false;
+      for (int64_t c = 0; c < 256; ++c) {
+        const uint8_t e = tf[(size_t)j * 256 + c];
+        nd |= (e & TE_ND) != 0;
+        const int f = e >> 4;
+        if (!f) continue;
+        const snp_rule& R = rules[rule_off[j] + f - 1];
+        if (R.consumed > 15 || R.produced > 1) { ok = false; break; }
+        xyf[(size_t)j * 256 + c] = (uint8_t)(R.consumed | (R.produced << 4));
+      }
+      if (nd) ndl.push_back((int32_t)j);
+      std::copy(xyf.begin() + j * 256, xyf.begin() + j * 256 + 32, xyt.begin() + j * 32);
+    }
+    std::vector<uint64_t> Ro0(m, 0), Ro1(m, 0);
+    for (int64_t j = 0; j < m; ++j)
+      for (int32_t t : out_syn[j]) { Ro0[j] += R0[t]; Ro1[j] += R1[t]; }
+    for (int64_t r = 0; r < n && ok; ++r) {
+      const snp_rule& R = rules[r];
+      const uint64_t c = (uint64_t)(int64_t)R.consumed, p = (uint64_t)(int64_t)R.produced;
+      if (h0[r] != (0 - c) * R0[R.neuron] + p * Ro0[R.neuron] || h1[r] != (0 - c) * R1[R.neuron] + p * Ro1[R.neuron])
+        ok = false;
+    }
+    if ((int64_t)ndl.size() > KMAX) ok = false;
+    if (ok) {
+      const int64_t nch = (m + 63) / 64;
+      std::vector<uint8_t> bt((size_t)nch * 4096, 0);
+      for (int64_t j = 0; j < m; ++j) {
+        const int64_t ch = j / 64, k = j % 64;
+        auto put = [&](int half, int col, uint64_t w) {
+          bt[(size_t)ch * 4096 + half * 2048 + (k / 16) * 512 + (col / 8) * 128 + (col % 8) * 16 + k % 16] =
+              (uint8_t)w;
+        };
+        for (int b = 0; b < 8; ++b) {
+          put(0, b, (0 - R0[j]) >> (8 * b));
+          put(0, 8 + b, (0 - R1[j]) >> (8 * b));
+          put(1, b, Ro0[j] >> (8 * b));
+          put(1, 8 + b, Ro1[j] >> (8 * b));
+        }
+        put(0, 16, 1);  // total consumption: 0 <=> halting
+      }
+      SNP_TRY(upload(s, s->d_xyt, xyt));
+      SNP_TRY(upload(s, s->d_xyf, xyf));
+      SNP_TRY(upload(s, s->d_btile, bt));
+      SNP_TRY(upload(s, s->d_ndl, ndl));
+      v.tc_ok = 1;
+      v.n_nd = (int32_t)ndl.size();
+      v.nd_list = s->d_ndl.as<int32_t>();
+      v.xyt = s->d_xyt.as<uint8_t>();
+      v.xyf = s->d_xyf.as<uint8_t>();
+      v.btile = s->d_btile.as<uint8_t>();
+    }
+  }
   CUDA_TRY(cudaEventCreate(&s->ev0));
   CUDA_TRY(cudaEventCreate(&s->ev1));
   return SNP_OK;
@@ -1274,6 +1341,11 @@ snp_status snp_profile(const snp_system* s, double* ms) {
 }
 
 int64_t snp_kernel_launches(void) { return snp::g_kernel_launches.load(); }
+
+int32_t snp_kernel_paths(const snp_system* s) {
+  if (!s) return 0;
+  return (s->view.tc_ok && !(s->view.kernel_flags & (snp::KF_NO_TC | snp::KF_EXPAND_T))) ? SNP_PATH_TC_EXPAND : 0;
+}
 
 int64_t snp_level_size(const snp_system* s, int32_t level) {
   if (!s || level < 0 || level >= (int32_t)s->levels.size()) return -1;

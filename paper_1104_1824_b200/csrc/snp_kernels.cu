@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include "snp_internal.h"
+#include "snp_tc.cuh"
 
 namespace snp {
 
@@ -797,6 +798,224 @@ __global__ void k_build_hs(SysView S, uint8_t* hsg) {
   ulonglong2 h = make_ulonglong2(0ULL, 0ULL);
   if (f >= 1 && f <= r1 - r0) h = make_ulonglong2(S.h0[r0 + f - 1], S.h1[r0 + f - 1]);
   reinterpret_cast<ulonglong2*>(hsg)[i] = h;
+}
+
+// ---------------------------------------------------------------------------
+// K-a on the tensor cores (SysView::tc_ok).  The base-child fingerprint is a
+// contraction over the neurons (reading A18):
+//   fp_ℓ(base(C)) = fp_ℓ(C) + Σ_s X_s·(−R_ℓ[s]) + Σ_s Y_s·Rout_ℓ[s]  (mod 2^64)
+// X_s / Y_s = consumption / emission of the first applicable rule of s
+// (Def. 2 at 115-119), 0 when none applies.  A CTA owns M = 128
+// configurations (two storage blocks) and walks the neurons in chunks of 64:
+// thread (h, k) loads the 64 counts of neuron c0 + k in block h (two 32-B
+// loads), maps them to X|Y bytes by byte-permute lookups in the neuron's
+// 32-entry table, writes the block's emit word, and stores X and Y into the
+// chunk's A tiles (MN-major, one 16-B store per 16 configurations); one
+// thread issues the chunk's four u8 MMAs (K = 32, N = 32) into a TMEM s32
+// accumulator: columns 0-7 / 8-15 are the byte planes of the two
+// fingerprint lanes, column 16 the total consumption (0 <=> halting,
+// reading A5).  Accumulators stay < 2^31 (m·15·255 + m·255 for m ≤ 2^19).
+// Ψ and the ND lists come from k_nd_pass over the few neurons that can be
+// nondeterministic.
+// ---------------------------------------------------------------------------
+constexpr int TCM = 128;                        // configurations per CTA (MMA M)
+constexpr int TCK = 64;                         // neurons per chunk
+constexpr int TCN = 32;                         // accumulator columns per operand (MMA N)
+constexpr int TCT = 256;                        // threads: (block h, half q, neuron k)
+constexpr int TC_A_LBO = 1024;                  // A: K-group (8 neurons) stride = 8 MN groups × 128 B
+constexpr int TC_B_LBO = 512;                   // B: K-chunk (16 neurons) stride = 4 N groups × 128 B
+constexpr int TC_ATILE = TCM * TCK;             // 8 KB
+constexpr int TC_BTILE = TCK * TCN;             // 2 KB
+constexpr int TC_STAGE = 2 * TC_ATILE + 2 * TC_BTILE;
+constexpr int TC_STAGES = 2;
+
+size_t expand_tc_smem_bytes() { return (size_t)TC_STAGES * TC_STAGE + 64 + 1024; }
+
+// t[v] for the four byte counts v < 16 of v4, t = 16 bytes in tt[0..3]
+__device__ __forceinline__ uint32_t lut16(uint32_t v4, const uint32_t (&tt)[8]) {
+  const uint32_t x = v4 & 0x07070707u;
+  const uint32_t sel = prmt(x | (x >> 4), 0u, 0x4420u);
+  const uint32_t m3 = prmt(v4 << 4, 0u, 0xBA98u);  // 0xFF in bytes whose bit 3 is set
+  const uint32_t a = prmt(tt[0], tt[1], sel), b = prmt(tt[2], tt[3], sel);
+  return (a & ~m3) | (b & m3);
+}
+
+__global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, ExpandOut O) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + TC_STAGES);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int32_t m = S.m;
+  const int64_t mE = (m + 1) & ~1;
+  const int64_t nblk = (L.F + PB - 1) / PB;
+  const int64_t blk0 = (int64_t)blockIdx.x * 2;
+  const int k = tid & 63, q = (tid >> 6) & 1, h = tid >> 7;
+  const int64_t blk = blk0 + h;
+  const bool bvalid = blk < nblk;
+  // parents of block blk that exist (the tail block may be partial): mask of this half
+  const int64_t nv = bvalid ? (L.F - blk * PB < PB ? L.F - blk * PB : PB) : 0;
+  const int64_t nvq = nv - 32 * q;
+  const uint32_t vmask = nvq >= 32 ? ~0u : (nvq <= 0 ? 0u : ((1u << nvq) - 1));
+  const int nch = (m + TCK - 1) / TCK;
+  uint32_t* ew_out = (O.ebits != nullptr && !O.classify_only) ? reinterpret_cast<uint32_t*>(O.ebits) : nullptr;
+  const uint8_t* data = reinterpret_cast<const uint8_t*>(L.data);
+
+  if (warp == 0) tc::tmem_alloc(tslot, 64);
+  if (tid == 0) {
+    tc::bar_init(&bar[0], 1);
+    tc::bar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  constexpr uint32_t IDESC = tc::idesc_u8(TCM, TCN, true, false);
+
+  // chunk c's 32 counts of neuron c·64 + k (block h, half q) and its table,
+  // loaded one chunk ahead
+  uint32_t w[8], tt[8];
+  auto load = [&](int c) {
+    const int32_t s = c * TCK + k;
+    if (bvalid && s < m) {
+      ldg256(data + ((blk * m + s) << 6) + 32 * q, w);
+      const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(S.xyt + (int64_t)s * 32));
+      const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(S.xyt + (int64_t)s * 32) + 1);
+      tt[0] = t0.x; tt[1] = t0.y; tt[2] = t0.z; tt[3] = t0.w;
+      tt[4] = t1.x; tt[5] = t1.y; tt[6] = t1.z; tt[7] = t1.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = tt[i] = 0;  // count 0 -> entry 0 (nothing fires)
+    }
+  };
+  load(0);
+  for (int c = 0; c < nch; ++c) {
+    const int st = c & 1;
+    uint8_t* sX = smem + st * TC_STAGE;
+    uint8_t* sY = sX + TC_ATILE;
+    uint8_t* sB = sY + TC_ATILE;
+    const int32_t s = c * TCK + k;
+    // entries (c | p << 4) of the 32 counts: 16- or 32-entry byte-permute
+    // lookups (warp-uniform choice), the full table for a count >= 32
+    uint32_t e[8];
+    {
+      uint32_t hiv = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) hiv |= w[i];
+      if (__all_sync(0xFFFFFFFFu, (hiv & 0xF0F0F0F0u) == 0)) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) e[i] = lut16(w[i], tt);
+      } else if ((hiv & 0xE0E0E0E0u) == 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) e[i] = lut32(w[i], tt);
+      } else {  // rare
+        const uint8_t* xf = S.xyf + (int64_t)s * 256;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if ((w[i] & 0xE0E0E0E0u) == 0) {
+            e[i] = lut32(w[i], tt);
+          } else {
+            uint32_t x = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) x |= (uint32_t)__ldg(xf + ((w[i] >> (8 * b)) & 0xFFu)) << (8 * b);
+            e[i] = x;
+          }
+        }
+      }
+    }
+    if (c + 1 < nch) load(c + 1);
+    uint32_t X[8], Y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      X[i] = e[i] & 0x0F0F0F0Fu;
+      Y[i] = e[i] & 0x10101010u;  // 16·p: its accumulator is shifted back in the epilogue
+    }
+    if (ew_out && bvalid && s < m) {
+      // emit bits of configurations 8j..8j+7: bit 0 (4i+b) and bit 4 (4i+4+b)
+      // of byte b, gathered into the top byte by one multiply
+      uint32_t ew = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t z = (Y[2 * j] >> 4) | Y[2 * j + 1];
+        ew = prmt(ew, z * 0x01020408u, (0x3210u & ~(0xFu << (4 * j))) | (7u << (4 * j)));
+      }
+      ew_out[(blk * mE + s) * 2 + q] = ew & vmask;
+    }
+    // the MMAs that read this stage two chunks ago must be done
+    if (c >= 2) tc::bar_wait(&bar[st], (uint32_t)(((c - 2) >> 1) & 1));
+    {
+      const int off = (k >> 3) * TC_A_LBO + (4 * h + 2 * q) * 128 + (k & 7) * 16;
+      *reinterpret_cast<uint4*>(sX + off) = make_uint4(X[0], X[1], X[2], X[3]);
+      *reinterpret_cast<uint4*>(sX + off + 128) = make_uint4(X[4], X[5], X[6], X[7]);
+      *reinterpret_cast<uint4*>(sY + off) = make_uint4(Y[0], Y[1], Y[2], Y[3]);
+      *reinterpret_cast<uint4*>(sY + off + 128) = make_uint4(Y[4], Y[5], Y[6], Y[7]);
+      reinterpret_cast<uint4*>(sB)[tid] = __ldg(reinterpret_cast<const uint4*>(S.btile + (int64_t)c * (2 * TC_BTILE)) + tid);
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+#pragma unroll
+      for (int ks = 0; ks < TCK / 32; ++ks) {
+        tc::mma_u8(tmem, tc::sdesc(tc::smem_u32(sX + ks * 4 * TC_A_LBO), TC_A_LBO, 128),
+                   tc::sdesc(tc::smem_u32(sB + ks * 2 * TC_B_LBO), TC_B_LBO, 128), IDESC, (c > 0 || ks > 0) ? 1u : 0u);
+        tc::mma_u8(tmem + TCN, tc::sdesc(tc::smem_u32(sY + ks * 4 * TC_A_LBO), TC_A_LBO, 128),
+                   tc::sdesc(tc::smem_u32(sB + TC_BTILE + ks * 2 * TC_B_LBO), TC_B_LBO, 128), IDESC,
+                   (c > 0 || ks > 0) ? 1u : 0u);
+      }
+      tc::commit(&bar[st]);
+    }
+  }
+  const int cl = nch - 1;
+  tc::bar_wait(&bar[cl & 1], (uint32_t)((cl >> 1) & 1));
+  tc::fence_after();
+  if (warp < 4) {
+    uint32_t rx[32], ry[32];
+    tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), rx);
+    tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + TCN, ry);
+    const int64_t p = blk0 * PB + 32 * warp + lane;
+    bool halt = false;
+    if (p < L.F) {
+      uint64_t a = L.fp0[p], b = L.fp1[p];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        a += (uint64_t)(rx[i] + (ry[i] >> 4)) << (8 * i);
+        b += (uint64_t)(rx[8 + i] + (ry[8 + i] >> 4)) << (8 * i);
+      }
+      halt = rx[16] == 0;
+      O.halting[p] = halt ? 1 : 0;
+      if (!O.classify_only) {
+        O.fpb0[p] = a;
+        O.fpb1[p] = b;
+      }
+    }
+    const unsigned nh = __popc(__ballot_sync(0xFFFFFFFFu, halt));
+    if (lane == 0 && nh) atomicAdd(O.n_halting, (unsigned long long)nh);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 64);
+}
+
+// Ψ (eq. (8), readings A3/A5) and the ND lists for k_expand_tc:
+// only neurons in S.nd_list can have d_s >= 2; visited in increasing order so
+// the list is in total order (reading A7).
+__global__ void k_nd_pass(SysView S, LevelView L, ExpandOut O) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= L.F) return;
+  const uint8_t* data = reinterpret_cast<const uint8_t*>(L.data);
+  int ndc = 0;
+  uint64_t psi = 1;
+  for (int i = 0; i < S.n_nd; ++i) {
+    const int32_t s = __ldg(S.nd_list + i);
+    const uint32_t v = data[eidx(p, s, S.m)];
+    if (__ldg(S.tab_full + (int64_t)s * 256 + v) & TE_ND) nd_event(S, O, s, v, p, ndc, psi);
+  }
+  if (O.halting[p]) psi = 0;  // halting: no children (reading A5)
+  O.psi[p] = psi;
+  O.ndc[p] = ndc;
+  if (psi > PSI_LIMIT || ndc > KMAX) atomicOr(O.err, ERR_CAPACITY);
 }
 
 // Generic K-a (systems whose neurons cannot all be tabulated): the same walk,
@@ -1871,7 +2090,16 @@ void launch_expand(const SysView& S, int32_t bytes, const LevelView& L, const Ex
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<expand_grid(L.F), XW * 32, smem, st>>>(S, L, O);
       };
-      if (full && S.any_generic == 0 && S.hsg != nullptr && !(S.kernel_flags & KF_EXPAND_T)) {
+      if (full && S.tc_ok && !(S.kernel_flags & (KF_EXPAND_T | KF_NO_TC))) {
+        const size_t sm = expand_tc_smem_bytes();
+        cudaFuncSetAttribute(k_expand_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const int64_t nblk = (L.F + PB - 1) / PB;
+        k_expand_tc<<<(unsigned)((nblk + 1) / 2), TCT, sm, st>>>(S, L, O);
+        if (!O.classify_only) {
+          k_nd_pass<<<grid_for(L.F), BLK, 0, st>>>(S, L, O);
+          count_launch();
+        }
+      } else if (full && S.any_generic == 0 && S.hsg != nullptr && !(S.kernel_flags & KF_EXPAND_T)) {
         const size_t sq = expand_q_smem_bytes();
         cudaFuncSetAttribute(k_expand_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq);
         const unsigned g = (unsigned)((L.F + QB * PB - 1) / (QB * PB));

@@ -1,0 +1,106 @@
+// snp_tc.cuh — the few tcgen05 / TMEM primitives the engine uses (sm_100a).
+//
+// Only one contraction in the path is tensor-core shaped: the base-child
+// fingerprint of K-a (reading A18),
+//     fp_ℓ(base(C)) = fp_ℓ(C) + Σ_s X_s·(−R_ℓ[s]) + Σ_s Y_s·Rout_ℓ[s]  (mod 2^64)
+// with X_s = consumption and Y_s = emission of neuron s's first applicable
+// rule, Rout_ℓ[s] = Σ_{j ∈ out(s)} R_ℓ[j].  It runs as an unsigned 8-bit GEMM
+// (tcgen05.mma kind::i8, s32 accumulators in TMEM): A = X|Y bytes (M = 128
+// configurations, K = neurons, MN-major), B = the byte planes of −R and Rout
+// (K-major), N = 32 columns (16 fingerprint bytes + the firing count).
+//
+// Shared-memory operands use the no-swizzle canonical layouts:
+//   MN-major (A): core matrix = 8 K-rows of 16 contiguous MN bytes (128 B);
+//                 MN groups of 16 at SBO bytes, K groups of 8 at LBO bytes.
+//   K-major  (B): core matrix = 8 N-rows of 16 contiguous K bytes (128 B);
+//                 N groups of 8 at SBO bytes, K chunks of 16 at LBO bytes.
+#pragma once
+#include <cstdint>
+
+namespace snp {
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// tcgen05 shared-memory matrix descriptor, no swizzle, version 1 (sm_100)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+// instruction descriptor: kind::i8, u8 × u8 → s32, A MN-major (a_mn), B K-major
+__host__ __device__ constexpr uint32_t idesc_u8(int M, int N, bool a_mn, bool b_mn) {
+  return (2u << 4)                          // D format S32
+         | (0u << 7) | (0u << 10)           // A, B unsigned 8-bit
+         | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16)
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// generic-proxy shared-memory writes → visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// whole warp: allocate ncols TMEM columns, address written to *dst (shared)
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// 32 lanes × 32 columns of 32 bits: lane i of the warp gets TMEM lane
+// (taddr.lane + i), columns taddr.col .. +31
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// mbarrier helpers (CTA scope)
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// A operand (MN-major, no swizzle) of one K=32 MMA step inside a chunk laid
+// out as  addr(mn, k) = (k/8)·a_lbo + (mn/16)·128 + (k%8)·16 + mn%16.
+// B operand (K-major, no swizzle): addr(n, k) = (k/16)·b_lbo + (n/8)·128 + (n%8)·16 + k%16.
+
+}  // namespace tc
+}  // namespace snp

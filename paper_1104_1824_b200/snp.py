@@ -39,10 +39,11 @@ EXPORTED = [
     "snp_tree_num_levels", "snp_tree_num_configs", "snp_tree_level_offsets", "snp_tree_configs",
     "snp_tree_edges", "snp_tree_counters", "snp_tree_spiking_vectors", "snp_tree_free",
     "snp_level_size", "snp_level_edges", "snp_level_columns", "snp_set_profiling", "snp_profile",
-    "snp_kernel_launches", "snp_dist_begin", "snp_dist_expand", "snp_dist_pack", "snp_dist_owner_dedup",
+    "snp_kernel_launches", "snp_kernel_paths", "snp_dist_begin", "snp_dist_expand", "snp_dist_pack", "snp_dist_owner_dedup",
     "snp_dist_owner_keep", "snp_dist_finalize", "snp_dist_commit",
 ]
 SNP_NUM_PHASES = 5
+SNP_PATH_TC_EXPAND = 1
 PHASES = ["expand", "keys", "dedup", "materialize", "verify"]
 
 
@@ -135,6 +136,8 @@ def lib() -> ctypes.CDLL:
         L.snp_set_profiling.argtypes = [_P, ctypes.c_int32]
         L.snp_profile.argtypes = [_P, _P]
         L.snp_kernel_launches.restype = ctypes.c_int64
+        L.snp_kernel_paths.argtypes = [_P]
+        L.snp_kernel_paths.restype = ctypes.c_int32
         _I64P = ctypes.POINTER(ctypes.c_int64)
         L.snp_dist_begin.argtypes = [_P, ctypes.POINTER(snp_configs), ctypes.c_int32, _I64P]
         L.snp_dist_expand.argtypes = [_P, _I64P]
@@ -144,7 +147,7 @@ def lib() -> ctypes.CDLL:
         L.snp_dist_finalize.argtypes = [_P, _P, _I64P]
         L.snp_dist_commit.argtypes = [_P, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(snp_level_counters)]
         for f in EXPORTED:
-            if f not in ("snp_kernel_launches", "snp_system_free", "snp_tree_free", "snp_frontier_size", "snp_depth", "snp_level_size",
+            if f not in ("snp_kernel_launches", "snp_kernel_paths", "snp_system_free", "snp_tree_free", "snp_frontier_size", "snp_depth", "snp_level_size",
                          "snp_tree_num_levels", "snp_tree_num_configs", "snp_abi_version", "snp_last_error"):
                 getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -222,6 +225,11 @@ class System:
         _check(lib().snp_generated_numbers(self._h, _ptr(words), words.shape[0], None))
         bits = np.unpackbits(words.view(np.uint8), bitorder="little")
         return set(int(i) for i in np.nonzero(bits)[0])
+
+    @property
+    def kernel_paths(self) -> int:
+        """snp_kernel_paths: SNP_PATH_* bits of the kernels this system runs."""
+        return int(lib().snp_kernel_paths(self._h))
 
     def close(self):
         if self._h:

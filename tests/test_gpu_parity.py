@@ -140,7 +140,7 @@ def test_random_system_parity(snp, m, F, depth, bits, dedup, target):
     assert_same_tree(tree, ref)
 
 
-@pytest.mark.parametrize("kernels", ["", "expand_t", "kc_global_e"])
+@pytest.mark.parametrize("kernels", ["", "expand_t", "kc_global_e", "no_tc"])
 def test_uint8_large_counts(snp, monkeypatch, kernels):
     """uint8 storage with counts well above the 32-entry register tables, so
     the table-fallback paths of K-a and K-c run; SNP_KERNELS=expand_t selects
@@ -154,6 +154,26 @@ def test_uint8_large_counts(snp, monkeypatch, kernels):
     tree = snp.System(w, count_bits=8, dedup=1, frontier_target=800).explore(L0, depth=3)
     ref = oracle.System.from_workload(w).explore(L0, depth=3, dedup=1, count_bits=8, frontier_target=800)
     assert_same_tree(tree, ref)
+
+
+@pytest.mark.parametrize("kernels", ["", "no_tc"])
+def test_tc_expand_selected_and_equal(snp, monkeypatch, kernels):
+    """The tensor-core K-a (k_expand_tc) is the path for uint8 systems of the
+    generator family and for Π; SNP_KERNELS=no_tc runs the CUDA-core K-a.
+    Both give the oracle's tree (ragged F: a partial last 128-configuration
+    tile and a partial 64-configuration block; m not a multiple of 64)."""
+    monkeypatch.setenv("SNP_KERNELS", kernels)
+    want = 0 if kernels else snp.SNP_PATH_TC_EXPAND
+    w = W.random_system(1000, outdeg=8, k_nd=6, seed=5)
+    L0 = W.level0_counts(w, 1100, 5)
+    eng = snp.System(w, count_bits=8, dedup=1, frontier_target=1000)
+    assert eng.kernel_paths == want
+    tree = eng.explore(L0, depth=4)
+    ref = oracle.System.from_workload(w).explore(L0, depth=4, dedup=1, count_bits=8, frontier_target=1000)
+    assert_same_tree(tree, ref)
+    pi = W.pi_system("simulator")
+    assert snp.System(pi, count_bits=8, dedup=0).kernel_paths == want
+    assert snp.System(pi, count_bits=32, dedup=0).kernel_paths == 0  # int32 storage: CUDA-core K-a
 
 
 def test_config5_shape_parity(snp):
