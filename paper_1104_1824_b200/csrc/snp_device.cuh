@@ -112,6 +112,7 @@ struct SysView {
   // lane l = e-th in-synapse of target 32g + l), padded with the index m_even
   // (a zero word)
   const int32_t* in_pad;
+  const uint16_t* in_pad16;    // the same as uint16 when m < 65535 (else null)
   const int64_t* in_pad_off;   // m/32 + 1 row offsets (×32 entries)
   const int32_t* out_off;    // m + 1
   const int32_t* out_dst;    // targets j with (s, j) ∈ syn, grouped by source s

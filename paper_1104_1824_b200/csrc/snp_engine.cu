@@ -184,7 +184,7 @@ struct snp_system {
   std::vector<int32_t> C0;
   bool binary_emit = true;
   // ---- device system
-  DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1, d_in_pad, d_in_pad_off;
+  DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1, d_in_pad, d_in_pad16, d_in_pad_off;
   SysView view{};
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -617,6 +617,10 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
         for (int32_t e = in_off[j]; e < in_off[j + 1]; ++e)
           in_pad[(size_t)(pad_off[g] + (e - in_off[j])) * 32 + (j - 32 * g)] = in_src[e];
     SNP_TRY(upload(s, s->d_in_pad, in_pad));
+    if (m < 65535) {
+      std::vector<uint16_t> in16(in_pad.begin(), in_pad.end());
+      SNP_TRY(upload(s, s->d_in_pad16, in16));
+    }
     SNP_TRY(upload(s, s->d_in_pad_off, pad_off));
   }
   SNP_TRY(upload(s, s->d_out_off, out_off));
@@ -709,6 +713,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.in_off = s->d_in_off.as<int32_t>();
   v.in_src = s->d_in_src.as<int32_t>();
   v.in_pad = s->d_in_pad.as<int32_t>();
+  v.in_pad16 = m < 65535 ? s->d_in_pad16.as<uint16_t>() : nullptr;
   v.in_pad_off = s->d_in_pad_off.as<int64_t>();
   v.out_off = s->d_out_off.as<int32_t>();
   v.out_dst = s->d_out_dst.as<int32_t>();
@@ -735,7 +740,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     std::vector<uint8_t> tf((size_t)m * 256);
     CUDA_TRY(cudaMemcpy(tf.data(), s->d_tab_full.p, tf.size(), cudaMemcpyDeviceToHost));
     bool ok = true;
-    std::vector<uint8_t> xyf((size_t)m * 256, 0), xyt((size_t)m * 32, 0);
+    std::vector<uint8_t> xyf((size_t)m * 256, 0), xyt((size_t)((m + 63) / 64) * 64 * 32, 0);  // whole chunks
     std::vector<int32_t> ndl;
     for (int64_t j = 0; j < m && ok; ++j) {
       bool nd = false;

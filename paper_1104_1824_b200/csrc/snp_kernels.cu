@@ -807,10 +807,12 @@ __global__ void k_build_hs(SysView S, uint8_t* hsg) {
 // X_s / Y_s = consumption / emission of the first applicable rule of s
 // (Def. 2 at 115-119), 0 when none applies.  A CTA owns M = 128
 // configurations (two storage blocks) and walks the neurons in chunks of 64:
-// thread (h, k) loads the 64 counts of neuron c0 + k in block h (two 32-B
-// loads), maps them to X|Y bytes by byte-permute lookups in the neuron's
-// 32-entry table, writes the block's emit word, and stores X and Y into the
-// chunk's A tiles (MN-major, one 16-B store per 16 configurations); one
+// thread (h, q, k) loads the 32 counts of neuron c0 + k in half q of block h
+// (one 32-B load, one chunk ahead), maps them to X|Y bytes by byte-permute
+// lookups in the neuron's 16/32-entry table (the chunk's tables are staged
+// in shared memory), writes its half of the block's emit word, and stores X
+// and Y into the chunk's A tiles (MN-major, one 16-B store per 16
+// configurations); one
 // thread issues the chunk's four u8 MMAs (K = 32, N = 32) into a TMEM s32
 // accumulator: columns 0-7 / 8-15 are the byte planes of the two
 // fingerprint lanes, column 16 the total consumption (0 <=> halting,
@@ -829,7 +831,9 @@ constexpr int TC_BTILE = TCK * TCN;             // 2 KB
 constexpr int TC_STAGE = 2 * TC_ATILE + 2 * TC_BTILE;
 constexpr int TC_STAGES = 2;
 
-size_t expand_tc_smem_bytes() { return (size_t)TC_STAGES * TC_STAGE + 64 + 1024; }
+constexpr int TC_TTAB = TCK * 32;              // the chunk's 32-entry X|Y tables (2 KB), double-buffered
+
+size_t expand_tc_smem_bytes() { return (size_t)TC_STAGES * TC_STAGE + 2 * TC_TTAB + 64; }
 
 // t[v] for the four byte counts v < 16 of v4, t = 16 bytes in tt[0..3]
 __device__ __forceinline__ uint32_t lut16(uint32_t v4, const uint32_t (&tt)[8]) {
@@ -841,9 +845,10 @@ __device__ __forceinline__ uint32_t lut16(uint32_t v4, const uint32_t (&tt)[8]) 
 }
 
 __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, ExpandOut O) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE);
+  extern __shared__ __align__(128) uint8_t smem_tc[];
+  uint8_t* smem = smem_tc;
+  uint8_t* sT = smem + TC_STAGES * TC_STAGE;  // [2][TC_TTAB]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sT + 2 * TC_TTAB);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + TC_STAGES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int32_t m = S.m;
@@ -867,30 +872,31 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
     tc::bar_init(&bar[1], 1);
     fence_barrier_init();
   }
+  // X|Y tables of chunk c in sT[c & 1] (xyt is padded to whole chunks)
+  auto stage_tables = [&](int c) {
+    if (tid < TC_TTAB / 16)
+      reinterpret_cast<uint4*>(sT + (c & 1) * TC_TTAB)[tid] =
+          __ldg(reinterpret_cast<const uint4*>(S.xyt + (int64_t)c * TC_TTAB) + tid);
+  };
+  stage_tables(0);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tslot;
   constexpr uint32_t IDESC = tc::idesc_u8(TCM, TCN, true, false);
 
-  // chunk c's 32 counts of neuron c·64 + k (block h, half q) and its table,
-  // loaded one chunk ahead
-  uint32_t w[8], tt[8];
-  auto load = [&](int c) {
+  // the 32 counts of neuron c·64 + k (block h, half q) of chunk c, loaded
+  // one chunk ahead
+  auto load = [&](int c, uint32_t (&w)[8]) {
     const int32_t s = c * TCK + k;
-    if (bvalid && s < m) {
+    if (c < nch && bvalid && s < m) {
       ldg256(data + ((blk * m + s) << 6) + 32 * q, w);
-      const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(S.xyt + (int64_t)s * 32));
-      const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(S.xyt + (int64_t)s * 32) + 1);
-      tt[0] = t0.x; tt[1] = t0.y; tt[2] = t0.z; tt[3] = t0.w;
-      tt[4] = t1.x; tt[5] = t1.y; tt[6] = t1.z; tt[7] = t1.w;
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = tt[i] = 0;  // count 0 -> entry 0 (nothing fires)
+      for (int i = 0; i < 8; ++i) w[i] = 0;  // count 0 -> entry 0 (nothing fires: padded neurons have zero tables)
     }
   };
-  load(0);
-  for (int c = 0; c < nch; ++c) {
+  auto chunk = [&](int c, uint32_t (&w)[8]) {
     const int st = c & 1;
     uint8_t* sX = smem + st * TC_STAGE;
     uint8_t* sY = sX + TC_ATILE;
@@ -898,7 +904,13 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
     const int32_t s = c * TCK + k;
     // entries (c | p << 4) of the 32 counts: 16- or 32-entry byte-permute
     // lookups (warp-uniform choice), the full table for a count >= 32
-    uint32_t e[8];
+    uint32_t e[8], tt[8];
+    {
+      const uint4 t0 = reinterpret_cast<const uint4*>(sT + st * TC_TTAB + k * 32)[0];
+      const uint4 t1 = reinterpret_cast<const uint4*>(sT + st * TC_TTAB + k * 32)[1];
+      tt[0] = t0.x; tt[1] = t0.y; tt[2] = t0.z; tt[3] = t0.w;
+      tt[4] = t1.x; tt[5] = t1.y; tt[6] = t1.z; tt[7] = t1.w;
+    }
     {
       uint32_t hiv = 0;
 #pragma unroll
@@ -924,7 +936,7 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
         }
       }
     }
-    if (c + 1 < nch) load(c + 1);
+    load(c + 1, w);
     uint32_t X[8], Y[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -951,6 +963,7 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
       *reinterpret_cast<uint4*>(sY + off) = make_uint4(Y[0], Y[1], Y[2], Y[3]);
       *reinterpret_cast<uint4*>(sY + off + 128) = make_uint4(Y[4], Y[5], Y[6], Y[7]);
       reinterpret_cast<uint4*>(sB)[tid] = __ldg(reinterpret_cast<const uint4*>(S.btile + (int64_t)c * (2 * TC_BTILE)) + tid);
+      if (c + 1 < nch) stage_tables(c + 1);
     }
     tc::fence_async_smem();
     __syncthreads();
@@ -966,7 +979,10 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
       }
       tc::commit(&bar[st]);
     }
-  }
+  };
+  uint32_t w[8];
+  load(0, w);
+  for (int c = 0; c < nch; ++c) chunk(c, w);
   const int cl = nch - 1;
   tc::bar_wait(&bar[cl & 1], (uint32_t)((cl >> 1) & 1));
   tc::fence_after();
@@ -1548,6 +1564,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       const int64_t g = jbase >> 5;
       const int64_t r0 = __ldg(S.in_pad_off + g), r1 = __ldg(S.in_pad_off + g + 1);
       const int32_t* col = S.in_pad + r0 * 32 + lane;
+      const uint16_t* col16 = S.in_pad16 ? S.in_pad16 + r0 * 32 + lane : nullptr;  // m < 65535: half the index bytes
       const int ne = (int)(r1 - r0);
       auto word = [&](int32_t s) -> uint64_t { return ES ? sE[s] : __ldg(s < mE ? gE + s : &g_zero_word); };
       auto ripple = [&](int b0, uint64_t carry) {
@@ -1563,7 +1580,8 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       for (; e0 + 8 <= ne || (e0 < ne && ne - e0 > 4); e0 += 8) {
         int32_t src[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) src[u] = (e0 + u < ne) ? __ldg(col + (e0 + u) * 32) : (int32_t)mE;  // batch the loads
+        for (int u = 0; u < 8; ++u)  // batch the loads
+          src[u] = (e0 + u < ne) ? (col16 ? (int32_t)__ldg(col16 + (e0 + u) * 32) : __ldg(col + (e0 + u) * 32)) : (int32_t)mE;
         uint64_t x[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) x[u] = word(src[u]);
@@ -1580,7 +1598,8 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       if (e0 < ne) {  // 1..4 rows left
         int32_t src[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) src[u] = (e0 + u < ne) ? __ldg(col + (e0 + u) * 32) : (int32_t)mE;
+        for (int u = 0; u < 4; ++u)
+          src[u] = (e0 + u < ne) ? (col16 ? (int32_t)__ldg(col16 + (e0 + u) * 32) : __ldg(col + (e0 + u) * 32)) : (int32_t)mE;
         uint64_t x[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) x[u] = word(src[u]);
@@ -1591,7 +1610,10 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         ripple(2, foursA);
       }
     }
-    const NeuronMeta mt = S.meta[j];
+    // the descriptor is only needed for untabulated neurons and the rare
+    // count >= 32 fallback (loaded there)
+    NeuronMeta mt{};
+    if (S.any_generic || sizeof(T) != 1) mt = S.meta[j];
     const T* crow_g = ctab + (int64_t)j * S.tabw;
     const bool generic = mt.flags & NM_GENERIC;
     uint64_t ovf_bits = 0;
@@ -1629,7 +1651,10 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         uint32_t t[8], hiv = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) hiv |= vw[i];
-        if ((hiv & 0xE0E0E0E0u) == 0) {
+        if (__all_sync(__activemask(), (hiv & 0xF0F0F0F0u) == 0)) {  // every count of the warp < 16
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = lut16(vw[i], tt);
+        } else if ((hiv & 0xE0E0E0E0u) == 0) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) t[i] = lut32(vw[i], tt);
         } else {
@@ -1642,7 +1667,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
 #pragma unroll
               for (int b = 0; b < 4; ++b) {
                 const uint32_t v = (vw[i] >> (8 * b)) & 0xFFu;
-                t[i] |= (v - (uint32_t)crow8[table_index(v, mt)]) << (8 * b);
+                t[i] |= (v - (uint32_t)crow8[table_index(v, S.meta[j])]) << (8 * b);
               }
             }
           }
