@@ -138,7 +138,7 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-KERNEL_OF = {"expand": "K-a k_expand_q (uint8) / k_expand_t", "materialize": "K-c k_materialize_bs + k_patch",
+KERNEL_OF = {"expand": "K-a k_expand_tc (tensor cores) + k_nd_pass, else k_expand_q / k_expand_t", "materialize": "K-c k_materialize_bs + k_patch",
              "dedup": "K-d k_dedup..k_compact", "keys": "K-b k_child_keys"}
 
 

@@ -242,6 +242,28 @@ snp_status snp_dist_owner_keep(snp_system *sys, int64_t n_new_global, void *verd
 snp_status snp_dist_finalize(snp_system *sys, const void *verdict_back, int64_t *K_local);
 snp_status snp_dist_commit(snp_system *sys, int64_t parent_offset, int64_t q_offset, snp_level_counters *out);
 
+/* Single-path sampling with an input spike train (Def. 1
+ * `in`; deep computation trees take long to
+ * explore).  Each of W walkers follows ONE computation path for `steps` steps:
+ * at step k a walker with Ψ > 0 (eq. (8)) takes the child
+ * t = u mod Ψ in the enumeration order of Alg. 2 (reading
+ * A7), u = splitmix64(splitmix64(seed ^ (k << 32)) ^ w) (reading A25), i.e.
+ * C <- C + S_t·M (eq. (2)); then the input neuron (input_neuron >= 0)
+ * receives train[k] spikes from the environment while k < train_len.  A
+ * walker with no applicable rule keeps its configuration while input is
+ * still to come and stops once it is not: halted_step[w] = k (-1 = still
+ * running after `steps` steps; reading A5).
+ *   configs      W × m int32 row-major, in/out (host); every count must lie in
+ *                [0, storage max] on entry (SNP_E_ARG otherwise)
+ *   train        train_len int32 (host), may be NULL when train_len == 0
+ *   halted_step  W int32 (host), out
+ * Errors: SNP_E_ARG (bad arguments), SNP_E_STATE (system loaded with
+ * out_rule1), SNP_E_CAPACITY (some Ψ > 2^62), SNP_E_OVERFLOW (a count left
+ * the storage range after a step; capacity is reported first); configs and
+ * halted_step are then unspecified.  Synchronous; one kernel launch. */
+snp_status snp_sample(snp_system *sys, int64_t W, int32_t *configs, uint64_t seed, int32_t steps,
+                      int32_t input_neuron, const int32_t *train, int32_t train_len, int32_t *halted_step);
+
 /* snp_begin + `depth` × snp_advance + halting classification of the last
  * level; the tree is a snapshot owned by the caller.                          */
 snp_status snp_explore(snp_system *sys, const snp_configs *level0, int32_t depth, snp_tree **out);

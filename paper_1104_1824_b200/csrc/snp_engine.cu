@@ -1399,6 +1399,43 @@ snp_status snp_level_columns(snp_system* s, int32_t level, const int64_t* idx, i
   return sync(s);
 }
 
+snp_status snp_sample(snp_system* s, int64_t W, int32_t* configs, uint64_t seed, int32_t steps, int32_t input_neuron,
+                      const int32_t* train, int32_t train_len, int32_t* halted_step) {
+  if (!s || W < 0 || steps < 0 || (W > 0 && (!configs || !halted_step)) || train_len < 0 ||
+      (train_len > 0 && !train) || input_neuron >= s->m || input_neuron < -1)
+    return fail(SNP_E_ARG, "snp_sample: bad arguments");
+  if (s->view.aug_rule >= 0) return fail(SNP_E_STATE, "snp_sample: not available with generated numbers (out_rule1)");
+  const int64_t m = s->m;
+  for (int64_t i = 0; i < W * m; ++i)
+    if (configs[i] < 0 || configs[i] > s->count_max)
+      return fail(SNP_E_ARG, "snp_sample: count %d at walker %lld neuron %lld outside [0, %lld]", configs[i],
+                  (long long)(i / m), (long long)(i % m), (long long)s->count_max);
+  if (W == 0) return SNP_OK;
+  DBuf cur, nxt, fired, halted, dtrain, derr;
+  const size_t bytes = (size_t)W * m * 4;
+  SNP_TRY(derr.ensure(sizeof(int32_t), false));
+  SNP_TRY(cur.ensure(bytes, false));
+  SNP_TRY(nxt.ensure(bytes, false));
+  SNP_TRY(fired.ensure(bytes, false));
+  SNP_TRY(halted.ensure((size_t)W * 4, false));
+  SNP_TRY(dtrain.ensure(std::max<size_t>(1, (size_t)train_len) * 4, false));
+  CUDA_TRY(cudaMemsetAsync(derr.p, 0, sizeof(int32_t), s->stream));
+  CUDA_TRY(cudaMemcpyAsync(cur.p, configs, bytes, cudaMemcpyHostToDevice, s->stream));
+  if (train_len > 0)
+    CUDA_TRY(cudaMemcpyAsync(dtrain.p, train, (size_t)train_len * 4, cudaMemcpyHostToDevice, s->stream));
+  launch_sample(s->view, W, cur.as<int32_t>(), nxt.as<int32_t>(), fired.as<int32_t>(), seed, steps, input_neuron,
+                dtrain.as<int32_t>(), train_len, halted.as<int32_t>(), derr.as<int32_t>(), s->stream);
+  CUDA_TRY(cudaGetLastError());
+  int32_t err = 0;
+  CUDA_TRY(cudaMemcpyAsync(&err, derr.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (err & ERR_CAPACITY) return fail(SNP_E_CAPACITY, "snp_sample: a walker has more than 2^62 children");
+  if (err & ERR_OVERFLOW) return fail(SNP_E_OVERFLOW, "snp_sample: a count left [0, %lld]", (long long)s->count_max);
+  CUDA_TRY(cudaMemcpyAsync(configs, cur.p, bytes, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(halted_step, halted.p, (size_t)W * 4, cudaMemcpyDeviceToHost, s->stream));
+  return sync(s);
+}
+
 snp_status snp_explore(snp_system* s, const snp_configs* level0, int32_t depth, snp_tree** out) {
   if (!s || !out || depth < 0) return fail(SNP_E_ARG, "snp_explore: bad arguments");
   snp_status st = snp_begin(s, level0);

@@ -131,6 +131,11 @@ void launch_unperm(const uint64_t* perm, const uint8_t* back, uint64_t T, uint64
 void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_data, const int64_t* parent,
                             const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st);
 
+// single-path sampling: W walkers, all steps in one launch
+void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, int32_t* fired, uint64_t seed,
+                   int32_t steps, int32_t input_neuron, const int32_t* train, int32_t train_len, int32_t* halted,
+                   int32_t* err, cudaStream_t st);
+
 // CUB exclusive scan of n uint64 values (temp storage managed by the caller).
 size_t scan_temp_bytes(int64_t n);
 void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint64_t* in, uint64_t* out, int64_t n,

@@ -828,12 +828,14 @@ constexpr int TC_A_LBO = 1024;                  // A: K-group (8 neurons) stride
 constexpr int TC_B_LBO = 512;                   // B: K-chunk (16 neurons) stride = 4 N groups × 128 B
 constexpr int TC_ATILE = TCM * TCK;             // 8 KB
 constexpr int TC_BTILE = TCK * TCN;             // 2 KB
-constexpr int TC_STAGE = 2 * TC_ATILE + 2 * TC_BTILE;
-constexpr int TC_STAGES = 2;
+constexpr int TC_STAGE = 2 * TC_ATILE;           // X and Y tiles of one chunk
+constexpr int TC_STAGES = 2;                     // X|Y tiles: double-buffered
+constexpr int TC_IN = 3;                         // B tile + tables: a ring of 3 (loaded one chunk ahead)
 
-constexpr int TC_TTAB = TCK * 32;              // the chunk's 32-entry X|Y tables (2 KB), double-buffered
+constexpr int TC_TTAB = TCK * 32;              // the chunk's 32-entry X|Y tables (2 KB)
+constexpr int TC_INB = 2 * TC_BTILE + TC_TTAB;  // one input slot: B tiles (X, Y) + tables
 
-size_t expand_tc_smem_bytes() { return (size_t)TC_STAGES * TC_STAGE + 2 * TC_TTAB + 64; }
+size_t expand_tc_smem_bytes() { return (size_t)TC_STAGES * TC_STAGE + (size_t)TC_IN * TC_INB + 64 + 16; }
 
 // t[v] for the four byte counts v < 16 of v4, t = 16 bytes in tt[0..3]
 __device__ __forceinline__ uint32_t lut16(uint32_t v4, const uint32_t (&tt)[8]) {
@@ -847,9 +849,10 @@ __device__ __forceinline__ uint32_t lut16(uint32_t v4, const uint32_t (&tt)[8]) 
 __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, ExpandOut O) {
   extern __shared__ __align__(128) uint8_t smem_tc[];
   uint8_t* smem = smem_tc;
-  uint8_t* sT = smem + TC_STAGES * TC_STAGE;  // [2][TC_TTAB]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sT + 2 * TC_TTAB);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + TC_STAGES);
+  uint8_t* sIn = smem + TC_STAGES * TC_STAGE;                       // [TC_IN][B_X | B_Y | tables]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sIn + TC_IN * TC_INB);  // [2] MMAs done with an X|Y stage
+  uint64_t* lbar = bar + TC_STAGES;                                    // [3] an input slot landed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(lbar + TC_IN);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int32_t m = S.m;
   const int64_t mE = (m + 1) & ~1;
@@ -867,18 +870,21 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
   const uint8_t* data = reinterpret_cast<const uint8_t*>(L.data);
 
   if (warp == 0) tc::tmem_alloc(tslot, 64);
+  // chunk c's B tiles and X|Y tables (xyt is padded to whole chunks) into
+  // input slot c % 3: two bulk copies (TMA engine, no LSU work) on lbar[c % 3]
+  auto stage_inputs = [&](int c) {
+    const int sl = c % TC_IN;
+    mbar_arrive_expect_tx(&lbar[sl], (uint32_t)TC_INB);
+    bulk_g2s(sIn + sl * TC_INB, S.btile + (int64_t)c * (2 * TC_BTILE), 2 * TC_BTILE, &lbar[sl]);
+    bulk_g2s(sIn + sl * TC_INB + 2 * TC_BTILE, S.xyt + (int64_t)c * TC_TTAB, TC_TTAB, &lbar[sl]);
+  };
   if (tid == 0) {
     tc::bar_init(&bar[0], 1);
     tc::bar_init(&bar[1], 1);
+    for (int i = 0; i < TC_IN; ++i) tc::bar_init(&lbar[i], 1);
     fence_barrier_init();
+    stage_inputs(0);
   }
-  // X|Y tables of chunk c in sT[c & 1] (xyt is padded to whole chunks)
-  auto stage_tables = [&](int c) {
-    if (tid < TC_TTAB / 16)
-      reinterpret_cast<uint4*>(sT + (c & 1) * TC_TTAB)[tid] =
-          __ldg(reinterpret_cast<const uint4*>(S.xyt + (int64_t)c * TC_TTAB) + tid);
-  };
-  stage_tables(0);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -900,14 +906,25 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
     const int st = c & 1;
     uint8_t* sX = smem + st * TC_STAGE;
     uint8_t* sY = sX + TC_ATILE;
-    uint8_t* sB = sY + TC_ATILE;
+    const int sl = c % TC_IN;
+    uint8_t* sB = sIn + sl * TC_INB;
+    const uint8_t* sT = sB + 2 * TC_BTILE;
     const int32_t s = c * TCK + k;
     // entries (c | p << 4) of the 32 counts: 16- or 32-entry byte-permute
     // lookups (warp-uniform choice), the full table for a count >= 32
     uint32_t e[8], tt[8];
+    tc::bar_wait(&lbar[sl], (uint32_t)((c / TC_IN) & 1));
+    // the next chunk's inputs go to slot (c + 1) % 3, last read by the MMAs
+    // of chunk c - 2 (done: issued two chunks ago) and by the table loads of
+    // chunk c - 2 (before this thread's previous __syncthreads)
+    if (tid == 0 && c + 1 < nch) {
+      if (c >= 2) tc::bar_wait(&bar[st], (uint32_t)(((c - 2) >> 1) & 1));
+      tc::fence_async_smem();
+      stage_inputs(c + 1);
+    }
     {
-      const uint4 t0 = reinterpret_cast<const uint4*>(sT + st * TC_TTAB + k * 32)[0];
-      const uint4 t1 = reinterpret_cast<const uint4*>(sT + st * TC_TTAB + k * 32)[1];
+      const uint4 t0 = reinterpret_cast<const uint4*>(sT + k * 32)[0];
+      const uint4 t1 = reinterpret_cast<const uint4*>(sT + k * 32)[1];
       tt[0] = t0.x; tt[1] = t0.y; tt[2] = t0.z; tt[3] = t0.w;
       tt[4] = t1.x; tt[5] = t1.y; tt[6] = t1.z; tt[7] = t1.w;
     }
@@ -962,8 +979,6 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
       *reinterpret_cast<uint4*>(sX + off + 128) = make_uint4(X[4], X[5], X[6], X[7]);
       *reinterpret_cast<uint4*>(sY + off) = make_uint4(Y[0], Y[1], Y[2], Y[3]);
       *reinterpret_cast<uint4*>(sY + off + 128) = make_uint4(Y[4], Y[5], Y[6], Y[7]);
-      reinterpret_cast<uint4*>(sB)[tid] = __ldg(reinterpret_cast<const uint4*>(S.btile + (int64_t)c * (2 * TC_BTILE)) + tid);
-      if (c + 1 < nch) stage_tables(c + 1);
     }
     tc::fence_async_smem();
     __syncthreads();
@@ -2032,6 +2047,127 @@ void dispatch_bytes(int32_t bytes, F&& f) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Single-path sampling with an input spike train (Def. 1
+// `in`; deep trees take long to explore).  One
+// warp per walker runs every step (walkers are independent: no grid sync).
+// Step k: applicable rules per neuron, Ψ = Π_{d_s>0} d_s
+// (eq. (8), reading A3; > 2^62 is SNP_E_CAPACITY), the child
+// t = u mod Ψ with u = splitmix64(splitmix64(seed ^ (k << 32)) ^ w)
+// (reading A25) decoded in mixed radix, first nondeterministic neuron most
+// significant (Alg. 2 II-2/II-3, reading A7), C' = C + S_t·M as the column
+// sums of Def. 2, then the input neuron gets train[k] spikes (k < train_len).
+// A walker with no applicable rule keeps C while input is still to come and
+// stops (halted = k) once it is not (reading A5).  Counts outside
+// [0, count_max] after a step are SNP_E_OVERFLOW.
+// cur / nxt / fired: W × m int32 walker-major scratch; the final states end
+// in cur.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64_dev(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+constexpr int SAMPLE_WARPS = 4;
+
+__global__ void __launch_bounds__(SAMPLE_WARPS * 32) k_sample(SysView S, int64_t W, int32_t* cur, int32_t* nxt,
+                                                             int32_t* fired, uint64_t seed, int32_t steps,
+                                                             int32_t input_neuron, const int32_t* train,
+                                                             int32_t train_len, int32_t* halted, int32_t* err) {
+  __shared__ int32_t nd_s[SAMPLE_WARPS][KMAX];
+  __shared__ uint8_t nd_d[SAMPLE_WARPS][KMAX];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= W) return;
+  const int32_t m = S.m;
+  int32_t* C = cur + w * m;
+  int32_t* N = nxt + w * m;
+  int32_t* Fr = fired + w * m;
+  int32_t hs = -1;
+  bool bad = false;
+  for (int32_t k = 0; k < steps && !bad; ++k) {
+    // first applicable rule and d_s of every neuron; the nondeterministic ones in order
+    uint64_t psi = 1;
+    bool any = false;
+    int nnd = 0;
+    for (int32_t base = 0; base < m; base += 32) {
+      const int32_t s = base + lane;
+      int d = 0, first = -1;
+      if (s < m) {
+        const int32_t v = C[s];
+        for (int r = S.rule_off[s]; r < S.rule_off[s + 1]; ++r)
+          if (rule_app(S.rules[r], v)) {
+            if (!d) first = r;
+            ++d;
+          }
+        Fr[s] = first;
+      }
+      any |= d > 0;
+      if (d > 1) psi = sat_mul(psi, (uint64_t)d);
+      const unsigned b = __ballot_sync(0xFFFFFFFFu, d >= 2);
+      const int pos = nnd + __popc(b & ((1u << lane) - 1));
+      if (d >= 2 && pos < KMAX) {
+        nd_s[wl][pos] = s;
+        nd_d[wl][pos] = (uint8_t)d;
+      }
+      nnd += __popc(b);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) psi = sat_mul(psi, __shfl_xor_sync(0xFFFFFFFFu, psi, o));
+    any = __any_sync(0xFFFFFFFFu, any);
+    if (psi > PSI_LIMIT) {
+      if (lane == 0) atomicOr(err, ERR_CAPACITY);
+      bad = true;
+      break;
+    }
+    const bool input_left = input_neuron >= 0 && k < train_len;
+    if (!any && !input_left) {
+      hs = k;
+      break;
+    }
+    if (any) {
+      __syncwarp();
+      if (lane == 0) {
+        uint64_t t = splitmix64_dev(splitmix64_dev(seed ^ ((uint64_t)k << 32)) ^ (uint64_t)w) % psi;
+        for (int i = nnd - 1; i >= 0; --i) {
+          const int32_t s = nd_s[wl][i];
+          const uint64_t d = nd_d[wl][i];
+          Fr[s] = nth_applicable(S, s, C[s], (int)(t % d));
+          t /= d;
+        }
+      }
+      __syncwarp();
+      for (int32_t j = lane; j < m; j += 32) {
+        const int32_t rj = Fr[j];
+        int64_t val = (int64_t)C[j] - (rj >= 0 ? S.rules[rj].c : 0);
+        for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) {
+          const int32_t rs = Fr[S.in_src[e]];
+          if (rs >= 0) val += S.rules[rs].p;
+        }
+        if (j == input_neuron && input_left) val += train[k];
+        bad |= val < 0 || val > S.count_max;
+        N[j] = (int32_t)val;
+      }
+      __syncwarp();
+      int32_t* t_ = C;
+      C = N;
+      N = t_;
+    } else if (lane == 0) {  // nothing fires: only the input arrives
+      const int64_t val = (int64_t)C[input_neuron] + train[k];
+      bad |= val < 0 || val > S.count_max;
+      C[input_neuron] = (int32_t)val;
+    }
+    bad = __any_sync(0xFFFFFFFFu, bad);
+    if (bad && lane == 0) atomicOr(err, ERR_OVERFLOW);
+    __syncwarp();
+  }
+  if (C != cur + w * m)
+    for (int32_t j = lane; j < m; j += 32) cur[w * m + j] = C[j];
+  if (lane == 0) halted[w] = hs;
+}
+
 // ===========================================================================
 // launchers
 // ===========================================================================
@@ -2370,6 +2506,15 @@ void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_
     k_spiking_vectors<T><<<grid_for(K, 128), 128, 0, st>>>(S, reinterpret_cast<const T*>(parent_data), parent, t, K,
                                                          S_out);
   });
+  count_launch();
+}
+
+void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, int32_t* fired, uint64_t seed,
+                   int32_t steps, int32_t input_neuron, const int32_t* train, int32_t train_len, int32_t* halted,
+                   int32_t* err, cudaStream_t st) {
+  const int64_t blocks = (W + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
+  k_sample<<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, st>>>(S, W, cur, nxt, fired, seed, steps, input_neuron, train,
+                                                           train_len, halted, err);
   count_launch();
 }
 

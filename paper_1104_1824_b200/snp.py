@@ -35,7 +35,7 @@ SNP_LAYOUT_NEURON_MAJOR = 1
 EXPORTED = [
     "snp_abi_version", "snp_last_error", "snp_load", "snp_load_unary", "snp_system_free", "snp_set_stream", "snp_begin",
     "snp_advance", "snp_frontier_size", "snp_state_width", "snp_generated_numbers", "snp_depth", "snp_summary",
-    "snp_explore", "snp_step",
+    "snp_explore", "snp_step", "snp_sample",
     "snp_tree_num_levels", "snp_tree_num_configs", "snp_tree_level_offsets", "snp_tree_configs",
     "snp_tree_edges", "snp_tree_counters", "snp_tree_spiking_vectors", "snp_tree_free",
     "snp_level_size", "snp_level_edges", "snp_level_columns", "snp_set_profiling", "snp_profile",
@@ -136,6 +136,8 @@ def lib() -> ctypes.CDLL:
         L.snp_set_profiling.argtypes = [_P, ctypes.c_int32]
         L.snp_profile.argtypes = [_P, _P]
         L.snp_kernel_launches.restype = ctypes.c_int64
+        L.snp_sample.argtypes = [_P, ctypes.c_int64, _P, ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32, _P,
+                                 ctypes.c_int32, _P]
         L.snp_kernel_paths.argtypes = [_P]
         L.snp_kernel_paths.restype = ctypes.c_int32
         _I64P = ctypes.POINTER(ctypes.c_int64)
@@ -225,6 +227,18 @@ class System:
         _check(lib().snp_generated_numbers(self._h, _ptr(words), words.shape[0], None))
         bits = np.unpackbits(words.view(np.uint8), bitorder="little")
         return set(int(i) for i in np.nonzero(bits)[0])
+
+    def sample(self, walkers, seed: int, steps: int, input_neuron: int = -1, train=None):
+        """snp_sample: single-path sampling of W walkers (SURVEY §8(f) NEXT-4);
+        returns (final configurations W × m int32, halted_step W int32)."""
+        C = np.ascontiguousarray(np.atleast_2d(walkers), dtype=np.int32).copy()
+        if C.shape[1] != self.m:
+            raise ValueError(f"walkers have {C.shape[1]} columns, the system has {self.m} neurons")
+        tr = np.ascontiguousarray(np.zeros(0) if train is None else train, dtype=np.int32)
+        hs = np.zeros(C.shape[0], np.int32)
+        _check(lib().snp_sample(self._h, C.shape[0], _ptr(C), seed, steps, input_neuron,
+                                _ptr(tr) if tr.size else None, tr.size, _ptr(hs)))
+        return C, hs
 
     @property
     def kernel_paths(self) -> int:

@@ -1,7 +1,7 @@
 # scratch GPU session: parity tests + default / no_tc bench A/B
 O=gpurun_out/${TAG:-tc2}; mkdir -p $O
 if [ -z "$SKIP_TESTS" ]; then
-timeout 900 python -m pytest tests -m gpu -x -q $PYTEST_ARGS > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
+timeout 900 python -m pytest tests -m gpu -x -q ${PYTEST_K:+-k "$PYTEST_K"} > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
 tail -4 $O/pytest.log
 fi
 for K in ${VARIANTS:-"" no_tc}; do

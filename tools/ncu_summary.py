@@ -3,7 +3,7 @@ profiles/ncu_summary.json (read by bench.py for roofline.traffic).
 
 Capture (one GPU, full bench size; three metrics = one pass, no replay):
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-      --clock-control none --csv -k regex:"k_expand|k_materialize|k_patch" -s 6 -c 6 \
+      --clock-control none --csv -k regex:"k_expand|k_nd_pass|k_materialize|k_patch" -s 6 -c 6 \
       --log-file gpurun_out/dram_full.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu
 Usage: python tools/ncu_summary.py gpurun_out/dram_full.csv [profiles/ncu_summary.json]
 """
@@ -12,7 +12,7 @@ import json
 import sys
 from collections import defaultdict
 
-PHASE = {"k_expand": "expand", "k_materialize": "materialize", "k_patch": "materialize",
+PHASE = {"k_expand": "expand", "k_nd_pass": "expand", "k_materialize": "materialize", "k_patch": "materialize",
          "k_overflow_fix": "materialize"}
 
 
