@@ -609,7 +609,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     for (int64_t g = 0; g < ng; ++g) {
       int32_t mx = 0;
       for (int64_t j = 32 * g; j < std::min<int64_t>(m, 32 * g + 32); ++j) mx = std::max(mx, in_off[j + 1] - in_off[j]);
-      pad_off[g + 1] = pad_off[g] + mx;
+      pad_off[g + 1] = pad_off[g] + (mx + 3) / 4 * 4;  // K-c consumes rows in blocks of 8 and 4
     }
     std::vector<int32_t> in_pad((size_t)pad_off[ng] * 32, pad);
     for (int64_t g = 0; g < ng; ++g)

@@ -1504,15 +1504,16 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       uint32_t d = 0x80000000u;
       if (q >= Q0 && q + 3 < Q1) {
         const uint32_t a = sR[q - Qb] >> 2;
-        uint32_t sel = 0;
+        uint32_t sel = 0, hb = 0;
         bool ok = true;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t o = (uint32_t)sR[q + k - Qb] - 4 * a;
-          ok &= o < 8;
+          ok &= o < 16;
+          hb |= (o >> 3) << k;  // byte k from words a+2, a+3
           sel |= (o & 7) << (4 * k);
         }
-        if (ok) d = (a << 16) | sel;
+        if (ok) d = (hb << 24) | (a << 16) | sel;
       }
       sD[i] = d;
     }
@@ -1578,8 +1579,8 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       // <= 4 rows in one block of 4 (3 full adders)
       const int64_t g = jbase >> 5;
       const int64_t r0 = __ldg(S.in_pad_off + g), r1 = __ldg(S.in_pad_off + g + 1);
-      const int32_t* col = S.in_pad + r0 * 32 + lane;
-      const uint16_t* col16 = S.in_pad16 ? S.in_pad16 + r0 * 32 + lane : nullptr;  // m < 65535: half the index bytes
+      // rows per group are padded to a multiple of 4 (snp_load), so every
+      // index load is in bounds; uint16 indices when m < 65535
       const int ne = (int)(r1 - r0);
       auto word = [&](int32_t s) -> uint64_t { return ES ? sE[s] : __ldg(s < mE ? gE + s : &g_zero_word); };
       auto ripple = [&](int b0, uint64_t carry) {
@@ -1591,39 +1592,41 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
           carry = t;
         }
       };
-      int e0 = 0;
-      for (; e0 + 8 <= ne || (e0 < ne && ne - e0 > 4); e0 += 8) {
-        int32_t src[8];
+      auto gather = [&](const auto* col) {
+        int e0 = 0;
+        for (; e0 + 8 <= ne; e0 += 8) {
+          int32_t src[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)  // batch the loads
-          src[u] = (e0 + u < ne) ? (col16 ? (int32_t)__ldg(col16 + (e0 + u) * 32) : __ldg(col + (e0 + u) * 32)) : (int32_t)mE;
-        uint64_t x[8];
+          for (int u = 0; u < 8; ++u) src[u] = (int32_t)__ldg(col + (e0 + u) * 32);  // batch the loads
+          uint64_t x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = word(src[u]);
-        uint64_t twosA, twosB, foursA, foursB, eightsA;
-        csa(twosA, c[0], c[0], x[0], x[1]);
-        csa(twosB, c[0], c[0], x[2], x[3]);
-        csa(foursA, c[1], c[1], twosA, twosB);
-        csa(twosA, c[0], c[0], x[4], x[5]);
-        csa(twosB, c[0], c[0], x[6], x[7]);
-        csa(foursB, c[1], c[1], twosA, twosB);
-        csa(eightsA, c[2], c[2], foursA, foursB);
-        ripple(3, eightsA);
-      }
-      if (e0 < ne) {  // 1..4 rows left
-        int32_t src[4];
+          for (int u = 0; u < 8; ++u) x[u] = word(src[u]);
+          uint64_t twosA, twosB, foursA, foursB, eightsA;
+          csa(twosA, c[0], c[0], x[0], x[1]);
+          csa(twosB, c[0], c[0], x[2], x[3]);
+          csa(foursA, c[1], c[1], twosA, twosB);
+          csa(twosA, c[0], c[0], x[4], x[5]);
+          csa(twosB, c[0], c[0], x[6], x[7]);
+          csa(foursB, c[1], c[1], twosA, twosB);
+          csa(eightsA, c[2], c[2], foursA, foursB);
+          ripple(3, eightsA);
+        }
+        if (e0 < ne) {  // 4 rows left
+          int32_t src[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          src[u] = (e0 + u < ne) ? (col16 ? (int32_t)__ldg(col16 + (e0 + u) * 32) : __ldg(col + (e0 + u) * 32)) : (int32_t)mE;
-        uint64_t x[4];
+          for (int u = 0; u < 4; ++u) src[u] = (int32_t)__ldg(col + (e0 + u) * 32);
+          uint64_t x[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = word(src[u]);
-        uint64_t twosA, twosB, foursA;
-        csa(twosA, c[0], c[0], x[0], x[1]);
-        csa(twosB, c[0], c[0], x[2], x[3]);
-        csa(foursA, c[1], c[1], twosA, twosB);
-        ripple(2, foursA);
-      }
+          for (int u = 0; u < 4; ++u) x[u] = word(src[u]);
+          uint64_t twosA, twosB, foursA;
+          csa(twosA, c[0], c[0], x[0], x[1]);
+          csa(twosB, c[0], c[0], x[2], x[3]);
+          csa(foursA, c[1], c[1], twosA, twosB);
+          ripple(2, foursA);
+        }
+      };
+      if (S.in_pad16) gather(S.in_pad16 + r0 * 32 + lane);
+      else gather(S.in_pad + r0 * 32 + lane);
     }
     // the descriptor is only needed for untabulated neurons and the rare
     // count >= 32 fallback (loaded there)
@@ -1749,8 +1752,12 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       const uint32_t* xw = reinterpret_cast<const uint32_t*>(xsb);
       auto quad = [&](uint32_t d, uint32_t qi) -> uint32_t {
         if (!(d & 0x80000000u)) {
-          const uint32_t* w = xw + (d >> 16);
-          return prmt(w[0], w[1], d & 0xFFFFu);
+          const uint32_t* w = xw + ((d >> 16) & 31);
+          const uint32_t sel = d & 0xFFFFu, hb = d >> 24;
+          const uint32_t lo = prmt(w[0], w[1], sel);
+          if (!hb) return lo;
+          const uint32_t mask = (hb * 0x00204081u & 0x01010101u) * 0xFFu;  // 0xFF in bytes k with bit k of hb
+          return (lo & ~mask) | (prmt(w[2], w[3], sel) & mask);
         }
         const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + 4 * qi);  // 4 parent indices
         return (uint32_t)xsb[rr & 0xFF] | ((uint32_t)xsb[(rr >> 8) & 0xFF] << 8) |
