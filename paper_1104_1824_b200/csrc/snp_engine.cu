@@ -1416,14 +1416,14 @@ snp_status snp_sample(snp_system* s, int64_t W, int32_t* configs, uint64_t seed,
   SNP_TRY(derr.ensure(sizeof(int32_t), false));
   SNP_TRY(cur.ensure(bytes, false));
   SNP_TRY(nxt.ensure(bytes, false));
-  SNP_TRY(fired.ensure(bytes, false));
+  SNP_TRY(fired.ensure(2 * bytes, false));
   SNP_TRY(halted.ensure((size_t)W * 4, false));
   SNP_TRY(dtrain.ensure(std::max<size_t>(1, (size_t)train_len) * 4, false));
   CUDA_TRY(cudaMemsetAsync(derr.p, 0, sizeof(int32_t), s->stream));
   CUDA_TRY(cudaMemcpyAsync(cur.p, configs, bytes, cudaMemcpyHostToDevice, s->stream));
   if (train_len > 0)
     CUDA_TRY(cudaMemcpyAsync(dtrain.p, train, (size_t)train_len * 4, cudaMemcpyHostToDevice, s->stream));
-  launch_sample(s->view, W, cur.as<int32_t>(), nxt.as<int32_t>(), fired.as<int32_t>(), seed, steps, input_neuron,
+  launch_sample(s->view, W, cur.as<int32_t>(), nxt.as<int32_t>(), fired.as<uint64_t>(), seed, steps, input_neuron,
                 dtrain.as<int32_t>(), train_len, halted.as<int32_t>(), derr.as<int32_t>(), s->stream);
   CUDA_TRY(cudaGetLastError());
   int32_t err = 0;

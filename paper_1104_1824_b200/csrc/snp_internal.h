@@ -132,7 +132,7 @@ void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_
                             const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st);
 
 // single-path sampling: W walkers, all steps in one launch
-void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, int32_t* fired, uint64_t seed,
+void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, uint64_t* fired, uint64_t seed,
                    int32_t steps, int32_t input_neuron, const int32_t* train, int32_t train_len, int32_t* halted,
                    int32_t* err, cudaStream_t st);
 

@@ -2067,8 +2067,8 @@ void dispatch_bytes(int32_t bytes, F&& f) {
 // A walker with no applicable rule keeps C while input is still to come and
 // stops (halted = k) once it is not (reading A5).  Counts outside
 // [0, count_max] after a step are SNP_E_OVERFLOW.
-// cur / nxt / fired: W × m int32 walker-major scratch; the final states end
-// in cur.
+// cur / nxt: W × m int32 walker-major scratch (the final states end in cur);
+// fired: W × m uint64, the fired rule's c | p << 32 per neuron.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t splitmix64_dev(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ULL;
@@ -2080,7 +2080,7 @@ __device__ __forceinline__ uint64_t splitmix64_dev(uint64_t x) {
 constexpr int SAMPLE_WARPS = 4;
 
 __global__ void __launch_bounds__(SAMPLE_WARPS * 32) k_sample(SysView S, int64_t W, int32_t* cur, int32_t* nxt,
-                                                             int32_t* fired, uint64_t seed, int32_t steps,
+                                                             uint64_t* fired, uint64_t seed, int32_t steps,
                                                              int32_t input_neuron, const int32_t* train,
                                                              int32_t train_len, int32_t* halted, int32_t* err) {
   __shared__ int32_t nd_s[SAMPLE_WARPS][KMAX];
@@ -2091,7 +2091,8 @@ __global__ void __launch_bounds__(SAMPLE_WARPS * 32) k_sample(SysView S, int64_t
   const int32_t m = S.m;
   int32_t* C = cur + w * m;
   int32_t* N = nxt + w * m;
-  int32_t* Fr = fired + w * m;
+  uint64_t* Fr = fired + w * m;  // fired rule's c | p << 32 per neuron (0: none)
+  const bool tab8 = S.tables_ok && S.full8 && S.tab_full != nullptr;
   int32_t hs = -1;
   bool bad = false;
   for (int32_t k = 0; k < steps && !bad; ++k) {
@@ -2104,12 +2105,22 @@ __global__ void __launch_bounds__(SAMPLE_WARPS * 32) k_sample(SysView S, int64_t
       int d = 0, first = -1;
       if (s < m) {
         const int32_t v = C[s];
-        for (int r = S.rule_off[s]; r < S.rule_off[s + 1]; ++r)
-          if (rule_app(S.rules[r], v)) {
-            if (!d) first = r;
-            ++d;
+        if (tab8 && !(S.meta[s].flags & NM_GENERIC)) {  // uint8 tables: first rule, ND flag
+          const uint32_t e = __ldg(S.tab_full + (int64_t)s * 256 + (uint32_t)v);
+          if (e >> 4) {
+            first = S.rule_off[s] + (int)(e >> 4) - 1;
+            d = (e & TE_ND) ? count_applicable(S, s, v) : 1;
           }
-        Fr[s] = first;
+        } else {
+          for (int r = S.rule_off[s]; r < S.rule_off[s + 1]; ++r)
+            if (rule_app(S.rules[r], v)) {
+              if (!d) first = r;
+              ++d;
+            }
+        }
+        // consumption and emission of the fired rule (the ND choices below
+        // overwrite theirs)
+        Fr[s] = first >= 0 ? ((uint64_t)(uint32_t)S.rules[first].c | ((uint64_t)(uint32_t)S.rules[first].p << 32)) : 0;
       }
       any |= d > 0;
       if (d > 1) psi = sat_mul(psi, (uint64_t)d);
@@ -2141,18 +2152,15 @@ __global__ void __launch_bounds__(SAMPLE_WARPS * 32) k_sample(SysView S, int64_t
         for (int i = nnd - 1; i >= 0; --i) {
           const int32_t s = nd_s[wl][i];
           const uint64_t d = nd_d[wl][i];
-          Fr[s] = nth_applicable(S, s, C[s], (int)(t % d));
+          const int r = nth_applicable(S, s, C[s], (int)(t % d));
+          Fr[s] = (uint64_t)(uint32_t)S.rules[r].c | ((uint64_t)(uint32_t)S.rules[r].p << 32);
           t /= d;
         }
       }
       __syncwarp();
       for (int32_t j = lane; j < m; j += 32) {
-        const int32_t rj = Fr[j];
-        int64_t val = (int64_t)C[j] - (rj >= 0 ? S.rules[rj].c : 0);
-        for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) {
-          const int32_t rs = Fr[S.in_src[e]];
-          if (rs >= 0) val += S.rules[rs].p;
-        }
+        int64_t val = (int64_t)C[j] - (int64_t)(uint32_t)Fr[j];
+        for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) val += (int64_t)(Fr[S.in_src[e]] >> 32);
         if (j == input_neuron && input_left) val += train[k];
         bad |= val < 0 || val > S.count_max;
         N[j] = (int32_t)val;
@@ -2516,7 +2524,7 @@ void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_
   count_launch();
 }
 
-void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, int32_t* fired, uint64_t seed,
+void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, uint64_t* fired, uint64_t seed,
                    int32_t steps, int32_t input_neuron, const int32_t* train, int32_t train_len, int32_t* halted,
                    int32_t* err, cudaStream_t st) {
   const int64_t blocks = (W + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
