@@ -73,6 +73,11 @@ def lib() -> ctypes.CDLL:
         L.oracle_explore_gen.argtypes = [_P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _U64, _U64, _I32,
                                          ctypes.POINTER(_P)]
         L.oracle_explore_gen.restype = ctypes.c_int
+        L.oracle_children_delay.argtypes = [_P, _P, _P, _I64, _P, _P, ctypes.POINTER(_U64)]
+        L.oracle_children_delay.restype = ctypes.c_int
+        L.oracle_explore_delay.argtypes = [_P, _P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _U64, _U64,
+                                           ctypes.POINTER(_P)]
+        L.oracle_explore_delay.restype = ctypes.c_int
         L.oracle_sample.argtypes = [_P, _I64, _P, _U64, _I32, _I32, _P, _I32, _I32, _P]
         L.oracle_sample.restype = ctypes.c_int
         L.oracle_run_num_numbers.argtypes = [_P]
@@ -167,6 +172,39 @@ class System:
         Cn = np.zeros((k, self.m), np.int64)
         lib().oracle_children(self._h, _ptr(C), k, _ptr(S), _ptr(Cn), ctypes.byref(psi))
         return int(psi.value), S, Cn
+
+    # systems with delays (reading A26).  A state is the
+    # row [C | τ | π] of width 3m; `delays` gives d >= 0 per rule.
+    def children_delay(self, delays, X, cap: int = 1 << 20):
+        d = np.ascontiguousarray(delays, dtype=np.int32)
+        X = np.ascontiguousarray(X, dtype=np.int32)
+        assert d.shape == (self.n,) and X.shape == (3 * self.m,)
+        psi = _U64()
+        st = lib().oracle_children_delay(self._h, _ptr(d), _ptr(X), 0, None, None, ctypes.byref(psi))
+        if st != OR_OK:
+            raise OracleError(st)
+        k = min(int(psi.value), cap)
+        S = np.zeros((k, self.n), np.uint8)
+        Y = np.zeros((k, 3 * self.m), np.int64)
+        lib().oracle_children_delay(self._h, _ptr(d), _ptr(X), k, _ptr(S), _ptr(Y), ctypes.byref(psi))
+        return int(psi.value), S, Y
+
+    def explore_delay(self, delays, level0, depth: int, dedup: int = 0, count_bits: int = 32,
+                      frontier_target: int = 0, max_transitions: int = 0, seeds=(0x5EED0, 0x5EED1)) -> "Run":
+        """BFS over delayed states; level-0 rows have m columns (all neurons
+        open, τ = π = 0 appended) or 3m (oracle.cpp ``oracle_explore_delay``)."""
+        d = np.ascontiguousarray(delays, dtype=np.int32)
+        assert d.shape == (self.n,)
+        L0 = np.ascontiguousarray(np.atleast_2d(level0), dtype=np.int32)
+        if L0.shape[1] == self.m:
+            L0 = np.ascontiguousarray(np.hstack([L0, np.zeros((L0.shape[0], 2 * self.m), np.int32)]))
+        assert L0.shape[1] == 3 * self.m
+        h = _P()
+        st = lib().oracle_explore_delay(self._h, _ptr(d), L0.shape[0], _ptr(L0), depth, dedup, count_bits,
+                                        frontier_target, max_transitions, seeds[0], seeds[1], ctypes.byref(h))
+        if st == OR_E_ARG and not h:
+            raise OracleError(st, "bad argument")
+        return Run(self, h, st, 3 * self.m)
 
     def sample(self, walkers, seed: int, steps: int, input_neuron: int = -1, train=None, count_bits: int = 32):
         """Single-path sampling (oracle.cpp ``oracle_sample``): returns (final

@@ -524,6 +524,205 @@ int oracle_sample(const oracle_system* h, int64_t W, int32_t* configs, uint64_t 
   return OR_OK;
 }
 
+// ---------------------------------------------------------------------------
+// SN P systems WITH delays (the paper treats systems
+// without delays only, and names the delayed variant as the
+// adjacent model).  Reading A26, the standard semantics of
+// Ionescu-Păun-Yokomori: a rule E/a^c -> a^p; d fired at step t consumes c at
+// once; with d = 0 it emits p at step t; with d >= 1 the neuron is CLOSED at
+// steps t .. t+d-1 (it cannot fire and spikes sent to it are lost) and at step
+// t+d it emits p and is open again (it receives the spikes sent at t+d).
+// State of a neuron: (C, τ, π) = (spikes, remaining closed steps, spikes it
+// will emit when it reopens); a configuration is the row
+// [C_0..C_{m-1} | τ_0..τ_{m-1} | π_0..π_{m-1}] (width 3m).  One step:
+//   * open neurons (τ = 0) choose their rule exactly as without delays
+//     (applicability, one rule per neuron with applicable rules,
+//     readings A3/A4; enumeration order of Alg. 2, reading A7);
+//   * a closed neuron counts down: τ' = τ - 1, and emits π when τ' = 0;
+//   * a firing open neuron loses c; d = 0: emits p now; d >= 1: τ' = d, π' = p;
+//   * every neuron open after the step (τ' = 0) receives, from each in-neighbour
+//     that emits, its p spikes (one per synapse, reading A11).
+// Halting (reading A5 extended): no open neuron has an applicable rule and no
+// neuron is closed.  With no applicable rule but a closed neuron the state has
+// exactly one child (nobody fires, the clocks run).  With every d = 0 this is
+// eq. (2) on the first m columns and τ = π = 0 throughout.
+std::vector<std::vector<int64_t>> applicable_open(const System& sys, const std::vector<int64_t>& X) {
+  std::vector<std::vector<int64_t>> A(sys.m);
+  for (int64_t r = 0; r < sys.n; ++r) {
+    const int64_t sgm = sys.rules[r].neuron;
+    if (X[sys.m + sgm] == 0 && applicable(sys.rules[r], X)) A[sgm].push_back(r);
+  }
+  return A;
+}
+
+// syn of Def. 1 recovered from M (Def. 2): the out-neighbours of σ are the
+// nonzero off-diagonal columns of its spiking rules' rows (validate() checks
+// that they agree).
+std::vector<std::vector<int64_t>> synapses(const System& sys) {
+  std::vector<std::vector<int64_t>> syn(sys.m);
+  std::vector<int> done(sys.m, 0);
+  for (int64_t r = 0; r < sys.n; ++r) {
+    const Rule& R = sys.rules[r];
+    if (R.produced == 0 || done[R.neuron]) continue;
+    done[R.neuron] = 1;
+    for (const auto& jv : sys.M_rows[r])
+      if (jv.first != R.neuron && jv.second != 0) syn[R.neuron].push_back(jv.first);
+  }
+  return syn;
+}
+
+std::vector<int64_t> delayed_step(const System& sys, const std::vector<std::vector<int64_t>>& syn,
+                                  const std::vector<int32_t>& delay, const std::vector<int64_t>& X,
+                                  const std::vector<uint8_t>& S) {
+  const int64_t m = sys.m;
+  std::vector<int64_t> Y = X;
+  std::vector<int64_t> emit(m, 0);
+  for (int64_t s = 0; s < m; ++s)
+    if (X[m + s] >= 1) {  // closed: the clock runs
+      Y[m + s] = X[m + s] - 1;
+      if (Y[m + s] == 0) { emit[s] = X[2 * m + s]; Y[2 * m + s] = 0; }
+    }
+  for (int64_t r = 0; r < sys.n; ++r) {
+    if (!S[r]) continue;
+    const Rule& R = sys.rules[r];
+    Y[R.neuron] -= R.consumed;
+    if (delay[r] == 0) emit[R.neuron] = R.produced;
+    else { Y[m + R.neuron] = delay[r]; Y[2 * m + R.neuron] = R.produced; }
+  }
+  for (int64_t s = 0; s < m; ++s)
+    for (int64_t j : syn[s])
+      if (Y[m + j] == 0) Y[j] += emit[s];  // only open neurons receive
+  return Y;
+}
+
+// All children of one delayed state (width 3m), t = 0..Ψ-1.
+int oracle_children_delay(const oracle_system* h, const int32_t* delay32, const int32_t* X32, int64_t cap,
+                          uint8_t* S_out, int64_t* X_out, uint64_t* psi_out) {
+  const System& s = h->s;
+  std::vector<int32_t> delay(delay32, delay32 + s.n);
+  std::vector<int64_t> X(X32, X32 + 3 * s.m);
+  const auto syn = synapses(s);
+  auto A = applicable_open(s, X);
+  uint64_t psi = 0;
+  if (!count_children(A, &psi)) return OR_E_CAPACITY;
+  bool closed = false;
+  for (int64_t j = 0; j < s.m; ++j) closed = closed || X[s.m + j] != 0;
+  if (psi == 0 && closed) psi = 1;
+  *psi_out = psi;
+  for (uint64_t t = 0; t < psi && (int64_t)t < cap; ++t) {
+    auto S = spiking_vector(s, A, t);
+    auto Y = delayed_step(s, syn, delay, X, S);
+    if (S_out) memcpy(S_out + t * s.n, S.data(), s.n);
+    if (X_out) memcpy(X_out + t * 3 * s.m, Y.data(), 3 * s.m * sizeof(int64_t));
+  }
+  return OR_OK;
+}
+
+// Breadth-first tree over delayed states: the BFS, dedup (readings A6, A18),
+// thinning (A19) and overflow rules (A16, applied to all 3m columns) of
+// oracle_explore_gen; level0 rows have 3m columns.
+int oracle_explore_delay(const oracle_system* h, const int32_t* delay32, int64_t F0, const int32_t* level0,
+                         int32_t depth, int32_t dedup, int32_t count_bits, int64_t frontier_target,
+                         int64_t max_transitions, uint64_t seed0, uint64_t seed1, oracle_run** out) {
+  const System& s = h->s;
+  const int64_t width = 3 * s.m;
+  if (!out || !delay32 || F0 < 1 || depth < 0 || (dedup != 0 && dedup != 1)) return OR_E_ARG;
+  if (count_bits != 8 && count_bits != 16 && count_bits != 32) return OR_E_ARG;
+  std::vector<int32_t> delay(delay32, delay32 + s.n);
+  for (int32_t d : delay)
+    if (d < 0) return OR_E_ARG;
+  const auto syn = synapses(s);
+  const int64_t cmax = count_bits == 8 ? 255 : count_bits == 16 ? 65535 : 2147483647LL;
+  auto* hr = new oracle_run();
+  Run& run = hr->r;
+  *out = hr;
+  std::set<std::vector<int64_t>> visited_rows;
+  std::set<std::pair<uint64_t, uint64_t>> visited_fp;
+  auto seen = [&](const std::vector<int64_t>& X, const std::pair<uint64_t, uint64_t>& f) {
+    return dedup == 0 ? visited_rows.count(X) > 0 : visited_fp.count(f) > 0;
+  };
+  auto insert = [&](const std::vector<int64_t>& X, const std::pair<uint64_t, uint64_t>& f) {
+    if (dedup == 0) visited_rows.insert(X);
+    else visited_fp.insert(f);
+  };
+  auto push = [&](const std::vector<int64_t>& X, const std::pair<uint64_t, uint64_t>& f, int64_t parent, uint64_t t) {
+    run.configs.push_back(X);
+    run.parent.push_back(parent);
+    run.t.push_back(t);
+    run.fp0.push_back(f.first);
+    run.fp1.push_back(f.second);
+  };
+  auto children_count = [&](const std::vector<int64_t>& X, std::vector<std::vector<int64_t>>* A, uint64_t* psi) {
+    *A = applicable_open(s, X);
+    if (!count_children(*A, psi)) return false;
+    bool closed = false;
+    for (int64_t j = 0; j < s.m; ++j) closed = closed || X[s.m + j] != 0;
+    if (*psi == 0 && closed) *psi = 1;
+    return true;
+  };
+  run.level_offsets.push_back(0);
+  for (int64_t i = 0; i < F0; ++i) {
+    std::vector<int64_t> X(level0 + i * width, level0 + (i + 1) * width);
+    for (int64_t v : X)
+      if (v < 0 || v > cmax) { run.status = OR_E_OVERFLOW; run.error = "level 0 value out of range"; return run.status; }
+    auto f = fingerprint(X, seed0, seed1);
+    if (seen(X, f)) continue;
+    insert(X, f);
+    push(X, f, -1, 0);
+  }
+  run.level_offsets.push_back((int64_t)run.configs.size());
+  for (int32_t L = 0; L < depth; ++L) {
+    const int64_t lo = run.level_offsets[L], hi = run.level_offsets[L + 1];
+    if (lo == hi) break;
+    struct Cand { int64_t parent; uint64_t t; std::vector<int64_t> X; std::pair<uint64_t, uint64_t> f; };
+    std::vector<Cand> fresh;
+    std::set<std::vector<int64_t>> level_rows;
+    std::set<std::pair<uint64_t, uint64_t>> level_fp;
+    int64_t T = 0;
+    for (int64_t i = lo; i < hi; ++i) {
+      const std::vector<int64_t> X = run.configs[i];
+      std::vector<std::vector<int64_t>> A;
+      uint64_t psi = 0;
+      if (!children_count(X, &A, &psi)) { run.status = OR_E_CAPACITY; run.error = "psi above 2^62"; return run.status; }
+      for (uint64_t t = 0; t < psi; ++t) {
+        ++T;
+        if (max_transitions > 0 && T > max_transitions) { run.status = OR_E_CAPACITY; run.error = "transition budget exceeded"; return run.status; }
+        auto Y = delayed_step(s, syn, delay, X, spiking_vector(s, A, t));
+        auto f = fingerprint(Y, seed0, seed1);
+        if (seen(Y, f)) continue;
+        bool dup_here = dedup == 0 ? !level_rows.insert(Y).second : !level_fp.insert(f).second;
+        if (dup_here) continue;
+        fresh.push_back(Cand{i - lo, t, Y, f});
+      }
+    }
+    const int64_t n_new = (int64_t)fresh.size();
+    int64_t kept = 0;
+    const bool thin = frontier_target > 0 && n_new > frontier_target;
+    const uint64_t tau = thin ? oracle_thinning_tau(frontier_target, n_new) : 0;
+    for (const Cand& c : fresh) {
+      if (thin && !(fmix64(c.f.first) < tau)) continue;
+      for (int64_t v : c.X)
+        if (v < 0 || v > cmax) { run.status = OR_E_OVERFLOW; run.error = "value outside the storage range"; return run.status; }
+      insert(c.X, c.f);
+      push(c.X, c.f, c.parent, c.t);
+      ++kept;
+    }
+    run.level_T.push_back(T);
+    run.level_new.push_back(n_new);
+    run.level_kept.push_back(kept);
+    run.level_offsets.push_back((int64_t)run.configs.size());
+    if (kept == 0) break;
+  }
+  run.halting.resize(run.configs.size());
+  for (size_t i = 0; i < run.configs.size(); ++i) {
+    std::vector<std::vector<int64_t>> A;
+    uint64_t psi = 0;
+    children_count(run.configs[i], &A, &psi);
+    run.halting[i] = psi == 0 ? 1 : 0;
+  }
+  return OR_OK;
+}
+
 int64_t oracle_run_num_numbers(const oracle_run* h) { return (int64_t)h->r.numbers.size(); }
 void oracle_run_numbers(const oracle_run* h, int64_t* out) { std::copy(h->r.numbers.begin(), h->r.numbers.end(), out); }
 int oracle_run_status(const oracle_run* h) { return h->r.status; }
