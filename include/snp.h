@@ -159,6 +159,21 @@ snp_status snp_load(const snp_matrix *M, const snp_rule *rules, int64_t n_rules,
  * read for SNP_RE_UNARY rules only; may be NULL if there are none.           */
 snp_status snp_load_unary(const snp_matrix *M, const snp_rule *rules, int64_t n_rules, const uint64_t *re_bits,
                           const int32_t *C0, int64_t m, const snp_options *opt, snp_system **out);
+/* SN P systems WITH delays (the paper treats systems
+ * without delays; reading A26 in DESIGN.md §3).  delays: n_rules
+ * int32 d >= 0 (host, copied); a rule fired at step t with d >= 1 closes its
+ * neuron at steps t .. t+d-1 (it cannot fire; spikes sent to it are lost) and
+ * emits its p spikes at step t+d, when the neuron is open again.  The state
+ * is the row [C | τ | π] of snp_state_width = 3m entries (spikes, remaining
+ * closed steps, pending emission); C0 has m entries (τ = π = 0 appended) and
+ * level0 rows (snp_begin) have 3m.  Halting: no open neuron can fire and no
+ * neuron is closed.  Requires opt->dedup = 1 (child keys are fingerprints of
+ * the materialised children: the child state is not linear in the rule
+ * choice) and out_rule1 = 0; snp_sample, snp_dist_* and
+ * snp_tree_spiking_vectors return SNP_E_STATE for such a system.
+ * Errors as snp_load, plus SNP_E_ARG for a negative delay.                   */
+snp_status snp_load_delay(const snp_matrix *M, const snp_rule *rules, int64_t n_rules, const int32_t *delays,
+                          const int32_t *C0, int64_t m, const snp_options *opt, snp_system **out);
 void       snp_system_free(snp_system *sys);
 
 /* Launch all device work of `sys` on this cudaStream_t (NULL = library stream). */

@@ -147,6 +147,10 @@ struct SysView {
   const uint8_t* xyt;        // m × 32   first rule c | p << 4 for v < 32 (0 = none)
   const uint8_t* xyf;        // m × 256  the same for every uint8 count
   const uint8_t* btile;      // ceil(m/64) × 4096: B chunks (−R bytes | 1, Rout bytes), K-major core matrices
+  // SN P systems with delays (reading A26): delay_m > 0
+  // real neurons, the state row is [C | τ | π] (m = 3·delay_m columns)
+  int32_t delay_m;
+  const int32_t* delay;      // n: d >= 0 per rule
 };
 // key of a terminal child (second output spike): skipped by the dedup
 constexpr uint64_t KEY_TERMINAL1 = ~0ULL - 1;

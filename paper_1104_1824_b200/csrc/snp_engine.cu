@@ -204,7 +204,7 @@ struct snp_system {
   uint64_t vis_cap = 0, ltab_cap = 0, child_cap = 0;
   // scratch
   DBuf psi, off, fpb0, fpb1, ndc, nd, ebits;
-  DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab, d_elut, d_hsg, d_xyt, d_xyf, d_btile, d_ndl;
+  DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab, d_elut, d_hsg, d_xyt, d_xyf, d_btile, d_ndl, d_delay;
   DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   DBuf gen;           // generated-number bitmap (out_rule1 > 0)
@@ -1012,7 +1012,8 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     const uint64_t tag_base = 0;
     phase_begin(s, 1);
     launch_child_parent(off, F, C.cpar, st);
-    launch_child_keys(s->view, off, O, T, C, st);
+    if (s->view.delay_m > 0) launch_child_keys_delay(s->view, s->bytes, LV, off, O, T, C, st);
+    else launch_child_keys(s->view, off, O, T, C, st);
     if (s->view.aug_rule >= 0) launch_aug_keys(s->view, s->bytes, LV, off, O, T, C, err, st);
     phase_end(s);
     phase_begin(s, 2);
@@ -1169,23 +1170,10 @@ snp_status tree_check(const snp_tree* t, bool need_data) {
   return SNP_OK;
 }
 
-}  // namespace
-
-// ===========================================================================
-// C ABI
-// ===========================================================================
-extern "C" {
-
-int snp_abi_version(void) { return SNP_ABI_VERSION; }
-const char* snp_last_error(void) { return g_err.c_str(); }
-
-snp_status snp_load(const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const int32_t* C0, int64_t m,
-                    const snp_options* opt, snp_system** out) {
-  return snp_load_unary(M, rules, n_rules, nullptr, C0, m, opt, out);
-}
-
-snp_status snp_load_unary(const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const uint64_t* re_bits,
-                          const int32_t* C0, int64_t m, const snp_options* opt, snp_system** out) {
+// snp_load_unary / snp_load_delay: validate, widen the state (generated
+// numbers: + 1 column; delays: + 2m columns for τ and π), build the device system.
+snp_status load_full(const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const uint64_t* re_bits,
+                     const int32_t* delays, const int32_t* C0, int64_t m, const snp_options* opt, snp_system** out) {
   if (!M || !C0 || !out || m < 1 || m > 0x7FFFFFFF || n_rules < 0 || (n_rules > 0 && !rules))
     return fail(SNP_E_ARG, "snp_load: bad arguments");
   if (M->n_rules != n_rules || M->n_neurons != m) return fail(SNP_E_ARG, "snp_load: matrix shape != (n_rules, m)");
@@ -1211,10 +1199,18 @@ snp_status snp_load_unary(const snp_matrix* M, const snp_rule* rules, int64_t n_
   // k_aug_fix); M and C0 are widened by one zero column
   const int32_t out_rule = o.out_rule1 - 1;
   if (o.out_rule1 < 0 || out_rule >= n_rules) return fail(SNP_E_ARG, "out_rule1 must be 0 (off) or 1..n_rules");
+  // systems with delays (reading A26): + 2m columns τ, π
+  if (delays) {
+    if (out_rule >= 0) return fail(SNP_E_ARG, "delays and generated numbers cannot be combined");
+    if (o.dedup != 1) return fail(SNP_E_ARG, "systems with delays need dedup = 1 (fingerprint keys)");
+    for (int64_t r = 0; r < n_rules; ++r)
+      if (delays[r] < 0) return fail(SNP_E_ARG, "rule %lld: delay < 0", (long long)r);
+  }
+  const int64_t extra = out_rule >= 0 ? 1 : (delays ? 2 * m : 0);
   snp_matrix Maug{};
   std::vector<int64_t> arp;
   std::vector<int32_t> acol, aval, aC0;
-  if (out_rule >= 0) {
+  if (extra > 0) {
     arp.push_back(0);
     for (int64_t r = 0; r < n_rules; ++r) {
       if (M->dense) {
@@ -1231,18 +1227,26 @@ snp_status snp_load_unary(const snp_matrix* M, const snp_rule* rules, int64_t n_
     }
     acol.push_back(0);  // keep data() non-null
     aval.push_back(0);
-    Maug = snp_matrix{n_rules, m + 1, nullptr, arp.data(), acol.data(), aval.data()};
+    Maug = snp_matrix{n_rules, m + extra, nullptr, arp.data(), acol.data(), aval.data()};
     aC0.assign(C0, C0 + m);
-    aC0.push_back(0);
+    aC0.resize(m + extra, 0);
   }
   auto s = std::make_unique<snp_system>();
-  s->m = out_rule >= 0 ? m + 1 : m;
+  s->m = m + extra;
   s->opt = o;
   s->bytes = o.count_bits / 8;
   s->count_max = o.count_bits == 8 ? 255 : o.count_bits == 16 ? 65535 : 0x7FFFFFFF;
-  snp_status st = out_rule >= 0 ? load_impl(s.get(), &Maug, rules, n_rules, re_bits, aC0.data())
-                                : load_impl(s.get(), M, rules, n_rules, re_bits, C0);
+  snp_status st = extra > 0 ? load_impl(s.get(), &Maug, rules, n_rules, re_bits, aC0.data())
+                            : load_impl(s.get(), M, rules, n_rules, re_bits, C0);
   if (st != SNP_OK) return st;
+  s->view.delay_m = 0;
+  s->view.delay = nullptr;
+  if (delays) {
+    SNP_TRY(upload(s.get(), s->d_delay, std::vector<int32_t>(delays, delays + n_rules)));
+    s->view.delay_m = (int32_t)m;
+    s->view.delay = s->d_delay.as<int32_t>();
+    s->view.tc_ok = 0;  // child keys are not linear in the rule choice (reading A26)
+  }
   s->view.aug_rule = out_rule;
   s->view.aug_neuron = out_rule >= 0 ? rules[out_rule].neuron : -1;
   s->view.gen_bits = nullptr;
@@ -1255,6 +1259,33 @@ snp_status snp_load_unary(const snp_matrix* M, const snp_rule* rules, int64_t n_
   }
   *out = s.release();
   return SNP_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int snp_abi_version(void) { return SNP_ABI_VERSION; }
+const char* snp_last_error(void) { return g_err.c_str(); }
+
+snp_status snp_load(const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const int32_t* C0, int64_t m,
+                    const snp_options* opt, snp_system** out) {
+  return snp_load_unary(M, rules, n_rules, nullptr, C0, m, opt, out);
+}
+
+snp_status snp_load_unary(const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const uint64_t* re_bits,
+                          const int32_t* C0, int64_t m, const snp_options* opt, snp_system** out) {
+  return load_full(M, rules, n_rules, re_bits, nullptr, C0, m, opt, out);
+}
+
+snp_status snp_load_delay(const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const int32_t* delays,
+                          const int32_t* C0, int64_t m, const snp_options* opt, snp_system** out) {
+  if (!delays && n_rules > 0) return fail(SNP_E_ARG, "snp_load_delay: no delays");
+  static const int32_t none = 0;
+  return load_full(M, rules, n_rules, nullptr, delays ? delays : &none, C0, m, opt, out);
 }
 
 void snp_system_free(snp_system* s) {
@@ -1405,6 +1436,7 @@ snp_status snp_sample(snp_system* s, int64_t W, int32_t* configs, uint64_t seed,
       (train_len > 0 && !train) || input_neuron >= s->m || input_neuron < -1)
     return fail(SNP_E_ARG, "snp_sample: bad arguments");
   if (s->view.aug_rule >= 0) return fail(SNP_E_STATE, "snp_sample: not available with generated numbers (out_rule1)");
+  if (s->view.delay_m > 0) return fail(SNP_E_STATE, "snp_sample: not available for systems with delays");
   const int64_t m = s->m;
   for (int64_t i = 0; i < W * m; ++i)
     if (configs[i] < 0 || configs[i] > s->count_max)
@@ -1499,6 +1531,7 @@ snp_status snp_tree_spiking_vectors(const snp_tree* t, int32_t level, uint8_t* S
   SNP_TRY(tree_check(t, true));
   snp_system* s = t->sys;
   if (level < 1 || level >= snp_tree_num_levels(t)) return fail(SNP_E_ARG, "level must be in [1, num_levels)");
+  if (s->view.delay_m > 0) return fail(SNP_E_STATE, "spiking vectors of systems with delays are not available");
   const Level* par = s->levels[level - 1].get();
   const Level* lv = s->levels[level].get();
   if (!lv->F) return SNP_OK;
@@ -1549,6 +1582,7 @@ snp_status snp_dist_begin(snp_system* s, const snp_configs* level0, int32_t nran
   if (!s || !level0 || nranks < 1) return fail(SNP_E_ARG, "snp_dist_begin: bad arguments");
   if (s->opt.dedup != 1) return fail(SNP_E_STATE, "distributed exploration needs dedup = 1 (fingerprint keys)");
   if (s->view.aug_rule >= 0) return fail(SNP_E_STATE, "distributed exploration does not support generated numbers");
+  if (s->view.delay_m > 0) return fail(SNP_E_STATE, "distributed exploration does not support delays");
   const int64_t F0 = level0->n_configs, m = s->m;
   if (F0 < 0 || F0 > 0x7FFFFFFFLL || (F0 > 0 && !level0->data)) return fail(SNP_E_ARG, "level0: bad n_configs / data");
   if (level0->elem_bytes != 1 && level0->elem_bytes != 2 && level0->elem_bytes != 4) return fail(SNP_E_ARG, "level0: elem_bytes");

@@ -131,6 +131,9 @@ void launch_unperm(const uint64_t* perm, const uint8_t* back, uint64_t T, uint64
 void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_data, const int64_t* parent,
                             const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st);
 
+// systems with delays: child keys of materialised children
+void launch_child_keys_delay(const SysView& S, int32_t bytes, const LevelView& L, const uint64_t* off,
+                             const ExpandOut& O, uint64_t T, const ChildArrays& C, cudaStream_t st);
 // single-path sampling: W walkers, all steps in one launch
 void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, uint64_t* fired, uint64_t seed,
                    int32_t steps, int32_t input_neuron, const int32_t* train, int32_t train_len, int32_t* halted,

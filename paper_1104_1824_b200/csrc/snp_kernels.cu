@@ -2055,6 +2055,132 @@ void dispatch_bytes(int32_t bytes, F&& f) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// SN P systems WITH delays (reading A26; SysView::
+// delay_m = m > 0).  A state is the row [C | τ | π] of width S.m = 3m
+// (spikes, remaining closed steps, pending emission).  Open neurons (τ = 0)
+// choose rules as without delays; a closed neuron counts down and emits π
+// when it reopens; a firing rule with d >= 1 closes its neuron for d steps
+// (τ' = d, π' = p); only neurons open after the step receive.  The child
+// state is not linear in the rule choice (a neuron that closes loses its
+// incoming spikes), so child keys are computed from the materialised child.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_expand_delay(SysView S, LevelView L, ExpandOut O) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool valid = p < L.F;
+  bool halt = false;
+  if (valid) {
+    const int32_t m = S.delay_m;
+    int ndc = 0;
+    uint64_t psi = 1;
+    bool any = false, closed = false;
+    for (int32_t s = 0; s < m; ++s) {
+      if (ld_count<T>(L.data, p, m + s, S.m) != 0) {
+        closed = true;
+        continue;
+      }
+      const int32_t v = ld_count<T>(L.data, p, s, S.m);
+      const int d = count_applicable(S, s, v);
+      any |= d > 0;
+      if (d >= 2 && !O.classify_only) nd_event(S, O, s, (uint32_t)v, p, ndc, psi);
+    }
+    halt = !any && !closed;  // reading A26: nothing can fire and no clock runs
+    O.halting[p] = halt ? 1 : 0;
+    if (!O.classify_only) {
+      psi = any ? psi : (closed ? 1 : 0);  // only clocks running: one child
+      O.psi[p] = psi;
+      O.ndc[p] = ndc;
+      if (psi > PSI_LIMIT || ndc > KMAX) atomicOr(O.err, ERR_CAPACITY);
+    }
+  }
+  const unsigned nh = __popc(__ballot_sync(0xFFFFFFFFu, halt));
+  if ((threadIdx.x & 31) == 0 && nh) atomicAdd(O.n_halting, (unsigned long long)nh);
+}
+
+// column j of the child of parent p described by cx (reading A26)
+template <typename T>
+__device__ int64_t delay_value(const SysView& S, const void* data, int64_t p, int32_t j, const ChildCtx& cx) {
+  const int32_t m = S.delay_m;
+  auto tau = [&](int32_t s) { return (int64_t)ld_count<T>(data, p, m + s, S.m); };
+  auto fired = [&](int32_t s) { return tau(s) ? -1 : fired_rule(S, s, ld_count<T>(data, p, s, S.m), cx); };
+  auto tau_next = [&](int32_t s) -> int64_t {
+    const int64_t t0 = tau(s);
+    if (t0 >= 1) return t0 - 1;
+    const int r = fired(s);
+    return r >= 0 ? S.delay[r] : 0;
+  };
+  auto emit = [&](int32_t s) -> int64_t {
+    const int64_t t0 = tau(s);
+    if (t0 >= 1) return t0 == 1 ? (int64_t)ld_count<T>(data, p, 2 * m + s, S.m) : 0;
+    const int r = fired(s);
+    return (r >= 0 && S.delay[r] == 0) ? S.rules[r].p : 0;
+  };
+  if (j >= 2 * m) {  // π'
+    const int32_t s = j - 2 * m;
+    const int64_t t0 = tau(s);
+    if (t0 >= 1) return t0 == 1 ? 0 : (int64_t)ld_count<T>(data, p, 2 * m + s, S.m);
+    const int r = fired(s);
+    return (r >= 0 && S.delay[r] >= 1) ? S.rules[r].p : 0;
+  }
+  if (j >= m) return tau_next(j - m);  // τ'
+  const int r = fired(j);
+  int64_t val = (int64_t)ld_count<T>(data, p, j, S.m) - (r >= 0 ? S.rules[r].c : 0);
+  if (tau_next(j) == 0)  // open after the step: receives
+    for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) val += emit(S.in_src[e]);
+  return val;
+}
+
+// child keys: warp per child, fingerprint of the materialised child (A18)
+template <typename T>
+__global__ void k_child_keys_delay(SysView S, LevelView L, const uint64_t* off, ExpandOut O, uint64_t T_,
+                                   ChildArrays C) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = warp; c < T_; c += nwarps) {
+    const int64_t p = C.cpar[c];
+    ChildCtx cx;
+    decode_child(S, O.nd + p * KMAX, O.ndc[p], c - off[p], cx);
+    uint64_t f0 = 0, f1 = 0;
+    for (int32_t j = lane; j < S.m; j += 32) {
+      const uint64_t v = (uint64_t)delay_value<T>(S, L.data, p, j, cx);
+      f0 += v * S.R0[j];
+      f1 += v * S.R1[j];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      f0 += __shfl_xor_sync(0xFFFFFFFFu, f0, o);
+      f1 += __shfl_xor_sync(0xFFFFFFFFu, f1, o);
+    }
+    if (lane == 0) {
+      C.cfp0[c] = f0;
+      C.cfp1[c] = f1;
+    }
+  }
+}
+
+// K-c: every kept child, exactly (warp per child)
+template <typename T>
+__global__ void k_materialize_delay(SysView S, LevelView L, ExpandOut O, NextArrays N, int64_t K, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  T* out = reinterpret_cast<T*>(N.data);
+  for (int64_t q = warp; q < K; q += nwarps) {
+    const int64_t p = N.parent[q];
+    ChildCtx cx;
+    decode_child(S, O.nd + p * KMAX, O.ndc[p], N.t[q], cx);
+    bool bad = false;
+    for (int32_t j = lane; j < S.m; j += 32) {
+      const int64_t val = delay_value<T>(S, L.data, p, j, cx);
+      bad |= val < 0 || val > S.count_max;
+      out[eidx(q, j, S.m)] = (T)val;
+    }
+    if (bad) atomicOr(err, ERR_OVERFLOW);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Single-path sampling with an input spike train (Def. 1
 // `in`; deep trees take long to explore).  One
 // warp per walker runs every step (walkers are independent: no grid sync).
@@ -2217,7 +2343,7 @@ bool materialize_stage_e(const SysView& S, int32_t bytes) {
 
 bool fast_materialize_ok(const SysView& S) {
   const int32_t w = S.count_max <= 255 ? 1 : S.count_max <= 65535 ? 2 : 4;
-  return S.tables_ok && S.binary_emit && S.max_indeg < 256 && materialize_smem_bytes(S, w, false) <= KC_SMEM_MAX;
+  return S.delay_m == 0 && S.tables_ok && S.binary_emit && S.max_indeg < 256 && materialize_smem_bytes(S, w, false) <= KC_SMEM_MAX;
 }
 
 void launch_import(const void* src, int32_t src_bytes, int32_t src_layout, int64_t src_ld, int64_t F, int32_t m,
@@ -2257,7 +2383,9 @@ static unsigned expand_grid(int64_t F) { return (unsigned)((F + XW * XTILE - 1) 
 void launch_expand(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, cudaStream_t st) {
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    if (!fast_expand_ok(S)) {
+    if (S.delay_m > 0) {
+      k_expand_delay<T><<<grid_for(L.F), BLK, 0, st>>>(S, L, O);
+    } else if (!fast_expand_ok(S)) {
       k_expand_g<T><<<expand_grid(L.F), XW * 32, 0, st>>>(S, L, O);
     } else {
       const bool full = S.full8 && sizeof(T) == 1;
@@ -2363,7 +2491,8 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
     if (g > 148u * 32u) g = 148u * 32u;
     dispatch_bytes(bytes, [&](auto tt) {
       using T = decltype(tt);
-      k_materialize_exact<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
+      if (S.delay_m > 0) k_materialize_delay<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
+      else k_materialize_exact<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
     });
   }
   count_launch();
@@ -2520,6 +2649,17 @@ void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_
     using T = decltype(tt);
     k_spiking_vectors<T><<<grid_for(K, 128), 128, 0, st>>>(S, reinterpret_cast<const T*>(parent_data), parent, t, K,
                                                          S_out);
+  });
+  count_launch();
+}
+
+void launch_child_keys_delay(const SysView& S, int32_t bytes, const LevelView& L, const uint64_t* off,
+                             const ExpandOut& O, uint64_t T, const ChildArrays& C, cudaStream_t st) {
+  unsigned g = grid_for(T * 32, 256);
+  if (g > 148u * 64u) g = 148u * 64u;
+  dispatch_bytes(bytes, [&](auto tt) {
+    using TT = decltype(tt);
+    k_child_keys_delay<TT><<<g, 256, 0, st>>>(S, L, off, O, T, C);
   });
   count_launch();
 }

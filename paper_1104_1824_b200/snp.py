@@ -33,7 +33,7 @@ SNP_LAYOUT_ROW_MAJOR = 0
 SNP_LAYOUT_NEURON_MAJOR = 1
 
 EXPORTED = [
-    "snp_abi_version", "snp_last_error", "snp_load", "snp_load_unary", "snp_system_free", "snp_set_stream", "snp_begin",
+    "snp_abi_version", "snp_last_error", "snp_load", "snp_load_unary", "snp_load_delay", "snp_system_free", "snp_set_stream", "snp_begin",
     "snp_advance", "snp_frontier_size", "snp_state_width", "snp_generated_numbers", "snp_depth", "snp_summary",
     "snp_explore", "snp_step", "snp_sample",
     "snp_tree_num_levels", "snp_tree_num_configs", "snp_tree_level_offsets", "snp_tree_configs",
@@ -110,6 +110,8 @@ def lib() -> ctypes.CDLL:
         L.snp_frontier_size.restype = ctypes.c_int64
         L.snp_load_unary.argtypes = [ctypes.POINTER(snp_matrix), _P, ctypes.c_int64, _P, _P, ctypes.c_int64,
                                      ctypes.POINTER(snp_options), ctypes.POINTER(_P)]
+        L.snp_load_delay.argtypes = [ctypes.POINTER(snp_matrix), _P, ctypes.c_int64, _P, _P, ctypes.c_int64,
+                                     ctypes.POINTER(snp_options), ctypes.POINTER(_P)]
         L.snp_state_width.argtypes = [_P]
         L.snp_state_width.restype = ctypes.c_int64
         L.snp_generated_numbers.argtypes = [_P, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
@@ -168,7 +170,7 @@ def _ptr(a: np.ndarray):
 # ---- C-named entry points (marshalling only) --------------------------------
 def snp_load(rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.ndarray, C0: np.ndarray,
              count_bits=32, dedup=0, frontier_target=0, max_transitions=0, fp_seed=(0x5EED0, 0x5EED1),
-             keep_tree=1, out_rule=None, re_bits=None):
+             keep_tree=1, out_rule=None, re_bits=None, delays=None):
     rules = np.ascontiguousarray(rules, np.int32).reshape(-1, 6)
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col = np.ascontiguousarray(col, np.int32)
@@ -178,7 +180,13 @@ def snp_load(rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.nd
     o = snp_options(count_bits, dedup, frontier_target, max_transitions, (ctypes.c_uint64 * 2)(*fp_seed),
                     keep_tree, 0 if out_rule is None else int(out_rule) + 1)
     h = _P()
-    if re_bits is None:
+    if delays is not None:
+        d = np.ascontiguousarray(delays, np.int32)
+        if d.shape != (rules.shape[0],):
+            raise ValueError("delays: one int32 per rule")
+        _check(lib().snp_load_delay(ctypes.byref(M), _ptr(rules), rules.shape[0], _ptr(d), _ptr(C0), C0.shape[0],
+                                    ctypes.byref(o), ctypes.byref(h)))
+    elif re_bits is None:
         _check(lib().snp_load(ctypes.byref(M), _ptr(rules), rules.shape[0], _ptr(C0), C0.shape[0], ctypes.byref(o),
                               ctypes.byref(h)))
     else:
@@ -205,16 +213,18 @@ class System:
     """Owning wrapper of an ``snp_system*``."""
 
     def __init__(self, workload, count_bits=32, dedup=0, frontier_target=0, max_transitions=0,
-                 fp_seed=(0x5EED0, 0x5EED1), keep_tree=1, out_rule=None):
+                 fp_seed=(0x5EED0, 0x5EED1), keep_tree=1, out_rule=None, delays=None):
         """out_rule: generated numbers (include/snp.h) with that output rule;
-        configurations then have ``width = m + 1`` entries (last = A)."""
+        configurations then have ``width = m + 1`` entries (last = A).
+        delays: one d >= 0 per rule (snp_load_delay, SURVEY §8(f) NEXT-3);
+        configurations then have ``width = 3m`` entries [C | τ | π]."""
         self.m = int(workload.m)
         self.n = int(workload.rules.shape[0])
         self.count_bits = count_bits
         self._h = None
         self._h = snp_load(workload.rules, workload.row_ptr, workload.col, workload.val, workload.C0,
                            count_bits, dedup, frontier_target, max_transitions, fp_seed, keep_tree, out_rule,
-                           getattr(workload, "re_bits", None))
+                           getattr(workload, "re_bits", None), delays)
         self.width = int(lib().snp_state_width(self._h))
 
     def generated_numbers(self) -> set:
@@ -269,10 +279,11 @@ class System:
             _check(lib().snp_begin(self._h, ctypes.byref(c)))
 
     def _widen(self, rows):
-        """Generated-numbers mode: rows of m counts get A = 0 appended."""
+        """Generated-numbers mode: rows of m counts get A = 0 appended; delays
+        mode: rows of m counts get τ = π = 0 (2m zero columns) appended."""
         rows = np.atleast_2d(rows)
-        if self.width == self.m + 1 and rows.shape[1] == self.m:
-            rows = np.hstack([rows, np.zeros((rows.shape[0], 1), rows.dtype)])
+        if self.width != self.m and rows.shape[1] == self.m:
+            rows = np.hstack([rows, np.zeros((rows.shape[0], self.width - self.m), rows.dtype)])
         return rows
 
     def advance(self) -> dict:
