@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
     const int32_t s = c * TCK + k;
     // entries (c | p << 4) of the 32 counts: 16- or 32-entry byte-permute
     // lookups (warp-uniform choice), the full table for a count >= 32
-    uint32_t e[8], tt[8];
+    uint32_t e[8], tt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     tc::bar_wait(&lbar[sl], (uint32_t)((c / TC_IN) & 1));
     // the next chunk's inputs go to slot (c + 1) % 3, last read by the MMAs
     // of chunk c - 2 (done: issued two chunks ago) and by the table loads of
@@ -923,16 +923,19 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
       stage_inputs(c + 1);
     }
     {
-      const uint4 t0 = reinterpret_cast<const uint4*>(sT + k * 32)[0];
-      const uint4 t1 = reinterpret_cast<const uint4*>(sT + k * 32)[1];
-      tt[0] = t0.x; tt[1] = t0.y; tt[2] = t0.z; tt[3] = t0.w;
-      tt[4] = t1.x; tt[5] = t1.y; tt[6] = t1.z; tt[7] = t1.w;
-    }
-    {
       uint32_t hiv = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) hiv |= w[i];
-      if (__all_sync(0xFFFFFFFFu, (hiv & 0xF0F0F0F0u) == 0)) {
+      // the first 16 table entries always; the next 16 only when some count
+      // of the warp is >= 16
+      const uint4 t0 = reinterpret_cast<const uint4*>(sT + k * 32)[0];
+      tt[0] = t0.x; tt[1] = t0.y; tt[2] = t0.z; tt[3] = t0.w;
+      const bool small = __all_sync(0xFFFFFFFFu, (hiv & 0xF0F0F0F0u) == 0);
+      if (!small) {
+        const uint4 t1 = reinterpret_cast<const uint4*>(sT + k * 32)[1];
+        tt[4] = t1.x; tt[5] = t1.y; tt[6] = t1.z; tt[7] = t1.w;
+      }
+      if (small) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) e[i] = lut16(w[i], tt);
       } else if ((hiv & 0xE0E0E0E0u) == 0) {
