@@ -835,7 +835,7 @@ constexpr int TC_IN = 3;                         // B tile + tables: a ring of 3
 constexpr int TC_TTAB = TCK * 32;              // the chunk's 32-entry X|Y tables (2 KB)
 constexpr int TC_INB = 2 * TC_BTILE + TC_TTAB;  // one input slot: B tiles (X, Y) + tables
 
-size_t expand_tc_smem_bytes() { return (size_t)TC_STAGES * TC_STAGE + (size_t)TC_IN * TC_INB + 64 + 16; }
+size_t expand_tc_smem_bytes() { return (size_t)TC_STAGES * TC_STAGE + (size_t)TC_IN * TC_INB + 64 + 32; }
 
 // t[v] for the four byte counts v < 16 of v4, t = 16 bytes in tt[0..3]
 __device__ __forceinline__ uint32_t lut16(uint32_t v4, const uint32_t (&tt)[8]) {
@@ -916,7 +916,7 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
     tc::bar_wait(&lbar[sl], (uint32_t)((c / TC_IN) & 1));
     // the next chunk's inputs go to slot (c + 1) % 3, last read by the MMAs
     // of chunk c - 2 (done: issued two chunks ago) and by the table loads of
-    // chunk c - 2 (before this thread's previous __syncthreads)
+    // chunk c - 2 (before every thread's __syncthreads of chunk c - 2)
     if (tid == 0 && c + 1 < nch) {
       if (c >= 2) tc::bar_wait(&bar[st], (uint32_t)(((c - 2) >> 1) & 1));
       tc::fence_async_smem();
@@ -983,6 +983,8 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
       *reinterpret_cast<uint4*>(sY + off) = make_uint4(Y[0], Y[1], Y[2], Y[3]);
       *reinterpret_cast<uint4*>(sY + off + 128) = make_uint4(Y[4], Y[5], Y[6], Y[7]);
     }
+    // (a per-stage mbarrier that only the MMA-issuing thread waits on, letting
+    // the other warps run ahead, measured slower than this barrier)
     tc::fence_async_smem();
     __syncthreads();
     if (tid == 0) {
