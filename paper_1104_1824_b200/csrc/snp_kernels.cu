@@ -1825,8 +1825,9 @@ __global__ void k_materialize_exact(SysView S, LevelView L, ExpandOut O, NextArr
   }
 }
 
-// Exact correction of every (neuron, child) touched by a non-first ND choice:
-// the ND neuron itself (consumption) and its out-neighbours (emission).
+// Correction of every (neuron, child) touched by a non-first ND choice: the
+// ND neuron itself (consumption) and its out-neighbours (emission), by the
+// linear delta of eq. (2) on K-c's base values.
 template <typename T>
 __global__ void k_patch(SysView S, LevelView L, ExpandOut O, NextArrays N, int64_t K, int32_t* err) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < K; q += (int64_t)gridDim.x * blockDim.x) {
@@ -1836,14 +1837,29 @@ __global__ void k_patch(SysView S, LevelView L, ExpandOut O, NextArrays N, int64
     ChildCtx cx;
     decode_child(S, O.nd + p * KMAX, O.ndc[p], t, cx);
     T* out = reinterpret_cast<T*>(N.data);
+    // eq. (2) is linear in S: child = base child + Σ_{ND s, x_s ≠ 0}
+    // (M[chosen_s] − M[first_s]), i.e. −(c_chosen − c_first) at s and
+    // +(p_chosen − p_first) at every out-neighbour of s, applied to the base
+    // values K-c wrote (a base value outside the storage range is rewritten
+    // exactly afterwards by k_overflow_fix)
     for (int i = 0; i < cx.K; ++i) {
       if (!cx.x[i]) continue;
       const int32_t s = cx.s[i];
+      const int32_t v = (int32_t)(uint32_t)O.nd[p * KMAX + i];
+      const DevRule& rf = S.rules[nth_applicable(S, s, v, 0)];
+      const DevRule& rc = S.rules[nth_applicable(S, s, v, cx.x[i])];
+      const int64_t dc = (int64_t)rc.c - rf.c, dp = (int64_t)rc.p - rf.p;
       for (int e = -1; e < S.out_off[s + 1] - S.out_off[s]; ++e) {
         const int32_t j = e < 0 ? s : S.out_dst[S.out_off[s] + e];
-        const int64_t val = exact_value<T>(S, L.data, p, j, cx);
-        if (val < 0 || val > S.count_max) atomicOr(err, ERR_OVERFLOW);
-        out[eidx(q, j, S.m)] = (T)val;
+        const int64_t d = e < 0 ? -dc : dp;
+        if (!d) continue;
+        T* o = out + eidx(q, j, S.m);
+        int64_t val = (int64_t)*o + d;
+        if (val < 0 || val > S.count_max) {  // rare: recompute exactly (the base may have wrapped)
+          val = exact_value<T>(S, L.data, p, j, cx);
+          if (val < 0 || val > S.count_max) atomicOr(err, ERR_OVERFLOW);
+        }
+        *o = (T)val;
       }
     }
   }
