@@ -1398,6 +1398,10 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_WARPS
 #define SNP_KC_WARPS 32
 #endif
+// tuning toggles (tools/gpu_ab.sh), measured at config 4: 32 warps with
+// 64 registers beat 24 warps (70.4 ms) and 16 warps (83 ms); loading the row
+// before the gather (SNP_KC_PREFETCH=1: 68.6 ms) or one iteration ahead
+// (77 ms, spills) loses to loading it where it is used (66.5 ms)
 #ifndef SNP_KC_PREFETCH
 #define SNP_KC_PREFETCH 0
 #endif
