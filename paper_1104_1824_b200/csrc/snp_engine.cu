@@ -183,6 +183,7 @@ struct snp_system {
   int64_t count_max = 0;
   std::vector<int32_t> C0;
   bool binary_emit = true;
+  bool small_rules = true;  // every c, p <= 255 (k_sample_cta)
   // ---- device system
   DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1, d_in_pad, d_in_pad16, d_in_pad_off;
   SysView view{};
@@ -540,6 +541,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   std::vector<int32_t> rule_off(m + 1, 0);
   std::vector<DevRule> dr(n);
   s->binary_emit = true;
+  s->small_rules = true;
   for (int64_t r = 0; r < n; ++r) {
     const snp_rule& R = rules[r];
     rule_off[R.neuron + 1]++;
@@ -568,6 +570,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     d.jmask = (d.j & (d.j - 1)) == 0 ? d.j - 1 : -1;
     dr[r] = d;
     if (R.produced > 1) s->binary_emit = false;
+    if (R.consumed > 255 || R.produced > 255) s->small_rules = false;
   }
   for (int64_t j = 0; j < m; ++j) rule_off[j + 1] += rule_off[j];
   // fingerprint weights R_ℓ[j] = splitmix64(seed_ℓ ^ j) | 1 and h_ℓ[r] = Σ_j M[r][j]·R_ℓ[j]
@@ -1456,7 +1459,7 @@ snp_status snp_sample(snp_system* s, int64_t W, int32_t* configs, uint64_t seed,
   if (train_len > 0)
     CUDA_TRY(cudaMemcpyAsync(dtrain.p, train, (size_t)train_len * 4, cudaMemcpyHostToDevice, s->stream));
   launch_sample(s->view, W, cur.as<int32_t>(), nxt.as<int32_t>(), fired.as<uint64_t>(), seed, steps, input_neuron,
-                dtrain.as<int32_t>(), train_len, halted.as<int32_t>(), derr.as<int32_t>(), s->stream);
+                dtrain.as<int32_t>(), train_len, halted.as<int32_t>(), derr.as<int32_t>(), s->small_rules, s->stream);
   CUDA_TRY(cudaGetLastError());
   int32_t err = 0;
   CUDA_TRY(cudaMemcpyAsync(&err, derr.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));

@@ -137,7 +137,7 @@ void launch_child_keys_delay(const SysView& S, int32_t bytes, const LevelView& L
 // single-path sampling: W walkers, all steps in one launch
 void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, uint64_t* fired, uint64_t seed,
                    int32_t steps, int32_t input_neuron, const int32_t* train, int32_t train_len, int32_t* halted,
-                   int32_t* err, cudaStream_t st);
+                   int32_t* err, bool small_rules, cudaStream_t st);
 
 // CUB exclusive scan of n uint64 values (temp storage managed by the caller).
 size_t scan_temp_bytes(int64_t n);

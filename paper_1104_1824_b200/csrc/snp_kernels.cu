@@ -2334,6 +2334,137 @@ __global__ void __launch_bounds__(SAMPLE_WARPS * 32) k_sample(SysView S, int64_t
   if (lane == 0) halted[w] = hs;
 }
 
+// Sampling, one CTA per walker (every rule has c, p <= 255): the fired
+// rule's (c, p) of every neuron lives in shared memory as 16 bits, so the
+// in-synapse gather of the transition reads shared memory; the few neurons
+// with >= 2 applicable rules are collected unordered and sorted by thread 0
+// (their order is the mixed-radix order, reading A7).  Same arithmetic and
+// the same u as k_sample (reading A25).
+constexpr int SAMPLE_CTA = 256;
+
+__global__ void __launch_bounds__(SAMPLE_CTA) k_sample_cta(SysView S, int32_t* cur, int32_t* nxt, uint64_t seed,
+                                                          int32_t steps, int32_t input_neuron,
+                                                          const int32_t* train, int32_t train_len,
+                                                          int32_t* halted, int32_t* err) {
+  extern __shared__ uint16_t Fs[];  // m entries: c | p << 8 of the fired rule (0: none)
+  __shared__ int32_t nd_s[KMAX + 1];
+  __shared__ uint8_t nd_d[KMAX + 1];
+  __shared__ int32_t nnd;
+  __shared__ int32_t verdict;  // 0 go on, 1 halted, 2 capacity
+  const int tid = threadIdx.x;
+  const int64_t w = blockIdx.x;
+  const int32_t m = S.m;
+  int32_t* C = cur + w * m;
+  int32_t* N = nxt + w * m;
+  const bool tab8 = S.tables_ok && S.full8 && S.tab_full != nullptr;
+  int32_t hs = -1;
+  bool bad = false;
+  for (int32_t k = 0; k < steps; ++k) {
+    if (tid == 0) nnd = 0;
+    __syncthreads();
+    int any = 0;
+    for (int32_t s = tid; s < m; s += SAMPLE_CTA) {
+      const int32_t v = C[s];
+      int d = 0, first = -1;
+      if (tab8 && !(S.meta[s].flags & NM_GENERIC)) {
+        const uint32_t e = __ldg(S.tab_full + (int64_t)s * 256 + (uint32_t)v);
+        if (e >> 4) {
+          first = S.rule_off[s] + (int)(e >> 4) - 1;
+          d = (e & TE_ND) ? count_applicable(S, s, v) : 1;
+        }
+      } else {
+        for (int r = S.rule_off[s]; r < S.rule_off[s + 1]; ++r)
+          if (rule_app(S.rules[r], v)) {
+            if (!d) first = r;
+            ++d;
+          }
+      }
+      Fs[s] = first >= 0 ? (uint16_t)(S.rules[first].c | (S.rules[first].p << 8)) : (uint16_t)0;
+      any |= d > 0;
+      if (d >= 2) {
+        const int i = atomicAdd(&nnd, 1);
+        if (i < KMAX) {
+          nd_s[i] = s;
+          nd_d[i] = (uint8_t)d;
+        }
+      }
+    }
+    any = __syncthreads_or(any);
+    const bool input_left = input_neuron >= 0 && k < train_len;
+    if (tid == 0) {
+      verdict = 0;
+      const int n = nnd;
+      uint64_t psi = 1;
+      if (n > KMAX) psi = PSI_LIMIT + 1;  // every factor is >= 2
+      for (int i = 0; i < n && i < KMAX; ++i) psi = sat_mul(psi, nd_d[i]);
+      if (psi > PSI_LIMIT) {
+        verdict = 2;
+      } else if (!any && !input_left) {
+        verdict = 1;
+      } else if (any && n > 0) {
+        for (int i = 1; i < n; ++i) {  // insertion sort: increasing neuron (first = most significant)
+          const int32_t ks = nd_s[i];
+          const uint8_t kd = nd_d[i];
+          int j = i - 1;
+          for (; j >= 0 && nd_s[j] > ks; --j) {
+            nd_s[j + 1] = nd_s[j];
+            nd_d[j + 1] = nd_d[j];
+          }
+          nd_s[j + 1] = ks;
+          nd_d[j + 1] = kd;
+        }
+        uint64_t t = splitmix64_dev(splitmix64_dev(seed ^ ((uint64_t)k << 32)) ^ (uint64_t)w) % psi;
+        for (int i = n - 1; i >= 0; --i) {
+          const int32_t s = nd_s[i];
+          const uint64_t d = nd_d[i];
+          const int r = nth_applicable(S, s, C[s], (int)(t % d));
+          Fs[s] = (uint16_t)(S.rules[r].c | (S.rules[r].p << 8));
+          t /= d;
+        }
+      }
+    }
+    __syncthreads();
+    if (verdict == 2) {
+      if (tid == 0) atomicOr(err, ERR_CAPACITY);
+      bad = true;
+      break;
+    }
+    if (verdict == 1) {
+      hs = k;
+      break;
+    }
+    int ovf = 0;
+    if (any) {
+      for (int32_t j = tid; j < m; j += SAMPLE_CTA) {
+        int64_t val = (int64_t)C[j] - (Fs[j] & 0xFF);
+        for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) val += Fs[S.in_src[e]] >> 8;
+        if (j == input_neuron && input_left) val += train[k];
+        ovf |= val < 0 || val > S.count_max;
+        N[j] = (int32_t)val;
+      }
+    } else if (tid == 0) {  // nothing fires: only the input arrives
+      const int64_t val = (int64_t)C[input_neuron] + train[k];
+      ovf |= val < 0 || val > S.count_max;
+      C[input_neuron] = (int32_t)val;
+    }
+    ovf = __syncthreads_or(ovf);
+    if (ovf) {
+      if (tid == 0) atomicOr(err, ERR_OVERFLOW);
+      bad = true;
+      break;
+    }
+    if (any) {
+      int32_t* t_ = C;
+      C = N;
+      N = t_;
+    }
+  }
+  (void)bad;
+  if (C != cur + w * m)
+    for (int32_t j = tid; j < m; j += SAMPLE_CTA) cur[w * m + j] = C[j];
+  if (tid == 0) halted[w] = hs;
+}
+
 // ===========================================================================
 // launchers
 // ===========================================================================
@@ -2691,7 +2822,15 @@ void launch_child_keys_delay(const SysView& S, int32_t bytes, const LevelView& L
 
 void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, uint64_t* fired, uint64_t seed,
                    int32_t steps, int32_t input_neuron, const int32_t* train, int32_t train_len, int32_t* halted,
-                   int32_t* err, cudaStream_t st) {
+                   int32_t* err, bool small_rules, cudaStream_t st) {
+  const size_t smem = (size_t)S.m * 2;
+  if (small_rules && smem <= 200 * 1024) {
+    cudaFuncSetAttribute(k_sample_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_sample_cta<<<(unsigned)W, SAMPLE_CTA, smem, st>>>(S, cur, nxt, seed, steps, input_neuron, train, train_len,
+                                                        halted, err);
+    count_launch();
+    return;
+  }
   const int64_t blocks = (W + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   k_sample<<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, st>>>(S, W, cur, nxt, fired, seed, steps, input_neuron, train,
                                                            train_len, halted, err);

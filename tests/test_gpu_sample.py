@@ -122,3 +122,18 @@ def test_bad_arguments(snp):
     assert ex.value.status == snp.SNP_E_ARG
     C, hs = eng.sample(np.zeros((0, 3), np.int32), 1, 3)
     assert C.shape == (0, 3) and hs.shape == (0,)
+
+
+def test_large_rule_values_take_the_warp_kernel(snp):
+    """a rule with p > 255 cannot use the shared-memory (c, p) bytes of
+    k_sample_cta: the warp-per-walker kernel runs and must agree too."""
+    rules = np.array([[0, W.PERIODIC, 1, 1, 1, 300], [1, W.PERIODIC, 1, 1, 1, 2], [1, W.PERIODIC, 2, 1, 2, 1]],
+                     np.int32)
+    rows = W.matrix_rows_from_rules(rules, [np.array([1]), np.array([0])])
+    row_ptr, col, val = W._csr_from_rows(rows)
+    wg = W.Workload(name="bigp", m=2, rules=rules, row_ptr=row_ptr, col=col, val=val,
+                    C0=np.array([1, 1], np.int32), level0_range=np.array([2, 2], np.int32))
+    for seed in range(3):
+        e, o = _both(snp, wg, np.tile(wg.C0, (17, 1)), seed, 12, bits=32, input_neuron=1,
+                     train=np.array([1, 0, 3], np.int32))
+        _assert_same(e, o)
