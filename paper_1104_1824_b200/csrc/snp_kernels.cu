@@ -1402,6 +1402,12 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 // 64 registers beat 24 warps (70.4 ms) and 16 warps (83 ms); loading the row
 // before the gather (SNP_KC_PREFETCH=1: 68.6 ms) or one iteration ahead
 // (77 ms, spills) loses to loading it where it is used (66.5 ms)
+#ifndef SNP_KC_COOP
+#define SNP_KC_COOP 1  // warp-cooperative stores of the full 4-child quads (else the per-lane store program)
+#endif
+#ifndef SNP_KC_ABLATE
+#define SNP_KC_ABLATE 0  // diagnostics only (wrong results): 1 / 4 skip the per-lane / cooperative stores, 2 the gather
+#endif
 #ifndef SNP_KC_PREFETCH
 #define SNP_KC_PREFETCH 0
 #endif
@@ -1527,7 +1533,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       sD[i] = d;
     }
   }
-  if (prog && tid == 64) {  // the store program (one thread; overlaps the emit-word staging)
+  if (!SNP_KC_COOP && prog && tid == 64) {  // the store program (one thread; overlaps the emit-word staging)
     int n = 0;
     const uint64_t ob0 = Q0 >> 6;
     for (uint64_t ob = ob0; ob <= (Q1 - 1) >> 6; ++ob) {
@@ -1634,8 +1640,12 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
           ripple(2, foursA);
         }
       };
-      if (S.in_pad16) gather(S.in_pad16 + r0 * 32 + lane);
-      else gather(S.in_pad + r0 * 32 + lane);
+      if (SNP_KC_ABLATE & 2) {
+      } else if (S.in_pad16) {
+        gather(S.in_pad16 + r0 * 32 + lane);
+      } else {
+        gather(S.in_pad + r0 * 32 + lane);
+      }
     }
     // the descriptor is only needed for untabulated neurons and the rare
     // count >= 32 fallback (loaded there)
@@ -1756,6 +1766,16 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       if (slot < ovf_cap) ovf[slot] = ((uint64_t)(uint32_t)j << 32) | (uint64_t)(pb0 + r);
     }
     // ---- write x to every kept child of the block's parents (row j of the output)
+#if SNP_KC_COOP
+    if (prog) {
+      // bytes of [Q0, Q1) whose 4-child quad is not inside the range (<= 3
+      // at each end): lane = row, one byte store per position for all rows
+      uint8_t* orow = reinterpret_cast<uint8_t*>(out);
+      const uint64_t qa = (Q0 + 3) & ~3ULL, qb = Q1 & ~3ULL;  // full quads: [qa, qb)
+      for (uint64_t q = Q0; q < Q1 && q < qa; ++q) orow[eidx((int64_t)q, j, m)] = xsb[sR[q - Qb]];
+      for (uint64_t q = (qb > qa ? qb : qa); q < Q1; ++q) orow[eidx((int64_t)q, j, m)] = xsb[sR[q - Qb]];
+    } else
+#else
     if (prog) {
       uint8_t* obase = reinterpret_cast<uint8_t*>(out) + (((int64_t)(Q0 >> 6) * m + j) << 6);
       const uint32_t* xw = reinterpret_cast<const uint32_t*>(xsb);
@@ -1772,7 +1792,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         return (uint32_t)xsb[rr & 0xFF] | ((uint32_t)xsb[(rr >> 8) & 0xFF] << 8) |
                ((uint32_t)xsb[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xsb[rr >> 24] << 24);
       };
-      for (int i = 0; i < nops; ++i) {
+      for (int i = 0; i < ((SNP_KC_ABLATE & 1) ? 0 : nops); ++i) {
         const uint64_t op = sOps[i];
         uint8_t* dst = obase + (uint32_t)op;
         const uint32_t hi = (uint32_t)(op >> 32), kind = hi & 3u, qi = hi >> 16;
@@ -1799,13 +1819,59 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
           *dst = xsb[qi];
         }
       }
-    } else if (nq <= QCAP) {
+    } else
+#endif
+    if (nq <= QCAP) {
       for (uint64_t q = Q0; q < Q1; ++q) out[eidx((int64_t)q, j, m)] = xs[sR[q - Qb]];
     } else {
       for (int r = 0; r < np; ++r)
         for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = xs[r];
     }
     }  // j < m
+#if SNP_KC_COOP
+    if (prog) {
+      // full 4-child quads, warp-cooperative: a half-warp covers one 64-child
+      // output row (lane = quad; a byte permute of the neuron's x row when
+      // the 4 parents lie in a 16-byte window, else 4 byte loads), so each
+      // 4-byte store instruction of the warp fills 128 contiguous bytes (4
+      // whole sectors) instead of touching 32 rows
+      __syncwarp();
+      const int hl = lane & 15, j0 = lane >> 4;
+      const int32_t jn = m - jbase;  // rows of this warp that exist
+      const uint8_t* xr0 = sX + (size_t)(warp * 32 + j0) * xs_stride<T>();
+      const uint64_t qa = (Q0 + 3) & ~3ULL, qb = Q1 & ~3ULL;
+      for (uint64_t ob = qa >> 6; !(SNP_KC_ABLATE & 4) && qa < qb && ob <= (qb - 1) >> 6; ++ob) {
+        const uint64_t q = (ob << 6) + 4 * hl;
+        if (q >= qa && q < qb) {
+          const uint32_t d = sD[(q - Qb) >> 2];
+          uint8_t* dst0 = reinterpret_cast<uint8_t*>(out) + (((int64_t)ob * m + jbase + j0) << 6) + 4 * hl;
+          if (!(d & 0x80000000u)) {
+            const uint32_t* w0 = reinterpret_cast<const uint32_t*>(xr0) + ((d >> 16) & 31);
+            const uint32_t sel = d & 0xFFFFu, hb = d >> 24;
+            const uint32_t mask = (hb * 0x00204081u & 0x01010101u) * 0xFFu;  // 0xFF in bytes k with bit k of hb
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(w0) +
+                                                                    2 * i * xs_stride<T>());
+              uint32_t v = prmt(w[0], w[1], sel);
+              if (hb) v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
+              if (j0 + 2 * i < jn) *reinterpret_cast<uint32_t*>(dst0 + i * 128) = v;
+            }
+          } else {
+            const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (q - Qb));  // 4 parent indices
+#pragma unroll 4
+            for (int i = 0; i < 16; ++i) {
+              const uint8_t* xr = xr0 + 2 * i * xs_stride<T>();
+              const uint32_t v = (uint32_t)xr[rr & 0xFF] | ((uint32_t)xr[(rr >> 8) & 0xFF] << 8) |
+                                 ((uint32_t)xr[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xr[rr >> 24] << 24);
+              if (j0 + 2 * i < jn) *reinterpret_cast<uint32_t*>(dst0 + i * 128) = v;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+#endif
   }
 }
 // K-c (generic): every (kept child, neuron) computed exactly.
