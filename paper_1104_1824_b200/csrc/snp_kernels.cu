@@ -2221,6 +2221,121 @@ __device__ int64_t delay_value(const SysView& S, const void* data, int64_t p, in
   return val;
 }
 
+// Per-neuron step data of one child (reading A26), computed once per neuron
+// into the warp's shared-memory slice: consumption, τ', π', emission.
+struct DelayCols {
+  int32_t* cons;
+  int32_t* taun;
+  int32_t* pin;
+  int32_t* emit;
+};
+
+template <typename T>
+__device__ void delay_neurons(const SysView& S, const void* data, int64_t p, const ChildCtx& cx, const DelayCols& D,
+                              int lane) {
+  const int32_t m = S.delay_m;
+  for (int32_t s = lane; s < m; s += 32) {
+    const int64_t t0 = ld_count<T>(data, p, m + s, S.m);
+    int32_t cons = 0, taun = 0, pin = 0, emit = 0;
+    if (t0 >= 1) {  // closed: the clock runs, emits π when it reopens
+      taun = (int32_t)(t0 - 1);
+      const int32_t pi0 = ld_count<T>(data, p, 2 * m + s, S.m);
+      pin = taun ? pi0 : 0;
+      emit = taun ? 0 : pi0;
+    } else {
+      const int r = fired_rule(S, s, ld_count<T>(data, p, s, S.m), cx);
+      if (r >= 0) {
+        cons = S.rules[r].c;
+        if (S.delay[r] == 0) emit = S.rules[r].p;
+        else { taun = S.delay[r]; pin = S.rules[r].p; }
+      }
+    }
+    D.cons[s] = cons;
+    D.taun[s] = taun;
+    D.pin[s] = pin;
+    D.emit[s] = emit;
+  }
+  __syncwarp();
+}
+
+template <typename T>
+__device__ __forceinline__ int64_t delay_column(const SysView& S, const void* data, int64_t p, int32_t j,
+                                                const DelayCols& D) {
+  const int32_t m = S.delay_m;
+  if (j >= 2 * m) return D.pin[j - 2 * m];
+  if (j >= m) return D.taun[j - m];
+  int64_t val = (int64_t)ld_count<T>(data, p, j, S.m) - D.cons[j];
+  if (D.taun[j] == 0)
+    for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) val += D.emit[S.in_src[e]];
+  return val;
+}
+
+constexpr int DELAY_WARPS = 8;
+size_t delay_smem_bytes(int32_t m) { return (size_t)DELAY_WARPS * 16 * (size_t)m; }
+
+// child keys (shared-memory variant, 16·m bytes per warp): the per-neuron
+// step data once per child, then the 3m columns and their fingerprint
+template <typename T>
+__global__ void __launch_bounds__(DELAY_WARPS * 32) k_child_keys_delay_s(SysView S, LevelView L, const uint64_t* off,
+                                                                         ExpandOut O, uint64_t T_, ChildArrays C) {
+  extern __shared__ int32_t dsm[];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int32_t m = S.delay_m;
+  const DelayCols D{dsm + (size_t)wl * 4 * m, dsm + (size_t)wl * 4 * m + m, dsm + (size_t)wl * 4 * m + 2 * m,
+                    dsm + (size_t)wl * 4 * m + 3 * m};
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = warp; c < T_; c += nwarps) {
+    const int64_t p = C.cpar[c];
+    ChildCtx cx;
+    decode_child(S, O.nd + p * KMAX, O.ndc[p], c - off[p], cx);
+    delay_neurons<T>(S, L.data, p, cx, D, lane);
+    uint64_t f0 = 0, f1 = 0;
+    for (int32_t j = lane; j < S.m; j += 32) {
+      const uint64_t v = (uint64_t)delay_column<T>(S, L.data, p, j, D);
+      f0 += v * S.R0[j];
+      f1 += v * S.R1[j];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      f0 += __shfl_xor_sync(0xFFFFFFFFu, f0, o);
+      f1 += __shfl_xor_sync(0xFFFFFFFFu, f1, o);
+    }
+    if (lane == 0) {
+      C.cfp0[c] = f0;
+      C.cfp1[c] = f1;
+    }
+    __syncwarp();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(DELAY_WARPS * 32) k_materialize_delay_s(SysView S, LevelView L, ExpandOut O,
+                                                                          NextArrays N, int64_t K, int32_t* err) {
+  extern __shared__ int32_t dsm[];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int32_t m = S.delay_m;
+  const DelayCols D{dsm + (size_t)wl * 4 * m, dsm + (size_t)wl * 4 * m + m, dsm + (size_t)wl * 4 * m + 2 * m,
+                    dsm + (size_t)wl * 4 * m + 3 * m};
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  T* out = reinterpret_cast<T*>(N.data);
+  for (int64_t q = warp; q < K; q += nwarps) {
+    const int64_t p = N.parent[q];
+    ChildCtx cx;
+    decode_child(S, O.nd + p * KMAX, O.ndc[p], N.t[q], cx);
+    delay_neurons<T>(S, L.data, p, cx, D, lane);
+    bool bad = false;
+    for (int32_t j = lane; j < S.m; j += 32) {
+      const int64_t val = delay_column<T>(S, L.data, p, j, D);
+      bad |= val < 0 || val > S.count_max;
+      out[eidx(q, j, S.m)] = (T)val;
+    }
+    if (bad) atomicOr(err, ERR_OVERFLOW);
+    __syncwarp();
+  }
+}
+
 // child keys: warp per child, fingerprint of the materialised child (A18)
 template <typename T>
 __global__ void k_child_keys_delay(SysView S, LevelView L, const uint64_t* off, ExpandOut O, uint64_t T_,
@@ -2713,7 +2828,11 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
     if (g > 148u * 32u) g = 148u * 32u;
     dispatch_bytes(bytes, [&](auto tt) {
       using T = decltype(tt);
-      if (S.delay_m > 0) k_materialize_delay<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
+      const size_t sm = delay_smem_bytes(S.delay_m);
+      if (S.delay_m > 0 && sm <= 200 * 1024) {
+        cudaFuncSetAttribute(k_materialize_delay_s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_materialize_delay_s<T><<<g, DELAY_WARPS * 32, sm, st>>>(S, L, O, N, K, err);
+      } else if (S.delay_m > 0) k_materialize_delay<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
       else k_materialize_exact<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
     });
   }
@@ -2879,9 +2998,15 @@ void launch_child_keys_delay(const SysView& S, int32_t bytes, const LevelView& L
                              const ExpandOut& O, uint64_t T, const ChildArrays& C, cudaStream_t st) {
   unsigned g = grid_for(T * 32, 256);
   if (g > 148u * 64u) g = 148u * 64u;
+  const size_t sm = delay_smem_bytes(S.delay_m);
   dispatch_bytes(bytes, [&](auto tt) {
     using TT = decltype(tt);
-    k_child_keys_delay<TT><<<g, 256, 0, st>>>(S, L, off, O, T, C);
+    if (sm <= 200 * 1024) {
+      cudaFuncSetAttribute(k_child_keys_delay_s<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_child_keys_delay_s<TT><<<g, DELAY_WARPS * 32, sm, st>>>(S, L, off, O, T, C);
+    } else {
+      k_child_keys_delay<TT><<<g, 256, 0, st>>>(S, L, off, O, T, C);
+    }
   });
   count_launch();
 }

@@ -101,3 +101,12 @@ def test_clock_overflow_and_state_errors(snp):
     with pytest.raises(snp.SnpError) as ex:
         eng.sample(np.array([[1, 0]], np.int32), 1, 2)
     assert ex.value.status == snp.SNP_E_STATE
+
+
+def test_wide_system_takes_the_global_scratch_kernels(snp):
+    """m = 2000: the per-warp shared-memory step data (16·m B × 8 warps) does
+    not fit, so the kernels that recompute per column run; same tree."""
+    w = W.random_system(2000, outdeg=8, k_nd=4, seed=8)
+    rng = np.random.default_rng(8)
+    delays = np.where(rng.random(w.n) < 0.2, rng.integers(1, 3, size=w.n), 0).astype(np.int32)
+    _check(snp, w, delays, _wide(W.level0_counts(w, 30, 8), w.m), 3, bits=8, target=40)
