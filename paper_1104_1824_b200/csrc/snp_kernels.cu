@@ -1954,6 +1954,125 @@ __global__ void k_overflow_fix(SysView S, LevelView L, ExpandOut O, const uint64
   }
 }
 
+// first applicable rule of neuron s at count v (tables when tabulated)
+__device__ __forceinline__ int first_rule(const SysView& S, int32_t s, int32_t v) {
+  if (S.tables_ok) {
+    const NeuronMeta mt = S.meta[s];
+    if (!(mt.flags & NM_GENERIC)) {
+      const uint32_t e = S.full8 ? S.tab_full[(int64_t)s * 256 + ((uint32_t)v & 0xFFu)]
+                                 : S.tab[(int64_t)s * S.tabw + table_index((uint32_t)v, mt)];
+      return (e >> 4) ? mt.rbase + (int)(e >> 4) - 1 : -1;
+    }
+  }
+  return nth_applicable(S, s, v, 0);
+}
+
+// The fired rule's (c, p) of every neuron of one child into a warp's
+// shared-memory slice: first applicable rules, then the ND digits of cx.
+template <typename T>
+__device__ void fired_cp(const SysView& S, const void* data, int64_t p, const ChildCtx& cx, int2* fc, int lane) {
+  for (int32_t s = lane; s < S.m; s += 32) {
+    const int r = first_rule(S, s, ld_count<T>(data, p, s, S.m));
+    fc[s] = r >= 0 ? make_int2(S.rules[r].c, S.rules[r].p) : make_int2(0, 0);
+  }
+  __syncwarp();
+  for (int i = lane; i < cx.K; i += 32) {
+    if (!cx.x[i]) continue;
+    const int32_t s = cx.s[i];
+    const int r = nth_applicable(S, s, ld_count<T>(data, p, s, S.m), cx.x[i]);
+    fc[s] = make_int2(S.rules[r].c, S.rules[r].p);
+  }
+  __syncwarp();
+}
+
+// column j of that child: eq. (2) restricted to column j (Def. 2)
+template <typename T>
+__device__ __forceinline__ int64_t fired_value(const SysView& S, const void* data, int64_t p, int32_t j,
+                                               const ChildCtx& cx, const int2* fc) {
+  if (S.aug_rule >= 0 && j == S.m - 1) return exact_value<T>(S, data, p, j, cx);
+  int64_t val = (int64_t)ld_count<T>(data, p, j, S.m) - fc[j].x;
+  for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) val += fc[S.in_src[e]].y;
+  return val;
+}
+
+// K-c (generic) with the fired (c, p) of each child in shared memory
+template <typename T>
+__global__ void __launch_bounds__(256) k_materialize_exact_s(SysView S, LevelView L, ExpandOut O, NextArrays N,
+                                                             int64_t K, int32_t* err) {
+  extern __shared__ int2 msm[];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  int2* fc = msm + (size_t)wl * S.m;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  T* out = reinterpret_cast<T*>(N.data);
+  for (int64_t q = warp; q < K; q += nwarps) {
+    const int64_t p = N.parent[q];
+    ChildCtx cx;
+    decode_child(S, O.nd + p * KMAX, O.ndc[p], N.t[q], cx);
+    fired_cp<T>(S, L.data, p, cx, fc, lane);
+    bool bad = false;
+    for (int32_t j = lane; j < S.m; j += 32) {
+      const int64_t val = fired_value<T>(S, L.data, p, j, cx, fc);
+      bad |= (val < 0 || val > S.count_max);
+      out[eidx(q, j, S.m)] = (T)val;
+    }
+    if (bad) atomicOr(err, ERR_OVERFLOW);
+    __syncwarp();
+  }
+}
+
+constexpr int VERIFY_WARPS = 8;
+size_t verify_smem_bytes(int32_t m) { return (size_t)VERIFY_WARPS * 2 * 8 * (size_t)m; }
+
+// k_verify with the fired (c, p) of both children in shared memory
+template <typename T>
+__global__ void __launch_bounds__(VERIFY_WARPS * 32) k_verify_s(SysView S, LevelView L, ExpandOut O,
+                                                                const uint64_t* off, ChildArrays C, uint64_t T_,
+                                                                uint64_t tag_base, Tables tb,
+                                                                const StoredLevel* stored, int32_t* err) {
+  extern __shared__ int2 vsm[];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  int2* fa = vsm + (size_t)wl * 2 * S.m;
+  int2* fb = fa + S.m;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = warp; c < T_; c += nwarps) {
+    const uint8_t vd = C.verdict[c];
+    uint64_t other = EMPTY;
+    if (vd == 1) {
+      const uint64_t wtag = tb.ltab[C.cslot[c]].tag;
+      if (wtag == tag_base + c) continue;  // the winner itself
+      other = wtag - tag_base;
+    } else if (C.cref[c] == EMPTY) {
+      continue;
+    }
+    const uint32_t p = C.cpar[c];
+    ChildCtx cx, co;
+    decode_child(S, O.nd + (uint64_t)p * KMAX, O.ndc[p], c - off[p], cx);
+    fired_cp<T>(S, L.data, p, cx, fa, lane);
+    uint32_t po = 0;
+    if (vd == 1) {
+      po = C.cpar[other];
+      decode_child(S, O.nd + (uint64_t)po * KMAX, O.ndc[po], other - off[po], co);
+      fired_cp<T>(S, L.data, po, co, fb, lane);
+    }
+    bool diff = false;
+    for (int32_t j = lane; j < S.m; j += 32) {
+      const int64_t a = fired_value<T>(S, L.data, p, j, cx, fa);
+      int64_t b;
+      if (vd == 1) {
+        b = fired_value<T>(S, L.data, po, j, co, fb);
+      } else {
+        const uint64_t ref = C.cref[c];
+        b = ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, S.m);
+      }
+      diff |= (a != b);
+    }
+    if (__any_sync(0xFFFFFFFFu, diff) && lane == 0) atomicOr(err, ERR_COLLISION);
+    __syncwarp();
+  }
+}
+
 // dedup = 0: every fingerprint match is checked by comparing the two full
 // configurations (candidate computed exactly from (parent, t)).  A mismatch
 // is a 128-bit collision: reported, never merged (reading A18).
@@ -2832,8 +2951,15 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
       if (S.delay_m > 0 && sm <= 200 * 1024) {
         cudaFuncSetAttribute(k_materialize_delay_s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_materialize_delay_s<T><<<g, DELAY_WARPS * 32, sm, st>>>(S, L, O, N, K, err);
-      } else if (S.delay_m > 0) k_materialize_delay<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
-      else k_materialize_exact<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
+      } else if (S.delay_m > 0) {
+        k_materialize_delay<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
+      } else if ((size_t)8 * 8 * S.m <= 200 * 1024) {
+        const size_t sme = (size_t)8 * 8 * S.m;
+        cudaFuncSetAttribute(k_materialize_exact_s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sme);
+        k_materialize_exact_s<T><<<g, 256, sme, st>>>(S, L, O, N, K, err);
+      } else {
+        k_materialize_exact<T><<<g, 256, 0, st>>>(S, L, O, N, K, err);
+      }
     });
   }
   count_launch();
@@ -2888,7 +3014,13 @@ void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const Ex
   if (g > 148u * 64u) g = 148u * 64u;
   dispatch_bytes(bytes, [&](auto tt) {
     using TT = decltype(tt);
-    k_verify<TT><<<g, 256, 0, st>>>(S, L, O, off, C, T, tag_base, tb, stored, err);
+    const size_t sm = verify_smem_bytes(S.m);
+    if (sm <= 200 * 1024 && S.delay_m == 0) {
+      cudaFuncSetAttribute(k_verify_s<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_verify_s<TT><<<g, VERIFY_WARPS * 32, sm, st>>>(S, L, O, off, C, T, tag_base, tb, stored, err);
+    } else {
+      k_verify<TT><<<g, 256, 0, st>>>(S, L, O, off, C, T, tag_base, tb, stored, err);
+    }
   });
   count_launch();
 }
