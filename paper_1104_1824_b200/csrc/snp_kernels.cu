@@ -830,6 +830,9 @@ constexpr int TC_ATILE = TCM * TCK;             // 8 KB
 constexpr int TC_BTILE = TCK * TCN;             // 2 KB
 constexpr int TC_STAGE = 2 * TC_ATILE;           // X and Y tiles of one chunk
 constexpr int TC_STAGES = 2;                     // X|Y tiles: double-buffered
+#ifndef SNP_TC_WS
+#define SNP_TC_WS 1  // producer warp for copies + MMAs (else thread 0 issues them after a CTA barrier)
+#endif
 constexpr int TC_IN = 3;                         // B tile + tables: a ring of 3 (loaded one chunk ahead)
 
 constexpr int TC_TTAB = TCK * 32;              // the chunk's 32-entry X|Y tables (2 KB)
@@ -846,13 +849,17 @@ __device__ __forceinline__ uint32_t lut16(uint32_t v4, const uint32_t (&tt)[8]) 
   return (a & ~m3) | (b & m3);
 }
 
-__global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, ExpandOut O) {
+// WS: a ninth (producer) warp issues the bulk copies and the MMAs; the 256
+// compute threads only arrive on a per-stage mbarrier (no CTA barrier per chunk)
+template <bool WS>
+__global__ void __launch_bounds__(TCT + 32) k_expand_tc(SysView S, LevelView L, ExpandOut O) {
   extern __shared__ __align__(128) uint8_t smem_tc[];
   uint8_t* smem = smem_tc;
   uint8_t* sIn = smem + TC_STAGES * TC_STAGE;                       // [TC_IN][B_X | B_Y | tables]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sIn + TC_IN * TC_INB);  // [2] MMAs done with an X|Y stage
   uint64_t* lbar = bar + TC_STAGES;                                    // [3] an input slot landed
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(lbar + TC_IN);
+  uint64_t* fbar = lbar + TC_IN;                                       // [2] (WS) X|Y stage written
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + TC_STAGES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int32_t m = S.m;
   const int64_t mE = (m + 1) & ~1;
@@ -882,8 +889,10 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
     tc::bar_init(&bar[0], 1);
     tc::bar_init(&bar[1], 1);
     for (int i = 0; i < TC_IN; ++i) tc::bar_init(&lbar[i], 1);
+    tc::bar_init(&fbar[0], TCT);
+    tc::bar_init(&fbar[1], TCT);
     fence_barrier_init();
-    stage_inputs(0);
+    if (!WS) stage_inputs(0);
   }
   tc::fence_before();
   __syncthreads();
@@ -917,7 +926,7 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
     // the next chunk's inputs go to slot (c + 1) % 3, last read by the MMAs
     // of chunk c - 2 (done: issued two chunks ago) and by the table loads of
     // chunk c - 2 (before every thread's __syncthreads of chunk c - 2)
-    if (tid == 0 && c + 1 < nch) {
+    if (!WS && tid == 0 && c + 1 < nch) {
       if (c >= 2) tc::bar_wait(&bar[st], (uint32_t)(((c - 2) >> 1) & 1));
       tc::fence_async_smem();
       stage_inputs(c + 1);
@@ -986,6 +995,10 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
     // (a per-stage mbarrier that only the MMA-issuing thread waits on, letting
     // the other warps run ahead, measured slower than this barrier)
     tc::fence_async_smem();
+    if (WS) {
+      mbar_arrive(&fbar[st]);
+      return;
+    }
     __syncthreads();
     if (tid == 0) {
       tc::fence_after();
@@ -1000,9 +1013,44 @@ __global__ void __launch_bounds__(TCT) k_expand_tc(SysView S, LevelView L, Expan
       tc::commit(&bar[st]);
     }
   };
-  uint32_t w[8];
-  load(0, w);
-  for (int c = 0; c < nch; ++c) chunk(c, w);
+  if (WS && warp == TCT / 32) {
+    // producer: inputs two chunks ahead, the MMAs of each chunk once its
+    // X|Y stage is written
+    if (lane == 0) {
+      stage_inputs(0);
+      if (nch > 1) stage_inputs(1);
+      for (int c = 0; c < nch; ++c) {
+        const int st = c & 1, sl = c % TC_IN;
+        uint8_t* sX = smem + st * TC_STAGE;
+        uint8_t* sY = sX + TC_ATILE;
+        uint8_t* sB = sIn + sl * TC_INB;
+        tc::bar_wait(&lbar[sl], (uint32_t)((c / TC_IN) & 1));
+        tc::bar_wait(&fbar[st], (uint32_t)((c >> 1) & 1));
+        tc::fence_after();
+#pragma unroll
+        for (int ks = 0; ks < TCK / 32; ++ks) {
+          tc::mma_u8(tmem, tc::sdesc(tc::smem_u32(sX + ks * 4 * TC_A_LBO), TC_A_LBO, 128),
+                     tc::sdesc(tc::smem_u32(sB + ks * 2 * TC_B_LBO), TC_B_LBO, 128), IDESC,
+                     (c > 0 || ks > 0) ? 1u : 0u);
+          tc::mma_u8(tmem + TCN, tc::sdesc(tc::smem_u32(sY + ks * 4 * TC_A_LBO), TC_A_LBO, 128),
+                     tc::sdesc(tc::smem_u32(sB + TC_BTILE + ks * 2 * TC_B_LBO), TC_B_LBO, 128), IDESC,
+                     (c > 0 || ks > 0) ? 1u : 0u);
+        }
+        tc::commit(&bar[st]);
+        // slot (c + 2) % 3 was last used by chunk c - 1: its tables were read
+        // before fbar(c - 1), its B tiles by the MMAs of chunk c - 1
+        if (c + 2 < nch) {
+          if (c >= 1) tc::bar_wait(&bar[st ^ 1], (uint32_t)(((c - 1) >> 1) & 1));
+          tc::fence_async_smem();
+          stage_inputs(c + 2);
+        }
+      }
+    }
+  } else {
+    uint32_t w[8];
+    load(0, w);
+    for (int c = 0; c < nch; ++c) chunk(c, w);
+  }
   const int cl = nch - 1;
   tc::bar_wait(&bar[cl & 1], (uint32_t)((cl >> 1) & 1));
   tc::fence_after();
@@ -2852,9 +2900,10 @@ void launch_expand(const SysView& S, int32_t bytes, const LevelView& L, const Ex
       };
       if (full && S.tc_ok && !(S.kernel_flags & (KF_EXPAND_T | KF_NO_TC))) {
         const size_t sm = expand_tc_smem_bytes();
-        cudaFuncSetAttribute(k_expand_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        auto kern = SNP_TC_WS ? k_expand_tc<true> : k_expand_tc<false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const int64_t nblk = (L.F + PB - 1) / PB;
-        k_expand_tc<<<(unsigned)((nblk + 1) / 2), TCT, sm, st>>>(S, L, O);
+        kern<<<(unsigned)((nblk + 1) / 2), TCT + (SNP_TC_WS ? 32 : 0), sm, st>>>(S, L, O);
         if (!O.classify_only) {
           k_nd_pass<<<grid_for(L.F), BLK, 0, st>>>(S, L, O);
           count_launch();
