@@ -176,6 +176,33 @@ def test_tc_expand_selected_and_equal(snp, monkeypatch, kernels):
     assert snp.System(pi, count_bits=32, dedup=0).kernel_paths == 0  # int32 storage: CUDA-core K-a
 
 
+def test_tc_expand_declined_when_not_applicable(snp):
+    """k_expand_tc needs c <= 15, p <= 1 and at most 64 possibly
+    nondeterministic neurons; otherwise the CUDA-core K-a runs (and agrees)."""
+    w = W.random_system(300, outdeg=8, k_nd=80, seed=31)  # 80 ND neurons > 64
+    L0 = W.level0_counts(w, 200, 31)
+    L0[:, w.meta["nd_neurons"]] = 0  # below threshold at first: Ψ stays small for 3 levels
+    eng = snp.System(w, count_bits=8, dedup=1, frontier_target=300)
+    assert eng.kernel_paths == 0
+    tree = eng.explore(L0, depth=3)
+    ref = oracle.System.from_workload(w).explore(L0, depth=3, dedup=1, count_bits=8, frontier_target=300)
+    assert_same_tree(tree, ref)
+    w2 = W.random_system(200, outdeg=8, k_nd=3, seed=32)
+    w2.rules[w2.rules[:, 0] == 5, 2] += 20  # neuron 5: thresholds and consumption above 15
+    w2.rules[w2.rules[:, 0] == 5, 4] += 20
+    w2 = W.Workload(name="bigc", m=w2.m, rules=w2.rules, row_ptr=w2.row_ptr,
+                    col=w2.col, val=np.where(w2.val < 0, -w2.rules[np.repeat(np.arange(w2.n), np.diff(w2.row_ptr)), 4],
+                                             w2.val).astype(np.int32),
+                    C0=w2.C0, level0_range=w2.level0_range)
+    eng2 = snp.System(w2, count_bits=8, dedup=1, frontier_target=300)
+    assert eng2.kernel_paths == 0
+    L0 = W.level0_counts(w2, 150, 32)
+    L0[:, 5] = 30
+    tree = eng2.explore(L0, depth=3)
+    ref = oracle.System.from_workload(w2).explore(L0, depth=3, dedup=1, count_bits=8, frontier_target=300)
+    assert_same_tree(tree, ref)
+
+
 def test_config5_shape_parity(snp):
     """Config 5's system family at full width (m = 65536, n = 262144, k_nd = 7:
     mean Ψ ≈ 38 children per parent), scaled-down frontier, bit-exact."""
