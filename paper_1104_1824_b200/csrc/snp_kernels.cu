@@ -1453,6 +1453,9 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_COOP
 #define SNP_KC_COOP 1  // warp-cooperative stores of the full 4-child quads (else the per-lane store program)
 #endif
+#ifndef SNP_KC_EDGE
+#define SNP_KC_EDGE 1  // boundary bytes of a row end as <= 2 aligned stores (else one byte store per child)
+#endif
 #ifndef SNP_KC_ABLATE
 #define SNP_KC_ABLATE 0  // diagnostics only (wrong results): 1 / 4 skip the per-lane / cooperative stores, 2 the gather
 #endif
@@ -1820,8 +1823,32 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       // at each end): lane = row, one byte store per position for all rows
       uint8_t* orow = reinterpret_cast<uint8_t*>(out);
       const uint64_t qa = (Q0 + 3) & ~3ULL, qb = Q1 & ~3ULL;  // full quads: [qa, qb)
+#if SNP_KC_EDGE
+      // each end is <= 3 contiguous bytes of one quad of row j: assembled in
+      // a register and written by <= 2 aligned stores (a byte, a halfword)
+      // instead of one byte store per child
+      auto edge = [&](uint64_t q0, uint64_t q1) {
+        if (q0 >= q1) return;
+        uint32_t v = 0;
+        for (uint64_t q = q0; q < q1; ++q) v |= (uint32_t)xsb[sR[q - Qb]] << (8 * (q - q0));
+        uint8_t* d = orow + eidx((int64_t)q0, j, m);
+        int n = (int)(q1 - q0);
+        if ((q0 & 1) && n) {
+          *d = (uint8_t)v;
+          v >>= 8; ++d; --n;
+        }
+        if (n >= 2) {
+          *reinterpret_cast<uint16_t*>(d) = (uint16_t)v;
+          v >>= 16; d += 2; n -= 2;
+        }
+        if (n) *d = (uint8_t)v;
+      };
+      edge(Q0, Q1 < qa ? Q1 : qa);
+      edge(qb > qa ? qb : qa, Q1);
+#else
       for (uint64_t q = Q0; q < Q1 && q < qa; ++q) orow[eidx((int64_t)q, j, m)] = xsb[sR[q - Qb]];
       for (uint64_t q = (qb > qa ? qb : qa); q < Q1; ++q) orow[eidx((int64_t)q, j, m)] = xsb[sR[q - Qb]];
+#endif
     } else
 #else
     if (prog) {
