@@ -830,6 +830,9 @@ constexpr int TC_ATILE = TCM * TCK;             // 8 KB
 constexpr int TC_BTILE = TCK * TCN;             // 2 KB
 constexpr int TC_STAGE = 2 * TC_ATILE;           // X and Y tiles of one chunk
 constexpr int TC_STAGES = 2;                     // X|Y tiles: double-buffered
+#ifndef SNP_TC_L2PF
+#define SNP_TC_L2PF 0  // K-a: L2 bulk prefetch of the counts this many chunks ahead (producer warp); measured slower: 2 / 4 / 8 chunks 19.9 / 20.1 / 20.1 ms vs 19.6 off
+#endif
 #ifndef SNP_TC_WS
 #define SNP_TC_WS 1  // producer warp for copies + MMAs (else thread 0 issues them after a CTA barrier)
 #endif
@@ -1024,6 +1027,16 @@ __global__ void __launch_bounds__(TCT + 32) k_expand_tc(SysView S, LevelView L, 
         uint8_t* sX = smem + st * TC_STAGE;
         uint8_t* sY = sX + TC_ATILE;
         uint8_t* sB = sIn + sl * TC_INB;
+#if SNP_TC_L2PF
+        // the counts of chunk c + SNP_TC_L2PF (both blocks, 4 KB each) pulled
+        // into L2 ahead of the compute warps' loads
+        if (c + SNP_TC_L2PF < nch) {
+          const int64_t s0 = (int64_t)(c + SNP_TC_L2PF) * TCK;
+          const uint32_t nb = (uint32_t)((m - s0 < TCK ? m - s0 : TCK) * PB);
+          for (int hh = 0; hh < 2; ++hh)
+            if (blk0 + hh < nblk) bulk_prefetch_l2(data + (((blk0 + hh) * m + s0) << 6), nb);
+        }
+#endif
         tc::bar_wait(&lbar[sl], (uint32_t)((c / TC_IN) & 1));
         tc::bar_wait(&fbar[st], (uint32_t)((c >> 1) & 1));
         tc::fence_after();
@@ -1453,6 +1466,9 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_COOP
 #define SNP_KC_COOP 1  // warp-cooperative stores of the full 4-child quads (else the per-lane store program)
 #endif
+#ifndef SNP_KC_L2PF
+#define SNP_KC_L2PF 2  // k > 0: L2 bulk prefetch of the warp's parent rows k - 1 iterations ahead (measured: 0 64.2 ms, 1 64.0, 2 63.7, 3 63.9)
+#endif
 #ifndef SNP_KC_EDGE
 #define SNP_KC_EDGE 1  // boundary bytes of a row end as <= 2 aligned stores (else one byte store per child)
 #endif
@@ -1625,6 +1641,17 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   for (int it = 0; it < j_iters; ++it) {
     const int32_t jbase = it * MW * 32 + warp * 32;
     if (jbase >= m) break;  // warp-uniform
+#if SNP_KC_L2PF
+    // the warp's 32 rows of the parent block (2 KB contiguous for u8) pulled
+    // into L2 while the gather runs, so the row load after it hits L2
+    if (sizeof(T) == 1 && lane == 0) {
+      const int32_t jp = jbase + (SNP_KC_L2PF - 1) * MW * 32;
+      if (jp < m) {
+        const int32_t nr = (m - jp < 32) ? (m - jp) : 32;
+        bulk_prefetch_l2(data + eidx(pb0, jp, m), (uint32_t)(nr * PB * sizeof(T)));
+      }
+    }
+#endif
     const int32_t j = jbase + lane;
     if (j < m) {
     const T* row = data + eidx(pb0, j, m);
