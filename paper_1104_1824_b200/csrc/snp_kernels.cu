@@ -1469,6 +1469,9 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_L2PF
 #define SNP_KC_L2PF 2  // k > 0: L2 bulk prefetch of the warp's parent rows k - 1 iterations ahead (measured: 0 64.2 ms, 1 64.0, 2 63.7, 3 63.9)
 #endif
+#ifndef SNP_KC_BRANCHLESS
+#define SNP_KC_BRANCHLESS 0  // cooperative quads: the upper-window permute unconditionally (no per-lane branch); measured 64.1 vs 63.9 ms
+#endif
 #ifndef SNP_KC_EDGE
 #define SNP_KC_EDGE 1  // boundary bytes of a row end as <= 2 aligned stores (else one byte store per child)
 #endif
@@ -1956,7 +1959,11 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
               const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(w0) +
                                                                     2 * i * xs_stride<T>());
               uint32_t v = prmt(w[0], w[1], sel);
+#if SNP_KC_BRANCHLESS
+              v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);  // mask = 0 when hb = 0 (words past the row are masked out)
+#else
               if (hb) v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
+#endif
               if (j0 + 2 * i < jn) *reinterpret_cast<uint32_t*>(dst0 + i * 128) = v;
             }
           } else {
