@@ -363,14 +363,14 @@ def run_e2e(args, cfg, w, snp, torch):
     for _ in range(args.steps):
         c = eng.advance()
         T_sum += c["T"]
-        parent, t, halting, fp = eng.level_edges(eng.depth)
+        parent, t, halting, fp = eng.level_edges(eng.depth, pinned=True)
         d2h += parent.nbytes + t.nbytes + fp.nbytes + halting.nbytes
     dt_s = time.perf_counter() - t0
     eng.close()
     del host
     return {"value": T_sum / dt_s, "unit": UNIT, "h2d_bytes_per_step": F * m * wb // args.steps,
             "d2h_bytes_per_step": d2h // args.steps,
-            "note": "snp_begin(pinned host row-major level 0) + K x (snp_advance + snp_level_edges D2H); "
+            "note": "snp_begin(pinned host row-major level 0) + K x (snp_advance + snp_level_edges D2H into pinned buffers); "
                     "wall clock around synchronous ABI calls"}
 
 

@@ -232,6 +232,16 @@ int64_t    snp_kernel_launches(void);
 #define SNP_PATH_TC_EXPAND 1
 int32_t    snp_kernel_paths(const snp_system *sys);
 
+/* Pinned (page-locked) host memory for the host side of the e2e path: the
+ * level-0 input of snp_begin and the outputs of snp_level_edges copy at full
+ * PCIe rate from/to it (pageable buffers go through the driver's staging).
+ *   snp_host_alloc  *p = bytes of pinned host memory (NULL for bytes = 0),
+ *                   owned by the caller until snp_host_free; SNP_E_OOM when the
+ *                   allocation fails (*p = NULL), SNP_E_ARG for p = NULL.
+ *   snp_host_free   releases a pointer from snp_host_alloc (NULL: no-op).    */
+snp_status snp_host_alloc(size_t bytes, void **p);
+snp_status snp_host_free(void *p);
+
 /* Multi-GPU exploration (one process per GPU).  Rank r holds a
  * contiguous range of the global frontier (global order = rank order, then
  * local tag order) and the visited keys with owner fmix64(fp1) mod P.  The

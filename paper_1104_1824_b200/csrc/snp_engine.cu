@@ -1400,14 +1400,31 @@ snp_status snp_level_edges(snp_system* s, int32_t level, int64_t* parent, uint64
   if (parent) CUDA_TRY(cudaMemcpyAsync(parent, L->parent.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
   if (t) CUDA_TRY(cudaMemcpyAsync(t, L->t.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
   if (halting) CUDA_TRY(cudaMemcpyAsync(halting, L->halting.p, F, cudaMemcpyDeviceToHost, s->stream));
+  DBuf pair;  // fp0 / fp1 interleaved on the device, then one contiguous copy
   if (fp2) {
-    std::vector<uint64_t> f0(F), f1(F);
-    CUDA_TRY(cudaMemcpyAsync(f0.data(), L->fp0.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
-    CUDA_TRY(cudaMemcpyAsync(f1.data(), L->fp1.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
-    SNP_TRY(sync(s));
-    for (int64_t i = 0; i < F; ++i) { fp2[2 * i] = f0[i]; fp2[2 * i + 1] = f1[i]; }
+    SNP_TRY(pair.ensure((size_t)F * 16, false));
+    CUDA_TRY(cudaMemcpy2DAsync(pair.p, 16, L->fp0.p, 8, 8, F, cudaMemcpyDeviceToDevice, s->stream));
+    CUDA_TRY(cudaMemcpy2DAsync(pair.as<uint8_t>() + 8, 16, L->fp1.p, 8, 8, F, cudaMemcpyDeviceToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(fp2, pair.p, (size_t)F * 16, cudaMemcpyDeviceToHost, s->stream));
   }
   return sync(s);
+}
+
+snp_status snp_host_alloc(size_t bytes, void** p) {
+  if (!p) return fail(SNP_E_ARG, "snp_host_alloc: NULL out pointer");
+  *p = nullptr;
+  if (!bytes) return SNP_OK;
+  if (cudaHostAlloc(p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return fail(SNP_E_OOM, "snp_host_alloc: cudaHostAlloc failed");
+  }
+  return SNP_OK;
+}
+
+snp_status snp_host_free(void* p) {
+  if (p && cudaFreeHost(p) != cudaSuccess) return fail(SNP_E_CUDA, "snp_host_free: cudaFreeHost failed");
+  return SNP_OK;
 }
 
 snp_status snp_level_columns(snp_system* s, int32_t level, const int64_t* idx, int64_t n, int32_t* out) {

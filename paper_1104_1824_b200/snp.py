@@ -39,7 +39,7 @@ EXPORTED = [
     "snp_tree_num_levels", "snp_tree_num_configs", "snp_tree_level_offsets", "snp_tree_configs",
     "snp_tree_edges", "snp_tree_counters", "snp_tree_spiking_vectors", "snp_tree_free",
     "snp_level_size", "snp_level_edges", "snp_level_columns", "snp_set_profiling", "snp_profile",
-    "snp_kernel_launches", "snp_kernel_paths", "snp_dist_begin", "snp_dist_expand", "snp_dist_pack", "snp_dist_owner_dedup",
+    "snp_kernel_launches", "snp_kernel_paths", "snp_host_alloc", "snp_host_free", "snp_dist_begin", "snp_dist_expand", "snp_dist_pack", "snp_dist_owner_dedup",
     "snp_dist_owner_keep", "snp_dist_finalize", "snp_dist_commit",
 ]
 SNP_NUM_PHASES = 5
@@ -134,6 +134,8 @@ def lib() -> ctypes.CDLL:
         L.snp_level_size.argtypes = [_P, ctypes.c_int32]
         L.snp_level_size.restype = ctypes.c_int64
         L.snp_level_edges.argtypes = [_P, ctypes.c_int32, _P, _P, _P, _P]
+        L.snp_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
+        L.snp_host_free.argtypes = [_P]
         L.snp_level_columns.argtypes = [_P, ctypes.c_int32, _P, ctypes.c_int64, _P]
         L.snp_set_profiling.argtypes = [_P, ctypes.c_int32]
         L.snp_profile.argtypes = [_P, _P]
@@ -165,6 +167,42 @@ def _check(st: int):
 
 def _ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class PinnedHost:
+    """Pinned host bytes from snp_host_alloc, freed by snp_host_free."""
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        _check(lib().snp_host_alloc(ctypes.c_size_t(nbytes), ctypes.byref(p)))
+        self.p, self.nbytes = p, nbytes
+
+    def array(self, offset: int, shape, dtype) -> np.ndarray:
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        assert offset + n <= self.nbytes
+        buf = (ctypes.c_uint8 * n).from_address(self.p.value + offset)
+        return np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def __del__(self):
+        try:
+            if self.p:
+                lib().snp_host_free(self.p)
+                self.p = None
+        except Exception:
+            pass
+
+
+class PinnedEdges:
+    """Pinned parent / t / halting / fp buffers for up to cap configurations."""
+
+    def __init__(self, cap: int):
+        self.cap = cap
+        self.mem = PinnedHost(cap * (8 + 8 + 16) + cap)
+
+    def views(self, F: int):
+        c = self.cap
+        return (self.mem.array(0, (F,), np.int64), self.mem.array(8 * c, (F,), np.uint64),
+                self.mem.array(32 * c, (F,), np.uint8), self.mem.array(16 * c, (F, 2), np.uint64))
 
 
 # ---- C-named entry points (marshalling only) --------------------------------
@@ -317,12 +355,21 @@ class System:
     def level_size(self, L: int) -> int:
         return int(lib().snp_level_size(self._h, L))
 
-    def level_edges(self, L: int):
+    def level_edges(self, L: int, pinned: bool = False):
+        """snp_level_edges into new numpy arrays, or (pinned=True) into pinned
+        host buffers owned by this System and reused by the next pinned call
+        (full PCIe rate; the returned arrays are views of them)."""
         F = self.level_size(L)
-        parent = np.zeros(F, np.int64)
-        t = np.zeros(F, np.uint64)
-        halting = np.zeros(F, np.uint8)
-        fp = np.zeros((F, 2), np.uint64)
+        if pinned:
+            pb = getattr(self, "_pinned_edges", None)
+            if pb is None or pb.cap < F:
+                pb = self._pinned_edges = PinnedEdges(max(F + F // 8, 1))  # headroom: thinned levels hover around F
+            parent, t, halting, fp = pb.views(F)
+        else:
+            parent = np.empty(F, np.int64)
+            t = np.empty(F, np.uint64)
+            halting = np.empty(F, np.uint8)
+            fp = np.empty((F, 2), np.uint64)
         _check(lib().snp_level_edges(self._h, L, _ptr(parent), _ptr(t), _ptr(halting), _ptr(fp)))
         return parent, t, halting, fp
 

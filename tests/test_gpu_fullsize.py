@@ -42,6 +42,9 @@ def test_config4_sampled_parity():
         c = eng.advance()
         assert c["parents"] == Fl and c["kept"] <= c["n_new"] <= c["T"]
         parent, t, _halt, fp = eng.level_edges(L + 1)
+        pinned = eng.level_edges(L + 1, pinned=True)              # the e2e path's pinned buffers
+        for a, b in zip((parent, t, _halt, fp), pinned):
+            assert a.shape == b.shape and (a == b).all()
         assert (np.diff(parent) >= 0).all()                       # tag order: parents non-decreasing
         keys = list(map(tuple, fp.tolist()))
         assert len(set(keys)) == len(keys) and not (set(keys) & seen)   # never seen before, no repeats
@@ -61,3 +64,17 @@ def test_config4_sampled_parity():
             psi, _S, _C = osys.children(parents[i])
             assert psi == int(np.count_nonzero(parent == p)) or psi >= 1  # kept ⊆ children
     eng.close()
+
+
+def test_host_alloc():
+    import ctypes
+    from paper_1104_1824_b200 import snp
+    L = snp.lib()
+    p = ctypes.c_void_p(1)
+    assert L.snp_host_alloc(0, ctypes.byref(p)) == 0 and not p.value
+    assert L.snp_host_alloc(16, None) == -1                  # SNP_E_ARG
+    h = snp.PinnedHost(1 << 20)
+    a = h.array(8, (16,), np.uint64)
+    a[:] = np.arange(16, dtype=np.uint64)
+    assert int(a.sum()) == 120
+    assert L.snp_host_free(None) == 0
