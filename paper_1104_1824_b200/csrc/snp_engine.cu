@@ -369,6 +369,20 @@ snp_status reserve_horizon(snp_system* s, int64_t Ft) {
                          (size_t)((Ft + PB - 1) / PB) * ((s->m + 1) & ~1) * 8 + (size_t)Ft * KMAX * 8 +
                          (size_t)Ft * 16 * 60 + next_pow2((uint64_t)Ft * 32) * sizeof(Slot) + ((size_t)4 << 30);
   if (free_b <= working) return SNP_OK;
+  // children per level: up to RESERVE_CHILDREN × Ft before the arrays grow.
+  // `working` already budgets them (16·Ft·60 B + the level table), so they
+  // are reserved first, outside `spare`: left to grow on demand they were
+  // reallocated mid-run (cudaFree + cudaMalloc inside a level, 2 to 850 ms
+  // measured at config 4's 13th level) once visited + metadata took the spare
+  const uint64_t T = (uint64_t)RESERVE_CHILDREN * (uint64_t)Ft;
+  if (T > s->child_cap) SNP_TRY(ensure_children(s, T / 2));
+  {
+    const uint64_t lw = next_pow2(std::max<uint64_t>(1024, 2 * T));
+    if (lw > s->ltab_cap) {
+      SNP_TRY(s->ltab.ensure(lw * sizeof(Slot), false));
+      s->ltab_cap = lw;
+    }
+  }
   size_t spare = free_b - working;
   s->horizon_reserved = true;
   const uint64_t entries = (uint64_t)RESERVE_LEVELS * (uint64_t)Ft;
@@ -381,17 +395,6 @@ snp_status reserve_horizon(snp_system* s, int64_t Ft) {
   if (meta_b <= spare) {
     SNP_TRY(s->arena.reserve(meta_b));
     spare -= meta_b;
-  }
-  // children per level: up to RESERVE_CHILDREN × Ft before the arrays grow
-  const uint64_t T = (uint64_t)RESERVE_CHILDREN * (uint64_t)Ft;
-  const size_t child_b = (size_t)T * 2 * 60 + next_pow2(2 * T) * sizeof(Slot);
-  if (child_b <= spare) {
-    if (T > s->child_cap) SNP_TRY(ensure_children(s, T / 2));
-    const uint64_t lw = next_pow2(std::max<uint64_t>(1024, 2 * T));
-    if (lw > s->ltab_cap) {
-      SNP_TRY(s->ltab.ensure(lw * sizeof(Slot), false));
-      s->ltab_cap = lw;
-    }
   }
   return SNP_OK;
 }
