@@ -853,20 +853,68 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
   const int64_t ld = level0->ld ? level0->ld : (level0->layout == SNP_LAYOUT_ROW_MAJOR ? m : F0);
   const size_t in_bytes = (size_t)(level0->layout == SNP_LAYOUT_ROW_MAJOR ? (F0 - 1) * ld + m : (m - 1) * ld + F0) *
                           level0->elem_bytes;
-  // stage host input on the device
-  DBuf staged;
-  const void* src = level0->data;
-  if (!level0->on_device) {
-    SNP_TRY(staged.ensure(in_bytes, false));
-    CUDA_TRY(cudaMemcpyAsync(staged.p, level0->data, in_bytes, cudaMemcpyHostToDevice, s->stream));
-    src = staged.p;
-  }
   SNP_TRY(zero_counters(s));
   DBuf raw;
   SNP_TRY(take_buffer(s, level_bytes(F0, m, s->bytes), &raw));
   int32_t* err = &dc(s)->err;
-  launch_import(src, level0->elem_bytes, level0->layout, ld, F0, (int32_t)m, raw.p, s->bytes, s->count_max, err,
-                s->stream);
+  if (!level0->on_device && level0->layout == SNP_LAYOUT_ROW_MAJOR) {
+    // host rows in chunks of R (a multiple of the 64-configuration block, so
+    // a chunk's blocks are a contiguous range of the level): two staging
+    // buffers, the copy of chunk i + 1 (side stream) overlaps the import of
+    // chunk i, and no level-sized staging allocation is needed
+    const size_t row_b = (size_t)ld * level0->elem_bytes;
+    int64_t R = std::max<int64_t>(PB, (int64_t)(((size_t)256 << 20) / row_b) & ~(int64_t)(PB - 1));
+    if (R > F0) R = F0;
+    DBuf stg[2];
+    for (auto& b : stg) SNP_TRY(b.ensure((size_t)((R - 1) * ld + m) * level0->elem_bytes, false));
+    cudaStream_t cs = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr};
+    auto cleanup = [&]() {
+      for (int b = 0; b < 2; ++b) {
+        if (copied[b]) cudaEventDestroy(copied[b]);
+        if (used[b]) cudaEventDestroy(used[b]);
+      }
+      if (cs) cudaStreamDestroy(cs);
+    };
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+      e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&used[b], cudaEventDisableTiming);
+    }
+    const uint8_t* hsrc = reinterpret_cast<const uint8_t*>(level0->data);
+    for (int64_t r0 = 0, i = 0; r0 < F0 && e == cudaSuccess; r0 += R, ++i) {
+      const int64_t n = std::min<int64_t>(R, F0 - r0);
+      const int b = (int)(i & 1);
+      if (i >= 2) e = cudaStreamWaitEvent(cs, used[b], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(stg[b].p, hsrc + (size_t)r0 * row_b, (size_t)((n - 1) * ld + m) * level0->elem_bytes,
+                            cudaMemcpyHostToDevice, cs);
+      if (e == cudaSuccess) e = cudaEventRecord(copied[b], cs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, copied[b], 0);
+      if (e != cudaSuccess) break;
+      launch_import(stg[b].p, level0->elem_bytes, SNP_LAYOUT_ROW_MAJOR, ld, n, (int32_t)m,
+                    raw.as<uint8_t>() + (size_t)r0 * m * s->bytes, s->bytes, s->count_max, err, s->stream);
+      e = cudaEventRecord(used[b], s->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);  // staging buffers are released below
+    cleanup();
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SNP_E_CUDA, "level0 upload: %s", cudaGetErrorString(e));
+    }
+  } else {
+    // stage other host input on the device in one piece
+    DBuf staged;
+    const void* src = level0->data;
+    if (!level0->on_device) {
+      SNP_TRY(staged.ensure(in_bytes, false));
+      CUDA_TRY(cudaMemcpyAsync(staged.p, level0->data, in_bytes, cudaMemcpyHostToDevice, s->stream));
+      src = staged.p;
+    }
+    launch_import(src, level0->elem_bytes, level0->layout, ld, F0, (int32_t)m, raw.p, s->bytes, s->count_max, err,
+                  s->stream);
+    if (!level0->on_device) CUDA_TRY(cudaStreamSynchronize(s->stream));
+  }
   CUDA_TRY(cudaGetLastError());
   // fingerprints of level 0
   DBuf fp0, fp1;
