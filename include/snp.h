@@ -182,6 +182,11 @@ snp_status snp_set_stream(snp_system *sys, void *cuda_stream);
 /* Incremental exploration (what bench.py times one level at a time):
  *   snp_begin    level 0 := distinct configurations of `level0` (first
  *                occurrence kept; NULL = {C0}) (reading A20), visited := level 0.
+ *                Host row-major input is uploaded in 256 MB chunks (two device
+ *                staging buffers, the copy of the next chunk overlapping the
+ *                import of the current one); pinned memory (snp_host_alloc)
+ *                copies at full PCIe rate, pageable memory works.  The input
+ *                may be released once snp_begin returns.
  *   snp_advance  expand the current frontier by one level (§8(a) a1-a6);
  *                fills *counters (may be NULL).  An empty frontier is a no-op. */
 snp_status snp_begin(snp_system *sys, const snp_configs *level0);
