@@ -355,6 +355,7 @@ def run_e2e(args, cfg, w, snp, torch):
     eng = snp.System(w, count_bits=cfg["count_bits"], dedup=cfg["dedup"], frontier_target=cfg["frontier_target"],
                      keep_tree=0)
     c0 = snp.snp_configs(host.data_ptr(), F, m, wb, snp.SNP_LAYOUT_ROW_MAJOR, 0, 0)
+    eng.reserve_edges(F + F // 8)  # the pinned result buffers, like the pinned input: allocated before timing
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     eng.begin(c0)

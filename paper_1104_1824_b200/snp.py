@@ -355,6 +355,13 @@ class System:
     def level_size(self, L: int) -> int:
         return int(lib().snp_level_size(self._h, L))
 
+    def reserve_edges(self, cap: int) -> None:
+        """Allocate the pinned buffers level_edges(pinned=True) uses for up to
+        cap configurations now (cudaHostAlloc is slow: keep it out of a loop)."""
+        pb = getattr(self, "_pinned_edges", None)
+        if pb is None or pb.cap < cap:
+            self._pinned_edges = PinnedEdges(max(cap, 1))
+
     def level_edges(self, L: int, pinned: bool = False):
         """snp_level_edges into new numpy arrays, or (pinned=True) into pinned
         host buffers owned by this System and reused by the next pinned call
