@@ -1461,7 +1461,7 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #endif
 // tuning toggles (tools/gpu_ab.sh), measured at config 4: 32 warps with
 // 64 registers beat 24 warps (70.4 ms) and 16 warps (83 ms); loading the row
-// before the gather (SNP_KC_PREFETCH=1: 68.6 ms) or one iteration ahead
+// before the gather (SNP_KC_PREFETCH=1: 68.6 ms; 64.2 vs 63.7 with the L2 row prefetch on) or one iteration ahead
 // (77 ms, spills) loses to loading it where it is used (66.5 ms)
 #ifndef SNP_KC_COOP
 #define SNP_KC_COOP 1  // warp-cooperative stores of the full 4-child quads (else the per-lane store program)
@@ -1472,6 +1472,11 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_BRANCHLESS
 #define SNP_KC_BRANCHLESS 0  // cooperative quads: the upper-window permute unconditionally (no per-lane branch); measured 64.1 vs 63.9 ms
 #endif
+#ifndef SNP_KC_GUNROLL
+#define SNP_KC_GUNROLL 2  // the two 32-parent halves unrolled (measured 61.4 vs 63.7 ms rolled)
+#endif
+#define SNP_PRAGMA_(x) _Pragma(#x)
+#define SNP_PRAGMA(x) SNP_PRAGMA_(x)
 #ifndef SNP_KC_EDGE
 #define SNP_KC_EDGE 1  // boundary bytes of a row end as <= 2 aligned stores (else one byte store per child)
 #endif
@@ -1749,7 +1754,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
 #pragma unroll
       for (int b = 4; b < NPL; ++b) up |= c[b];
       const bool upper = __any_sync(__activemask(), up != 0);
-#pragma unroll 1  // two halves of 32 parents; rolled keeps the hot loop in the instruction cache
+      SNP_PRAGMA(unroll SNP_KC_GUNROLL)  // two halves of 32 parents; rolled (1) keeps the hot loop in the instruction cache
       for (int g = 0; g < 2; ++g) {
 #if SNP_KC_PREFETCH
         uint32_t vn[8];
