@@ -1467,7 +1467,7 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #define SNP_KC_COOP 1  // warp-cooperative stores of the full 4-child quads (else the per-lane store program)
 #endif
 #ifndef SNP_KC_L2PF
-#define SNP_KC_L2PF 2  // k > 0: L2 bulk prefetch of the warp's parent rows k - 1 iterations ahead (measured: 0 64.2 ms, 1 64.0, 2 63.7, 3 63.9)
+#define SNP_KC_L2PF 1  // k > 0: L2 bulk prefetch of the warp's parent rows k - 1 iterations ahead (rolled halves: 0 64.2 ms, 1 64.0, 2 63.7, 3 63.9; unrolled: 1 60.8, 2 61.3)
 #endif
 #ifndef SNP_KC_BRANCHLESS
 #define SNP_KC_BRANCHLESS 0  // cooperative quads: the upper-window permute unconditionally (no per-lane branch); measured 64.1 vs 63.9 ms
