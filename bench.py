@@ -16,8 +16,8 @@ e2e         the same metric through the public C ABI from a pinned HOST level 0
             result (edges + fingerprints of the new frontier) read back.
 roofline    dominant kernel phase: algorithmic bytes ÷ its
             CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline  the CPU oracle (oracle/, single thread, as it stands) on a
-            bounded sample of the same workload.
+cpu_baseline  the CPU oracle (oracle/, as it stands: oracle_explore_par with
+            one thread per host core) on a bounded sample of the same workload.
 --impl reference  the oracle as the reference arm (this tier has no reference
             code): each step = the oracle on a bounded sample of the workload.
 """
@@ -156,41 +156,67 @@ def ncu_traffic(kernel_phase):
 # ---------------------------------------------------------------------------
 # CPU oracle sample (cpu_baseline and the reference arm)
 # ---------------------------------------------------------------------------
-def oracle_sample(w, cfg, rows_begin, n_rows):
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_sample(w, cfg, rows_begin, n_rows, threads):
+    """the oracle (oracle_explore_par: children of each parent on `threads`
+    host threads, decisions in canonical order) expanding n_rows level-0
+    parents of the workload by one level; returns (T, seconds)."""
     import oracle
     sysw = oracle.System.from_workload(w)
     L0 = W.level0_counts(w, n_rows, cfg["seed"], row_begin=rows_begin)
     t0 = time.perf_counter()
-    run = sysw.explore(L0, depth=1, dedup=cfg["dedup"], count_bits=cfg["count_bits"])
+    run = sysw.explore_par(L0, depth=1, dedup=cfg["dedup"], count_bits=cfg["count_bits"], n_threads=threads)
     dt = time.perf_counter() - t0
     assert run.status == 0, run.error
-    return int(run.counters.T.sum()), dt
+    T = int(run.counters.T.sum())
+    run.close()
+    return T, dt
 
 
-def calibrate_rows(w, cfg, target_s):
-    T, dt = oracle_sample(w, cfg, 0, 4)
-    per_row = max(dt / 4, 1e-4)
-    return max(4, min(4096, int(target_s / per_row)))
+def calibrate_rows(w, cfg, target_s, threads):
+    n0 = 4 * threads
+    T, dt = oracle_sample(w, cfg, 0, n0, threads)
+    per_row = max(dt / n0, 1e-5)
+    return max(n0, min(1 << 17, int(target_s / per_row)))
 
 
 def cpu_baseline(w, cfg, target_s=12.0):
-    rows = calibrate_rows(w, cfg, target_s)
-    T, dt = oracle_sample(w, cfg, 0, rows)
-    return {"value": T / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle BFS (C++ oracle/, 1 thread) expanding {rows} level-0 parents of the same workload "
-                      f"by one level: {T} transitions in {dt:.1f} s"}
+    cores = host_cores()
+    rows = calibrate_rows(w, cfg, target_s, cores)
+    T, dt = oracle_sample(w, cfg, 0, rows, cores)
+    return {"value": T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"oracle BFS (C++ oracle/ oracle_explore_par, {cores} threads on {cores} host cores, "
+                      f"{cpu_model()}) expanding {rows} level-0 parents of the same workload by one level: "
+                      f"{T} transitions in {dt:.1f} s"}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg, w = workload_for(args)
-    rows = calibrate_rows(w, cfg, 2.0)
+    cores = host_cores()
+    rows = calibrate_rows(w, cfg, 2.0, cores)
     for i in range(args.warmup):
-        oracle_sample(w, cfg, i * rows, rows)
+        oracle_sample(w, cfg, i * rows, rows, cores)
     Ts, dts = [], []
     for i in range(args.steps):
-        T, dt = oracle_sample(w, cfg, (args.warmup + i) * rows, rows)
+        T, dt = oracle_sample(w, cfg, (args.warmup + i) * rows, rows, cores)
         Ts.append(T)
         dts.append(dt)
     value = sum(Ts) / sum(dts)
@@ -198,8 +224,9 @@ def run_reference(args, rank, world):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(dts) / len(dts),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
            "data": "synthetic", "config": config_json(args, cfg, w, args.steps),
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": f"each step: oracle BFS expanding {rows} level-0 parents by one level"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"each step: oracle BFS (oracle_explore_par, {cores} threads, {cpu_model()}) "
+                                      f"expanding {rows} level-0 parents by one level"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -262,9 +289,11 @@ def run_native(args, rank, world):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    levels = []
+    levels, lvl_prof = [], []
     for _ in range(args.steps):
         levels.append(runner.advance())
+        if not use_dist:
+            lvl_prof.append(eng.profile())  # cumulative phase times: per-level deltas below (drift attribution)
     e1.record(stream)
     torch.cuda.synchronize()
     if dist:
@@ -312,7 +341,9 @@ def run_native(args, rank, world):
         "phase_ms_per_step": {**{k: v / args.steps for k, v in phase_ms.items()},
                               "other": elapsed_ms / args.steps - sum(phase_ms.values()) / args.steps},
         "levels": [{k: c[k] for k in ("parents", "halting", "T", "n_new", "kept")} | {"ms": round(c["ms"], 3)}
-                   for c in levels],
+                   | ({"phase_ms": {k: round(lvl_prof[i][k] - (lvl_prof[i - 1] if i else prof0)[k], 3)
+                                    for k in ("expand", "keys", "dedup", "materialize")}} if lvl_prof else {})
+                   for i, c in enumerate(levels)],
         "digest": f"{digest:016x}", "gpu_launches": launches, "clocks": clk,
     }
     eng.close()
@@ -364,8 +395,8 @@ def run_e2e(args, cfg, w, snp, torch):
     for _ in range(args.steps):
         c = eng.advance()
         T_sum += c["T"]
-        parent, t, halting, fp = eng.level_edges(eng.depth, pinned=True)
-        d2h += parent.nbytes + t.nbytes + fp.nbytes + halting.nbytes
+        parent, t, _h, fp = eng.level_edges(eng.depth, pinned=True, halting=False)
+        d2h += parent.nbytes + t.nbytes + fp.nbytes
     dt_s = time.perf_counter() - t0
     eng.close()
     del host

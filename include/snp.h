@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SNP_ABI_VERSION 1
+#define SNP_ABI_VERSION 2
 
 typedef enum {
   SNP_OK = 0,
@@ -100,6 +100,12 @@ typedef struct {
   int32_t out_rule1;         /* 0 = off.  r + 1: generated numbers with
                                 rule r of the output neuron (PAPER.md:89 `out`) as its spiking
                                 rule — see "Generated numbers" below                          */
+  int32_t keep_all_edges;    /* 1 = also record EVERY transition (parent, t) of each level with
+                                the configuration it reached (reading A17; the computation tree
+                                of Fig. 4, including the edges to configurations
+                                already seen): snp_level_all_edges.  Costs 8 B per transition
+                                + 8 B per parent of device memory per level.                   */
+  int32_t reserved;          /* 0 */
 } snp_options;
 
 /* Generated numbers (Π "generates all numbers in N - {1}"; the
@@ -141,6 +147,11 @@ typedef struct {
   int64_t kept;        /* children kept in the next frontier (after thinning)   */
   uint64_t tau;        /* thinning threshold used (0 = no thinning)             */
   double ms;           /* device time of the level (CUDA events)                */
+  int64_t overflow_fixes; /* (parent, neuron) base values (every neuron fires its first
+                             applicable rule) outside the storage range, for parents with a
+                             kept child: their kept children's entries were recomputed
+                             exactly (k_overflow_fix); 0 on the paths that compute every
+                             entry exactly                                                  */
 } snp_level_counters;
 
 typedef struct snp_system snp_system;
@@ -174,6 +185,9 @@ snp_status snp_load_unary(const snp_matrix *M, const snp_rule *rules, int64_t n_
  * Errors as snp_load, plus SNP_E_ARG for a negative delay.                   */
 snp_status snp_load_delay(const snp_matrix *M, const snp_rule *rules, int64_t n_rules, const int32_t *delays,
                           const int32_t *C0, int64_t m, const snp_options *opt, snp_system **out);
+/* Releases the caller's reference.  Trees taken from the system (snp_tree)
+ * keep it alive: the device state is released when the last of the system
+ * and its trees is freed, so a tree stays readable after snp_system_free.  */
 void       snp_system_free(snp_system *sys);
 
 /* Launch all device work of `sys` on this cudaStream_t (NULL = library stream). */
@@ -216,6 +230,45 @@ int64_t    snp_level_size(const snp_system *sys, int32_t level);
 snp_status snp_level_edges(snp_system *sys, int32_t level, int64_t *parent, uint64_t *t, uint8_t *halting,
                            uint64_t *fp2);
 snp_status snp_level_columns(snp_system *sys, int32_t level, const int64_t *idx, int64_t n, int32_t *out);
+
+/* The spiking vectors S ("generate the succeeding C_k's and
+ * their corresponding S_k's"; Alg. 2 II-2/II-3, order of
+ * reading A7) — n bytes of 0/1 per vector, rule order = the total order of
+ * snp_load:
+ *   snp_spiking_vector         the t-th valid spiking vector of the host
+ *                              configuration C (snp_state_width int32 counts,
+ *                              each in the storage range); SNP_E_ARG when
+ *                              t >= Ψ(C) (a halting C has no spiking vector).
+ *   snp_level_spiking_vectors  the vector that produced configurations
+ *                              idx[0..n) of level L >= 1 from their parents;
+ *                              needs level L-1's counts on the device: every
+ *                              level with keep_tree = 1 or dedup = 0, else
+ *                              the newest level (the engine keeps its parent
+ *                              level until the next snp_advance).
+ * Systems with delays: SNP_E_STATE.  Synchronous.                            */
+snp_status snp_spiking_vector(snp_system *sys, const int32_t *C, uint64_t t, uint8_t *S_out /* n */);
+snp_status snp_level_spiking_vectors(snp_system *sys, int32_t level, const int64_t *idx, int64_t n,
+                                     uint8_t *S_out /* n_idx × n_rules */);
+
+/* The current frontier (the newest level) copied to host buffers, any of them
+ * NULL: configs (F × snp_state_width int32, row-major), parent (index in the
+ * previous level, -1 at level 0), t (spiking-vector index).  cap = rows the
+ * buffers hold; SNP_E_CAPACITY (nothing copied) when F > cap.  *n_out = F.   */
+snp_status snp_frontier_copy(snp_system *sys, int32_t *configs, int64_t *parent, uint64_t *t, int64_t cap,
+                             int64_t *n_out);
+
+/* Every transition of the expansion that produced level L >= 1 (options
+ * keep_all_edges = 1; reading A17): T(L-1) edges in tag order (parents of
+ * level L-1 in order, t increasing), edge e = (parent[e], t[e]) reached the
+ * configuration ref[e] = its global discovery index (level offsets as in
+ * snp_tree: Σ sizes of the earlier levels + index in its level), or -1 when
+ * the child was not stored (dropped by thinning, reading A19, or a terminal
+ * transition of generated numbers).  The first-discovery edge of a stored
+ * child (snp_level_edges) is among them.  *n_edges = T(L-1); the arrays
+ * (any may be NULL) must hold cap entries, SNP_E_CAPACITY when T > cap.
+ * SNP_E_STATE without keep_all_edges or in distributed mode.                */
+snp_status snp_level_all_edges(snp_system *sys, int32_t level, int64_t *parent, uint64_t *t, int64_t *ref,
+                               int64_t cap, int64_t *n_edges);
 
 /* Phase timing (CUDA events on the system's stream), accumulated since the
  * last snp_begin while profiling is on.  Phases (SNP_NUM_PHASES):

@@ -43,7 +43,7 @@ def build(force: bool = False) -> str:
     """Compile oracle.cpp into liboracle.so (plain g++, no GPU code)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-o", tmp, _SRC])
+        subprocess.check_call(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-pthread", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -94,6 +94,23 @@ def lib() -> ctypes.CDLL:
         L.oracle_run_tree.argtypes = [_P, _P, _P, _P, _P]
         L.oracle_run_counters.argtypes = [_P, _P, _P, _P]
         L.oracle_run_free.argtypes = [_P]
+        L.oracle_run_num_edges.argtypes = [_P, _I64]
+        L.oracle_run_num_edges.restype = _I64
+        L.oracle_run_edges.argtypes = [_P, _I64, _P]
+        L.oracle_explore_par.argtypes = [_P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _U64, _U64, _I32,
+                                         ctypes.POINTER(_P)]
+        L.oracle_explore_par.restype = ctypes.c_int
+        L.oracle_prun_free.argtypes = [_P]
+        L.oracle_prun_status.argtypes = [_P]
+        L.oracle_prun_error.argtypes = [_P]
+        L.oracle_prun_error.restype = ctypes.c_char_p
+        for f in ("oracle_prun_num_configs", "oracle_prun_num_levels", "oracle_prun_num_expanded"):
+            getattr(L, f).argtypes = [_P]
+            getattr(L, f).restype = _I64
+        L.oracle_prun_level_offsets.argtypes = [_P, _P]
+        L.oracle_prun_tree.argtypes = [_P, _P, _P, _P, _P]
+        L.oracle_prun_counters.argtypes = [_P, _P, _P, _P]
+        L.oracle_prun_rows.argtypes = [_P, _P, _I64, _P]
         _lib = L
     return _lib
 
@@ -239,6 +256,66 @@ class System:
             raise OracleError(st, "bad argument")
         return Run(self, h, st, width)
 
+    def explore_par(self, level0, depth: int, dedup: int = 0, count_bits: int = 32, frontier_target: int = 0,
+                    max_transitions: int = 0, seeds=(0x5EED0, 0x5EED1), n_threads: int | None = None) -> "ParRun":
+        """oracle_explore_par: the tree of ``explore`` (no generated numbers)
+        with the children of each parent computed by ``n_threads`` threads and
+        every decision taken in canonical order by one thread (oracle.cpp);
+        pinned against ``explore`` in tests/test_oracle_par.py."""
+        L0 = np.ascontiguousarray(np.atleast_2d(level0), dtype=np.int32)
+        assert L0.shape[1] == self.m
+        n_threads = n_threads or os.cpu_count() or 1
+        h = _P()
+        st = lib().oracle_explore_par(self._h, L0.shape[0], _ptr(L0), depth, dedup, count_bits, frontier_target,
+                                      max_transitions, seeds[0], seeds[1], n_threads, ctypes.byref(h))
+        if st == OR_E_ARG and not h:
+            raise OracleError(st, "bad argument")
+        return ParRun(self, h, st)
+
+
+class ParRun:
+    """Result of ``System.explore_par``: the tree's edges, fingerprints and
+    counters on the host; configuration rows fetched on demand (``rows``)."""
+
+    def __init__(self, sys: System, h, status: int):
+        L = lib()
+        self._h, self.m, self.status = h, sys.m, status
+        self.error = L.oracle_prun_error(h).decode() if h else ""
+        nc = L.oracle_prun_num_configs(h)
+        nl = L.oracle_prun_num_levels(h)
+        ne = L.oracle_prun_num_expanded(h)
+        self.level_offsets = np.zeros(nl + 1, np.int64)
+        L.oracle_prun_level_offsets(h, _ptr(self.level_offsets))
+        self.parent = np.zeros(nc, np.int64)
+        self.t = np.zeros(nc, np.uint64)
+        self.halting = np.zeros(nc, np.uint8)
+        self.fp = np.zeros((nc, 2), np.uint64)
+        L.oracle_prun_tree(h, _ptr(self.parent), _ptr(self.t), _ptr(self.halting), _ptr(self.fp))
+        T, nn, kp = (np.zeros(ne, np.int64) for _ in range(3))
+        L.oracle_prun_counters(h, _ptr(T), _ptr(nn), _ptr(kp))
+        self.counters = Counters(T, nn, kp)
+
+    def rows(self, idx) -> np.ndarray:
+        idx = np.ascontiguousarray(idx, np.int64)
+        out = np.zeros((idx.shape[0], self.m), np.int32)
+        lib().oracle_prun_rows(self._h, _ptr(idx), idx.shape[0], _ptr(out))
+        return out
+
+    @property
+    def num_levels(self) -> int:
+        return len(self.level_offsets) - 1
+
+    def close(self):
+        if self._h:
+            lib().oracle_prun_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
 
 @dataclass
 class Counters:
@@ -277,6 +354,12 @@ class Run:
             nums = np.zeros(L.oracle_run_num_numbers(h), np.int64)
             L.oracle_run_numbers(h, _ptr(nums))
             self.numbers = set(int(x) for x in nums)
+            # reading A17: every transition of expanded level L -> configuration index (-1 = not stored)
+            self.edge_ref = []
+            for lv in range(ne):
+                e = np.zeros(L.oracle_run_num_edges(h, lv), np.int64)
+                L.oracle_run_edges(h, lv, _ptr(e))
+                self.edge_ref.append(e)
         finally:
             L.oracle_run_free(h)
 

@@ -24,6 +24,9 @@
 #include <string>
 #include <vector>
 #include <set>
+#include <map>
+#include <thread>
+#include <unordered_map>
 #include <utility>
 #include <algorithm>
 
@@ -245,6 +248,11 @@ struct Run {
   std::vector<uint64_t> fp0, fp1;
   std::vector<int64_t> level_T, level_new, level_kept;  // per expanded level
   std::set<int64_t> numbers;                   // generated numbers (out_rule >= 0)
+  // Reading A17 (every edge of the computation tree, Fig. 4):
+  // for expanded level L, one entry per transition in (parent, t) order = the
+  // global discovery index of the configuration it reached, or -1 when that
+  // child was not stored (thinned, reading A19; terminal, generated numbers)
+  std::vector<std::vector<int64_t>> edge_ref;
 };
 
 }  // namespace
@@ -377,14 +385,22 @@ int oracle_explore_gen(const oracle_system* h, int64_t F0, const int32_t* level0
   Run& run = hr->r;
   *out = hr;
 
-  std::set<std::vector<int64_t>> visited_rows;      // dedup = 0
-  std::set<std::pair<uint64_t, uint64_t>> visited_fp;  // dedup = 1
-  auto seen = [&](const std::vector<int64_t>& C, const std::pair<uint64_t, uint64_t>& f) {
-    return dedup == 0 ? visited_rows.count(C) > 0 : visited_fp.count(f) > 0;
+  // visited configurations (all earlier levels, reading A6) -> global index
+  std::map<std::vector<int64_t>, int64_t> visited_rows;      // dedup = 0
+  std::map<std::pair<uint64_t, uint64_t>, int64_t> visited_fp;  // dedup = 1
+  auto seen_at = [&](const std::vector<int64_t>& C, const std::pair<uint64_t, uint64_t>& f) -> int64_t {
+    if (dedup == 0) {
+      auto it = visited_rows.find(C);
+      return it == visited_rows.end() ? -1 : it->second;
+    }
+    auto it = visited_fp.find(f);
+    return it == visited_fp.end() ? -1 : it->second;
   };
+  auto seen = [&](const std::vector<int64_t>& C, const std::pair<uint64_t, uint64_t>& f) { return seen_at(C, f) >= 0; };
   auto insert = [&](const std::vector<int64_t>& C, const std::pair<uint64_t, uint64_t>& f) {
-    if (dedup == 0) visited_rows.insert(C);
-    else visited_fp.insert(f);
+    const int64_t idx = (int64_t)run.configs.size();  // the index push() gives it
+    if (dedup == 0) visited_rows.emplace(C, idx);
+    else visited_fp.emplace(f, idx);
   };
   auto push = [&](const std::vector<int64_t>& C, const std::pair<uint64_t, uint64_t>& f,
                   int64_t parent, uint64_t t) {
@@ -413,8 +429,11 @@ int oracle_explore_gen(const oracle_system* h, int64_t F0, const int32_t* level0
     if (lo == hi) break;  // stopping criterion 2: nothing new
     struct Cand { int64_t parent; uint64_t t; std::vector<int64_t> C; std::pair<uint64_t, uint64_t> f; };
     std::vector<Cand> fresh;  // new children in tag order (parent order, then t)
-    std::set<std::vector<int64_t>> level_rows;
-    std::set<std::pair<uint64_t, uint64_t>> level_fp;
+    std::map<std::vector<int64_t>, int64_t> level_rows;         // -> index in fresh
+    std::map<std::pair<uint64_t, uint64_t>, int64_t> level_fp;
+    // per transition: global index of a configuration seen earlier (>= 0), or
+    // -(2 + i) for the new child fresh[i] (resolved after thinning), or -1
+    std::vector<int64_t> eref;
     int64_t T = 0;
     for (int64_t i = lo; i < hi; ++i) {
       const std::vector<int64_t> Caug = run.configs[i];
@@ -432,14 +451,31 @@ int oracle_explore_gen(const oracle_system* h, int64_t F0, const int32_t* level0
           const bool fired = S[out_rule] != 0;
           if (a >= 1 && fired) {  // second output spike: the number a is generated
             run.numbers.insert(a);
+            eref.push_back(-1);
             continue;
           }
           Cn.push_back(a == 0 ? (fired ? 1 : 0) : a + 1);
         }
         auto f = fingerprint(Cn, seed0, seed1);
-        if (seen(Cn, f)) continue;  // produced at an earlier level (A6)
-        bool dup_here = dedup == 0 ? !level_rows.insert(Cn).second : !level_fp.insert(f).second;
-        if (dup_here) continue;  // same-level duplicate: first (minimum) tag wins
+        const int64_t old = seen_at(Cn, f);
+        if (old >= 0) {  // produced at an earlier level (A6)
+          eref.push_back(old);
+          continue;
+        }
+        const int64_t slot = (int64_t)fresh.size();
+        int64_t first = slot;  // the level's first child with this key
+        if (dedup == 0) {
+          auto ins = level_rows.emplace(Cn, slot);
+          first = ins.first->second;
+        } else {
+          auto ins = level_fp.emplace(f, slot);
+          first = ins.first->second;
+        }
+        if (first != slot) {  // same-level duplicate: first (minimum) tag wins
+          eref.push_back(-(2 + first));
+          continue;
+        }
+        eref.push_back(-(2 + slot));
         fresh.push_back(Cand{i - lo, t, Cn, f});
       }
     }
@@ -447,8 +483,11 @@ int oracle_explore_gen(const oracle_system* h, int64_t F0, const int32_t* level0
     int64_t kept = 0;
     const bool thin = frontier_target > 0 && n_new > frontier_target;
     const uint64_t tau = thin ? oracle_thinning_tau(frontier_target, n_new) : 0;
-    for (const Cand& c : fresh) {
+    std::vector<int64_t> fresh_index(fresh.size(), -1);  // global index of each kept new child
+    for (size_t ci = 0; ci < fresh.size(); ++ci) {
+      const Cand& c = fresh[ci];
       if (thin && !(fmix64(c.f.first) < tau)) continue;  // reading A19
+      fresh_index[ci] = (int64_t)run.configs.size();
       for (int64_t v : c.C) {
         if (v < 0) { run.status = OR_E_OVERFLOW; run.error = "negative count"; return run.status; }
         if (v > cmax) { run.status = OR_E_OVERFLOW; run.error = "count above storage range"; return run.status; }
@@ -461,6 +500,9 @@ int oracle_explore_gen(const oracle_system* h, int64_t F0, const int32_t* level0
     run.level_new.push_back(n_new);
     run.level_kept.push_back(kept);
     run.level_offsets.push_back((int64_t)run.configs.size());
+    for (int64_t& r : eref)
+      if (r <= -2) r = fresh_index[(size_t)(-r - 2)];
+    run.edge_ref.push_back(std::move(eref));
     if (kept == 0) break;
   }
   // Halting classification of every configuration (reading A5).
@@ -751,5 +793,284 @@ void oracle_run_counters(const oracle_run* h, int64_t* T, int64_t* n_new, int64_
   for (size_t i = 0; i < r.level_T.size(); ++i) { T[i] = r.level_T[i]; n_new[i] = r.level_new[i]; kept[i] = r.level_kept[i]; }
 }
 void oracle_run_free(oracle_run* h) { delete h; }
+// reading A17: transitions of expanded level L (= T of that level) and the
+// configuration each reached (global discovery index, -1 = not stored)
+int64_t oracle_run_num_edges(const oracle_run* h, int64_t L) {
+  return L >= 0 && L < (int64_t)h->r.edge_ref.size() ? (int64_t)h->r.edge_ref[L].size() : 0;
+}
+void oracle_run_edges(const oracle_run* h, int64_t L, int64_t* ref) {
+  if (L >= 0 && L < (int64_t)h->r.edge_ref.size()) std::copy(h->r.edge_ref[L].begin(), h->r.edge_ref[L].end(), ref);
+}
+
+}  // extern "C"
+
+// ============================================================================
+// oracle_explore_par — the breadth-first tree of oracle_explore (dedup 0/1,
+// thinning, overflow; no generated numbers) for frontiers of 10^5-10^6
+// configurations (configs 3 and 5 of BASELINE.json at their stated sizes).
+// Same definitions, same order of decisions:
+//   * children of each parent: applicable_rules_per_neuron, count_children,
+//     spiking_vector, transition, fingerprint — the functions above, called by
+//     n_threads threads over disjoint ranges of parents (a child depends only
+//     on its parent, Alg. 1 II-III);
+//   * the dedup / thinning / insertion decisions are taken by ONE thread over
+//     the children in canonical (parent, t) order, exactly as oracle_explore
+//     (readings A6, A7, A16, A19, A20).
+// Storage differs only in representation: visited configurations live in a
+// flat arena of count_bits / 8 bytes per count (every stored count is in
+// [0, 2^count_bits - 1] by the overflow check, so the slot holds it exactly), the visited set is a hash map from fp0 to arena
+// indices compared row by row (dedup = 0: exact equality; dedup = 1: equality
+// of (fp0, fp1)), and a new child's row is recomputed from (parent, t) when a
+// comparison or the kept row needs it instead of being held for the level.
+// Pinned against oracle_explore on every shape of the parity suite
+// (tests/test_oracle_par.py).
+// ============================================================================
+namespace {
+
+struct ParRun {
+  int status = OR_OK;
+  std::string error;
+  int64_t m = 0;
+  int64_t w = 4;                       // bytes per stored count: 1 / 2 / 4 for count_bits 8 / 16 / 32
+  std::vector<uint8_t> arena;          // stored configurations, m counts of w bytes each, discovery order
+  std::vector<int64_t> level_offsets;
+  std::vector<int64_t> parent;
+  std::vector<uint64_t> t, fp0, fp1;
+  std::vector<uint8_t> halting;
+  std::vector<int64_t> level_T, level_new, level_kept;
+  // count j of stored configuration i (every stored count is in [0, 2^(8w) - 1], reading A16)
+  int64_t at(int64_t i, int64_t j) const {
+    const uint8_t* p = arena.data() + ((size_t)i * (size_t)m + (size_t)j) * (size_t)w;
+    if (w == 1) return p[0];
+    if (w == 2) return (int64_t)p[0] | ((int64_t)p[1] << 8);
+    int32_t v;
+    memcpy(&v, p, 4);
+    return v;
+  }
+  void append(const std::vector<int64_t>& C) {
+    for (int64_t v : C)
+      for (int64_t b = 0; b < w; ++b) arena.push_back((uint8_t)((uint64_t)v >> (8 * b)));
+  }
+};
+
+// run f(i) for i in [lo, hi) on n threads (contiguous ranges)
+template <class F>
+void parallel_for(int64_t lo, int64_t hi, int n, F f) {
+  if (hi <= lo) return;
+  if (n <= 1 || hi - lo < 2) {
+    for (int64_t i = lo; i < hi; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t len = hi - lo;
+  for (int k = 0; k < n; ++k) {
+    const int64_t a = lo + len * k / n, b = lo + len * (k + 1) / n;
+    th.emplace_back([=]() { for (int64_t i = a; i < b; ++i) f(i); });
+  }
+  for (auto& x : th) x.join();
+}
+
+}  // namespace
+
+extern "C" {
+
+struct oracle_prun { ParRun r; };
+
+int oracle_explore_par(const oracle_system* h, int64_t F0, const int32_t* level0, int32_t depth, int32_t dedup,
+                       int32_t count_bits, int64_t frontier_target, int64_t max_transitions, uint64_t seed0,
+                       uint64_t seed1, int32_t n_threads, oracle_prun** out) {
+  const System& s = h->s;
+  if (!out || F0 < 1 || depth < 0 || (dedup != 0 && dedup != 1)) return OR_E_ARG;
+  if (count_bits != 8 && count_bits != 16 && count_bits != 32) return OR_E_ARG;
+  const int64_t cmax = count_bits == 8 ? 255 : count_bits == 16 ? 65535 : 2147483647LL;
+  const int64_t m = s.m;
+  auto* hr = new oracle_prun();
+  ParRun& run = hr->r;
+  *out = hr;
+  run.m = m;
+  run.w = count_bits / 8;
+  if (n_threads < 1) n_threads = 1;
+  // visited: fp0 -> arena indices (dedup 0: rows compared; dedup 1: fp1 compared)
+  std::unordered_multimap<uint64_t, int64_t> visited;
+  auto row_equal = [&](int64_t i, const int64_t* C) {
+    for (int64_t j = 0; j < m; ++j)
+      if (run.at(i, j) != C[j]) return false;
+    return true;
+  };
+  auto seen = [&](const int64_t* C, const std::pair<uint64_t, uint64_t>& f) {
+    auto rg = visited.equal_range(f.first);
+    for (auto it = rg.first; it != rg.second; ++it) {
+      const int64_t i = it->second;
+      if (dedup == 1 ? run.fp1[i] == f.second : row_equal(i, C)) return true;
+    }
+    return false;
+  };
+  auto push = [&](const std::vector<int64_t>& C, const std::pair<uint64_t, uint64_t>& f, int64_t parent, uint64_t t) {
+    const int64_t idx = (int64_t)run.parent.size();
+    run.append(C);
+    run.parent.push_back(parent);
+    run.t.push_back(t);
+    run.fp0.push_back(f.first);
+    run.fp1.push_back(f.second);
+    visited.emplace(f.first, idx);
+  };
+  auto row_of = [&](int64_t i) {
+    std::vector<int64_t> r(m);
+    for (int64_t j = 0; j < m; ++j) r[j] = run.at(i, j);
+    return r;
+  };
+  // Level 0 (reading A20)
+  run.level_offsets.push_back(0);
+  for (int64_t i = 0; i < F0; ++i) {
+    std::vector<int64_t> C(level0 + i * m, level0 + (i + 1) * m);
+    for (int64_t v : C)
+      if (v < 0 || v > cmax) { run.status = OR_E_OVERFLOW; run.error = "level 0 count out of range"; return run.status; }
+    auto f = fingerprint(C, seed0, seed1);
+    if (seen(C.data(), f)) continue;
+    push(C, f, -1, 0);
+  }
+  run.level_offsets.push_back((int64_t)run.parent.size());
+  for (int32_t L = 0; L < depth; ++L) {
+    const int64_t lo = run.level_offsets[L], hi = run.level_offsets[L + 1];
+    if (lo == hi) break;
+    const int64_t F = hi - lo;
+    // applicable rules and Ψ of every parent (eq. (8), readings A3-A5)
+    std::vector<uint64_t> psi(F, 0);
+    std::vector<char> cap_err(F, 0);
+    parallel_for(0, F, n_threads, [&](int64_t i) {
+      auto A = applicable_rules_per_neuron(s, row_of(lo + i));
+      if (!count_children(A, &psi[i])) cap_err[i] = 1;
+    });
+    for (int64_t i = 0; i < F; ++i)
+      if (cap_err[i]) { run.status = OR_E_CAPACITY; run.error = "psi above 2^62"; return run.status; }
+    struct Cand { int64_t parent; uint64_t t; std::pair<uint64_t, uint64_t> f; };
+    std::vector<Cand> fresh;
+    std::unordered_multimap<uint64_t, int64_t> level_keys;  // fp0 -> index in fresh
+    auto child_row = [&](int64_t parent_in_level, uint64_t t) {
+      const std::vector<int64_t> C = row_of(lo + parent_in_level);
+      auto A = applicable_rules_per_neuron(s, C);
+      return transition(s, C, spiking_vector(s, A, t));
+    };
+    int64_t T = 0;
+    // parents in chunks whose children fit a bounded buffer
+    const uint64_t budget = std::max<uint64_t>(1, ((uint64_t)1 << 28) / (uint64_t)m);  // children per chunk
+    for (int64_t c0 = 0; c0 < F;) {
+      int64_t c1 = c0;
+      uint64_t nch = 0;
+      while (c1 < F && (c1 == c0 || nch + psi[c1] <= budget)) nch += psi[c1++];
+      std::vector<uint64_t> base(c1 - c0 + 1, 0);
+      for (int64_t i = c0; i < c1; ++i) base[i - c0 + 1] = base[i - c0] + psi[i];
+      std::vector<int64_t> rows((size_t)nch * (size_t)m);
+      std::vector<std::pair<uint64_t, uint64_t>> fps(nch);
+      parallel_for(c0, c1, n_threads, [&](int64_t i) {
+        const std::vector<int64_t> C = row_of(lo + i);
+        auto A = applicable_rules_per_neuron(s, C);
+        for (uint64_t t = 0; t < psi[i]; ++t) {
+          auto Cn = transition(s, C, spiking_vector(s, A, t));
+          const uint64_t k = base[i - c0] + t;
+          std::copy(Cn.begin(), Cn.end(), rows.begin() + (size_t)k * (size_t)m);
+          fps[k] = fingerprint(Cn, seed0, seed1);
+        }
+      });
+      // canonical order: parents in order, t increasing (reading A7)
+      for (int64_t i = c0; i < c1; ++i) {
+        for (uint64_t t = 0; t < psi[i]; ++t) {
+          ++T;
+          if (max_transitions > 0 && T > max_transitions) { run.status = OR_E_CAPACITY; run.error = "transition budget exceeded"; return run.status; }
+          const uint64_t k = base[i - c0] + t;
+          const int64_t* Cn = rows.data() + (size_t)k * m;
+          const auto& f = fps[k];
+          if (seen(Cn, f)) continue;  // produced at an earlier level (A6)
+          bool dup = false;
+          auto rg = level_keys.equal_range(f.first);
+          for (auto it = rg.first; it != rg.second && !dup; ++it) {
+            const Cand& o = fresh[it->second];
+            dup = dedup == 1 ? o.f.second == f.second
+                             : child_row(o.parent, o.t) == std::vector<int64_t>(Cn, Cn + m);
+          }
+          if (dup) continue;  // same-level duplicate: first (minimum) tag wins
+          level_keys.emplace(f.first, (int64_t)fresh.size());
+          fresh.push_back(Cand{i, t, f});
+        }
+      }
+      c0 = c1;
+    }
+    const int64_t n_new = (int64_t)fresh.size();
+    const bool thin = frontier_target > 0 && n_new > frontier_target;
+    const uint64_t tau = thin ? oracle_thinning_tau(frontier_target, n_new) : 0;
+    std::vector<int64_t> keep;
+    for (int64_t ci = 0; ci < n_new; ++ci)
+      if (!thin || fmix64(fresh[ci].f.first) < tau) keep.push_back(ci);  // reading A19
+    // kept rows recomputed in parallel, then stored in tag order
+    std::vector<int64_t> krows;
+    std::vector<char> bad(keep.size(), 0);
+    const size_t KB = (size_t)1 << 16;
+    for (size_t k0 = 0; k0 < keep.size(); k0 += KB) {
+      const size_t k1 = std::min(keep.size(), k0 + KB);
+      krows.assign((k1 - k0) * (size_t)m, 0);
+      parallel_for((int64_t)k0, (int64_t)k1, n_threads, [&](int64_t k) {
+        const Cand& c = fresh[keep[k]];
+        auto Cn = child_row(c.parent, c.t);
+        for (int64_t v : Cn) bad[k] |= (v < 0 ? 1 : v > cmax ? 2 : 0);
+        std::copy(Cn.begin(), Cn.end(), krows.begin() + (size_t)(k - k0) * m);
+      });
+      for (size_t k = k0; k < k1; ++k) {
+        if (bad[k]) { run.status = OR_E_OVERFLOW; run.error = (bad[k] & 1) ? "negative count" : "count above storage range"; return run.status; }
+        const Cand& c = fresh[keep[k]];
+        std::vector<int64_t> Cn(krows.begin() + (k - k0) * m, krows.begin() + (k - k0 + 1) * m);
+        push(Cn, c.f, c.parent, c.t);
+      }
+    }
+    run.level_T.push_back(T);
+    run.level_new.push_back(n_new);
+    run.level_kept.push_back((int64_t)keep.size());
+    run.level_offsets.push_back((int64_t)run.parent.size());
+    if (keep.empty()) break;
+  }
+  // halting classification of every configuration (reading A5)
+  const int64_t N = (int64_t)run.parent.size();
+  run.halting.assign(N, 0);
+  parallel_for(0, N, n_threads, [&](int64_t i) {
+    auto A = applicable_rules_per_neuron(s, row_of(i));
+    bool any = false;
+    for (const auto& As : A) any = any || !As.empty();
+    run.halting[i] = any ? 0 : 1;
+  });
+  return OR_OK;
+}
+
+void oracle_prun_free(oracle_prun* h) { delete h; }
+int oracle_prun_status(const oracle_prun* h) { return h->r.status; }
+const char* oracle_prun_error(const oracle_prun* h) { return h->r.error.c_str(); }
+int64_t oracle_prun_num_configs(const oracle_prun* h) { return (int64_t)h->r.parent.size(); }
+int64_t oracle_prun_num_levels(const oracle_prun* h) { return (int64_t)h->r.level_offsets.size() - 1; }
+int64_t oracle_prun_num_expanded(const oracle_prun* h) { return (int64_t)h->r.level_T.size(); }
+void oracle_prun_level_offsets(const oracle_prun* h, int64_t* out) {
+  std::copy(h->r.level_offsets.begin(), h->r.level_offsets.end(), out);
+}
+void oracle_prun_tree(const oracle_prun* h, int64_t* parent, uint64_t* t, uint8_t* halting, uint64_t* fp2) {
+  const ParRun& r = h->r;
+  for (size_t i = 0; i < r.parent.size(); ++i) {
+    parent[i] = r.parent[i];
+    t[i] = r.t[i];
+    halting[i] = i < r.halting.size() ? r.halting[i] : 0;  // classified only when the run completes
+    fp2[2 * i] = r.fp0[i];
+    fp2[2 * i + 1] = r.fp1[i];
+  }
+}
+void oracle_prun_counters(const oracle_prun* h, int64_t* T, int64_t* n_new, int64_t* kept) {
+  const ParRun& r = h->r;
+  for (size_t i = 0; i < r.level_T.size(); ++i) {
+    T[i] = r.level_T[i];
+    n_new[i] = r.level_new[i];
+    kept[i] = r.level_kept[i];
+  }
+}
+// rows idx[0..n) (global discovery indices) as int32
+void oracle_prun_rows(const oracle_prun* h, const int64_t* idx, int64_t n, int32_t* out) {
+  const ParRun& r = h->r;
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t j = 0; j < r.m; ++j) out[k * r.m + j] = (int32_t)r.at(idx[k], j);
+}
 
 }  // extern "C"

@@ -21,6 +21,7 @@
 
 namespace snp {
 
+constexpr int64_t TC_M_MAX = 1 << 19;        // k_expand_tc: s32 accumulators exact up to this m
 constexpr int KMAX = 64;                    // nondeterministic neurons recorded per parent
 constexpr int PB = 64;                      // configurations per storage block
 constexpr uint64_t PSI_LIMIT = 1ULL << 62;  // Ψ above this is SNP_E_CAPACITY

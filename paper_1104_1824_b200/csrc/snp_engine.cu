@@ -170,12 +170,20 @@ struct Level {
   DBuf data;  // blocked counts, ceil(F/64) × m × 64 (may be released when not retained)
   int64_t F = 0;
   DView fp0, fp1, parent, t, halting;
+  // keep_all_edges (reading A17): every transition of the expansion that
+  // produced this level — the visited ref it reached (EMPTY = not stored),
+  // in tag order, and the parents' child offsets (F_parent + 1) to recover
+  // (parent, t) of each edge
+  DBuf all_ref, all_off;
+  int64_t all_T = 0, all_F = 0;
   bool has_data() const { return data.p != nullptr; }
 };
 
 }  // namespace
 
 struct snp_system {
+  // ---- lifetime: the caller's reference + one per snp_tree taken from it
+  int refs = 1;
   // ---- host copy of the system
   int64_t m = 0, n = 0;
   snp_options opt{};
@@ -208,6 +216,7 @@ struct snp_system {
   DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab, d_elut, d_hsg, d_xyt, d_xyf, d_btile, d_ndl, d_delay;
   DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
   DBuf counters_dev;  // [0] err, [1..] u64 counters
+  DBuf edge_scratch;  // snp_level_edges: fp0/fp1 interleave
   DBuf gen;           // generated-number bitmap (out_rule1 > 0)
   std::vector<DBuf> spare;  // released level buffers kept for reuse
   Arena arena;              // per-level metadata
@@ -238,7 +247,7 @@ struct snp_system {
 };
 
 struct snp_tree {
-  snp_system* sys = nullptr;
+  snp_system* sys = nullptr;  // holds a reference (snp_system_free defers until the last tree is freed)
   uint64_t generation = 0;
   int64_t m = 0, n = 0;
   std::vector<int64_t> level_offsets;
@@ -742,7 +751,9 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   // h_ℓ[r] = −c_r·R_ℓ[s] + p_r·Rout_ℓ[s] (reading A18) with c <= 15, p <= 1.
   v.tc_ok = 0;
   v.n_nd = 0;
-  if (s->bytes == 1 && !v.any_generic && s->binary_emit) {
+  // the s32 TMEM accumulators of k_expand_tc hold at most m·15·255 (X part)
+  // and m·16·255 (Y' part): exact below 2^31 for m <= TC_M_MAX = 2^19
+  if (s->bytes == 1 && !v.any_generic && s->binary_emit && m <= TC_M_MAX) {
     std::vector<uint8_t> tf((size_t)m * 256);
     CUDA_TRY(cudaMemcpy(tf.data(), s->d_tab_full.p, tf.size(), cudaMemcpyDeviceToHost));
     bool ok = true;
@@ -863,7 +874,11 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
     // buffers, the copy of chunk i + 1 (side stream) overlaps the import of
     // chunk i, and no level-sized staging allocation is needed
     const size_t row_b = (size_t)ld * level0->elem_bytes;
-    int64_t R = std::max<int64_t>(PB, (int64_t)(((size_t)256 << 20) / row_b) & ~(int64_t)(PB - 1));
+    // chunk bytes: 256 MB (SNP_UPLOAD_CHUNK_BYTES overrides, tests use it to
+    // run the multi-chunk path on small inputs); a multiple of 64 rows
+    size_t chunk_b = (size_t)256 << 20;
+    if (const char* e = getenv("SNP_UPLOAD_CHUNK_BYTES")) chunk_b = std::max<size_t>(1, strtoull(e, nullptr, 10));
+    int64_t R = std::max<int64_t>(PB, (int64_t)(chunk_b / row_b) & ~(int64_t)(PB - 1));
     if (R > F0) R = F0;
     DBuf stg[2];
     for (auto& b : stg) SNP_TRY(b.ensure((size_t)((R - 1) * ld + m) * level0->elem_bytes, false));
@@ -997,6 +1012,8 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     return SNP_OK;
   }
   if (!cur->has_data()) return fail(SNP_E_STATE, "current level has no data");
+  // the parent level of `cur` was kept for snp_level_spiking_vectors until now
+  if (!retain_levels(s) && s->levels.size() >= 2) release_level_data(s, s->levels[s->levels.size() - 2].get());
   // the caller may have released its level-0 input since snp_begin
   if (!s->horizon_reserved) SNP_TRY(reserve_horizon(s, std::max<int64_t>(F, s->opt.frontier_target)));
   cudaStream_t st = s->stream;
@@ -1108,6 +1125,14 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     phase_begin(s, 2);
     launch_compact(C, off, T, N, tb, (uint64_t)s->levels.size() << 40, 1, err, st);
     phase_end(s);
+    if (s->opt.keep_all_edges) {  // reading A17: every transition with the configuration it reached
+      SNP_TRY(next->all_ref.ensure(T * 8, false));
+      SNP_TRY(next->all_off.ensure((size_t)(F + 1) * 8, false));
+      launch_all_edges(C, T, tag_base, tb, (uint64_t)s->levels.size() << 40, next->all_ref.as<uint64_t>(), st);
+      CUDA_TRY(cudaMemcpyAsync(next->all_off.p, off, (size_t)(F + 1) * 8, cudaMemcpyDeviceToDevice, st));
+      next->all_T = (int64_t)T;
+      next->all_F = F;
+    }
     if (K > 0) {
       SNP_TRY(take_buffer(s, level_bytes(K, m, s->bytes), &next->data));
       g_trace.mark("take_buffer");
@@ -1125,6 +1150,7 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
       CUDA_TRY(cudaGetLastError());
       SNP_TRY(read_counters(s, &hc));
       if (hc.n_ovf > ovf_cap) return fail(SNP_E_CAPACITY, "too many counts at the storage limit (%llu)", hc.n_ovf);
+      lc.overflow_fixes = (int64_t)hc.n_ovf;
       if (hc.n_ovf) {
         phase_begin(s, 3);
         launch_overflow_fix(s->view, s->bytes, LV, O, s->kq_off.as<uint64_t>(), N, s->ovf.as<uint64_t>(), hc.n_ovf,
@@ -1158,7 +1184,6 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
   s->n_visited += K;
   s->total_T += (int64_t)T;
   s->counters.push_back(lc);
-  if (!retain_levels(s)) release_level_data(s, cur);
   s->levels.push_back(std::move(next));
   s->halting_current_valid = false;
   if (out) *out = lc;
@@ -1175,6 +1200,7 @@ snp_status snapshot(snp_system* s, snp_tree** out) {
   }
   auto t = std::make_unique<snp_tree>();
   t->sys = s;
+  s->refs++;
   t->generation = s->generation;
   t->m = s->m;
   t->n = s->n;
@@ -1241,6 +1267,7 @@ snp_status load_full(const snp_matrix* M, const snp_rule* rules, int64_t n_rules
   if (opt) o = *opt;
   if (o.count_bits != 8 && o.count_bits != 16 && o.count_bits != 32) return fail(SNP_E_ARG, "count_bits must be 8, 16 or 32");
   if (o.dedup != 0 && o.dedup != 1) return fail(SNP_E_ARG, "dedup must be 0 or 1");
+  if (o.keep_all_edges != 0 && o.keep_all_edges != 1) return fail(SNP_E_ARG, "keep_all_edges must be 0 or 1");
   if (o.frontier_target < 0 || o.max_transitions < 0) return fail(SNP_E_ARG, "negative frontier_target / max_transitions");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -1342,8 +1369,10 @@ snp_status snp_load_delay(const snp_matrix* M, const snp_rule* rules, int64_t n_
   return load_full(M, rules, n_rules, nullptr, delays ? delays : &none, C0, m, opt, out);
 }
 
-void snp_system_free(snp_system* s) {
-  if (!s) return;
+}  // extern "C"
+
+namespace {
+void system_destroy(snp_system* s) {
   if (s->stream) cudaStreamSynchronize(s->stream);
   s->levels.clear();
   s->spare.clear();
@@ -1352,6 +1381,16 @@ void snp_system_free(snp_system* s) {
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   delete s;
+}
+void system_unref(snp_system* s) {
+  if (--s->refs == 0) system_destroy(s);
+}
+}  // namespace
+
+extern "C" {
+
+void snp_system_free(snp_system* s) {
+  if (s) system_unref(s);
 }
 
 snp_status snp_set_stream(snp_system* s, void* stream) {
@@ -1450,10 +1489,16 @@ snp_status snp_level_edges(snp_system* s, int32_t level, int64_t* parent, uint64
   if (!F) return SNP_OK;
   if (parent) CUDA_TRY(cudaMemcpyAsync(parent, L->parent.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
   if (t) CUDA_TRY(cudaMemcpyAsync(t, L->t.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
-  if (halting) CUDA_TRY(cudaMemcpyAsync(halting, L->halting.p, F, cudaMemcpyDeviceToHost, s->stream));
-  DBuf pair;  // fp0 / fp1 interleaved on the device, then one contiguous copy
-  if (fp2) {
-    SNP_TRY(pair.ensure((size_t)F * 16, false));
+  if (halting) {
+    // the newest level is classified only once it is expanded (or by
+    // snp_explore's snapshot): its flags are not known yet
+    if (level == (int32_t)s->levels.size() - 1 && !s->halting_current_valid)
+      return fail(SNP_E_STATE, "snp_level_edges: halting flags of level %d are not computed yet (pass halting = NULL)", level);
+    CUDA_TRY(cudaMemcpyAsync(halting, L->halting.p, F, cudaMemcpyDeviceToHost, s->stream));
+  }
+  if (fp2) {  // fp0 / fp1 interleaved on the device (persistent scratch), then one contiguous copy
+    SNP_TRY(s->edge_scratch.ensure((size_t)F * 16));
+    DBuf& pair = s->edge_scratch;
     CUDA_TRY(cudaMemcpy2DAsync(pair.p, 16, L->fp0.p, 8, 8, F, cudaMemcpyDeviceToDevice, s->stream));
     CUDA_TRY(cudaMemcpy2DAsync(pair.as<uint8_t>() + 8, 16, L->fp1.p, 8, 8, F, cudaMemcpyDeviceToDevice, s->stream));
     CUDA_TRY(cudaMemcpyAsync(fp2, pair.p, (size_t)F * 16, cudaMemcpyDeviceToHost, s->stream));
@@ -1609,13 +1654,136 @@ snp_status snp_tree_spiking_vectors(const snp_tree* t, int32_t level, uint8_t* S
   DBuf tmp;
   SNP_TRY(tmp.ensure((size_t)lv->F * s->n));
   launch_spiking_vectors(s->view, s->bytes, par->data.p, lv->parent.as<int64_t>(), lv->t.as<uint64_t>(),
-                         lv->F, tmp.as<uint8_t>(), s->stream);
+                         lv->F, tmp.as<uint8_t>(), nullptr, s->stream);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(S_out, tmp.p, (size_t)lv->F * s->n, cudaMemcpyDeviceToHost, s->stream));
   return sync(s);
 }
 
-void snp_tree_free(snp_tree* t) { delete t; }
+void snp_tree_free(snp_tree* t) {
+  if (!t) return;
+  snp_system* s = t->sys;
+  delete t;
+  if (s) system_unref(s);
+}
+
+snp_status snp_level_spiking_vectors(snp_system* s, int32_t level, const int64_t* idx, int64_t n, uint8_t* S_out) {
+  if (!s || level < 1 || level >= (int32_t)s->levels.size() || n < 0 || (n > 0 && (!idx || !S_out)))
+    return fail(SNP_E_ARG, "snp_level_spiking_vectors: bad arguments");
+  if (s->view.delay_m > 0) return fail(SNP_E_STATE, "spiking vectors of systems with delays are not available");
+  const Level* par = s->levels[level - 1].get();
+  const Level* lv = s->levels[level].get();
+  if (!par->has_data()) return fail(SNP_E_STATE, "level %d counts are not retained (keep_tree = 0: only the newest level's parents)", level - 1);
+  if (n == 0) return SNP_OK;
+  std::vector<int64_t> hp(n);
+  std::vector<uint64_t> ht(n), hi(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (idx[i] < 0 || idx[i] >= lv->F) return fail(SNP_E_ARG, "snp_level_spiking_vectors: index out of range");
+    hi[i] = (uint64_t)idx[i];
+  }
+  DBuf didx, dpar, dt, out;
+  SNP_TRY(didx.ensure(n * 8, false));
+  SNP_TRY(dpar.ensure(n * 8, false));
+  SNP_TRY(dt.ensure(n * 8, false));
+  SNP_TRY(out.ensure((size_t)n * s->n + 16, false));
+  CUDA_TRY(cudaMemcpyAsync(didx.p, hi.data(), n * 8, cudaMemcpyHostToDevice, s->stream));
+  // (parent, t) of the requested configurations, gathered on the host side of
+  // two small copies (the level's edge arrays stay on the device)
+  std::vector<int64_t> allp(lv->F);
+  std::vector<uint64_t> allt(lv->F);
+  CUDA_TRY(cudaMemcpyAsync(allp.data(), lv->parent.p, lv->F * 8, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(allt.data(), lv->t.p, lv->F * 8, cudaMemcpyDeviceToHost, s->stream));
+  SNP_TRY(sync(s));
+  for (int64_t i = 0; i < n; ++i) {
+    hp[i] = allp[hi[i]];
+    ht[i] = allt[hi[i]];
+  }
+  CUDA_TRY(cudaMemcpyAsync(dpar.p, hp.data(), n * 8, cudaMemcpyHostToDevice, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(dt.p, ht.data(), n * 8, cudaMemcpyHostToDevice, s->stream));
+  launch_spiking_vectors(s->view, s->bytes, par->data.p, dpar.as<int64_t>(), dt.as<uint64_t>(), n, out.as<uint8_t>(),
+                         nullptr, s->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(S_out, out.p, (size_t)n * s->n, cudaMemcpyDeviceToHost, s->stream));
+  return sync(s);
+}
+
+snp_status snp_spiking_vector(snp_system* s, const int32_t* C, uint64_t t, uint8_t* S_out) {
+  if (!s || !C || !S_out) return fail(SNP_E_ARG, "snp_spiking_vector: bad arguments");
+  if (s->view.delay_m > 0) return fail(SNP_E_STATE, "spiking vectors of systems with delays are not available");
+  const int64_t m = s->m;
+  for (int64_t j = 0; j < m; ++j)
+    if (C[j] < 0 || C[j] > s->count_max) return fail(SNP_E_ARG, "snp_spiking_vector: count %d at neuron %lld outside [0, %lld]", C[j], (long long)j, (long long)s->count_max);
+  DBuf row, blk, dpar, dt, out, derr;
+  SNP_TRY(row.ensure((size_t)m * 4, false));
+  SNP_TRY(blk.ensure(level_bytes(1, m, s->bytes), false));
+  SNP_TRY(dpar.ensure(8, false));
+  SNP_TRY(dt.ensure(8, false));
+  SNP_TRY(out.ensure((size_t)s->n + 16, false));
+  SNP_TRY(derr.ensure(4, false));
+  const int64_t zero = 0;
+  CUDA_TRY(cudaMemcpyAsync(row.p, C, (size_t)m * 4, cudaMemcpyHostToDevice, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(dpar.p, &zero, 8, cudaMemcpyHostToDevice, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(dt.p, &t, 8, cudaMemcpyHostToDevice, s->stream));
+  CUDA_TRY(cudaMemsetAsync(derr.p, 0, 4, s->stream));
+  launch_import(row.p, 4, SNP_LAYOUT_ROW_MAJOR, m, 1, (int32_t)m, blk.p, s->bytes, s->count_max, derr.as<int32_t>(),
+                s->stream);
+  launch_spiking_vectors(s->view, s->bytes, blk.p, dpar.as<int64_t>(), dt.as<uint64_t>(), 1, out.as<uint8_t>(),
+                         derr.as<int32_t>(), s->stream);
+  CUDA_TRY(cudaGetLastError());
+  int32_t err = 0;
+  CUDA_TRY(cudaMemcpyAsync(&err, derr.p, 4, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(S_out, out.p, (size_t)s->n, cudaMemcpyDeviceToHost, s->stream));
+  SNP_TRY(sync(s));
+  if (err & ERR_CAPACITY) return fail(SNP_E_ARG, "snp_spiking_vector: t = %llu >= Ψ(C)", (unsigned long long)t);
+  return SNP_OK;
+}
+
+snp_status snp_frontier_copy(snp_system* s, int32_t* configs, int64_t* parent, uint64_t* t, int64_t cap,
+                             int64_t* n_out) {
+  if (!s || s->levels.empty()) return fail(SNP_E_ARG, "snp_frontier_copy: no exploration");
+  const int32_t L = (int32_t)s->levels.size() - 1;
+  const int64_t F = s->levels[L]->F;
+  if (n_out) *n_out = F;
+  if (F > cap) return fail(SNP_E_CAPACITY, "snp_frontier_copy: frontier has %lld configurations > cap %lld", (long long)F, (long long)cap);
+  if (parent || t) SNP_TRY(snp_level_edges(s, L, parent, t, nullptr, nullptr));
+  if (configs && F) {
+    std::vector<int64_t> idx(F);
+    for (int64_t i = 0; i < F; ++i) idx[i] = i;
+    SNP_TRY(snp_level_columns(s, L, idx.data(), F, configs));
+  }
+  return SNP_OK;
+}
+
+snp_status snp_level_all_edges(snp_system* s, int32_t level, int64_t* parent, uint64_t* t, int64_t* ref, int64_t cap,
+                               int64_t* n_edges) {
+  if (!s || level < 1 || level >= (int32_t)s->levels.size()) return fail(SNP_E_ARG, "snp_level_all_edges: bad level");
+  if (!s->opt.keep_all_edges) return fail(SNP_E_STATE, "snp_level_all_edges needs options.keep_all_edges = 1");
+  const Level* lv = s->levels[level].get();
+  if (!lv->all_ref.p && lv->all_T) return fail(SNP_E_STATE, "edges of level %d were not recorded", level);
+  const int64_t T = lv->all_T;
+  if (n_edges) *n_edges = T;
+  if (T > cap) return fail(SNP_E_CAPACITY, "snp_level_all_edges: %lld edges > cap %lld", (long long)T, (long long)cap);
+  if (!T) return SNP_OK;
+  std::vector<uint64_t> raw(T), off(lv->all_F + 1);
+  CUDA_TRY(cudaMemcpyAsync(raw.data(), lv->all_ref.p, T * 8, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(off.data(), lv->all_off.p, (lv->all_F + 1) * 8, cudaMemcpyDeviceToHost, s->stream));
+  SNP_TRY(sync(s));
+  std::vector<int64_t> base(s->levels.size() + 1, 0);
+  for (size_t i = 0; i < s->levels.size(); ++i) base[i + 1] = base[i] + s->levels[i]->F;
+  for (int64_t p = 0, e = 0; p < lv->all_F; ++p)
+    for (uint64_t c = off[p]; c < off[p + 1]; ++c, ++e) {
+      if (parent) parent[e] = p;
+      if (t) t[e] = c - off[p];
+    }
+  if (ref)
+    for (int64_t e = 0; e < T; ++e) {
+      const uint64_t r = raw[e];
+      if (r == ~0ULL) { ref[e] = -1; continue; }
+      const uint64_t L2 = r >> 40, q = r & ((1ULL << 40) - 1);
+      ref[e] = L2 < s->levels.size() ? base[L2] + (int64_t)q : -1;
+    }
+  return SNP_OK;
+}
 
 }  // extern "C"
 
@@ -1652,6 +1820,7 @@ extern "C" {
 snp_status snp_dist_begin(snp_system* s, const snp_configs* level0, int32_t nranks, int64_t* n_local) {
   if (!s || !level0 || nranks < 1) return fail(SNP_E_ARG, "snp_dist_begin: bad arguments");
   if (s->opt.dedup != 1) return fail(SNP_E_STATE, "distributed exploration needs dedup = 1 (fingerprint keys)");
+  if (s->opt.keep_all_edges) return fail(SNP_E_STATE, "keep_all_edges is not available in distributed exploration");
   if (s->view.aug_rule >= 0) return fail(SNP_E_STATE, "distributed exploration does not support generated numbers");
   if (s->view.delay_m > 0) return fail(SNP_E_STATE, "distributed exploration does not support delays");
   const int64_t F0 = level0->n_configs, m = s->m;

@@ -129,7 +129,10 @@ void launch_owner_keep(const uint64_t* recv, uint64_t R, const Tables& tb, const
                        int32_t* err, cudaStream_t st);
 void launch_unperm(const uint64_t* perm, const uint8_t* back, uint64_t T, uint64_t* kept, cudaStream_t st);
 void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_data, const int64_t* parent,
-                            const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st);
+                            const uint64_t* t, int64_t K, uint8_t* S_out, int32_t* err, cudaStream_t st);
+// keep_all_edges: the visited ref every transition reached (EMPTY = not stored)
+void launch_all_edges(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, uint64_t next_ref,
+                      uint64_t* ref, cudaStream_t st);
 
 // systems with delays: child keys of materialised children
 void launch_child_keys_delay(const SysView& S, int32_t bytes, const LevelView& L, const uint64_t* off,

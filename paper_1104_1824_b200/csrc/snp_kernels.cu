@@ -1333,6 +1333,23 @@ __device__ void visited_insert(const Tables& tb, uint64_t k0, uint64_t k1, uint6
   atomicOr(err, ERR_TABLE_FULL);
 }
 
+// keep_all_edges (reading A17): the configuration every transition reached,
+// as a visited ref (level << 40 | index), or EMPTY when it was not stored
+// (thinned, or a terminal transition of generated numbers).  A child seen at
+// an earlier level carries the visited ref k_dedup found; a new one points at
+// its key's winner (minimum tag) in the next level when that was kept.
+__global__ void k_all_edges(ChildArrays C, uint64_t T, uint64_t tag_base, Tables tb, uint64_t next_ref,
+                            uint64_t* ref) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T; c += (uint64_t)gridDim.x * blockDim.x) {
+    if (C.verdict[c] == 0) {
+      ref[c] = C.cref[c];
+    } else {
+      const uint64_t w = tb.ltab[C.cslot[c]].tag - tag_base;
+      ref[c] = C.kept[w] ? (next_ref | C.kpos[w]) : EMPTY;
+    }
+  }
+}
+
 __global__ void k_compact(ChildArrays C, const uint64_t* off, uint64_t T, NextArrays N, Tables tb,
                           uint64_t level_ref, int insert_visited, int32_t* err) {
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T; c += (uint64_t)gridDim.x * blockDim.x) {
@@ -2309,7 +2326,7 @@ __global__ void k_digest(NextArrays N, int64_t K, uint64_t level, int64_t q_offs
 // The spiking vector that produced each child (Alg. 2 II-2/II-3 decode).
 template <typename T>
 __global__ void k_spiking_vectors(SysView S, const T* pdata, const int64_t* parent, const uint64_t* tt, int64_t K,
-                                  uint8_t* S_out) {
+                                  uint8_t* S_out, int32_t* err) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < K; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = parent[q];
     uint64_t t = tt[q];
@@ -2323,6 +2340,7 @@ __global__ void k_spiking_vectors(SysView S, const T* pdata, const int64_t* pare
       t /= (uint64_t)d;
       Sq[nth_applicable(S, s, v, x)] = 1;
     }
+    if (t && err) atomicOr(err, ERR_CAPACITY);  // t >= Ψ: no such spiking vector
   }
 }
 
@@ -3231,13 +3249,20 @@ void launch_unperm(const uint64_t* perm, const uint8_t* back, uint64_t T, uint64
 }
 
 void launch_spiking_vectors(const SysView& S, int32_t bytes, const void* parent_data, const int64_t* parent,
-                            const uint64_t* t, int64_t K, uint8_t* S_out, cudaStream_t st) {
+                            const uint64_t* t, int64_t K, uint8_t* S_out, int32_t* err, cudaStream_t st) {
   if (K <= 0) return;
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
     k_spiking_vectors<T><<<grid_for(K, 128), 128, 0, st>>>(S, reinterpret_cast<const T*>(parent_data), parent, t, K,
-                                                         S_out);
+                                                         S_out, err);
   });
+  count_launch();
+}
+
+void launch_all_edges(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, uint64_t next_ref,
+                      uint64_t* ref, cudaStream_t st) {
+  if (T == 0) return;
+  k_all_edges<<<grid_for((int64_t)T, BLK), BLK, 0, st>>>(C, T, tag_base, tb, next_ref, ref);
   count_launch();
 }
 

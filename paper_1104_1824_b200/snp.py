@@ -41,6 +41,7 @@ EXPORTED = [
     "snp_level_size", "snp_level_edges", "snp_level_columns", "snp_set_profiling", "snp_profile",
     "snp_kernel_launches", "snp_kernel_paths", "snp_host_alloc", "snp_host_free", "snp_dist_begin", "snp_dist_expand", "snp_dist_pack", "snp_dist_owner_dedup",
     "snp_dist_owner_keep", "snp_dist_finalize", "snp_dist_commit",
+    "snp_spiking_vector", "snp_level_spiking_vectors", "snp_frontier_copy", "snp_level_all_edges",
 ]
 SNP_NUM_PHASES = 5
 SNP_PATH_TC_EXPAND = 1
@@ -60,7 +61,8 @@ class snp_matrix(ctypes.Structure):
 class snp_options(ctypes.Structure):
     _fields_ = [("count_bits", ctypes.c_int32), ("dedup", ctypes.c_int32), ("frontier_target", ctypes.c_int64),
                 ("max_transitions", ctypes.c_int64), ("fp_seed", ctypes.c_uint64 * 2),
-                ("keep_tree", ctypes.c_int32), ("out_rule1", ctypes.c_int32)]
+                ("keep_tree", ctypes.c_int32), ("out_rule1", ctypes.c_int32), ("keep_all_edges", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class snp_configs(ctypes.Structure):
@@ -72,7 +74,7 @@ class snp_configs(ctypes.Structure):
 class snp_level_counters(ctypes.Structure):
     _fields_ = [("parents", ctypes.c_int64), ("halting", ctypes.c_int64), ("T", ctypes.c_int64),
                 ("n_new", ctypes.c_int64), ("kept", ctypes.c_int64), ("tau", ctypes.c_uint64),
-                ("ms", ctypes.c_double)]
+                ("ms", ctypes.c_double), ("overflow_fixes", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -152,6 +154,10 @@ def lib() -> ctypes.CDLL:
         L.snp_dist_owner_keep.argtypes = [_P, ctypes.c_int64, _P]
         L.snp_dist_finalize.argtypes = [_P, _P, _I64P]
         L.snp_dist_commit.argtypes = [_P, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(snp_level_counters)]
+        L.snp_spiking_vector.argtypes = [_P, _P, ctypes.c_uint64, _P]
+        L.snp_level_spiking_vectors.argtypes = [_P, ctypes.c_int32, _P, ctypes.c_int64, _P]
+        L.snp_frontier_copy.argtypes = [_P, _P, _P, _P, ctypes.c_int64, _I64P]
+        L.snp_level_all_edges.argtypes = [_P, ctypes.c_int32, _P, _P, _P, ctypes.c_int64, _I64P]
         for f in EXPORTED:
             if f not in ("snp_kernel_launches", "snp_kernel_paths", "snp_system_free", "snp_tree_free", "snp_frontier_size", "snp_depth", "snp_level_size",
                          "snp_tree_num_levels", "snp_tree_num_configs", "snp_abi_version", "snp_last_error"):
@@ -163,6 +169,11 @@ def lib() -> ctypes.CDLL:
 def _check(st: int):
     if st != SNP_OK:
         raise SnpError(st, lib().snp_last_error().decode(errors="replace"))
+
+
+def _check_allow(st: int, *ok):
+    if st != SNP_OK and st not in ok:
+        _check(st)
 
 
 def _ptr(a: np.ndarray):
@@ -178,9 +189,13 @@ class PinnedHost:
         self.p, self.nbytes = p, nbytes
 
     def array(self, offset: int, shape, dtype) -> np.ndarray:
+        """A numpy view of bytes [offset, offset + size); the view keeps this
+        PinnedHost alive (its base chain holds it), so the pinned block is
+        freed only after the last view is gone."""
         n = int(np.prod(shape)) * np.dtype(dtype).itemsize
         assert offset + n <= self.nbytes
         buf = (ctypes.c_uint8 * n).from_address(self.p.value + offset)
+        buf._owner = self
         return np.frombuffer(buf, dtype=dtype).reshape(shape)
 
     def __del__(self):
@@ -208,7 +223,7 @@ class PinnedEdges:
 # ---- C-named entry points (marshalling only) --------------------------------
 def snp_load(rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.ndarray, C0: np.ndarray,
              count_bits=32, dedup=0, frontier_target=0, max_transitions=0, fp_seed=(0x5EED0, 0x5EED1),
-             keep_tree=1, out_rule=None, re_bits=None, delays=None):
+             keep_tree=1, out_rule=None, re_bits=None, delays=None, keep_all_edges=0):
     rules = np.ascontiguousarray(rules, np.int32).reshape(-1, 6)
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col = np.ascontiguousarray(col, np.int32)
@@ -216,7 +231,7 @@ def snp_load(rules: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, val: np.nd
     C0 = np.ascontiguousarray(C0, np.int32)
     M = snp_matrix(rules.shape[0], C0.shape[0], None, _ptr(row_ptr).value, _ptr(col).value, _ptr(val).value)
     o = snp_options(count_bits, dedup, frontier_target, max_transitions, (ctypes.c_uint64 * 2)(*fp_seed),
-                    keep_tree, 0 if out_rule is None else int(out_rule) + 1)
+                    keep_tree, 0 if out_rule is None else int(out_rule) + 1, int(keep_all_edges), 0)
     h = _P()
     if delays is not None:
         d = np.ascontiguousarray(delays, np.int32)
@@ -251,7 +266,7 @@ class System:
     """Owning wrapper of an ``snp_system*``."""
 
     def __init__(self, workload, count_bits=32, dedup=0, frontier_target=0, max_transitions=0,
-                 fp_seed=(0x5EED0, 0x5EED1), keep_tree=1, out_rule=None, delays=None):
+                 fp_seed=(0x5EED0, 0x5EED1), keep_tree=1, out_rule=None, delays=None, keep_all_edges=0):
         """out_rule: generated numbers (include/snp.h) with that output rule;
         configurations then have ``width = m + 1`` entries (last = A).
         delays: one d >= 0 per rule (snp_load_delay, SURVEY §8(f) NEXT-3);
@@ -262,7 +277,7 @@ class System:
         self._h = None
         self._h = snp_load(workload.rules, workload.row_ptr, workload.col, workload.val, workload.C0,
                            count_bits, dedup, frontier_target, max_transitions, fp_seed, keep_tree, out_rule,
-                           getattr(workload, "re_bits", None), delays)
+                           getattr(workload, "re_bits", None), delays, keep_all_edges)
         self.width = int(lib().snp_state_width(self._h))
 
     def generated_numbers(self) -> set:
@@ -362,23 +377,61 @@ class System:
         if pb is None or pb.cap < cap:
             self._pinned_edges = PinnedEdges(max(cap, 1))
 
-    def level_edges(self, L: int, pinned: bool = False):
+    def level_edges(self, L: int, pinned: bool = False, halting: bool = True):
         """snp_level_edges into new numpy arrays, or (pinned=True) into pinned
         host buffers owned by this System and reused by the next pinned call
-        (full PCIe rate; the returned arrays are views of them)."""
+        (full PCIe rate; the returned arrays are views of them, valid until the
+        next pinned call).  halting=False skips the flags (the newest level's
+        are known only once it is expanded or classified); None is returned."""
         F = self.level_size(L)
         if pinned:
             pb = getattr(self, "_pinned_edges", None)
             if pb is None or pb.cap < F:
                 pb = self._pinned_edges = PinnedEdges(max(F + F // 8, 1))  # headroom: thinned levels hover around F
-            parent, t, halting, fp = pb.views(F)
+            parent, t, hb, fp = pb.views(F)
         else:
             parent = np.empty(F, np.int64)
             t = np.empty(F, np.uint64)
-            halting = np.empty(F, np.uint8)
+            hb = np.empty(F, np.uint8)
             fp = np.empty((F, 2), np.uint64)
-        _check(lib().snp_level_edges(self._h, L, _ptr(parent), _ptr(t), _ptr(halting), _ptr(fp)))
-        return parent, t, halting, fp
+        _check(lib().snp_level_edges(self._h, L, _ptr(parent), _ptr(t), _ptr(hb) if halting else None, _ptr(fp)))
+        return parent, t, (hb if halting else None), fp
+
+    def spiking_vector(self, C, t: int) -> np.ndarray:
+        """snp_spiking_vector: the t-th valid spiking vector of configuration C."""
+        C = np.ascontiguousarray(C, np.int32).reshape(-1)
+        S = np.zeros(self.n, np.uint8)
+        _check(lib().snp_spiking_vector(self._h, _ptr(C), int(t), _ptr(S)))
+        return S
+
+    def level_spiking_vectors(self, L: int, idx) -> np.ndarray:
+        """snp_level_spiking_vectors: S that produced configurations idx of level L."""
+        idx = np.ascontiguousarray(idx, np.int64)
+        out = np.zeros((idx.shape[0], self.n), np.uint8)
+        _check(lib().snp_level_spiking_vectors(self._h, L, _ptr(idx), idx.shape[0], _ptr(out)))
+        return out
+
+    def frontier_copy(self):
+        """snp_frontier_copy: (configs F × width int32, parent, t) of the newest level."""
+        n = ctypes.c_int64()
+        _check_allow(lib().snp_frontier_copy(self._h, None, None, None, 0, ctypes.byref(n)), SNP_E_CAPACITY)
+        F = int(n.value)
+        C = np.zeros((F, self.width), np.int32)
+        parent = np.zeros(F, np.int64)
+        t = np.zeros(F, np.uint64)
+        _check(lib().snp_frontier_copy(self._h, _ptr(C), _ptr(parent), _ptr(t), F, ctypes.byref(n)))
+        return C, parent, t
+
+    def level_all_edges(self, L: int):
+        """snp_level_all_edges: (parent, t, ref) of every transition that produced level L."""
+        n = ctypes.c_int64()
+        _check_allow(lib().snp_level_all_edges(self._h, L, None, None, None, 0, ctypes.byref(n)), SNP_E_CAPACITY)
+        T = int(n.value)
+        parent = np.zeros(T, np.int64)
+        t = np.zeros(T, np.uint64)
+        ref = np.zeros(T, np.int64)
+        _check(lib().snp_level_all_edges(self._h, L, _ptr(parent), _ptr(t), _ptr(ref), T, ctypes.byref(n)))
+        return parent, t, ref
 
     def level_columns(self, L: int, idx) -> np.ndarray:
         idx = np.ascontiguousarray(idx, np.int64)
@@ -412,6 +465,7 @@ class Counters:
     halting: np.ndarray
     tau: np.ndarray
     ms: np.ndarray
+    overflow_fixes: np.ndarray
 
 
 class Tree:
@@ -435,7 +489,7 @@ class Tree:
         _check(L.snp_tree_counters(h, ctypes.cast(arr, ctypes.c_void_p)))
         rows = [arr[i].as_dict() for i in range(nl)]
         self.counters = Counters(*(np.array([r[k] for r in rows]) for k in ("T", "n_new", "kept", "halting", "tau",
-                                                                          "ms")))
+                                                                          "ms", "overflow_fixes")))
         self._configs = None
 
     @property

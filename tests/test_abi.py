@@ -52,7 +52,7 @@ def test_sm100a_code_present(built):
 
 def test_abi_version(built):
     lib = ctypes.CDLL(built.LIB_SNP)
-    assert lib.snp_abi_version() == 1
+    assert lib.snp_abi_version() == 2  # round 2: keep_all_edges, overflow_fixes fields
 
 
 @pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU failure mode")

@@ -103,6 +103,75 @@ def test_splitmix64_known_vector():
     assert f0 == 0xE220A8397B1DCDAF | 1
 
 
+_M64 = (1 << 64) - 1
+
+
+def _rotl64(x, r):
+    return ((x << r) | (x >> (64 - r))) & _M64
+
+
+def _murmur3_x64_128(key: bytes, seed: int, fmix) -> bytes:
+    """MurmurHash3_x64_128 (Austin Appleby, public domain), written out here
+    with the ORACLE's fmix64 as its finalizer: the oracle's thinning key and
+    owner hash (readings A19, §8(e)) are exactly MurmurHash3's fmix64, so a
+    wrong constant or shift in oracle.cpp:fmix64 breaks the published
+    verification value below."""
+    n = len(key)
+    h1 = h2 = seed
+    c1, c2 = 0x87C37B91114253D5, 0x4CF5AD432745937F
+    nb = n // 16
+    for i in range(nb):
+        k1 = int.from_bytes(key[16 * i:16 * i + 8], "little")
+        k2 = int.from_bytes(key[16 * i + 8:16 * i + 16], "little")
+        k1 = (_rotl64((k1 * c1) & _M64, 31) * c2) & _M64
+        h1 ^= k1
+        h1 = (((_rotl64(h1, 27) + h2) & _M64) * 5 + 0x52DCE729) & _M64
+        k2 = (_rotl64((k2 * c2) & _M64, 33) * c1) & _M64
+        h2 ^= k2
+        h2 = (((_rotl64(h2, 31) + h1) & _M64) * 5 + 0x38495AB5) & _M64
+    tail, r = key[16 * nb:], n & 15
+    k1 = k2 = 0
+    if r > 8:
+        for i in range(r - 1, 7, -1):
+            k2 ^= tail[i] << (8 * (i - 8))
+        h2 ^= (_rotl64((k2 * c2) & _M64, 33) * c1) & _M64
+    if r > 0:
+        for i in range(min(r, 8) - 1, -1, -1):
+            k1 ^= tail[i] << (8 * i)
+        h1 ^= (_rotl64((k1 * c1) & _M64, 31) * c2) & _M64
+    h1 ^= n
+    h2 ^= n
+    h1 = (h1 + h2) & _M64
+    h2 = (h2 + h1) & _M64
+    h1, h2 = fmix(h1), fmix(h2)
+    h1 = (h1 + h2) & _M64
+    h2 = (h2 + h1) & _M64
+    return h1.to_bytes(8, "little") + h2.to_bytes(8, "little")
+
+
+def test_fmix64_pinned_by_murmur3_verification_value():
+    """Pin of oracle fmix64 (oracle.cpp; thinning key A19, owner hash §8(e))
+    against published values, not against another copy of itself:
+      * SMHasher's VerificationTest for MurmurHash3_x64_128 (key i = bytes
+        0..i-1 hashed with seed 256 - i, i = 0..255; the 4096 hash bytes hashed
+        with seed 0; first 4 bytes little-endian) = 0x6384BA69 — the value
+        SMHasher's hash table lists for "Murmur3F";
+      * MurmurHash3_x64_128("The quick brown fox jumps over the lazy dog", 0)
+        = 6c1b07bc7bbc4be3 47939ac4a93c437a (the widely quoted test vector);
+      * fmix64(0) = 0 (every step maps 0 to 0)."""
+    fmix = lambda k: int(oracle.fmix64(k))
+    key = bytes(range(256))
+    hashes = b"".join(_murmur3_x64_128(key[:i], 256 - i, fmix) for i in range(256))
+    final = _murmur3_x64_128(hashes, 0, fmix)
+    assert int.from_bytes(final[:4], "little") == 0x6384BA69
+    assert _murmur3_x64_128(b"The quick brown fox jumps over the lazy dog", 0, fmix).hex() == \
+        "6c1b07bc7bbc4be347939ac4a93c437a"
+    assert fmix(0) == 0
+    # a typo in either multiplier or shift breaks the verification value
+    bad = lambda k: (fmix(k) ^ (k >> 40)) & _M64
+    assert int.from_bytes(_murmur3_x64_128(hashes, 0, bad)[:4], "little") != 0x6384BA69
+
+
 @pytest.mark.parametrize("seed", range(30))
 def test_fingerprint_linearity(seed):
     # H(C + S·M) = H(C) + Σ_{r∈S} H(M_r) mod 2^64 (reading A18)
