@@ -27,6 +27,7 @@
 #include <map>
 #include <thread>
 #include <unordered_map>
+#include <functional>
 #include <utility>
 #include <algorithm>
 
@@ -140,6 +141,10 @@ std::vector<uint8_t> spiking_vector(const System& sys, const std::vector<std::ve
   std::vector<uint8_t> S(sys.n, 0);
   for (int64_t s = sys.m - 1; s >= 0; --s) {  // least significant digit last
     if (A[s].empty()) continue;
+    if (A[s].size() == 1) {  // radix 1: the digit is 0 and t is unchanged (t mod 1 = 0, t / 1 = t)
+      S[A[s][0]] = 1;
+      continue;
+    }
     uint64_t d = A[s].size();
     uint64_t x = t % d;
     t /= d;
@@ -187,6 +192,26 @@ std::pair<uint64_t, uint64_t> fingerprint(const std::vector<int64_t>& C, uint64_
   }
   return {f0, f1};
 }
+
+// The same fingerprint with the weights R_ℓ[j] computed once per run instead
+// of once per (configuration, neuron) — for the large runs of oracle_explore_par.
+struct FpWeights {
+  std::vector<uint64_t> R0, R1;
+  FpWeights(int64_t m, uint64_t seed0, uint64_t seed1) : R0(m), R1(m) {
+    for (int64_t j = 0; j < m; ++j) {
+      R0[j] = splitmix64(seed0 ^ (uint64_t)j) | 1ULL;
+      R1[j] = splitmix64(seed1 ^ (uint64_t)j) | 1ULL;
+    }
+  }
+  std::pair<uint64_t, uint64_t> operator()(const std::vector<int64_t>& C) const {
+    uint64_t f0 = 0, f1 = 0;
+    for (size_t j = 0; j < C.size(); ++j) {
+      f0 += (uint64_t)C[j] * R0[j];
+      f1 += (uint64_t)C[j] * R1[j];
+    }
+    return {f0, f1};
+  }
+};
 
 // ---- validation (SURVEY §8(b) list; Def. 1 and Def. 2) --------------------
 std::string validate(const System& sys) {
@@ -890,6 +915,7 @@ int oracle_explore_par(const oracle_system* h, int64_t F0, const int32_t* level0
   run.m = m;
   run.w = count_bits / 8;
   if (n_threads < 1) n_threads = 1;
+  const FpWeights fingerprint_of(m, seed0, seed1);
   // visited: fp0 -> arena indices (dedup 0: rows compared; dedup 1: fp1 compared)
   std::unordered_multimap<uint64_t, int64_t> visited;
   auto row_equal = [&](int64_t i, const int64_t* C) {
@@ -897,11 +923,19 @@ int oracle_explore_par(const oracle_system* h, int64_t F0, const int32_t* level0
       if (run.at(i, j) != C[j]) return false;
     return true;
   };
-  auto seen = [&](const int64_t* C, const std::pair<uint64_t, uint64_t>& f) {
+  // row(): the configuration itself, materialised only when a dedup = 0
+  // comparison needs it (an fp0 match)
+  auto seen = [&](const std::pair<uint64_t, uint64_t>& f, const std::function<std::vector<int64_t>()>& row) {
     auto rg = visited.equal_range(f.first);
+    std::vector<int64_t> C;
     for (auto it = rg.first; it != rg.second; ++it) {
       const int64_t i = it->second;
-      if (dedup == 1 ? run.fp1[i] == f.second : row_equal(i, C)) return true;
+      if (dedup == 1) {
+        if (run.fp1[i] == f.second) return true;
+        continue;
+      }
+      if (C.empty()) C = row();
+      if (row_equal(i, C.data())) return true;
     }
     return false;
   };
@@ -925,8 +959,8 @@ int oracle_explore_par(const oracle_system* h, int64_t F0, const int32_t* level0
     std::vector<int64_t> C(level0 + i * m, level0 + (i + 1) * m);
     for (int64_t v : C)
       if (v < 0 || v > cmax) { run.status = OR_E_OVERFLOW; run.error = "level 0 count out of range"; return run.status; }
-    auto f = fingerprint(C, seed0, seed1);
-    if (seen(C.data(), f)) continue;
+    auto f = fingerprint_of(C);
+    if (seen(f, [&]() { return C; })) continue;
     push(C, f, -1, 0);
   }
   run.level_offsets.push_back((int64_t)run.parent.size());
@@ -953,23 +987,20 @@ int oracle_explore_par(const oracle_system* h, int64_t F0, const int32_t* level0
     };
     int64_t T = 0;
     // parents in chunks whose children fit a bounded buffer
-    const uint64_t budget = std::max<uint64_t>(1, ((uint64_t)1 << 28) / (uint64_t)m);  // children per chunk
+    const uint64_t budget = (uint64_t)1 << 22;  // children per chunk (their fingerprints are held)
     for (int64_t c0 = 0; c0 < F;) {
       int64_t c1 = c0;
       uint64_t nch = 0;
       while (c1 < F && (c1 == c0 || nch + psi[c1] <= budget)) nch += psi[c1++];
       std::vector<uint64_t> base(c1 - c0 + 1, 0);
       for (int64_t i = c0; i < c1; ++i) base[i - c0 + 1] = base[i - c0] + psi[i];
-      std::vector<int64_t> rows((size_t)nch * (size_t)m);
       std::vector<std::pair<uint64_t, uint64_t>> fps(nch);
       parallel_for(c0, c1, n_threads, [&](int64_t i) {
         const std::vector<int64_t> C = row_of(lo + i);
         auto A = applicable_rules_per_neuron(s, C);
         for (uint64_t t = 0; t < psi[i]; ++t) {
           auto Cn = transition(s, C, spiking_vector(s, A, t));
-          const uint64_t k = base[i - c0] + t;
-          std::copy(Cn.begin(), Cn.end(), rows.begin() + (size_t)k * (size_t)m);
-          fps[k] = fingerprint(Cn, seed0, seed1);
+          fps[base[i - c0] + t] = fingerprint_of(Cn);
         }
       });
       // canonical order: parents in order, t increasing (reading A7)
@@ -977,16 +1008,18 @@ int oracle_explore_par(const oracle_system* h, int64_t F0, const int32_t* level0
         for (uint64_t t = 0; t < psi[i]; ++t) {
           ++T;
           if (max_transitions > 0 && T > max_transitions) { run.status = OR_E_CAPACITY; run.error = "transition budget exceeded"; return run.status; }
-          const uint64_t k = base[i - c0] + t;
-          const int64_t* Cn = rows.data() + (size_t)k * m;
-          const auto& f = fps[k];
-          if (seen(Cn, f)) continue;  // produced at an earlier level (A6)
+          const auto& f = fps[base[i - c0] + t];
+          std::vector<int64_t> Cn;  // this child's row, recomputed only for a dedup = 0 comparison
+          auto cn = [&]() {
+            if (Cn.empty()) Cn = child_row(i, t);
+            return Cn;
+          };
+          if (seen(f, cn)) continue;  // produced at an earlier level (A6)
           bool dup = false;
           auto rg = level_keys.equal_range(f.first);
           for (auto it = rg.first; it != rg.second && !dup; ++it) {
             const Cand& o = fresh[it->second];
-            dup = dedup == 1 ? o.f.second == f.second
-                             : child_row(o.parent, o.t) == std::vector<int64_t>(Cn, Cn + m);
+            dup = dedup == 1 ? o.f.second == f.second : child_row(o.parent, o.t) == cn();
           }
           if (dup) continue;  // same-level duplicate: first (minimum) tag wins
           level_keys.emplace(f.first, (int64_t)fresh.size());

@@ -1955,7 +1955,56 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = xs[r];
     }
     }  // j < m
-#if SNP_KC_COOP
+#if SNP_KC_COOP == 2
+    if (prog) {
+      // full 4-child quads, warp-cooperative over the flat list of (row,
+      // quad) pairs of this warp: lane i takes pairs i, i + 32, ... (row =
+      // one of the warp's 32 neurons, quad = one of the CTA's nq full output
+      // quads), so every lane stores on every iteration; a byte permute of
+      // the neuron's x row when the 4 parents lie in a 16-byte window, else 4
+      // byte loads
+      __syncwarp();
+      const uint64_t qa = (Q0 + 3) & ~3ULL, qb = Q1 & ~3ULL;
+      const int32_t jn = m - jbase;  // rows of this warp that exist
+      if (!(SNP_KC_ABLATE & 4) && qa < qb) {
+        const uint32_t nq = (uint32_t)((qb - qa) >> 2);
+        const uint32_t nrow = jn < 32 ? (uint32_t)jn : 32u;
+        const uint32_t total = nq * nrow;
+        const uint32_t dr = 32u / nq, dk = 32u % nq;   // step of (row, quad) per 32 pairs
+        uint32_t r = (uint32_t)lane / nq, k = (uint32_t)lane % nq;
+        const uint64_t qoff = (qa - Qb) >> 2;
+        const uint64_t mrow = (uint64_t)m << 6;       // output-block stride in bytes
+        uint8_t* obase = reinterpret_cast<uint8_t*>(out) + ((int64_t)jbase << 6);
+        for (uint32_t idx = lane; idx < total; idx += 32) {
+          const uint64_t q = qa + 4 * (uint64_t)k;
+          const uint32_t d = sD[qoff + k];
+          const uint8_t* xr = sX + (size_t)(warp * 32 + r) * xs_stride<T>();
+          uint32_t v;
+          if (!(d & 0x80000000u)) {
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(xr) + ((d >> 16) & 31);
+            const uint32_t sel = d & 0xFFFFu, hb = d >> 24;
+            v = prmt(w[0], w[1], sel);
+            if (hb) {
+              const uint32_t mask = (hb * 0x00204081u & 0x01010101u) * 0xFFu;
+              v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
+            }
+          } else {
+            const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (q - Qb));
+            v = (uint32_t)xr[rr & 0xFF] | ((uint32_t)xr[(rr >> 8) & 0xFF] << 8) |
+                ((uint32_t)xr[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xr[rr >> 24] << 24);
+          }
+          *reinterpret_cast<uint32_t*>(obase + (q >> 6) * mrow + ((uint64_t)r << 6) + (q & 63)) = v;
+          k += dk;
+          r += dr;
+          if (k >= nq) {
+            k -= nq;
+            ++r;
+          }
+        }
+      }
+      __syncwarp();
+    }
+#elif SNP_KC_COOP
     if (prog) {
       // full 4-child quads, warp-cooperative: a half-warp covers one 64-child
       // output row (lane = quad; a byte permute of the neuron's x row when
@@ -2332,15 +2381,17 @@ __global__ void k_spiking_vectors(SysView S, const T* pdata, const int64_t* pare
     uint64_t t = tt[q];
     uint8_t* Sq = S_out + q * S.n;
     for (int64_t r = 0; r < S.n; ++r) Sq[r] = 0;
+    bool any = false;
     for (int32_t s = S.m - 1; s >= 0; --s) {  // least significant digit = last neuron
       const int32_t v = (int32_t)pdata[eidx(p, s, S.m)];
       const int d = count_applicable(S, s, v);
       if (d == 0) continue;
+      any = true;
       const int x = (int)(t % (uint64_t)d);
       t /= (uint64_t)d;
       Sq[nth_applicable(S, s, v, x)] = 1;
     }
-    if (t && err) atomicOr(err, ERR_CAPACITY);  // t >= Ψ: no such spiking vector
+    if ((t || !any) && err) atomicOr(err, ERR_CAPACITY);  // t >= Ψ (Ψ = 0 when halting): no such vector
   }
 }
 
