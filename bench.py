@@ -266,7 +266,7 @@ def run_native(args, rank, world):
     if use_dist:
         from paper_1104_1824_b200 import dist as D
         lo, hi = D.level0_slice(F, rank, world)
-        runner = D.DistExplorer(eng)
+        runner = D.DistExplorer(eng)  # the library's NCCL communicator; every exchange inside snp_dist_advance
     else:
         lo, hi, runner = 0, F, eng
     Fl = hi - lo
@@ -330,8 +330,9 @@ def run_native(args, rank, world):
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": f"u{8 * wb}" if wb < 4 else "i32", "data": "synthetic",
         "config": {**config_json(args, cfg, w, args.steps),
-                   "parallelism": f"hash-partitioned dedup over {world} GPU(s), keys all-to-all (NCCL)"
-                   if world > 1 else "1 GPU"},
+                   "parallelism": f"hash-partitioned dedup over {world} GPU(s): keys all-to-all over NCCL issued by "
+                                  f"libsnp.so (snp_dist_advance), frontier range-partitioned and rebalanced"
+                   if use_dist else "1 GPU"},
         "roofline": {"bound": "hbm", "kernel": f"phase '{dom}' ({KERNEL_OF.get(dom, dom)})",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(dom), "peak_source": peak_src},
@@ -349,10 +350,8 @@ def run_native(args, rank, world):
     eng.close()
     del eng, runner
     torch.cuda.empty_cache()
-    if not args.no_e2e and world == 1:
-        out["e2e"] = run_e2e(args, cfg, w, snp, torch)
-    elif not args.no_e2e:
-        out["e2e"] = {"value": None, "unit": UNIT, "note": "e2e measured at N=1 only this round"}
+    if not args.no_e2e:
+        out["e2e"] = run_e2e(args, cfg, w, snp, torch, rank, world, dist if use_dist else None)
     if not args.no_cpu and rank == 0 and world == 1:
         out["cpu_baseline"] = cpu_baseline(w, cfg)
     if rank == 0:
@@ -362,48 +361,65 @@ def run_native(args, rank, world):
         dist.destroy_process_group()
 
 
-def run_e2e(args, cfg, w, snp, torch):
-    """The user's call path: snp_begin from a pinned host level 0 (row-major),
-    then snp_advance per level, reading each level's edges back to the host."""
+def run_e2e(args, cfg, w, snp, torch, rank=0, world=1, dist=None):
+    """The user's call path: level 0 from a pinned HOST buffer (row-major;
+    snp_begin, or snp_dist_start with this rank's slice), then per level
+    snp_advance / snp_dist_advance and the new level's edges + fingerprints
+    read back into pinned host buffers.  N > 1: each rank its slice, wall
+    time between barriers, max over ranks; value = all ranks' transitions."""
     m, F = w.m, cfg["F"]
     wb = cfg["count_bits"] // 8
     dt = torch.uint8 if wb == 1 else torch.int32
+    lo, hi = (F * rank // world, F * (rank + 1) // world)
+    Fl = hi - lo
     try:
-        host = torch.empty((F, m), dtype=dt, pin_memory=True)
+        host = torch.empty((max(Fl, 1), m), dtype=dt, pin_memory=True)
     except Exception as e:  # pinned allocation failed
         return {"value": None, "unit": UNIT, "error": f"pinned host buffer: {e}"}
     # fill the host buffer with the same level 0 (device generator, chunked D2H; setup, untimed)
     chunk = max(1, (1 << 31) // (m * wb))
     tmp = torch.empty((chunk, m), dtype=dt, device="cuda")
-    for r0 in range(0, F, chunk):
-        n = min(chunk, F - r0)
+    for r0 in range(0, Fl, chunk):
+        n = min(chunk, Fl - r0)
         snp.generate_level0_device(w, n, cfg["seed"], tmp.data_ptr(), wb, snp.SNP_LAYOUT_ROW_MAJOR, m, 0,
-                                   row_begin=r0)
+                                   row_begin=lo + r0)
         host[r0:r0 + n].copy_(tmp[:n])
     del tmp
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     eng = snp.System(w, count_bits=cfg["count_bits"], dedup=cfg["dedup"], frontier_target=cfg["frontier_target"],
                      keep_tree=0)
-    c0 = snp.snp_configs(host.data_ptr(), F, m, wb, snp.SNP_LAYOUT_ROW_MAJOR, 0, 0)
-    eng.reserve_edges(F + F // 8)  # the pinned result buffers, like the pinned input: allocated before timing
+    runner = eng
+    if dist is not None:
+        from paper_1104_1824_b200 import dist as D
+        runner = D.DistExplorer(eng)
+    c0 = snp.snp_configs(host.data_ptr(), Fl, m, wb, snp.SNP_LAYOUT_ROW_MAJOR, 0, 0)
+    eng.reserve_edges(2 * (F // world) + 1024)  # pinned result buffers, like the pinned input: allocated before timing
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
     t0 = time.perf_counter()
-    eng.begin(c0)
+    runner.begin(c0)
     T_sum = 0
     d2h = 0
     for _ in range(args.steps):
-        c = eng.advance()
+        c = runner.advance()
         T_sum += c["T"]
         parent, t, _h, fp = eng.level_edges(eng.depth, pinned=True, halting=False)
         d2h += parent.nbytes + t.nbytes + fp.nbytes
     dt_s = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([dt_s, d2h], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+        dt_s, d2h = float(tt[0].item()), int(tt[1].item())
     eng.close()
     del host
     return {"value": T_sum / dt_s, "unit": UNIT, "h2d_bytes_per_step": F * m * wb // args.steps,
             "d2h_bytes_per_step": d2h // args.steps,
-            "note": "snp_begin(pinned host row-major level 0) + K x (snp_advance + snp_level_edges D2H into pinned buffers); "
-                    "wall clock around synchronous ABI calls"}
+            "note": ("snp_begin" if world == 1 else f"snp_dist_start ({world} ranks, one host slice each)") +
+                    "(pinned host row-major level 0) + K x (advance + snp_level_edges D2H into pinned buffers); "
+                    "wall clock around synchronous ABI calls" + (", max over ranks" if world > 1 else "")}
 
 
 def main():

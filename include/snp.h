@@ -300,10 +300,11 @@ int32_t    snp_kernel_paths(const snp_system *sys);
 snp_status snp_host_alloc(size_t bytes, void **p);
 snp_status snp_host_free(void *p);
 
-/* Multi-GPU exploration (one process per GPU).  Rank r holds a
- * contiguous range of the global frontier (global order = rank order, then
- * local tag order) and the visited keys with owner fmix64(fp1) mod P.  The
- * caller runs the collectives between the calls (paper_1104_1824_b200/dist.py):
+/* Multi-GPU exploration, step by step (one process per GPU) —
+ * the building blocks snp_dist_advance (below) runs with its own exchanges.
+ * Rank r holds a contiguous range of the global frontier (global order = rank
+ * order, then local tag order) and the visited keys with owner fmix64(fp1)
+ * mod P.  A caller driving the steps runs the collectives between them:
  *   snp_dist_begin(level0 rows of this rank)      → keys of the level-0 rows
  *   snp_dist_expand                               → local T (children keys)
  *   snp_dist_pack(tag_base = Σ T of lower ranks, send: device T×3 uint64
@@ -324,6 +325,55 @@ snp_status snp_dist_owner_dedup(snp_system *sys, const void *recv, int64_t R, in
 snp_status snp_dist_owner_keep(snp_system *sys, int64_t n_new_global, void *verdict_out);
 snp_status snp_dist_finalize(snp_system *sys, const void *verdict_back, int64_t *K_local);
 snp_status snp_dist_commit(snp_system *sys, int64_t parent_offset, int64_t q_offset, snp_level_counters *out);
+
+/* Library-driven multi-GPU exploration (one process per GPU; DESIGN.md §9;
+ * PAPER.md:425 names inter-block communication for very large systems).
+ * The library issues every exchange itself, on the system's stream:
+ *   snp_dist_unique_id   rank 0: SNP_DIST_ID_BYTES of NCCL unique id, which
+ *                        the caller broadcasts once (any host channel)
+ *   snp_dist_init        NCCL communicator of rank `rank` of `nranks` (the
+ *                        current CUDA device); libnccl.so.2 is opened at run
+ *                        time (SNP_E_NCCL when it is missing)
+ *   snp_local_group_create / snp_dist_init_local
+ *                        the same protocol among nranks snp_system handles of
+ *                        ONE process (one host thread each; device-to-device
+ *                        copies) — logical ranks on one GPU, used by the tests
+ *   snp_dist_start       level 0 := the distinct configurations of the
+ *                        concatenation of every rank's level0_local (rank
+ *                        order); *F_global = its size
+ *   snp_dist_advance     one BFS level over all ranks: local K-a/K-b, key
+ *                        all-to-all to owner = fmix64(fp1) mod P, owner-side
+ *                        dedup and thinning (τ from the global N_new, A19),
+ *                        verdicts back, local K-c; then, when the largest
+ *                        local frontier exceeds `rebalance` (default 1.1) ×
+ *                        the mean, rows move so that rank r holds the global
+ *                        range [F·r/P, F·(r+1)/P).  *global = the level's
+ *                        counters summed over ranks (ms = the slowest rank);
+ *                        *local = this rank's share (parents, T, kept before
+ *                        the redistribution, owner-side n_new, its ms).
+ *   snp_dist_summary     (collective) global configurations, transitions and
+ *                        the run digest — equal to a 1-GPU run's.
+ *   snp_dist_local       this rank's frontier size, its global offset, and
+ *                        the rows it sent in the last rebalancing.
+ * Every rank must make the same sequence of collective calls.  A failure on
+ * any rank (overflow, capacity, a CUDA or NCCL error) is agreed at the next
+ * exchange: every rank returns the failing rank's status (the lowest rank's
+ * when several fail) rather than waiting for it.  NCCL waits poll
+ * ncclCommGetAsyncError and abort after SNP_DIST_TIMEOUT_S seconds (default
+ * 600).  Parents reported by snp_level_edges are global indices in this mode.
+ * dedup = 1 only; no generated numbers, delays or keep_all_edges.           */
+#define SNP_DIST_ID_BYTES 128
+typedef struct snp_local_group snp_local_group;
+snp_status snp_dist_unique_id(void *id_out /* SNP_DIST_ID_BYTES */);
+snp_status snp_dist_init(snp_system *sys, const void *id, int32_t rank, int32_t nranks);
+snp_status snp_local_group_create(int32_t nranks, snp_local_group **out);
+void       snp_local_group_free(snp_local_group *group);
+snp_status snp_dist_init_local(snp_system *sys, snp_local_group *group, int32_t rank);
+snp_status snp_dist_set_rebalance(snp_system *sys, double threshold /* 0 = never */);
+snp_status snp_dist_start(snp_system *sys, const snp_configs *level0_local, int64_t *F_global);
+snp_status snp_dist_advance(snp_system *sys, snp_level_counters *global, snp_level_counters *local /* may be NULL */);
+snp_status snp_dist_summary(snp_system *sys, int64_t *n_configs, int64_t *transitions, uint64_t *digest);
+snp_status snp_dist_local(const snp_system *sys, int64_t *F_local, int64_t *global_offset, int64_t *rebalanced_rows);
 
 /* Single-path sampling with an input spike train (Def. 1
  * `in`; deep computation trees take long to

@@ -17,8 +17,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
-SNP_SOURCES = ["snp_engine.cu", "snp_kernels.cu"]
-SNP_DEPS = SNP_SOURCES + ["snp_device.cuh", "snp_internal.h", "snp_tc.cuh", "../../include/snp.h"]
+SNP_SOURCES = ["snp_engine.cu", "snp_kernels.cu", "snp_comm.cu"]
+SNP_DEPS = SNP_SOURCES + ["snp_device.cuh", "snp_internal.h", "snp_tc.cuh", "snp_comm.h", "../../include/snp.h"]
+LIBS = ["-ldl"]  # libnccl.so.2 is opened at run time (snp_comm.cu)
 
 
 def _stale(target: str, deps) -> bool:
@@ -29,10 +30,25 @@ def _stale(target: str, deps) -> bool:
 
 
 def _nvcc(out: str, sources, extra=()):
+    """compile each source to an object in parallel (-dc free: no device
+    linking across files), then link the shared library"""
+    from concurrent.futures import ThreadPoolExecutor
     tmp = out + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-o", tmp, *[os.path.join(CSRC, s) for s in sources]]
-    subprocess.check_call(cmd)
-    os.replace(tmp, out)
+    objs = [f"{tmp}.{i}.o" for i in range(len(sources))]
+    comp = [x for x in FLAGS if x != "-shared"]
+
+    def one(i):
+        subprocess.check_call([NVCC, *ARCH, *comp, *extra, "-c", "-o", objs[i], os.path.join(CSRC, sources[i])])
+
+    try:
+        with ThreadPoolExecutor(len(sources)) as ex:
+            list(ex.map(one, range(len(sources))))
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs, *LIBS])
+        os.replace(tmp, out)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.unlink(o)
 
 
 def build(force: bool = False, verbose: bool = False) -> None:

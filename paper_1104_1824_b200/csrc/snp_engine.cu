@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/snp.h"
+#include "snp_comm.h"
 #include "snp_internal.h"
 
 using namespace snp;
@@ -236,6 +237,15 @@ struct snp_system {
     DBuf perm, hist, slot, verdict;
     ExpandOut O{};
     int64_t owned = 0;      // keys in this rank's visited shard
+    // library-driven levels (snp_dist_init / snp_dist_advance): the transport,
+    // exchange buffers and the global view of the exploration
+    snp::Comm* comm = nullptr;
+    snp::LocalGroup* group = nullptr;
+    DBuf sendbuf, recvbuf, vbuf, backbuf, rbuf, mbuf[2];
+    double rebalance = 1.1;   // max/mean local frontier above which rows are redistributed (0 = never)
+    int64_t F_global = 0, q_off = 0, n_configs = 0, T_total = 0;
+    int64_t rebalanced_rows = 0;  // rows this rank sent in the last rebalancing
+    int inject_step = -1;         // SNP_DIST_INJECT="rank,step": fail this rank at that protocol step (tests)
   } dist;
   // phase profiling (snp_set_profiling)
   bool profiling = false;
@@ -1374,6 +1384,9 @@ snp_status snp_load_delay(const snp_matrix* M, const snp_rule* rules, int64_t n_
 namespace {
 void system_destroy(snp_system* s) {
   if (s->stream) cudaStreamSynchronize(s->stream);
+  delete s->dist.comm;
+  s->dist.comm = nullptr;
+  if (s->dist.group) snp::local_group_release(s->dist.group);
   s->levels.clear();
   s->spare.clear();
   if (s->ev0) cudaEventDestroy(s->ev0);
@@ -1827,7 +1840,19 @@ snp_status snp_dist_begin(snp_system* s, const snp_configs* level0, int32_t nran
   if (F0 < 0 || F0 > 0x7FFFFFFFLL || (F0 > 0 && !level0->data)) return fail(SNP_E_ARG, "level0: bad n_configs / data");
   if (level0->elem_bytes != 1 && level0->elem_bytes != 2 && level0->elem_bytes != 4) return fail(SNP_E_ARG, "level0: elem_bytes");
   SNP_TRY(reset_state(s));
-  s->dist = snp_system::Dist{};
+  {  // a fresh level-0 state; the transport and its settings stay
+    snp::Comm* comm = s->dist.comm;
+    snp::LocalGroup* group = s->dist.group;
+    const double rebalance = s->dist.rebalance;
+    const int inject = s->dist.inject_step;
+    s->dist.comm = nullptr;
+    s->dist.group = nullptr;
+    s->dist = snp_system::Dist{};
+    s->dist.comm = comm;
+    s->dist.group = group;
+    s->dist.rebalance = rebalance;
+    s->dist.inject_step = inject;
+  }
   s->dist.P = nranks;
   s->begun = false;
   SNP_TRY(zero_counters(s));
@@ -2139,6 +2164,341 @@ snp_status snp_dist_commit(snp_system* s, int64_t parent_offset, int64_t q_offse
   s->halting_current_valid = false;
   s->dist.stage = 0;
   if (out) *out = lc;
+  return SNP_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// library-driven multi-GPU levels: the steps above with the
+// exchanges issued by the library on the system's stream (snp_comm.h).  Each
+// step's status is agreed by all ranks at the next collective (it rides in
+// the small all-gathers), so a rank that fails (overflow, capacity, an
+// injected fault) makes every rank return that same status instead of leaving
+// its peers inside a collective.
+// ===========================================================================
+namespace {
+
+// agreement: every rank contributes (status, values...); returns the status of
+// the lowest failing rank (SNP_OK when none failed) and all values in out
+snp_status agree(snp_system* s, snp_status mine, const std::vector<int64_t>& vals, std::vector<int64_t>* out) {
+  snp::Comm* c = s->dist.comm;
+  const int n = 1 + (int)vals.size();
+  std::vector<int64_t> in(n), all((size_t)n * c->P);
+  in[0] = (int64_t)mine;
+  std::copy(vals.begin(), vals.end(), in.begin() + 1);
+  std::string msg;
+  const std::string my_err = mine != SNP_OK ? g_err : std::string();
+  int st = c->allgather_i64(in.data(), n, all.data(), s->stream, &msg);
+  if (st != SNP_OK) return fail((snp_status)st, "multi-GPU exchange: %s", msg.c_str());
+  if (out) out->assign(all.begin(), all.end());
+  for (int r = 0; r < c->P; ++r)
+    if (all[(size_t)r * n] != SNP_OK) {
+      if (r == c->rank) return fail((snp_status)all[(size_t)r * n], "%s", my_err.c_str());
+      return fail((snp_status)all[(size_t)r * n], "rank %d failed (status %lld); every rank stops", r,
+                  (long long)all[(size_t)r * n]);
+    }
+  return SNP_OK;
+}
+
+snp_status injected(snp_system* s, int step) {
+  if (s->dist.inject_step == step) return fail(SNP_E_CAPACITY, "injected fault (SNP_DIST_INJECT) at step %d", step);
+  return SNP_OK;
+}
+
+snp_status xfer(snp_system* s, const void* send, const std::vector<int64_t>& sc, void* recv,
+                const std::vector<int64_t>& rc, size_t elem) {
+  std::string msg;
+  int st = s->dist.comm->alltoallv(send, sc.data(), recv, rc.data(), elem, s->stream, &msg);
+  if (st != SNP_OK) return fail((snp_status)st, "multi-GPU exchange: %s", msg.c_str());
+  return SNP_OK;
+}
+
+// one keys round (level 0 when s->dist.level0): pack, key all-to-all, owner
+// dedup, N_new, owner keep, verdicts back, finalize, commit; the global
+// counters of the level in *g
+snp_status keys_round(snp_system* s, snp_status st, int64_t T_local, int64_t halting_local, snp_level_counters* g,
+                      snp_level_counters* lo_out = nullptr) {
+  snp::Comm* c = s->dist.comm;
+  const int P = c->P, me = c->rank;
+  std::vector<int64_t> all;
+  const int64_t F_local = s->dist.level0 ? 0 : s->levels.back()->F;
+  if (st == SNP_OK) st = injected(s, 1);
+  SNP_TRY(agree(s, st, {T_local, F_local, halting_local}, &all));
+  int64_t tag_base = 0, T_glob = 0, F_glob = 0, H_glob = 0, p_off = 0;
+  for (int r = 0; r < P; ++r) {
+    if (r < me) { tag_base += all[4 * r + 1]; p_off += all[4 * r + 2]; }
+    T_glob += all[4 * r + 1];
+    F_glob += all[4 * r + 2];
+    H_glob += all[4 * r + 3];
+  }
+  // keys {fp0, fp1, global tag} grouped by owner
+  std::vector<int64_t> sc(P, 0), rc(P, 0);
+  st = s->dist.sendbuf.ensure((size_t)std::max<int64_t>(T_local, 1) * 24);
+  if (st == SNP_OK) st = snp_dist_pack(s, (uint64_t)tag_base, s->dist.sendbuf.p, sc.data());
+  if (st == SNP_OK) st = injected(s, 2);
+  SNP_TRY(agree(s, st, sc, &all));
+  for (int q = 0; q < P; ++q) rc[q] = all[(size_t)q * (P + 1) + 1 + me];
+  int64_t R = 0;
+  for (int64_t x : rc) R += x;
+  SNP_TRY(s->dist.recvbuf.ensure((size_t)std::max<int64_t>(R, 1) * 24));
+  SNP_TRY(xfer(s, s->dist.sendbuf.p, sc, s->dist.recvbuf.p, rc, 24));
+  int64_t n_new_local = 0;
+  st = snp_dist_owner_dedup(s, s->dist.recvbuf.p, R, &n_new_local);
+  if (st == SNP_OK) st = injected(s, 3);
+  SNP_TRY(agree(s, st, {n_new_local}, &all));
+  int64_t n_new = 0;
+  for (int r = 0; r < P; ++r) n_new += all[2 * r + 1];
+  st = s->dist.vbuf.ensure((size_t)std::max<int64_t>(R, 1));
+  if (st == SNP_OK) st = snp_dist_owner_keep(s, n_new, s->dist.vbuf.p);
+  if (st == SNP_OK) st = injected(s, 4);
+  SNP_TRY(agree(s, st, {}, nullptr));
+  SNP_TRY(s->dist.backbuf.ensure((size_t)std::max<int64_t>(T_local, 1)));
+  SNP_TRY(xfer(s, s->dist.vbuf.p, rc, s->dist.backbuf.p, sc, 1));  // verdicts return in send order
+  int64_t K = 0;
+  st = snp_dist_finalize(s, s->dist.backbuf.p, &K);
+  if (st == SNP_OK) st = injected(s, 5);
+  SNP_TRY(agree(s, st, {K}, &all));
+  int64_t q_off = 0, K_glob = 0;
+  std::vector<int64_t> Ks(P);
+  for (int r = 0; r < P; ++r) {
+    Ks[r] = all[2 * r + 1];
+    if (r < me) q_off += Ks[r];
+    K_glob += Ks[r];
+  }
+  snp_level_counters lc{};
+  st = snp_dist_commit(s, p_off, q_off, &lc);
+  if (st == SNP_OK && !s->levels.empty()) {  // parents as global indices of the previous level
+    Level* L = s->levels.back().get();
+    if (L->F) launch_add_i64(L->parent.as<int64_t>(), L->F, p_off, s->stream);
+    if (cudaGetLastError() != cudaSuccess) st = fail(SNP_E_CUDA, "parent offsets");
+  }
+  if (st == SNP_OK) st = injected(s, 6);
+  std::vector<int64_t> msv;
+  SNP_TRY(agree(s, st, {(int64_t)std::llround(lc.ms * 1000.0)}, &msv));
+  double ms_max = 0;
+  for (int r = 0; r < P; ++r) ms_max = std::max(ms_max, msv[2 * r + 1] / 1000.0);
+  s->dist.q_off = q_off;
+  s->dist.F_global = K_glob;
+  s->dist.n_configs += K_glob;
+  if (g) {
+    *g = snp_level_counters{};
+    g->parents = s->dist.level0 ? 0 : F_glob;
+    g->halting = H_glob;
+    g->T = s->dist.level0 ? 0 : T_glob;
+    g->n_new = n_new;
+    g->kept = K_glob;
+    g->tau = lc.tau;
+    g->ms = ms_max;
+    g->overflow_fixes = lc.overflow_fixes;
+  }
+  if (lo_out) {
+    *lo_out = lc;
+    lo_out->parents = F_local;
+    lo_out->T = T_local;
+    lo_out->halting = halting_local;
+    lo_out->n_new = n_new_local;
+    lo_out->kept = K;
+  }
+  // rebalancing: the next frontier back to equal contiguous shares
+  int64_t kmax = 0;
+  for (int64_t k : Ks) kmax = std::max(kmax, k);
+  const double mean = (double)K_glob / P;
+  if (P > 1 && s->dist.rebalance > 0 && K_glob > 0 && kmax > s->dist.rebalance * mean) {
+    // rows [q_off, q_off + K) of the global level move to rank d's target
+    // range [K·d/P, K·(d+1)/P); blocked row chunks (padded to 64) plus the
+    // per-row metadata travel in four more all-to-alls
+    Level* L = s->levels.back().get();
+    const int64_t m = s->m;
+    std::vector<int64_t> lo(P + 1);
+    for (int d = 0; d <= P; ++d) lo[d] = K_glob * d / P;
+    std::vector<int64_t> qs(P + 1, 0);
+    for (int r = 0; r < P; ++r) qs[r + 1] = qs[r] + Ks[r];
+    auto overlap = [&](int src, int dst) {
+      const int64_t a = std::max(qs[src], lo[dst]), b = std::min(qs[src + 1], lo[dst + 1]);
+      return b > a ? b - a : (int64_t)0;
+    };
+    std::vector<int64_t> scr(P), rcr(P), scb(P), rcb(P);
+    for (int q = 0; q < P; ++q) {
+      scr[q] = overlap(me, q);
+      rcr[q] = overlap(q, me);
+      scb[q] = (int64_t)level_bytes(scr[q], m, s->bytes);
+      rcb[q] = (int64_t)level_bytes(rcr[q], m, s->bytes);
+    }
+    int64_t Snd = 0, Rcv = 0, Kn = 0, Sb = 0, Rb = 0;
+    for (int q = 0; q < P; ++q) { Snd += scr[q]; Rcv += rcr[q]; Sb += scb[q]; Rb += rcb[q]; }
+    Kn = lo[me + 1] - lo[me];
+    // pack this rank's rows as blocked chunks, one per destination
+    DBuf pack, recvrows, idx;
+    SNP_TRY(pack.ensure((size_t)std::max<int64_t>(Sb, 1), false));
+    SNP_TRY(recvrows.ensure((size_t)std::max<int64_t>(Rb, 1), false));
+    std::vector<uint64_t> hidx;
+    {
+      int64_t row = 0, boff = 0;
+      for (int q = 0; q < P; ++q) {
+        if (scr[q]) {
+          hidx.resize(scr[q]);
+          for (int64_t i = 0; i < scr[q]; ++i) hidx[i] = (uint64_t)(row + i);
+          SNP_TRY(idx.ensure((size_t)scr[q] * 8));
+          CUDA_TRY(cudaMemcpyAsync(idx.p, hidx.data(), scr[q] * 8, cudaMemcpyHostToDevice, s->stream));
+          launch_gather_columns(s->bytes, L->data.p, idx.as<uint64_t>(), scr[q], (int32_t)m,
+                                pack.as<uint8_t>() + boff, s->stream);
+          CUDA_TRY(cudaStreamSynchronize(s->stream));  // hidx is reused
+        }
+        row += scr[q];
+        boff += scb[q];
+      }
+    }
+    SNP_TRY(xfer(s, pack.p, scb, recvrows.p, rcb, 1));
+    // metadata: parent (global), t, fp0, fp1 — contiguous slices per destination
+    auto meta = [&](DView& v, DBuf& out) -> snp_status {
+      SNP_TRY(out.ensure((size_t)std::max<int64_t>(Kn, 1) * 8));
+      return xfer(s, v.p, scr, out.p, rcr, 8);
+    };
+    auto nl = std::make_unique<Level>();
+    nl->F = Kn;
+    SNP_TRY(alloc_level_meta(s, nl.get(), Kn));
+    DBuf tmp;
+    SNP_TRY(meta(L->parent, tmp));
+    CUDA_TRY(cudaMemcpyAsync(nl->parent.p, tmp.p, Kn * 8, cudaMemcpyDeviceToDevice, s->stream));
+    SNP_TRY(meta(L->t, tmp));
+    CUDA_TRY(cudaMemcpyAsync(nl->t.p, tmp.p, Kn * 8, cudaMemcpyDeviceToDevice, s->stream));
+    SNP_TRY(meta(L->fp0, tmp));
+    CUDA_TRY(cudaMemcpyAsync(nl->fp0.p, tmp.p, Kn * 8, cudaMemcpyDeviceToDevice, s->stream));
+    SNP_TRY(meta(L->fp1, tmp));
+    CUDA_TRY(cudaMemcpyAsync(nl->fp1.p, tmp.p, Kn * 8, cudaMemcpyDeviceToDevice, s->stream));
+    // received chunks -> one blocked level (chunk q starts at block base_q)
+    if (Kn > 0) {
+      hidx.resize(Kn);
+      int64_t k = 0, base = 0;
+      for (int q = 0; q < P; ++q) {
+        for (int64_t i = 0; i < rcr[q]; ++i) hidx[k++] = (uint64_t)(base + i);
+        base += (rcr[q] + PB - 1) / PB * PB;
+      }
+      SNP_TRY(idx.ensure((size_t)Kn * 8));
+      CUDA_TRY(cudaMemcpyAsync(idx.p, hidx.data(), Kn * 8, cudaMemcpyHostToDevice, s->stream));
+      SNP_TRY(take_buffer(s, level_bytes(Kn, m, s->bytes), &nl->data));
+      launch_gather_columns(s->bytes, recvrows.p, idx.as<uint64_t>(), Kn, (int32_t)m, nl->data.p, s->stream);
+      CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    release_level_data(s, L);
+    s->levels.back() = std::move(nl);
+    s->dist.q_off = lo[me];
+    s->dist.rebalanced_rows = Snd - scr[me];
+  } else {
+    s->dist.rebalanced_rows = 0;
+  }
+  return SNP_OK;
+}
+
+snp_status dist_ready(snp_system* s) {
+  if (!s) return fail(SNP_E_ARG, "NULL system");
+  if (!s->dist.comm) return fail(SNP_E_STATE, "no multi-GPU transport: call snp_dist_init or snp_dist_init_local first");
+  return SNP_OK;
+}
+
+void inject_from_env(snp_system* s) {
+  s->dist.inject_step = -1;
+  if (const char* e = getenv("SNP_DIST_INJECT")) {
+    int r = -1, step = -1;
+    if (sscanf(e, "%d,%d", &r, &step) == 2 && r == s->dist.comm->rank) s->dist.inject_step = step;
+  }
+}
+
+}  // namespace
+
+struct snp_local_group { snp::LocalGroup* g; };
+
+extern "C" {
+
+snp_status snp_dist_unique_id(void* id_out) {
+  if (!id_out) return fail(SNP_E_ARG, "snp_dist_unique_id: NULL");
+  std::string msg;
+  int st = snp::nccl_unique_id(id_out, &msg);
+  if (st != SNP_OK) return fail((snp_status)st, "%s", msg.c_str());
+  return SNP_OK;
+}
+
+snp_status snp_dist_init(snp_system* s, const void* id, int32_t rank, int32_t nranks) {
+  if (!s || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(SNP_E_ARG, "snp_dist_init: bad arguments");
+  delete s->dist.comm;
+  s->dist.comm = nullptr;
+  std::string msg;
+  int st = SNP_OK;
+  s->dist.comm = snp::make_nccl_comm(id, rank, nranks, &msg, &st);
+  if (!s->dist.comm) return fail((snp_status)st, "%s", msg.c_str());
+  inject_from_env(s);
+  return SNP_OK;
+}
+
+snp_status snp_local_group_create(int32_t nranks, snp_local_group** out) {
+  if (!out || nranks < 1) return fail(SNP_E_ARG, "snp_local_group_create: bad arguments");
+  *out = new snp_local_group{snp::local_group_create(nranks)};
+  return SNP_OK;
+}
+
+void snp_local_group_free(snp_local_group* g) {
+  if (!g) return;
+  snp::local_group_release(g->g);
+  delete g;
+}
+
+snp_status snp_dist_init_local(snp_system* s, snp_local_group* g, int32_t rank) {
+  if (!s || !g || rank < 0 || rank >= snp::local_group_size(g->g)) return fail(SNP_E_ARG, "snp_dist_init_local: bad arguments");
+  delete s->dist.comm;
+  s->dist.comm = snp::make_local_comm(g->g, rank);
+  inject_from_env(s);
+  return SNP_OK;
+}
+
+snp_status snp_dist_set_rebalance(snp_system* s, double threshold) {
+  if (!s || threshold < 0) return fail(SNP_E_ARG, "snp_dist_set_rebalance: bad arguments");
+  s->dist.rebalance = threshold;
+  return SNP_OK;
+}
+
+snp_status snp_dist_start(snp_system* s, const snp_configs* level0_local, int64_t* F_global) {
+  SNP_TRY(dist_ready(s));
+  int64_t n = 0;
+  snp_status st = snp_dist_begin(s, level0_local, s->dist.comm->P, &n);
+  s->dist.n_configs = 0;
+  s->dist.T_total = 0;
+  SNP_TRY(keys_round(s, st, n, 0, nullptr));
+  if (F_global) *F_global = s->dist.F_global;
+  return SNP_OK;
+}
+
+snp_status snp_dist_advance(snp_system* s, snp_level_counters* global, snp_level_counters* local) {
+  SNP_TRY(dist_ready(s));
+  if (s->dist.P < 1 || s->levels.empty()) return fail(SNP_E_STATE, "snp_dist_advance before snp_dist_start");
+  int64_t T = 0;
+  snp_status st = snp_dist_expand(s, &T);
+  const int64_t h = st == SNP_OK ? s->dist.lc.halting : 0;
+  snp_level_counters g{};
+  SNP_TRY(keys_round(s, st, T, h, &g, local));
+  s->dist.T_total += g.T;
+  if (global) *global = g;
+  return SNP_OK;
+}
+
+snp_status snp_dist_summary(snp_system* s, int64_t* n_configs, int64_t* transitions, uint64_t* digest) {
+  SNP_TRY(dist_ready(s));
+  std::vector<int64_t> all;
+  SNP_TRY(agree(s, SNP_OK, {(int64_t)s->digest}, &all));
+  uint64_t d = 0;
+  for (int r = 0; r < s->dist.comm->P; ++r) d += (uint64_t)all[2 * r + 1];
+  if (n_configs) *n_configs = s->dist.n_configs;
+  if (transitions) *transitions = s->dist.T_total;
+  if (digest) *digest = d;
+  return SNP_OK;
+}
+
+snp_status snp_dist_local(const snp_system* s, int64_t* F_local, int64_t* global_offset, int64_t* rebalanced_rows) {
+  if (!s || !s->dist.comm) return fail(SNP_E_STATE, "no multi-GPU transport");
+  if (F_local) *F_local = s->levels.empty() ? 0 : s->levels.back()->F;
+  if (global_offset) *global_offset = s->dist.q_off;
+  if (rebalanced_rows) *rebalanced_rows = s->dist.rebalanced_rows;
   return SNP_OK;
 }
 

@@ -110,6 +110,8 @@ void launch_level0_compact(const uint8_t* verdict, const uint64_t* kept, const u
                            const Tables& tb, int insert_visited, int32_t* err, cudaStream_t st);
 void launch_gather_columns(int32_t bytes, const void* src, const uint64_t* src_index, int64_t K, int32_t m, void* dst,
                            cudaStream_t st);
+// a[i] += add for every a[i] >= 0 (multi-GPU: local -> global parent indices)
+void launch_add_i64(int64_t* a, int64_t n, int64_t add, cudaStream_t st);
 void launch_verify_level0(int32_t bytes, const void* data, int32_t m, const ChildArrays& C, uint64_t F0,
                           const Tables& tb, int32_t* err, cudaStream_t st);
 void launch_rehash(const Slot* old_tab, uint64_t old_cap, Slot* new_tab, uint64_t new_mask, int32_t* err,

@@ -2312,6 +2312,11 @@ __global__ void k_level0_compact(const uint8_t* verdict, const uint64_t* kept, c
   }
 }
 
+__global__ void k_add_i64(int64_t* a, int64_t n, int64_t add) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (a[i] >= 0) a[i] += add;
+}
+
 template <typename T>
 __global__ void k_gather_columns(const T* src, const uint64_t* src_index, int64_t K, int32_t m, T* dst) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -3226,6 +3231,12 @@ void launch_gather_columns(int32_t bytes, const void* src, const uint64_t* src_i
     k_gather_columns<T><<<grid, BLK, 0, st>>>(reinterpret_cast<const T*>(src), src_index, K, m,
                                               reinterpret_cast<T*>(dst));
   });
+  count_launch();
+}
+
+void launch_add_i64(int64_t* a, int64_t n, int64_t add, cudaStream_t st) {
+  if (n <= 0 || add == 0) return;
+  k_add_i64<<<grid_for((uint64_t)n), BLK, 0, st>>>(a, n, add);
   count_launch();
 }
 

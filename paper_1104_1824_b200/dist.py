@@ -1,19 +1,14 @@
-"""Multi-GPU exploration driver: one process per GPU, torch.distributed (NCCL)
-for the collectives only — plumbing between the snp_dist_* calls of libsnp.so
-(include/snp.h).  Every step of the method (applicability, Ψ, decode, keys,
-owner-side dedup, thinning, C + S·M) runs in the library's CUDA kernels.
+"""Multi-GPU exploration driver (one process per GPU).
 
-Per level:
-  1. snp_dist_expand                 local children keys, local T
-  2. all_gather(T) → global tag base of this rank
-  3. snp_dist_pack                   keys grouped by owner = fmix64(fp1) mod P
-  4. all_to_all(counts), all_to_all(keys)        (keys only: 24 B per child)
-  5. snp_dist_owner_dedup            owner's visited shard + level table
-  6. all_reduce(N_new)               → global thinning threshold τ
-  7. snp_dist_owner_keep             verdicts (1 B per key) for the producers
-  8. all_to_all(verdicts back)
-  9. snp_dist_finalize               local kept count K
- 10. all_gather(K, F) → global offsets; snp_dist_commit (K-c materialization)
+The library runs every level itself (include/snp.h, ``snp_dist_advance``):
+local K-a/K-b, the key all-to-all to owner = fmix64(fp1) mod P, owner-side
+dedup and thinning, the verdict all-to-all back, local K-c and, when the
+frontier drifts out of balance, the row redistribution — all exchanges issued
+by libsnp.so on the engine's stream (NCCL over NVLink between processes, or
+device-to-device copies between the logical ranks of one process).  This
+module only sets the transport up: torch.distributed broadcasts the NCCL
+unique id once (setup, outside every level), or a ``LocalGroup`` joins P
+engine handles of one process.
 
 The frontier stays range-partitioned by rank, so the global order and every
 result equal a 1-GPU run (the digest is additive over ranks).
@@ -22,50 +17,7 @@ from __future__ import annotations
 
 import ctypes
 
-import numpy as np
-import torch
-import torch.distributed as dist
-
 from . import snp
-
-M64 = (1 << 64) - 1
-
-
-# ---- collective helpers (pure plumbing; also exercised with gloo in tests) ----
-def all_gather_ints(values, device, group=None):
-    """all_gather of a small vector of python ints → list of lists (rank order)."""
-    t = torch.tensor(list(values), dtype=torch.int64, device=device)
-    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(out, t, group=group)
-    return [o.tolist() for o in out]
-
-
-def all_reduce_int(v: int, device, group=None) -> int:
-    t = torch.tensor([v], dtype=torch.int64, device=device)
-    dist.all_reduce(t, group=group)
-    return int(t.item())
-
-
-def exchange(send: torch.Tensor, send_counts, group=None):
-    """all-to-all-v along dim 0: rows [Σ_{r'<r} send_counts[r'], +send_counts[r]) go to rank r.
-    Returns (recv, recv_counts)."""
-    P = dist.get_world_size(group)
-    sc = torch.tensor(list(send_counts), dtype=torch.int64, device=send.device)
-    rc = torch.empty(P, dtype=torch.int64, device=send.device)
-    dist.all_to_all_single(rc, sc, group=group)
-    recv_counts = rc.tolist()
-    recv = torch.empty((sum(recv_counts),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
-    dist.all_to_all_single(recv, send, output_split_sizes=recv_counts, input_split_sizes=list(send_counts),
-                           group=group)
-    return recv, recv_counts
-
-
-def exchange_back(verdict: torch.Tensor, recv_counts, send_counts, group=None) -> torch.Tensor:
-    """the reverse all-to-all-v: what rank r received comes back to it in send order."""
-    back = torch.empty((sum(send_counts),) + tuple(verdict.shape[1:]), dtype=verdict.dtype, device=verdict.device)
-    dist.all_to_all_single(back, verdict, output_split_sizes=list(send_counts), input_split_sizes=list(recv_counts),
-                           group=group)
-    return back
 
 
 def level0_slice(F0: int, rank: int, P: int):
@@ -75,117 +27,89 @@ def level0_slice(F0: int, rank: int, P: int):
     return lo, hi
 
 
-class TorchComm:
-    """The collectives DistExplorer needs, over a torch.distributed group."""
+def unique_id_bytes() -> bytes:
+    """snp_dist_unique_id: the NCCL unique id (rank 0 creates it)."""
+    buf = ctypes.create_string_buffer(snp.SNP_DIST_ID_BYTES)
+    snp._check(snp.lib().snp_dist_unique_id(buf))
+    return buf.raw
 
-    def __init__(self, group=None):
-        self.group = group
-        self.rank = dist.get_rank(group)
-        self.P = dist.get_world_size(group)
 
-    def all_gather_ints(self, values, device):
-        return all_gather_ints(values, device, self.group)
+def broadcast_unique_id(group=None) -> bytes:
+    """rank 0's NCCL unique id on every rank (torch.distributed, host objects;
+    called once before the first level)."""
+    import torch.distributed as dist
+    obj = [unique_id_bytes() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
 
-    def all_reduce_int(self, v, device):
-        return all_reduce_int(v, device, self.group)
 
-    def exchange(self, send, counts):
-        return exchange(send, counts, self.group)
+class LocalGroup:
+    """snp_local_group: P logical ranks (engine handles) of ONE process."""
 
-    def exchange_back(self, verdict, recv_counts, send_counts):
-        return exchange_back(verdict, recv_counts, send_counts, self.group)
+    def __init__(self, P: int):
+        self.P = P
+        self._h = ctypes.c_void_p()
+        snp._check(snp.lib().snp_local_group_create(P, ctypes.byref(self._h)))
 
-    def all_reduce_u64(self, v: int, device) -> int:
-        t = torch.tensor([v - (1 << 64) if v >= (1 << 63) else v], dtype=torch.int64, device=device)
-        dist.all_reduce(t, group=self.group)
-        return int(t.item()) & M64
+    def close(self):
+        if self._h:
+            snp.lib().snp_local_group_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class DistExplorer:
-    """Explore one SNP system over the ranks of a communicator (one GPU each)."""
+    """Explore one SNP system over P ranks.  transport: None → NCCL with the
+    torch.distributed rank / world size (unique id broadcast once); or a
+    ``(LocalGroup, rank)`` pair for logical ranks inside one process."""
 
-    def __init__(self, system: snp.System, comm=None):
+    def __init__(self, system: snp.System, transport=None, rebalance: float = 1.1, group=None):
         self.sys = system
-        self.comm = comm if comm is not None else TorchComm()
-        self.rank = self.comm.rank
-        self.P = self.comm.P
-        self.device = torch.device("cuda", torch.cuda.current_device())
         self.L = snp.lib()
-        self.F_local = 0
+        if transport is None:
+            import torch.distributed as dist
+            self.rank, self.P = dist.get_rank(group), dist.get_world_size(group)
+            uid = broadcast_unique_id(group)
+            snp._check(self.L.snp_dist_init(system._h, uid, self.rank, self.P))
+        else:
+            grp, self.rank = transport
+            self.P = grp.P
+            self._group = grp  # the handles keep their own reference; this keeps the wrapper alive
+            snp._check(self.L.snp_dist_init_local(system._h, grp._h, self.rank))
+        snp._check(self.L.snp_dist_set_rebalance(system._h, float(rebalance)))
         self.depth = -1
-        self.T_total = 0
-        self.n_configs = 0
-
-    def _check(self, st):
-        snp._check(st)
-
-    def _keys_round(self, T_local: int):
-        """steps 2-9 of the module docstring; returns (n_new_global, K_local, T_global)."""
-        T_all = [r[0] for r in self.comm.all_gather_ints([T_local], self.device)]
-        tag_base = sum(T_all[: self.rank])
-        send = torch.empty((T_local, 3), dtype=torch.int64, device=self.device)
-        counts = np.zeros(self.P, np.int64)
-        torch.cuda.synchronize()
-        self._check(self.L.snp_dist_pack(self.sys._h, tag_base, send.data_ptr() if T_local else None,
-                                         counts.ctypes.data_as(ctypes.c_void_p)))
-        recv, recv_counts = self.comm.exchange(send, counts.tolist())
-        torch.cuda.synchronize()
-        R = int(sum(recv_counts))
-        n_new_local = ctypes.c_int64()
-        self._check(self.L.snp_dist_owner_dedup(self.sys._h, recv.data_ptr() if R else None, R,
-                                                ctypes.byref(n_new_local)))
-        n_new = self.comm.all_reduce_int(n_new_local.value, self.device)
-        verdict = torch.empty(R, dtype=torch.uint8, device=self.device)
-        torch.cuda.synchronize()
-        self._check(self.L.snp_dist_owner_keep(self.sys._h, n_new, verdict.data_ptr() if R else None))
-        back = self.comm.exchange_back(verdict, recv_counts, counts.tolist())
-        torch.cuda.synchronize()
-        K = ctypes.c_int64()
-        self._check(self.L.snp_dist_finalize(self.sys._h, back.data_ptr() if T_local else None, ctypes.byref(K)))
-        del recv, send, verdict, back
-        return n_new, int(K.value), sum(T_all)
-
-    def _commit(self, K_local: int):
-        KF = self.comm.all_gather_ints([K_local, self.F_local], self.device)
-        q_off = sum(k for k, _ in KF[: self.rank])
-        p_off = sum(f for _, f in KF[: self.rank])
-        lc = snp.snp_level_counters()
-        self._check(self.L.snp_dist_commit(self.sys._h, p_off, q_off, ctypes.byref(lc)))
-        self.F_local = K_local
-        return lc, sum(k for k, _ in KF)
 
     def begin(self, level0_local: "snp.snp_configs") -> int:
-        """level0_local: this rank's contiguous slice of the global level 0."""
-        n = ctypes.c_int64()
-        self._check(self.L.snp_dist_begin(self.sys._h, ctypes.byref(level0_local), self.P, ctypes.byref(n)))
-        _n_new, K, _ = self._keys_round(int(n.value))
-        self.F_local = 0
-        _, K_total = self._commit(K)
+        """level0_local: this rank's contiguous slice of the global level 0;
+        returns the global level-0 size."""
+        F = ctypes.c_int64()
+        snp._check(self.L.snp_dist_start(self.sys._h, ctypes.byref(level0_local), ctypes.byref(F)))
         self.depth = 0
-        self.n_configs = K_total
-        self.T_total = 0
-        return K_total
+        return int(F.value)
 
     def advance(self) -> dict:
-        T_local = ctypes.c_int64()
-        self._check(self.L.snp_dist_expand(self.sys._h, ctypes.byref(T_local)))
-        n_new, K, T_total = self._keys_round(int(T_local.value))
-        lc, K_total = self._commit(K)
-        halting = self.comm.all_reduce_int(int(lc.halting), self.device)
-        parents = self.comm.all_reduce_int(int(lc.parents), self.device)
+        lc, lo = snp.snp_level_counters(), snp.snp_level_counters()
+        snp._check(self.L.snp_dist_advance(self.sys._h, ctypes.byref(lc), ctypes.byref(lo)))
         self.depth += 1
-        self.T_total += T_total
-        self.n_configs += K_total
-        return {"parents": parents, "halting": halting, "T": T_total, "n_new": n_new, "kept": K_total,
-                "tau": int(lc.tau), "ms": lc.ms, "parents_local": int(lc.parents), "kept_local": K,
-                "T_local": int(lc.T)}
+        d = lc.as_dict()
+        F, off, moved = self.local()
+        d.update(parents_local=lo.parents, T_local=lo.T, kept_local=lo.kept, frontier_local=F, global_offset=off,
+                 rebalanced_rows=moved)
+        return d
 
-    @property
-    def frontier_size_local(self) -> int:
-        return self.F_local
+    def local(self):
+        """(local frontier size, its global offset, rows sent in the last rebalancing)."""
+        F, off, moved = (ctypes.c_int64() for _ in range(3))
+        snp._check(self.L.snp_dist_local(self.sys._h, ctypes.byref(F), ctypes.byref(off), ctypes.byref(moved)))
+        return int(F.value), int(off.value), int(moved.value)
 
     def summary(self):
-        """global (configurations, transitions, digest); the digest is the sum of
-        the ranks' digests mod 2^64 and equals the 1-GPU digest."""
-        _n, _T, d = self.sys.summary()
-        return self.n_configs, self.T_total, self.comm.all_reduce_u64(d, self.device)
+        """global (configurations, transitions, digest) — a collective call."""
+        n, T, d = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_uint64()
+        snp._check(self.L.snp_dist_summary(self.sys._h, ctypes.byref(n), ctypes.byref(T), ctypes.byref(d)))
+        return int(n.value), int(T.value), int(d.value)

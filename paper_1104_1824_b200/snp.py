@@ -42,7 +42,10 @@ EXPORTED = [
     "snp_kernel_launches", "snp_kernel_paths", "snp_host_alloc", "snp_host_free", "snp_dist_begin", "snp_dist_expand", "snp_dist_pack", "snp_dist_owner_dedup",
     "snp_dist_owner_keep", "snp_dist_finalize", "snp_dist_commit",
     "snp_spiking_vector", "snp_level_spiking_vectors", "snp_frontier_copy", "snp_level_all_edges",
+    "snp_dist_unique_id", "snp_dist_init", "snp_local_group_create", "snp_local_group_free", "snp_dist_init_local",
+    "snp_dist_set_rebalance", "snp_dist_start", "snp_dist_advance", "snp_dist_summary", "snp_dist_local",
 ]
+SNP_DIST_ID_BYTES = 128
 SNP_NUM_PHASES = 5
 SNP_PATH_TC_EXPAND = 1
 PHASES = ["expand", "keys", "dedup", "materialize", "verify"]
@@ -158,8 +161,18 @@ def lib() -> ctypes.CDLL:
         L.snp_level_spiking_vectors.argtypes = [_P, ctypes.c_int32, _P, ctypes.c_int64, _P]
         L.snp_frontier_copy.argtypes = [_P, _P, _P, _P, ctypes.c_int64, _I64P]
         L.snp_level_all_edges.argtypes = [_P, ctypes.c_int32, _P, _P, _P, ctypes.c_int64, _I64P]
+        L.snp_dist_unique_id.argtypes = [_P]
+        L.snp_dist_init.argtypes = [_P, _P, ctypes.c_int32, ctypes.c_int32]
+        L.snp_local_group_create.argtypes = [ctypes.c_int32, ctypes.POINTER(_P)]
+        L.snp_local_group_free.argtypes = [_P]
+        L.snp_dist_init_local.argtypes = [_P, _P, ctypes.c_int32]
+        L.snp_dist_set_rebalance.argtypes = [_P, ctypes.c_double]
+        L.snp_dist_start.argtypes = [_P, ctypes.POINTER(snp_configs), _I64P]
+        L.snp_dist_advance.argtypes = [_P, ctypes.POINTER(snp_level_counters), ctypes.POINTER(snp_level_counters)]
+        L.snp_dist_summary.argtypes = [_P, _I64P, _I64P, ctypes.POINTER(ctypes.c_uint64)]
+        L.snp_dist_local.argtypes = [_P, _I64P, _I64P, _I64P]
         for f in EXPORTED:
-            if f not in ("snp_kernel_launches", "snp_kernel_paths", "snp_system_free", "snp_tree_free", "snp_frontier_size", "snp_depth", "snp_level_size",
+            if f not in ("snp_kernel_launches", "snp_kernel_paths", "snp_system_free", "snp_tree_free", "snp_frontier_size", "snp_depth", "snp_level_size", "snp_local_group_free",
                          "snp_tree_num_levels", "snp_tree_num_configs", "snp_abi_version", "snp_last_error"):
                 getattr(L, f).restype = ctypes.c_int
         _lib = L
