@@ -400,13 +400,19 @@ def run_e2e(args, cfg, w, snp, torch, rank=0, world=1, dist=None):
         dist.barrier()
     t0 = time.perf_counter()
     runner.begin(c0)
+    t_begin = time.perf_counter() - t0
     T_sum = 0
     d2h = 0
+    t_adv = t_edges = 0.0
     for _ in range(args.steps):
+        ta = time.perf_counter()
         c = runner.advance()
+        tb = time.perf_counter()
         T_sum += c["T"]
         parent, t, _h, fp = eng.level_edges(eng.depth, pinned=True, halting=False)
         d2h += parent.nbytes + t.nbytes + fp.nbytes
+        t_adv += tb - ta
+        t_edges += time.perf_counter() - tb
     dt_s = time.perf_counter() - t0
     if dist is not None:
         tt = torch.tensor([dt_s, d2h], dtype=torch.float64, device="cuda")
@@ -417,6 +423,9 @@ def run_e2e(args, cfg, w, snp, torch, rank=0, world=1, dist=None):
     del host
     return {"value": T_sum / dt_s, "unit": UNIT, "h2d_bytes_per_step": F * m * wb // args.steps,
             "d2h_bytes_per_step": d2h // args.steps,
+            "breakdown_s": {"begin (level-0 H2D + import + dedup)": round(t_begin, 4), "advance": round(t_adv, 4),
+                            "edges D2H": round(t_edges, 4), "total": round(dt_s, 4),
+                            "h2d_GBps_through_begin": round(Fl * m * wb / t_begin / 1e9, 2)},
             "note": ("snp_begin" if world == 1 else f"snp_dist_start ({world} ranks, one host slice each)") +
                     "(pinned host row-major level 0) + K x (advance + snp_level_edges D2H into pinned buffers); "
                     "wall clock around synchronous ABI calls" + (", max over ranks" if world > 1 else "")}
