@@ -77,8 +77,11 @@ struct System {
 bool regex_matches(const Rule& r, int64_t v) {
   if (r.kind == RE_EXACT) return v == r.a;
   if (r.kind == RE_UNARY) return r.member[v < r.a + r.b ? v : r.a + (v - r.a) % r.b] != 0;
-  // PERIODIC(i, j): v = i + x·j for some x >= 0
-  return v >= r.a && (v - r.a) % r.b == 0;
+  // PERIODIC(i, j): v = i + x·j for some x >= 0  ((v - i) mod j == 0; for a
+  // power-of-two j that is a mask of the low bits)
+  if (v < r.a) return false;
+  if ((r.b & (r.b - 1)) == 0) return ((v - r.a) & (r.b - 1)) == 0;
+  return (v - r.a) % r.b == 0;
 }
 
 // Rule applicability: the neuron holds v spikes, a^v ∈ L(E) and
@@ -103,13 +106,43 @@ std::vector<int64_t> mark_applicable(const System& sys, const std::vector<int64_
   return tmp;
 }
 
+// A_s for every neuron s: its applicable rules in total order, held in one
+// buffer (rules are grouped by non-decreasing neuron, validate()): A[s] is a
+// view with empty() / size() / operator[], A.size() = m.
+class RuleSets {
+ public:
+  struct View {
+    const int64_t* p;
+    size_t n;
+    bool empty() const { return n == 0; }
+    size_t size() const { return n; }
+    int64_t operator[](size_t i) const { return p[i]; }
+  };
+  explicit RuleSets(int64_t m = 0) : off_(m + 1, 0), last_(-1) {}
+  void add(int64_t s, int64_t r) {  // s non-decreasing
+    for (int64_t k = last_ + 1; k <= s; ++k) off_[k] = (int64_t)rules_.size();
+    last_ = s;
+    rules_.push_back(r);
+  }
+  void finish() {
+    for (int64_t k = last_ + 1; k < (int64_t)off_.size(); ++k) off_[k] = (int64_t)rules_.size();
+    last_ = (int64_t)off_.size() - 1;
+  }
+  size_t size() const { return off_.size() - 1; }
+  View operator[](int64_t s) const { return View{rules_.data() + off_[s], (size_t)(off_[s + 1] - off_[s])}; }
+
+ private:
+  std::vector<int64_t> rules_, off_;
+  int64_t last_;
+};
+
 // |σ_{V_i}| of eq. (8): the number of applicable rules of
 // each neuron, in increasing neuron order; A_s = those rules in total order.
-std::vector<std::vector<int64_t>> applicable_rules_per_neuron(const System& sys,
-                                                              const std::vector<int64_t>& C) {
-  std::vector<std::vector<int64_t>> A(sys.m);
+RuleSets applicable_rules_per_neuron(const System& sys, const std::vector<int64_t>& C) {
+  RuleSets A(sys.m);
   for (int64_t r = 0; r < sys.n; ++r)
-    if (applicable(sys.rules[r], C)) A[sys.rules[r].neuron].push_back(r);
+    if (applicable(sys.rules[r], C)) A.add(sys.rules[r].neuron, r);
+  A.finish();
   return A;
 }
 
@@ -117,10 +150,11 @@ std::vector<std::vector<int64_t>> applicable_rules_per_neuron(const System& sys,
 // A3: a neuron with no applicable rule contributes a factor 1 (it does not
 // fire); reading A5: if no neuron has an applicable rule the configuration is
 // halting and has no children (Ψ = 0).  Returns false if Ψ exceeds 2^62.
-bool count_children(const std::vector<std::vector<int64_t>>& A, uint64_t* psi) {
+bool count_children(const RuleSets& A, uint64_t* psi) {
   bool any = false;
   unsigned __int128 prod = 1;
-  for (const auto& As : A) {
+  for (int64_t s = 0; s < (int64_t)A.size(); ++s) {
+    const auto As = A[s];
     if (As.empty()) continue;
     any = true;
     prod *= (unsigned __int128)As.size();
@@ -136,8 +170,7 @@ bool count_children(const std::vector<std::vector<int64_t>>& A, uint64_t* psi) {
 // the most significant mixed-radix digit (tmp3 = ['10110','01110'],
 // PAPER.md:351, 376; reading A7).  Digit x_s selects A_s[x_s]; exactly one
 // rule fires per neuron with applicable rules (reading A4).
-std::vector<uint8_t> spiking_vector(const System& sys, const std::vector<std::vector<int64_t>>& A,
-                                    uint64_t t) {
+std::vector<uint8_t> spiking_vector(const System& sys, const RuleSets& A, uint64_t t) {
   std::vector<uint8_t> S(sys.n, 0);
   for (int64_t s = sys.m - 1; s >= 0; --s) {  // least significant digit last
     if (A[s].empty()) continue;
@@ -536,7 +569,7 @@ int oracle_explore_gen(const oracle_system* h, int64_t F0, const int32_t* level0
     const std::vector<int64_t> C(run.configs[i].begin(), run.configs[i].begin() + s.m);
     auto A = applicable_rules_per_neuron(s, C);
     bool any = false;
-    for (const auto& As : A) any = any || !As.empty();
+    for (int64_t q = 0; q < (int64_t)A.size(); ++q) any = any || !A[q].empty();
     run.halting[i] = any ? 0 : 1;
   }
   return OR_OK;
@@ -613,12 +646,13 @@ int oracle_sample(const oracle_system* h, int64_t W, int32_t* configs, uint64_t 
 // neuron is closed.  With no applicable rule but a closed neuron the state has
 // exactly one child (nobody fires, the clocks run).  With every d = 0 this is
 // eq. (2) on the first m columns and τ = π = 0 throughout.
-std::vector<std::vector<int64_t>> applicable_open(const System& sys, const std::vector<int64_t>& X) {
-  std::vector<std::vector<int64_t>> A(sys.m);
+RuleSets applicable_open(const System& sys, const std::vector<int64_t>& X) {
+  RuleSets A(sys.m);
   for (int64_t r = 0; r < sys.n; ++r) {
     const int64_t sgm = sys.rules[r].neuron;
-    if (X[sys.m + sgm] == 0 && applicable(sys.rules[r], X)) A[sgm].push_back(r);
+    if (X[sys.m + sgm] == 0 && applicable(sys.rules[r], X)) A.add(sgm, r);
   }
+  A.finish();
   return A;
 }
 
@@ -719,7 +753,7 @@ int oracle_explore_delay(const oracle_system* h, const int32_t* delay32, int64_t
     run.fp0.push_back(f.first);
     run.fp1.push_back(f.second);
   };
-  auto children_count = [&](const std::vector<int64_t>& X, std::vector<std::vector<int64_t>>* A, uint64_t* psi) {
+  auto children_count = [&](const std::vector<int64_t>& X, RuleSets* A, uint64_t* psi) {
     *A = applicable_open(s, X);
     if (!count_children(*A, psi)) return false;
     bool closed = false;
@@ -748,7 +782,7 @@ int oracle_explore_delay(const oracle_system* h, const int32_t* delay32, int64_t
     int64_t T = 0;
     for (int64_t i = lo; i < hi; ++i) {
       const std::vector<int64_t> X = run.configs[i];
-      std::vector<std::vector<int64_t>> A;
+      RuleSets A;
       uint64_t psi = 0;
       if (!children_count(X, &A, &psi)) { run.status = OR_E_CAPACITY; run.error = "psi above 2^62"; return run.status; }
       for (uint64_t t = 0; t < psi; ++t) {
@@ -782,7 +816,7 @@ int oracle_explore_delay(const oracle_system* h, const int32_t* delay32, int64_t
   }
   run.halting.resize(run.configs.size());
   for (size_t i = 0; i < run.configs.size(); ++i) {
-    std::vector<std::vector<int64_t>> A;
+    RuleSets A;
     uint64_t psi = 0;
     children_count(run.configs[i], &A, &psi);
     run.halting[i] = psi == 0 ? 1 : 0;
@@ -857,7 +891,9 @@ struct ParRun {
   std::string error;
   int64_t m = 0;
   int64_t w = 4;                       // bytes per stored count: 1 / 2 / 4 for count_bits 8 / 16 / 32
-  std::vector<uint8_t> arena;          // stored configurations, m counts of w bytes each, discovery order
+  static constexpr int64_t CPB = 4096;  // configurations per arena chunk
+  std::vector<std::vector<uint8_t>> arena;  // stored configurations, m counts of w bytes each, discovery order
+  int64_t stored = 0;
   std::vector<int64_t> level_offsets;
   std::vector<int64_t> parent;
   std::vector<uint64_t> t, fp0, fp1;
@@ -865,16 +901,33 @@ struct ParRun {
   std::vector<int64_t> level_T, level_new, level_kept;
   // count j of stored configuration i (every stored count is in [0, 2^(8w) - 1], reading A16)
   int64_t at(int64_t i, int64_t j) const {
-    const uint8_t* p = arena.data() + ((size_t)i * (size_t)m + (size_t)j) * (size_t)w;
+    const uint8_t* p = arena[(size_t)(i / CPB)].data() + ((size_t)(i % CPB) * (size_t)m + (size_t)j) * (size_t)w;
     if (w == 1) return p[0];
     if (w == 2) return (int64_t)p[0] | ((int64_t)p[1] << 8);
     int32_t v;
     memcpy(&v, p, 4);
     return v;
   }
+  // chunks for configurations [0, n)
+  void reserve(int64_t n) {
+    while ((int64_t)arena.size() * CPB < n) arena.emplace_back((size_t)(CPB * m * w));
+  }
+  // the counts of configuration i (its chunk reserved)
+  void put(int64_t i, const std::vector<int64_t>& C) {
+    uint8_t* p = arena[(size_t)(i / CPB)].data() + (size_t)(i % CPB) * (size_t)(m * w);
+    for (size_t j = 0; j < C.size(); ++j)
+      for (int64_t b = 0; b < w; ++b) p[j * w + b] = (uint8_t)((uint64_t)C[j] >> (8 * b));
+  }
   void append(const std::vector<int64_t>& C) {
-    for (int64_t v : C)
-      for (int64_t b = 0; b < w; ++b) arena.push_back((uint8_t)((uint64_t)v >> (8 * b)));
+    reserve(stored + 1);
+    uint8_t* p = arena[(size_t)(stored / CPB)].data() + (size_t)(stored % CPB) * (size_t)(m * w);
+    ++stored;
+    for (size_t j = 0; j < C.size(); ++j)
+      for (int64_t b = 0; b < w; ++b) p[j * w + b] = (uint8_t)((uint64_t)C[j] >> (8 * b));
+  }
+  void row(int64_t i, std::vector<int64_t>& r) const {
+    r.resize((size_t)m);
+    for (int64_t j = 0; j < m; ++j) r[j] = at(i, j);
   }
 };
 
@@ -949,8 +1002,8 @@ int oracle_explore_par(const oracle_system* h, int64_t F0, const int32_t* level0
     visited.emplace(f.first, idx);
   };
   auto row_of = [&](int64_t i) {
-    std::vector<int64_t> r(m);
-    for (int64_t j = 0; j < m; ++j) r[j] = run.at(i, j);
+    std::vector<int64_t> r;
+    run.row(i, r);
     return r;
   };
   // Level 0 (reading A20)
@@ -968,16 +1021,8 @@ int oracle_explore_par(const oracle_system* h, int64_t F0, const int32_t* level0
     const int64_t lo = run.level_offsets[L], hi = run.level_offsets[L + 1];
     if (lo == hi) break;
     const int64_t F = hi - lo;
-    // applicable rules and Ψ of every parent (eq. (8), readings A3-A5)
-    std::vector<uint64_t> psi(F, 0);
-    std::vector<char> cap_err(F, 0);
-    parallel_for(0, F, n_threads, [&](int64_t i) {
-      auto A = applicable_rules_per_neuron(s, row_of(lo + i));
-      if (!count_children(A, &psi[i])) cap_err[i] = 1;
-    });
-    for (int64_t i = 0; i < F; ++i)
-      if (cap_err[i]) { run.status = OR_E_CAPACITY; run.error = "psi above 2^62"; return run.status; }
-    struct Cand { int64_t parent; uint64_t t; std::pair<uint64_t, uint64_t> f; };
+    std::vector<uint64_t> psi_of(F, 0);
+    struct Cand { int64_t parent; uint64_t t; std::pair<uint64_t, uint64_t> f; const int64_t* row; };
     std::vector<Cand> fresh;
     std::unordered_multimap<uint64_t, int64_t> level_keys;  // fp0 -> index in fresh
     auto child_row = [&](int64_t parent_in_level, uint64_t t) {
@@ -986,87 +1031,112 @@ int oracle_explore_par(const oracle_system* h, int64_t F0, const int32_t* level0
       return transition(s, C, spiking_vector(s, A, t));
     };
     int64_t T = 0;
-    // parents in chunks whose children fit a bounded buffer
-    const uint64_t budget = (uint64_t)1 << 22;  // children per chunk (their fingerprints are held)
-    for (int64_t c0 = 0; c0 < F;) {
-      int64_t c1 = c0;
-      uint64_t nch = 0;
-      while (c1 < F && (c1 == c0 || nch + psi[c1] <= budget)) nch += psi[c1++];
-      std::vector<uint64_t> base(c1 - c0 + 1, 0);
-      for (int64_t i = c0; i < c1; ++i) base[i - c0 + 1] = base[i - c0] + psi[i];
-      std::vector<std::pair<uint64_t, uint64_t>> fps(nch);
-      parallel_for(c0, c1, n_threads, [&](int64_t i) {
-        const std::vector<int64_t> C = row_of(lo + i);
-        auto A = applicable_rules_per_neuron(s, C);
-        for (uint64_t t = 0; t < psi[i]; ++t) {
-          auto Cn = transition(s, C, spiking_vector(s, A, t));
-          fps[base[i - c0] + t] = fingerprint_of(Cn);
-        }
-      });
-      // canonical order: parents in order, t increasing (reading A7)
-      for (int64_t i = c0; i < c1; ++i) {
-        for (uint64_t t = 0; t < psi[i]; ++t) {
-          ++T;
-          if (max_transitions > 0 && T > max_transitions) { run.status = OR_E_CAPACITY; run.error = "transition budget exceeded"; return run.status; }
-          const auto& f = fps[base[i - c0] + t];
-          std::vector<int64_t> Cn;  // this child's row, recomputed only for a dedup = 0 comparison
-          auto cn = [&]() {
-            if (Cn.empty()) Cn = child_row(i, t);
-            return Cn;
-          };
-          if (seen(f, cn)) continue;  // produced at an earlier level (A6)
-          bool dup = false;
-          auto rg = level_keys.equal_range(f.first);
-          for (auto it = rg.first; it != rg.second && !dup; ++it) {
-            const Cand& o = fresh[it->second];
-            dup = dedup == 1 ? o.f.second == f.second : child_row(o.parent, o.t) == cn();
+    // parents in chunks; a chunk is split into n_threads contiguous ranges,
+    // each producing, parent by parent, Ψ (eq. (8), readings A3-A5) and the
+    // children's fingerprints — plus their rows for dedup = 0, which the
+    // merge compares exactly — in canonical order (parents, then t, A7)
+    const int64_t chunk = std::max<int64_t>(n_threads, dedup == 0 ? ((int64_t)1 << 23) / m : (int64_t)1 << 16);
+    for (int64_t c0 = 0; c0 < F; c0 += chunk) {
+      const int64_t c1 = std::min<int64_t>(F, c0 + chunk);
+      struct Part {
+        std::vector<std::pair<uint64_t, uint64_t>> fps;
+        std::vector<int64_t> rows;
+        bool cap = false;
+      };
+      const int nparts = (int)std::min<int64_t>(n_threads, c1 - c0);
+      std::vector<Part> parts(nparts);
+      std::vector<std::thread> th;
+      for (int k = 0; k < nparts; ++k) {
+        const int64_t a = c0 + (c1 - c0) * k / nparts, b = c0 + (c1 - c0) * (k + 1) / nparts;
+        th.emplace_back([&, a, b, k]() {
+          Part& P = parts[k];
+          for (int64_t i = a; i < b; ++i) {
+            const std::vector<int64_t> C = row_of(lo + i);
+            auto A = applicable_rules_per_neuron(s, C);
+            if (!count_children(A, &psi_of[i])) { P.cap = true; return; }
+            for (uint64_t t = 0; t < psi_of[i]; ++t) {
+              auto Cn = transition(s, C, spiking_vector(s, A, t));
+              P.fps.push_back(fingerprint_of(Cn));
+              if (dedup == 0) P.rows.insert(P.rows.end(), Cn.begin(), Cn.end());
+            }
           }
-          if (dup) continue;  // same-level duplicate: first (minimum) tag wins
-          level_keys.emplace(f.first, (int64_t)fresh.size());
-          fresh.push_back(Cand{i, t, f});
+        });
+      }
+      for (auto& x : th) x.join();
+      for (const Part& P : parts)
+        if (P.cap) { run.status = OR_E_CAPACITY; run.error = "psi above 2^62"; return run.status; }
+      const size_t fresh_chunk0 = fresh.size();  // rows of fresh[fresh_chunk0..] live in `parts`
+      for (int k = 0; k < nparts; ++k) {
+        const int64_t a = c0 + (c1 - c0) * k / nparts, b = c0 + (c1 - c0) * (k + 1) / nparts;
+        size_t pos = 0;
+        for (int64_t i = a; i < b; ++i) {
+          for (uint64_t t = 0; t < psi_of[i]; ++t, ++pos) {
+            ++T;
+            if (max_transitions > 0 && T > max_transitions) { run.status = OR_E_CAPACITY; run.error = "transition budget exceeded"; return run.status; }
+            const auto& f = parts[k].fps[pos];
+            const int64_t* crow = dedup == 0 ? parts[k].rows.data() + pos * (size_t)m : nullptr;
+            auto cn = [&]() { return std::vector<int64_t>(crow, crow + m); };
+            if (seen(f, cn)) continue;  // produced at an earlier level (A6)
+            bool dup = false;
+            auto rg = level_keys.equal_range(f.first);
+            for (auto it = rg.first; it != rg.second && !dup; ++it) {
+              const Cand& o = fresh[it->second];
+              if (dedup == 1) dup = o.f.second == f.second;
+              else if ((size_t)it->second >= fresh_chunk0) dup = std::equal(crow, crow + m, o.row);
+              else dup = child_row(o.parent, o.t) == cn();
+            }
+            if (dup) continue;  // same-level duplicate: first (minimum) tag wins
+            level_keys.emplace(f.first, (int64_t)fresh.size());
+            fresh.push_back(Cand{i, t, f, crow});
+          }
         }
       }
-      c0 = c1;
     }
+    // halting flags of this level (reading A5: halting <=> Ψ = 0)
+    for (int64_t i = 0; i < F; ++i) run.halting.push_back(psi_of[i] == 0 ? 1 : 0);
     const int64_t n_new = (int64_t)fresh.size();
     const bool thin = frontier_target > 0 && n_new > frontier_target;
     const uint64_t tau = thin ? oracle_thinning_tau(frontier_target, n_new) : 0;
     std::vector<int64_t> keep;
     for (int64_t ci = 0; ci < n_new; ++ci)
       if (!thin || fmix64(fresh[ci].f.first) < tau) keep.push_back(ci);  // reading A19
-    // kept rows recomputed in parallel, then stored in tag order
-    std::vector<int64_t> krows;
+    // kept rows recomputed in parallel straight into their arena slots (the
+    // next indices, tag order), then recorded in tag order; the first
+    // out-of-range kept row (in tag order) is the overflow (reading A16)
     std::vector<char> bad(keep.size(), 0);
-    const size_t KB = (size_t)1 << 16;
-    for (size_t k0 = 0; k0 < keep.size(); k0 += KB) {
-      const size_t k1 = std::min(keep.size(), k0 + KB);
-      krows.assign((k1 - k0) * (size_t)m, 0);
-      parallel_for((int64_t)k0, (int64_t)k1, n_threads, [&](int64_t k) {
-        const Cand& c = fresh[keep[k]];
-        auto Cn = child_row(c.parent, c.t);
-        for (int64_t v : Cn) bad[k] |= (v < 0 ? 1 : v > cmax ? 2 : 0);
-        std::copy(Cn.begin(), Cn.end(), krows.begin() + (size_t)(k - k0) * m);
-      });
-      for (size_t k = k0; k < k1; ++k) {
-        if (bad[k]) { run.status = OR_E_OVERFLOW; run.error = (bad[k] & 1) ? "negative count" : "count above storage range"; return run.status; }
-        const Cand& c = fresh[keep[k]];
-        std::vector<int64_t> Cn(krows.begin() + (k - k0) * m, krows.begin() + (k - k0 + 1) * m);
-        push(Cn, c.f, c.parent, c.t);
-      }
+    const int64_t first = run.stored;
+    run.reserve(first + (int64_t)keep.size());
+    parallel_for(0, (int64_t)keep.size(), n_threads, [&](int64_t k) {
+      const Cand& c = fresh[keep[k]];
+      auto Cn = child_row(c.parent, c.t);
+      for (int64_t v : Cn) bad[k] |= (v < 0 ? 1 : v > cmax ? 2 : 0);
+      if (!bad[k]) run.put(first + k, Cn);
+    });
+    for (size_t k = 0; k < keep.size(); ++k) {
+      if (bad[k]) { run.status = OR_E_OVERFLOW; run.error = (bad[k] & 1) ? "negative count" : "count above storage range"; return run.status; }
+      const Cand& c = fresh[keep[k]];
+      run.parent.push_back(c.parent);
+      run.t.push_back(c.t);
+      run.fp0.push_back(c.f.first);
+      run.fp1.push_back(c.f.second);
+      visited.emplace(c.f.first, first + (int64_t)k);
     }
+    run.stored = first + (int64_t)keep.size();
     run.level_T.push_back(T);
     run.level_new.push_back(n_new);
     run.level_kept.push_back((int64_t)keep.size());
     run.level_offsets.push_back((int64_t)run.parent.size());
     if (keep.empty()) break;
   }
-  // halting classification of every configuration (reading A5)
+  // halting classification (reading A5) of the configurations of the levels
+  // that were not expanded (the expanded ones got Ψ = 0 above)
   const int64_t N = (int64_t)run.parent.size();
-  run.halting.assign(N, 0);
-  parallel_for(0, N, n_threads, [&](int64_t i) {
+  const int64_t classified = (int64_t)run.halting.size();
+  run.halting.resize(N, 0);
+  parallel_for(classified, N, n_threads, [&](int64_t i) {
     auto A = applicable_rules_per_neuron(s, row_of(i));
     bool any = false;
-    for (const auto& As : A) any = any || !As.empty();
+    for (int64_t q = 0; q < (int64_t)A.size(); ++q) any = any || !A[q].empty();
     run.halting[i] = any ? 0 : 1;
   });
   return OR_OK;

@@ -22,7 +22,6 @@
 namespace snp {
 
 constexpr int64_t TC_M_MAX = 1 << 19;        // k_expand_tc: s32 accumulators exact up to this m
-constexpr int KC_PERM_CHUNK = 1024;         // K-c: neurons per CTA iteration (32 warps × 32 lanes)
 constexpr int KMAX = 64;                    // nondeterministic neurons recorded per parent
 constexpr int PB = 64;                      // configurations per storage block
 constexpr uint64_t PSI_LIMIT = 1ULL << 62;  // Ψ above this is SNP_E_CAPACITY
@@ -109,15 +108,10 @@ struct SysView {
   const uint64_t* h1;
   const int32_t* in_off;     // m + 1
   const int32_t* in_src;     // sources s with (s, j) ∈ syn, grouped by target j
-  // K-c lane order: position i of a chunk of KC_PERM_CHUNK consecutive
-  // neurons handles neuron kc_perm[i] of that chunk, the chunk's neurons
-  // sorted by in-degree, so the 32 targets of a warp have similar in-degrees
-  // and the padded gather below does little padding work
-  const int32_t* kc_perm;    // m
-  // the same in-synapses "edge-major" per group of 32 consecutive positions:
+  // the same in-synapses "edge-major" per group of 32 consecutive targets:
   // group g holds in_pad_off[g+1] - in_pad_off[g] rows of 32 sources (row e,
-  // lane l = e-th in-synapse of target kc_perm[32g + l]), padded with the
-  // index m_even (a zero word)
+  // lane l = e-th in-synapse of target 32g + l), padded with the index m_even
+  // (a zero word)
   const int32_t* in_pad;
   const uint16_t* in_pad16;    // the same as uint16 when m < 65535 (else null)
   const int64_t* in_pad_off;   // m/32 + 1 row offsets (×32 entries)

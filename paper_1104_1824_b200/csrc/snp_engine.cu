@@ -194,7 +194,7 @@ struct snp_system {
   bool binary_emit = true;
   bool small_rules = true;  // every c, p <= 255 (k_sample_cta)
   // ---- device system
-  DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1, d_in_pad, d_in_pad16, d_in_pad_off, d_kc_perm;
+  DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1, d_in_pad, d_in_pad16, d_in_pad_off;
   SysView view{};
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -626,36 +626,21 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   SNP_TRY(upload(s, s->d_h1, h1));
   SNP_TRY(upload(s, s->d_in_off, in_off));
   SNP_TRY(upload(s, s->d_in_src, in_src));
-  // K-c lane order: within each chunk of KC_PERM_CHUNK neurons, sorted by
-  // in-degree (stable), then the edge-major padded in-CSR per group of 32
-  // positions (coalesced K-c gathers, padding = the group's max in-degree)
-  std::vector<int32_t> kc_perm(m);
-  for (int64_t c = 0; c < m; c += KC_PERM_CHUNK) {
-    const int64_t e = std::min<int64_t>(m, c + KC_PERM_CHUNK);
-    for (int64_t j = c; j < e; ++j) kc_perm[j] = (int32_t)j;
-    std::stable_sort(kc_perm.begin() + c, kc_perm.begin() + e,
-                     [&](int32_t a, int32_t b) { return in_off[a + 1] - in_off[a] < in_off[b + 1] - in_off[b]; });
-  }
-  SNP_TRY(upload(s, s->d_kc_perm, kc_perm));
+  // edge-major padded in-CSR per group of 32 targets (coalesced K-c gathers)
   {
     const int64_t ng = (m + 31) / 32;
     const int32_t pad = (int32_t)((m + 1) & ~1);  // index of the zero emit word
     std::vector<int64_t> pad_off(ng + 1, 0);
     for (int64_t g = 0; g < ng; ++g) {
       int32_t mx = 0;
-      for (int64_t i = 32 * g; i < std::min<int64_t>(m, 32 * g + 32); ++i) {
-        const int32_t j = kc_perm[i];
-        mx = std::max(mx, in_off[j + 1] - in_off[j]);
-      }
+      for (int64_t j = 32 * g; j < std::min<int64_t>(m, 32 * g + 32); ++j) mx = std::max(mx, in_off[j + 1] - in_off[j]);
       pad_off[g + 1] = pad_off[g] + (mx + 3) / 4 * 4;  // K-c consumes rows in blocks of 8 and 4
     }
     std::vector<int32_t> in_pad((size_t)pad_off[ng] * 32, pad);
     for (int64_t g = 0; g < ng; ++g)
-      for (int64_t i = 32 * g; i < std::min<int64_t>(m, 32 * g + 32); ++i) {
-        const int32_t j = kc_perm[i];
+      for (int64_t j = 32 * g; j < std::min<int64_t>(m, 32 * g + 32); ++j)
         for (int32_t e = in_off[j]; e < in_off[j + 1]; ++e)
-          in_pad[(size_t)(pad_off[g] + (e - in_off[j])) * 32 + (i - 32 * g)] = in_src[e];
-      }
+          in_pad[(size_t)(pad_off[g] + (e - in_off[j])) * 32 + (j - 32 * g)] = in_src[e];
     SNP_TRY(upload(s, s->d_in_pad, in_pad));
     if (m < 65535) {
       std::vector<uint16_t> in16(in_pad.begin(), in_pad.end());
@@ -752,7 +737,6 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.h1 = s->d_h1.as<uint64_t>();
   v.in_off = s->d_in_off.as<int32_t>();
   v.in_src = s->d_in_src.as<int32_t>();
-  v.kc_perm = s->d_kc_perm.as<int32_t>();
   v.in_pad = s->d_in_pad.as<int32_t>();
   v.in_pad16 = m < 65535 ? s->d_in_pad16.as<uint16_t>() : nullptr;
   v.in_pad_off = s->d_in_pad_off.as<int64_t>();

@@ -1481,10 +1481,11 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 // before the gather (SNP_KC_PREFETCH=1: 68.6 ms; 64.2 vs 63.7 with the L2 row prefetch on) or one iteration ahead
 // (77 ms, spills) loses to loading it where it is used (66.5 ms)
 #ifndef SNP_KC_COOP
-#define SNP_KC_COOP 4  // warp-cooperative stores: 4 lane = output quad over all rows (descriptor decoded once per
-                       // lane); 1 full quads per 64-child output row (half-warps); 2 the flat (row, quad) list,
-                       // 3 the same with the partial end quads (measured slower: 68.7 vs 60.6 ms for 1);
-                       // 0 the per-lane store program
+#define SNP_KC_COOP 1  // warp-cooperative stores of the full 4-child quads (else the per-lane store program).
+                       // Measured and rejected in round 2 (config 4, K-c ms): a flat (row, quad) lane list
+                       // 68.7 vs 60.6; lane = output quad over all rows 64.3 vs 62.3, with the partial end
+                       // quads folded in 87.2; in-degree-sorted lane order (padding 15.9 -> 9.8 gather rows
+                       // per lane, but each warp's 32 row loads scattered over 64 KB) +23 ms
 #endif
 #ifndef SNP_KC_L2PF
 #define SNP_KC_L2PF 1  // k > 0: L2 bulk prefetch of the warp's parent rows k - 1 iterations ahead (rolled halves: 0 64.2 ms, 1 64.0, 2 63.7, 3 63.9; unrolled: 1 60.8, 2 61.3)
@@ -1505,15 +1506,6 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #endif
 #ifndef SNP_KC_PREFETCH
 #define SNP_KC_PREFETCH 0
-#endif
-#ifndef SNP_KC_PERM
-#define SNP_KC_PERM 1  // lanes follow SysView::kc_perm (in-degree order within each 1024-neuron chunk)
-#endif
-#ifndef SNP_KC_EDGEQ
-#define SNP_KC_EDGEQ 1  // SNP_KC_COOP 4: the partial end quads in the cooperative loop (else the per-lane edge stores)
-#endif
-#if SNP_KC_PERM && SNP_KC_COOP < 2
-#error "SNP_KC_PERM needs the flat cooperative stores (SNP_KC_COOP >= 2)"
 #endif
 constexpr int MW = SNP_KC_WARPS;  // warps per K-c CTA
 constexpr int QCAP = 4064;   // outputs per block resolved through the r(q) table (+32 alignment slack)
@@ -1689,16 +1681,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       }
     }
 #endif
-#if SNP_KC_PERM
-    // positions jbase + lane are in-degree sorted within chunks of
-    // KC_PERM_CHUNK neurons (= one CTA iteration at 32 warps)
-    const int32_t j = jbase + lane < m ? __ldg(S.kc_perm + jbase + lane) : jbase + lane;
-#else
     const int32_t j = jbase + lane;
-#endif
-#if SNP_KC_COOP >= 2
-    reinterpret_cast<int32_t*>(sOps)[warp * 32 + lane] = j;  // row r of the warp's stores = neuron sJ[r]
-#endif
     if (j < m) {
     const T* row = data + eidx(pb0, j, m);
 #if SNP_KC_PREFETCH
@@ -1887,12 +1870,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       if (slot < ovf_cap) ovf[slot] = ((uint64_t)(uint32_t)j << 32) | (uint64_t)(pb0 + r);
     }
     // ---- write x to every kept child of the block's parents (row j of the output)
-#if SNP_KC_COOP == 3 || (SNP_KC_COOP == 4 && SNP_KC_EDGEQ)
-    if (prog) {
-      // every quad, partial ones at the ends included, is written by the
-      // warp-cooperative loop below
-    } else
-#elif SNP_KC_COOP
+#if SNP_KC_COOP
     if (prog) {
       // bytes of [Q0, Q1) whose 4-child quad is not inside the range (<= 3
       // at each end): lane = row, one byte store per position for all rows
@@ -1978,173 +1956,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
         for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = xs[r];
     }
     }  // j < m
-#if SNP_KC_COOP == 4
-    if (prog) {
-      // warp-cooperative stores, lane = output quad: each lane decodes its
-      // quad's descriptor once and writes that quad for every row of the
-      // warp; <= 16 quads: half-warps take alternate rows (each 4-byte store
-      // instruction fills two 64-child row segments), else all 32 lanes one
-      // row.  SNP_KC_EDGEQ: the partial quads at the two ends of [Q0, Q1)
-      // too (their bytes inside the range by <= 3 narrow stores)
-      __syncwarp();
-#if SNP_KC_EDGEQ
-      const uint64_t qa = Q0 & ~3ULL, qb = (Q1 + 3) & ~3ULL;
-#else
-      const uint64_t qa = (Q0 + 3) & ~3ULL, qb = Q1 & ~3ULL;
-#endif
-      const int32_t jn = m - jbase;  // rows of this warp that exist
-      if (!(SNP_KC_ABLATE & 4) && qa < qb) {
-        const uint32_t nq = (uint32_t)((qb - qa) >> 2);
-        const bool halves = nq <= 16;  // CTA-uniform
-        const uint32_t lanes = halves ? 16u : 32u, rstep = halves ? 2u : 1u;
-        const uint32_t r0 = halves ? (uint32_t)(lane >> 4) : 0u;
-        const uint32_t nrow = jn < 32 ? (uint32_t)jn : 32u;
-        const uint64_t mrow = (uint64_t)m << 6;
-#if SNP_KC_PERM
-        const int32_t* sJ = reinterpret_cast<const int32_t*>(sOps) + warp * 32;
-#endif
-        uint8_t* obase = reinterpret_cast<uint8_t*>(out);
-        const uint8_t* xw = sX + (size_t)(warp * 32) * xs_stride<T>();
-        for (uint32_t k = halves ? (uint32_t)(lane & 15) : (uint32_t)lane; k < nq; k += lanes) {
-          const uint64_t q = qa + 4 * (uint64_t)k;
-          const uint32_t d = sD[(q - Qb) >> 2];
-          const bool direct = !(d & 0x80000000u);
-          const uint32_t woff = 4 * ((d >> 16) & 31), sel = d & 0xFFFFu, hb = d >> 24;
-          const uint32_t mask = (hb * 0x00204081u & 0x01010101u) * 0xFFu;
-          uint32_t rr = direct ? 0u : *reinterpret_cast<const uint32_t*>(sR + (q - Qb));
-#if SNP_KC_EDGEQ
-          const uint32_t ea = q >= Q0 ? 0u : (uint32_t)(Q0 - q), eb = q + 4 <= Q1 ? 4u : (uint32_t)(Q1 - q);
-          if (!direct) rr &= (0xFFFFFFFFu << (8 * ea)) & (0xFFFFFFFFu >> (8 * (4 - eb)));  // no parent: byte 0
-          const bool full = ea == 0 && eb == 4;
-#endif
-          uint8_t* dk = obase + (q >> 6) * mrow + (q & 63);
-#pragma unroll 4
-          for (uint32_t r = r0; r < nrow; r += rstep) {
-            const uint8_t* xr = xw + (size_t)r * xs_stride<T>();
-            uint32_t v;
-            if (direct) {
-              const uint32_t* w = reinterpret_cast<const uint32_t*>(xr + woff);
-              v = prmt(w[0], w[1], sel);
-              if (hb) v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
-            } else {
-              v = (uint32_t)xr[rr & 0xFF] | ((uint32_t)xr[(rr >> 8) & 0xFF] << 8) |
-                  ((uint32_t)xr[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xr[rr >> 24] << 24);
-            }
-#if SNP_KC_PERM
-            uint8_t* dq = dk + ((uint64_t)sJ[r] << 6);
-#else
-            uint8_t* dq = dk + ((uint64_t)(jbase + r) << 6);
-#endif
-#if SNP_KC_EDGEQ
-            if (full) {
-              *reinterpret_cast<uint32_t*>(dq) = v;
-            } else {
-              uint32_t a = ea;
-              v >>= 8 * a;
-              if ((a & 1) && a < eb) {
-                dq[a] = (uint8_t)v;
-                v >>= 8;
-                ++a;
-              }
-              if (a + 2 <= eb) {
-                *reinterpret_cast<uint16_t*>(dq + a) = (uint16_t)v;
-                v >>= 16;
-                a += 2;
-              }
-              if (a < eb) dq[a] = (uint8_t)v;
-            }
-#else
-            *reinterpret_cast<uint32_t*>(dq) = v;
-#endif
-          }
-        }
-      }
-      __syncwarp();
-    }
-#elif SNP_KC_COOP == 2 || SNP_KC_COOP == 3
-    if (prog) {
-      // full 4-child quads, warp-cooperative over the flat list of (row,
-      // quad) pairs of this warp: lane i takes pairs i, i + 32, ... (row =
-      // one of the warp's 32 neurons, quad = one of the CTA's nq full output
-      // quads), so every lane stores on every iteration; a byte permute of
-      // the neuron's x row when the 4 parents lie in a 16-byte window, else 4
-      // byte loads
-      __syncwarp();
-#if SNP_KC_COOP == 3
-      // every quad touching [Q0, Q1): the partial ones at the two ends store
-      // only their bytes inside the range (<= 3 narrow stores)
-      const uint64_t qa = Q0 & ~3ULL, qb = (Q1 + 3) & ~3ULL;
-#else
-      const uint64_t qa = (Q0 + 3) & ~3ULL, qb = Q1 & ~3ULL;
-#endif
-      const int32_t jn = m - jbase;  // rows of this warp that exist
-      if (!(SNP_KC_ABLATE & 4) && qa < qb) {
-        const uint32_t nq = (uint32_t)((qb - qa) >> 2);
-        const uint32_t nrow = jn < 32 ? (uint32_t)jn : 32u;
-        const uint32_t total = nq * nrow;
-        const uint32_t dr = 32u / nq, dk = 32u % nq;   // step of (row, quad) per 32 pairs
-        uint32_t r = (uint32_t)lane / nq, k = (uint32_t)lane % nq;
-        const uint64_t qoff = (qa - Qb) >> 2;
-        const uint64_t mrow = (uint64_t)m << 6;       // output-block stride in bytes
-        const int32_t* sJ = reinterpret_cast<const int32_t*>(sOps) + warp * 32;
-        uint8_t* obase = reinterpret_cast<uint8_t*>(out);
-        for (uint32_t idx = lane; idx < total; idx += 32) {
-          const uint64_t q = qa + 4 * (uint64_t)k;
-          const uint32_t d = sD[qoff + k];
-          const uint8_t* xr = sX + (size_t)(warp * 32 + r) * xs_stride<T>();
-          uint32_t v;
-          if (!(d & 0x80000000u)) {
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(xr) + ((d >> 16) & 31);
-            const uint32_t sel = d & 0xFFFFu, hb = d >> 24;
-            v = prmt(w[0], w[1], sel);
-            if (hb) {
-              const uint32_t mask = (hb * 0x00204081u & 0x01010101u) * 0xFFu;
-              v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
-            }
-          } else {
-            uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (q - Qb));
-#if SNP_KC_COOP == 3
-            // children outside [Q0, Q1) have no parent entry: read byte 0 instead
-            const uint32_t lo_ok = q >= Q0 ? 0xFFFFFFFFu : (0xFFFFFFFFu << (8 * (uint32_t)(Q0 - q)));
-            const uint32_t hi_ok = q + 4 <= Q1 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (8 * (uint32_t)(q + 4 - Q1)));
-            rr &= lo_ok & hi_ok;
-#endif
-            v = (uint32_t)xr[rr & 0xFF] | ((uint32_t)xr[(rr >> 8) & 0xFF] << 8) |
-                ((uint32_t)xr[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xr[rr >> 24] << 24);
-          }
-          uint8_t* dq = obase + (q >> 6) * mrow + ((uint64_t)sJ[r] << 6) + (q & 63);
-#if SNP_KC_COOP == 3
-          if (q >= Q0 && q + 4 <= Q1) {
-            *reinterpret_cast<uint32_t*>(dq) = v;
-          } else {  // partial quad: bytes [a, b) of it
-            uint32_t a = q >= Q0 ? 0u : (uint32_t)(Q0 - q), b = q + 4 <= Q1 ? 4u : (uint32_t)(Q1 - q);
-            v >>= 8 * a;
-            if ((a & 1) && a < b) {
-              dq[a] = (uint8_t)v;
-              v >>= 8;
-              ++a;
-            }
-            if (a + 2 <= b) {
-              *reinterpret_cast<uint16_t*>(dq + a) = (uint16_t)v;
-              v >>= 16;
-              a += 2;
-            }
-            if (a < b) dq[a] = (uint8_t)v;
-          }
-#else
-          *reinterpret_cast<uint32_t*>(dq) = v;
-#endif
-          k += dk;
-          r += dr;
-          if (k >= nq) {
-            k -= nq;
-            ++r;
-          }
-        }
-      }
-      __syncwarp();
-    }
-#elif SNP_KC_COOP
+#if SNP_KC_COOP
     if (prog) {
       // full 4-child quads, warp-cooperative: a half-warp covers one 64-child
       // output row (lane = quad; a byte permute of the neuron's x row when
