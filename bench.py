@@ -384,7 +384,16 @@ def run_e2e(args, cfg, w, snp, torch, rank=0, world=1, dist=None):
         snp.generate_level0_device(w, n, cfg["seed"], tmp.data_ptr(), wb, snp.SNP_LAYOUT_ROW_MAJOR, m, 0,
                                    row_begin=lo + r0)
         host[r0:r0 + n].copy_(tmp[:n])
-    del tmp
+    # this box's pinned host -> device copy rate (context for the e2e number: level 0 is H2D-bound)
+    nb = min(Fl, max(1, (4 << 30) // (m * wb)))
+    probe = torch.empty((nb, m), dtype=dt, device="cuda")
+    probe.copy_(host[:nb], non_blocking=True)
+    torch.cuda.synchronize()
+    tp = time.perf_counter()
+    probe.copy_(host[:nb], non_blocking=True)
+    torch.cuda.synchronize()
+    box_h2d = nb * m * wb / (time.perf_counter() - tp) / 1e9
+    del tmp, probe
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     eng = snp.System(w, count_bits=cfg["count_bits"], dedup=cfg["dedup"], frontier_target=cfg["frontier_target"],
@@ -425,7 +434,8 @@ def run_e2e(args, cfg, w, snp, torch, rank=0, world=1, dist=None):
             "d2h_bytes_per_step": d2h // args.steps,
             "breakdown_s": {"begin (level-0 H2D + import + dedup)": round(t_begin, 4), "advance": round(t_adv, 4),
                             "edges D2H": round(t_edges, 4), "total": round(dt_s, 4),
-                            "h2d_GBps_through_begin": round(Fl * m * wb / t_begin / 1e9, 2)},
+                            "h2d_GBps_through_begin": round(Fl * m * wb / t_begin / 1e9, 2),
+                            "box_pinned_h2d_GBps (torch copy, 4 GB)": round(box_h2d, 2)},
             "note": ("snp_begin" if world == 1 else f"snp_dist_start ({world} ranks, one host slice each)") +
                     "(pinned host row-major level 0) + K x (advance + snp_level_edges D2H into pinned buffers); "
                     "wall clock around synchronous ABI calls" + (", max over ranks" if world > 1 else "")}

@@ -128,7 +128,7 @@ struct SysView {
   const uint8_t* tab;        // m × tabw   (compact)
   const uint8_t* tab_full;   // m × 256    (count_bits == 8)
   const void* ctab;          // m × tabw   consumption of the first rule, storage type
-  const uint8_t* ttab;       // m × 256    (count_bits == 8) v - c_first(v) for every count v
+  const uint8_t* ttab;       // (count_bits == 8) v - c_first(v): m × 32 for v < 32, then m × 256 for every v
   const uint8_t* elut;       // m × 32     (count_bits == 8) outcome entries for v < 32
   const uint8_t* hsg;        // m × 256    (count_bits == 8) 16-B fingerprint delta per first-rule slot
   int32_t any_generic;       // some neuron has no table

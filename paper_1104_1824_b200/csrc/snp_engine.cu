@@ -698,7 +698,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   SNP_TRY(s->d_tab.ensure((size_t)m * tabw, false));
   SNP_TRY(s->d_ctab.ensure((size_t)m * tabw * s->bytes, false));
   if (s->bytes == 1) SNP_TRY(s->d_tab_full.ensure((size_t)m * 256, false));
-  if (s->bytes == 1) SNP_TRY(s->d_ttab.ensure((size_t)m * 256, false));
+  if (s->bytes == 1) SNP_TRY(s->d_ttab.ensure((size_t)m * (32 + 256), false));
   if (s->bytes == 1) SNP_TRY(s->d_elut.ensure((size_t)m * 32, false));
   if (s->bytes == 1) SNP_TRY(s->d_hsg.ensure((size_t)m * 256, false));
   SysView& v = s->view;

@@ -1555,16 +1555,18 @@ constexpr int OPCAP = 1100;  // >= 16 ops per output block × (QCAP / 64 + 2)
 
 // ES: the block's emit words are staged in shared memory (m·8 B fit); else
 // (large m) the in-synapse gather reads them from global memory (L2/L1).
-template <typename T, int NPL, bool ES>
-__global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView L, ExpandOut O,
+// MWT: warps per CTA (MW; fewer for wide counts, whose per-lane staging of
+// 64 values would not fit shared memory at MW warps — int32 at config 3).
+template <typename T, int NPL, bool ES, int MWT = MW>
+__global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelView L, ExpandOut O,
                                                              const uint64_t* kq_off, NextArrays N, uint64_t* ovf,
                                                              unsigned long long* n_ovf, uint64_t ovf_cap) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int32_t m = S.m;
   const int64_t mE = (m + 1) & ~1;
   uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words + 2 zero words
-  uint8_t* sX = smem + (ES ? (mE + 2) * 8 : 0);                         // MW×32×xs_stride
-  uint8_t* sR = sX + (size_t)MW * 32 * xs_stride<T>();                  // QCAP + 32
+  uint8_t* sX = smem + (ES ? (mE + 2) * 8 : 0);                         // MWT×32×xs_stride
+  uint8_t* sR = sX + (size_t)MWT * 32 * xs_stride<T>();                 // QCAP + 32
   uint32_t* sD = reinterpret_cast<uint32_t*>(sR + QCAP + 32);           // (QCAP+32)/4 quad descriptors
   uint64_t* sOps = reinterpret_cast<uint64_t*>(sD + (QCAP + 32) / 4);   // OPCAP store ops
   uint64_t* sQ = sOps + OPCAP;                                          // 65 (+1 pad)
@@ -1666,15 +1668,15 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
   uint8_t* xsb = sX + (size_t)(warp * 32 + lane) * xs_stride<T>();
   T* xs = reinterpret_cast<T*>(xsb);
   const T* ctab = reinterpret_cast<const T*>(S.ctab);
-  const int j_iters = (m + MW * 32 - 1) / (MW * 32);
+  const int j_iters = (m + MWT * 32 - 1) / (MWT * 32);
   for (int it = 0; it < j_iters; ++it) {
-    const int32_t jbase = it * MW * 32 + warp * 32;
+    const int32_t jbase = it * MWT * 32 + warp * 32;
     if (jbase >= m) break;  // warp-uniform
 #if SNP_KC_L2PF
     // the warp's 32 rows of the parent block (2 KB contiguous for u8) pulled
     // into L2 while the gather runs, so the row load after it hits L2
     if (sizeof(T) == 1 && lane == 0) {
-      const int32_t jp = jbase + (SNP_KC_L2PF - 1) * MW * 32;
+      const int32_t jp = jbase + (SNP_KC_L2PF - 1) * MWT * 32;
       if (jp < m) {
         const int32_t nr = (m - jp < 32) ? (m - jp) : 32;
         bulk_prefetch_l2(data + eidx(pb0, jp, m), (uint32_t)(nr * PB * sizeof(T)));
@@ -1767,7 +1769,7 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
       // byte permutes; the bit-sliced counts become bytes by an 8x8 bit
       // transpose per 8 parents; x = t + count is one 32-bit add per 4 parents
       uint32_t tt[8];
-      ldg256(S.ttab + (int64_t)j * 256, tt);
+      ldg256(S.ttab + (int64_t)j * 32, tt);
       // counts >= 16 are rare: when no lane of the warp has one, the upper
       // planes are skipped (warp-uniform branch)
       uint64_t up = 0;
@@ -1809,7 +1811,8 @@ __global__ void __launch_bounds__(MW * 32) k_materialize_bs(SysView S, LevelView
               t[i] = 0;
 #pragma unroll
               for (int b = 0; b < 4; ++b)  // counts >= 32: the neuron's 256-entry row (L2-resident)
-                t[i] |= (uint32_t)__ldg(S.ttab + (int64_t)j * 256 + ((vw[i] >> (8 * b)) & 0xFFu)) << (8 * b);
+                t[i] |= (uint32_t)__ldg(S.ttab + (int64_t)m * 32 + (int64_t)j * 256 + ((vw[i] >> (8 * b)) & 0xFFu))
+                        << (8 * b);
             }
           }
         }
@@ -2386,9 +2389,11 @@ __global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_fu
   }
   if (full) {
     tab_full[i - n_c] = (uint8_t)entry;
-    // post-consumption value v - c_first(v) for every uint8 count (K-c
-    // lookup: the first 32 by byte permutes in registers, the rest by load)
-    ttab[(int64_t)s * 256 + slot] = (uint8_t)(slot - (uint32_t)cons);
+    // post-consumption value v - c_first(v) (K-c lookups): counts < 32 in
+    // the 32-byte rows (one coalesced 32-B load per lane, then byte
+    // permutes in registers), every count in the 256-byte rows
+    if (slot < 32) ttab[(int64_t)s * 32 + slot] = (uint8_t)(slot - (uint32_t)cons);
+    ttab[(int64_t)S.m * 32 + (int64_t)s * 256 + slot] = (uint8_t)(slot - (uint32_t)cons);
     if (slot < 32) elut[(int64_t)s * 32 + slot] = (uint8_t)entry;
   } else {
     tab[i] = (uint8_t)entry;
@@ -2927,9 +2932,12 @@ void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ct
 
 constexpr size_t KC_SMEM_MAX = 220 * 1024;
 
+// K-c warps per CTA: MW for 1-2 byte counts, 8 for int32 (staging fits)
+int kc_warps(int32_t bytes) { return bytes == 4 ? 8 : MW; }
+
 size_t materialize_smem_bytes(const SysView& S, int32_t bytes, bool staged_e) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
-  const size_t xs = (size_t)MW * 32 * (PB * bytes + 4);
+  const size_t xs = (size_t)kc_warps(bytes) * 32 * (PB * bytes + 4);
   return (staged_e ? (mE + 2) * 8 : 0) + xs + 2 * (QCAP + 32) + 8 * OPCAP + 67 * 8 + 16 + 16;
 }
 
@@ -3068,20 +3076,21 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
     const unsigned nblk = (unsigned)((L.F + PB - 1) / PB);
     dispatch_bytes(bytes, [&](auto tt) {
       using T = decltype(tt);
+      constexpr int W = sizeof(T) == 4 ? 8 : MW;  // = kc_warps(bytes)
       auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<nblk, MW * 32, smem, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
+        kern<<<nblk, W * 32, smem, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
       };
       if (staged) {
-        if (S.max_indeg < 16) go(k_materialize_bs<T, 4, true>);
-        else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, true>);
-        else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, true>);
-        else go(k_materialize_bs<T, 8, true>);
+        if (S.max_indeg < 16) go(k_materialize_bs<T, 4, true, W>);
+        else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, true, W>);
+        else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, true, W>);
+        else go(k_materialize_bs<T, 8, true, W>);
       } else {
-        if (S.max_indeg < 16) go(k_materialize_bs<T, 4, false>);
-        else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, false>);
-        else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, false>);
-        else go(k_materialize_bs<T, 8, false>);
+        if (S.max_indeg < 16) go(k_materialize_bs<T, 4, false, W>);
+        else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, false, W>);
+        else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, false, W>);
+        else go(k_materialize_bs<T, 8, false, W>);
       }
     });
   } else {

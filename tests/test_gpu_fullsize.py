@@ -14,6 +14,7 @@
   k_nd = 7, 20 levels) in full, and one level of the full-width system
   (m = 65536) with sampled parents."""
 import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import pytest
@@ -55,10 +56,18 @@ def check_sampled_children(eng, osys, L, rng, n_children, min_nonzero_t):
     par_rows = eng.level_columns(L, parent[pick])
     child_rows = eng.level_columns(L + 1, pick)
     psi_of = {}
-    for k, q in enumerate(pick):
+
+    def expected(k):  # the oracle, one sampled child (ctypes releases the GIL: host threads run in parallel)
+        q = pick[k]
         psi, _S, Cn = osys.children(par_rows[k], cap=int(t[q]) + 1)
-        assert (Cn[int(t[q])] == child_rows[k]).all()
-        assert oracle.fingerprint(Cn[int(t[q])]) == (int(fp[q][0]), int(fp[q][1]))
+        return psi, Cn[int(t[q])], oracle.fingerprint(Cn[int(t[q])])
+
+    with ThreadPoolExecutor(THREADS) as ex:
+        res = list(ex.map(expected, range(len(pick))))
+    for k, q in enumerate(pick):
+        psi, child, f = res[k]
+        assert (child == child_rows[k]).all()
+        assert f == (int(fp[q][0]), int(fp[q][1]))
         psi_of[int(parent[q])] = psi
     # siblings kept from one parent: distinct t < Ψ(parent), tag order
     for p, psi in psi_of.items():
