@@ -88,19 +88,21 @@ size_t level_bytes(int64_t F, int64_t m, int32_t w) { return (size_t)((F + PB - 
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool owned = true;  // false: a piece of a larger allocation (the retained-level pool)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), owned(o.owned) { o.p = nullptr; o.bytes = 0; o.owned = true; }
   DBuf& operator=(DBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; owned = o.owned; o.p = nullptr; o.bytes = 0; o.owned = true; }
     return *this;
   }
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     bytes = 0;
+    owned = true;
   }
   snp_status ensure(size_t need, bool slack = true) {
     if (need <= bytes && p) return SNP_OK;
@@ -218,9 +220,15 @@ struct snp_system {
   DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   DBuf edge_scratch;  // snp_level_edges: fp0/fp1 interleave
+  DBuf vlist;         // dedup = 0: the transitions to verify
   DBuf gen;           // generated-number bitmap (out_rule1 > 0)
   std::vector<DBuf> spare;  // released level buffers kept for reuse
   Arena arena;              // per-level metadata
+  // retained levels (keep_tree / dedup = 0): their blocked counts carved from
+  // one allocation reserved with the horizon, so no cudaMalloc lands inside a
+  // level (a 4.3 GB cudaMalloc per level cost ~25 ms at config 3)
+  DBuf lpool;
+  size_t lpool_used = 0;
   // multi-GPU exploration (snp_dist_*): this rank's share of the frontier and
   // of the visited keys (owner = fmix64(fp1) mod P)
   struct Dist {
@@ -278,6 +286,7 @@ struct DevCounters {
   unsigned long long n_halting;
   unsigned long long n_ovf;
   unsigned long long digest;
+  unsigned long long n_verify;
 };
 
 snp_status sync(snp_system* s) {
@@ -331,7 +340,20 @@ snp_status check_err(int32_t err) {
   return SNP_OK;
 }
 
+bool retain_levels(const snp_system* s);
+
 snp_status take_buffer(snp_system* s, size_t bytes, DBuf* out) {
+  if (s->lpool.p && retain_levels(s)) {
+    const size_t b = (bytes + 255) & ~(size_t)255;
+    if (s->lpool_used + b <= s->lpool.bytes) {
+      out->release();
+      out->p = static_cast<uint8_t*>(s->lpool.p) + s->lpool_used;
+      out->bytes = b;
+      out->owned = false;
+      s->lpool_used += b;
+      return SNP_OK;
+    }
+  }
   // reuse the smallest spare that fits
   int best = -1;
   for (int i = 0; i < (int)s->spare.size(); ++i)
@@ -414,6 +436,18 @@ snp_status reserve_horizon(snp_system* s, int64_t Ft) {
   if (meta_b <= spare) {
     SNP_TRY(s->arena.reserve(meta_b));
     spare -= meta_b;
+  }
+  // retained levels: a pool for up to RESERVE_LEVELS more levels of Ft
+  // configurations, within what is left (minus 4 GB of slack)
+  if (retain_levels(s) && !s->lpool.p) {
+    const size_t per = level_bytes(Ft + Ft / 10, s->m, s->bytes) + 256;
+    size_t want = per * (size_t)RESERVE_LEVELS;
+    const size_t slack = (size_t)4 << 30;
+    if (spare > slack && want > spare - slack) want = (spare - slack) / per * per;
+    if (spare > slack && want >= per) {
+      if (s->lpool.ensure(want, false) == SNP_OK) s->lpool_used = 0;
+      else s->lpool.release();
+    }
   }
   return SNP_OK;
 }
@@ -836,7 +870,8 @@ snp_status reset_state(snp_system* s) {
   for (double& x : s->prof_ms) x = 0;
   s->marks.clear();
   s->ev_used = 0;
-  s->levels.clear();
+  s->levels.clear();  // pooled level buffers are non-owning: the pool is reused from the start
+  s->lpool_used = 0;
   s->arena.reset();
   s->counters.clear();
   s->n_visited = 0;
@@ -985,6 +1020,7 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
     launch_gather_columns(s->bytes, raw.p, s->src_index.as<uint64_t>(), K, (int32_t)m, L->data.p, s->stream);
   }
   N.data = L->data.p;
+  launch_zero_tail(s->bytes, L->data.p, K, (int32_t)m, s->stream);
   launch_digest(N, K, 0, 0, 0, &dc(s)->digest, s->stream);
   CUDA_TRY(cudaGetLastError());
   SNP_TRY(read_counters(s, &hc));
@@ -1169,12 +1205,15 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
         CUDA_TRY(cudaGetLastError());
       }
       if (s->view.aug_rule >= 0) launch_aug_fix(s->view, s->bytes, LV, O, N, K, err, st);
+      launch_zero_tail(s->bytes, N.data, K, (int32_t)m, st);
       launch_digest(N, K, (uint64_t)s->levels.size(), 0, 0, &dc(s)->digest, st);
     }
     if (s->opt.dedup == 0) {
       SNP_TRY(update_stored_table(s));
       phase_begin(s, 4);
-      launch_verify(s->view, s->bytes, LV, O, off, C, T, tag_base, tb, s->stored.as<StoredLevel>(), err, st);
+      SNP_TRY(s->vlist.ensure(T * 8 + 16));
+      launch_verify(s->view, s->bytes, LV, O, off, C, T, tag_base, tb, s->stored.as<StoredLevel>(),
+                    s->vlist.as<uint64_t>(), &dc(s)->n_verify, err, st);
       phase_end(s);
       CUDA_TRY(cudaGetLastError());
     }
@@ -2095,6 +2134,7 @@ snp_status snp_dist_commit(snp_system* s, int64_t parent_offset, int64_t q_offse
       launch_gather_columns(s->bytes, s->dist.raw.p, s->src_index.as<uint64_t>(), K, (int32_t)m, L->data.p, st);
     }
     N.data = L->data.p;
+    launch_zero_tail(s->bytes, L->data.p, K, (int32_t)m, st);
     launch_digest(N, K, 0, q_offset, 0, &dc(s)->digest, st);
     CUDA_TRY(cudaGetLastError());
     DevCounters hc;
@@ -2144,6 +2184,7 @@ snp_status snp_dist_commit(snp_system* s, int64_t parent_offset, int64_t q_offse
     }
   }
   // parents are indices in the previous level: global = local + parent_offset
+  if (K > 0) launch_zero_tail(s->bytes, N.data, K, (int32_t)m, st);
   launch_digest(N, K, (uint64_t)s->levels.size(), q_offset, parent_offset, &dc(s)->digest, st);
   CUDA_TRY(cudaEventRecord(s->ev1, st));
   DevCounters hc;
@@ -2379,6 +2420,7 @@ snp_status keys_round(snp_system* s, snp_status st, int64_t T_local, int64_t hal
       CUDA_TRY(cudaMemcpyAsync(idx.p, hidx.data(), Kn * 8, cudaMemcpyHostToDevice, s->stream));
       SNP_TRY(take_buffer(s, level_bytes(Kn, m, s->bytes), &nl->data));
       launch_gather_columns(s->bytes, recvrows.p, idx.as<uint64_t>(), Kn, (int32_t)m, nl->data.p, s->stream);
+      launch_zero_tail(s->bytes, nl->data.p, Kn, (int32_t)m, s->stream);
       CUDA_TRY(cudaGetLastError());
     }
     CUDA_TRY(cudaStreamSynchronize(s->stream));

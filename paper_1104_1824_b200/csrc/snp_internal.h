@@ -104,12 +104,15 @@ void launch_overflow_fix(const SysView& S, int32_t bytes, const LevelView& L, co
                          int32_t* err, cudaStream_t st);
 void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
                    const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb,
-                   const StoredLevel* stored, int32_t* err, cudaStream_t st);
+                   const StoredLevel* stored, uint64_t* list, unsigned long long* n_list, int32_t* err,
+                   cudaStream_t st);
 void launch_level0_compact(const uint8_t* verdict, const uint64_t* kept, const uint64_t* kpos, int64_t F0,
                            const uint64_t* fp0, const uint64_t* fp1, const NextArrays& N, uint64_t* src_index,
                            const Tables& tb, int insert_visited, int32_t* err, cudaStream_t st);
 void launch_gather_columns(int32_t bytes, const void* src, const uint64_t* src_index, int64_t K, int32_t m, void* dst,
                            cudaStream_t st);
+// zero the unused configurations of a level's last 64-configuration block
+void launch_zero_tail(int32_t bytes, void* data, int64_t F, int32_t m, cudaStream_t st);
 // a[i] += add for every a[i] >= 0 (multi-GPU: local -> global parent indices)
 void launch_add_i64(int64_t* a, int64_t n, int64_t add, cudaStream_t st);
 void launch_verify_level0(int32_t bytes, const void* data, int32_t m, const ChildArrays& C, uint64_t F0,

@@ -1507,6 +1507,9 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_PREFETCH
 #define SNP_KC_PREFETCH 0
 #endif
+#ifndef SNP_KC_EPF
+#define SNP_KC_EPF 0  // k > 0: L2 bulk prefetch of block blk + k's emit words at CTA start (A/B: 148 = one wave ahead)
+#endif
 constexpr int MW = SNP_KC_WARPS;  // warps per K-c CTA
 constexpr int QCAP = 4064;   // outputs per block resolved through the r(q) table (+32 alignment slack)
 
@@ -1589,6 +1592,16 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
     const uint8_t* src = reinterpret_cast<const uint8_t*>(O.ebits) + (size_t)blk * ebytes;
     for (uint32_t off = 0; off < ebytes; off += 32768u)
       bulk_g2s(reinterpret_cast<uint8_t*>(sE) + off, src + off, min(32768u, ebytes - off), bar);
+#if SNP_KC_EPF
+    // the emit words of the block an SM is likely to take next (blocks are
+    // handed out in order, one resident CTA per SM) pulled into L2, so that
+    // CTA's staging copy does not wait on HBM
+    const int64_t nb = blk + SNP_KC_EPF;
+    if (nb < (L.F + PB - 1) / PB) {
+      const uint8_t* nsrc = reinterpret_cast<const uint8_t*>(O.ebits) + (size_t)nb * ebytes;
+      for (uint32_t off = 0; off < ebytes; off += 32768u) bulk_prefetch_l2(nsrc + off, min(32768u, ebytes - off));
+    }
+#endif
   }
   if (tid <= np) sQ[tid] = kq_off[pb0 + tid];
   if (ES && tid < 2) sE[mE + tid] = 0;  // target of padded in-synapses
@@ -2159,10 +2172,25 @@ __global__ void __launch_bounds__(256) k_materialize_exact_s(SysView S, LevelVie
 constexpr int VERIFY_WARPS = 8;
 size_t verify_smem_bytes(int32_t m) { return (size_t)VERIFY_WARPS * 2 * 8 * (size_t)m; }
 
-// k_verify with the fired (c, p) of both children in shared memory
+// the children whose key matched another configuration (seen at an earlier
+// level, or a same-level duplicate that lost to the minimum tag): appended to
+// `list` (order irrelevant: each is only compared), so the verification warps
+// touch ~2 % of the transitions instead of scanning them all
+__global__ void k_verify_need(ChildArrays C, uint64_t T_, uint64_t tag_base, Tables tb, uint64_t* list,
+                              unsigned long long* n_list) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T_; c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t vd = C.verdict[c];
+    const bool need = vd == 1 ? tb.ltab[C.cslot[c]].tag != tag_base + c : C.cref[c] != EMPTY;
+    if (need) list[atomicAdd(n_list, 1ULL)] = c;
+  }
+}
+
+// k_verify with the fired (c, p) of both children in shared memory, over
+// the list k_verify_need built
 template <typename T>
 __global__ void __launch_bounds__(VERIFY_WARPS * 32) k_verify_s(SysView S, LevelView L, ExpandOut O,
-                                                                const uint64_t* off, ChildArrays C, uint64_t T_,
+                                                                const uint64_t* off, ChildArrays C,
+                                                                const uint64_t* list, const unsigned long long* n_list,
                                                                 uint64_t tag_base, Tables tb,
                                                                 const StoredLevel* stored, int32_t* err) {
   extern __shared__ int2 vsm[];
@@ -2171,16 +2199,12 @@ __global__ void __launch_bounds__(VERIFY_WARPS * 32) k_verify_s(SysView S, Level
   int2* fb = fa + S.m;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t c = warp; c < T_; c += nwarps) {
+  const uint64_t nl = *n_list;
+  for (uint64_t i = warp; i < nl; i += nwarps) {
+    const uint64_t c = list[i];
     const uint8_t vd = C.verdict[c];
     uint64_t other = EMPTY;
-    if (vd == 1) {
-      const uint64_t wtag = tb.ltab[C.cslot[c]].tag;
-      if (wtag == tag_base + c) continue;  // the winner itself
-      other = wtag - tag_base;
-    } else if (C.cref[c] == EMPTY) {
-      continue;
-    }
+    if (vd == 1) other = tb.ltab[C.cslot[c]].tag - tag_base;
     const uint32_t p = C.cpar[c];
     ChildCtx cx, co;
     decode_child(S, O.nd + (uint64_t)p * KMAX, O.ndc[p], c - off[p], cx);
@@ -2265,6 +2289,18 @@ __global__ void k_level0_compact(const uint8_t* verdict, const uint64_t* kept, c
     src_index[q] = (uint64_t)c;
     if (insert_visited) visited_insert(tb, fp0[c], fp1[c], q, err);
   }
+}
+
+// zero the unused tail of a level's last storage block (configurations F ..
+// 64·ceil(F/64) - 1 of every neuron row): K-a and K-c load whole 32-byte row
+// halves, so the tail is read (and masked out) — zeroed it is also initialised
+template <typename T>
+__global__ void k_zero_tail(T* data, int64_t F, int32_t m) {
+  const int64_t b = F / PB;
+  const int r0 = (int)(F % PB);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)m * (PB - r0);
+       i += (int64_t)gridDim.x * blockDim.x)
+    data[(b * m + i / (PB - r0)) * PB + r0 + i % (PB - r0)] = 0;
 }
 
 __global__ void k_add_i64(int64_t* a, int64_t n, int64_t add) {
@@ -3159,7 +3195,7 @@ void launch_overflow_fix(const SysView& S, int32_t bytes, const LevelView& L, co
 
 void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
                    const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, const StoredLevel* stored,
-                   int32_t* err, cudaStream_t st) {
+                   uint64_t* list, unsigned long long* n_list, int32_t* err, cudaStream_t st) {
   if (!T) return;
   unsigned g = grid_for(T * 32, 256);
   if (g > 148u * 64u) g = 148u * 64u;
@@ -3167,8 +3203,12 @@ void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const Ex
     using TT = decltype(tt);
     const size_t sm = verify_smem_bytes(S.m);
     if (sm <= 200 * 1024 && S.delay_m == 0) {
+      cudaMemsetAsync(n_list, 0, sizeof(unsigned long long), st);
+      k_verify_need<<<grid_for(T), BLK, 0, st>>>(C, T, tag_base, tb, list, n_list);
+      count_launch();
       cudaFuncSetAttribute(k_verify_s<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_verify_s<TT><<<g, VERIFY_WARPS * 32, sm, st>>>(S, L, O, off, C, T, tag_base, tb, stored, err);
+      k_verify_s<TT><<<148u * 2u, VERIFY_WARPS * 32, sm, st>>>(S, L, O, off, C, list, n_list, tag_base, tb, stored,
+                                                              err);
     } else {
       k_verify<TT><<<g, 256, 0, st>>>(S, L, O, off, C, T, tag_base, tb, stored, err);
     }
@@ -3192,6 +3232,15 @@ void launch_gather_columns(int32_t bytes, const void* src, const uint64_t* src_i
     using T = decltype(tt);
     k_gather_columns<T><<<grid, BLK, 0, st>>>(reinterpret_cast<const T*>(src), src_index, K, m,
                                               reinterpret_cast<T*>(dst));
+  });
+  count_launch();
+}
+
+void launch_zero_tail(int32_t bytes, void* data, int64_t F, int32_t m, cudaStream_t st) {
+  if (F % PB == 0 || !data) return;
+  dispatch_bytes(bytes, [&](auto tt) {
+    using T = decltype(tt);
+    k_zero_tail<T><<<grid_for((uint64_t)m * (PB - F % PB)), BLK, 0, st>>>(reinterpret_cast<T*>(data), F, m);
   });
   count_launch();
 }
