@@ -151,6 +151,7 @@ struct SysView {
   // SN P systems with delays (reading A26): delay_m > 0
   // real neurons, the state row is [C | τ | π] (m = 3·delay_m columns)
   int32_t delay_m;
+  int32_t small_cp;          // every rule has c, p <= 255 (packed fired (c, p) tables)
   const int32_t* delay;      // n: d >= 0 per rule
 };
 // key of a terminal child (second output spike): skipped by the dedup

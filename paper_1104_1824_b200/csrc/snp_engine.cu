@@ -229,6 +229,11 @@ struct snp_system {
   // level (a 4.3 GB cudaMalloc per level cost ~25 ms at config 3)
   DBuf lpool;
   size_t lpool_used = 0;
+  // small frontiers (k_small_bfs): scratch, per-launch level pools (kept until
+  // the next snp_begin: the levels they hold are views into them)
+  DBuf small_scratch, small_out, small_stored;
+  std::vector<DBuf> small_pools;
+  size_t small_skip = (size_t)-1;  // levels.size() at which a level had > SMALL_T transitions
   // multi-GPU exploration (snp_dist_*): this rank's share of the frontier and
   // of the visited keys (owner = fmix64(fp1) mod P)
   struct Dist {
@@ -369,6 +374,10 @@ snp_status take_buffer(snp_system* s, size_t bytes, DBuf* out) {
 }
 
 void release_level_data(snp_system* s, Level* L) {
+  if (L->data.p && !L->data.owned) {  // a view into a pool: nothing to recycle
+    L->data.release();
+    return;
+  }
   if (L->data.p) {
     s->spare.push_back(std::move(L->data));
     while (s->spare.size() > 2) s->spare.erase(s->spare.begin());
@@ -755,6 +764,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     // memory even when they fit in shared memory (the large-m path)
     const char* k = getenv("SNP_KERNELS");
     v.kernel_flags = 0;
+    v.small_cp = s->small_rules ? 1 : 0;  // c, p <= 255: packed (c, p) tables in the verification
     v.aug_rule = -1;  // set by snp_load after the tables are built
     v.aug_neuron = -1;
     if (k && strstr(k, "expand_t")) v.kernel_flags |= KF_EXPAND_T;
@@ -872,6 +882,8 @@ snp_status reset_state(snp_system* s) {
   s->ev_used = 0;
   s->levels.clear();  // pooled level buffers are non-owning: the pool is reused from the start
   s->lpool_used = 0;
+  s->small_pools.clear();
+  s->small_skip = (size_t)-1;
   s->arena.reset();
   s->counters.clear();
   s->n_visited = 0;
@@ -1239,6 +1251,147 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
   return SNP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// small frontiers: up to max_levels levels in one k_small_bfs launch
+// (configs 1-2).  *done = levels committed; fewer than asked when a level has
+// more than SMALL_T transitions (left for advance_impl), a frontier outgrew
+// SMALL_F, or it emptied.  SNP_SMALL=0 turns the path off (tests run both).
+// ---------------------------------------------------------------------------
+bool small_ok(const snp_system* s) {
+  const char* e = getenv("SNP_SMALL");
+  const bool off = e && e[0] == '0';
+  if (off || s->levels.empty() || s->dist.P != 0 || s->view.aug_rule >= 0 || s->view.delay_m > 0 ||
+      s->opt.keep_all_edges || s->levels.size() == s->small_skip)
+    return false;
+  const Level* cur = s->levels.back().get();
+  return cur->F > 0 && cur->F <= SMALL_F && cur->has_data();
+}
+
+snp_status advance_small(snp_system* s, int32_t want, int32_t* done) {
+  *done = 0;
+  Level* cur = s->levels.back().get();
+  const int64_t m = s->m, F = cur->F;
+  const size_t slot = level_bytes(SMALL_T, m, s->bytes);
+  const size_t meta = (size_t)SMALL_T * (8 + 8 + 8 + 8 + 1);
+  const size_t per = ((slot + 255) & ~(size_t)255) + ((meta + 255) & ~(size_t)255);
+  int32_t L = std::max<int32_t>(1, std::min<int32_t>(want, (int32_t)std::max<size_t>(1, ((size_t)256 << 20) / per)));
+  // capacity: every configuration the launch can add enters visited
+  SNP_TRY(ensure_visited(s, (uint64_t)s->n_visited + (uint64_t)L * SMALL_F + SMALL_T));
+  SNP_TRY(ensure_ltab(s, SMALL_T));
+  const uint64_t lslots = next_pow2(std::max<uint64_t>(1024, 2 * (uint64_t)SMALL_T));
+  Tables tb = tables(s, lslots);
+  // scratch
+  const size_t sc_b = (size_t)(SMALL_F + 1) * 8 * 2 + (size_t)SMALL_F * (8 + 8 + 4) + (size_t)SMALL_F * KMAX * 8 +
+                      (size_t)SMALL_T * (4 + 8 + 8 + 1 + 8 + 8) + (size_t)(SMALL_T + 1) * 16 + 1024;
+  SNP_TRY(s->small_scratch.ensure(sc_b, false));
+  uint8_t* sp = s->small_scratch.as<uint8_t>();
+  auto take = [&](size_t b) {
+    uint8_t* r = sp;
+    sp += (b + 15) & ~(size_t)15;
+    return r;
+  };
+  SmallArgs a{};
+  a.psi = reinterpret_cast<uint64_t*>(take((SMALL_F + 1) * 8));
+  a.off = reinterpret_cast<uint64_t*>(take((SMALL_F + 1) * 8));
+  a.fpb0 = reinterpret_cast<uint64_t*>(take(SMALL_F * 8));
+  a.fpb1 = reinterpret_cast<uint64_t*>(take(SMALL_F * 8));
+  a.ndc = reinterpret_cast<int32_t*>(take(SMALL_F * 4));
+  a.nd = reinterpret_cast<uint64_t*>(take((size_t)SMALL_F * KMAX * 8));
+  a.cpar = reinterpret_cast<uint32_t*>(take(SMALL_T * 4));
+  a.cfp0 = reinterpret_cast<uint64_t*>(take(SMALL_T * 8));
+  a.cfp1 = reinterpret_cast<uint64_t*>(take(SMALL_T * 8));
+  a.verdict = take(SMALL_T);
+  a.cslot = reinterpret_cast<uint64_t*>(take(SMALL_T * 8));
+  a.cref = reinterpret_cast<uint64_t*>(take(SMALL_T * 8));
+  a.kept = reinterpret_cast<uint64_t*>(take((SMALL_T + 1) * 8));
+  a.kpos = reinterpret_cast<uint64_t*>(take((SMALL_T + 1) * 8));
+  // pool of the new levels
+  DBuf pool;
+  SNP_TRY(pool.ensure(per * (size_t)L, false));
+  uint8_t* pp = pool.as<uint8_t>();
+  a.data_pool = pp;
+  a.data_stride = (slot + 255) & ~(size_t)255;
+  uint8_t* mp = pp + a.data_stride * (size_t)L;
+  a.parent_pool = reinterpret_cast<int64_t*>(mp);
+  a.t_pool = reinterpret_cast<uint64_t*>(mp + (size_t)L * SMALL_T * 8);
+  a.fp0_pool = reinterpret_cast<uint64_t*>(mp + (size_t)L * SMALL_T * 16);
+  a.fp1_pool = reinterpret_cast<uint64_t*>(mp + (size_t)L * SMALL_T * 24);
+  a.halting_pool = mp + (size_t)L * SMALL_T * 32;
+  // dedup = 0: the data of every tree level, the new ones written by the kernel
+  std::vector<StoredLevel> st(s->levels.size() + L, StoredLevel{nullptr});
+  for (size_t i = 0; i < s->levels.size(); ++i) st[i] = StoredLevel{s->levels[i]->data.p};
+  SNP_TRY(s->small_stored.ensure(st.size() * sizeof(StoredLevel) + 16));
+  CUDA_TRY(cudaMemcpyAsync(s->small_stored.p, st.data(), st.size() * sizeof(StoredLevel), cudaMemcpyHostToDevice,
+                           s->stream));
+  SNP_TRY(s->small_out.ensure((size_t)L * sizeof(SmallLevelOut) + 64, false));
+  a.data = cur->data.p;
+  a.F = F;
+  a.fp0 = cur->fp0.as<uint64_t>();
+  a.fp1 = cur->fp1.as<uint64_t>();
+  a.halting = cur->halting.as<uint8_t>();
+  a.level0 = (int32_t)s->levels.size() - 1;
+  a.max_levels = L;
+  a.tb = tb;
+  a.stored = s->small_stored.as<StoredLevel>();
+  a.frontier_target = s->opt.frontier_target;
+  a.dedup = s->opt.dedup;
+  a.out = s->small_out.as<SmallLevelOut>();
+  a.levels_done = reinterpret_cast<int32_t*>(s->small_out.as<uint8_t>() + (size_t)L * sizeof(SmallLevelOut));
+  CUDA_TRY(cudaMemsetAsync(a.levels_done, 0, 4, s->stream));
+  CUDA_TRY(cudaMemsetAsync(a.out, 0, (size_t)L * sizeof(SmallLevelOut), s->stream));
+  CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
+  launch_small_bfs(s->view, s->bytes, a, s->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
+  std::vector<SmallLevelOut> out(L);
+  int32_t nd = 0;
+  CUDA_TRY(cudaMemcpyAsync(out.data(), a.out, (size_t)L * sizeof(SmallLevelOut), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(&nd, a.levels_done, 4, cudaMemcpyDeviceToHost, s->stream));
+  SNP_TRY(sync(s));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  const double ms_lvl = nd > 0 ? ms / nd : 0.0;
+  uint8_t* base = pool.as<uint8_t>();
+  s->small_pools.push_back(std::move(pool));
+  for (int32_t k = 0; k < nd; ++k) {
+    Level* prev = s->levels.back().get();
+    const SmallLevelOut& o = out[k];
+    auto nl = std::make_unique<Level>();
+    nl->F = o.kept;
+    nl->data.p = base + (size_t)k * a.data_stride;
+    nl->data.bytes = slot;
+    nl->data.owned = false;
+    const size_t mo = a.data_stride * (size_t)L + (size_t)k * SMALL_T * 8;
+    nl->parent.p = base + mo;
+    nl->t.p = base + mo + (size_t)L * SMALL_T * 8;
+    nl->fp0.p = base + mo + (size_t)L * SMALL_T * 16;
+    nl->fp1.p = base + mo + (size_t)L * SMALL_T * 24;
+    nl->halting.p = base + a.data_stride * (size_t)L + (size_t)L * SMALL_T * 32 + (size_t)k * SMALL_T;
+    snp_level_counters lc{};
+    lc.parents = prev->F;
+    lc.halting = o.n_halting;
+    lc.T = o.T;
+    lc.n_new = o.n_new;
+    lc.kept = o.kept;
+    lc.tau = o.tau;
+    lc.ms = ms_lvl;
+    s->counters.push_back(lc);
+    s->digest += o.digest;
+    s->n_visited += o.kept;
+    s->total_T += o.T;
+    s->levels.push_back(std::move(nl));
+  }
+  // keep_tree = 0: only the newest level and its parent keep their counts
+  if (!retain_levels(s))
+    for (size_t i = 0; i + 2 < s->levels.size(); ++i)
+      if (s->levels[i]->has_data()) release_level_data(s, s->levels[i].get());
+  *done = nd;
+  if (nd < L && out[nd].stop == 1) s->small_skip = s->levels.size();  // that level goes to advance_impl
+  s->halting_current_valid = false;
+  if (nd < L && out[nd].err) SNP_TRY(check_err(out[nd].err));
+  return SNP_OK;
+}
+
 snp_status snapshot(snp_system* s, snp_tree** out) {
   // halting flags of the last level
   Level* last = s->levels.back().get();
@@ -1474,7 +1627,14 @@ snp_status snp_begin(snp_system* s, const snp_configs* level0) {
 snp_status snp_advance(snp_system* s, snp_level_counters* counters) {
   if (!s) return fail(SNP_E_ARG, "NULL system");
   if (!s->begun) return fail(SNP_E_STATE, "snp_advance before snp_begin (or after an error, or in distributed mode)");
-  snp_status st = advance_impl(s, counters);
+  snp_status st = SNP_OK;
+  int32_t done = 0;
+  if (small_ok(s)) st = advance_small(s, 1, &done);
+  if (st == SNP_OK && done == 1) {
+    if (counters) *counters = s->counters.back();
+  } else if (st == SNP_OK) {
+    st = advance_impl(s, counters);
+  }
   if (st != SNP_OK) s->begun = false;
   return st;
 }
@@ -1640,10 +1800,22 @@ snp_status snp_explore(snp_system* s, const snp_configs* level0, int32_t depth, 
   if (!s || !out || depth < 0) return fail(SNP_E_ARG, "snp_explore: bad arguments");
   snp_status st = snp_begin(s, level0);
   if (st != SNP_OK) return st;
-  for (int32_t d = 0; d < depth; ++d) {
+  for (int32_t d = 0; d < depth;) {
     if (s->levels.back()->F == 0) break;
-    st = snp_advance(s, nullptr);
-    if (st != SNP_OK) return st;
+    int32_t done = 0;
+    if (small_ok(s)) {  // several small levels per launch
+      st = advance_small(s, depth - d, &done);
+      if (st != SNP_OK) {
+        s->begun = false;
+        return st;
+      }
+    }
+    if (done == 0) {
+      st = snp_advance(s, nullptr);
+      if (st != SNP_OK) return st;
+      done = 1;
+    }
+    d += done;
     if (s->levels.back()->F == 0) break;
   }
   return snapshot(s, out);

@@ -147,6 +147,56 @@ void launch_sample(const SysView& S, int64_t W, int32_t* cur, int32_t* nxt, uint
                    int32_t steps, int32_t input_neuron, const int32_t* train, int32_t train_len, int32_t* halted,
                    int32_t* err, bool small_rules, cudaStream_t st);
 
+// Small frontiers (configs 1-2: the paper's Π): whole levels in ONE launch of
+// ONE CTA, several levels per launch (k_small_bfs).
+constexpr int SMALL_F = 256;    // parents of a level the single CTA expands
+constexpr int SMALL_T = 4096;   // transitions of a level it handles
+struct SmallLevelOut {
+  int64_t T, n_new, kept, n_halting;
+  uint64_t tau;
+  unsigned long long digest;
+  int32_t err;   // ERR_* of this level (the level is not committed)
+  int32_t stop;  // 0 committed; 1 more than SMALL_T transitions (nothing committed, level left to the big path)
+};
+struct SmallArgs {
+  const void* data;          // current level (tree level `level0`), blocked counts
+  int64_t F;
+  const uint64_t* fp0;
+  const uint64_t* fp1;
+  uint8_t* halting;          // its halting flags (written)
+  int32_t level0;
+  int32_t max_levels;
+  uint8_t* data_pool;        // new level k: data_pool + k · data_stride (blocked, SMALL_T configurations)
+  size_t data_stride;
+  int64_t* parent_pool;      // new level k: + k · SMALL_T entries
+  uint64_t* t_pool;
+  uint64_t* fp0_pool;
+  uint64_t* fp1_pool;
+  uint8_t* halting_pool;
+  // scratch
+  uint64_t* psi;             // SMALL_F + 1
+  uint64_t* off;             // SMALL_F + 1
+  uint64_t* fpb0;            // SMALL_F
+  uint64_t* fpb1;
+  int32_t* ndc;
+  uint64_t* nd;              // SMALL_F × KMAX
+  uint32_t* cpar;            // SMALL_T
+  uint64_t* cfp0;
+  uint64_t* cfp1;
+  uint8_t* verdict;
+  uint64_t* cslot;
+  uint64_t* cref;
+  uint64_t* kept;            // SMALL_T + 1
+  uint64_t* kpos;            // SMALL_T + 1
+  Tables tb;                 // visited + a level table of >= 2·SMALL_T slots
+  StoredLevel* stored;       // dedup = 0: data of every tree level (new ones written here)
+  int64_t frontier_target;
+  int32_t dedup;
+  SmallLevelOut* out;        // max_levels
+  int32_t* levels_done;
+};
+void launch_small_bfs(const SysView& S, int32_t bytes, const SmallArgs& a, cudaStream_t st);
+
 // CUB exclusive scan of n uint64 values (temp storage managed by the caller).
 size_t scan_temp_bytes(int64_t n);
 void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint64_t* in, uint64_t* out, int64_t n,

@@ -2133,13 +2133,35 @@ __device__ void fired_cp(const SysView& S, const void* data, int64_t p, const Ch
   __syncwarp();
 }
 
-// column j of that child: eq. (2) restricted to column j (Def. 2)
+// the same with (c, p) packed as c | p << 8 (every rule has c, p <= 255):
+// 2 bytes per neuron instead of 8, so 4x the verification warps fit an SM
 template <typename T>
+__device__ void fired_cp(const SysView& S, const void* data, int64_t p, const ChildCtx& cx, uint16_t* fc, int lane) {
+  for (int32_t s = lane; s < S.m; s += 32) {
+    const int r = first_rule(S, s, ld_count<T>(data, p, s, S.m));
+    fc[s] = r >= 0 ? (uint16_t)(S.rules[r].c | (S.rules[r].p << 8)) : (uint16_t)0;
+  }
+  __syncwarp();
+  for (int i = lane; i < cx.K; i += 32) {
+    if (!cx.x[i]) continue;
+    const int32_t s = cx.s[i];
+    const int r = nth_applicable(S, s, ld_count<T>(data, p, s, S.m), cx.x[i]);
+    fc[s] = (uint16_t)(S.rules[r].c | (S.rules[r].p << 8));
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ int32_t fc_c(int2 v) { return v.x; }
+__device__ __forceinline__ int32_t fc_p(int2 v) { return v.y; }
+__device__ __forceinline__ int32_t fc_c(uint16_t v) { return v & 0xFF; }
+__device__ __forceinline__ int32_t fc_p(uint16_t v) { return v >> 8; }
+
+// column j of that child: eq. (2) restricted to column j (Def. 2)
+template <typename T, typename FC>
 __device__ __forceinline__ int64_t fired_value(const SysView& S, const void* data, int64_t p, int32_t j,
-                                               const ChildCtx& cx, const int2* fc) {
+                                               const ChildCtx& cx, const FC* fc) {
   if (S.aug_rule >= 0 && j == S.m - 1) return exact_value<T>(S, data, p, j, cx);
-  int64_t val = (int64_t)ld_count<T>(data, p, j, S.m) - fc[j].x;
-  for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) val += fc[S.in_src[e]].y;
+  int64_t val = (int64_t)ld_count<T>(data, p, j, S.m) - fc_c(fc[j]);
+  for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) val += fc_p(fc[S.in_src[e]]);
   return val;
 }
 
@@ -2170,7 +2192,7 @@ __global__ void __launch_bounds__(256) k_materialize_exact_s(SysView S, LevelVie
 }
 
 constexpr int VERIFY_WARPS = 8;
-size_t verify_smem_bytes(int32_t m) { return (size_t)VERIFY_WARPS * 2 * 8 * (size_t)m; }
+size_t verify_smem_bytes(int32_t m, size_t entry = 8) { return (size_t)VERIFY_WARPS * 2 * entry * (size_t)m; }
 
 // the children whose key matched another configuration (seen at an earlier
 // level, or a same-level duplicate that lost to the minimum tag): appended to
@@ -2187,16 +2209,16 @@ __global__ void k_verify_need(ChildArrays C, uint64_t T_, uint64_t tag_base, Tab
 
 // k_verify with the fired (c, p) of both children in shared memory, over
 // the list k_verify_need built
-template <typename T>
+template <typename T, typename FC>
 __global__ void __launch_bounds__(VERIFY_WARPS * 32) k_verify_s(SysView S, LevelView L, ExpandOut O,
                                                                 const uint64_t* off, ChildArrays C,
                                                                 const uint64_t* list, const unsigned long long* n_list,
                                                                 uint64_t tag_base, Tables tb,
                                                                 const StoredLevel* stored, int32_t* err) {
-  extern __shared__ int2 vsm[];
+  extern __shared__ __align__(16) uint8_t vsm_raw[];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  int2* fa = vsm + (size_t)wl * 2 * S.m;
-  int2* fb = fa + S.m;
+  FC* fa = reinterpret_cast<FC*>(vsm_raw) + (size_t)wl * 2 * S.m;
+  FC* fb = fa + S.m;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t nl = *n_list;
@@ -2347,6 +2369,329 @@ __global__ void k_rehash(const Slot* old_tab, uint64_t old_cap, Slot* new_tab, u
     }
     if (!ok) atomicOr(err, ERR_TABLE_FULL);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Small frontiers (configs 1-2, the paper's Π with <= 5 configurations per
+// level): up to `max_levels` whole BFS levels in ONE launch of ONE CTA.  Each
+// level runs the steps of the multi-kernel path in order — K-a (first rule,
+// Ψ, ND list, base fingerprint, halting), the offsets, K-b child keys by
+// linearity, K-d (visited probe, level table with the minimum tag, N_new,
+// thinning τ, kept flags, compaction + visited insert), K-c (each kept child
+// exactly, eq. (2) column by column), the dedup = 0 verification and the
+// digest — on the same device functions and with the same tags, so the tree
+// is the one the big path builds (same parity tests).  A level with more
+// than SMALL_T transitions is left untouched for the big path; a level whose
+// frontier exceeds SMALL_F ends the launch after it is committed.
+// ---------------------------------------------------------------------------
+// floor(F·2^64 / N) for F < N (reading A19), by restoring long division
+__device__ uint64_t tau_div(uint64_t F, uint64_t N) {
+  uint64_t q = 0, r = F;  // remainder < N throughout; dividend F·2^64: 64 zero bits enter
+  for (int i = 0; i < 64; ++i) {
+    const bool carry = (r >> 63) != 0;
+    r <<= 1;
+    q <<= 1;
+    if (carry || r >= N) {
+      r -= N;
+      q |= 1;
+    }
+  }
+  return q;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_small_bfs(SysView S, SmallArgs a) {
+  __shared__ unsigned long long sh_u64[4];  // [0] n_new, [1] n_halting, [2] digest
+  __shared__ int32_t sh_err, sh_stop;
+  __shared__ uint64_t sh_T, sh_K, sh_tau, sh_part[1024];
+  __shared__ int sh_thin;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int32_t m = S.m;
+  const void* data = a.data;
+  int64_t F = a.F;
+  const uint64_t* fp0 = a.fp0;
+  const uint64_t* fp1 = a.fp1;
+  uint8_t* halting = a.halting;
+  int done = 0;
+  for (int lev = 0; lev < a.max_levels; ++lev) {
+    if (tid == 0) {
+      sh_u64[0] = sh_u64[1] = sh_u64[2] = 0;
+      sh_err = 0;
+      sh_stop = 0;
+    }
+    __syncthreads();
+    // ---- K-a: applicability, Ψ (eq. (8), A3/A5), ND list, base fingerprint
+    for (int64_t p = tid; p < F; p += nt) {
+      uint64_t fa = fp0[p], fb = fp1[p], psi = 1;
+      int ndc = 0;
+      bool any = false;
+      for (int32_t s = 0; s < m; ++s) {
+        const int32_t v = ld_count<T>(data, p, s, m);
+        int first = -1, d = 0;
+        for (int r = S.rule_off[s]; r < S.rule_off[s + 1]; ++r)
+          if (rule_app(S.rules[r], v)) {
+            if (!d) first = r;
+            ++d;
+          }
+        if (!d) continue;
+        any = true;
+        fa += __ldg(S.h0 + first);
+        fb += __ldg(S.h1 + first);
+        if (d >= 2) {
+          if (ndc < KMAX) a.nd[p * KMAX + ndc] = ((uint64_t)(uint32_t)s << 32) | (uint32_t)v;
+          ++ndc;
+          psi = sat_mul(psi, (uint64_t)d);
+        }
+      }
+      halting[p] = any ? 0 : 1;
+      if (!any) atomicAdd(&sh_u64[1], 1ULL);
+      a.psi[p] = any ? psi : 0;
+      a.fpb0[p] = fa;
+      a.fpb1[p] = fb;
+      a.ndc[p] = ndc;
+      if ((any && psi > PSI_LIMIT) || ndc > KMAX) atomicOr(&sh_err, ERR_CAPACITY);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t acc = 0;
+      for (int64_t p = 0; p < F; ++p) {
+        a.off[p] = acc;
+        acc += a.psi[p];
+        if (acc > (1ULL << 40)) acc = 1ULL << 40;  // saturate: only the SMALL_T test below reads it
+      }
+      a.off[F] = acc;
+      sh_T = acc;
+      if (!sh_err && acc > (uint64_t)SMALL_T) sh_stop = 1;
+    }
+    __syncthreads();
+    SmallLevelOut* o = a.out + lev;
+    if (sh_err || sh_stop) {
+      if (tid == 0) {
+        o->err = sh_err;
+        o->stop = sh_stop;
+        o->T = (int64_t)sh_T;
+        o->n_halting = (int64_t)sh_u64[1];
+      }
+      break;
+    }
+    const uint64_t Tn = sh_T;
+    // ---- K-b: child -> parent, keys by linearity (reading A18), clear the level table
+    for (int64_t p = tid; p < F; p += nt)
+      for (uint64_t c = a.off[p]; c < a.off[p + 1]; ++c) a.cpar[c] = (uint32_t)p;
+    for (uint64_t i = tid; i <= a.tb.lmask; i += nt) {
+      a.tb.ltab[i].k0 = EMPTY;
+      a.tb.ltab[i].k1 = EMPTY;
+      a.tb.ltab[i].tag = EMPTY;
+      a.tb.ltab[i].ref = EMPTY;
+    }
+    __syncthreads();
+    for (uint64_t c = tid; c < Tn; c += nt) {
+      const uint32_t p = a.cpar[c];
+      uint64_t t = c - a.off[p];
+      uint64_t fa = a.fpb0[p], fb = a.fpb1[p];
+      const uint64_t* nd = a.nd + (uint64_t)p * KMAX;
+      for (int i = a.ndc[p] - 1; i >= 0 && t; --i) {
+        const int32_t s = (int32_t)(nd[i] >> 32), v = (int32_t)(uint32_t)nd[i];
+        const uint64_t d = (uint64_t)count_applicable(S, s, v);
+        const int x = (int)(t % d);
+        t /= d;
+        if (x) {
+          const int rf = nth_applicable(S, s, v, 0), rc = nth_applicable(S, s, v, x);
+          fa += __ldg(S.h0 + rc) - __ldg(S.h0 + rf);
+          fb += __ldg(S.h1 + rc) - __ldg(S.h1 + rf);
+        }
+      }
+      a.cfp0[c] = fa;
+      a.cfp1[c] = fb;
+    }
+    __syncthreads();
+    // ---- K-d: visited (earlier levels, A6), level table with the minimum tag (A7)
+    for (uint64_t c = tid; c < Tn; c += nt) {
+      const uint64_t k0 = a.cfp0[c], k1 = a.cfp1[c];
+      if (k0 == EMPTY && k1 == EMPTY) {
+        atomicOr(&sh_err, ERR_COLLISION);
+        a.verdict[c] = 0;
+        a.cref[c] = EMPTY;
+        continue;
+      }
+      const uint64_t h = fmix64(k0);
+      bool old = false;
+      uint64_t i = h & a.tb.vmask;
+      for (uint64_t probes = 0; probes <= a.tb.vmask; ++probes, i = (i + 1) & a.tb.vmask) {
+        const Key128 key = *reinterpret_cast<const Key128*>(a.tb.vis + i);
+        if (key.k0 == k0 && key.k1 == k1) {
+          old = true;
+          a.cref[c] = a.tb.vis[i].ref;
+          break;
+        }
+        if (key.k0 == EMPTY && key.k1 == EMPTY) break;
+      }
+      if (old) {
+        a.verdict[c] = 0;
+        continue;
+      }
+      bool ins = false;
+      i = h & a.tb.lmask;
+      for (uint64_t probes = 0; probes <= a.tb.lmask; ++probes, i = (i + 1) & a.tb.lmask) {
+        Key128 empty{EMPTY, EMPTY}, mine{k0, k1};
+        const Key128 prev = atomicCAS(reinterpret_cast<Key128*>(a.tb.ltab + i), empty, mine);
+        if ((prev.k0 == EMPTY && prev.k1 == EMPTY) || (prev.k0 == k0 && prev.k1 == k1)) {
+          atomicMin(&a.tb.ltab[i].tag, (unsigned long long)c);
+          a.cslot[c] = i;
+          a.verdict[c] = 1;
+          ins = true;
+          break;
+        }
+      }
+      if (!ins) atomicOr(&sh_err, ERR_TABLE_FULL);
+    }
+    __syncthreads();
+    for (uint64_t c = tid; c < Tn; c += nt)
+      if (a.verdict[c] == 1 && a.tb.ltab[a.cslot[c]].tag == c) atomicAdd(&sh_u64[0], 1ULL);
+    __syncthreads();
+    if (tid == 0) {
+      const uint64_t n_new = sh_u64[0];
+      sh_thin = a.frontier_target > 0 && n_new > (uint64_t)a.frontier_target;
+      sh_tau = sh_thin ? tau_div((uint64_t)a.frontier_target, n_new) : 0;  // reading A19
+    }
+    __syncthreads();
+    // kept flags and their exclusive scan (1024 contiguous partial sums)
+    const uint64_t per = (Tn + nt - 1) / nt;
+    {
+      uint64_t sum = 0;
+      for (uint64_t c = tid * per; c < Tn && c < (tid + 1) * per; ++c) {
+        uint64_t k = 0;
+        if (a.verdict[c] == 1 && a.tb.ltab[a.cslot[c]].tag == c) k = sh_thin ? (fmix64(a.cfp0[c]) < sh_tau) : 1;
+        a.kept[c] = k;
+        sum += k;
+      }
+      sh_part[tid] = sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t acc = 0;
+      for (int i = 0; i < nt; ++i) {
+        const uint64_t x = sh_part[i];
+        sh_part[i] = acc;
+        acc += x;
+      }
+      sh_K = acc;
+    }
+    __syncthreads();
+    {
+      uint64_t acc = sh_part[tid];
+      for (uint64_t c = tid * per; c < Tn && c < (tid + 1) * per; ++c) {
+        a.kpos[c] = acc;
+        acc += a.kept[c];
+      }
+    }
+    __syncthreads();
+    const int64_t K = (int64_t)sh_K;
+    const uint64_t level = (uint64_t)(a.level0 + lev + 1);
+    uint8_t* ndata = a.data_pool + (size_t)lev * a.data_stride;
+    int64_t* npar = a.parent_pool + (size_t)lev * SMALL_T;
+    uint64_t* nt_ = a.t_pool + (size_t)lev * SMALL_T;
+    uint64_t* nfp0 = a.fp0_pool + (size_t)lev * SMALL_T;
+    uint64_t* nfp1 = a.fp1_pool + (size_t)lev * SMALL_T;
+    // compaction in tag order + visited insert
+    for (uint64_t c = tid; c < Tn; c += nt) {
+      if (!a.kept[c]) continue;
+      const uint64_t q = a.kpos[c];
+      const uint32_t p = a.cpar[c];
+      npar[q] = p;
+      nt_[q] = c - a.off[p];
+      nfp0[q] = a.cfp0[c];
+      nfp1[q] = a.cfp1[c];
+      visited_insert(a.tb, a.cfp0[c], a.cfp1[c], (level << 40) | q, &sh_err);
+    }
+    __syncthreads();
+    // ---- K-c: every kept child exactly (eq. (2) column by column), tail zeroed
+    T* nd_out = reinterpret_cast<T*>(ndata);
+    for (int64_t q = tid; q < K; q += nt) {
+      const int64_t p = npar[q];
+      ChildCtx cx;
+      decode_child(S, a.nd + p * KMAX, a.ndc[p], nt_[q], cx);
+      bool bad = false;
+      for (int32_t j = 0; j < m; ++j) {
+        const int64_t val = exact_value<T>(S, data, p, j, cx);
+        bad |= (val < 0 || val > S.count_max);
+        nd_out[eidx(q, j, m)] = (T)val;
+      }
+      if (bad) atomicOr(&sh_err, ERR_OVERFLOW);
+    }
+    if (K % PB)
+      for (int64_t i = tid; i < (int64_t)m * (PB - K % PB); i += nt)
+        nd_out[((K / PB) * m + i / (PB - K % PB)) * PB + K % PB + i % (PB - K % PB)] = 0;
+    if (a.dedup == 0 && tid == 0) a.stored[level].data = ndata;
+    __syncthreads();
+    // ---- dedup = 0: every key match compared as full configurations (A18)
+    if (a.dedup == 0) {
+      for (uint64_t c = tid; c < Tn; c += nt) {
+        const uint8_t vd = a.verdict[c];
+        uint64_t other = EMPTY;
+        if (vd == 1) {
+          const uint64_t wtag = a.tb.ltab[a.cslot[c]].tag;
+          if (wtag == c) continue;
+          other = wtag;
+        } else if (a.cref[c] == EMPTY) {
+          continue;
+        }
+        const uint32_t p = a.cpar[c];
+        ChildCtx cx, co;
+        decode_child(S, a.nd + (uint64_t)p * KMAX, a.ndc[p], c - a.off[p], cx);
+        uint32_t po = 0;
+        if (vd == 1) {
+          po = a.cpar[other];
+          decode_child(S, a.nd + (uint64_t)po * KMAX, a.ndc[po], other - a.off[po], co);
+        }
+        bool diff = false;
+        for (int32_t j = 0; j < m && !diff; ++j) {
+          const int64_t x = exact_value<T>(S, data, p, j, cx);
+          int64_t y;
+          if (vd == 1) {
+            y = exact_value<T>(S, data, po, j, co);
+          } else {
+            const uint64_t ref = a.cref[c];
+            y = ld_count<T>(a.stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, m);
+          }
+          diff = x != y;
+        }
+        if (diff) atomicOr(&sh_err, ERR_COLLISION);
+      }
+    }
+    // ---- digest
+    for (int64_t q = tid; q < K; q += nt) {
+      uint64_t z = fmix64((level << 40) ^ (uint64_t)q);
+      z = fmix64(z ^ nfp0[q]);
+      z = fmix64(z ^ nfp1[q]);
+      z = fmix64(z ^ (uint64_t)(npar[q] + 1));
+      z = fmix64(z ^ nt_[q]);
+      atomicAdd(&sh_u64[2], (unsigned long long)z);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      o->T = (int64_t)Tn;
+      o->n_new = (int64_t)sh_u64[0];
+      o->kept = K;
+      o->n_halting = (int64_t)sh_u64[1];
+      o->tau = sh_tau;
+      o->digest = sh_u64[2];
+      o->err = sh_err;
+      o->stop = 0;
+    }
+    __syncthreads();
+    if (sh_err) break;
+    ++done;
+    // the new level becomes the current one
+    data = ndata;
+    F = K;
+    fp0 = nfp0;
+    fp1 = nfp1;
+    halting = a.halting_pool + (size_t)lev * SMALL_T;
+    if (K == 0 || K > SMALL_F) break;
+    __syncthreads();
+  }
+  if (tid == 0) *a.levels_done = done;
 }
 
 // order-sensitive run digest
@@ -3201,14 +3546,21 @@ void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const Ex
   if (g > 148u * 64u) g = 148u * 64u;
   dispatch_bytes(bytes, [&](auto tt) {
     using TT = decltype(tt);
-    const size_t sm = verify_smem_bytes(S.m);
+    const size_t sm = verify_smem_bytes(S.m, S.small_cp ? 2 : 8);
     if (sm <= 200 * 1024 && S.delay_m == 0) {
       cudaMemsetAsync(n_list, 0, sizeof(unsigned long long), st);
       k_verify_need<<<grid_for(T), BLK, 0, st>>>(C, T, tag_base, tb, list, n_list);
       count_launch();
-      cudaFuncSetAttribute(k_verify_s<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_verify_s<TT><<<148u * 2u, VERIFY_WARPS * 32, sm, st>>>(S, L, O, off, C, list, n_list, tag_base, tb, stored,
-                                                              err);
+      const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(8, (200u * 1024u) / sm));
+      if (S.small_cp) {
+        cudaFuncSetAttribute(k_verify_s<TT, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_verify_s<TT, uint16_t><<<148u * per_sm, VERIFY_WARPS * 32, sm, st>>>(S, L, O, off, C, list, n_list,
+                                                                                tag_base, tb, stored, err);
+      } else {
+        cudaFuncSetAttribute(k_verify_s<TT, int2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_verify_s<TT, int2><<<148u * per_sm, VERIFY_WARPS * 32, sm, st>>>(S, L, O, off, C, list, n_list, tag_base,
+                                                                            tb, stored, err);
+      }
     } else {
       k_verify<TT><<<g, 256, 0, st>>>(S, L, O, off, C, T, tag_base, tb, stored, err);
     }
@@ -3241,6 +3593,14 @@ void launch_zero_tail(int32_t bytes, void* data, int64_t F, int32_t m, cudaStrea
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
     k_zero_tail<T><<<grid_for((uint64_t)m * (PB - F % PB)), BLK, 0, st>>>(reinterpret_cast<T*>(data), F, m);
+  });
+  count_launch();
+}
+
+void launch_small_bfs(const SysView& S, int32_t bytes, const SmallArgs& a, cudaStream_t st) {
+  dispatch_bytes(bytes, [&](auto tt) {
+    using T = decltype(tt);
+    k_small_bfs<T><<<1, 1024, 0, st>>>(S, a);
   });
   count_launch();
 }

@@ -365,3 +365,36 @@ def test_generic_neurons(snp):
             ref = oracle.System.from_workload(w).explore(C0, depth=4, dedup=dedup, count_bits=bits,
                                                          frontier_target=300)
             assert_same_tree(tree, ref)
+
+
+# ---- the single-CTA small-frontier path (k_small_bfs) against the big path ---
+@pytest.mark.parametrize("case", ["pi_sim", "pi_text", "tiny", "random_thin", "random_exact16", "grow"])
+def test_small_path_equals_big_path(snp, monkeypatch, case):
+    """k_small_bfs runs whole levels of small frontiers in one launch; the
+    multi-kernel path (SNP_SMALL=0) and the oracle give the same tree."""
+    kw, L0, depth = {}, None, 12
+    if case == "pi_sim":
+        w, depth = W.pi_system("simulator"), 60
+    elif case == "pi_text":
+        w = W.pi_system("textbook")
+    elif case == "tiny":
+        w = W.tiny_random_system(17)
+        kw = dict(dedup=1)
+    elif case == "random_thin":
+        w = W.random_system(40, outdeg=4, k_nd=6, seed=2)
+        L0, depth, kw = W.level0_counts(w, 30, 2), 6, dict(count_bits=8, dedup=1, frontier_target=40)
+    elif case == "random_exact16":
+        w = W.random_system(30, outdeg=4, k_nd=5, seed=3)
+        L0, depth, kw = W.level0_counts(w, 20, 3), 5, dict(count_bits=16, dedup=0, frontier_target=100)
+    else:  # frontier outgrows SMALL_F / SMALL_T: the levels move to the big path mid-run
+        w = W.random_system(64, outdeg=6, k_nd=8, seed=4)
+        L0, depth, kw = W.level0_counts(w, 8, 4), 4, dict(count_bits=8, dedup=1)
+    monkeypatch.setenv("SNP_SMALL", "1")
+    small = snp.System(w, **kw).explore(L0, depth=depth)
+    monkeypatch.setenv("SNP_SMALL", "0")
+    big = snp.System(w, **kw).explore(L0, depth=depth)
+    ref = oracle.System.from_workload(w).explore(w.C0 if L0 is None else L0, depth=depth,
+                                                 **{k: v for k, v in kw.items()})
+    assert_same_tree(small, ref)
+    assert_same_tree(big, ref)
+    assert small.counters.halting.tolist() == big.counters.halting.tolist()
