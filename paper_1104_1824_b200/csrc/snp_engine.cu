@@ -1334,6 +1334,7 @@ snp_status advance_small(snp_system* s, int32_t want, int32_t* done) {
   a.tb = tb;
   a.stored = s->small_stored.as<StoredLevel>();
   a.frontier_target = s->opt.frontier_target;
+  a.max_transitions = s->opt.max_transitions;
   a.dedup = s->opt.dedup;
   a.out = s->small_out.as<SmallLevelOut>();
   a.levels_done = reinterpret_cast<int32_t*>(s->small_out.as<uint8_t>() + (size_t)L * sizeof(SmallLevelOut));
@@ -1417,25 +1418,24 @@ snp_status snapshot(snp_system* s, snp_tree** out) {
   t->t.resize(total);
   t->halting.resize(total);
   t->fp.resize(2 * total);
-  std::vector<uint64_t> f0, f1;
+  // every level's arrays copied on the stream, one synchronisation
+  std::vector<uint64_t> f0(total), f1(total);
   int64_t o = 0;
   for (auto& L : s->levels) {
     const int64_t F = L->F;
     if (F) {
-      f0.resize(F);
-      f1.resize(F);
       CUDA_TRY(cudaMemcpyAsync(t->parent.data() + o, L->parent.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
       CUDA_TRY(cudaMemcpyAsync(t->t.data() + o, L->t.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
       CUDA_TRY(cudaMemcpyAsync(t->halting.data() + o, L->halting.p, F, cudaMemcpyDeviceToHost, s->stream));
-      CUDA_TRY(cudaMemcpyAsync(f0.data(), L->fp0.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
-      CUDA_TRY(cudaMemcpyAsync(f1.data(), L->fp1.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
-      SNP_TRY(sync(s));
-      for (int64_t i = 0; i < F; ++i) {
-        t->fp[2 * (o + i)] = f0[i];
-        t->fp[2 * (o + i) + 1] = f1[i];
-      }
+      CUDA_TRY(cudaMemcpyAsync(f0.data() + o, L->fp0.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(cudaMemcpyAsync(f1.data() + o, L->fp1.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
     }
     o += F;
+  }
+  SNP_TRY(sync(s));
+  for (int64_t i = 0; i < total; ++i) {
+    t->fp[2 * i] = f0[i];
+    t->fp[2 * i + 1] = f1[i];
   }
   *out = t.release();
   return SNP_OK;

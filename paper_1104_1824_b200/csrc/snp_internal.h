@@ -191,6 +191,7 @@ struct SmallArgs {
   Tables tb;                 // visited + a level table of >= 2·SMALL_T slots
   StoredLevel* stored;       // dedup = 0: data of every tree level (new ones written here)
   int64_t frontier_target;
+  int64_t max_transitions;   // per-level budget (0 = none)
   int32_t dedup;
   SmallLevelOut* out;        // max_levels
   int32_t* levels_done;

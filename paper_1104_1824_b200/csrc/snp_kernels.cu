@@ -2399,8 +2399,11 @@ __device__ uint64_t tau_div(uint64_t F, uint64_t N) {
   return q;
 }
 
+using SmallScan = cub::BlockScan<uint64_t, 1024>;
+
 template <typename T>
 __global__ void __launch_bounds__(1024) k_small_bfs(SysView S, SmallArgs a) {
+  __shared__ typename SmallScan::TempStorage scan_tmp;
   __shared__ unsigned long long sh_u64[4];  // [0] n_new, [1] n_halting, [2] digest
   __shared__ int32_t sh_err, sh_stop;
   __shared__ uint64_t sh_T, sh_K, sh_tau, sh_part[1024];
@@ -2461,6 +2464,7 @@ __global__ void __launch_bounds__(1024) k_small_bfs(SysView S, SmallArgs a) {
       }
       a.off[F] = acc;
       sh_T = acc;
+      if (!sh_err && a.max_transitions > 0 && acc > (uint64_t)a.max_transitions) sh_err = ERR_CAPACITY;  // budget
       if (!sh_err && acc > (uint64_t)SMALL_T) sh_stop = 1;
     }
     __syncthreads();
@@ -2555,27 +2559,20 @@ __global__ void __launch_bounds__(1024) k_small_bfs(SysView S, SmallArgs a) {
       sh_tau = sh_thin ? tau_div((uint64_t)a.frontier_target, n_new) : 0;  // reading A19
     }
     __syncthreads();
-    // kept flags and their exclusive scan (1024 contiguous partial sums)
+    // kept flags and their exclusive scan (contiguous chunks, block scan of the chunk sums)
     const uint64_t per = (Tn + nt - 1) / nt;
-    {
-      uint64_t sum = 0;
-      for (uint64_t c = tid * per; c < Tn && c < (tid + 1) * per; ++c) {
-        uint64_t k = 0;
-        if (a.verdict[c] == 1 && a.tb.ltab[a.cslot[c]].tag == c) k = sh_thin ? (fmix64(a.cfp0[c]) < sh_tau) : 1;
-        a.kept[c] = k;
-        sum += k;
-      }
-      sh_part[tid] = sum;
+    uint64_t sum = 0;
+    for (uint64_t c = tid * per; c < Tn && c < (tid + 1) * per; ++c) {
+      uint64_t k = 0;
+      if (a.verdict[c] == 1 && a.tb.ltab[a.cslot[c]].tag == c) k = sh_thin ? (fmix64(a.cfp0[c]) < sh_tau) : 1;
+      a.kept[c] = k;
+      sum += k;
     }
-    __syncthreads();
-    if (tid == 0) {
-      uint64_t acc = 0;
-      for (int i = 0; i < nt; ++i) {
-        const uint64_t x = sh_part[i];
-        sh_part[i] = acc;
-        acc += x;
-      }
-      sh_K = acc;
+    {
+      uint64_t excl, total;
+      SmallScan(scan_tmp).ExclusiveSum(sum, excl, total);
+      sh_part[tid] = excl;
+      if (tid == 0) sh_K = total;
     }
     __syncthreads();
     {

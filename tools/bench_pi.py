@@ -29,13 +29,22 @@ def main():
             tree = eng.explore(None, depth=depth)
             te = time.perf_counter() - t0
             launches = snp.snp_kernel_launches()
+            # the ABI call alone (snp_explore + snp_tree_free, no Python-side copies)
+            import ctypes
+            L = snp.lib()
+            h = ctypes.c_void_p()
+            t0 = time.perf_counter()
+            st = L.snp_explore(eng._h, None, depth, ctypes.byref(h))
+            ta = time.perf_counter() - t0
+            L.snp_tree_free(h)
+            assert st == 0
             t0 = time.perf_counter()
             ref = oracle.System.from_workload(w).explore(w.C0, depth=depth)
             to = time.perf_counter() - t0
             same = bool((tree.configs == ref.configs).all() and (tree.parent == ref.parent).all())
             print(json.dumps({"workload": f"Π ({enc} encoding) to depth {depth}", "configs": int(tree.num_configs),
                               "transitions": int(tree.counters.T.sum()), "engine_ms": 1e3 * te,
-                              "engine_first_run_ms": 1e3 * tf,
+                              "engine_first_run_ms": 1e3 * tf, "abi_snp_explore_ms": 1e3 * ta,
                               "oracle_ms": 1e3 * to, "levels": int(tree.num_levels),
                               "equal_to_oracle": same, "kernel_launches_total": launches}))
 
