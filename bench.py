@@ -277,8 +277,11 @@ def run_native(args, rank, world):
     runner.begin(snp.configs_from_device(buf.data_ptr(), Fl, max(Fl, 1), wb, snp.SNP_LAYOUT_NEURON_MAJOR))
     del buf
     torch.cuda.empty_cache()
+    digest_at = {}  # run digest after `steps` levels, compared with the e2e run's (same levels from the same level 0)
     for _ in range(args.warmup):
         runner.advance()
+        if eng.depth == args.steps and not use_dist:
+            digest_at[args.steps] = eng.summary()[2]
     prof0 = eng.profile()
     launches0 = snp.snp_kernel_launches()
     clocks = Clocks(torch.cuda.current_device())
@@ -294,6 +297,8 @@ def run_native(args, rank, world):
         levels.append(runner.advance())
         if not use_dist:
             lvl_prof.append(eng.profile())  # cumulative phase times: per-level deltas below (drift attribution)
+            if eng.depth == args.steps:
+                digest_at[args.steps] = eng.summary()[2]  # a host read of the running sum: no device work
     e1.record(stream)
     torch.cuda.synchronize()
     if dist:
@@ -351,7 +356,8 @@ def run_native(args, rank, world):
     del eng, runner
     torch.cuda.empty_cache()
     if not args.no_e2e:
-        out["e2e"] = run_e2e(args, cfg, w, snp, torch, rank, world, dist if use_dist else None)
+        out["e2e"] = run_e2e(args, cfg, w, snp, torch, rank, world, dist if use_dist else None,
+                             digest_at.get(args.steps))
     if not args.no_cpu and rank == 0 and world == 1:
         out["cpu_baseline"] = cpu_baseline(w, cfg)
     if rank == 0:
@@ -361,7 +367,7 @@ def run_native(args, rank, world):
         dist.destroy_process_group()
 
 
-def run_e2e(args, cfg, w, snp, torch, rank=0, world=1, dist=None):
+def run_e2e(args, cfg, w, snp, torch, rank=0, world=1, dist=None, device_digest=None):
     """The user's call path: level 0 from a pinned HOST buffer (row-major;
     snp_begin, or snp_dist_start with this rank's slice), then per level
     snp_advance / snp_dist_advance and the new level's edges + fingerprints
@@ -423,6 +429,7 @@ def run_e2e(args, cfg, w, snp, torch, rank=0, world=1, dist=None):
         t_adv += tb - ta
         t_edges += time.perf_counter() - tb
     dt_s = time.perf_counter() - t0
+    e2e_digest = runner.summary()[2]
     if dist is not None:
         tt = torch.tensor([dt_s, d2h], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
@@ -432,6 +439,8 @@ def run_e2e(args, cfg, w, snp, torch, rank=0, world=1, dist=None):
     del host
     return {"value": T_sum / dt_s, "unit": UNIT, "h2d_bytes_per_step": F * m * wb // args.steps,
             "d2h_bytes_per_step": d2h // args.steps,
+            "digest": f"{e2e_digest:016x}",
+            "digest_equal_device_run": (None if device_digest is None else e2e_digest == device_digest),
             "breakdown_s": {"begin (level-0 H2D + import + dedup)": round(t_begin, 4), "advance": round(t_adv, 4),
                             "edges D2H": round(t_edges, 4), "total": round(dt_s, 4),
                             "h2d_GBps_through_begin": round(Fl * m * wb / t_begin / 1e9, 2),

@@ -29,6 +29,11 @@ def main():
             tree = eng.explore(None, depth=depth)
             te = time.perf_counter() - t0
             launches = snp.snp_kernel_launches()
+            t0 = time.perf_counter()
+            ref = oracle.System.from_workload(w).explore(w.C0, depth=depth)
+            to = time.perf_counter() - t0
+            same = bool((tree.configs == ref.configs).all() and (tree.parent == ref.parent).all())
+            tree.close()
             # the ABI call alone (snp_explore + snp_tree_free, no Python-side copies)
             import ctypes
             L = snp.lib()
@@ -38,10 +43,6 @@ def main():
             ta = time.perf_counter() - t0
             L.snp_tree_free(h)
             assert st == 0
-            t0 = time.perf_counter()
-            ref = oracle.System.from_workload(w).explore(w.C0, depth=depth)
-            to = time.perf_counter() - t0
-            same = bool((tree.configs == ref.configs).all() and (tree.parent == ref.parent).all())
             print(json.dumps({"workload": f"Π ({enc} encoding) to depth {depth}", "configs": int(tree.num_configs),
                               "transitions": int(tree.counters.T.sum()), "engine_ms": 1e3 * te,
                               "engine_first_run_ms": 1e3 * tf, "abi_snp_explore_ms": 1e3 * ta,
