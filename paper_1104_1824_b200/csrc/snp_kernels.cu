@@ -1507,6 +1507,9 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_PREFETCH
 #define SNP_KC_PREFETCH 0
 #endif
+#ifndef SNP_KC_FLATQ
+#define SNP_KC_FLATQ 0  // cooperative quads in passes over the CTA's own quad range (else per output block)
+#endif
 #ifndef SNP_KC_EPF
 #define SNP_KC_EPF 0  // k > 0: L2 bulk prefetch of block blk + k's emit words at CTA start (A/B: 148 = one wave ahead)
 #endif
@@ -1984,11 +1987,23 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       const int32_t jn = m - jbase;  // rows of this warp that exist
       const uint8_t* xr0 = sX + (size_t)(warp * 32 + j0) * xs_stride<T>();
       const uint64_t qa = (Q0 + 3) & ~3ULL, qb = Q1 & ~3ULL;
+#if SNP_KC_FLATQ
+      // passes over the CTA's own full quads [qa, qb), 16 per pass (lane
+      // hl takes quad qa + 4·(16·pass + hl), whichever output block it is
+      // in): one pass when the CTA has <= 16 full quads
+      for (uint64_t q0 = qa; !(SNP_KC_ABLATE & 4) && q0 < qb; q0 += 64) {
+        const uint64_t q = q0 + 4 * hl;
+        if (q < qb) {
+          const uint64_t ob = q >> 6;
+          const uint32_t d = sD[(q - Qb) >> 2];
+          uint8_t* dst0 = reinterpret_cast<uint8_t*>(out) + (((int64_t)ob * m + jbase + j0) << 6) + (q & 63);
+#else
       for (uint64_t ob = qa >> 6; !(SNP_KC_ABLATE & 4) && qa < qb && ob <= (qb - 1) >> 6; ++ob) {
         const uint64_t q = (ob << 6) + 4 * hl;
         if (q >= qa && q < qb) {
           const uint32_t d = sD[(q - Qb) >> 2];
           uint8_t* dst0 = reinterpret_cast<uint8_t*>(out) + (((int64_t)ob * m + jbase + j0) << 6) + 4 * hl;
+#endif
           if (!(d & 0x80000000u)) {
             const uint32_t* w0 = reinterpret_cast<const uint32_t*>(xr0) + ((d >> 16) & 31);
             const uint32_t sel = d & 0xFFFFu, hb = d >> 24;
