@@ -833,6 +833,9 @@ constexpr int TC_STAGES = 2;                     // X|Y tiles: double-buffered
 #ifndef SNP_TC_L2PF
 #define SNP_TC_L2PF 0  // K-a: L2 bulk prefetch of the counts this many chunks ahead (producer warp); measured slower: 2 / 4 / 8 chunks 19.9 / 20.1 / 20.1 ms vs 19.6 off
 #endif
+#ifndef SNP_TC_MINB
+#define SNP_TC_MINB 1  // K-a: resident CTAs the register budget is sized for (3 by default at 72 registers; A/B 4)
+#endif
 #ifndef SNP_TC_WS
 #define SNP_TC_WS 1  // producer warp for copies + MMAs (else thread 0 issues them after a CTA barrier)
 #endif
@@ -855,7 +858,7 @@ __device__ __forceinline__ uint32_t lut16(uint32_t v4, const uint32_t (&tt)[8]) 
 // WS: a ninth (producer) warp issues the bulk copies and the MMAs; the 256
 // compute threads only arrive on a per-stage mbarrier (no CTA barrier per chunk)
 template <bool WS>
-__global__ void __launch_bounds__(TCT + 32) k_expand_tc(SysView S, LevelView L, ExpandOut O) {
+__global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, LevelView L, ExpandOut O) {
   extern __shared__ __align__(128) uint8_t smem_tc[];
   uint8_t* smem = smem_tc;
   uint8_t* sIn = smem + TC_STAGES * TC_STAGE;                       // [TC_IN][B_X | B_Y | tables]
@@ -3396,6 +3399,7 @@ void launch_expand(const SysView& S, int32_t bytes, const LevelView& L, const Ex
         const size_t sm = expand_tc_smem_bytes();
         auto kern = SNP_TC_WS ? k_expand_tc<true> : k_expand_tc<false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (SNP_TC_MINB > 3) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         const int64_t nblk = (L.F + PB - 1) / PB;
         kern<<<(unsigned)((nblk + 1) / 2), TCT + (SNP_TC_WS ? 32 : 0), sm, st>>>(S, L, O);
         if (!O.classify_only) {
