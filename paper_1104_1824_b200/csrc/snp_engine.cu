@@ -221,6 +221,7 @@ struct snp_system {
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   DBuf edge_scratch;  // snp_level_edges: fp0/fp1 interleave
   DBuf vlist;         // dedup = 0: the transitions to verify
+  DBuf snap_scratch;  // snapshot: packed edge arrays
   DBuf gen;           // generated-number bitmap (out_rule1 > 0)
   std::vector<DBuf> spare;  // released level buffers kept for reuse
   Arena arena;              // per-level metadata
@@ -1418,24 +1419,34 @@ snp_status snapshot(snp_system* s, snp_tree** out) {
   t->t.resize(total);
   t->halting.resize(total);
   t->fp.resize(2 * total);
-  // every level's arrays copied on the stream, one synchronisation
-  std::vector<uint64_t> f0(total), f1(total);
-  int64_t o = 0;
-  for (auto& L : s->levels) {
-    const int64_t F = L->F;
-    if (F) {
-      CUDA_TRY(cudaMemcpyAsync(t->parent.data() + o, L->parent.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
-      CUDA_TRY(cudaMemcpyAsync(t->t.data() + o, L->t.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
-      CUDA_TRY(cudaMemcpyAsync(t->halting.data() + o, L->halting.p, F, cudaMemcpyDeviceToHost, s->stream));
-      CUDA_TRY(cudaMemcpyAsync(f0.data() + o, L->fp0.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
-      CUDA_TRY(cudaMemcpyAsync(f1.data() + o, L->fp1.p, F * 8, cudaMemcpyDeviceToHost, s->stream));
+  // every level's arrays packed on the device (one kernel), then one copy per
+  // array and one synchronisation (configs 1-2 have hundreds of tiny levels)
+  if (total > 0) {
+    std::vector<EdgeSrc> src;
+    int64_t o = 0, max_F = 0;
+    for (auto& L : s->levels) {
+      if (L->F)
+        src.push_back(EdgeSrc{L->parent.as<int64_t>(), L->t.as<uint64_t>(), L->halting.as<uint8_t>(),
+                              L->fp0.as<uint64_t>(), L->fp1.as<uint64_t>(), L->F, o});
+      o += L->F;
+      max_F = std::max(max_F, L->F);
     }
-    o += F;
-  }
-  SNP_TRY(sync(s));
-  for (int64_t i = 0; i < total; ++i) {
-    t->fp[2 * i] = f0[i];
-    t->fp[2 * i + 1] = f1[i];
+    const size_t need = src.size() * sizeof(EdgeSrc) + (size_t)total * (8 + 8 + 16 + 1) + 256;
+    SNP_TRY(s->snap_scratch.ensure(need));
+    uint8_t* b = s->snap_scratch.as<uint8_t>();
+    EdgeSrc* d_src = reinterpret_cast<EdgeSrc*>(b);
+    int64_t* d_par = reinterpret_cast<int64_t*>(b + ((src.size() * sizeof(EdgeSrc) + 15) & ~(size_t)15));
+    uint64_t* d_t = reinterpret_cast<uint64_t*>(d_par + total);
+    uint64_t* d_fp = d_t + total;
+    uint8_t* d_h = reinterpret_cast<uint8_t*>(d_fp + 2 * total);
+    CUDA_TRY(cudaMemcpyAsync(d_src, src.data(), src.size() * sizeof(EdgeSrc), cudaMemcpyHostToDevice, s->stream));
+    launch_pack_edges(d_src, (int32_t)src.size(), max_F, d_par, d_t, d_h, d_fp, s->stream);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(t->parent.data(), d_par, (size_t)total * 8, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(t->t.data(), d_t, (size_t)total * 8, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(t->fp.data(), d_fp, (size_t)total * 16, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(t->halting.data(), d_h, (size_t)total, cudaMemcpyDeviceToHost, s->stream));
+    SNP_TRY(sync(s));
   }
   *out = t.release();
   return SNP_OK;
@@ -1854,15 +1865,29 @@ snp_status snp_tree_configs(const snp_tree* t, int32_t* out) {
   snp_system* s = t->sys;
   DBuf tmp;
   const int32_t nl = snp_tree_num_levels(t);
-  for (int32_t L = 0; L < nl; ++L) {
-    const Level* lv = s->levels[L].get();
-    if (!lv->F) continue;
-    SNP_TRY(tmp.ensure((size_t)lv->F * s->m * 4));
-    launch_export(lv->data.p, s->bytes, lv->F, (int32_t)s->m, tmp.as<int32_t>(), s->stream);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(out + t->level_offsets[L] * s->m, tmp.p, (size_t)lv->F * s->m * 4,
-                             cudaMemcpyDeviceToHost, s->stream));
-    SNP_TRY(sync(s));
+  // consecutive levels exported into one staging buffer of up to 1 GB (or one
+  // level when larger), one copy and one synchronisation per batch
+  const size_t cap = std::max<size_t>((size_t)1 << 30, 0);
+  for (int32_t L0 = 0; L0 < nl;) {
+    size_t bytes = 0;
+    int32_t L1 = L0;
+    while (L1 < nl && (L1 == L0 || bytes + (size_t)s->levels[L1]->F * s->m * 4 <= cap))
+      bytes += (size_t)s->levels[L1++]->F * s->m * 4;
+    if (bytes) {
+      SNP_TRY(tmp.ensure(bytes));
+      size_t o = 0;
+      for (int32_t L = L0; L < L1; ++L) {
+        const Level* lv = s->levels[L].get();
+        if (!lv->F) continue;
+        launch_export(lv->data.p, s->bytes, lv->F, (int32_t)s->m, reinterpret_cast<int32_t*>(tmp.as<uint8_t>() + o),
+                      s->stream);
+        o += (size_t)lv->F * s->m * 4;
+      }
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpyAsync(out + t->level_offsets[L0] * s->m, tmp.p, bytes, cudaMemcpyDeviceToHost, s->stream));
+      SNP_TRY(sync(s));
+    }
+    L0 = L1;
   }
   return SNP_OK;
 }

@@ -111,6 +111,17 @@ void launch_level0_compact(const uint8_t* verdict, const uint64_t* kept, const u
                            const Tables& tb, int insert_visited, int32_t* err, cudaStream_t st);
 void launch_gather_columns(int32_t bytes, const void* src, const uint64_t* src_index, int64_t K, int32_t m, void* dst,
                            cudaStream_t st);
+// snapshot: one level's edge arrays and where they go in the packed output
+struct EdgeSrc {
+  const int64_t* parent;
+  const uint64_t* t;
+  const uint8_t* halting;
+  const uint64_t* fp0;
+  const uint64_t* fp1;
+  int64_t F, offset;
+};
+void launch_pack_edges(const EdgeSrc* lv, int32_t nlev, int64_t max_F, int64_t* parent, uint64_t* t,
+                       uint8_t* halting, uint64_t* fp2, cudaStream_t st);
 // zero the unused configurations of a level's last 64-configuration block
 void launch_zero_tail(int32_t bytes, void* data, int64_t F, int32_t m, cudaStream_t st);
 // a[i] += add for every a[i] >= 0 (multi-GPU: local -> global parent indices)

@@ -2343,6 +2343,22 @@ __global__ void k_zero_tail(T* data, int64_t F, int32_t m) {
     data[(b * m + i / (PB - r0)) * PB + r0 + i % (PB - r0)] = 0;
 }
 
+// snapshot: every level's edge arrays into one contiguous set (one D2H each)
+__global__ void k_pack_edges(const EdgeSrc* lv, int32_t nlev, int64_t* parent, uint64_t* t, uint8_t* halting,
+                             uint64_t* fp2) {
+  for (int32_t L = blockIdx.y; L < nlev; L += gridDim.y) {
+    const EdgeSrc e = lv[L];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e.F; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t o = e.offset + i;
+      parent[o] = e.parent[i];
+      t[o] = e.t[i];
+      halting[o] = e.halting[i];
+      fp2[2 * o] = e.fp0[i];
+      fp2[2 * o + 1] = e.fp1[i];
+    }
+  }
+}
+
 __global__ void k_add_i64(int64_t* a, int64_t n, int64_t add) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (a[i] >= 0) a[i] += add;
@@ -3618,6 +3634,14 @@ void launch_small_bfs(const SysView& S, int32_t bytes, const SmallArgs& a, cudaS
     using T = decltype(tt);
     k_small_bfs<T><<<1, 1024, 0, st>>>(S, a);
   });
+  count_launch();
+}
+
+void launch_pack_edges(const EdgeSrc* lv, int32_t nlev, int64_t max_F, int64_t* parent, uint64_t* t,
+                       uint8_t* halting, uint64_t* fp2, cudaStream_t st) {
+  if (nlev <= 0 || max_F <= 0) return;
+  dim3 grid((unsigned)std::min<int64_t>((max_F + BLK - 1) / BLK, 4096), (unsigned)std::min(nlev, 65535));
+  k_pack_edges<<<grid, BLK, 0, st>>>(lv, nlev, parent, t, halting, fp2);
   count_launch();
 }
 
