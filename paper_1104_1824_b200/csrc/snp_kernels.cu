@@ -834,7 +834,7 @@ constexpr int TC_STAGES = 2;                     // X|Y tiles: double-buffered
 #define SNP_TC_L2PF 0  // K-a: L2 bulk prefetch of the counts this many chunks ahead (producer warp); measured slower: 2 / 4 / 8 chunks 19.9 / 20.1 / 20.1 ms vs 19.6 off
 #endif
 #ifndef SNP_TC_MINB
-#define SNP_TC_MINB 1  // K-a: resident CTAs the register budget is sized for (3 by default at 72 registers; A/B 4)
+#define SNP_TC_MINB 4  // K-a: resident CTAs the register budget is sized for (56 registers, 4 CTAs/SM; 1 = 72 registers, 3 CTAs: 24.3 vs 19.2 ms)
 #endif
 #ifndef SNP_TC_WS
 #define SNP_TC_WS 1  // producer warp for copies + MMAs (else thread 0 issues them after a CTA barrier)
@@ -1511,7 +1511,7 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #define SNP_KC_PREFETCH 0
 #endif
 #ifndef SNP_KC_FLATQ
-#define SNP_KC_FLATQ 0  // cooperative quads in passes over the CTA's own quad range (else per output block)
+#define SNP_KC_FLATQ 1  // cooperative quads in passes over the CTA's own quad range (else per output block: 61.0 vs 56.4 ms)
 #endif
 #ifndef SNP_KC_EPF
 #define SNP_KC_EPF 0  // k > 0: L2 bulk prefetch of block blk + k's emit words at CTA start (A/B: 148 = one wave ahead)
