@@ -196,7 +196,7 @@ snp_status snp_set_stream(snp_system *sys, void *cuda_stream);
 /* Incremental exploration (what bench.py times one level at a time):
  *   snp_begin    level 0 := distinct configurations of `level0` (first
  *                occurrence kept; NULL = {C0}) (reading A20), visited := level 0.
- *                Host row-major input is uploaded in 256 MB chunks (two device
+ *                Host row-major input is uploaded in 1 GB chunks (two device
  *                staging buffers, the copy of the next chunk overlapping the
  *                import of the current one); pinned memory (snp_host_alloc)
  *                copies at full PCIe rate, pageable memory works.  The input

@@ -932,9 +932,9 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
     // buffers, the copy of chunk i + 1 (side stream) overlaps the import of
     // chunk i, and no level-sized staging allocation is needed
     const size_t row_b = (size_t)ld * level0->elem_bytes;
-    // chunk bytes: 256 MB (SNP_UPLOAD_CHUNK_BYTES overrides, tests use it to
+    // chunk bytes: 1 GB (SNP_UPLOAD_CHUNK_BYTES overrides, tests use it to
     // run the multi-chunk path on small inputs); a multiple of 64 rows
-    size_t chunk_b = (size_t)256 << 20;
+    size_t chunk_b = (size_t)1 << 30;
     if (const char* e = getenv("SNP_UPLOAD_CHUNK_BYTES")) chunk_b = std::max<size_t>(1, strtoull(e, nullptr, 10));
     int64_t R = std::max<int64_t>(PB, (int64_t)(chunk_b / row_b) & ~(int64_t)(PB - 1));
     if (R > F0) R = F0;
