@@ -221,6 +221,7 @@ struct snp_system {
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   DBuf edge_scratch;  // snp_level_edges: fp0/fp1 interleave
   DBuf vlist;         // dedup = 0: the transitions to verify
+  DBuf vfc;           // dedup = 0: fired (c, p) rows of a verification batch
   DBuf snap_scratch;  // snapshot: packed edge arrays
   DBuf gen;           // generated-number bitmap (out_rule1 > 0)
   std::vector<DBuf> spare;  // released level buffers kept for reuse
@@ -1225,8 +1226,23 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
       SNP_TRY(update_stored_table(s));
       phase_begin(s, 4);
       SNP_TRY(s->vlist.ensure(T * 8 + 16));
-      launch_verify(s->view, s->bytes, LV, O, off, C, T, tag_base, tb, s->stored.as<StoredLevel>(),
-                    s->vlist.as<uint64_t>(), &dc(s)->n_verify, err, st);
+      if (s->view.aug_rule < 0) {
+        // the key matches listed, then verified in batches by the two fully
+        // parallel passes (fired (c, p) rows, then one thread per column)
+        launch_verify_list(C, T, tag_base, tb, s->vlist.as<uint64_t>(), &dc(s)->n_verify, st);
+        unsigned long long nv = 0;
+        CUDA_TRY(cudaMemcpyAsync(&nv, &dc(s)->n_verify, 8, cudaMemcpyDeviceToHost, st));
+        SNP_TRY(sync(s));
+        const size_t row = verify2_row_bytes(s->view);
+        const uint64_t B = std::max<uint64_t>(1, std::min<uint64_t>(nv, ((size_t)256 << 20) / row));
+        if (nv) SNP_TRY(s->vfc.ensure((size_t)B * row));
+        for (uint64_t i0 = 0; i0 < nv; i0 += B)
+          launch_verify_batch(s->view, s->bytes, LV, O, off, C, s->vlist.as<uint64_t>(), i0, std::min<uint64_t>(B, nv - i0),
+                              tag_base, tb, s->stored.as<StoredLevel>(), s->vfc.p, err, st);
+      } else {
+        launch_verify(s->view, s->bytes, LV, O, off, C, T, tag_base, tb, s->stored.as<StoredLevel>(),
+                      s->vlist.as<uint64_t>(), &dc(s)->n_verify, err, st);
+      }
       phase_end(s);
       CUDA_TRY(cudaGetLastError());
     }

@@ -106,6 +106,13 @@ void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const Ex
                    const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb,
                    const StoredLevel* stored, uint64_t* list, unsigned long long* n_list, int32_t* err,
                    cudaStream_t st);
+// dedup = 0 two-pass verification (the list of key matches, then batches)
+void launch_verify_list(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, uint64_t* list,
+                        unsigned long long* n_list, cudaStream_t st);
+size_t verify2_row_bytes(const SysView& S);
+void launch_verify_batch(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
+                         const ChildArrays& C, const uint64_t* list, uint64_t i0, uint64_t n, uint64_t tag_base,
+                         const Tables& tb, const StoredLevel* stored, void* fc, int32_t* err, cudaStream_t st);
 void launch_level0_compact(const uint8_t* verdict, const uint64_t* kept, const uint64_t* kpos, int64_t F0,
                            const uint64_t* fp0, const uint64_t* fp1, const NextArrays& N, uint64_t* src_index,
                            const Tables& tb, int insert_visited, int32_t* err, cudaStream_t st);

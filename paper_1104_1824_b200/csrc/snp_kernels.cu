@@ -2272,6 +2272,63 @@ __global__ void __launch_bounds__(VERIFY_WARPS * 32) k_verify_s(SysView S, Level
   }
 }
 
+// dedup = 0, two fully parallel passes over a batch of the listed key
+// matches: (1) a warp per match writes the fired (c, p) of every neuron of
+// the child (and, for a same-level duplicate, of its key's winner) to global
+// rows; (2) a thread per (match, column) rebuilds the column of eq. (2) from
+// them and compares it with the other row (the winner's, or the stored
+// configuration of an earlier level).  A mismatch is a 128-bit collision.
+template <typename T, typename FC>
+__global__ void k_verify_fc(SysView S, LevelView L, ExpandOut O, const uint64_t* off, ChildArrays C,
+                            const uint64_t* list, uint64_t i0, uint64_t n, uint64_t tag_base, Tables tb, FC* fcg) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = warp; i < n; i += nwarps) {
+    const uint64_t c = list[i0 + i];
+    FC* fa = fcg + i * 2 * (uint64_t)S.m;
+    const uint32_t p = C.cpar[c];
+    ChildCtx cx;
+    decode_child(S, O.nd + (uint64_t)p * KMAX, O.ndc[p], c - off[p], cx);
+    fired_cp<T>(S, L.data, p, cx, fa, lane);
+    if (C.verdict[c] == 1) {
+      const uint64_t o = tb.ltab[C.cslot[c]].tag - tag_base;
+      const uint32_t po = C.cpar[o];
+      ChildCtx co;
+      decode_child(S, O.nd + (uint64_t)po * KMAX, O.ndc[po], o - off[po], co);
+      fired_cp<T>(S, L.data, po, co, fa + S.m, lane);
+    }
+  }
+}
+
+template <typename T, typename FC>
+__global__ void k_verify_cols(SysView S, LevelView L, ChildArrays C, const uint64_t* list, uint64_t i0, uint64_t n,
+                              uint64_t tag_base, Tables tb, const FC* fcg, const StoredLevel* stored, int32_t* err) {
+  for (uint64_t i = blockIdx.y; i < n; i += gridDim.y) {
+    const uint64_t c = list[i0 + i];
+    const uint8_t vd = C.verdict[c];
+    const uint32_t p = C.cpar[c];
+    const FC* fa = fcg + i * 2 * (uint64_t)S.m;
+    const uint32_t po = vd == 1 ? C.cpar[tb.ltab[C.cslot[c]].tag - tag_base] : 0;
+    const uint64_t ref = vd == 1 ? 0 : C.cref[c];
+    bool diff = false;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < S.m; j += gridDim.x * blockDim.x) {
+      int64_t a = (int64_t)ld_count<T>(L.data, p, j, S.m) - fc_c(fa[j]);
+      for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) a += fc_p(fa[S.in_src[e]]);
+      int64_t b;
+      if (vd == 1) {
+        const FC* fb = fa + S.m;
+        b = (int64_t)ld_count<T>(L.data, po, j, S.m) - fc_c(fb[j]);
+        for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) b += fc_p(fb[S.in_src[e]]);
+      } else {
+        b = ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, S.m);
+      }
+      diff |= a != b;
+    }
+    if (diff) atomicOr(err, ERR_COLLISION);
+  }
+}
+
 // dedup = 0: every fingerprint match is checked by comparing the two full
 // configurations (candidate computed exactly from (parent, t)).  A mismatch
 // is a 128-bit collision: reported, never merged (reading A18).
@@ -3568,6 +3625,38 @@ void launch_overflow_fix(const SysView& S, int32_t bytes, const LevelView& L, co
     k_overflow_fix<T><<<grid_for(n_ovf, 128), 128, 0, st>>>(S, L, O, kq_off, N, ovf, n_ovf, err);
   });
   count_launch();
+}
+
+void launch_verify_list(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, uint64_t* list,
+                        unsigned long long* n_list, cudaStream_t st) {
+  cudaMemsetAsync(n_list, 0, sizeof(unsigned long long), st);
+  if (!T) return;
+  k_verify_need<<<grid_for(T), BLK, 0, st>>>(C, T, tag_base, tb, list, n_list);
+  count_launch();
+}
+
+size_t verify2_row_bytes(const SysView& S) { return (size_t)2 * S.m * (S.small_cp ? 2 : 8); }
+
+void launch_verify_batch(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
+                         const ChildArrays& C, const uint64_t* list, uint64_t i0, uint64_t n, uint64_t tag_base,
+                         const Tables& tb, const StoredLevel* stored, void* fc, int32_t* err, cudaStream_t st) {
+  if (!n) return;
+  dispatch_bytes(bytes, [&](auto tt) {
+    using TT = decltype(tt);
+    const unsigned gw = (unsigned)std::min<uint64_t>((n * 32 + 255) / 256, 148u * 32u);
+    dim3 gc((unsigned)std::min<int64_t>((S.m + 255) / 256, 64), (unsigned)std::min<uint64_t>(n, 65535));
+    if (S.small_cp) {
+      k_verify_fc<TT, uint16_t><<<gw, 256, 0, st>>>(S, L, O, off, C, list, i0, n, tag_base, tb,
+                                                     reinterpret_cast<uint16_t*>(fc));
+      k_verify_cols<TT, uint16_t><<<gc, 256, 0, st>>>(S, L, C, list, i0, n, tag_base, tb,
+                                                       reinterpret_cast<const uint16_t*>(fc), stored, err);
+    } else {
+      k_verify_fc<TT, int2><<<gw, 256, 0, st>>>(S, L, O, off, C, list, i0, n, tag_base, tb, reinterpret_cast<int2*>(fc));
+      k_verify_cols<TT, int2><<<gc, 256, 0, st>>>(S, L, C, list, i0, n, tag_base, tb, reinterpret_cast<const int2*>(fc),
+                                                   stored, err);
+    }
+  });
+  count_launch(2);
 }
 
 void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
