@@ -906,6 +906,7 @@ snp_status zero_counters(snp_system* s) {
 DevCounters* dc(snp_system* s) { return s->counters_dev.as<DevCounters>(); }
 
 snp_status begin_impl(snp_system* s, const snp_configs* level0) {
+  g_trace.start();
   SNP_TRY(reset_state(s));
   snp_configs c0{};
   if (!level0) {
@@ -990,6 +991,7 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
     if (!level0->on_device) CUDA_TRY(cudaStreamSynchronize(s->stream));
   }
   CUDA_TRY(cudaGetLastError());
+  g_trace.mark("upload");
   // fingerprints of level 0
   DBuf fp0, fp1;
   SNP_TRY(fp0.ensure(F0 * 8, false));
@@ -1011,6 +1013,7 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
   CUDA_TRY(cudaGetLastError());
   DevCounters hc;
   SNP_TRY(read_counters(s, &hc));
+  g_trace.mark("fingerprint_dedup");
   SNP_TRY(check_err(hc.err));
   if (s->opt.dedup == 0 && (int64_t)hc.n_new < F0) {
     launch_verify_level0(s->bytes, raw.p, (int32_t)m, C, (uint64_t)F0, tb, err, s->stream);
@@ -1045,7 +1048,11 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
   s->levels.push_back(std::move(L));
   s->begun = true;
   s->horizon_reserved = false;
-  return reserve_horizon(s, std::max<int64_t>(K, s->opt.frontier_target));
+  g_trace.mark("compact_digest");
+  const snp_status st = reserve_horizon(s, std::max<int64_t>(K, s->opt.frontier_target));
+  g_trace.mark("reserve_horizon");
+  g_trace.flush("begin");
+  return st;
 }
 
 snp_status classify_level(snp_system* s, Level* L) {
