@@ -1510,6 +1510,9 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_PREFETCH
 #define SNP_KC_PREFETCH 0
 #endif
+#ifndef SNP_KC_WIDE_COOP
+#define SNP_KC_WIDE_COOP 1  // 16/32-bit counts: warp-cooperative row stores (else one lane per row)
+#endif
 #ifndef SNP_KC_FLATQ
 #define SNP_KC_FLATQ 1  // cooperative quads in passes over the CTA's own quad range (else per output block: 61.0 vs 56.4 ms)
 #endif
@@ -1972,12 +1975,26 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
     } else
 #endif
     if (nq <= QCAP) {
-      for (uint64_t q = Q0; q < Q1; ++q) out[eidx((int64_t)q, j, m)] = xs[sR[q - Qb]];
+      if (!(SNP_KC_WIDE_COOP && sizeof(T) > 1))  // wide counts: the warp-cooperative rows below
+        for (uint64_t q = Q0; q < Q1; ++q) out[eidx((int64_t)q, j, m)] = xs[sR[q - Qb]];
     } else {
       for (int r = 0; r < np; ++r)
         for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = xs[r];
     }
     }  // j < m
+#if SNP_KC_WIDE_COOP
+    if (sizeof(T) > 1 && nq <= QCAP) {
+      // 16/32-bit counts: the warp writes its rows one at a time, lane = child,
+      // so each store instruction fills 32 consecutive children of one row
+      __syncwarp();
+      const int32_t jn = m - jbase;
+      for (int r = 0; r < 32 && r < jn; ++r) {
+        const T* xr = reinterpret_cast<const T*>(sX + (size_t)(warp * 32 + r) * xs_stride<T>());
+        for (uint64_t q = Q0 + lane; q < Q1; q += 32) out[eidx((int64_t)q, jbase + r, m)] = xr[sR[q - Qb]];
+      }
+      __syncwarp();
+    }
+#endif
 #if SNP_KC_COOP
     if (prog) {
       // full 4-child quads, warp-cooperative: a half-warp covers one 64-child
