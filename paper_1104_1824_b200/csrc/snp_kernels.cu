@@ -1869,6 +1869,31 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
         for (int i = 0; i < 8; ++i) vw[i] = vn[i];
 #endif
       }
+    } else if (sizeof(T) == 4 && !generic) {
+      // int32 counts: the row in 16-byte loads, 16 parents at a time
+      for (int r0 = 0; r0 < PB; r0 += 16) {
+        int32_t vv[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int4 q4 = r0 + 4 * k < np ? __ldg(reinterpret_cast<const int4*>(row) + (r0 >> 2) + k) : make_int4(0, 0, 0, 0);
+          vv[4 * k] = q4.x;
+          vv[4 * k + 1] = q4.y;
+          vv[4 * k + 2] = q4.z;
+          vv[4 * k + 3] = q4.w;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int r = r0 + k;
+          const int32_t v = r < np ? vv[k] : 0;
+          const int32_t cons = (int32_t)crow_g[table_index((uint32_t)v, mt)];
+          int32_t cnt = 0;
+#pragma unroll
+          for (int b = 0; b < NPL; ++b) cnt |= (int32_t)((c[b] >> r) & 1ULL) << b;
+          const int64_t x = (int64_t)v - cons + cnt;
+          if (x > S.count_max) ovf_bits |= 1ULL << r;
+          xs[r] = (T)x;
+        }
+      }
     } else {
       for (int r = 0; r < PB; ++r) {
         const int32_t v = (r < np) ? (int32_t)row[r] : 0;
