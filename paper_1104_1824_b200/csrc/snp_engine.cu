@@ -1232,7 +1232,7 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
     if (s->opt.dedup == 0) {
       SNP_TRY(update_stored_table(s));
       phase_begin(s, 4);
-      SNP_TRY(s->vlist.ensure(T * 8 + 16));
+      SNP_TRY(s->vlist.ensure(std::max<uint64_t>(T, s->child_cap) * 8 + 16));  // sized with the child arrays
       if (s->view.aug_rule < 0) {
         // the key matches listed, then verified in batches by the two fully
         // parallel passes (fired (c, p) rows, then one thread per column)
@@ -1241,8 +1241,9 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
         CUDA_TRY(cudaMemcpyAsync(&nv, &dc(s)->n_verify, 8, cudaMemcpyDeviceToHost, st));
         SNP_TRY(sync(s));
         const size_t row = verify2_row_bytes(s->view);
-        const uint64_t B = std::max<uint64_t>(1, std::min<uint64_t>(nv, ((size_t)256 << 20) / row));
-        if (nv) SNP_TRY(s->vfc.ensure((size_t)B * row));
+        const uint64_t Bmax = std::max<uint64_t>(1, ((size_t)256 << 20) / row);
+        const uint64_t B = std::max<uint64_t>(1, std::min<uint64_t>(nv, Bmax));
+        if (nv) SNP_TRY(s->vfc.ensure((size_t)Bmax * row, false));  // one allocation for the run, not per level
         for (uint64_t i0 = 0; i0 < nv; i0 += B)
           launch_verify_batch(s->view, s->bytes, LV, O, off, C, s->vlist.as<uint64_t>(), i0, std::min<uint64_t>(B, nv - i0),
                               tag_base, tb, s->stored.as<StoredLevel>(), s->vfc.p, err, st);
