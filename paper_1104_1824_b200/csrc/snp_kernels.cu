@@ -2615,11 +2615,18 @@ __global__ void __launch_bounds__(1024) k_small_bfs(SysView S, SmallArgs a) {
     // ---- K-b: child -> parent, keys by linearity (reading A18), clear the level table
     for (int64_t p = tid; p < F; p += nt)
       for (uint64_t c = a.off[p]; c < a.off[p + 1]; ++c) a.cpar[c] = (uint32_t)p;
-    for (uint64_t i = tid; i <= a.tb.lmask; i += nt) {
-      a.tb.ltab[i].k0 = EMPTY;
-      a.tb.ltab[i].k1 = EMPTY;
-      a.tb.ltab[i].tag = EMPTY;
-      a.tb.ltab[i].ref = EMPTY;
+    // the level table sized for this level's transitions (>= 2T slots, a power of two)
+    Tables tl = a.tb;
+    {
+      uint64_t sl = 64;
+      while (sl < 2 * Tn) sl <<= 1;
+      tl.lmask = sl - 1 < a.tb.lmask ? sl - 1 : a.tb.lmask;
+    }
+    for (uint64_t i = tid; i <= tl.lmask; i += nt) {
+      tl.ltab[i].k0 = EMPTY;
+      tl.ltab[i].k1 = EMPTY;
+      tl.ltab[i].tag = EMPTY;
+      tl.ltab[i].ref = EMPTY;
     }
     __syncthreads();
     for (uint64_t c = tid; c < Tn; c += nt) {
@@ -2668,12 +2675,12 @@ __global__ void __launch_bounds__(1024) k_small_bfs(SysView S, SmallArgs a) {
         continue;
       }
       bool ins = false;
-      i = h & a.tb.lmask;
-      for (uint64_t probes = 0; probes <= a.tb.lmask; ++probes, i = (i + 1) & a.tb.lmask) {
+      i = h & tl.lmask;
+      for (uint64_t probes = 0; probes <= tl.lmask; ++probes, i = (i + 1) & tl.lmask) {
         Key128 empty{EMPTY, EMPTY}, mine{k0, k1};
-        const Key128 prev = atomicCAS(reinterpret_cast<Key128*>(a.tb.ltab + i), empty, mine);
+        const Key128 prev = atomicCAS(reinterpret_cast<Key128*>(tl.ltab + i), empty, mine);
         if ((prev.k0 == EMPTY && prev.k1 == EMPTY) || (prev.k0 == k0 && prev.k1 == k1)) {
-          atomicMin(&a.tb.ltab[i].tag, (unsigned long long)c);
+          atomicMin(&tl.ltab[i].tag, (unsigned long long)c);
           a.cslot[c] = i;
           a.verdict[c] = 1;
           ins = true;
