@@ -410,7 +410,7 @@ snp_status ensure_visited(snp_system* s, uint64_t needed_entries) {
 // words, child arrays, level table).
 snp_status ensure_children(snp_system* s, uint64_t T);
 constexpr int64_t RESERVE_LEVELS = 32;
-constexpr int64_t RESERVE_CHILDREN = 8;
+constexpr int64_t RESERVE_CHILDREN = 16;  // T/F reaches 9 at config 3, 6 at config 4
 snp_status reserve_horizon(snp_system* s, int64_t Ft) {
   if (Ft <= 0) return SNP_OK;
   size_t free_b = 0, total_b = 0;
@@ -429,7 +429,10 @@ snp_status reserve_horizon(snp_system* s, int64_t Ft) {
   const uint64_t T = (uint64_t)RESERVE_CHILDREN * (uint64_t)Ft;
   if (T > s->child_cap) SNP_TRY(ensure_children(s, T / 2));
   {
-    const uint64_t lw = next_pow2(std::max<uint64_t>(1024, 2 * T));
+    // the level table for 8·Ft transitions (2 slots each): config 4 stays
+    // below (T/F <= 6.1); a rarer larger level grows it (a 1 GB reallocation
+    // at config 3's tenth level, T/F = 8.8)
+    const uint64_t lw = next_pow2(std::max<uint64_t>(1024, 2 * (T / 2)));
     if (lw > s->ltab_cap) {
       SNP_TRY(s->ltab.ensure(lw * sizeof(Slot), false));
       s->ltab_cap = lw;
