@@ -597,6 +597,75 @@ snp_status upload(snp_system* s, DBuf& b, const std::vector<U>& v) {
   return SNP_OK;
 }
 
+// Row assignment of one half-warp's in-synapse sources for K-c's gather.
+// In row r, lane l reads the staged emit word of source lane_row[l][r] (-1:
+// padding, the shared zero word).  K-c keeps the 64-bit emit words in shared
+// memory, word s in bank pair s mod 16, so the 16 lanes of a half-warp read
+// one row in one wavefront when their bank pairs differ.  The order of a
+// lane's sources is free (their counts are summed), so the rows are a proper
+// edge colouring of the bipartite multigraph lanes × bank pairs (colour =
+// row).  König: max-degree colours suffice; with R rows (the group's padded
+// row count, >= every in-degree) a bank pair with more than R sources is
+// split round-robin into ceil(deg / R) nodes (two of its lanes then share a
+// row), so the padding stays that of the plain layout.  Colouring by
+// alternating-path swaps.
+static void bank_rows(const std::vector<std::vector<int32_t>>& lane_src, int R, std::vector<std::vector<int32_t>>& lane_row) {
+  const int NL = (int)lane_src.size();
+  int D = R;  // rows available (>= every lane's in-degree)
+  for (auto& v : lane_src) D = std::max(D, (int)v.size());
+  lane_row.assign(NL, std::vector<int32_t>(D, -1));
+  if (D == 0) return;
+  int deg[16] = {0};
+  for (auto& v : lane_src)
+    for (int32_t s : v) deg[s & 15]++;
+  int vbase[17] = {0};
+  for (int k = 0; k < 16; ++k) vbase[k + 1] = vbase[k] + std::max(1, (deg[k] + D - 1) / D);
+  const int NV = vbase[16];
+  struct E { int u, v; int32_t s; int c; };
+  std::vector<E> es;
+  int rr[16] = {0};
+  for (int l = 0; l < NL; ++l)
+    for (int32_t s : lane_src[l]) {
+      const int k = s & 15, nk = vbase[k + 1] - vbase[k];
+      es.push_back({l, vbase[k] + (rr[k]++ % nk), s, -1});
+    }
+  std::vector<int> atL((size_t)NL * D, -1), atV((size_t)NV * D, -1);  // edge id holding colour c at a node
+  for (int e = 0; e < (int)es.size(); ++e) {
+    const int u = es[e].u, v = es[e].v;
+    int a = 0, b = 0;
+    while (atL[(size_t)u * D + a] >= 0) ++a;  // free at u (deg u <= D)
+    while (atV[(size_t)v * D + b] >= 0) ++b;  // free at v (deg v <= D)
+    if (atV[(size_t)v * D + a] >= 0) {
+      // swap a/b on the alternating path from v that starts with colour a;
+      // bipartite: it never reaches u, so a becomes free at v and stays free at u
+      std::vector<int> path;
+      int x = v, col = a;
+      bool right = true;
+      for (;;) {
+        const int pe = right ? atV[(size_t)x * D + col] : atL[(size_t)x * D + col];
+        if (pe < 0) break;
+        path.push_back(pe);
+        x = right ? es[pe].u : es[pe].v;
+        right = !right;
+        col = col == a ? b : a;
+      }
+      for (int pe : path) {
+        atL[(size_t)es[pe].u * D + es[pe].c] = -1;
+        atV[(size_t)es[pe].v * D + es[pe].c] = -1;
+      }
+      for (int pe : path) {
+        es[pe].c = es[pe].c == a ? b : a;
+        atL[(size_t)es[pe].u * D + es[pe].c] = pe;
+        atV[(size_t)es[pe].v * D + es[pe].c] = pe;
+      }
+    }
+    es[e].c = a;
+    atL[(size_t)u * D + a] = e;
+    atV[(size_t)v * D + a] = e;
+  }
+  for (auto& e : es) lane_row[e.u][e.c] = e.s;
+}
+
 snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, int64_t n_rules, const uint64_t* re_bits,
                      const int32_t* C0) {
   std::vector<std::vector<std::pair<int32_t, int32_t>>> rows;
@@ -685,10 +754,29 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
       pad_off[g + 1] = pad_off[g] + (mx + 3) / 4 * 4;  // K-c consumes rows in blocks of 8 and 4
     }
     std::vector<int32_t> in_pad((size_t)pad_off[ng] * 32, pad);
-    for (int64_t g = 0; g < ng; ++g)
+    const char* bk = getenv("SNP_INPAD_BANKS");
+    const bool banks = !(bk && bk[0] == '0');
+    std::vector<std::vector<int32_t>> lane_src(16), lane_row;
+    for (int64_t g = 0; g < ng; ++g) {
+      if (banks) {
+        // each half-warp's rows bank-conflict-free in K-c's staged emit words
+        for (int h = 0; h < 2; ++h) {
+          for (int l = 0; l < 16; ++l) {
+            lane_src[l].clear();
+            const int64_t j = 32 * g + 16 * h + l;
+            if (j < m) lane_src[l].assign(in_src.begin() + in_off[j], in_src.begin() + in_off[j + 1]);
+          }
+          bank_rows(lane_src, (int)(pad_off[g + 1] - pad_off[g]), lane_row);
+          for (int l = 0; l < 16; ++l)
+            for (size_t r = 0; r < lane_row[l].size(); ++r)
+              if (lane_row[l][r] >= 0) in_pad[(size_t)(pad_off[g] + r) * 32 + 16 * h + l] = lane_row[l][r];
+        }
+        continue;
+      }
       for (int64_t j = 32 * g; j < std::min<int64_t>(m, 32 * g + 32); ++j)
         for (int32_t e = in_off[j]; e < in_off[j + 1]; ++e)
           in_pad[(size_t)(pad_off[g] + (e - in_off[j])) * 32 + (j - 32 * g)] = in_src[e];
+    }
     SNP_TRY(upload(s, s->d_in_pad, in_pad));
     if (m < 65535) {
       std::vector<uint16_t> in16(in_pad.begin(), in_pad.end());
@@ -766,7 +854,8 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   {
     // SNP_KERNELS (tests / tuning): "expand_t" = the 8-configuration-per-lane
     // K-a for uint8 too; "kc_global_e" = K-c reads emit words from global
-    // memory even when they fit in shared memory (the large-m path)
+    // memory even when they fit in shared memory (the large-m path); "kc_tc"
+    // = K-c's output permutation on the tensor cores (measured slower)
     const char* k = getenv("SNP_KERNELS");
     v.kernel_flags = 0;
     v.small_cp = s->small_rules ? 1 : 0;  // c, p <= 255: packed (c, p) tables in the verification
@@ -775,6 +864,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     if (k && strstr(k, "expand_t")) v.kernel_flags |= KF_EXPAND_T;
     if (k && strstr(k, "kc_global_e")) v.kernel_flags |= KF_KC_GLOBAL_E;
     if (k && strstr(k, "no_tc")) v.kernel_flags |= KF_NO_TC;
+    if (k && strstr(k, "kc_tc")) v.kernel_flags |= KF_KC_TC;
   }
   v.m = (int32_t)m;
   v.n = n;

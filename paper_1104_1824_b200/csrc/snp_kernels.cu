@@ -1565,25 +1565,47 @@ __device__ const uint64_t g_zero_word = 0;  // padded in-synapses when the emit 
 // 16/32-byte store are one/two aligned 16-B loads.
 constexpr int OPCAP = 1100;  // >= 16 ops per output block × (QCAP / 64 + 2)
 
+// K-c store on the tensor cores (TCS, uint8): the output permutation
+// out[j][q] = x[j][r(q)] (q = kept child, r(q) its parent in the block) is a
+// product with a one-hot matrix, D = X·P, done by tcgen05.mma kind::i8 into
+// TMEM instead of byte permutes through shared memory.  A tile = 128 neurons ×
+// 64 parents (K-major, no swizzle: addr(m, k) = (k/16)·2048 + (m/8)·128 +
+// (m%8)·16 + k%16), written by the 4 warps that computed those rows.  Two
+// children per accumulator column: column c of the CTA's child window (Qb =
+// Q0 rounded down to 32) holds x(Qb+2c) + 256·x(Qb+2c+1), from two MMAs over
+// the same A: P1[k][c] = [r(Qb+2c) = k] + 128·[r(Qb+2c+1) = k] and P2[k][c] =
+// 128·[r(Qb+2c+1) = k] (entries <= 129 fit u8).  So 64 columns per tile cover
+// 128 children (4 sectors), the 8 tiles of a CTA fill the 512 TMEM columns,
+// and one PRMT packs 4 children; each lane then writes whole 32-byte sectors
+// of its row (partial ones only at the window's two ends).  CTAs whose window
+// exceeds 8 sectors (2 rounds) take a per-lane byte path (rare: ~64 children
+// per block once the frontier is thinned).
+constexpr int KCT_ATILE = 128 * 64;                // one A tile (bytes)
+constexpr int KCT_A_LBO = 2048;                    // A: K-chunk (16 parents) stride
+constexpr int KCT_B_LBO = 1024;                    // B: K-chunk stride (64 columns × 16 B)
+constexpr int KCT_BHALF = 64 * 64;                 // one B matrix (P1 or P2) of one round
+constexpr int KCT_BBYTES = 2 * 2 * KCT_BHALF;      // 2 rounds × (P1, P2)
+
 // ES: the block's emit words are staged in shared memory (m·8 B fit); else
 // (large m) the in-synapse gather reads them from global memory (L2/L1).
 // MWT: warps per CTA (MW; fewer for wide counts, whose per-lane staging of
 // 64 values would not fit shared memory at MW warps — int32 at config 3).
-template <typename T, int NPL, bool ES, int MWT = MW>
+template <typename T, int NPL, bool ES, int MWT = MW, bool TCS = false>
 __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelView L, ExpandOut O,
                                                              const uint64_t* kq_off, NextArrays N, uint64_t* ovf,
                                                              unsigned long long* n_ovf, uint64_t ovf_cap) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   const int32_t m = S.m;
   const int64_t mE = (m + 1) & ~1;
   uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words + 2 zero words
-  uint8_t* sX = smem + (ES ? (mE + 2) * 8 : 0);                         // MWT×32×xs_stride
-  uint8_t* sR = sX + (size_t)MWT * 32 * xs_stride<T>();                 // QCAP + 32
+  uint8_t* sX = smem + (ES ? (mE + 2) * 8 : 0);                         // MWT×32×xs_stride (TCS: the A tiles)
+  uint8_t* sR = sX + (TCS ? (size_t)MWT / 4 * KCT_ATILE + KCT_BBYTES : (size_t)MWT * 32 * xs_stride<T>());  // QCAP + 32
   uint32_t* sD = reinterpret_cast<uint32_t*>(sR + QCAP + 32);           // (QCAP+32)/4 quad descriptors
-  uint64_t* sOps = reinterpret_cast<uint64_t*>(sD + (QCAP + 32) / 4);   // OPCAP store ops
-  uint64_t* sQ = sOps + OPCAP;                                          // 65 (+1 pad)
+  uint64_t* sOps = reinterpret_cast<uint64_t*>(sD + (TCS ? 0 : (QCAP + 32) / 4));  // OPCAP store ops
+  uint64_t* sQ = sOps + (TCS ? 0 : OPCAP);                              // 65 (+1 pad)
   uint64_t* bar = sQ + 66;
-  uint32_t* sMisc = reinterpret_cast<uint32_t*>(bar + 1);              // [0,1] haskids, [2] #ops
+  uint64_t* tbar = bar + 1;                                             // TCS: one mbarrier per A tile
+  uint32_t* sMisc = reinterpret_cast<uint32_t*>(tbar + (TCS ? MWT / 4 : 0));  // [0,1] haskids, [2] #ops, [3] TMEM
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t blk = blockIdx.x;
   const int64_t pb0 = blk * PB;
@@ -1593,9 +1615,14 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
   const uint32_t ebytes = (uint32_t)(mE * 8);
   if (tid == 0) {
     mbar_init(bar, 1);
+    if (TCS)
+      for (int t = 0; t < MWT / 4; ++t) mbar_init(&tbar[t], 1);
     fence_barrier_init();
   }
+  if (TCS && warp == 0) tc::tmem_alloc(&sMisc[3], 512);
+  tc::fence_before();
   __syncthreads();
+  tc::fence_after();
   if (ES && tid == 0) {
     mbar_arrive_expect_tx(bar, ebytes);
     const uint8_t* src = reinterpret_cast<const uint8_t*>(O.ebits) + (size_t)blk * ebytes;
@@ -1617,8 +1644,10 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
   const uint64_t* gE = O.ebits + blk * mE;
   __syncthreads();
   const uint64_t nq = Q1 - Q0;
-  const bool prog = sizeof(T) == 1 && nq <= QCAP;  // CTA-uniform: the store program applies
+  const bool prog = !TCS && sizeof(T) == 1 && nq <= QCAP;  // CTA-uniform: the store program applies
   const uint64_t Qb = Q0 & ~31ULL;                  // sR[q - Qb]
+  const int nsec = (int)((Q1 - Qb + 31) >> 5);      // TCS: 32-child sectors of the window
+  const bool tcp = TCS && nsec <= 8;                // CTA-uniform: the tensor-core store applies
   if (nq <= QCAP) {
     if (tid < np)
       for (uint64_t q = sQ[tid]; q < sQ[tid + 1]; ++q) sR[q - Qb] = (uint8_t)tid;
@@ -1652,6 +1681,26 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       }
       sD[i] = d;
     }
+  }
+  if (TCS && tcp) {
+    // the one-hot operands P1 / P2 of both rounds (see KCT_ATILE): item i =
+    // (round, matrix, K-chunk, column), one 16-byte core-matrix row each
+    for (int i = tid; i < 2 * 2 * 4 * 64; i += blockDim.x) {
+      const int n = i & 63, kc = (i >> 6) & 3, h = (i >> 8) & 1, rd = i >> 9;
+      const uint64_t q0 = Qb + 2 * (64 * rd + n), q1 = q0 + 1;
+      const int r0 = (q0 >= Q0 && q0 < Q1) ? (int)sR[q0 - Qb] : -1;
+      const int r1 = (q1 >= Q0 && q1 < Q1) ? (int)sR[q1 - Qb] : -1;
+      uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const int k = 16 * kc + b;
+        const uint32_t v = (h == 0 && k == r0 ? 1u : 0u) + (k == r1 ? 128u : 0u);
+        w[b >> 2] |= v << (8 * (b & 3));
+      }
+      *reinterpret_cast<uint4*>(sX + (size_t)MWT / 4 * KCT_ATILE + rd * 2 * KCT_BHALF + h * KCT_BHALF +
+                                kc * KCT_B_LBO + (n >> 3) * 128 + (n & 7) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    tc::fence_async_smem();
   }
   if (!SNP_KC_COOP && prog && tid == 64) {  // the store program (one thread; overlaps the emit-word staging)
     int n = 0;
@@ -1687,13 +1736,18 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
 
   const T* data = reinterpret_cast<const T*>(L.data);
   T* out = reinterpret_cast<T*>(N.data);
-  uint8_t* xsb = sX + (size_t)(warp * 32 + lane) * xs_stride<T>();
+  // this lane's x row: the staging row (xs_stride), or (TCS) row 32·(warp%4) +
+  // lane of the warp's A tile, byte r at (r/16)·KCT_A_LBO + r%16
+  uint8_t* xsb = TCS ? sX + (warp >> 2) * KCT_ATILE + (((warp & 3) * 32 + lane) >> 3) * 128 + (lane & 7) * 16
+                     : sX + (size_t)(warp * 32 + lane) * xs_stride<T>();
   T* xs = reinterpret_cast<T*>(xsb);
+  auto xb = [&](int r) -> uint8_t* { return TCS ? xsb + (r >> 4) * KCT_A_LBO + (r & 15) : xsb + r; };
   const T* ctab = reinterpret_cast<const T*>(S.ctab);
   const int j_iters = (m + MWT * 32 - 1) / (MWT * 32);
+  uint32_t tph = 0;  // TCS: parity of this warp's tile mbarrier
   for (int it = 0; it < j_iters; ++it) {
     const int32_t jbase = it * MWT * 32 + warp * 32;
-    if (jbase >= m) break;  // warp-uniform
+    if (TCS ? it * MWT * 32 + (warp & ~3) * 32 >= m : jbase >= m) break;  // warp- (TCS: tile-) uniform
 #if SNP_KC_L2PF
     // the warp's 32 rows of the parent block (2 KB contiguous for u8) pulled
     // into L2 while the gather runs, so the row load after it hits L2
@@ -1840,7 +1894,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
         }
         // x = t + count: plain 32-bit adds; a byte can only carry when some
         // operand byte has its top bit set (rare: redo those quads bytewise)
-        uint32_t kq[8], chk = 0;
+        uint32_t kq[8], chk = 0, xw[8];
         if (upper) {
 #pragma unroll
           for (int h = 0; h < 4; ++h) counts8<NPL, NPL>(c, 4 * g + h, kq[2 * h], kq[2 * h + 1]);
@@ -1862,7 +1916,12 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
             for (int b = 0; b < 4; ++b)
               if ((co >> (8 * b + 7)) & 1u) ovf_bits |= 1ULL << (32 * g + 4 * i + b);
           }
-          reinterpret_cast<uint32_t*>(xsb)[8 * g + i] = x4;
+          if (TCS) xw[i] = x4;
+          else reinterpret_cast<uint32_t*>(xsb)[8 * g + i] = x4;
+        }
+        if (TCS) {  // parents 32g .. 32g+31 = K-chunks 2g, 2g+1 of the A row
+          *reinterpret_cast<uint4*>(xsb + (2 * g) * KCT_A_LBO) = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+          *reinterpret_cast<uint4*>(xsb + (2 * g + 1) * KCT_A_LBO) = make_uint4(xw[4], xw[5], xw[6], xw[7]);
         }
 #if SNP_KC_PREFETCH
 #pragma unroll
@@ -1891,7 +1950,8 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
           for (int b = 0; b < NPL; ++b) cnt |= (int32_t)((c[b] >> r) & 1ULL) << b;
           const int64_t x = (int64_t)v - cons + cnt;
           if (x > S.count_max) ovf_bits |= 1ULL << r;
-          xs[r] = (T)x;
+          if (TCS) *xb(r) = (uint8_t)x;
+          else xs[r] = (T)x;
         }
       }
     } else {
@@ -1909,7 +1969,8 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
         for (int b = 0; b < NPL; ++b) cnt |= (int32_t)((c[b] >> r) & 1ULL) << b;
         const int64_t x = (int64_t)v - cons + cnt;
         if (x > S.count_max) ovf_bits |= 1ULL << r;
-        xs[r] = (T)x;
+        if (TCS) *xb(r) = (uint8_t)x;
+        else xs[r] = (T)x;
       }
     }
     ovf_bits &= haskids;
@@ -1999,7 +2060,16 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       }
     } else
 #endif
-    if (nq <= QCAP) {
+    if (TCS) {
+      if (!tcp) {  // window > 8 sectors (rare): one byte store per (row, child)
+        if (nq <= QCAP) {
+          for (uint64_t q = Q0; q < Q1; ++q) out[eidx((int64_t)q, j, m)] = *xb(sR[q - Qb]);
+        } else {
+          for (int r = 0; r < np; ++r)
+            for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = *xb(r);
+        }
+      }
+    } else if (nq <= QCAP) {
       if (!(SNP_KC_WIDE_COOP && sizeof(T) > 1))  // wide counts: the warp-cooperative rows below
         for (uint64_t q = Q0; q < Q1; ++q) out[eidx((int64_t)q, j, m)] = xs[sR[q - Qb]];
     } else {
@@ -2007,6 +2077,85 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
         for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = xs[r];
     }
     }  // j < m
+    if constexpr (TCS) {
+      if (tcp) {
+        // the tile's 128 rows are in its A tile: D = X·P on the tensor cores
+        // (KCT_ATILE), then every lane writes whole sectors of its row
+        const int t = warp >> 2, wq = warp & 3;
+        const uint32_t tmem = sMisc[3] + ((uint32_t)(32 * wq) << 16) + 64u * t;
+        uint8_t* sA = sX + t * KCT_ATILE;
+        const uint8_t* sB = sX + (size_t)MWT / 4 * KCT_ATILE;
+        tc::fence_async_smem();  // this thread's A row → the async proxy
+        for (int rd = 0; 4 * rd < nsec; ++rd) {
+          tc::fence_before();  // the previous round's TMEM loads are complete (wait_ld)
+          tc::named_sync(1 + t, 128);
+          if (wq == 0 && lane == 0) {
+            tc::fence_after();
+            const int ns = nsec - 4 * rd < 4 ? nsec - 4 * rd : 4;
+            const uint32_t idesc = tc::idesc_u8(128, 16 * ns, false, false);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks)
+                tc::mma_u8(sMisc[3] + 64u * t, tc::sdesc(tc::smem_u32(sA + ks * 2 * KCT_A_LBO), KCT_A_LBO, 128),
+                           tc::sdesc(tc::smem_u32(sB + (2 * rd + h) * KCT_BHALF + ks * 2 * KCT_B_LBO), KCT_B_LBO, 128),
+                           idesc, (h | ks) ? 1u : 0u);
+            tc::commit(&tbar[t]);
+          }
+          tc::bar_wait(&tbar[t], tph);
+          tph ^= 1;
+          tc::fence_after();
+          for (int sl = 0; sl < 4 && 4 * rd + sl < nsec; ++sl) {
+            uint32_t v[16];
+            tc::tmem_ld16_nw(tmem + 16u * sl, v);
+            tc::wait_ld();
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = prmt(v[2 * i], v[2 * i + 1], 0x5410u);
+            const int32_t jj = jbase + lane;
+            if (jbase < m && jj < m) {
+              const uint64_t q = Qb + 32 * (uint64_t)(4 * rd + sl);
+              uint8_t* dst = reinterpret_cast<uint8_t*>(out) + ((((int64_t)(q >> 6) * m + jj) << 6) | (int64_t)(q & 63));
+              const int lo = Q0 > q ? (int)(Q0 - q) : 0;
+              const int hi = Q1 < q + 32 ? (int)(Q1 - q) : 32;
+              if (lo == 0 && hi == 32) {
+                stg256(dst, w);
+              } else {
+                // partial sector at a window end (warp-uniform bounds): the
+                // widest aligned pieces inside [lo, hi)
+#pragma unroll
+                for (int h16 = 0; h16 < 2; ++h16) {
+                  if (lo <= 16 * h16 && 16 * h16 + 16 <= hi) {
+                    *reinterpret_cast<uint4*>(dst + 16 * h16) =
+                        make_uint4(w[4 * h16], w[4 * h16 + 1], w[4 * h16 + 2], w[4 * h16 + 3]);
+                    continue;
+                  }
+#pragma unroll
+                  for (int h8 = 0; h8 < 2; ++h8) {
+                    const int b8 = 16 * h16 + 8 * h8;
+                    if (lo <= b8 && b8 + 8 <= hi) {
+                      *reinterpret_cast<uint2*>(dst + b8) = make_uint2(w[b8 >> 2], w[(b8 >> 2) + 1]);
+                      continue;
+                    }
+#pragma unroll
+                    for (int h4 = 0; h4 < 2; ++h4) {
+                      const int b4 = b8 + 4 * h4;
+                      const uint32_t x = w[b4 >> 2];
+                      if (lo <= b4 && b4 + 4 <= hi) {
+                        *reinterpret_cast<uint32_t*>(dst + b4) = x;
+                      } else if (lo < b4 + 4 && hi > b4) {
+                        for (int b = (lo > b4 ? lo : b4); b < (hi < b4 + 4 ? hi : b4 + 4); ++b)
+                          dst[b] = (uint8_t)(x >> (8 * (b - b4)));
+                      }
+                    }
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+    }
 #if SNP_KC_WIDE_COOP
     if (sizeof(T) > 1 && nq <= QCAP) {
       // 16/32-bit counts: the warp writes its rows one at a time, lane = child,
@@ -2080,6 +2229,11 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       __syncwarp();
     }
 #endif
+  }
+  if constexpr (TCS) {
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(sMisc[3], 512);
   }
 }
 // K-c (generic): every (kept child, neuron) computed exactly.
@@ -3459,6 +3613,24 @@ size_t materialize_smem_bytes(const SysView& S, int32_t bytes, bool staged_e) {
   return (staged_e ? (mE + 2) * 8 : 0) + xs + 2 * (QCAP + 32) + 8 * OPCAP + 67 * 8 + 16 + 16;
 }
 
+// the tensor-core store variant (uint8): A tiles + one-hot operands instead of
+// the staging rows, descriptors and store program; one mbarrier per tile
+size_t materialize_tc_smem_bytes(const SysView& S, bool staged_e) {
+  const size_t mE = (size_t)((S.m + 1) & ~1);
+  return (staged_e ? (mE + 2) * 8 : 0) + (size_t)MW / 4 * KCT_ATILE + KCT_BBYTES + (QCAP + 32) + 66 * 8 + 8 +
+         8 * (MW / 4) + 16 + 16;
+}
+
+// opt-in (SNP_KERNELS=kc_tc): measured slower at config 4 (K-c 73.2 vs 55.3 ms
+// per level, profiles/r02/ab_kc_tc.json): correct, and it moves the shared
+// wavefronts off the LSU (1.83e9 -> 0.70e9 at F = 2^20), but each lane's
+// sector stores touch 32 rows (16 lines per instruction) and the window ends
+// need up to 9 masked pieces, and the per-tile barrier + MMA round trip every
+// 1024 neurons leaves warps waiting (long-scoreboard 40 % of the samples)
+bool materialize_tc_ok(const SysView& S, int32_t bytes, bool staged_e) {
+  return bytes == 1 && (S.kernel_flags & KF_KC_TC) && materialize_tc_smem_bytes(S, staged_e) <= KC_SMEM_MAX;
+}
+
 // emit words staged in shared memory when they fit (else read from L2)
 bool materialize_stage_e(const SysView& S, int32_t bytes) {
   return !(S.kernel_flags & KF_KC_GLOBAL_E) && materialize_smem_bytes(S, bytes, true) <= KC_SMEM_MAX;
@@ -3591,7 +3763,8 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
   if (K <= 0) return;
   if (fast_materialize_ok(S)) {
     const bool staged = materialize_stage_e(S, bytes);
-    const size_t smem = materialize_smem_bytes(S, bytes, staged);
+    const bool tcs = materialize_tc_ok(S, bytes, staged);
+    const size_t smem = tcs ? materialize_tc_smem_bytes(S, staged) : materialize_smem_bytes(S, bytes, staged);
     const unsigned nblk = (unsigned)((L.F + PB - 1) / PB);
     dispatch_bytes(bytes, [&](auto tt) {
       using T = decltype(tt);
@@ -3600,6 +3773,22 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<nblk, W * 32, smem, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
       };
+      if constexpr (sizeof(T) == 1) {
+        if (tcs) {
+          if (staged) {
+            if (S.max_indeg < 16) go(k_materialize_bs<T, 4, true, W, true>);
+            else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, true, W, true>);
+            else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, true, W, true>);
+            else go(k_materialize_bs<T, 8, true, W, true>);
+          } else {
+            if (S.max_indeg < 16) go(k_materialize_bs<T, 4, false, W, true>);
+            else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, false, W, true>);
+            else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, false, W, true>);
+            else go(k_materialize_bs<T, 8, false, W, true>);
+          }
+          return;
+        }
+      }
       if (staged) {
         if (S.max_indeg < 16) go(k_materialize_bs<T, 4, true, W>);
         else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, true, W>);

@@ -113,7 +113,7 @@ def test_tiny_random(snp, seed):
 
 
 # ---- random systems shaped like configs 3-5, scaled to oracle size ---------
-@pytest.mark.parametrize("kernels", ["kc_global_e"])
+@pytest.mark.parametrize("kernels", ["kc_global_e", "kc_tc"])
 def test_random_parity_global_emit_words(snp, monkeypatch, kernels):
     monkeypatch.setenv("SNP_KERNELS", kernels)
     for m, F, bits, dedup in [(300, 700, 16, 0), (1024, 900, 8, 1)]:
@@ -140,12 +140,14 @@ def test_random_system_parity(snp, m, F, depth, bits, dedup, target):
     assert_same_tree(tree, ref)
 
 
-@pytest.mark.parametrize("kernels", ["", "expand_t", "kc_global_e", "no_tc"])
+@pytest.mark.parametrize("kernels", ["", "expand_t", "kc_global_e", "no_tc", "kc_tc", "kc_tc,kc_global_e"])
 def test_uint8_large_counts(snp, monkeypatch, kernels):
     """uint8 storage with counts well above the 32-entry register tables, so
     the table-fallback paths of K-a and K-c run; SNP_KERNELS=expand_t selects
     the 8-configurations-per-lane K-a instead of the 4-per-lane one,
-    kc_global_e the K-c variant that gathers emit words from global memory."""
+    kc_global_e the K-c variant that gathers emit words from global memory,
+    kc_tc the K-c whose output permutation runs on the tensor cores (level 1
+    has > 8 sectors of children per block: its per-lane byte fallback)."""
     monkeypatch.setenv("SNP_KERNELS", kernels)
     w = W.random_system(700, outdeg=8, k_nd=5, seed=77)
     rng = np.random.default_rng(77)
