@@ -834,7 +834,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   SNP_TRY(s->d_tab.ensure((size_t)m * tabw, false));
   SNP_TRY(s->d_ctab.ensure((size_t)m * tabw * s->bytes, false));
   if (s->bytes == 1) SNP_TRY(s->d_tab_full.ensure((size_t)m * 256, false));
-  if (s->bytes == 1) SNP_TRY(s->d_ttab.ensure((size_t)m * (32 + 256), false));
+  SNP_TRY(s->d_ttab.ensure((size_t)m * (32 + 256), false));  // every width (K-c NARROW for 16/32-bit counts)
   if (s->bytes == 1) SNP_TRY(s->d_elut.ensure((size_t)m * 32, false));
   if (s->bytes == 1) SNP_TRY(s->d_hsg.ensure((size_t)m * 256, false));
   SysView& v = s->view;
@@ -846,7 +846,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.tab = s->d_tab.as<uint8_t>();
   v.tab_full = s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr;
   v.ctab = s->d_ctab.p;
-  v.ttab = s->bytes == 1 ? s->d_ttab.as<uint8_t>() : nullptr;
+  v.ttab = s->d_ttab.as<uint8_t>();
   v.elut = s->bytes == 1 ? s->d_elut.as<uint8_t>() : nullptr;
   v.hsg = s->bytes == 1 ? s->d_hsg.as<uint8_t>() : nullptr;
   v.any_generic = 0;
@@ -865,6 +865,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     if (k && strstr(k, "kc_global_e")) v.kernel_flags |= KF_KC_GLOBAL_E;
     if (k && strstr(k, "no_tc")) v.kernel_flags |= KF_NO_TC;
     if (k && strstr(k, "kc_tc")) v.kernel_flags |= KF_KC_TC;
+    if (k && strstr(k, "kc_wide_exact")) v.kernel_flags |= KF_KC_WIDE_EXACT;  // 16/32-bit K-c in full width
   }
   v.m = (int32_t)m;
   v.n = n;
@@ -888,7 +889,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   s->own_stream = true;
   launch_build_tables(v, s->bytes, s->d_tab.as<uint8_t>(), s->d_ctab.p,
                       s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr,
-                      s->bytes == 1 ? s->d_ttab.as<uint8_t>() : nullptr,
+                      s->d_ttab.as<uint8_t>(),
                       s->bytes == 1 ? s->d_elut.as<uint8_t>() : nullptr,
                       s->bytes == 1 ? s->d_hsg.as<uint8_t>() : nullptr, s->stream);
   CUDA_TRY(cudaGetLastError());
@@ -996,7 +997,33 @@ snp_status zero_counters(snp_system* s) {
   return SNP_OK;
 }
 
+// entries of the K-c overflow list (2^22; SNP_OVF_CAP overrides it for tests)
+uint64_t ovf_capacity() {
+  const char* e = getenv("SNP_OVF_CAP");
+  const long long v = e ? atoll(e) : 0;
+  return v > 0 ? (uint64_t)v : (1ULL << 22);
+}
 DevCounters* dc(snp_system* s) { return s->counters_dev.as<DevCounters>(); }
+
+// 16/32-bit counts: K-c computes x in bytes (NARROW) and lists every x outside
+// [0, 255] for an exact rewrite; a level with more of them than the list holds
+// is materialised again in full width (K-c and k_patch overwrite every kept
+// child, so nothing of the first pass survives)
+snp_status rematerialize_wide(snp_system* s, const LevelView& LV, const ExpandOut& O, const NextArrays& N, int64_t K,
+                              uint64_t ovf_cap, int32_t* err, DevCounters* hc) {
+  if (hc->n_ovf <= ovf_cap || !materialize_narrow_ok(s->view, s->bytes)) return SNP_OK;
+  cudaStream_t st = s->stream;
+  SysView wv = s->view;
+  wv.kernel_flags |= KF_KC_WIDE_EXACT;
+  CUDA_TRY(cudaMemsetAsync(&dc(s)->n_ovf, 0, sizeof(unsigned long long), st));
+  phase_begin(s, 3);
+  launch_materialize(wv, s->bytes, LV, O, s->kq_off.as<uint64_t>(), N, K, s->ovf.as<uint64_t>(), &dc(s)->n_ovf,
+                     ovf_cap, err, st);
+  launch_patch(wv, s->bytes, LV, O, N, K, err, st);
+  phase_end(s);
+  CUDA_TRY(cudaGetLastError());
+  return read_counters(s, hc);
+}
 
 snp_status begin_impl(snp_system* s, const snp_configs* level0) {
   g_trace.start();
@@ -1299,7 +1326,7 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
       N.data = next->data.p;
       // ---- K-c materialize kept children
       SNP_TRY(s->kq_off.ensure((F + 1) * 8));
-      const uint64_t ovf_cap = 1ULL << 22;
+      const uint64_t ovf_cap = ovf_capacity();
       SNP_TRY(s->ovf.ensure(ovf_cap * 8));
       phase_begin(s, 3);
       launch_kq_off(off, C.kpos, F, s->kq_off.as<uint64_t>(), st);
@@ -1309,6 +1336,7 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
       phase_end(s);
       CUDA_TRY(cudaGetLastError());
       SNP_TRY(read_counters(s, &hc));
+      SNP_TRY(rematerialize_wide(s, LV, O, N, K, ovf_cap, err, &hc));
       if (hc.n_ovf > ovf_cap) return fail(SNP_E_CAPACITY, "too many counts at the storage limit (%llu)", hc.n_ovf);
       lc.overflow_fixes = (int64_t)hc.n_ovf;
       if (hc.n_ovf) {
@@ -2477,7 +2505,7 @@ snp_status snp_dist_commit(snp_system* s, int64_t parent_offset, int64_t q_offse
     SNP_TRY(take_buffer(s, level_bytes(K, m, s->bytes), &L->data));
     N.data = L->data.p;
     SNP_TRY(s->kq_off.ensure((F + 1) * 8));
-    const uint64_t ovf_cap = 1ULL << 22;
+    const uint64_t ovf_cap = ovf_capacity();
     SNP_TRY(s->ovf.ensure(ovf_cap * 8));
     LevelView LV{cur->data.p, F, cur->fp0.as<uint64_t>(), cur->fp1.as<uint64_t>()};
     const ExpandOut& O = s->dist.O;
@@ -2490,6 +2518,7 @@ snp_status snp_dist_commit(snp_system* s, int64_t parent_offset, int64_t q_offse
     CUDA_TRY(cudaGetLastError());
     DevCounters hc;
     SNP_TRY(read_counters(s, &hc));
+    SNP_TRY(rematerialize_wide(s, LV, O, N, K, ovf_cap, err, &hc));
     if (hc.n_ovf > ovf_cap) return fail(SNP_E_CAPACITY, "too many counts at the storage limit (%llu)", hc.n_ovf);
     if (hc.n_ovf) {
       launch_overflow_fix(s->view, s->bytes, LV, O, s->kq_off.as<uint64_t>(), N, s->ovf.as<uint64_t>(), hc.n_ovf, err,

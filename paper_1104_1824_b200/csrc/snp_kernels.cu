@@ -1590,7 +1590,7 @@ constexpr int KCT_BBYTES = 2 * 2 * KCT_BHALF;      // 2 rounds × (P1, P2)
 // (large m) the in-synapse gather reads them from global memory (L2/L1).
 // MWT: warps per CTA (MW; fewer for wide counts, whose per-lane staging of
 // 64 values would not fit shared memory at MW warps — int32 at config 3).
-template <typename T, int NPL, bool ES, int MWT = MW, bool TCS = false>
+template <typename T, int NPL, bool ES, int MWT = MW, bool TCS = false, bool NARROW = false>
 __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelView L, ExpandOut O,
                                                              const uint64_t* kq_off, NextArrays N, uint64_t* ovf,
                                                              unsigned long long* n_ovf, uint64_t ovf_cap) {
@@ -1599,7 +1599,8 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
   const int64_t mE = (m + 1) & ~1;
   uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words + 2 zero words
   uint8_t* sX = smem + (ES ? (mE + 2) * 8 : 0);                         // MWT×32×xs_stride (TCS: the A tiles)
-  uint8_t* sR = sX + (TCS ? (size_t)MWT / 4 * KCT_ATILE + KCT_BBYTES : (size_t)MWT * 32 * xs_stride<T>());  // QCAP + 32
+  constexpr int XS = NARROW ? xs_stride<uint8_t>() : xs_stride<T>();  // staging row stride (NARROW: bytes)
+  uint8_t* sR = sX + (TCS ? (size_t)MWT / 4 * KCT_ATILE + KCT_BBYTES : (size_t)MWT * 32 * XS);  // QCAP + 32
   uint32_t* sD = reinterpret_cast<uint32_t*>(sR + QCAP + 32);           // (QCAP+32)/4 quad descriptors
   uint64_t* sOps = reinterpret_cast<uint64_t*>(sD + (TCS ? 0 : (QCAP + 32) / 4));  // OPCAP store ops
   uint64_t* sQ = sOps + (TCS ? 0 : OPCAP);                              // 65 (+1 pad)
@@ -1739,7 +1740,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
   // this lane's x row: the staging row (xs_stride), or (TCS) row 32·(warp%4) +
   // lane of the warp's A tile, byte r at (r/16)·KCT_A_LBO + r%16
   uint8_t* xsb = TCS ? sX + (warp >> 2) * KCT_ATILE + (((warp & 3) * 32 + lane) >> 3) * 128 + (lane & 7) * 16
-                     : sX + (size_t)(warp * 32 + lane) * xs_stride<T>();
+                     : sX + (size_t)(warp * 32 + lane) * XS;
   T* xs = reinterpret_cast<T*>(xsb);
   auto xb = [&](int r) -> uint8_t* { return TCS ? xsb + (r >> 4) * KCT_A_LBO + (r & 15) : xsb + r; };
   const T* ctab = reinterpret_cast<const T*>(S.ctab);
@@ -1839,8 +1840,8 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
     const T* crow_g = ctab + (int64_t)j * S.tabw;
     const bool generic = mt.flags & NM_GENERIC;
     uint64_t ovf_bits = 0;
-    if (sizeof(T) == 1 && !generic) {
-      // fast path (u8): the post-consumption table t(v) = v - c_first(v) for
+    if ((sizeof(T) == 1 || NARROW) && !generic) {
+      // fast path (u8, and NARROW: wide counts < 256 as bytes): the post-consumption table t(v) = v - c_first(v) for
       // v < 32 lives in 8 registers and is looked up 4 parents at a time by
       // byte permutes; the bit-sliced counts become bytes by an 8x8 bit
       // transpose per 8 parents; x = t + count is one 32-bit add per 4 parents
@@ -1862,10 +1863,54 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
           for (int i = 0; i < 8; ++i) vn[i] = 0;
 #else
         uint32_t vw[8];
-        if (32 * g < np) ldg256(row + 32 * g, vw);
-        else
+        bool big = false;  // NARROW: a count of this half is >= 256 (or negative)
+        if (32 * g >= np) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) vw[i] = 0;
+        } else if constexpr (sizeof(T) == 1) {
+          ldg256(row + 32 * g, vw);
+        } else if constexpr (sizeof(T) == 2) {
+          // 32 uint16 counts (2 × 32 B): the low bytes, 4 per word
+          uint32_t u[8];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            ldg256(row + 32 * g + 16 * h, u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              vw[4 * h + i] = prmt(u[2 * i], u[2 * i + 1], 0x6420u);
+              big |= ((u[2 * i] | u[2 * i + 1]) & 0xFF00FF00u) != 0;
+            }
+          }
+        } else {
+          // 32 int32 counts (4 × 32 B): the low bytes, 4 per word
+          uint32_t u[8];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            ldg256(row + 32 * g + 8 * h, u);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              vw[2 * h + i] = prmt(prmt(u[4 * i], u[4 * i + 1], 0x0040u), prmt(u[4 * i + 2], u[4 * i + 3], 0x0040u),
+                                   0x5410u);
+              big |= ((u[4 * i] | u[4 * i + 1] | u[4 * i + 2] | u[4 * i + 3]) & 0xFFFFFF00u) != 0;
+            }
+          }
+        }
+        if (NARROW && __any_sync(__activemask(), big)) {
+          // rare: exact per parent; x is kept as its low byte and every x
+          // outside [0, 255] is rewritten exactly by k_overflow_fix
+          for (int k = 0; k < 32; ++k) {
+            const int r = 32 * g + k;
+            const int64_t v = r < np ? (int64_t)row[r] : 0;
+            const int32_t cons = (int32_t)crow_g[table_index((uint32_t)v, mt)];
+            int32_t cnt = 0;
+#pragma unroll
+            for (int b = 0; b < NPL; ++b) cnt |= (int32_t)((c[b] >> r) & 1ULL) << b;
+            const int64_t x = v - cons + cnt;
+            xsb[r] = (uint8_t)x;
+            if (x < 0 || x > 255) ovf_bits |= 1ULL << r;
+          }
+          continue;
+        }
 #endif
         // t = v - c_first(v) for the 32 counts: byte permutes unless some
         // count >= 32 (rare: that quad folds through the compact table)
@@ -2074,7 +2119,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
         for (uint64_t q = Q0; q < Q1; ++q) out[eidx((int64_t)q, j, m)] = xs[sR[q - Qb]];
     } else {
       for (int r = 0; r < np; ++r)
-        for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = xs[r];
+        for (uint64_t q = sQ[r]; q < sQ[r + 1]; ++q) out[eidx((int64_t)q, j, m)] = NARROW ? (T)xsb[r] : xs[r];
     }
     }  // j < m
     if constexpr (TCS) {
@@ -2163,8 +2208,9 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       __syncwarp();
       const int32_t jn = m - jbase;
       for (int r = 0; r < 32 && r < jn; ++r) {
-        const T* xr = reinterpret_cast<const T*>(sX + (size_t)(warp * 32 + r) * xs_stride<T>());
-        for (uint64_t q = Q0 + lane; q < Q1; q += 32) out[eidx((int64_t)q, jbase + r, m)] = xr[sR[q - Qb]];
+        const uint8_t* xr = sX + (size_t)(warp * 32 + r) * XS;
+        for (uint64_t q = Q0 + lane; q < Q1; q += 32)
+          out[eidx((int64_t)q, jbase + r, m)] = NARROW ? (T)xr[sR[q - Qb]] : reinterpret_cast<const T*>(xr)[sR[q - Qb]];
       }
       __syncwarp();
     }
@@ -3035,7 +3081,7 @@ __global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_fu
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t w = S.tabw;
   const int64_t n_c = (int64_t)S.m * w;
-  const int64_t n_f = tab_full ? (int64_t)S.m * 256 : 0;
+  const int64_t n_f = (tab_full || ttab) ? (int64_t)S.m * 256 : 0;  // ttab alone for wide counts (K-c NARROW)
   if (i >= n_c + n_f) return;
   const bool full = i >= n_c;
   const int32_t s = (int32_t)(full ? (i - n_c) / 256 : i / w);
@@ -3060,13 +3106,13 @@ __global__ void k_build_tables(SysView S, uint8_t* tab, T* ctab, uint8_t* tab_fu
     }
   }
   if (full) {
-    tab_full[i - n_c] = (uint8_t)entry;
+    if (tab_full) tab_full[i - n_c] = (uint8_t)entry;
     // post-consumption value v - c_first(v) (K-c lookups): counts < 32 in
     // the 32-byte rows (one coalesced 32-B load per lane, then byte
     // permutes in registers), every count in the 256-byte rows
     if (slot < 32) ttab[(int64_t)s * 32 + slot] = (uint8_t)(slot - (uint32_t)cons);
     ttab[(int64_t)S.m * 32 + (int64_t)s * 256 + slot] = (uint8_t)(slot - (uint32_t)cons);
-    if (slot < 32) elut[(int64_t)s * 32 + slot] = (uint8_t)entry;
+    if (slot < 32 && elut) elut[(int64_t)s * 32 + slot] = (uint8_t)entry;
   } else {
     tab[i] = (uint8_t)entry;
     ctab[i] = (T)cons;
@@ -3590,7 +3636,7 @@ bool fast_expand_ok(const SysView& S) { return S.tables_ok != 0; }
 
 void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ctab, uint8_t* tab_full,
                          uint8_t* ttab, uint8_t* elut, uint8_t* hsg, cudaStream_t st) {
-  const uint64_t n = (uint64_t)S.m * S.tabw + (tab_full ? (uint64_t)S.m * 256 : 0);
+  const uint64_t n = (uint64_t)S.m * S.tabw + ((tab_full || ttab) ? (uint64_t)S.m * 256 : 0);
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
     k_build_tables<T><<<grid_for(n), BLK, 0, st>>>(S, tab, reinterpret_cast<T*>(ctab), tab_full, ttab, elut);
@@ -3607,9 +3653,16 @@ constexpr size_t KC_SMEM_MAX = 220 * 1024;
 // K-c warps per CTA: MW for 1-2 byte counts, 8 for int32 (staging fits)
 int kc_warps(int32_t bytes) { return bytes == 4 ? 8 : MW; }
 
+// wide counts (16/32-bit) computed as bytes (NARROW): every count and x of a
+// level < 256 in the common case; staging rows of bytes, so the CTA keeps
+// MW warps; x outside [0, 255] goes through the overflow list (exact rewrite)
+bool materialize_narrow_ok(const SysView& S, int32_t bytes) {
+  return bytes > 1 && S.ttab != nullptr && !(S.kernel_flags & KF_KC_WIDE_EXACT);
+}
+
 size_t materialize_smem_bytes(const SysView& S, int32_t bytes, bool staged_e) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
-  const size_t xs = (size_t)kc_warps(bytes) * 32 * (PB * bytes + 4);
+  const size_t xs = materialize_narrow_ok(S, bytes) ? (size_t)MW * 32 * (PB + 4) : (size_t)kc_warps(bytes) * 32 * (PB * bytes + 4);
   return (staged_e ? (mE + 2) * 8 : 0) + xs + 2 * (QCAP + 32) + 8 * OPCAP + 67 * 8 + 16 + 16;
 }
 
@@ -3769,10 +3822,28 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
     dispatch_bytes(bytes, [&](auto tt) {
       using T = decltype(tt);
       constexpr int W = sizeof(T) == 4 ? 8 : MW;  // = kc_warps(bytes)
+      int threads = W * 32;
       auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<nblk, W * 32, smem, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
+        kern<<<nblk, threads, smem, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
       };
+      if constexpr (sizeof(T) > 1) {
+        if (materialize_narrow_ok(S, bytes)) {
+          threads = MW * 32;
+          if (staged) {
+            if (S.max_indeg < 16) go(k_materialize_bs<T, 4, true, MW, false, true>);
+            else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, true, MW, false, true>);
+            else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, true, MW, false, true>);
+            else go(k_materialize_bs<T, 8, true, MW, false, true>);
+          } else {
+            if (S.max_indeg < 16) go(k_materialize_bs<T, 4, false, MW, false, true>);
+            else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, false, MW, false, true>);
+            else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, false, MW, false, true>);
+            else go(k_materialize_bs<T, 8, false, MW, false, true>);
+          }
+          return;
+        }
+      }
       if constexpr (sizeof(T) == 1) {
         if (tcs) {
           if (staged) {

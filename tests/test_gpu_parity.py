@@ -400,3 +400,25 @@ def test_small_path_equals_big_path(snp, monkeypatch, case):
     assert_same_tree(small, ref)
     assert_same_tree(big, ref)
     assert small.counters.halting.tolist() == big.counters.halting.tolist()
+
+
+@pytest.mark.parametrize("bits", [16, 32])
+@pytest.mark.parametrize("cap", ["", "16"])
+def test_wide_counts_narrow_kc(snp, monkeypatch, bits, cap):
+    """16/32-bit storage: K-c computes x in bytes (NARROW) and rewrites every
+    x outside [0, 255] exactly (the overflow list); counts far above 255 take
+    the per-parent exact fallback; SNP_OVF_CAP=16 overflows the list so the
+    level is materialised again in full width.  Also SNP_KERNELS=kc_wide_exact
+    (full width from the start).  Every variant gives the oracle's tree."""
+    monkeypatch.setenv("SNP_OVF_CAP", cap)
+    w = W.random_system(700, outdeg=8, k_nd=5, seed=91)
+    rng = np.random.default_rng(91)
+    L0 = W.level0_counts(w, 900, 91)
+    L0[::5] = rng.integers(0, 900, size=L0[::5].shape)  # some rows far above one byte
+    L0[1::9] += 240                                        # x near the byte boundary
+    dedup = 0 if bits == 32 else 1
+    for kern in ["", "kc_wide_exact"]:
+        monkeypatch.setenv("SNP_KERNELS", kern)
+        tree = snp.System(w, count_bits=bits, dedup=dedup, frontier_target=800).explore(L0, depth=3)
+        ref = oracle.System.from_workload(w).explore(L0, depth=3, dedup=dedup, count_bits=bits, frontier_target=800)
+        assert_same_tree(tree, ref)
