@@ -142,12 +142,15 @@ KERNEL_OF = {"expand": "K-a k_expand_tc (tensor cores) + k_nd_pass, else k_expan
              "dedup": "K-d k_dedup..k_compact", "keys": "K-b k_child_keys"}
 
 
-def ncu_traffic(kernel_phase):
+def ncu_traffic(kernel_phase, config):
     """dram bytes per launch of the dominant kernel from the committed ncu
-    summary (profiles/ncu_summary.json), or None."""
+    summary (profiles/ncu_summary.json) when it was captured on this
+    workload (its "config"), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         d = json.load(open(path))
+        if int(d.get("config", 4)) != int(config):
+            return None
         return d["kernels"][kernel_phase]["dram_bytes_per_launch"]
     except Exception:
         return None
@@ -340,7 +343,7 @@ def run_native(args, rank, world):
                    if use_dist else "1 GPU"},
         "roofline": {"bound": "hbm", "kernel": f"phase '{dom}' ({KERNEL_OF.get(dom, dom)})",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(dom), "peak_source": peak_src},
+                     "traffic": ncu_traffic(dom, args.config), "peak_source": peak_src},
         "step_roofline": {"algorithmic_GB_per_step_per_gpu": sb / len(levels) / 1e9,
                           "achieved_per_gpu": sb / (elapsed_ms / 1e3) / 1e9,
                           "frac": sb / (elapsed_ms / 1e3) / 1e9 / peak},

@@ -2378,9 +2378,12 @@ __device__ __forceinline__ int first_rule(const SysView& S, int32_t s, int32_t v
 // The fired rule's (c, p) of every neuron of one child into a warp's
 // shared-memory slice: first applicable rules, then the ND digits of cx.
 template <typename T>
-__device__ void fired_cp(const SysView& S, const void* data, int64_t p, const ChildCtx& cx, int2* fc, int lane) {
+__device__ void fired_cp(const SysView& S, const void* data, int64_t p, const ChildCtx& cx, int2* fc, int lane,
+                         int32_t* cnt = nullptr) {
   for (int32_t s = lane; s < S.m; s += 32) {
-    const int r = first_rule(S, s, ld_count<T>(data, p, s, S.m));
+    const int32_t v = ld_count<T>(data, p, s, S.m);
+    if (cnt) cnt[s] = v;
+    const int r = first_rule(S, s, v);
     fc[s] = r >= 0 ? make_int2(S.rules[r].c, S.rules[r].p) : make_int2(0, 0);
   }
   __syncwarp();
@@ -2396,9 +2399,12 @@ __device__ void fired_cp(const SysView& S, const void* data, int64_t p, const Ch
 // the same with (c, p) packed as c | p << 8 (every rule has c, p <= 255):
 // 2 bytes per neuron instead of 8, so 4x the verification warps fit an SM
 template <typename T>
-__device__ void fired_cp(const SysView& S, const void* data, int64_t p, const ChildCtx& cx, uint16_t* fc, int lane) {
+__device__ void fired_cp(const SysView& S, const void* data, int64_t p, const ChildCtx& cx, uint16_t* fc, int lane,
+                         int32_t* cnt = nullptr) {
   for (int32_t s = lane; s < S.m; s += 32) {
-    const int r = first_rule(S, s, ld_count<T>(data, p, s, S.m));
+    const int32_t v = ld_count<T>(data, p, s, S.m);
+    if (cnt) cnt[s] = v;
+    const int r = first_rule(S, s, v);
     fc[s] = r >= 0 ? (uint16_t)(S.rules[r].c | (S.rules[r].p << 8)) : (uint16_t)0;
   }
   __syncwarp();
@@ -2520,47 +2526,59 @@ __global__ void __launch_bounds__(VERIFY_WARPS * 32) k_verify_s(SysView S, Level
 // rows; (2) a thread per (match, column) rebuilds the column of eq. (2) from
 // them and compares it with the other row (the winner's, or the stored
 // configuration of an earlier level).  A mismatch is a 128-bit collision.
+// batch row i: 2m fired (c, p) entries (child, other child), then 2m counts
+// of their parents (row-major, so the column pass reads them coalesced
+// instead of one sector per count from the block layout)
+template <typename FC>
+__device__ __forceinline__ FC* vrow_fc(uint8_t* base, uint64_t i, int32_t m) {
+  return reinterpret_cast<FC*>(base + i * (2 * (uint64_t)m * (sizeof(FC) + 4)));
+}
+template <typename FC>
+__device__ __forceinline__ int32_t* vrow_cnt(uint8_t* base, uint64_t i, int32_t m) {
+  return reinterpret_cast<int32_t*>(base + i * (2 * (uint64_t)m * (sizeof(FC) + 4)) + 2 * (uint64_t)m * sizeof(FC));
+}
+
 template <typename T, typename FC>
 __global__ void k_verify_fc(SysView S, LevelView L, ExpandOut O, const uint64_t* off, ChildArrays C,
-                            const uint64_t* list, uint64_t i0, uint64_t n, uint64_t tag_base, Tables tb, FC* fcg) {
+                            const uint64_t* list, uint64_t i0, uint64_t n, uint64_t tag_base, Tables tb, uint8_t* fcg) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t i = warp; i < n; i += nwarps) {
     const uint64_t c = list[i0 + i];
-    FC* fa = fcg + i * 2 * (uint64_t)S.m;
+    FC* fa = vrow_fc<FC>(fcg, i, S.m);
+    int32_t* ca = vrow_cnt<FC>(fcg, i, S.m);
     const uint32_t p = C.cpar[c];
     ChildCtx cx;
     decode_child(S, O.nd + (uint64_t)p * KMAX, O.ndc[p], c - off[p], cx);
-    fired_cp<T>(S, L.data, p, cx, fa, lane);
+    fired_cp<T>(S, L.data, p, cx, fa, lane, ca);
     if (C.verdict[c] == 1) {
       const uint64_t o = tb.ltab[C.cslot[c]].tag - tag_base;
       const uint32_t po = C.cpar[o];
       ChildCtx co;
       decode_child(S, O.nd + (uint64_t)po * KMAX, O.ndc[po], o - off[po], co);
-      fired_cp<T>(S, L.data, po, co, fa + S.m, lane);
+      fired_cp<T>(S, L.data, po, co, fa + S.m, lane, ca + S.m);
     }
   }
 }
 
 template <typename T, typename FC>
 __global__ void k_verify_cols(SysView S, LevelView L, ChildArrays C, const uint64_t* list, uint64_t i0, uint64_t n,
-                              uint64_t tag_base, Tables tb, const FC* fcg, const StoredLevel* stored, int32_t* err) {
+                              uint64_t tag_base, Tables tb, uint8_t* fcg, const StoredLevel* stored, int32_t* err) {
   for (uint64_t i = blockIdx.y; i < n; i += gridDim.y) {
     const uint64_t c = list[i0 + i];
     const uint8_t vd = C.verdict[c];
-    const uint32_t p = C.cpar[c];
-    const FC* fa = fcg + i * 2 * (uint64_t)S.m;
-    const uint32_t po = vd == 1 ? C.cpar[tb.ltab[C.cslot[c]].tag - tag_base] : 0;
+    const FC* fa = vrow_fc<FC>(fcg, i, S.m);
+    const int32_t* ca = vrow_cnt<FC>(fcg, i, S.m);
     const uint64_t ref = vd == 1 ? 0 : C.cref[c];
     bool diff = false;
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < S.m; j += gridDim.x * blockDim.x) {
-      int64_t a = (int64_t)ld_count<T>(L.data, p, j, S.m) - fc_c(fa[j]);
+      int64_t a = (int64_t)ca[j] - fc_c(fa[j]);
       for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) a += fc_p(fa[S.in_src[e]]);
       int64_t b;
       if (vd == 1) {
         const FC* fb = fa + S.m;
-        b = (int64_t)ld_count<T>(L.data, po, j, S.m) - fc_c(fb[j]);
+        b = (int64_t)ca[S.m + j] - fc_c(fb[j]);
         for (int e = S.in_off[j]; e < S.in_off[j + 1]; ++e) b += fc_p(fb[S.in_src[e]]);
       } else {
         b = ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, S.m);
@@ -3944,7 +3962,7 @@ void launch_verify_list(const ChildArrays& C, uint64_t T, uint64_t tag_base, con
   count_launch();
 }
 
-size_t verify2_row_bytes(const SysView& S) { return (size_t)2 * S.m * (S.small_cp ? 2 : 8); }
+size_t verify2_row_bytes(const SysView& S) { return (size_t)2 * S.m * ((S.small_cp ? 2 : 8) + 4); }
 
 void launch_verify_batch(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
                          const ChildArrays& C, const uint64_t* list, uint64_t i0, uint64_t n, uint64_t tag_base,
@@ -3954,15 +3972,13 @@ void launch_verify_batch(const SysView& S, int32_t bytes, const LevelView& L, co
     using TT = decltype(tt);
     const unsigned gw = (unsigned)std::min<uint64_t>((n * 32 + 255) / 256, 148u * 32u);
     dim3 gc((unsigned)std::min<int64_t>((S.m + 255) / 256, 64), (unsigned)std::min<uint64_t>(n, 65535));
+    uint8_t* fcb = reinterpret_cast<uint8_t*>(fc);
     if (S.small_cp) {
-      k_verify_fc<TT, uint16_t><<<gw, 256, 0, st>>>(S, L, O, off, C, list, i0, n, tag_base, tb,
-                                                     reinterpret_cast<uint16_t*>(fc));
-      k_verify_cols<TT, uint16_t><<<gc, 256, 0, st>>>(S, L, C, list, i0, n, tag_base, tb,
-                                                       reinterpret_cast<const uint16_t*>(fc), stored, err);
+      k_verify_fc<TT, uint16_t><<<gw, 256, 0, st>>>(S, L, O, off, C, list, i0, n, tag_base, tb, fcb);
+      k_verify_cols<TT, uint16_t><<<gc, 256, 0, st>>>(S, L, C, list, i0, n, tag_base, tb, fcb, stored, err);
     } else {
-      k_verify_fc<TT, int2><<<gw, 256, 0, st>>>(S, L, O, off, C, list, i0, n, tag_base, tb, reinterpret_cast<int2*>(fc));
-      k_verify_cols<TT, int2><<<gc, 256, 0, st>>>(S, L, C, list, i0, n, tag_base, tb, reinterpret_cast<const int2*>(fc),
-                                                   stored, err);
+      k_verify_fc<TT, int2><<<gw, 256, 0, st>>>(S, L, O, off, C, list, i0, n, tag_base, tb, fcb);
+      k_verify_cols<TT, int2><<<gc, 256, 0, st>>>(S, L, C, list, i0, n, tag_base, tb, fcb, stored, err);
     }
   });
   count_launch(2);

@@ -5,7 +5,7 @@ Capture (one GPU, full bench size; three metrics = one pass, no replay):
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
       --clock-control none --csv -k regex:"k_expand|k_nd_pass|k_materialize|k_patch" -s 6 -c 6 \
       --log-file gpurun_out/dram_full.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu
-Usage: python tools/ncu_summary.py gpurun_out/dram_full.csv [profiles/ncu_summary.json]
+Usage: python tools/ncu_summary.py gpurun_out/dram_full.csv [profiles/ncu_summary.json] [config]
 """
 import csv
 import json
@@ -16,7 +16,7 @@ PHASE = {"k_expand": "expand", "k_nd_pass": "expand", "k_materialize": "material
          "k_overflow_fix": "materialize"}
 
 
-def main(src, dst="profiles/ncu_summary.json"):
+def main(src, dst="profiles/ncu_summary.json", config=4):
     rows = [r for r in csv.reader(open(src)) if len(r) > 14 and r[0].isdigit()]
     per_launch = defaultdict(dict)  # launch id -> {kernel, metrics}
     for r in rows:
@@ -41,7 +41,7 @@ def main(src, dst="profiles/ncu_summary.json"):
         ph["dram_bytes_per_launch"] = ph["dram_read"] + ph["dram_write"]
     out = {"note": "dram bytes per launch (read + write) of each hot phase's kernels at the bench's "
                    "full size, one ncu pass with three metrics (no replay); cold-cache serialised launches",
-           "source": src, "kernels": phases}
+           "source": src, "config": int(config), "kernels": phases}
     json.dump(out, open(dst, "w"), indent=1)
     print(json.dumps(out, indent=1))
 
