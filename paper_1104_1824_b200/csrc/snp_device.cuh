@@ -87,7 +87,7 @@ enum : int32_t { NM_GENERIC = 1, NM_ND = 2 };
 // that rule's 16-B fingerprint delta in a neuron's 256-B slice.
 enum : uint32_t { TE_EMIT = 1u, TE_ND = 2u, TE_F = 0xF0u };
 // kernel selection flags (SysView::kernel_flags)
-enum : int32_t { KF_EXPAND_T = 1, KF_KC_GLOBAL_E = 2, KF_NO_TC = 4, KF_KC_TC = 8, KF_KC_WIDE_EXACT = 16 };
+enum : int32_t { KF_EXPAND_T = 1, KF_KC_GLOBAL_E = 2, KF_NO_TC = 4, KF_KC_TC = 8, KF_KC_WIDE_EXACT = 16, KF_FP_WEAK = 32 };
 
 __device__ __forceinline__ uint32_t table_index(uint32_t v, const NeuronMeta& mt) {
   // unsigned compare: lanes past F in a partial block may hold any bit

@@ -866,6 +866,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     if (k && strstr(k, "no_tc")) v.kernel_flags |= KF_NO_TC;
     if (k && strstr(k, "kc_tc")) v.kernel_flags |= KF_KC_TC;
     if (k && strstr(k, "kc_wide_exact")) v.kernel_flags |= KF_KC_WIDE_EXACT;  // 16/32-bit K-c in full width
+    if (k && strstr(k, "fp_weak")) v.kernel_flags |= KF_FP_WEAK;  // tests: 6-bit child keys (the verification must object)
   }
   v.m = (int32_t)m;
   v.n = n;
@@ -1354,10 +1355,15 @@ snp_status advance_impl(snp_system* s, snp_level_counters* out) {
       SNP_TRY(update_stored_table(s));
       phase_begin(s, 4);
       SNP_TRY(s->vlist.ensure(std::max<uint64_t>(T, s->child_cap) * 8 + 16));  // sized with the child arrays
-      if (s->view.aug_rule < 0) {
+      const char* vb = getenv("SNP_VERIFY_BATCH");  // tests: the batched two-pass path
+      if (s->view.aug_rule < 0) launch_verify_list(C, T, tag_base, tb, s->vlist.as<uint64_t>(), &dc(s)->n_verify, st);
+      if (s->view.aug_rule < 0 && !(vb && vb[0] == '1') &&
+          launch_verify_m(s->view, s->bytes, LV, O, off, C, s->vlist.as<uint64_t>(), &dc(s)->n_verify, tag_base, tb,
+                          s->stored.as<StoredLevel>(), err, st)) {
+        // the key matches listed, then one CTA per match (no host round trip)
+      } else if (s->view.aug_rule < 0) {
         // the key matches listed, then verified in batches by the two fully
         // parallel passes (fired (c, p) rows, then one thread per column)
-        launch_verify_list(C, T, tag_base, tb, s->vlist.as<uint64_t>(), &dc(s)->n_verify, st);
         unsigned long long nv = 0;
         CUDA_TRY(cudaMemcpyAsync(&nv, &dc(s)->n_verify, 8, cudaMemcpyDeviceToHost, st));
         SNP_TRY(sync(s));

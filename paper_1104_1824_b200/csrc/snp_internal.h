@@ -111,6 +111,9 @@ void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const Ex
 void launch_verify_list(const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, uint64_t* list,
                         unsigned long long* n_list, cudaStream_t st);
 size_t verify2_row_bytes(const SysView& S);
+bool launch_verify_m(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
+                     const ChildArrays& C, const uint64_t* list, const unsigned long long* n_list, uint64_t tag_base,
+                     const Tables& tb, const StoredLevel* stored, int32_t* err, cudaStream_t st);
 void launch_verify_batch(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
                          const ChildArrays& C, const uint64_t* list, uint64_t i0, uint64_t n, uint64_t tag_base,
                          const Tables& tb, const StoredLevel* stored, void* fc, int32_t* err, cudaStream_t st);

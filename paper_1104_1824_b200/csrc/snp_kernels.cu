@@ -1197,6 +1197,10 @@ __global__ void k_child_keys(SysView S, const uint64_t* off, ExpandOut O, uint64
         b += __ldg(S.h1 + rc) - __ldg(S.h1 + rf);
       }
     }
+    if (S.kernel_flags & KF_FP_WEAK) {  // tests only: 6-bit keys, so distinct children share keys
+      a &= 63;
+      b = 0;
+    }
     C.cfp0[c] = a;
     C.cfp1[c] = b;
   }
@@ -2589,6 +2593,96 @@ __global__ void k_verify_cols(SysView S, LevelView L, ChildArrays C, const uint6
   }
 }
 
+// dedup = 0, one CTA per listed key match (grid-stride): both children's
+// parent counts and fired (c, p) of every neuron into shared memory (the
+// counts come from the block layout, one sector each: the floor of this
+// pass), the ND digits decoded once, then a thread per column rebuilds eq.
+// (2) for both and compares (or against the stored configuration of an
+// earlier level).  A mismatch is a 128-bit collision (reading A18).
+constexpr int VM_THREADS = 256;
+template <typename FC>
+size_t verify_m_smem_bytes(int32_t m) { return (size_t)2 * m * (4 + sizeof(FC)) + 2 * KMAX * 8 + 64; }
+
+template <typename FC>
+__device__ __forceinline__ FC fc_pack(int32_t c, int32_t p);
+template <>
+__device__ __forceinline__ uint16_t fc_pack<uint16_t>(int32_t c, int32_t p) { return (uint16_t)(c | (p << 8)); }
+template <>
+__device__ __forceinline__ int2 fc_pack<int2>(int32_t c, int32_t p) { return make_int2(c, p); }
+
+template <typename T, typename FC>
+__global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L, ExpandOut O, const uint64_t* off,
+                                                         ChildArrays C, const uint64_t* list,
+                                                         const unsigned long long* n_list, uint64_t tag_base, Tables tb,
+                                                         const StoredLevel* stored, int32_t* err) {
+  extern __shared__ __align__(16) uint8_t vm_smem[];
+  const int32_t m = S.m;
+  int32_t* cnt = reinterpret_cast<int32_t*>(vm_smem);                 // [2][m]
+  FC* fc = reinterpret_cast<FC*>(vm_smem + (size_t)2 * m * 4);        // [2][m]
+  int32_t* nds = reinterpret_cast<int32_t*>(vm_smem + (size_t)2 * m * (4 + sizeof(FC)));  // [2][KMAX] neuron
+  uint8_t* ndx = reinterpret_cast<uint8_t*>(nds + 2 * KMAX);          // [2][KMAX] digit
+  __shared__ int sK[2];
+  __shared__ uint32_t sp[2];
+  const int tid = threadIdx.x;
+  const uint64_t nl = *n_list;
+  for (uint64_t i = blockIdx.x; i < nl; i += gridDim.x) {
+    const uint64_t c = list[i];
+    const uint8_t vd = C.verdict[c];
+    const int sides = vd == 1 ? 2 : 1;
+    if (tid < sides) {
+      // side 0: the child; side 1: its key's winner (same level)
+      const uint64_t cc = tid == 0 ? c : tb.ltab[C.cslot[c]].tag - tag_base;
+      const uint32_t p = C.cpar[cc];
+      const uint64_t* nd = O.nd + (uint64_t)p * KMAX;
+      const int K = O.ndc[p];
+      uint64_t t = cc - off[p];
+      for (int k = K - 1; k >= 0; --k) {  // mixed radix, first ND neuron most significant (reading A7)
+        const int32_t s = (int32_t)(nd[k] >> 32), v = (int32_t)(uint32_t)nd[k];
+        const uint64_t d = (uint64_t)count_applicable(S, s, v);
+        nds[tid * KMAX + k] = s;
+        ndx[tid * KMAX + k] = (uint8_t)(t % d);
+        t /= d;
+      }
+      sK[tid] = K;
+      sp[tid] = p;
+    }
+    __syncthreads();
+    for (int sd = 0; sd < sides; ++sd)
+      for (int32_t s = tid; s < m; s += VM_THREADS) {
+        const int32_t v = ld_count<T>(L.data, sp[sd], s, m);
+        cnt[sd * m + s] = v;
+        const int r = first_rule(S, s, v);
+        fc[sd * m + s] = r >= 0 ? fc_pack<FC>(S.rules[r].c, S.rules[r].p) : fc_pack<FC>(0, 0);
+      }
+    __syncthreads();
+    for (int sd = 0; sd < sides; ++sd)
+      for (int k = tid; k < sK[sd]; k += VM_THREADS) {
+        const int x = ndx[sd * KMAX + k];
+        if (!x) continue;
+        const int32_t s = nds[sd * KMAX + k];
+        const int r = nth_applicable(S, s, cnt[sd * m + s], x);
+        fc[sd * m + s] = fc_pack<FC>(S.rules[r].c, S.rules[r].p);
+      }
+    __syncthreads();
+    const uint64_t ref = vd == 1 ? 0 : C.cref[c];
+    bool diff = false;
+    for (int32_t j = tid; j < m; j += VM_THREADS) {
+      const int e0 = S.in_off[j], e1 = S.in_off[j + 1];
+      int64_t a = (int64_t)cnt[j] - fc_c(fc[j]);
+      for (int e = e0; e < e1; ++e) a += fc_p(fc[S.in_src[e]]);
+      int64_t b;
+      if (vd == 1) {
+        b = (int64_t)cnt[m + j] - fc_c(fc[m + j]);
+        for (int e = e0; e < e1; ++e) b += fc_p(fc[m + S.in_src[e]]);
+      } else {
+        b = ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, m);
+      }
+      diff |= a != b;
+    }
+    if (__syncthreads_or(diff) && tid == 0) atomicOr(err, ERR_COLLISION);
+  }
+}
+
 // dedup = 0: every fingerprint match is checked by comparing the two full
 // configurations (candidate computed exactly from (parent, t)).  A mismatch
 // is a 128-bit collision: reported, never merged (reading A18).
@@ -2750,14 +2844,14 @@ __device__ uint64_t tau_div(uint64_t F, uint64_t N) {
   return q;
 }
 
-using SmallScan = cub::BlockScan<uint64_t, 1024>;
-
-template <typename T>
-__global__ void __launch_bounds__(1024) k_small_bfs(SysView S, SmallArgs a) {
+// NT threads: 1024, or 128 for tiny frontiers (Π: cheaper barriers per level)
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) k_small_bfs(SysView S, SmallArgs a) {
+  using SmallScan = cub::BlockScan<uint64_t, NT>;
   __shared__ typename SmallScan::TempStorage scan_tmp;
   __shared__ unsigned long long sh_u64[4];  // [0] n_new, [1] n_halting, [2] digest
   __shared__ int32_t sh_err, sh_stop;
-  __shared__ uint64_t sh_T, sh_K, sh_tau, sh_part[1024];
+  __shared__ uint64_t sh_T, sh_K, sh_tau, sh_part[NT];
   __shared__ int sh_thin;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int32_t m = S.m;
@@ -3984,6 +4078,27 @@ void launch_verify_batch(const SysView& S, int32_t bytes, const LevelView& L, co
   count_launch(2);
 }
 
+// dedup = 0: the listed key matches, one CTA each (k_verify_m); false when the
+// per-CTA rows do not fit shared memory (the batched two-pass path instead)
+bool launch_verify_m(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
+                     const ChildArrays& C, const uint64_t* list, const unsigned long long* n_list, uint64_t tag_base,
+                     const Tables& tb, const StoredLevel* stored, int32_t* err, cudaStream_t st) {
+  const size_t sm = S.small_cp ? verify_m_smem_bytes<uint16_t>(S.m) : verify_m_smem_bytes<int2>(S.m);
+  if (sm > 200 * 1024 || S.delay_m > 0 || S.aug_rule >= 0) return false;
+  const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(8, (size_t)(220 * 1024) / (sm + 1024)));
+  dispatch_bytes(bytes, [&](auto tt) {
+    using TT = decltype(tt);
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<148u * per_sm, VM_THREADS, sm, st>>>(S, L, O, off, C, list, n_list, tag_base, tb, stored, err);
+    };
+    if (S.small_cp) go(k_verify_m<TT, uint16_t>);
+    else go(k_verify_m<TT, int2>);
+  });
+  count_launch();
+  return true;
+}
+
 void launch_verify(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
                    const ChildArrays& C, uint64_t T, uint64_t tag_base, const Tables& tb, const StoredLevel* stored,
                    uint64_t* list, unsigned long long* n_list, int32_t* err, cudaStream_t st) {
@@ -4046,7 +4161,10 @@ void launch_zero_tail(int32_t bytes, void* data, int64_t F, int32_t m, cudaStrea
 void launch_small_bfs(const SysView& S, int32_t bytes, const SmallArgs& a, cudaStream_t st) {
   dispatch_bytes(bytes, [&](auto tt) {
     using T = decltype(tt);
-    k_small_bfs<T><<<1, 1024, 0, st>>>(S, a);
+    const char* e = getenv("SNP_SMALL_NT");
+    const int nt = e ? atoi(e) : (a.F <= 32 ? 128 : 1024);
+    if (nt == 128) k_small_bfs<T, 128><<<1, 128, 0, st>>>(S, a);
+    else k_small_bfs<T, 1024><<<1, 1024, 0, st>>>(S, a);
   });
   count_launch();
 }

@@ -422,3 +422,23 @@ def test_wide_counts_narrow_kc(snp, monkeypatch, bits, cap):
         tree = snp.System(w, count_bits=bits, dedup=dedup, frontier_target=800).explore(L0, depth=3)
         ref = oracle.System.from_workload(w).explore(L0, depth=3, dedup=dedup, count_bits=bits, frontier_target=800)
         assert_same_tree(tree, ref)
+
+
+@pytest.mark.parametrize("batch", ["", "1"])
+def test_exact_dedup_verification(snp, monkeypatch, batch):
+    """dedup = 0 compares every key match as full configurations: both
+    verification paths (one CTA per match; SNP_VERIFY_BATCH=1 the batched
+    two-pass one) agree with the oracle on a config-3-shaped system, and with
+    6-bit child keys (SNP_KERNELS=fp_weak, tests only) distinct children
+    share keys and the verification reports a collision (reading A18)."""
+    monkeypatch.setenv("SNP_VERIFY_BATCH", batch)
+    monkeypatch.setenv("SNP_SMALL", "0")
+    w = W.random_system(1024, outdeg=8, k_nd=5, seed=123)
+    L0 = W.level0_counts(w, 700, 123)
+    tree = snp.System(w, count_bits=32, dedup=0, frontier_target=900).explore(L0, depth=3)
+    ref = oracle.System.from_workload(w).explore(L0, depth=3, dedup=0, count_bits=32, frontier_target=900)
+    assert_same_tree(tree, ref)
+    monkeypatch.setenv("SNP_KERNELS", "fp_weak")
+    with pytest.raises(snp.SnpError) as ei:
+        snp.System(w, count_bits=32, dedup=0, frontier_target=900).explore(L0, depth=3)
+    assert ei.value.status == snp.SNP_E_COLLISION
