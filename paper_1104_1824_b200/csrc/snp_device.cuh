@@ -124,6 +124,7 @@ struct SysView {
   int32_t tabw;              // compact table width (power of two >= every L + P)
   int32_t full8;             // count_bits == 8: tab_full has 256 entries per neuron
   int32_t max_indeg;
+  int64_t n_in;              // in-synapses (in_off[m])
   const NeuronMeta* meta;    // m
   const uint8_t* tab;        // m × tabw   (compact)
   const uint8_t* tab_full;   // m × 256    (count_bits == 8)

@@ -833,7 +833,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   SNP_TRY(upload(s, s->d_meta, meta));
   SNP_TRY(s->d_tab.ensure((size_t)m * tabw, false));
   SNP_TRY(s->d_ctab.ensure((size_t)m * tabw * s->bytes, false));
-  if (s->bytes == 1) SNP_TRY(s->d_tab_full.ensure((size_t)m * 256, false));
+  SNP_TRY(s->d_tab_full.ensure((size_t)m * 256, false));  // wide counts: host-side X|Y tables of the TC K-a
   SNP_TRY(s->d_ttab.ensure((size_t)m * (32 + 256), false));  // every width (K-c NARROW for 16/32-bit counts)
   if (s->bytes == 1) SNP_TRY(s->d_elut.ensure((size_t)m * 32, false));
   if (s->bytes == 1) SNP_TRY(s->d_hsg.ensure((size_t)m * 256, false));
@@ -842,6 +842,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.tabw = (int32_t)tabw;
   v.full8 = s->bytes == 1 ? 1 : 0;
   v.max_indeg = max_indeg;
+  v.n_in = in_off[m];
   v.meta = s->d_meta.as<NeuronMeta>();
   v.tab = s->d_tab.as<uint8_t>();
   v.tab_full = s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr;
@@ -888,8 +889,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   SNP_TRY(s->counters_dev.ensure(sizeof(DevCounters), false));
   CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   s->own_stream = true;
-  launch_build_tables(v, s->bytes, s->d_tab.as<uint8_t>(), s->d_ctab.p,
-                      s->bytes == 1 ? s->d_tab_full.as<uint8_t>() : nullptr,
+  launch_build_tables(v, s->bytes, s->d_tab.as<uint8_t>(), s->d_ctab.p, s->d_tab_full.as<uint8_t>(),
                       s->d_ttab.as<uint8_t>(),
                       s->bytes == 1 ? s->d_elut.as<uint8_t>() : nullptr,
                       s->bytes == 1 ? s->d_hsg.as<uint8_t>() : nullptr, s->stream);
@@ -904,9 +904,21 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.n_nd = 0;
   // the s32 TMEM accumulators of k_expand_tc hold at most m·15·255 (X part)
   // and m·16·255 (Y' part): exact below 2^31 for m <= TC_M_MAX = 2^19
-  if (s->bytes == 1 && !v.any_generic && s->binary_emit && m <= TC_M_MAX) {
-    std::vector<uint8_t> tf((size_t)m * 256);
+  // 16/32-bit counts (NARROW: low bytes, exact lookups for counts >= 256)
+  // when every rule has c <= 15, p <= 1; ND-capable neurons then from the
+  // folded table, which covers every count
+  bool wide_ok = s->bytes == 1;
+  if (s->bytes > 1) {
+    wide_ok = true;
+    for (int64_t r = 0; r < n; ++r) wide_ok &= rules[r].consumed <= 15 && rules[r].produced <= 1;
+  }
+  if (wide_ok && !v.any_generic && s->binary_emit && m <= TC_M_MAX) {
+    std::vector<uint8_t> tf((size_t)m * 256), tw;
     CUDA_TRY(cudaMemcpy(tf.data(), s->d_tab_full.p, tf.size(), cudaMemcpyDeviceToHost));
+    if (s->bytes > 1) {
+      tw.resize((size_t)m * tabw);
+      CUDA_TRY(cudaMemcpy(tw.data(), s->d_tab.p, tw.size(), cudaMemcpyDeviceToHost));
+    }
     bool ok = true;
     std::vector<uint8_t> xyf((size_t)m * 256, 0), xyt((size_t)((m + 63) / 64) * 64 * 32, 0);  // whole chunks
     std::vector<int32_t> ndl;
@@ -921,6 +933,8 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
         if (R.consumed > 15 || R.produced > 1) { ok = false; break; }
         xyf[(size_t)j * 256 + c] = (uint8_t)(R.consumed | (R.produced << 4));
       }
+      if (s->bytes > 1)
+        for (int64_t c = 0; c < tabw; ++c) nd |= (tw[(size_t)j * tabw + c] & TE_ND) != 0;
       if (nd) ndl.push_back((int32_t)j);
       std::copy(xyf.begin() + j * 256, xyf.begin() + j * 256 + 32, xyt.begin() + j * 32);
     }

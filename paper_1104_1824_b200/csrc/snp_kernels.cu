@@ -63,6 +63,8 @@ __device__ __forceinline__ int nth_applicable(const SysView& S, int32_t s, int32
 
 // A child described virtually by its parent's nondeterministic neurons and
 // the mixed-radix digits of t (least significant digit = last ND neuron).
+__device__ __forceinline__ int first_rule(const SysView& S, int32_t s, int32_t v);
+
 struct ChildCtx {
   int K;
   int32_t s[KMAX];
@@ -836,6 +838,9 @@ constexpr int TC_STAGES = 2;                     // X|Y tiles: double-buffered
 #ifndef SNP_TC_MINB
 #define SNP_TC_MINB 4  // K-a: resident CTAs the register budget is sized for (56 registers, 4 CTAs/SM; 1 = 72 registers, 3 CTAs: 24.3 vs 19.2 ms)
 #endif
+#ifndef SNP_TC_AHEAD
+#define SNP_TC_AHEAD 1  // K-a: chunks whose counts are loaded ahead (registers; 2 = two sets in flight)
+#endif
 #ifndef SNP_TC_WS
 #define SNP_TC_WS 1  // producer warp for copies + MMAs (else thread 0 issues them after a CTA barrier)
 #endif
@@ -857,7 +862,9 @@ __device__ __forceinline__ uint32_t lut16(uint32_t v4, const uint32_t (&tt)[8]) 
 
 // WS: a ninth (producer) warp issues the bulk copies and the MMAs; the 256
 // compute threads only arrive on a per-stage mbarrier (no CTA barrier per chunk)
-template <bool WS>
+// T: count storage; 16/32-bit counts are packed to their low bytes on load
+// (NARROW), a warp with a count >= 256 takes the exact per-count rule lookup
+template <bool WS, typename T = uint8_t>
 __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, LevelView L, ExpandOut O) {
   extern __shared__ __align__(128) uint8_t smem_tc[];
   uint8_t* smem = smem_tc;
@@ -908,14 +915,40 @@ __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, 
 
   // the 32 counts of neuron c·64 + k (block h, half q) of chunk c, loaded
   // one chunk ahead
+  uint32_t wbigm = 0;  // NARROW: bit (c & 1) = a count of chunk c's 32 is >= 256
   auto load = [&](int c, uint32_t (&w)[8]) {
     const int32_t s = c * TCK + k;
+    bool wbig = false;
     if (c < nch && bvalid && s < m) {
-      ldg256(data + ((blk * m + s) << 6) + 32 * q, w);
+      if constexpr (sizeof(T) == 1) {
+        ldg256(data + ((blk * m + s) << 6) + 32 * q, w);
+      } else {
+        const uint8_t* src = data + (((blk * m + s) << 6) + 32 * q) * (int64_t)sizeof(T);
+        uint32_t u[8];
+#pragma unroll
+        for (int h = 0; h < (int)sizeof(T); ++h) {
+          ldg256(src + 32 * h, u);
+          if constexpr (sizeof(T) == 2) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              w[4 * h + i] = prmt(u[2 * i], u[2 * i + 1], 0x6420u);
+              wbig |= ((u[2 * i] | u[2 * i + 1]) & 0xFF00FF00u) != 0;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              w[2 * h + i] = prmt(prmt(u[4 * i], u[4 * i + 1], 0x0040u), prmt(u[4 * i + 2], u[4 * i + 3], 0x0040u),
+                                  0x5410u);
+              wbig |= ((u[4 * i] | u[4 * i + 1] | u[4 * i + 2] | u[4 * i + 3]) & 0xFFFFFF00u) != 0;
+            }
+          }
+        }
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) w[i] = 0;  // count 0 -> entry 0 (nothing fires: padded neurons have zero tables)
     }
+    wbigm = (wbigm & ~(1u << (c & 1))) | ((wbig ? 1u : 0u) << (c & 1));
   };
   auto chunk = [&](int c, uint32_t (&w)[8]) {
     const int st = c & 1;
@@ -950,7 +983,20 @@ __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, 
         const uint4 t1 = reinterpret_cast<const uint4*>(sT + k * 32)[1];
         tt[4] = t1.x; tt[5] = t1.y; tt[6] = t1.z; tt[7] = t1.w;
       }
-      if (small) {
+      if (sizeof(T) > 1 && __any_sync(0xFFFFFFFFu, (wbigm >> (c & 1)) & 1u)) {
+        // NARROW, rare: the entries (c | p << 4) of the first applicable rule
+        // from the exact count (tables over the folded domain)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          uint32_t x = 0;
+          if (bvalid && s < m)
+            for (int b = 0; b < 4; ++b) {
+              const int r = first_rule(S, s, ld_count<T>(L.data, blk * PB + 32 * q + 4 * i + b, s, m));
+              if (r >= 0) x |= (uint32_t)(S.rules[r].c | (S.rules[r].p << 4)) << (8 * b);
+            }
+          e[i] = x;
+        }
+      } else if (small) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) e[i] = lut16(w[i], tt);
       } else if ((hiv & 0xE0E0E0E0u) == 0) {
@@ -971,7 +1017,7 @@ __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, 
         }
       }
     }
-    load(c + 1, w);
+    load(c + SNP_TC_AHEAD, w);
     uint32_t X[8], Y[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -1064,8 +1110,18 @@ __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, 
     }
   } else {
     uint32_t w[8];
-    load(0, w);
-    for (int c = 0; c < nch; ++c) chunk(c, w);
+    if (SNP_TC_AHEAD == 1) {
+      load(0, w);
+      for (int c = 0; c < nch; ++c) chunk(c, w);
+    } else {  // two register sets: the counts of chunks c + 1 and c + 2 in flight
+      uint32_t w2[8];
+      load(0, w);
+      load(1, w2);
+      for (int c = 0; c < nch; c += 2) {
+        chunk(c, w);
+        if (c + 1 < nch) chunk(c + 1, w2);
+      }
+    }
   }
   const int cl = nch - 1;
   tc::bar_wait(&bar[cl & 1], (uint32_t)((cl >> 1) & 1));
@@ -1101,16 +1157,18 @@ __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, 
 // Ψ (eq. (8), readings A3/A5) and the ND lists for k_expand_tc:
 // only neurons in S.nd_list can have d_s >= 2; visited in increasing order so
 // the list is in total order (reading A7).
+template <typename T>
 __global__ void k_nd_pass(SysView S, LevelView L, ExpandOut O) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= L.F) return;
-  const uint8_t* data = reinterpret_cast<const uint8_t*>(L.data);
   int ndc = 0;
   uint64_t psi = 1;
   for (int i = 0; i < S.n_nd; ++i) {
     const int32_t s = __ldg(S.nd_list + i);
-    const uint32_t v = data[eidx(p, s, S.m)];
-    if (__ldg(S.tab_full + (int64_t)s * 256 + v) & TE_ND) nd_event(S, O, s, v, p, ndc, psi);
+    const uint32_t v = (uint32_t)ld_count<T>(L.data, p, s, S.m);
+    const uint8_t e = sizeof(T) == 1 ? __ldg(S.tab_full + (int64_t)s * 256 + v)
+                                     : __ldg(S.tab + (int64_t)s * S.tabw + table_index(v, S.meta[s]));
+    if (e & TE_ND) nd_event(S, O, s, v, p, ndc, psi);
   }
   if (O.halting[p]) psi = 0;  // halting: no children (reading A5)
   O.psi[p] = psi;
@@ -2596,34 +2654,37 @@ __global__ void k_verify_cols(SysView S, LevelView L, ChildArrays C, const uint6
 // dedup = 0, one CTA per listed key match (grid-stride): both children's
 // parent counts and fired (c, p) of every neuron into shared memory (the
 // counts come from the block layout, one sector each: the floor of this
-// pass), the ND digits decoded once, then a thread per column rebuilds eq.
-// (2) for both and compares (or against the stored configuration of an
-// earlier level).  A mismatch is a 128-bit collision (reading A18).
+// pass), the ND digits decoded once, then a thread per column compares eq.
+// (2) for both — as the difference (C_a - c_a) - (C_b - c_b) + Σ_in (p_a - p_b),
+// one shared-memory word per in-synapse — or against the stored configuration
+// of an earlier level.  SIN: the in-CSR (uint16 sources) staged in shared
+// memory once per CTA.  A mismatch is a 128-bit collision (reading A18).
 constexpr int VM_THREADS = 256;
-template <typename FC>
-size_t verify_m_smem_bytes(int32_t m) { return (size_t)2 * m * (4 + sizeof(FC)) + 2 * KMAX * 8 + 64; }
+size_t verify_m_smem_bytes(int32_t m, int64_t n_in, bool sin) {
+  return (size_t)m * (4 + 4 + 16) + 2 * KMAX * 8 + 64 + (sin ? (size_t)(m + 1) * 4 + (size_t)n_in * 2 + 16 : 0);
+}
 
-template <typename FC>
-__device__ __forceinline__ FC fc_pack(int32_t c, int32_t p);
-template <>
-__device__ __forceinline__ uint16_t fc_pack<uint16_t>(int32_t c, int32_t p) { return (uint16_t)(c | (p << 8)); }
-template <>
-__device__ __forceinline__ int2 fc_pack<int2>(int32_t c, int32_t p) { return make_int2(c, p); }
-
-template <typename T, typename FC>
+template <typename T, bool SIN>
 __global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L, ExpandOut O, const uint64_t* off,
                                                          ChildArrays C, const uint64_t* list,
                                                          const unsigned long long* n_list, uint64_t tag_base, Tables tb,
                                                          const StoredLevel* stored, int32_t* err) {
   extern __shared__ __align__(16) uint8_t vm_smem[];
   const int32_t m = S.m;
-  int32_t* cnt = reinterpret_cast<int32_t*>(vm_smem);                 // [2][m]
-  FC* fc = reinterpret_cast<FC*>(vm_smem + (size_t)2 * m * 4);        // [2][m]
-  int32_t* nds = reinterpret_cast<int32_t*>(vm_smem + (size_t)2 * m * (4 + sizeof(FC)));  // [2][KMAX] neuron
+  int4* fc = reinterpret_cast<int4*>(vm_smem);                        // [m] (c_a, p_a, c_b, p_b)
+  int32_t* cnt = reinterpret_cast<int32_t*>(fc + m);                   // [2][m]
+  int32_t* nds = cnt + 2 * m;                                          // [2][KMAX] neuron
   uint8_t* ndx = reinterpret_cast<uint8_t*>(nds + 2 * KMAX);          // [2][KMAX] digit
+  int32_t* ioff = reinterpret_cast<int32_t*>(ndx + 2 * KMAX + 16);    // SIN: [m + 1]
+  uint16_t* isrc = reinterpret_cast<uint16_t*>(ioff + m + 1);         // SIN: [in_off[m]]
   __shared__ int sK[2];
   __shared__ uint32_t sp[2];
   const int tid = threadIdx.x;
+  if (SIN) {
+    for (int32_t j = tid; j <= m; j += VM_THREADS) ioff[j] = S.in_off[j];
+    const int32_t ne = S.in_off[m];
+    for (int32_t e = tid; e < ne; e += VM_THREADS) isrc[e] = (uint16_t)S.in_src[e];
+  }
   const uint64_t nl = *n_list;
   for (uint64_t i = blockIdx.x; i < nl; i += gridDim.x) {
     const uint64_t c = list[i];
@@ -2647,13 +2708,20 @@ __global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L,
       sp[tid] = p;
     }
     __syncthreads();
-    for (int sd = 0; sd < sides; ++sd)
-      for (int32_t s = tid; s < m; s += VM_THREADS) {
-        const int32_t v = ld_count<T>(L.data, sp[sd], s, m);
-        cnt[sd * m + s] = v;
-        const int r = first_rule(S, s, v);
-        fc[sd * m + s] = r >= 0 ? fc_pack<FC>(S.rules[r].c, S.rules[r].p) : fc_pack<FC>(0, 0);
+    for (int32_t s = tid; s < m; s += VM_THREADS) {
+      int4 f = make_int4(0, 0, 0, 0);
+      const int32_t va = ld_count<T>(L.data, sp[0], s, m);
+      cnt[s] = va;
+      int r = first_rule(S, s, va);
+      if (r >= 0) { f.x = S.rules[r].c; f.y = S.rules[r].p; }
+      if (sides == 2) {
+        const int32_t vb = ld_count<T>(L.data, sp[1], s, m);
+        cnt[m + s] = vb;
+        r = first_rule(S, s, vb);
+        if (r >= 0) { f.z = S.rules[r].c; f.w = S.rules[r].p; }
       }
+      fc[s] = f;
+    }
     __syncthreads();
     for (int sd = 0; sd < sides; ++sd)
       for (int k = tid; k < sK[sd]; k += VM_THREADS) {
@@ -2661,23 +2729,27 @@ __global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L,
         if (!x) continue;
         const int32_t s = nds[sd * KMAX + k];
         const int r = nth_applicable(S, s, cnt[sd * m + s], x);
-        fc[sd * m + s] = fc_pack<FC>(S.rules[r].c, S.rules[r].p);
+        if (sd == 0) { fc[s].x = S.rules[r].c; fc[s].y = S.rules[r].p; }
+        else { fc[s].z = S.rules[r].c; fc[s].w = S.rules[r].p; }
       }
     __syncthreads();
     const uint64_t ref = vd == 1 ? 0 : C.cref[c];
     bool diff = false;
     for (int32_t j = tid; j < m; j += VM_THREADS) {
-      const int e0 = S.in_off[j], e1 = S.in_off[j + 1];
-      int64_t a = (int64_t)cnt[j] - fc_c(fc[j]);
-      for (int e = e0; e < e1; ++e) a += fc_p(fc[S.in_src[e]]);
-      int64_t b;
+      const int e0 = SIN ? ioff[j] : S.in_off[j], e1 = SIN ? ioff[j + 1] : S.in_off[j + 1];
+      const int4 fj = fc[j];
       if (vd == 1) {
-        b = (int64_t)cnt[m + j] - fc_c(fc[m + j]);
-        for (int e = e0; e < e1; ++e) b += fc_p(fc[m + S.in_src[e]]);
+        int64_t d = ((int64_t)cnt[j] - fj.x) - ((int64_t)cnt[m + j] - fj.z);
+        for (int e = e0; e < e1; ++e) {
+          const int4 fs = fc[SIN ? (int32_t)isrc[e] : S.in_src[e]];
+          d += fs.y - fs.w;
+        }
+        diff |= d != 0;
       } else {
-        b = ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, m);
+        int64_t a = (int64_t)cnt[j] - fj.x;
+        for (int e = e0; e < e1; ++e) a += fc[SIN ? (int32_t)isrc[e] : S.in_src[e]].y;
+        diff |= a != ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, m);
       }
-      diff |= a != b;
     }
     if (__syncthreads_or(diff) && tid == 0) atomicOr(err, ERR_COLLISION);
   }
@@ -3854,15 +3926,15 @@ void launch_expand(const SysView& S, int32_t bytes, const LevelView& L, const Ex
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<expand_grid(L.F), XW * 32, smem, st>>>(S, L, O);
       };
-      if (full && S.tc_ok && !(S.kernel_flags & (KF_EXPAND_T | KF_NO_TC))) {
+      if ((full || sizeof(T) > 1) && S.tc_ok && !(S.kernel_flags & (KF_EXPAND_T | KF_NO_TC))) {
         const size_t sm = expand_tc_smem_bytes();
-        auto kern = SNP_TC_WS ? k_expand_tc<true> : k_expand_tc<false>;
+        auto kern = SNP_TC_WS ? k_expand_tc<true, T> : k_expand_tc<false, T>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (SNP_TC_MINB > 3) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         const int64_t nblk = (L.F + PB - 1) / PB;
         kern<<<(unsigned)((nblk + 1) / 2), TCT + (SNP_TC_WS ? 32 : 0), sm, st>>>(S, L, O);
         if (!O.classify_only) {
-          k_nd_pass<<<grid_for(L.F), BLK, 0, st>>>(S, L, O);
+          k_nd_pass<T><<<grid_for(L.F), BLK, 0, st>>>(S, L, O);
           count_launch();
         }
       } else if (full && S.any_generic == 0 && S.hsg != nullptr && !(S.kernel_flags & KF_EXPAND_T)) {
@@ -4083,8 +4155,10 @@ void launch_verify_batch(const SysView& S, int32_t bytes, const LevelView& L, co
 bool launch_verify_m(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
                      const ChildArrays& C, const uint64_t* list, const unsigned long long* n_list, uint64_t tag_base,
                      const Tables& tb, const StoredLevel* stored, int32_t* err, cudaStream_t st) {
-  const size_t sm = S.small_cp ? verify_m_smem_bytes<uint16_t>(S.m) : verify_m_smem_bytes<int2>(S.m);
-  if (sm > 200 * 1024 || S.delay_m > 0 || S.aug_rule >= 0) return false;
+  if (S.delay_m > 0 || S.aug_rule >= 0) return false;
+  const bool sin = S.m < 65536 && verify_m_smem_bytes(S.m, S.n_in, true) <= 64 * 1024;
+  const size_t sm = verify_m_smem_bytes(S.m, S.n_in, sin);
+  if (sm > 200 * 1024) return false;
   const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(8, (size_t)(220 * 1024) / (sm + 1024)));
   dispatch_bytes(bytes, [&](auto tt) {
     using TT = decltype(tt);
@@ -4092,8 +4166,8 @@ bool launch_verify_m(const SysView& S, int32_t bytes, const LevelView& L, const 
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       kern<<<148u * per_sm, VM_THREADS, sm, st>>>(S, L, O, off, C, list, n_list, tag_base, tb, stored, err);
     };
-    if (S.small_cp) go(k_verify_m<TT, uint16_t>);
-    else go(k_verify_m<TT, int2>);
+    if (sin) go(k_verify_m<TT, true>);
+    else go(k_verify_m<TT, false>);
   });
   count_launch();
   return true;

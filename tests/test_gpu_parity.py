@@ -168,14 +168,17 @@ def test_tc_expand_selected_and_equal(snp, monkeypatch, kernels):
     want = 0 if kernels else snp.SNP_PATH_TC_EXPAND
     w = W.random_system(1000, outdeg=8, k_nd=6, seed=5)
     L0 = W.level0_counts(w, 1100, 5)
-    eng = snp.System(w, count_bits=8, dedup=1, frontier_target=1000)
-    assert eng.kernel_paths == want
-    tree = eng.explore(L0, depth=4)
-    ref = oracle.System.from_workload(w).explore(L0, depth=4, dedup=1, count_bits=8, frontier_target=1000)
-    assert_same_tree(tree, ref)
+    L0[3::11] += 300  # 16/32-bit storage: counts >= 256 (the exact per-count lookups of the NARROW K-a)
+    for bits in (8, 16, 32):
+        L = L0 if bits > 8 else W.level0_counts(w, 1100, 5)
+        eng = snp.System(w, count_bits=bits, dedup=1, frontier_target=1000)
+        assert eng.kernel_paths == want
+        tree = eng.explore(L, depth=4)
+        ref = oracle.System.from_workload(w).explore(L, depth=4, dedup=1, count_bits=bits, frontier_target=1000)
+        assert_same_tree(tree, ref)
     pi = W.pi_system("simulator")
     assert snp.System(pi, count_bits=8, dedup=0).kernel_paths == want
-    assert snp.System(pi, count_bits=32, dedup=0).kernel_paths == 0  # int32 storage: CUDA-core K-a
+    assert snp.System(pi, count_bits=32, dedup=0).kernel_paths == want  # int32 storage: the NARROW TC K-a
 
 
 def test_tc_expand_declined_when_not_applicable(snp):

@@ -47,6 +47,7 @@ def main():
                               "transitions": int(tree.counters.T.sum()), "engine_ms": 1e3 * te,
                               "engine_first_run_ms": 1e3 * tf, "abi_snp_explore_ms": 1e3 * ta,
                               "oracle_ms": 1e3 * to, "levels": int(tree.num_levels),
+                              "level_kernels_ms": float(tree.counters.ms.sum()),
                               "equal_to_oracle": same, "kernel_launches_total": launches}))
 
 
