@@ -235,6 +235,7 @@ struct snp_system {
   // the next snp_begin: the levels they hold are views into them)
   DBuf small_scratch, small_out, small_stored;
   std::vector<DBuf> small_pools;
+  std::vector<DBuf> small_spare;  // pools of an earlier exploration, reused (no cudaMalloc per explore)
   size_t small_skip = (size_t)-1;  // levels.size() at which a level had > SMALL_T transitions
   // multi-GPU exploration (snp_dist_*): this rank's share of the frontier and
   // of the visited keys (owner = fmix64(fp1) mod P)
@@ -993,6 +994,8 @@ snp_status reset_state(snp_system* s) {
   s->ev_used = 0;
   s->levels.clear();  // pooled level buffers are non-owning: the pool is reused from the start
   s->lpool_used = 0;
+  for (auto& pl : s->small_pools)
+    if (s->small_spare.size() < 8) s->small_spare.push_back(std::move(pl));
   s->small_pools.clear();
   s->small_skip = (size_t)-1;
   s->arena.reset();
@@ -1473,6 +1476,12 @@ snp_status advance_small(snp_system* s, int32_t want, int32_t* done) {
   a.kpos = reinterpret_cast<uint64_t*>(take((SMALL_T + 1) * 8));
   // pool of the new levels
   DBuf pool;
+  for (size_t i = 0; i < s->small_spare.size(); ++i)
+    if (s->small_spare[i].bytes >= per * (size_t)L) {
+      pool = std::move(s->small_spare[i]);
+      s->small_spare.erase(s->small_spare.begin() + (long)i);
+      break;
+    }
   SNP_TRY(pool.ensure(per * (size_t)L, false));
   uint8_t* pp = pool.as<uint8_t>();
   a.data_pool = pp;

@@ -2654,37 +2654,44 @@ __global__ void k_verify_cols(SysView S, LevelView L, ChildArrays C, const uint6
 // dedup = 0, one CTA per listed key match (grid-stride): both children's
 // parent counts and fired (c, p) of every neuron into shared memory (the
 // counts come from the block layout, one sector each: the floor of this
-// pass), the ND digits decoded once, then a thread per column compares eq.
-// (2) for both — as the difference (C_a - c_a) - (C_b - c_b) + Σ_in (p_a - p_b),
-// one shared-memory word per in-synapse — or against the stored configuration
-// of an earlier level.  SIN: the in-CSR (uint16 sources) staged in shared
-// memory once per CTA.  A mismatch is a 128-bit collision (reading A18).
+// pass), the ND digits decoded once, then a warp per 32 columns compares eq.
+// (2) for both — as the difference (C_a - c_a) - (C_b - c_b) + Σ_in (p_a - p_b)
+// — or against the stored configuration of an earlier level.  The in-synapse
+// walk uses K-c's padded, bank-coloured in-CSR rows (one coalesced index load
+// per row, padding reads a zero entry).  PK: every rule has c, p <= 255, so a
+// neuron's (c_a, p_a, c_b, p_b) is one 32-bit word.  A mismatch is a 128-bit
+// collision (reading A18).
 constexpr int VM_THREADS = 256;
-size_t verify_m_smem_bytes(int32_t m, int64_t n_in, bool sin) {
-  return (size_t)m * (4 + 4 + 16) + 2 * KMAX * 8 + 64 + (sin ? (size_t)(m + 1) * 4 + (size_t)n_in * 2 + 16 : 0);
+size_t verify_m_smem_bytes(int32_t m, bool pk) {
+  const size_t mE = (size_t)((m + 1) & ~1) + 2;
+  return mE * (pk ? 4 : 16) + (size_t)m * 8 + 2 * KMAX * 8 + 64;
 }
 
-template <typename T, bool SIN>
+template <typename T, bool PK>
 __global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L, ExpandOut O, const uint64_t* off,
                                                          ChildArrays C, const uint64_t* list,
                                                          const unsigned long long* n_list, uint64_t tag_base, Tables tb,
                                                          const StoredLevel* stored, int32_t* err) {
+  using FW = typename std::conditional<PK, uint32_t, int4>::type;
   extern __shared__ __align__(16) uint8_t vm_smem[];
   const int32_t m = S.m;
-  int4* fc = reinterpret_cast<int4*>(vm_smem);                        // [m] (c_a, p_a, c_b, p_b)
-  int32_t* cnt = reinterpret_cast<int32_t*>(fc + m);                   // [2][m]
+  const int32_t mE = (m + 1) & ~1;
+  FW* fc = reinterpret_cast<FW*>(vm_smem);                            // [mE + 2] (c_a, p_a, c_b, p_b); zero pads
+  int32_t* cnt = reinterpret_cast<int32_t*>(fc + mE + 2);             // [2][m]
   int32_t* nds = cnt + 2 * m;                                          // [2][KMAX] neuron
   uint8_t* ndx = reinterpret_cast<uint8_t*>(nds + 2 * KMAX);          // [2][KMAX] digit
-  int32_t* ioff = reinterpret_cast<int32_t*>(ndx + 2 * KMAX + 16);    // SIN: [m + 1]
-  uint16_t* isrc = reinterpret_cast<uint16_t*>(ioff + m + 1);         // SIN: [in_off[m]]
   __shared__ int sK[2];
   __shared__ uint32_t sp[2];
-  const int tid = threadIdx.x;
-  if (SIN) {
-    for (int32_t j = tid; j <= m; j += VM_THREADS) ioff[j] = S.in_off[j];
-    const int32_t ne = S.in_off[m];
-    for (int32_t e = tid; e < ne; e += VM_THREADS) isrc[e] = (uint16_t)S.in_src[e];
-  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto mk = [](int ca, int pa, int cb, int pb) -> FW {
+    if constexpr (PK) return (uint32_t)ca | ((uint32_t)pa << 8) | ((uint32_t)cb << 16) | ((uint32_t)pb << 24);
+    else return make_int4(ca, pa, cb, pb);
+  };
+  auto ca_ = [](FW f) -> int32_t { if constexpr (PK) return (int32_t)(f & 0xFF); else return f.x; };
+  auto pa_ = [](FW f) -> int32_t { if constexpr (PK) return (int32_t)((f >> 8) & 0xFF); else return f.y; };
+  auto cb_ = [](FW f) -> int32_t { if constexpr (PK) return (int32_t)((f >> 16) & 0xFF); else return f.z; };
+  auto pb_ = [](FW f) -> int32_t { if constexpr (PK) return (int32_t)(f >> 24); else return f.w; };
+  if (tid < mE + 2 - m) fc[m + tid] = mk(0, 0, 0, 0);  // targets of padded in-synapses
   const uint64_t nl = *n_list;
   for (uint64_t i = blockIdx.x; i < nl; i += gridDim.x) {
     const uint64_t c = list[i];
@@ -2709,46 +2716,51 @@ __global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L,
     }
     __syncthreads();
     for (int32_t s = tid; s < m; s += VM_THREADS) {
-      int4 f = make_int4(0, 0, 0, 0);
+      int ca = 0, pa = 0, cb = 0, pb = 0;
       const int32_t va = ld_count<T>(L.data, sp[0], s, m);
       cnt[s] = va;
       int r = first_rule(S, s, va);
-      if (r >= 0) { f.x = S.rules[r].c; f.y = S.rules[r].p; }
+      if (r >= 0) { ca = S.rules[r].c; pa = S.rules[r].p; }
       if (sides == 2) {
         const int32_t vb = ld_count<T>(L.data, sp[1], s, m);
         cnt[m + s] = vb;
         r = first_rule(S, s, vb);
-        if (r >= 0) { f.z = S.rules[r].c; f.w = S.rules[r].p; }
+        if (r >= 0) { cb = S.rules[r].c; pb = S.rules[r].p; }
       }
-      fc[s] = f;
+      fc[s] = mk(ca, pa, cb, pb);
     }
     __syncthreads();
-    for (int sd = 0; sd < sides; ++sd)
-      for (int k = tid; k < sK[sd]; k += VM_THREADS) {
-        const int x = ndx[sd * KMAX + k];
-        if (!x) continue;
-        const int32_t s = nds[sd * KMAX + k];
-        const int r = nth_applicable(S, s, cnt[sd * m + s], x);
-        if (sd == 0) { fc[s].x = S.rules[r].c; fc[s].y = S.rules[r].p; }
-        else { fc[s].z = S.rules[r].c; fc[s].w = S.rules[r].p; }
+    for (int sd = 0; sd < sides; ++sd) {  // ND digits != 0 (a neuron appears once per side)
+      if (tid < sK[sd] && ndx[sd * KMAX + tid]) {
+        const int32_t s = nds[sd * KMAX + tid];
+        const int r = nth_applicable(S, s, cnt[sd * m + s], ndx[sd * KMAX + tid]);
+        const FW f = fc[s];
+        fc[s] = sd == 0 ? mk(S.rules[r].c, S.rules[r].p, cb_(f), pb_(f)) : mk(ca_(f), pa_(f), S.rules[r].c, S.rules[r].p);
       }
-    __syncthreads();
+      __syncthreads();
+    }
     const uint64_t ref = vd == 1 ? 0 : C.cref[c];
     bool diff = false;
-    for (int32_t j = tid; j < m; j += VM_THREADS) {
-      const int e0 = SIN ? ioff[j] : S.in_off[j], e1 = SIN ? ioff[j + 1] : S.in_off[j + 1];
-      const int4 fj = fc[j];
+    for (int32_t j0 = warp * 32; j0 < m; j0 += VM_THREADS) {
+      const int32_t j = j0 + lane;
+      const int64_t g = j0 >> 5;
+      const int64_t r0 = __ldg(S.in_pad_off + g), r1 = __ldg(S.in_pad_off + g + 1);
+      const FW fj = fc[j < m ? j : m];
       if (vd == 1) {
-        int64_t d = ((int64_t)cnt[j] - fj.x) - ((int64_t)cnt[m + j] - fj.z);
-        for (int e = e0; e < e1; ++e) {
-          const int4 fs = fc[SIN ? (int32_t)isrc[e] : S.in_src[e]];
-          d += fs.y - fs.w;
+        int64_t d = j < m ? ((int64_t)cnt[j] - ca_(fj)) - ((int64_t)cnt[m + j] - cb_(fj)) : 0;
+        for (int64_t r = r0; r < r1; ++r) {
+          const int32_t src = S.in_pad16 ? (int32_t)__ldg(S.in_pad16 + r * 32 + lane) : __ldg(S.in_pad + r * 32 + lane);
+          const FW f = fc[src];
+          d += pa_(f) - pb_(f);
         }
         diff |= d != 0;
       } else {
-        int64_t a = (int64_t)cnt[j] - fj.x;
-        for (int e = e0; e < e1; ++e) a += fc[SIN ? (int32_t)isrc[e] : S.in_src[e]].y;
-        diff |= a != ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, m);
+        int64_t a = j < m ? (int64_t)cnt[j] - ca_(fj) : 0;
+        for (int64_t r = r0; r < r1; ++r) {
+          const int32_t src = S.in_pad16 ? (int32_t)__ldg(S.in_pad16 + r * 32 + lane) : __ldg(S.in_pad + r * 32 + lane);
+          a += pa_(fc[src]);
+        }
+        if (j < m) diff |= a != ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, m);
       }
     }
     if (__syncthreads_or(diff) && tid == 0) atomicOr(err, ERR_COLLISION);
@@ -4155,9 +4167,9 @@ void launch_verify_batch(const SysView& S, int32_t bytes, const LevelView& L, co
 bool launch_verify_m(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O, const uint64_t* off,
                      const ChildArrays& C, const uint64_t* list, const unsigned long long* n_list, uint64_t tag_base,
                      const Tables& tb, const StoredLevel* stored, int32_t* err, cudaStream_t st) {
-  if (S.delay_m > 0 || S.aug_rule >= 0) return false;
-  const bool sin = S.m < 65536 && verify_m_smem_bytes(S.m, S.n_in, true) <= 64 * 1024;
-  const size_t sm = verify_m_smem_bytes(S.m, S.n_in, sin);
+  if (S.delay_m > 0 || S.aug_rule >= 0 || KMAX > VM_THREADS) return false;
+  const bool pk = S.small_cp != 0;
+  const size_t sm = verify_m_smem_bytes(S.m, pk);
   if (sm > 200 * 1024) return false;
   const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(8, (size_t)(220 * 1024) / (sm + 1024)));
   dispatch_bytes(bytes, [&](auto tt) {
@@ -4166,7 +4178,7 @@ bool launch_verify_m(const SysView& S, int32_t bytes, const LevelView& L, const 
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       kern<<<148u * per_sm, VM_THREADS, sm, st>>>(S, L, O, off, C, list, n_list, tag_base, tb, stored, err);
     };
-    if (sin) go(k_verify_m<TT, true>);
+    if (pk) go(k_verify_m<TT, true>);
     else go(k_verify_m<TT, false>);
   });
   count_launch();

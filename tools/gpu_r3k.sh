@@ -1,0 +1,13 @@
+#!/bin/bash
+# verification v2 (config 3), K-a load-ahead A/B (config 4), Π
+O=gpurun_out/r3k; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { tail -20 $O/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "exact_dedup or random_system_parity or wide_counts" > $O/pytest.log 2>&1; tail -2 $O/pytest.log
+timeout 600 python bench.py --config 3 --steps 6 --warmup 2 --no-e2e --no-cpu > $O/bench_c3.log 2>&1
+python - <<'PY'
+import json
+d=[json.loads(l) for l in open('gpurun_out/r3k/bench_c3.log') if l.startswith('{')][-1]
+print('config3', d['value'], d['ms_per_step'], d['phase_ms_per_step'], d['digest'])
+PY
+AB_STEPS=8 bash tools/gpu_ab.sh r3k_c4 "X=1" "X=2|SNP_TC_AHEAD=2"
+python tools/bench_pi.py > $O/pi.jsonl 2>&1; cut -c1-330 $O/pi.jsonl
