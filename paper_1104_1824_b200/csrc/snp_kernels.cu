@@ -1707,7 +1707,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
   const uint64_t* gE = O.ebits + blk * mE;
   __syncthreads();
   const uint64_t nq = Q1 - Q0;
-  const bool prog = !TCS && sizeof(T) == 1 && nq <= QCAP;  // CTA-uniform: the store program applies
+  const bool prog = !TCS && (sizeof(T) == 1 || NARROW) && nq <= QCAP;  // CTA-uniform: the quad stores apply
   const uint64_t Qb = Q0 & ~31ULL;                  // sR[q - Qb]
   const int nsec = (int)((Q1 - Qb + 31) >> 5);      // TCS: 32-child sectors of the window
   const bool tcp = TCS && nsec <= 8;                // CTA-uniform: the tensor-core store applies
@@ -2100,6 +2100,10 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       // instead of one byte store per child
       auto edge = [&](uint64_t q0, uint64_t q1) {
         if (q0 >= q1) return;
+        if constexpr (sizeof(T) > 1) {  // NARROW: <= 3 wide values
+          for (uint64_t q = q0; q < q1; ++q) out[eidx((int64_t)q, j, m)] = (T)xsb[sR[q - Qb]];
+          return;
+        }
         uint32_t v = 0;
         for (uint64_t q = q0; q < q1; ++q) v |= (uint32_t)xsb[sR[q - Qb]] << (8 * (q - q0));
         uint8_t* d = orow + eidx((int64_t)q0, j, m);
@@ -2264,7 +2268,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       }
     }
 #if SNP_KC_WIDE_COOP
-    if (sizeof(T) > 1 && nq <= QCAP) {
+    if (sizeof(T) > 1 && !prog && nq <= QCAP) {
       // 16/32-bit counts: the warp writes its rows one at a time, lane = child,
       // so each store instruction fills 32 consecutive children of one row
       __syncwarp();
@@ -2287,7 +2291,14 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       __syncwarp();
       const int hl = lane & 15, j0 = lane >> 4;
       const int32_t jn = m - jbase;  // rows of this warp that exist
-      const uint8_t* xr0 = sX + (size_t)(warp * 32 + j0) * xs_stride<T>();
+      // 4 children's values (bytes of v) as T (NARROW: zero-extended)
+      auto put4 = [](uint8_t* d, uint32_t v) {
+        if constexpr (sizeof(T) == 1) *reinterpret_cast<uint32_t*>(d) = v;
+        else if constexpr (sizeof(T) == 2) *reinterpret_cast<uint2*>(d) = make_uint2(prmt(v, 0u, 0x4140u), prmt(v, 0u, 0x4342u));
+        else *reinterpret_cast<uint4*>(d) = make_uint4(prmt(v, 0u, 0x4440u), prmt(v, 0u, 0x4441u), prmt(v, 0u, 0x4442u),
+                                                       prmt(v, 0u, 0x4443u));
+      };
+      const uint8_t* xr0 = sX + (size_t)(warp * 32 + j0) * XS;
       const uint64_t qa = (Q0 + 3) & ~3ULL, qb = Q1 & ~3ULL;
 #if SNP_KC_FLATQ
       // passes over the CTA's own full quads [qa, qb), 16 per pass (lane
@@ -2298,13 +2309,13 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
         if (q < qb) {
           const uint64_t ob = q >> 6;
           const uint32_t d = sD[(q - Qb) >> 2];
-          uint8_t* dst0 = reinterpret_cast<uint8_t*>(out) + (((int64_t)ob * m + jbase + j0) << 6) + (q & 63);
+          uint8_t* dst0 = reinterpret_cast<uint8_t*>(out + ((((int64_t)ob * m + jbase + j0) << 6) + (q & 63)));
 #else
       for (uint64_t ob = qa >> 6; !(SNP_KC_ABLATE & 4) && qa < qb && ob <= (qb - 1) >> 6; ++ob) {
         const uint64_t q = (ob << 6) + 4 * hl;
         if (q >= qa && q < qb) {
           const uint32_t d = sD[(q - Qb) >> 2];
-          uint8_t* dst0 = reinterpret_cast<uint8_t*>(out) + (((int64_t)ob * m + jbase + j0) << 6) + 4 * hl;
+          uint8_t* dst0 = reinterpret_cast<uint8_t*>(out + ((((int64_t)ob * m + jbase + j0) << 6) + 4 * hl));
 #endif
           if (!(d & 0x80000000u)) {
             const uint32_t* w0 = reinterpret_cast<const uint32_t*>(xr0) + ((d >> 16) & 31);
@@ -2313,23 +2324,23 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(w0) +
-                                                                    2 * i * xs_stride<T>());
+                                                                    2 * i * XS);
               uint32_t v = prmt(w[0], w[1], sel);
 #if SNP_KC_BRANCHLESS
               v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);  // mask = 0 when hb = 0 (words past the row are masked out)
 #else
               if (hb) v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
 #endif
-              if (j0 + 2 * i < jn) *reinterpret_cast<uint32_t*>(dst0 + i * 128) = v;
+              if (j0 + 2 * i < jn) put4(dst0 + i * 128 * (int)sizeof(T), v);
             }
           } else {
             const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (q - Qb));  // 4 parent indices
 #pragma unroll 4
             for (int i = 0; i < 16; ++i) {
-              const uint8_t* xr = xr0 + 2 * i * xs_stride<T>();
+              const uint8_t* xr = xr0 + 2 * i * XS;
               const uint32_t v = (uint32_t)xr[rr & 0xFF] | ((uint32_t)xr[(rr >> 8) & 0xFF] << 8) |
                                  ((uint32_t)xr[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xr[rr >> 24] << 24);
-              if (j0 + 2 * i < jn) *reinterpret_cast<uint32_t*>(dst0 + i * 128) = v;
+              if (j0 + 2 * i < jn) put4(dst0 + i * 128 * (int)sizeof(T), v);
             }
           }
         }
