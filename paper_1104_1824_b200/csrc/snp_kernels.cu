@@ -2694,6 +2694,12 @@ __global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L,
   __shared__ int sK[2];
   __shared__ uint32_t sp[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // fired (c, p) of the first applicable rule of neuron s at count v
+  auto first_cp = [&](int32_t s, int32_t v, int& c, int& p) {
+    const int r = first_rule(S, s, v);
+    c = r >= 0 ? S.rules[r].c : 0;
+    p = r >= 0 ? S.rules[r].p : 0;
+  };
   auto mk = [](int ca, int pa, int cb, int pb) -> FW {
     if constexpr (PK) return (uint32_t)ca | ((uint32_t)pa << 8) | ((uint32_t)cb << 16) | ((uint32_t)pb << 24);
     else return make_int4(ca, pa, cb, pb);
@@ -2729,14 +2735,12 @@ __global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L,
     for (int32_t s = tid; s < m; s += VM_THREADS) {
       int ca = 0, pa = 0, cb = 0, pb = 0;
       const int32_t va = ld_count<T>(L.data, sp[0], s, m);
+      const int32_t vb = sides == 2 ? ld_count<T>(L.data, sp[1], s, m) : 0;
       cnt[s] = va;
-      int r = first_rule(S, s, va);
-      if (r >= 0) { ca = S.rules[r].c; pa = S.rules[r].p; }
+      first_cp(s, va, ca, pa);
       if (sides == 2) {
-        const int32_t vb = ld_count<T>(L.data, sp[1], s, m);
         cnt[m + s] = vb;
-        r = first_rule(S, s, vb);
-        if (r >= 0) { cb = S.rules[r].c; pb = S.rules[r].p; }
+        first_cp(s, vb, cb, pb);
       }
       fc[s] = mk(ca, pa, cb, pb);
     }
@@ -3859,6 +3863,18 @@ constexpr size_t KC_SMEM_MAX = 220 * 1024;
 
 // K-c warps per CTA: MW for 1-2 byte counts, 8 for int32 (staging fits)
 int kc_warps(int32_t bytes) { return bytes == 4 ? 8 : MW; }
+bool materialize_narrow_ok(const SysView& S, int32_t bytes);
+
+// warps per K-c CTA for the byte-staged paths: 8 when m <= 4096 (one or a
+// few neuron passes per block, so several CTAs per SM overlap one block's
+// setup — emit-word staging, child tables — with another's passes), else MW
+int kc_cta_warps(const SysView& S, int32_t bytes, bool staged_e) {
+  if (bytes > 1 && !materialize_narrow_ok(S, bytes)) return kc_warps(bytes);
+  if (!staged_e) return MW;
+  const char* e = getenv("SNP_KC_CTA_WARPS");
+  if (e && atoi(e) > 0) return atoi(e) == 8 ? 8 : MW;
+  return S.m <= 4096 ? 8 : MW;
+}
 
 // wide counts (16/32-bit) computed as bytes (NARROW): every count and x of a
 // level < 256 in the common case; staging rows of bytes, so the CTA keeps
@@ -3869,7 +3885,8 @@ bool materialize_narrow_ok(const SysView& S, int32_t bytes) {
 
 size_t materialize_smem_bytes(const SysView& S, int32_t bytes, bool staged_e) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
-  const size_t xs = materialize_narrow_ok(S, bytes) ? (size_t)MW * 32 * (PB + 4) : (size_t)kc_warps(bytes) * 32 * (PB * bytes + 4);
+  const size_t xs = materialize_narrow_ok(S, bytes) ? (size_t)kc_cta_warps(S, bytes, staged_e) * 32 * (PB + 4)
+                    : (size_t)kc_cta_warps(S, bytes, staged_e) * 32 * (PB * bytes + 4);
   return (staged_e ? (mE + 2) * 8 : 0) + xs + 2 * (QCAP + 32) + 8 * OPCAP + 67 * 8 + 16 + 16;
 }
 
@@ -4017,6 +4034,22 @@ void launch_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, uint64_
   count_launch();
 }
 
+// one K-c variant, NPL (bit planes of the in-synapse count) by the largest in-degree
+template <typename T, bool ES, int MWT, bool TCS, bool NARROW>
+void go_materialize(const SysView& S, const LevelView& L, const ExpandOut& O, const uint64_t* kq_off,
+                    const NextArrays& N, uint64_t* ovf, unsigned long long* n_ovf, uint64_t ovf_cap, size_t smem,
+                    cudaStream_t st) {
+  const unsigned nblk = (unsigned)((L.F + PB - 1) / PB);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<nblk, MWT * 32, smem, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
+  };
+  if (S.max_indeg < 16) go(k_materialize_bs<T, 4, ES, MWT, TCS, NARROW>);
+  else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, ES, MWT, TCS, NARROW>);
+  else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, ES, MWT, TCS, NARROW>);
+  else go(k_materialize_bs<T, 8, ES, MWT, TCS, NARROW>);
+}
+
 void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, const ExpandOut& O,
                         const uint64_t* kq_off, const NextArrays& N, int64_t K, uint64_t* ovf,
                         unsigned long long* n_ovf, uint64_t ovf_cap, int32_t* err, cudaStream_t st) {
@@ -4024,59 +4057,27 @@ void launch_materialize(const SysView& S, int32_t bytes, const LevelView& L, con
   if (fast_materialize_ok(S)) {
     const bool staged = materialize_stage_e(S, bytes);
     const bool tcs = materialize_tc_ok(S, bytes, staged);
+    const bool narrow = materialize_narrow_ok(S, bytes);
+    const int cw = kc_cta_warps(S, bytes, staged);
     const size_t smem = tcs ? materialize_tc_smem_bytes(S, staged) : materialize_smem_bytes(S, bytes, staged);
-    const unsigned nblk = (unsigned)((L.F + PB - 1) / PB);
     dispatch_bytes(bytes, [&](auto tt) {
       using T = decltype(tt);
-      constexpr int W = sizeof(T) == 4 ? 8 : MW;  // = kc_warps(bytes)
-      int threads = W * 32;
-      auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<nblk, threads, smem, st>>>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap);
-      };
       if constexpr (sizeof(T) > 1) {
-        if (materialize_narrow_ok(S, bytes)) {
-          threads = MW * 32;
-          if (staged) {
-            if (S.max_indeg < 16) go(k_materialize_bs<T, 4, true, MW, false, true>);
-            else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, true, MW, false, true>);
-            else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, true, MW, false, true>);
-            else go(k_materialize_bs<T, 8, true, MW, false, true>);
-          } else {
-            if (S.max_indeg < 16) go(k_materialize_bs<T, 4, false, MW, false, true>);
-            else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, false, MW, false, true>);
-            else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, false, MW, false, true>);
-            else go(k_materialize_bs<T, 8, false, MW, false, true>);
-          }
-          return;
+        if (narrow) {
+          if (staged && cw == 8) go_materialize<T, true, 8, false, true>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
+          else if (staged) go_materialize<T, true, MW, false, true>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
+          else go_materialize<T, false, MW, false, true>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
+        } else if (staged) {
+          go_materialize<T, true, sizeof(T) == 4 ? 8 : MW, false, false>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
+        } else {
+          go_materialize<T, false, sizeof(T) == 4 ? 8 : MW, false, false>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
         }
-      }
-      if constexpr (sizeof(T) == 1) {
-        if (tcs) {
-          if (staged) {
-            if (S.max_indeg < 16) go(k_materialize_bs<T, 4, true, W, true>);
-            else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, true, W, true>);
-            else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, true, W, true>);
-            else go(k_materialize_bs<T, 8, true, W, true>);
-          } else {
-            if (S.max_indeg < 16) go(k_materialize_bs<T, 4, false, W, true>);
-            else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, false, W, true>);
-            else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, false, W, true>);
-            else go(k_materialize_bs<T, 8, false, W, true>);
-          }
-          return;
-        }
-      }
-      if (staged) {
-        if (S.max_indeg < 16) go(k_materialize_bs<T, 4, true, W>);
-        else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, true, W>);
-        else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, true, W>);
-        else go(k_materialize_bs<T, 8, true, W>);
       } else {
-        if (S.max_indeg < 16) go(k_materialize_bs<T, 4, false, W>);
-        else if (S.max_indeg < 32) go(k_materialize_bs<T, 5, false, W>);
-        else if (S.max_indeg < 64) go(k_materialize_bs<T, 6, false, W>);
-        else go(k_materialize_bs<T, 8, false, W>);
+        if (tcs && staged) go_materialize<T, true, MW, true, false>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
+        else if (tcs) go_materialize<T, false, MW, true, false>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
+        else if (staged && cw == 8) go_materialize<T, true, 8, false, false>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
+        else if (staged) go_materialize<T, true, MW, false, false>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
+        else go_materialize<T, false, MW, false, false>(S, L, O, kq_off, N, ovf, n_ovf, ovf_cap, smem, st);
       }
     });
   } else {

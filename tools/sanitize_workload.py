@@ -1,8 +1,9 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck /
-initcheck): Π (configs 1-2 shapes), 50 tiny random systems, and a m = 1024
+initcheck): Π (configs 1-2 shapes), 50 tiny random systems, a m = 1024
 uint8 system through the tensor-core K-a (k_expand_tc) and the bit-sliced
-K-c (k_materialize_bs), plus the delay, sampling and generated-number
-kernels.  Each result is checked against the oracle so a kernel that misbehaves
+K-c (k_materialize_bs, also its tensor-core permutation variant), a 32-bit
+exact-dedup system (NARROW K-a / K-c, k_verify_m), plus the delay, sampling
+and generated-number kernels.  Each result is checked against the oracle so a kernel that misbehaves
 under the tool also fails here.  usage: compute-sanitizer --tool T python tools/sanitize_workload.py"""
 import os
 import sys
@@ -35,6 +36,17 @@ def main():
     assert eng.kernel_paths == snp.SNP_PATH_TC_EXPAND
     same(eng.explore(L0, depth=3), oracle.System.from_workload(w).explore(L0, depth=3, dedup=1, count_bits=8,
                                                                           frontier_target=300))
+    # 32-bit counts, exact dedup: NARROW K-a / K-c and the per-match verification
+    w3 = W.random_system(1024, outdeg=8, k_nd=5, seed=123)
+    L3 = W.level0_counts(w3, 300, 123)
+    L3[::7] += 300
+    same(snp.System(w3, count_bits=32, dedup=0, frontier_target=400).explore(L3, depth=3),
+         oracle.System.from_workload(w3).explore(L3, depth=3, dedup=0, count_bits=32, frontier_target=400))
+    # the tensor-core output permutation variant of K-c (opt-in)
+    os.environ["SNP_KERNELS"] = "kc_tc"
+    same(snp.System(w, count_bits=8, dedup=1, frontier_target=300).explore(L0, depth=3),
+         oracle.System.from_workload(w).explore(L0, depth=3, dedup=1, count_bits=8, frontier_target=300))
+    os.environ["SNP_KERNELS"] = ""
     wg = W.pi_system("textbook")
     assert snp.System(wg, out_rule=3).explore(None, depth=20) is not None
     ws = W.random_system(200, outdeg=6, k_nd=5, seed=7)
