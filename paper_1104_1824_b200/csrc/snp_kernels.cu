@@ -1794,7 +1794,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
   }
   __syncthreads();
   const uint64_t haskids = (uint64_t)sMisc[0] | ((uint64_t)sMisc[1] << 32);
-  const int nops = prog ? (int)sMisc[2] : 0;
+  [[maybe_unused]] const int nops = prog ? (int)sMisc[2] : 0;  // the store program (SNP_KC_COOP=0)
   if (ES) mbar_wait(bar, 0);
 
   const T* data = reinterpret_cast<const T*>(L.data);
@@ -2672,7 +2672,10 @@ __global__ void k_verify_cols(SysView S, LevelView L, ChildArrays C, const uint6
 // per row, padding reads a zero entry).  PK: every rule has c, p <= 255, so a
 // neuron's (c_a, p_a, c_b, p_b) is one 32-bit word.  A mismatch is a 128-bit
 // collision (reading A18).
-constexpr int VM_THREADS = 256;
+#ifndef SNP_VM_THREADS
+#define SNP_VM_THREADS 256
+#endif
+constexpr int VM_THREADS = SNP_VM_THREADS;  // threads per match (CTA); CTAs per SM = min(2048 / VM_THREADS, smem)
 size_t verify_m_smem_bytes(int32_t m, bool pk) {
   const size_t mE = (size_t)((m + 1) & ~1) + 2;
   return mE * (pk ? 4 : 16) + (size_t)m * 8 + 2 * KMAX * 8 + 64;
@@ -3733,7 +3736,6 @@ __global__ void __launch_bounds__(SAMPLE_CTA) k_sample_cta(SysView S, int32_t* c
   int32_t* N = nxt + w * m;
   const bool tab8 = S.tables_ok && S.full8 && S.tab_full != nullptr;
   int32_t hs = -1;
-  bool bad = false;
   for (int32_t k = 0; k < steps; ++k) {
     if (tid == 0) nnd = 0;
     __syncthreads();
@@ -3801,7 +3803,6 @@ __global__ void __launch_bounds__(SAMPLE_CTA) k_sample_cta(SysView S, int32_t* c
     __syncthreads();
     if (verdict == 2) {
       if (tid == 0) atomicOr(err, ERR_CAPACITY);
-      bad = true;
       break;
     }
     if (verdict == 1) {
@@ -3825,7 +3826,6 @@ __global__ void __launch_bounds__(SAMPLE_CTA) k_sample_cta(SysView S, int32_t* c
     ovf = __syncthreads_or(ovf);
     if (ovf) {
       if (tid == 0) atomicOr(err, ERR_OVERFLOW);
-      bad = true;
       break;
     }
     if (any) {
@@ -3834,7 +3834,6 @@ __global__ void __launch_bounds__(SAMPLE_CTA) k_sample_cta(SysView S, int32_t* c
       N = t_;
     }
   }
-  (void)bad;
   if (C != cur + w * m)
     for (int32_t j = tid; j < m; j += SAMPLE_CTA) cur[w * m + j] = C[j];
   if (tid == 0) halted[w] = hs;
@@ -4183,7 +4182,8 @@ bool launch_verify_m(const SysView& S, int32_t bytes, const LevelView& L, const 
   const bool pk = S.small_cp != 0;
   const size_t sm = verify_m_smem_bytes(S.m, pk);
   if (sm > 200 * 1024) return false;
-  const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(8, (size_t)(220 * 1024) / (sm + 1024)));
+  const unsigned per_sm =
+      (unsigned)std::max<size_t>(1, std::min<size_t>(2048 / VM_THREADS, (size_t)(220 * 1024) / (sm + 1024)));
   dispatch_bytes(bytes, [&](auto tt) {
     using TT = decltype(tt);
     auto go = [&](auto kern) {
