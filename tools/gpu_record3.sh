@@ -22,10 +22,9 @@ timeout 1200 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_
   python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > $O/dram.log 2>&1
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_expand_tc|k_materialize_bs" -s 4 -c 2 \
   -o $O/prof python bench.py --F 1048576 --steps 2 --warmup 3 --no-e2e --no-cpu > $O/ncu.log 2>&1
-for T in memcheck racecheck synccheck; do
-  timeout 1500 compute-sanitizer --tool $T --print-limit 50 python tools/sanitize_workload.py > $O/sanitizer_$T.txt 2>&1
-done
-timeout 1500 compute-sanitizer --tool initcheck --print-limit 20 python tools/sanitize_workload.py > $O/sanitizer_initcheck.txt 2>&1
+# compute-sanitizer is closed on this GPU pool (runs under it left GPUs needing a reset): the
+# workload runs plain, with every result checked against the oracle
+timeout 900 python tools/sanitize_workload.py > $O/sanitize_workload_plain.txt 2>&1
 timeout 3000 python -m pytest tests -m gpu -q --timeout 1500 --durations=20 > $O/pytest.log 2>&1; echo pytest_rc=$? >> $O/pytest.log
 tail -3 $O/pytest.log
 ls -la $O
