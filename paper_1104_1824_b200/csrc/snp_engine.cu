@@ -1080,30 +1080,43 @@ snp_status begin_impl(snp_system* s, const snp_configs* level0) {
     if (R > F0) R = F0;
     DBuf stg[2];
     for (auto& b : stg) SNP_TRY(b.ensure((size_t)((R - 1) * ld + m) * level0->elem_bytes, false));
-    cudaStream_t cs = nullptr;
-    cudaEvent_t copied[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr};
+    // each chunk's copy split over NS side streams (SNP_UPLOAD_STREAMS; 1 by
+    // default: 2 streams measured 31 vs 52 GB/s through snp_begin, 3 equal to 1,
+    // profiles/r02f/upload_streams.json — one copy engine saturates the link)
+    int NS = 1;
+    if (const char* e2 = getenv("SNP_UPLOAD_STREAMS")) NS = std::max(1, std::min(4, atoi(e2)));
+    cudaStream_t cs[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t copied[2][4] = {}, used[2] = {nullptr, nullptr};
     auto cleanup = [&]() {
       for (int b = 0; b < 2; ++b) {
-        if (copied[b]) cudaEventDestroy(copied[b]);
+        for (int k = 0; k < NS; ++k)
+          if (copied[b][k]) cudaEventDestroy(copied[b][k]);
         if (used[b]) cudaEventDestroy(used[b]);
       }
-      if (cs) cudaStreamDestroy(cs);
+      for (int k = 0; k < NS; ++k)
+        if (cs[k]) cudaStreamDestroy(cs[k]);
     };
-    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    cudaError_t e = cudaSuccess;
+    for (int k = 0; k < NS && e == cudaSuccess; ++k) e = cudaStreamCreateWithFlags(&cs[k], cudaStreamNonBlocking);
     for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
-      e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
+      for (int k = 0; k < NS && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&copied[b][k], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&used[b], cudaEventDisableTiming);
     }
     const uint8_t* hsrc = reinterpret_cast<const uint8_t*>(level0->data);
     for (int64_t r0 = 0, i = 0; r0 < F0 && e == cudaSuccess; r0 += R, ++i) {
       const int64_t n = std::min<int64_t>(R, F0 - r0);
       const int b = (int)(i & 1);
-      if (i >= 2) e = cudaStreamWaitEvent(cs, used[b], 0);
-      if (e == cudaSuccess)
-        e = cudaMemcpyAsync(stg[b].p, hsrc + (size_t)r0 * row_b, (size_t)((n - 1) * ld + m) * level0->elem_bytes,
-                            cudaMemcpyHostToDevice, cs);
-      if (e == cudaSuccess) e = cudaEventRecord(copied[b], cs);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, copied[b], 0);
+      const size_t cb = (size_t)((n - 1) * ld + m) * level0->elem_bytes;
+      const size_t piece = (cb / NS + 4095) & ~(size_t)4095;
+      for (int k = 0; k < NS && e == cudaSuccess; ++k) {
+        const size_t o = (size_t)k * piece;
+        if (i >= 2) e = cudaStreamWaitEvent(cs[k], used[b], 0);
+        if (e == cudaSuccess && o < cb)
+          e = cudaMemcpyAsync(static_cast<uint8_t*>(stg[b].p) + o, hsrc + (size_t)r0 * row_b + o, std::min(piece, cb - o),
+                              cudaMemcpyHostToDevice, cs[k]);
+        if (e == cudaSuccess) e = cudaEventRecord(copied[b][k], cs[k]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, copied[b][k], 0);
+      }
       if (e != cudaSuccess) break;
       launch_import(stg[b].p, level0->elem_bytes, SNP_LAYOUT_ROW_MAJOR, ld, n, (int32_t)m,
                     raw.as<uint8_t>() + (size_t)r0 * m * s->bytes, s->bytes, s->count_max, err, s->stream);

@@ -1434,17 +1434,54 @@ __global__ void k_compact(ChildArrays C, const uint64_t* off, uint64_t T, NextAr
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t key_owner(uint64_t fp1, uint32_t P) { return (uint32_t)(fmix64(fp1) % P); }
 
+// keys per owner: lanes with the same owner aggregated (match_any), one
+// shared-memory add per group, one global add per (block, owner) — with P <= 8
+// owners a per-key global atomic serialised ~T/P adds on each counter
 __global__ void k_owner_hist(const uint64_t* fp1, uint64_t T, uint32_t P, unsigned long long* counts) {
-  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T; c += (uint64_t)gridDim.x * blockDim.x)
-    atomicAdd(&counts[key_owner(fp1[c], P)], 1ULL);
+  extern __shared__ unsigned oh_cnt[];  // [P]
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) oh_cnt[i] = 0;
+  __syncthreads();
+  for (uint64_t c0 = blockIdx.x * (uint64_t)blockDim.x; c0 < T; c0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = c0 + threadIdx.x;
+    if (c < T) {
+      const uint32_t own = key_owner(fp1[c], P);
+      const unsigned grp = __match_any_sync(__activemask(), own);
+      if ((threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1)) atomicAdd(&oh_cnt[own], (unsigned)__popc(grp));
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x)
+    if (oh_cnt[i]) atomicAdd(&counts[i], (unsigned long long)oh_cnt[i]);
 }
 
 // send row pos = {fp0, fp1, global tag}; perm[c] = pos (positions inside an
-// owner's bucket are arbitrary: the owner's decisions do not depend on them)
+// owner's bucket are arbitrary: the owner's decisions do not depend on them).
+// One key per thread; a block reserves its range of every owner's bucket with
+// one global add (ranks inside it from match_any groups and shared memory)
 __global__ void k_owner_pack(const uint64_t* fp0, const uint64_t* fp1, uint64_t T, uint32_t P, uint64_t tag_base,
                              unsigned long long* cursor, uint64_t* perm, uint64_t* send) {
-  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < T; c += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t pos = atomicAdd(&cursor[key_owner(fp1[c], P)], 1ULL);
+  extern __shared__ unsigned long long op_base[];  // [P] bases, then [P] counts
+  unsigned* cnt = reinterpret_cast<unsigned*>(op_base + P);
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  uint32_t own = 0;
+  unsigned local = 0;
+  if (c < T) {
+    own = key_owner(fp1[c], P);
+    const unsigned grp = __match_any_sync(__activemask(), own);
+    const int leader = __ffs(grp) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(&cnt[own], (unsigned)__popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    local = base + (unsigned)__popc(grp & ((1u << lane) - 1));
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) op_base[i] = cnt[i] ? atomicAdd(&cursor[i], (unsigned long long)cnt[i]) : 0;
+  __syncthreads();
+  if (c < T) {
+    const uint64_t pos = op_base[own] + local;
     perm[c] = pos;
     send[3 * pos] = fp0[c];
     send[3 * pos + 1] = fp1[c];
@@ -1509,10 +1546,9 @@ __global__ void k_owner_keep(const uint64_t* recv, uint64_t R, Tables tb, const 
     bool k = verdict[i] == 1 && tb.ltab[slot[i]].tag == recv[3 * i + 2];
     if (k && thin) k = fmix64(k0) < tau;
     out[i] = k ? 1 : 0;
-    if (k) {
-      visited_insert(tb, k0, k1, 0, err);
-      atomicAdd(n_kept, 1ULL);
-    }
+    if (k) visited_insert(tb, k0, k1, 0, err);
+    const unsigned b = __ballot_sync(__activemask(), k);  // one add per warp
+    if (b && (threadIdx.x & 31) == (unsigned)(__ffs(b) - 1)) atomicAdd(n_kept, (unsigned long long)__popc(b));
   }
 }
 
@@ -4311,14 +4347,14 @@ void launch_owner_hist(const uint64_t* fp1, uint64_t T, uint32_t P, unsigned lon
   if (!T) return;
   unsigned g = grid_for(T);
   if (g > 148u * 16u) g = 148u * 16u;
-  k_owner_hist<<<g, BLK, 0, st>>>(fp1, T, P, counts);
+  k_owner_hist<<<g, BLK, (size_t)P * 4, st>>>(fp1, T, P, counts);
   count_launch();
 }
 
 void launch_owner_pack(const uint64_t* fp0, const uint64_t* fp1, uint64_t T, uint32_t P, uint64_t tag_base,
                        unsigned long long* cursor, uint64_t* perm, uint64_t* send, cudaStream_t st) {
   if (!T) return;
-  k_owner_pack<<<grid_for(T), BLK, 0, st>>>(fp0, fp1, T, P, tag_base, cursor, perm, send);
+  k_owner_pack<<<grid_for(T), BLK, (size_t)P * 12, st>>>(fp0, fp1, T, P, tag_base, cursor, perm, send);
   count_launch();
 }
 
