@@ -249,6 +249,7 @@ def run_native(args, rank, world):
 
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local_rank)
+    snp.set_device(local_rank)  # libsnp.so's own CUDA runtime: the same GPU
     dev = torch.device("cuda", local_rank)
     dist = None
     use_dist = world > 1 or args.dist

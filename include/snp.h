@@ -282,6 +282,12 @@ snp_status snp_set_profiling(snp_system *sys, int32_t on);
 snp_status snp_profile(const snp_system *sys, double *ms /* SNP_NUM_PHASES */);
 /* Kernels launched by this process through libsnp.so so far. */
 int64_t    snp_kernel_launches(void);
+/* Make CUDA device `device` current for the calling thread inside libsnp.so
+ * (its CUDA runtime is its own: one process per GPU calls this with its local
+ * rank before snp_load, so every allocation, stream and kernel of the systems
+ * it loads lives on that GPU).  SNP_E_ARG for a device index out of range,
+ * SNP_E_CUDA when no device is present. */
+snp_status snp_set_device(int32_t device);
 /* Kernel paths the loaded system takes (bit mask, 0 for NULL):
  *   SNP_PATH_TC_EXPAND  K-a on the tensor cores (k_expand_tc: uint8 storage,
  *                       every neuron tabulated, c <= 15, p <= 1, rule deltas

@@ -1881,6 +1881,17 @@ snp_status snp_profile(const snp_system* s, double* ms) {
 
 int64_t snp_kernel_launches(void) { return snp::g_kernel_launches.load(); }
 
+snp_status snp_set_device(int32_t device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    return fail(SNP_E_CUDA, "snp_set_device: no CUDA device");
+  }
+  if (device < 0 || device >= n) return fail(SNP_E_ARG, "snp_set_device: device %d of %d", device, n);
+  CUDA_TRY(cudaSetDevice(device));
+  return SNP_OK;
+}
+
 int32_t snp_kernel_paths(const snp_system* s) {
   if (!s) return 0;
   return (s->view.tc_ok && !(s->view.kernel_flags & (snp::KF_NO_TC | snp::KF_EXPAND_T))) ? SNP_PATH_TC_EXPAND : 0;

@@ -2714,25 +2714,34 @@ __global__ void k_verify_cols(SysView S, LevelView L, ChildArrays C, const uint6
 constexpr int VM_THREADS = SNP_VM_THREADS;  // threads per match (CTA); CTAs per SM = min(2048 / VM_THREADS, smem)
 size_t verify_m_smem_bytes(int32_t m, bool pk) {
   const size_t mE = (size_t)((m + 1) & ~1) + 2;
-  return mE * (pk ? 4 : 16) + (size_t)m * 8 + 2 * KMAX * 8 + 64;
+  return mE * (pk ? 4 : 16) + (size_t)m * 8 + 4 * KMAX * 8 + 64;
 }
 
+// VM_THREADS compute threads plus one decoder warp: the decoder reads the
+// next match's key, parents and ND digits into the other half of a double
+// buffer while the compute warps verify the current one (their phase
+// barriers are named barriers over the compute threads only; the loop-end
+// barrier joins everyone), so the ≈ 6 dependent loads of a decode overlap
+// the count loads and the column pass
 template <typename T, bool PK>
-__global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L, ExpandOut O, const uint64_t* off,
-                                                         ChildArrays C, const uint64_t* list,
-                                                         const unsigned long long* n_list, uint64_t tag_base, Tables tb,
-                                                         const StoredLevel* stored, int32_t* err) {
+__global__ void __launch_bounds__(VM_THREADS + 32) k_verify_m(SysView S, LevelView L, ExpandOut O, const uint64_t* off,
+                                                              ChildArrays C, const uint64_t* list,
+                                                              const unsigned long long* n_list, uint64_t tag_base,
+                                                              Tables tb, const StoredLevel* stored, int32_t* err) {
   using FW = typename std::conditional<PK, uint32_t, int4>::type;
   extern __shared__ __align__(16) uint8_t vm_smem[];
   const int32_t m = S.m;
   const int32_t mE = (m + 1) & ~1;
   FW* fc = reinterpret_cast<FW*>(vm_smem);                            // [mE + 2] (c_a, p_a, c_b, p_b); zero pads
   int32_t* cnt = reinterpret_cast<int32_t*>(fc + mE + 2);             // [2][m]
-  int32_t* nds = cnt + 2 * m;                                          // [2][KMAX] neuron
-  uint8_t* ndx = reinterpret_cast<uint8_t*>(nds + 2 * KMAX);          // [2][KMAX] digit
-  __shared__ int sK[2];
-  __shared__ uint32_t sp[2];
+  int32_t* nds = cnt + 2 * m;                                          // [2 buf][2 sides][KMAX] neuron
+  uint8_t* ndx = reinterpret_cast<uint8_t*>(nds + 4 * KMAX);          // [2 buf][2 sides][KMAX] digit
+  __shared__ int sK[2][2];
+  __shared__ uint32_t sp[2][2];
+  __shared__ uint8_t svd[2];
+  __shared__ uint64_t sref[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool decoder = tid >= VM_THREADS;
   // fired (c, p) of the first applicable rule of neuron s at count v
   auto first_cp = [&](int32_t s, int32_t v, int& c, int& p) {
     const int r = first_rule(S, s, v);
@@ -2747,74 +2756,88 @@ __global__ void __launch_bounds__(VM_THREADS) k_verify_m(SysView S, LevelView L,
   auto pa_ = [](FW f) -> int32_t { if constexpr (PK) return (int32_t)((f >> 8) & 0xFF); else return f.y; };
   auto cb_ = [](FW f) -> int32_t { if constexpr (PK) return (int32_t)((f >> 16) & 0xFF); else return f.z; };
   auto pb_ = [](FW f) -> int32_t { if constexpr (PK) return (int32_t)(f >> 24); else return f.w; };
-  if (tid < mE + 2 - m) fc[m + tid] = mk(0, 0, 0, 0);  // targets of padded in-synapses
-  const uint64_t nl = *n_list;
-  for (uint64_t i = blockIdx.x; i < nl; i += gridDim.x) {
+  // decoder lanes 0 / 1: side 0 = the listed child, side 1 = its key's winner
+  auto decode = [&](uint64_t i, int b) {
+    if (lane > 1) return;
     const uint64_t c = list[i];
     const uint8_t vd = C.verdict[c];
-    const int sides = vd == 1 ? 2 : 1;
-    if (tid < sides) {
-      // side 0: the child; side 1: its key's winner (same level)
-      const uint64_t cc = tid == 0 ? c : tb.ltab[C.cslot[c]].tag - tag_base;
-      const uint32_t p = C.cpar[cc];
-      const uint64_t* nd = O.nd + (uint64_t)p * KMAX;
-      const int K = O.ndc[p];
-      uint64_t t = cc - off[p];
-      for (int k = K - 1; k >= 0; --k) {  // mixed radix, first ND neuron most significant (reading A7)
-        const int32_t s = (int32_t)(nd[k] >> 32), v = (int32_t)(uint32_t)nd[k];
-        const uint64_t d = (uint64_t)count_applicable(S, s, v);
-        nds[tid * KMAX + k] = s;
-        ndx[tid * KMAX + k] = (uint8_t)(t % d);
-        t /= d;
-      }
-      sK[tid] = K;
-      sp[tid] = p;
+    if (lane == 0) {
+      svd[b] = vd;
+      sref[b] = vd == 1 ? 0 : C.cref[c];
     }
-    __syncthreads();
-    for (int32_t s = tid; s < m; s += VM_THREADS) {
-      int ca = 0, pa = 0, cb = 0, pb = 0;
-      const int32_t va = ld_count<T>(L.data, sp[0], s, m);
-      const int32_t vb = sides == 2 ? ld_count<T>(L.data, sp[1], s, m) : 0;
-      cnt[s] = va;
-      first_cp(s, va, ca, pa);
-      if (sides == 2) {
-        cnt[m + s] = vb;
-        first_cp(s, vb, cb, pb);
-      }
-      fc[s] = mk(ca, pa, cb, pb);
+    if (lane == 1 && vd != 1) return;
+    const uint64_t cc = lane == 0 ? c : tb.ltab[C.cslot[c]].tag - tag_base;
+    const uint32_t p = C.cpar[cc];
+    const uint64_t* nd = O.nd + (uint64_t)p * KMAX;
+    const int K = O.ndc[p];
+    uint64_t t = cc - off[p];
+    for (int k = K - 1; k >= 0; --k) {  // mixed radix, first ND neuron most significant (reading A7)
+      const int32_t s = (int32_t)(nd[k] >> 32), v = (int32_t)(uint32_t)nd[k];
+      const uint64_t d = (uint64_t)count_applicable(S, s, v);
+      nds[(2 * b + lane) * KMAX + k] = s;
+      ndx[(2 * b + lane) * KMAX + k] = (uint8_t)(t % d);
+      t /= d;
     }
-    __syncthreads();
-    for (int sd = 0; sd < sides; ++sd) {  // ND digits != 0 (a neuron appears once per side)
-      if (tid < sK[sd] && ndx[sd * KMAX + tid]) {
-        const int32_t s = nds[sd * KMAX + tid];
-        const int r = nth_applicable(S, s, cnt[sd * m + s], ndx[sd * KMAX + tid]);
-        const FW f = fc[s];
-        fc[s] = sd == 0 ? mk(S.rules[r].c, S.rules[r].p, cb_(f), pb_(f)) : mk(ca_(f), pa_(f), S.rules[r].c, S.rules[r].p);
-      }
-      __syncthreads();
-    }
-    const uint64_t ref = vd == 1 ? 0 : C.cref[c];
+    sK[b][lane] = K;
+    sp[b][lane] = p;
+  };
+  if (tid < mE + 2 - m) fc[m + tid] = mk(0, 0, 0, 0);  // targets of padded in-synapses
+  const uint64_t nl = *n_list;
+  if (decoder && blockIdx.x < nl) decode(blockIdx.x, 0);
+  __syncthreads();
+  int b = 0;
+  for (uint64_t i = blockIdx.x; i < nl; i += gridDim.x, b ^= 1) {
     bool diff = false;
-    for (int32_t j0 = warp * 32; j0 < m; j0 += VM_THREADS) {
-      const int32_t j = j0 + lane;
-      const int64_t g = j0 >> 5;
-      const int64_t r0 = __ldg(S.in_pad_off + g), r1 = __ldg(S.in_pad_off + g + 1);
-      const FW fj = fc[j < m ? j : m];
-      if (vd == 1) {
-        int64_t d = j < m ? ((int64_t)cnt[j] - ca_(fj)) - ((int64_t)cnt[m + j] - cb_(fj)) : 0;
-        for (int64_t r = r0; r < r1; ++r) {
-          const int32_t src = S.in_pad16 ? (int32_t)__ldg(S.in_pad16 + r * 32 + lane) : __ldg(S.in_pad + r * 32 + lane);
-          const FW f = fc[src];
-          d += pa_(f) - pb_(f);
+    if (decoder) {
+      if (i + gridDim.x < nl) decode(i + gridDim.x, b ^ 1);
+    } else {
+      const uint8_t vd = svd[b];
+      const int sides = vd == 1 ? 2 : 1;
+      const uint32_t p0 = sp[b][0], p1 = sp[b][1];
+      for (int32_t s = tid; s < m; s += VM_THREADS) {
+        int ca = 0, pa = 0, cb = 0, pb = 0;
+        const int32_t va = ld_count<T>(L.data, p0, s, m);
+        const int32_t vb = sides == 2 ? ld_count<T>(L.data, p1, s, m) : 0;
+        cnt[s] = va;
+        first_cp(s, va, ca, pa);
+        if (sides == 2) {
+          cnt[m + s] = vb;
+          first_cp(s, vb, cb, pb);
         }
-        diff |= d != 0;
-      } else {
-        int64_t a = j < m ? (int64_t)cnt[j] - ca_(fj) : 0;
-        for (int64_t r = r0; r < r1; ++r) {
-          const int32_t src = S.in_pad16 ? (int32_t)__ldg(S.in_pad16 + r * 32 + lane) : __ldg(S.in_pad + r * 32 + lane);
-          a += pa_(fc[src]);
+        fc[s] = mk(ca, pa, cb, pb);
+      }
+      tc::named_sync(1, VM_THREADS);
+      for (int sd = 0; sd < sides; ++sd) {  // ND digits != 0 (a neuron appears once per side)
+        if (tid < sK[b][sd] && ndx[(2 * b + sd) * KMAX + tid]) {
+          const int32_t s = nds[(2 * b + sd) * KMAX + tid];
+          const int r = nth_applicable(S, s, cnt[sd * m + s], ndx[(2 * b + sd) * KMAX + tid]);
+          const FW f = fc[s];
+          fc[s] = sd == 0 ? mk(S.rules[r].c, S.rules[r].p, cb_(f), pb_(f)) : mk(ca_(f), pa_(f), S.rules[r].c, S.rules[r].p);
         }
-        if (j < m) diff |= a != ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, m);
+        tc::named_sync(1, VM_THREADS);
+      }
+      const uint64_t ref = sref[b];
+      for (int32_t j0 = warp * 32; j0 < m; j0 += VM_THREADS) {
+        const int32_t j = j0 + lane;
+        const int64_t g = j0 >> 5;
+        const int64_t r0 = __ldg(S.in_pad_off + g), r1 = __ldg(S.in_pad_off + g + 1);
+        const FW fj = fc[j < m ? j : m];
+        if (vd == 1) {
+          int64_t d = j < m ? ((int64_t)cnt[j] - ca_(fj)) - ((int64_t)cnt[m + j] - cb_(fj)) : 0;
+          for (int64_t r = r0; r < r1; ++r) {
+            const int32_t src = S.in_pad16 ? (int32_t)__ldg(S.in_pad16 + r * 32 + lane) : __ldg(S.in_pad + r * 32 + lane);
+            const FW f = fc[src];
+            d += pa_(f) - pb_(f);
+          }
+          diff |= d != 0;
+        } else {
+          int64_t a = j < m ? (int64_t)cnt[j] - ca_(fj) : 0;
+          for (int64_t r = r0; r < r1; ++r) {
+            const int32_t src = S.in_pad16 ? (int32_t)__ldg(S.in_pad16 + r * 32 + lane) : __ldg(S.in_pad + r * 32 + lane);
+            a += pa_(fc[src]);
+          }
+          if (j < m) diff |= a != ld_count<T>(stored[ref >> 40].data, (int64_t)(ref & ((1ULL << 40) - 1)), j, m);
+        }
       }
     }
     if (__syncthreads_or(diff) && tid == 0) atomicOr(err, ERR_COLLISION);
@@ -4219,12 +4242,12 @@ bool launch_verify_m(const SysView& S, int32_t bytes, const LevelView& L, const 
   const size_t sm = verify_m_smem_bytes(S.m, pk);
   if (sm > 200 * 1024) return false;
   const unsigned per_sm =
-      (unsigned)std::max<size_t>(1, std::min<size_t>(2048 / VM_THREADS, (size_t)(220 * 1024) / (sm + 1024)));
+      (unsigned)std::max<size_t>(1, std::min<size_t>(2048 / (VM_THREADS + 32), (size_t)(220 * 1024) / (sm + 1024)));
   dispatch_bytes(bytes, [&](auto tt) {
     using TT = decltype(tt);
     auto go = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      kern<<<148u * per_sm, VM_THREADS, sm, st>>>(S, L, O, off, C, list, n_list, tag_base, tb, stored, err);
+      kern<<<148u * per_sm, VM_THREADS + 32, sm, st>>>(S, L, O, off, C, list, n_list, tag_base, tb, stored, err);
     };
     if (pk) go(k_verify_m<TT, true>);
     else go(k_verify_m<TT, false>);

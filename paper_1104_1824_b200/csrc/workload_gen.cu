@@ -39,6 +39,11 @@ __global__ void k_level0(T* dst, int32_t m, int64_t F, int64_t ld, int32_t layou
 extern "C" int snpgen_level0(void* dst, int32_t elem_bytes, int32_t layout, int64_t ld, int32_t m, int64_t F,
                              uint64_t key, const int32_t* range_host, int64_t row_begin, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  {  // this library's CUDA runtime on the GPU that holds dst (one process per GPU)
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type == cudaMemoryTypeDevice) cudaSetDevice(pa.device);
+    cudaGetLastError();
+  }
   int32_t* range = nullptr;
   if (cudaMalloc(&range, sizeof(int32_t) * m) != cudaSuccess) return -5;
   cudaMemcpyAsync(range, range_host, sizeof(int32_t) * m, cudaMemcpyHostToDevice, st);

@@ -44,6 +44,7 @@ EXPORTED = [
     "snp_spiking_vector", "snp_level_spiking_vectors", "snp_frontier_copy", "snp_level_all_edges",
     "snp_dist_unique_id", "snp_dist_init", "snp_local_group_create", "snp_local_group_free", "snp_dist_init_local",
     "snp_dist_set_rebalance", "snp_dist_start", "snp_dist_advance", "snp_dist_summary", "snp_dist_local",
+    "snp_set_device",
 ]
 SNP_DIST_ID_BYTES = 128
 SNP_NUM_PHASES = 5
@@ -145,6 +146,7 @@ def lib() -> ctypes.CDLL:
         L.snp_set_profiling.argtypes = [_P, ctypes.c_int32]
         L.snp_profile.argtypes = [_P, _P]
         L.snp_kernel_launches.restype = ctypes.c_int64
+        L.snp_set_device.argtypes = [ctypes.c_int32]
         L.snp_sample.argtypes = [_P, ctypes.c_int64, _P, ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32, _P,
                                  ctypes.c_int32, _P]
         L.snp_kernel_paths.argtypes = [_P]
@@ -536,6 +538,12 @@ class Tree:
             self.close()
         except Exception:
             pass
+
+
+def set_device(device: int) -> None:
+    """snp_set_device: CUDA device `device` current inside libsnp.so (one
+    process per GPU: its local rank, before the first System)."""
+    _check(lib().snp_set_device(int(device)))
 
 
 def snp_kernel_launches() -> int:
