@@ -147,6 +147,7 @@ struct SysView {
   int32_t n_nd;              // neurons with some count making >= 2 rules applicable
   const int32_t* nd_list;    // n_nd, increasing
   const uint8_t* xyt;        // m × 32   first rule c | p << 4 for v < 32 (0 = none)
+  const uint16_t* cpT;       // 32 × m   first rule c | p << 8 at count v < 32, count-major (verification; c, p <= 255)
   const uint8_t* xyf;        // m × 256  the same for every uint8 count
   const uint8_t* btile;      // ceil(m/64) × 4096: B chunks (−R bytes | 1, Rout bytes), K-major core matrices
   // SN P systems with delays (reading A26): delay_m > 0

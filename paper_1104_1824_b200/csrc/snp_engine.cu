@@ -216,7 +216,7 @@ struct snp_system {
   uint64_t vis_cap = 0, ltab_cap = 0, child_cap = 0;
   // scratch
   DBuf psi, off, fpb0, fpb1, ndc, nd, ebits;
-  DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab, d_elut, d_hsg, d_xyt, d_xyf, d_btile, d_ndl, d_delay;
+  DBuf d_meta, d_tab, d_tab_full, d_ctab, d_ttab, d_elut, d_hsg, d_xyt, d_xyf, d_btile, d_ndl, d_delay, d_cpT;
   DBuf cpar, cfp0, cfp1, verdict, cslot, cref, kept, kpos, kq_off, scan_tmp, ovf, src_index, stored;
   DBuf counters_dev;  // [0] err, [1..] u64 counters
   DBuf edge_scratch;  // snp_level_edges: fp0/fp1 interleave
@@ -895,6 +895,13 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
                       s->bytes == 1 ? s->d_elut.as<uint8_t>() : nullptr,
                       s->bytes == 1 ? s->d_hsg.as<uint8_t>() : nullptr, s->stream);
   CUDA_TRY(cudaGetLastError());
+  v.cpT = nullptr;
+  if (s->small_rules) {  // count-major first-rule (c, p) for counts < 32 (k_verify_m)
+    SNP_TRY(s->d_cpT.ensure((size_t)32 * m * 2, false));
+    launch_build_cpT(v, s->d_cpT.as<uint16_t>(), s->stream);
+    CUDA_TRY(cudaGetLastError());
+    v.cpT = s->d_cpT.as<uint16_t>();
+  }
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   // ---- tensor-core K-a (k_expand_tc): X|Y bytes of the first
   // applicable rule per (neuron, count), the B operand chunks (byte planes of

@@ -67,6 +67,7 @@ bool fast_expand_ok(const SysView& S);
 bool fast_materialize_ok(const SysView& S);
 size_t materialize_smem_bytes(const SysView& S, int32_t bytes, bool staged_e);
 bool materialize_narrow_ok(const SysView& S, int32_t bytes);
+void launch_build_cpT(const SysView& S, uint16_t* cpT, cudaStream_t st);
 
 // ---- launchers (all asynchronous on `st`) ----------------------------------
 void launch_build_tables(const SysView& S, int32_t bytes, uint8_t* tab, void* ctab, uint8_t* tab_full,

@@ -2742,8 +2742,16 @@ __global__ void __launch_bounds__(VM_THREADS + 32) k_verify_m(SysView S, LevelVi
   __shared__ uint64_t sref[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool decoder = tid >= VM_THREADS;
-  // fired (c, p) of the first applicable rule of neuron s at count v
+  // fired (c, p) of the first applicable rule of neuron s at count v: counts
+  // < 32 from the count-major table (lanes = consecutive neurons share its
+  // rows when their counts agree), else the rule tables
   auto first_cp = [&](int32_t s, int32_t v, int& c, int& p) {
+    if (S.cpT && (uint32_t)v < 32u) {
+      const uint32_t e = __ldg(S.cpT + (int64_t)v * m + s);
+      c = (int)(e & 0xFFu);
+      p = (int)(e >> 8);
+      return;
+    }
     const int r = first_rule(S, s, v);
     c = r >= 0 ? S.rules[r].c : 0;
     p = r >= 0 ? S.rules[r].p : 0;
@@ -4230,6 +4238,20 @@ void launch_verify_batch(const SysView& S, int32_t bytes, const LevelView& L, co
     }
   });
   count_launch(2);
+}
+
+// cpT[v][s] = c | p << 8 of neuron s's first applicable rule at count v < 32
+__global__ void k_build_cpT(SysView S, uint16_t* cpT) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)32 * S.m) return;
+  const int32_t v = (int32_t)(i / S.m), s = (int32_t)(i % S.m);
+  const int r = first_rule(S, s, v);
+  cpT[i] = r >= 0 ? (uint16_t)(S.rules[r].c | (S.rules[r].p << 8)) : (uint16_t)0;
+}
+
+void launch_build_cpT(const SysView& S, uint16_t* cpT, cudaStream_t st) {
+  k_build_cpT<<<grid_for((uint64_t)32 * S.m), BLK, 0, st>>>(S, cpT);
+  count_launch();
 }
 
 // dedup = 0: the listed key matches, one CTA each (k_verify_m); false when the
