@@ -838,6 +838,9 @@ constexpr int TC_STAGES = 2;                     // X|Y tiles: double-buffered
 #ifndef SNP_TC_MINB
 #define SNP_TC_MINB 4  // K-a: resident CTAs the register budget is sized for (56 registers, 4 CTAs/SM; 1 = 72 registers, 3 CTAs: 24.3 vs 19.2 ms)
 #endif
+#ifndef SNP_TC_UADDR
+#define SNP_TC_UADDR 1  // K-a: mbarrier addresses converted to shared once, outside the chunk loop
+#endif
 #ifndef SNP_TC_AHEAD
 #define SNP_TC_AHEAD 1  // K-a: chunks whose counts are loaded ahead (registers; 2 = two sets in flight)
 #endif
@@ -911,6 +914,7 @@ __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, 
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tslot;
+  [[maybe_unused]] const uint32_t bar_u = tc::smem_u32(bar), lbar_u = tc::smem_u32(lbar), fbar_u = tc::smem_u32(fbar);
   constexpr uint32_t IDESC = tc::idesc_u8(TCM, TCN, true, false);
 
   // the 32 counts of neuron c·64 + k (block h, half q) of chunk c, loaded
@@ -961,7 +965,11 @@ __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, 
     // entries (c | p << 4) of the 32 counts: 16- or 32-entry byte-permute
     // lookups (warp-uniform choice), the full table for a count >= 32
     uint32_t e[8], tt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#if SNP_TC_UADDR
+    tc::bar_wait_u(lbar_u + 8u * sl, (uint32_t)((c / TC_IN) & 1));
+#else
     tc::bar_wait(&lbar[sl], (uint32_t)((c / TC_IN) & 1));
+#endif
     // the next chunk's inputs go to slot (c + 1) % 3, last read by the MMAs
     // of chunk c - 2 (done: issued two chunks ago) and by the table loads of
     // chunk c - 2 (before every thread's __syncthreads of chunk c - 2)
@@ -1036,7 +1044,11 @@ __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, 
       ew_out[(blk * mE + s) * 2 + q] = ew & vmask;
     }
     // the MMAs that read this stage two chunks ago must be done
+#if SNP_TC_UADDR
+    if (c >= 2) tc::bar_wait_u(bar_u + 8u * st, (uint32_t)(((c - 2) >> 1) & 1));
+#else
     if (c >= 2) tc::bar_wait(&bar[st], (uint32_t)(((c - 2) >> 1) & 1));
+#endif
     {
       const int off = (k >> 3) * TC_A_LBO + (4 * h + 2 * q) * 128 + (k & 7) * 16;
       *reinterpret_cast<uint4*>(sX + off) = make_uint4(X[0], X[1], X[2], X[3]);
@@ -1048,7 +1060,11 @@ __global__ void __launch_bounds__(TCT + 32, SNP_TC_MINB) k_expand_tc(SysView S, 
     // the other warps run ahead, measured slower than this barrier)
     tc::fence_async_smem();
     if (WS) {
+#if SNP_TC_UADDR
+      tc::bar_arrive_u(fbar_u + 8u * st);
+#else
       mbar_arrive(&fbar[st]);
+#endif
       return;
     }
     __syncthreads();
