@@ -22,6 +22,7 @@
 namespace snp {
 
 constexpr int64_t TC_M_MAX = 1 << 19;        // k_expand_tc: s32 accumulators exact up to this m
+constexpr int EPAD = 16;  // zero emit words after the m real ones: padded in-CSR entries (one per bank pair)
 constexpr int KMAX = 64;                    // nondeterministic neurons recorded per parent
 constexpr int PB = 64;                      // configurations per storage block
 constexpr uint64_t PSI_LIMIT = 1ULL << 62;  // Ψ above this is SNP_E_CAPACITY

@@ -767,10 +767,21 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
             const int64_t j = 32 * g + 16 * h + l;
             if (j < m) lane_src[l].assign(in_src.begin() + in_off[j], in_src.begin() + in_off[j + 1]);
           }
-          bank_rows(lane_src, (int)(pad_off[g + 1] - pad_off[g]), lane_row);
-          for (int l = 0; l < 16; ++l)
-            for (size_t r = 0; r < lane_row[l].size(); ++r)
-              if (lane_row[l][r] >= 0) in_pad[(size_t)(pad_off[g] + r) * 32 + 16 * h + l] = lane_row[l][r];
+          const int64_t R = pad_off[g + 1] - pad_off[g];
+          bank_rows(lane_src, (int)R, lane_row);
+          for (int64_t r = 0; r < R; ++r) {
+            // the half-row's padding lanes read one of the EPAD zero words, in
+            // a bank pair none of its real sources uses (broadcast, no conflict)
+            unsigned used = 0;
+            for (int l = 0; l < 16; ++l)
+              if (r < (int64_t)lane_row[l].size() && lane_row[l][r] >= 0) used |= 1u << (lane_row[l][r] & 15);
+            int z = 0;
+            while (z < 15 && ((used >> ((pad + z) & 15)) & 1u)) ++z;
+            for (int l = 0; l < 16; ++l) {
+              const bool real = r < (int64_t)lane_row[l].size() && lane_row[l][r] >= 0;
+              in_pad[(size_t)(pad_off[g] + r) * 32 + 16 * h + l] = real ? lane_row[l][r] : pad + z;
+            }
+          }
         }
         continue;
       }
@@ -779,7 +790,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
           in_pad[(size_t)(pad_off[g] + (e - in_off[j])) * 32 + (j - 32 * g)] = in_src[e];
     }
     SNP_TRY(upload(s, s->d_in_pad, in_pad));
-    if (m < 65535) {
+    if (m + EPAD < 65535) {
       std::vector<uint16_t> in16(in_pad.begin(), in_pad.end());
       SNP_TRY(upload(s, s->d_in_pad16, in16));
     }
@@ -881,7 +892,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.in_off = s->d_in_off.as<int32_t>();
   v.in_src = s->d_in_src.as<int32_t>();
   v.in_pad = s->d_in_pad.as<int32_t>();
-  v.in_pad16 = m < 65535 ? s->d_in_pad16.as<uint16_t>() : nullptr;
+  v.in_pad16 = m + EPAD < 65535 ? s->d_in_pad16.as<uint16_t>() : nullptr;
   v.in_pad_off = s->d_in_pad_off.as<int64_t>();
   v.out_off = s->d_out_off.as<int32_t>();
   v.out_dst = s->d_out_dst.as<int32_t>();

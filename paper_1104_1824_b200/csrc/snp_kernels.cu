@@ -1712,7 +1712,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
   const int32_t m = S.m;
   const int64_t mE = (m + 1) & ~1;
   uint64_t* sE = reinterpret_cast<uint64_t*>(smem);                    // mE words + 2 zero words
-  uint8_t* sX = smem + (ES ? (mE + 2) * 8 : 0);                         // MWT×32×xs_stride (TCS: the A tiles)
+  uint8_t* sX = smem + (ES ? (mE + EPAD) * 8 : 0);                      // MWT×32×xs_stride (TCS: the A tiles)
   constexpr int XS = NARROW ? xs_stride<uint8_t>() : xs_stride<T>();  // staging row stride (NARROW: bytes)
   uint8_t* sR = sX + (TCS ? (size_t)MWT / 4 * KCT_ATILE + KCT_BBYTES : (size_t)MWT * 32 * XS);  // QCAP + 32
   uint32_t* sD = reinterpret_cast<uint32_t*>(sR + QCAP + 32);           // (QCAP+32)/4 quad descriptors
@@ -1755,7 +1755,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
 #endif
   }
   if (tid <= np) sQ[tid] = kq_off[pb0 + tid];
-  if (ES && tid < 2) sE[mE + tid] = 0;  // target of padded in-synapses
+  if (ES && tid < EPAD) sE[mE + tid] = 0;  // targets of padded in-synapses (one per bank pair)
   const uint64_t* gE = O.ebits + blk * mE;
   __syncthreads();
   const uint64_t nq = Q1 - Q0;
@@ -2729,7 +2729,7 @@ __global__ void k_verify_cols(SysView S, LevelView L, ChildArrays C, const uint6
 #endif
 constexpr int VM_THREADS = SNP_VM_THREADS;  // threads per match (CTA); CTAs per SM = min(2048 / VM_THREADS, smem)
 size_t verify_m_smem_bytes(int32_t m, bool pk) {
-  const size_t mE = (size_t)((m + 1) & ~1) + 2;
+  const size_t mE = (size_t)((m + 1) & ~1) + EPAD;
   return mE * (pk ? 4 : 16) + (size_t)m * 8 + 4 * KMAX * 8 + 64;
 }
 
@@ -2748,8 +2748,8 @@ __global__ void __launch_bounds__(VM_THREADS + 32) k_verify_m(SysView S, LevelVi
   extern __shared__ __align__(16) uint8_t vm_smem[];
   const int32_t m = S.m;
   const int32_t mE = (m + 1) & ~1;
-  FW* fc = reinterpret_cast<FW*>(vm_smem);                            // [mE + 2] (c_a, p_a, c_b, p_b); zero pads
-  int32_t* cnt = reinterpret_cast<int32_t*>(fc + mE + 2);             // [2][m]
+  FW* fc = reinterpret_cast<FW*>(vm_smem);                            // [mE + EPAD] (c_a, p_a, c_b, p_b); zero pads
+  int32_t* cnt = reinterpret_cast<int32_t*>(fc + mE + EPAD);          // [2][m]
   int32_t* nds = cnt + 2 * m;                                          // [2 buf][2 sides][KMAX] neuron
   uint8_t* ndx = reinterpret_cast<uint8_t*>(nds + 4 * KMAX);          // [2 buf][2 sides][KMAX] digit
   __shared__ int sK[2][2];
@@ -2805,7 +2805,7 @@ __global__ void __launch_bounds__(VM_THREADS + 32) k_verify_m(SysView S, LevelVi
     sK[b][lane] = K;
     sp[b][lane] = p;
   };
-  if (tid < mE + 2 - m) fc[m + tid] = mk(0, 0, 0, 0);  // targets of padded in-synapses
+  if (tid < mE + EPAD - m) fc[m + tid] = mk(0, 0, 0, 0);  // targets of padded in-synapses
   const uint64_t nl = *n_list;
   if (decoder && blockIdx.x < nl) decode(blockIdx.x, 0);
   __syncthreads();
@@ -3969,14 +3969,14 @@ size_t materialize_smem_bytes(const SysView& S, int32_t bytes, bool staged_e) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
   const size_t xs = materialize_narrow_ok(S, bytes) ? (size_t)kc_cta_warps(S, bytes, staged_e) * 32 * (PB + 4)
                     : (size_t)kc_cta_warps(S, bytes, staged_e) * 32 * (PB * bytes + 4);
-  return (staged_e ? (mE + 2) * 8 : 0) + xs + 2 * (QCAP + 32) + 8 * OPCAP + 67 * 8 + 16 + 16;
+  return (staged_e ? (mE + EPAD) * 8 : 0) + xs + 2 * (QCAP + 32) + 8 * OPCAP + 67 * 8 + 16 + 16;
 }
 
 // the tensor-core store variant (uint8): A tiles + one-hot operands instead of
 // the staging rows, descriptors and store program; one mbarrier per tile
 size_t materialize_tc_smem_bytes(const SysView& S, bool staged_e) {
   const size_t mE = (size_t)((S.m + 1) & ~1);
-  return (staged_e ? (mE + 2) * 8 : 0) + (size_t)MW / 4 * KCT_ATILE + KCT_BBYTES + (QCAP + 32) + 66 * 8 + 8 +
+  return (staged_e ? (mE + EPAD) * 8 : 0) + (size_t)MW / 4 * KCT_ATILE + KCT_BBYTES + (QCAP + 32) + 66 * 8 + 8 +
          8 * (MW / 4) + 16 + 16;
 }
 
