@@ -1618,6 +1618,12 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_EDGE
 #define SNP_KC_EDGE 1  // boundary bytes of a row end as <= 2 aligned stores (else one byte store per child)
 #endif
+#ifndef SNP_KC_FULLROWS
+#define SNP_KC_FULLROWS 1  // cooperative quads: no per-store row predicate when the warp has all 32 rows
+#endif
+#ifndef SNP_KC_EDGEPRMT
+#define SNP_KC_EDGEPRMT 1  // row-end bytes gathered by the partial quad's byte permute (else byte by byte)
+#endif
 #ifndef SNP_KC_ABLATE
 #define SNP_KC_ABLATE 0  // diagnostics only (wrong results): 1 / 4 skip the per-lane / cooperative stores, 2 the gather
 #endif
@@ -1781,13 +1787,17 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
     for (uint64_t i = tid; i < nquad; i += blockDim.x) {
       const uint64_t q = Qb + 4 * i;
       uint32_t d = 0x80000000u;
-      if (q >= Q0 && q + 3 < Q1) {
-        const uint32_t a = sR[q - Qb] >> 2;
+      // partial quads at the window ends too (positions outside [Q0, Q1)
+      // repeat the first valid one): the row-end bytes use the same permute
+      const uint64_t qf = q >= Q0 ? q : Q0;
+      if (qf < Q1 && qf < q + 4) {
+        const uint32_t a = sR[qf - Qb] >> 2;
         uint32_t sel = 0, hb = 0;
         bool ok = true;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint32_t o = (uint32_t)sR[q + k - Qb] - 4 * a;
+          const uint64_t qk = (q + k >= Q0 && q + k < Q1) ? q + k : qf;
+          const uint32_t o = (uint32_t)sR[qk - Qb] - 4 * a;
           ok &= o < 16;
           hb |= (o >> 3) << k;  // byte k from words a+2, a+3
           sel |= (o & 7) << (4 * k);
@@ -2157,7 +2167,19 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
           return;
         }
         uint32_t v = 0;
-        for (uint64_t q = q0; q < q1; ++q) v |= (uint32_t)xsb[sR[q - Qb]] << (8 * (q - q0));
+        const uint32_t dq = sD[(q0 - Qb) >> 2];  // the partial quad's permute (SNP_KC_EDGEPRMT)
+        if (SNP_KC_EDGEPRMT && !(dq & 0x80000000u)) {
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(xsb) + ((dq >> 16) & 31);
+          const uint32_t sel = dq & 0xFFFFu, hb = dq >> 24;
+          v = prmt(w[0], w[1], sel);
+          if (hb) {
+            const uint32_t mask = (hb * 0x00204081u & 0x01010101u) * 0xFFu;
+            v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
+          }
+          v >>= 8 * (uint32_t)(q0 & 3);
+        } else {
+          for (uint64_t q = q0; q < q1; ++q) v |= (uint32_t)xsb[sR[q - Qb]] << (8 * (q - q0));
+        }
         uint8_t* d = orow + eidx((int64_t)q0, j, m);
         int n = (int)(q1 - q0);
         if ((q0 & 1) && n) {
@@ -2373,18 +2395,24 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
             const uint32_t* w0 = reinterpret_cast<const uint32_t*>(xr0) + ((d >> 16) & 31);
             const uint32_t sel = d & 0xFFFFu, hb = d >> 24;
             const uint32_t mask = (hb * 0x00204081u & 0x01010101u) * 0xFFu;  // 0xFF in bytes k with bit k of hb
+            // FULL: every row of the warp exists (warp-uniform), no per-store predicate
+            auto rows = [&](auto full_c) {
+              constexpr bool FULL = decltype(full_c)::value;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(w0) +
-                                                                    2 * i * XS);
-              uint32_t v = prmt(w[0], w[1], sel);
+              for (int i = 0; i < 16; ++i) {
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(w0) +
+                                                                      2 * i * XS);
+                uint32_t v = prmt(w[0], w[1], sel);
 #if SNP_KC_BRANCHLESS
-              v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);  // mask = 0 when hb = 0 (words past the row are masked out)
+                v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);  // mask = 0 when hb = 0 (words past the row are masked out)
 #else
-              if (hb) v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
+                if (hb) v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
 #endif
-              if (j0 + 2 * i < jn) put4(dst0 + i * 128 * (int)sizeof(T), v);
-            }
+                if (FULL || j0 + 2 * i < jn) put4(dst0 + i * 128 * (int)sizeof(T), v);
+              }
+            };
+            if (SNP_KC_FULLROWS && jn >= 32) rows(std::true_type{});
+            else rows(std::false_type{});
           } else {
             const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (q - Qb));  // 4 parent indices
 #pragma unroll 4
