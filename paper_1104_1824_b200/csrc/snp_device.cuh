@@ -115,6 +115,7 @@ struct SysView {
   // (a zero word)
   const int32_t* in_pad;
   const uint16_t* in_pad16;    // the same as uint16 when m < 65535 (else null)
+  const uint64_t* in_pad16x4;  // the same, 4 rows per lane packed: [row/4][lane] (null with in_pad16)
   const int64_t* in_pad_off;   // m/32 + 1 row offsets (×32 entries)
   const int32_t* out_off;    // m + 1
   const int32_t* out_dst;    // targets j with (s, j) ∈ syn, grouped by source s

@@ -196,7 +196,7 @@ struct snp_system {
   bool binary_emit = true;
   bool small_rules = true;  // every c, p <= 255 (k_sample_cta)
   // ---- device system
-  DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1, d_in_pad, d_in_pad16, d_in_pad_off;
+  DBuf d_rule_off, d_rules, d_h0, d_h1, d_in_off, d_in_src, d_out_off, d_out_dst, d_R0, d_R1, d_in_pad, d_in_pad16, d_in_pad16x4, d_in_pad_off;
   SysView view{};
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -793,6 +793,14 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
     if (m + EPAD < 65535) {
       std::vector<uint16_t> in16(in_pad.begin(), in_pad.end());
       SNP_TRY(upload(s, s->d_in_pad16, in16));
+      std::vector<uint64_t> in4(in16.size() / 4);  // rows per group are a multiple of 4
+      for (size_t q = 0; q < in4.size(); ++q) {
+        const size_t rq = q / 32, l = q % 32;
+        uint64_t v = 0;
+        for (int u = 0; u < 4; ++u) v |= (uint64_t)in16[(4 * rq + u) * 32 + l] << (16 * u);
+        in4[q] = v;
+      }
+      SNP_TRY(upload(s, s->d_in_pad16x4, in4));
     }
     SNP_TRY(upload(s, s->d_in_pad_off, pad_off));
   }
@@ -893,6 +901,7 @@ snp_status load_impl(snp_system* s, const snp_matrix* M, const snp_rule* rules, 
   v.in_src = s->d_in_src.as<int32_t>();
   v.in_pad = s->d_in_pad.as<int32_t>();
   v.in_pad16 = m + EPAD < 65535 ? s->d_in_pad16.as<uint16_t>() : nullptr;
+  v.in_pad16x4 = m + EPAD < 65535 ? s->d_in_pad16x4.as<uint64_t>() : nullptr;
   v.in_pad_off = s->d_in_pad_off.as<int64_t>();
   v.out_off = s->d_out_off.as<int32_t>();
   v.out_dst = s->d_out_dst.as<int32_t>();

@@ -20,6 +20,7 @@
 #include <atomic>
 
 #include <cub/cub.cuh>
+#include <type_traits>
 
 #include "snp_internal.h"
 #include "snp_tc.cuh"
@@ -1618,6 +1619,12 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_EDGE
 #define SNP_KC_EDGE 1  // boundary bytes of a row end as <= 2 aligned stores (else one byte store per child)
 #endif
+#ifndef SNP_KC_TAILQ
+#define SNP_KC_TAILQ 1  // cooperative quads: the last < 16 quads with several rows per step
+#endif
+#ifndef SNP_KC_IDX4
+#define SNP_KC_IDX4 1  // gather indices: 4 rows' uint16 sources in one 8-byte load per lane
+#endif
 #ifndef SNP_KC_FULLROWS
 #define SNP_KC_FULLROWS 1  // cooperative quads: no per-store row predicate when the warp has all 32 rows
 #endif
@@ -1917,12 +1924,29 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
           carry = t;
         }
       };
+      // the source of row e (0 <= e < ne) of this lane: u16 rows in 4-row
+      // packs (one 8-byte load per 4 rows), else one load per row
+      auto srcs4 = [&](const auto* col, int e0, int32_t (&src)[4]) {
+        if constexpr (std::is_same<std::remove_cv_t<std::remove_pointer_t<decltype(col)>>, uint64_t>::value) {
+          const uint64_t q = __ldg(col + (e0 >> 2) * 32);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) src[u] = (int32_t)((q >> (16 * u)) & 0xFFFFu);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) src[u] = (int32_t)__ldg(col + (e0 + u) * 32);
+        }
+      };
       auto gather = [&](const auto* col) {
         int e0 = 0;
         for (; e0 + 8 <= ne; e0 += 8) {
           int32_t src[8];
+          {  // batch the loads
+            int32_t a4[4], b4[4];
+            srcs4(col, e0, a4);
+            srcs4(col, e0 + 4, b4);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) src[u] = (int32_t)__ldg(col + (e0 + u) * 32);  // batch the loads
+            for (int u = 0; u < 4; ++u) { src[u] = a4[u]; src[4 + u] = b4[u]; }
+          }
           uint64_t x[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) x[u] = word(src[u]);
@@ -1938,8 +1962,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
         }
         if (e0 < ne) {  // 4 rows left
           int32_t src[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) src[u] = (int32_t)__ldg(col + (e0 + u) * 32);
+          srcs4(col, e0, src);
           uint64_t x[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) x[u] = word(src[u]);
@@ -1951,6 +1974,8 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
         }
       };
       if (SNP_KC_ABLATE & 2) {
+      } else if (SNP_KC_IDX4 && S.in_pad16x4) {
+        gather(S.in_pad16x4 + (r0 >> 2) * 32 + lane);
       } else if (S.in_pad16) {
         gather(S.in_pad16 + r0 * 32 + lane);
       } else {
@@ -2378,7 +2403,9 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       // passes over the CTA's own full quads [qa, qb), 16 per pass (lane
       // hl takes quad qa + 4·(16·pass + hl), whichever output block it is
       // in): one pass when the CTA has <= 16 full quads
-      for (uint64_t q0 = qa; !(SNP_KC_ABLATE & 4) && q0 < qb; q0 += 64) {
+      // (SNP_KC_TAILQ: whole passes only; the last < 16 quads below)
+      const uint64_t qpass = SNP_KC_TAILQ ? qa + ((qb - qa) & ~(uint64_t)63) : qb;
+      for (uint64_t q0 = qa; !(SNP_KC_ABLATE & 4) && q0 < qpass; q0 += 64) {
         const uint64_t q = q0 + 4 * hl;
         if (q < qb) {
           const uint64_t ob = q >> 6;
@@ -2425,6 +2452,37 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
           }
         }
       }
+#if SNP_KC_FLATQ && SNP_KC_TAILQ
+      // the last nrem < 16 quads: lpr = nrem rounded up to a power of two
+      // lanes per row, 32 / lpr rows per step, so a 2-quad tail takes 2 steps
+      // instead of a 16-step pass with 14 idle lanes per half-warp
+      if (!(SNP_KC_ABLATE & 4) && qpass < qb) {
+        const int nrem = (int)((qb - qpass) >> 2);
+        const int lpr = nrem <= 1 ? 1 : nrem <= 2 ? 2 : nrem <= 4 ? 4 : nrem <= 8 ? 8 : 16;
+        const int rps = 32 / lpr, qi = lane & (lpr - 1), ro = lane / lpr;
+        if (qi < nrem) {
+          const uint64_t q = qpass + 4 * (uint64_t)qi;
+          const uint64_t ob = q >> 6;
+          const uint32_t d = sD[(q - Qb) >> 2];
+          const uint32_t rr = *reinterpret_cast<const uint32_t*>(sR + (q - Qb));  // 4 parent indices
+          const uint32_t sel = d & 0xFFFFu, hb = d >> 24;
+          const uint32_t mask = (hb * 0x00204081u & 0x01010101u) * 0xFFu;
+          for (int jr = ro; jr < 32 && jr < jn; jr += rps) {
+            const uint8_t* xr = sX + (size_t)(warp * 32 + jr) * XS;
+            uint32_t v;
+            if (!(d & 0x80000000u)) {
+              const uint32_t* w = reinterpret_cast<const uint32_t*>(xr) + ((d >> 16) & 31);
+              v = prmt(w[0], w[1], sel);
+              if (hb) v = (v & ~mask) | (prmt(w[2], w[3], sel) & mask);
+            } else {
+              v = (uint32_t)xr[rr & 0xFF] | ((uint32_t)xr[(rr >> 8) & 0xFF] << 8) |
+                  ((uint32_t)xr[(rr >> 16) & 0xFF] << 16) | ((uint32_t)xr[rr >> 24] << 24);
+            }
+            put4(reinterpret_cast<uint8_t*>(out + ((((int64_t)ob * m + jbase + jr) << 6) + (q & 63))), v);
+          }
+        }
+      }
+#endif
       __syncwarp();
     }
 #endif

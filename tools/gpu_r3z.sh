@@ -1,0 +1,7 @@
+#!/bin/bash
+# K-c gather indices in 4-row packs (A/B)
+O=gpurun_out/r3z; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/build.log 2>&1 || { tail -20 $O/build.log; exit 1; }
+tail -1 $O/build.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q -x -k "random_system_parity or global_emit or uint8_large or tc_expand or tiny" > $O/pytest.log 2>&1; tail -2 $O/pytest.log
+AB_STEPS=8 bash tools/gpu_ab.sh r3z_c4 "X=0|SNP_KC_IDX4=0" "X=1"
