@@ -1620,7 +1620,7 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #define SNP_KC_EDGE 1  // boundary bytes of a row end as <= 2 aligned stores (else one byte store per child)
 #endif
 #ifndef SNP_KC_TAILQ
-#define SNP_KC_TAILQ 1  // cooperative quads: the last < 16 quads with several rows per step
+#define SNP_KC_TAILQ 0  // cooperative quads: the last < 16 quads with several rows per step (measured slower: 54.5 vs 50.7 ms, 64 registers)
 #endif
 #ifndef SNP_KC_IDX4
 #define SNP_KC_IDX4 1  // gather indices: 4 rows' uint16 sources in one 8-byte load per lane
@@ -2404,7 +2404,7 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
       // hl takes quad qa + 4·(16·pass + hl), whichever output block it is
       // in): one pass when the CTA has <= 16 full quads
       // (SNP_KC_TAILQ: whole passes only; the last < 16 quads below)
-      const uint64_t qpass = SNP_KC_TAILQ ? qa + ((qb - qa) & ~(uint64_t)63) : qb;
+      const uint64_t qpass = (SNP_KC_TAILQ && qa < qb) ? qa + ((qb - qa) & ~(uint64_t)63) : qb;
       for (uint64_t q0 = qa; !(SNP_KC_ABLATE & 4) && q0 < qpass; q0 += 64) {
         const uint64_t q = q0 + 4 * hl;
         if (q < qb) {

@@ -445,3 +445,16 @@ def test_exact_dedup_verification(snp, monkeypatch, batch):
     with pytest.raises(snp.SnpError) as ei:
         snp.System(w, count_bits=32, dedup=0, frontier_target=900).explore(L0, depth=3)
     assert ei.value.status == snp.SNP_E_COLLISION
+
+
+@pytest.mark.parametrize("bits", [8, 16])
+@pytest.mark.parametrize("target", [40, 150, 1100])
+def test_sparse_and_dense_kept_windows(snp, bits, target):
+    """K-c's per-block child windows from nearly empty (a few kept children
+    per 64-parent block: no whole 4-child quad, partial quads only) to more
+    than 16 whole quads (whole store passes plus a tail pass)."""
+    w = W.random_system(300, outdeg=8, k_nd=6, seed=321)
+    L0 = W.level0_counts(w, 1000, 321)
+    tree = snp.System(w, count_bits=bits, dedup=1, frontier_target=target).explore(L0, depth=3)
+    ref = oracle.System.from_workload(w).explore(L0, depth=3, dedup=1, count_bits=bits, frontier_target=target)
+    assert_same_tree(tree, ref)
