@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-2 final recording session (one B200): everything judged goes to gpurun_out/$TAG
-TAG=${1:-r02g}
+TAG=${1:-r02h}
 O=gpurun_out/$TAG; mkdir -p $O
 { nproc; free -g; lscpu | grep -E "Model name|^CPU\(s\)"; nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,driver_version --format=csv; } > $O/box.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { tail -30 $O/build.log; exit 1; }
