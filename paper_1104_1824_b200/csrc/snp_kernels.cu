@@ -1619,6 +1619,9 @@ __global__ void k_kq_off(const uint64_t* off, const uint64_t* kpos, int64_t F, u
 #ifndef SNP_KC_EDGE
 #define SNP_KC_EDGE 1  // boundary bytes of a row end as <= 2 aligned stores (else one byte store per child)
 #endif
+#ifndef SNP_KC_CARRYU
+#define SNP_KC_CARRYU 1  // byte-carry check of x = t + count warp-uniform (a real branch, not predication)
+#endif
 #ifndef SNP_KC_TAILQ
 #define SNP_KC_TAILQ 0  // cooperative quads: the last < 16 quads with several rows per step (measured slower: 54.5 vs 50.7 ms, 64 registers)
 #endif
@@ -2098,20 +2101,31 @@ __global__ void __launch_bounds__(MWT * 32) k_materialize_bs(SysView S, LevelVie
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) chk |= t[i] | kq[i];
+        // a byte can only carry when an operand byte has its top bit set
+        // (rare); CARRYU: the test is warp-uniform so the compiler keeps the
+        // careful path as a real branch instead of predicating it into every
+        // quad (the careful form is exact for every lane)
+        const bool carry = (chk & 0x80808080u) != 0;
+        if (SNP_KC_CARRYU ? __any_sync(__activemask(), carry) : carry) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          uint32_t x4 = t[i] + kq[i];
-          if (chk & 0x80808080u) {
+          for (int i = 0; i < 8; ++i) {
             const uint32_t t4 = t[i], k4 = kq[i];
             const uint32_t s7 = (t4 & 0x7F7F7F7Fu) + (k4 & 0x7F7F7F7Fu);
             const uint32_t co = ((t4 & k4) | ((t4 | k4) & s7)) & 0x80808080u;
-            x4 = s7 ^ ((t4 ^ k4) & 0x80808080u);
+            const uint32_t x4 = s7 ^ ((t4 ^ k4) & 0x80808080u);
 #pragma unroll
             for (int b = 0; b < 4; ++b)
               if ((co >> (8 * b + 7)) & 1u) ovf_bits |= 1ULL << (32 * g + 4 * i + b);
+            if (TCS) xw[i] = x4;
+            else reinterpret_cast<uint32_t*>(xsb)[8 * g + i] = x4;
           }
-          if (TCS) xw[i] = x4;
-          else reinterpret_cast<uint32_t*>(xsb)[8 * g + i] = x4;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t x4 = t[i] + kq[i];
+            if (TCS) xw[i] = x4;
+            else reinterpret_cast<uint32_t*>(xsb)[8 * g + i] = x4;
+          }
         }
         if (TCS) {  // parents 32g .. 32g+31 = K-chunks 2g, 2g+1 of the A row
           *reinterpret_cast<uint4*>(xsb + (2 * g) * KCT_A_LBO) = make_uint4(xw[0], xw[1], xw[2], xw[3]);
